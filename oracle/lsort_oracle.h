@@ -1,0 +1,140 @@
+/*
+ * lsort_oracle.h -- CPU ORACLE (test infrastructure only).
+ *
+ * Plain-C restatement of the reference's sort hot path (arXiv 2307.08637,
+ * parallel LearnedSort / AIPS2o) used as the CHECKER for the CUDA library.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load it. The product path (paper_2307_08637_b200)
+ * never links or calls anything in oracle/.
+ *
+ * Each function cites the reference file:line it restates
+ * (paths relative to /root/reference/proj/src/ unless noted).
+ * Compiled with -O2 -ffp-contract=off so the double arithmetic matches the
+ * reference's Release build bit for bit.
+ *
+ * Parity pinning: the model layer (codec, rng, fit/train/monotone, predict,
+ * bucket_index, SplitterTree, duplicate_fraction, verify) is pinned bit-exact
+ * against the reference compiled from /root/reference (oracle/_ref, see
+ * oracle/Makefile) and against the committed golden vectors in tests/golden/.
+ * The sort driver has no reference code; its output is
+ * pinned by std::sort / numpy.sort (a keys-only sorted array is unique).
+ */
+#ifndef LSORT_ORACLE_H
+#define LSORT_ORACLE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSO_MAX_TREE 1024 /* max bucket budget for a splitter tree */
+
+/* ---- keys.hpp ---------------------------------------------------------- */
+uint64_t lso_encode_double(double x);                       /* keys.hpp:24-27 */
+double lso_decode_double(uint64_t k);                       /* keys.hpp:29-32 */
+int64_t lso_encode_doubles(const double* in, uint64_t* out, size_t n); /* :36-42 */
+void lso_decode_doubles(const uint64_t* in, double* out, size_t n);    /* :44-46 */
+
+/* ---- rng.hpp ----------------------------------------------------------- */
+uint64_t lso_splitmix64(uint64_t x);                        /* rng.hpp:13-18 */
+/* Rng(seed) draw number `draw` (counter-based: splitmix64(seed + draw)). */
+uint64_t lso_rng_u64(uint64_t seed, uint64_t draw);         /* rng.hpp:24 */
+double lso_rng_unit(uint64_t seed, uint64_t draw);          /* rng.hpp:27-29 */
+double lso_rng_unit_open(uint64_t seed, uint64_t draw);     /* rng.hpp:32 */
+uint64_t lso_rng_below(uint64_t seed, uint64_t draw, uint64_t bound); /* :35-37 */
+double lso_rng_normal(uint64_t seed, uint64_t draw);        /* rng.hpp:41-45, uses draws draw, draw+1 */
+double lso_rng_exponential(uint64_t seed, uint64_t draw, double lambda); /* :47-49 */
+
+/* ---- models.hpp / models.cpp: RMI -------------------------------------- */
+/* Packed RMI parameters (same layout as lsort_rmi_header/lsort_rmi_entry in
+ * include/lsort_cuda.h): P[0]=root.slope P[1]=root.intercept P[2]=key_base
+ * P[3]=key_scale, then for m in [0,B): P[4+4m..4m+7] = slope, intercept,
+ * clamp_lo, clamp_hi. Size 4+4B doubles. */
+int lso_rmi_train(const uint64_t* sorted, size_t n, uint32_t B, double* P); /* models.cpp:39-73 */
+void lso_enforce_monotonic(double* P, uint32_t B, const uint64_t* sorted, size_t n); /* models.cpp:75-131 */
+double lso_rmi_predict(const double* P, uint32_t B, uint64_t x);    /* models.hpp:34-43 */
+uint32_t lso_rmi_route(const double* P, uint32_t B, double xn);     /* models.hpp:60-65 */
+uint32_t lso_learned_bucket(const double* P, uint32_t B, uint32_t bucket_count,
+                            double cdf_lo, double cdf_hi, uint64_t x); /* models.hpp:162-171 */
+
+/* ---- SplitterTree ------------------------------------------------------ */
+typedef struct lso_tree {
+    uint32_t levels, leaf_origin, nsplitters, bucket_count;
+    uint64_t tree[LSO_MAX_TREE];           /* implicit heap, 1-based, size leaf_origin */
+    uint64_t splitters[LSO_MAX_TREE];      /* strictly increasing */
+    uint32_t eq_offset[LSO_MAX_TREE + 1];  /* base region -> first bucket id */
+} lso_tree;
+int lso_tree_build(const uint64_t* sorted, size_t n, uint32_t budget, int equality_mode,
+                   lso_tree* t);                                    /* models.cpp:133-185 */
+uint32_t lso_tree_classify(const lso_tree* t, uint64_t x);          /* models.hpp:92-101 */
+double lso_duplicate_fraction(const uint64_t* sorted, size_t n);    /* models.cpp:187-193 */
+
+/* ---- verify.hpp -------------------------------------------------------- */
+/* returns 1 if sorted (first_violation=0) else 0 with the index i, a[i-1]>a[i] */
+int lso_verify_sorted(const uint64_t* a, size_t n, uint64_t* first_violation); /* verify.hpp:17-22 */
+uint64_t lso_multiset_hash(const uint64_t* a, size_t n);           /* verify.hpp:25-29 */
+
+/* ---- synthetic inputs (BASELINE.json configs) ---------- */
+enum {
+    LSO_GEN_UNIFORM = 0,      /* C1: next_unit, draw i */
+    LSO_GEN_NORMAL = 1,       /* C2: next_normal, draws 2i,2i+1 */
+    LSO_GEN_LOGNORMAL05 = 2,  /* C2: exp(0.5*normal) */
+    LSO_GEN_EXPONENTIAL2 = 3, /* C2: next_exponential(2), draw i */
+    LSO_GEN_MIXGAUSS = 4,     /* C3: 5 gaussians, 10 param draws then 3 per element */
+    LSO_GEN_ROOTDUPS = 5,     /* C4 (u64): i mod floor(sqrt(N)), Fisher-Yates shuffled */
+    LSO_GEN_TWODUPS = 6,      /* C4 (u64): (i*i + N/2) mod N, shuffled */
+    LSO_GEN_ZIPF = 7,         /* C4 (u64): Zipf(0.75) over 1e6 ranks, shuffled */
+    LSO_GEN_LOGNORMAL2 = 8    /* C5: exp(2*normal) */
+};
+int lso_gen_is_float(int dist);
+/* Elements [first, first+count) of the length-`total` dataset into out
+ * (double* for float datasets, uint64_t* otherwise). Shuffled datasets need
+ * first == 0 and count == total. */
+int lso_generate(int dist, uint64_t total, uint64_t seed, uint64_t first, uint64_t count,
+                 void* out, int threads);
+
+/* ---- sort driver (Alg. 5) ------------ */
+typedef struct lso_cfg {
+    uint32_t rmi_bucket_count;       /* SPEC.md:370  1024 */
+    uint32_t tree_bucket_count;      /* 256 */
+    uint64_t min_rmi_input;          /* 100000 */
+    double max_duplicate_fraction;   /* 0.10 */
+    uint32_t radix_base_case;        /* 4096 */
+    uint32_t insertion_base_case;    /* 16 */
+    uint32_t first_sample_cap;       /* 2*tree_bucket_count*16 */
+    uint32_t rmi_sample_cap;         /* 1<<20 */
+    double sample_fraction;          /* 0.01 */
+    uint64_t seed;
+    uint32_t workers;                /* OpenMP threads (0 = all) */
+} lso_cfg;
+void lso_cfg_default(lso_cfg* c);
+uint64_t lso_seg_seed(uint64_t cfg_seed, uint64_t seg_begin, uint32_t depth);
+uint64_t lso_first_sample_size(const lso_cfg* c, uint64_t n);
+uint64_t lso_rmi_sample_size(const lso_cfg* c, uint64_t n);
+
+/* Alg. 5 build_partition_model for segment a[0,n) that
+ * begins at absolute position seg_begin at recursion depth `depth`.
+ * kind_out: 0 learned, 1 tree. For learned, P (4+4*rmi_buckets doubles) is
+ * filled; for tree, *tree. dup_out = duplicate fraction of the first sample.
+ * Sample j of the segment stream is splitmix64(seg_seed + j) % n: the first
+ * sample uses j in [0,s1), the RMI sample j in [s1, s1+s2). */
+int lso_build_partition_model(const uint64_t* a, uint64_t n, uint64_t seg_begin, uint32_t depth,
+                              const lso_cfg* c, uint32_t rmi_buckets, uint32_t tree_buckets,
+                              int* kind_out, double* P, lso_tree* tree, double* dup_out);
+
+/* In-place sort of encoded keys (AIPS2o restatement; out-of-place scratch
+ * internally). Returns 0. */
+int lso_sort_keys(uint64_t* a, uint64_t n, const lso_cfg* c);
+/* double entry: encode (NaN -> returns 2, *nan_index set, array untouched),
+ * sort, decode. */
+int lso_sort_doubles(double* a, uint64_t n, const lso_cfg* c, int64_t* nan_index);
+
+/* radix_base_case_sort: MSD byte radix, insertion <= 16 */
+void lso_radix_base_case_sort(uint64_t* a, uint64_t n, uint32_t insertion_threshold);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
