@@ -1,0 +1,193 @@
+/*
+ * lsort_cuda.h -- C-ABI of the B200-native parallel LearnedSort (AIPS2o)
+ * library liblsort_cuda.so (hand-written sm_100a CUDA kernels + C++ host
+ * orchestrator). Plain pointers and sizes only; no torch or CUDA types.
+ *
+ * Reference interfaces each entry point replaces (paths under
+ * /root/reference; the reference ships only the model layer in code, the sort
+ * entry point is declared by its SPEC):
+ *   lsort_cuda_sort          <- sort(a, cfg)
+ *                               (+ encode_doubles/decode_doubles keys.hpp:36-46
+ *                               for LSORT_KEY_F64: NaN -> first index, keys.hpp:34-42)
+ *   lsort_cfg                <- SortConfig
+ *   lsort_cuda_build_model   <- build_partition_model
+ *   lsort_cuda_rmi_train     <- Rmi::train + enforce_monotonic
+ *                                                             proj/src/models.cpp:39-131
+ *   lsort_cuda_classify_rmi  <- PartitionModel::bucket_index (learned) + Rmi::predict
+ *                                                             proj/src/models.hpp:34-65,162-171
+ *   lsort_cuda_tree_build    <- SplitterTree::build          proj/src/models.cpp:133-185
+ *   lsort_cuda_classify_tree <- SplitterTree::classify       proj/src/models.hpp:92-101
+ *   lsort_cuda_verify        <- verify_sorted, multiset_hash proj/src/verify.hpp:17-29
+ *   lsort_gen_keys           <- data.generate
+ *   lsort_cuda_dist_*        <- (none: multi-GPU layer is new)
+ *
+ * Conventions: return 0 (LSORT_OK) or an LSORT_E* code; the message is
+ * available from lsort_cuda_last_error(ctx). LSORT_EINVAL mirrors the
+ * reference's std::invalid_argument (models.cpp:40-43,135-138). A context is
+ * single-threaded; concurrent sorts use separate contexts.
+ * Calls are synchronous on return. The caller owns `keys`; the library owns
+ * every workspace buffer (allocated per context, reused across calls).
+ */
+#ifndef LSORT_CUDA_H
+#define LSORT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSORT_OK 0
+#define LSORT_EINVAL 1
+#define LSORT_ENAN 2
+#define LSORT_ENOMEM 3
+#define LSORT_ECUDA 4
+#define LSORT_ENCCL 5
+#define LSORT_EINTERNAL 6
+
+#define LSORT_KEY_U64 0
+#define LSORT_KEY_F64 1
+
+#define LSORT_MEM_DEVICE 0
+#define LSORT_MEM_HOST 1
+
+#define LSORT_MAX_TREE 1024     /* max SplitterTree bucket budget */
+#define LSORT_MAX_RMI 2048      /* max RMI submodels / output buckets on the GPU */
+
+/* SortConfig plus GPU extensions. */
+typedef struct lsort_cfg {
+    uint32_t rmi_bucket_count;      /* 1024 */
+    uint32_t tree_bucket_count;     /* 256 */
+    uint64_t min_rmi_input;         /* 1e5 */
+    double max_duplicate_fraction;  /* 0.10 */
+    uint32_t radix_base_case;       /* 4096 (CPU reference; unused on the GPU) */
+    uint32_t insertion_base_case;   /* 16 */
+    uint32_t first_sample_cap;      /* 2*tree_bucket_count*16 = 8192 */
+    uint32_t rmi_sample_cap;        /* 1<<20 */
+    double sample_fraction;         /* 0.01 */
+    uint64_t seed;
+    uint32_t workers;               /* CPU reference only */
+    /* --- GPU extensions --- */
+    uint32_t base_case_capacity;    /* segments <= this go to the shared-memory base case (<=16384) */
+    uint32_t bucket_target;         /* adaptive fan-out: ~keys per output bucket; 0 = fixed fan-out */
+    uint32_t flags;                 /* reserved, 0 */
+} lsort_cfg;
+
+typedef struct lsort_rmi_header {
+    double root_slope, root_intercept;
+    double key_base, key_scale;     /* models.hpp:71-72 */
+    uint32_t submodels;
+    uint32_t reserved;
+} lsort_rmi_header;
+
+typedef struct lsort_rmi_entry {    /* LinearModel + clamp bounds, models.hpp:17-22,68-70 */
+    double slope, intercept, lo, hi;
+} lsort_rmi_entry;
+
+typedef struct lsort_tree {         /* SplitterTree, models.hpp:110-116 */
+    uint32_t levels, leaf_origin, nsplitters, bucket_count;
+    uint64_t tree[LSORT_MAX_TREE];        /* implicit heap, 1-based */
+    uint64_t splitters[LSORT_MAX_TREE];   /* strictly increasing */
+    uint32_t eq_offset[LSORT_MAX_TREE + 1];
+} lsort_tree;
+
+/* Partition model chosen by the Alg. 5 policy for one segment. */
+typedef struct lsort_model_info {
+    uint32_t kind;                  /* 0 learned, 1 tree */
+    uint32_t nbuckets;
+    uint64_t first_sample;          /* s1 */
+    uint64_t rmi_sample;            /* s2 (learned only) */
+    double duplicate_fraction;      /* of the first sample */
+} lsort_model_info;
+
+typedef struct lsort_stats {
+    double ms_total;                /* device time of the sort (events) */
+    double ms_h2d, ms_d2h;          /* LSORT_MEM_HOST transfers */
+    uint32_t levels;                /* distribution levels run */
+    uint32_t level0_kind;           /* 0 learned, 1 tree, 2 base case only */
+    uint64_t partitioned_keys;      /* keys moved by distribution passes (all levels) */
+    uint64_t base_case_keys;
+    uint64_t fill_keys;             /* keys written by equality/homogeneous fills */
+    uint64_t segments;              /* segments partitioned */
+    uint64_t base_segments;
+    uint64_t kernel_launches;
+    uint64_t h2d_bytes, d2h_bytes;
+} lsort_stats;
+
+typedef struct lsort_ctx lsort_ctx;
+
+void lsort_cfg_default(lsort_cfg* cfg);
+
+int lsort_cuda_ctx_create(lsort_ctx** out, int device, void* cuda_stream /* nullable */,
+                          size_t workspace_hint /* keys; 0 = grow on demand */);
+int lsort_cuda_ctx_destroy(lsort_ctx* ctx);
+const char* lsort_cuda_last_error(const lsort_ctx* ctx);
+/* Set the stream for subsequent calls (nullable = the context's own stream). */
+int lsort_cuda_set_stream(lsort_ctx* ctx, void* cuda_stream);
+
+/* In-place ascending sort of n keys (uint64 or float64). mem_kind DEVICE:
+ * keys is device memory; HOST: host memory, copied in and out inside the
+ * call. F64 keys containing NaN: returns LSORT_ENAN with the first NaN index
+ * in *nan_index_out and leaves the array unmodified. */
+int lsort_cuda_sort(lsort_ctx* ctx, void* keys, uint64_t n, int key_kind, int mem_kind,
+                    const lsort_cfg* cfg, lsort_stats* stats, uint64_t* nan_index_out);
+
+/* ---- unit entry points (parity tests; device pointers) ---- */
+int lsort_cuda_rmi_train(lsort_ctx* ctx, const uint64_t* d_sorted_sample, uint64_t s,
+                         uint32_t submodels, lsort_rmi_header* h_out,
+                         lsort_rmi_entry* h_entries_out);
+int lsort_cuda_classify_rmi(lsort_ctx* ctx, const lsort_rmi_header* h,
+                            const lsort_rmi_entry* entries, uint32_t bucket_count, double cdf_lo,
+                            double cdf_hi, const void* d_keys, uint64_t n, int key_kind,
+                            uint32_t* d_ids_opt, uint64_t* d_hist_opt);
+int lsort_cuda_tree_build(lsort_ctx* ctx, const uint64_t* d_sorted_sample, uint64_t s,
+                          uint32_t bucket_budget, int equality_mode, lsort_tree* h_out);
+int lsort_cuda_classify_tree(lsort_ctx* ctx, const lsort_tree* t, const void* d_keys, uint64_t n,
+                             int key_kind, uint32_t* d_ids_opt, uint64_t* d_hist_opt);
+/* Alg. 5 on a whole device array (level 0): first sample, duplicate
+ * fraction, RMI or tree. Learned params / tree are returned when non-null. */
+int lsort_cuda_build_model(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,
+                           const lsort_cfg* cfg, lsort_model_info* info,
+                           lsort_rmi_header* h_out, lsort_rmi_entry* entries_out,
+                           lsort_tree* tree_out);
+/* Device sort of a small device sample (the shared-memory block sort). */
+int lsort_cuda_block_sort(lsort_ctx* ctx, uint64_t* d_keys, uint64_t n);
+/* verify_sorted + multiset_hash on device keys (F64 keys hashed encoded). */
+int lsort_cuda_verify(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,
+                      uint64_t* first_violation /* 0 = sorted */, uint64_t* multiset_hash);
+
+/* ---- host-side synthetic generators (BASELINE.json configs) ---- */
+/* dist: 0 uniform, 1 normal, 2 lognormal(0,0.5), 3 exponential(2),
+ * 4 mixgauss, 5 rootdups, 6 twodups, 7 zipf(0.75), 8 lognormal(0,2).
+ * Writes elements [first, first+count) of the length-`total` dataset to host
+ * memory `out` (double for 0-4,8; uint64 for 5-7). */
+int lsort_gen_keys(int dist, uint64_t total, uint64_t seed, uint64_t first, uint64_t count,
+                   void* out, int threads);
+
+/* ---- multi-GPU phases (one process per GPU; collectives via the caller) ---- */
+/* Draw this rank's sample share (encoded keys) into device d_out[s]. */
+int lsort_cuda_dist_sample(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,
+                           uint64_t seed, uint64_t s, uint64_t* d_out);
+/* Sort the gathered global sample in place and train the global RMI with
+ * `buckets` output buckets (deterministic: identical on every rank). */
+int lsort_cuda_dist_train(lsort_ctx* ctx, uint64_t* d_sample, uint64_t s, uint32_t buckets,
+                          lsort_rmi_header* h_out, lsort_rmi_entry* entries_out);
+/* Histogram of the local shard under the global model: d_hist[buckets]. */
+int lsort_cuda_dist_histogram(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,
+                              const lsort_rmi_header* h, const lsort_rmi_entry* entries,
+                              uint64_t* d_hist);
+/* Partition the local shard into destination-major order in d_out (encoded
+ * keys): destination r receives buckets [bucket_bounds[r], bucket_bounds[r+1]).
+ * send_counts[p] (host) is filled. */
+int lsort_cuda_dist_partition(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,
+                              const lsort_rmi_header* h, const lsort_rmi_entry* entries,
+                              const uint32_t* bucket_bounds, uint32_t nranks, uint64_t* d_out,
+                              uint64_t* send_counts);
+/* Decode encoded keys to float64 in place (after a distributed sort). */
+int lsort_cuda_decode_inplace(lsort_ctx* ctx, uint64_t* d_keys, uint64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

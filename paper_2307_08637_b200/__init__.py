@@ -1,0 +1,284 @@
+"""B200-native parallel LearnedSort (AIPS2o, arXiv 2307.08637).
+
+Python host mirror of the reference's sort interface: ``sort(a, cfg)`` over a
+contiguous range of float64 / uint64 keys, in place, with
+``SortConfig``. Every call goes through the C-ABI of
+``liblsort_cuda.so`` (include/lsort_cuda.h): hand-written sm_100a kernels and a
+C++ orchestrator. Device arrays are torch CUDA tensors (float64, int64 or
+uint64); host arrays (numpy) are copied in and out inside the call. There is
+no CPU fallback: the native library must be built (``build()``).
+
+Error behaviour mirrors the reference: invalid arguments raise ValueError
+(std::invalid_argument, models.cpp:40-43,135-138); a NaN in float64 input
+raises ``NanError`` carrying the first NaN index (encode_doubles,
+keys.hpp:34-42) and leaves the array unmodified.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import threading
+from typing import Any
+
+import numpy as np
+
+from . import _native as N
+
+__all__ = ["SortConfig", "Context", "NanError", "LsortError", "sort", "generate", "DISTS",
+           "build", "default_context"]
+
+DISTS = {"uniform": 0, "normal": 1, "lognormal05": 2, "exponential2": 3, "mixgauss": 4,
+         "rootdups": 5, "twodups": 6, "zipf": 7, "lognormal2": 8}
+FLOAT_DISTS = {"uniform", "normal", "lognormal05", "exponential2", "mixgauss", "lognormal2"}
+
+
+def build(verbose: bool = False) -> str:
+    from .build import build as _b
+    return _b(verbose=verbose)
+
+
+class LsortError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"lsort error {code}: {msg}")
+        self.code = code
+
+
+class NanError(ValueError):
+    """NaN in float64 input (keys.hpp:34-42: rejected at ingestion with its index)."""
+
+    def __init__(self, index: int):
+        super().__init__(f"NaN at index {index}")
+        self.index = index
+
+
+@dataclasses.dataclass
+class SortConfig:
+    """SortConfig plus GPU extensions."""
+    rmi_bucket_count: int = 1024
+    tree_bucket_count: int = 256
+    min_rmi_input: int = 100_000
+    max_duplicate_fraction: float = 0.10
+    radix_base_case: int = 4096
+    insertion_base_case: int = 16
+    first_sample_cap: int = 2 * 256 * 16
+    rmi_sample_cap: int = 1 << 20
+    sample_fraction: float = 0.01
+    seed: int = 0x5EED
+    workers: int = 0
+    base_case_capacity: int = 16384
+    bucket_target: int = 4096
+    flags: int = 0
+
+    def to_c(self) -> N.lsort_cfg:
+        c = N.lsort_cfg()
+        for f in dataclasses.fields(self):
+            setattr(c, f.name, getattr(self, f.name))
+        return c
+
+
+def _check(ctx: "Context", rc: int):
+    if rc == N.LSORT_OK:
+        return
+    msg = N.lib().lsort_cuda_last_error(ctx._h).decode() if ctx._h else ""
+    if rc == N.LSORT_EINVAL:
+        raise ValueError(msg or "invalid argument")
+    raise LsortError(rc, msg)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _key_kind_of(arr) -> int:
+    dt = str(arr.dtype)
+    if "float64" in dt:
+        return N.KEY_F64
+    if "int64" in dt or "uint64" in dt:
+        return N.KEY_U64
+    raise ValueError(f"keys must be float64, int64 or uint64 (got {arr.dtype})")
+
+
+class Context:
+    """One lsort_ctx (workspace + stream) on one device. Not thread-safe."""
+
+    def __init__(self, device: int = 0, stream: Any = None, workspace_hint: int = 0):
+        L = N.lib()
+        h = C.c_void_p()
+        rc = L.lsort_cuda_ctx_create(C.byref(h), device, stream, workspace_hint)
+        if rc != N.LSORT_OK:
+            raise LsortError(rc, f"cannot create context on device {device}")
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().lsort_cuda_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- streams -----------------------------------------------------------
+    def _sync_stream(self):
+        """Run on torch's current stream so ordering with torch ops holds."""
+        torch = _torch()
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        N.lib().lsort_cuda_set_stream(self._h, C.c_void_p(s))
+
+    # -- the drop-in sort ----------------------------------------------------
+    def sort(self, keys, cfg: SortConfig | None = None) -> dict:
+        """In-place ascending sort. `keys`: torch CUDA tensor (device) or a
+        contiguous numpy array (host; copied in/out inside the call)."""
+        L = N.lib()
+        cfg_c = (cfg or SortConfig()).to_c()
+        stats = N.lsort_stats()
+        nan = C.c_uint64(0)
+        if isinstance(keys, np.ndarray):
+            if not keys.flags["C_CONTIGUOUS"]:
+                raise ValueError("host keys must be contiguous")
+            kind, mem, ptr, n = _key_kind_of(keys), N.MEM_HOST, keys.ctypes.data, keys.size
+            N.lib().lsort_cuda_set_stream(self._h, None)
+        else:
+            if not keys.is_cuda or not keys.is_contiguous():
+                raise ValueError("device keys must be a contiguous CUDA tensor")
+            self._sync_stream()
+            kind, mem, ptr, n = _key_kind_of(keys), N.MEM_DEVICE, keys.data_ptr(), keys.numel()
+        rc = L.lsort_cuda_sort(self._h, C.c_void_p(ptr), n, kind, mem, C.byref(cfg_c), C.byref(stats),
+                               C.byref(nan))
+        if rc == N.LSORT_ENAN:
+            raise NanError(int(nan.value))
+        _check(self, rc)
+        return stats.as_dict()
+
+    # -- unit entry points (parity tests) --------------------------------------
+    def rmi_train(self, d_sorted_sample, submodels: int):
+        """Rmi::train + enforce_monotonic on a sorted device sample -> packed P."""
+        self._sync_stream()
+        h = N.lsort_rmi_header()
+        e = np.zeros((submodels, 4), np.float64)
+        rc = N.lib().lsort_cuda_rmi_train(self._h, C.c_void_p(d_sorted_sample.data_ptr()),
+                                          d_sorted_sample.numel(), submodels, C.byref(h),
+                                          e.ctypes.data_as(C.c_void_p))
+        _check(self, rc)
+        return pack_rmi(h, e)
+
+    def classify_rmi(self, P: np.ndarray, submodels: int, bucket_count: int, d_keys, cdf_lo=0.0,
+                     cdf_hi=1.0, ids=True):
+        torch = _torch()
+        self._sync_stream()
+        h, e = unpack_rmi(P, submodels)
+        n = d_keys.numel()
+        d_ids = torch.empty(n, dtype=torch.int32, device=d_keys.device) if ids else None
+        d_hist = torch.empty(bucket_count, dtype=torch.int64, device=d_keys.device)
+        rc = N.lib().lsort_cuda_classify_rmi(
+            self._h, C.byref(h), e.ctypes.data_as(C.c_void_p), bucket_count, cdf_lo, cdf_hi,
+            C.c_void_p(d_keys.data_ptr()), n, _key_kind_of(d_keys),
+            C.c_void_p(d_ids.data_ptr()) if ids else None, C.c_void_p(d_hist.data_ptr()))
+        _check(self, rc)
+        return d_ids, d_hist
+
+    def tree_build(self, d_sorted_sample, budget: int, equality_mode: bool = True) -> N.lsort_tree:
+        self._sync_stream()
+        t = N.lsort_tree()
+        rc = N.lib().lsort_cuda_tree_build(self._h, C.c_void_p(d_sorted_sample.data_ptr()),
+                                           d_sorted_sample.numel(), budget, int(equality_mode),
+                                           C.byref(t))
+        _check(self, rc)
+        return t
+
+    def classify_tree(self, t: N.lsort_tree, d_keys, ids=True):
+        torch = _torch()
+        self._sync_stream()
+        n = d_keys.numel()
+        d_ids = torch.empty(n, dtype=torch.int32, device=d_keys.device) if ids else None
+        d_hist = torch.empty(t.bucket_count, dtype=torch.int64, device=d_keys.device)
+        rc = N.lib().lsort_cuda_classify_tree(self._h, C.byref(t), C.c_void_p(d_keys.data_ptr()), n,
+                                              _key_kind_of(d_keys),
+                                              C.c_void_p(d_ids.data_ptr()) if ids else None,
+                                              C.c_void_p(d_hist.data_ptr()))
+        _check(self, rc)
+        return d_ids, d_hist
+
+    def build_model(self, d_keys, cfg: SortConfig | None = None):
+        """Alg. 5 on the whole array: returns dict(kind, nbuckets, s1, s2, dup, P|tree)."""
+        self._sync_stream()
+        cfg_c = (cfg or SortConfig()).to_c()
+        info = N.lsort_model_info()
+        h = N.lsort_rmi_header()
+        e = np.zeros((N.MAX_RMI, 4), np.float64)
+        t = N.lsort_tree()
+        rc = N.lib().lsort_cuda_build_model(self._h, C.c_void_p(d_keys.data_ptr()), d_keys.numel(),
+                                            _key_kind_of(d_keys), C.byref(cfg_c), C.byref(info),
+                                            C.byref(h), e.ctypes.data_as(C.c_void_p), C.byref(t))
+        _check(self, rc)
+        out = {"kind": info.kind, "nbuckets": info.nbuckets, "s1": info.first_sample,
+               "s2": info.rmi_sample, "dup": info.duplicate_fraction}
+        if info.kind == 0:
+            out["P"] = pack_rmi(h, e[: h.submodels])
+            out["B"] = h.submodels
+        else:
+            out["tree"] = t
+        return out
+
+    def block_sort(self, d_keys):
+        self._sync_stream()
+        _check(self, N.lib().lsort_cuda_block_sort(self._h, C.c_void_p(d_keys.data_ptr()), d_keys.numel()))
+
+    def verify(self, d_keys):
+        """(sorted, first_violation, multiset_hash) -- verify.hpp:17-29 on device."""
+        self._sync_stream()
+        fv, hs = C.c_uint64(0), C.c_uint64(0)
+        rc = N.lib().lsort_cuda_verify(self._h, C.c_void_p(d_keys.data_ptr()), d_keys.numel(),
+                                       _key_kind_of(d_keys), C.byref(fv), C.byref(hs))
+        _check(self, rc)
+        return fv.value == 0, int(fv.value), int(hs.value)
+
+
+def pack_rmi(h: N.lsort_rmi_header, e: np.ndarray) -> np.ndarray:
+    """Packed P layout shared with the oracle: 4 header doubles then B x 4."""
+    P = np.empty(4 + e.size, np.float64)
+    P[:4] = [h.root_slope, h.root_intercept, h.key_base, h.key_scale]
+    P[4:] = e.reshape(-1)
+    return P
+
+
+def unpack_rmi(P: np.ndarray, B: int):
+    h = N.lsort_rmi_header(P[0], P[1], P[2], P[3], B, 0)
+    e = np.ascontiguousarray(P[4: 4 + 4 * B].reshape(B, 4))
+    return h, e
+
+
+_tls = threading.local()
+
+
+def default_context(device: int | None = None) -> Context:
+    if device is None:
+        device = _torch().cuda.current_device() if _torch().cuda.is_available() else 0
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]
+
+
+def sort(keys, cfg: SortConfig | None = None) -> dict:
+    """lsort::sort -- in-place ascending sort of float64 / uint64 keys."""
+    dev = keys.device.index if hasattr(keys, "device") and getattr(keys, "is_cuda", False) else None
+    return default_context(dev).sort(keys, cfg)
+
+
+def generate(dist: str, n: int, seed: int, first: int = 0, count: int | None = None,
+             threads: int = 0) -> np.ndarray:
+    """Synthetic config inputs (host, glibc libm, reference Rng stream)."""
+    count = n - first if count is None else count
+    out = np.empty(count, np.float64 if dist in FLOAT_DISTS else np.uint64)
+    rc = N.lib().lsort_gen_keys(DISTS[dist], n, seed, first, count, out.ctypes.data_as(C.c_void_p),
+                                threads)
+    if rc != N.LSORT_OK:
+        raise ValueError("generate: bad arguments")
+    return out

@@ -1,0 +1,863 @@
+// engine.cu -- host orchestrator and C-ABI of liblsort_cuda.so.
+//
+// Drives the AIPS2o recursion on the
+// GPU: per level, one batched launch sequence over all segments being
+// partitioned --
+//   build models -> classify+histogram -> scan/children -> scatter ->
+//   base cases + equality fills of the finished children
+// -- with the next level's segment list read back once per level. Workspace
+// (scratch keys, model arena, bucket counters, work lists) lives in the
+// context and is reused across calls. Out-of-place ping-pong between the
+// caller's buffer and one scratch buffer replaces IPS4o's in-place block
+// permutation; the result always lands in the caller's
+// buffer because base cases and fills write there directly.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/lsort_cuda.h"
+#include "kernels.cuh"
+
+using namespace lsort_dev;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    ~DevBuf() { if (p) cudaFree(p); }
+    bool ensure(size_t bytes) {
+        if (bytes <= cap) return true;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(bytes, 256);
+        want = want + want / 8;  // headroom against regrowth
+        if (cudaMalloc(&p, want) != cudaSuccess) {
+            cudaGetLastError();
+            if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); p = nullptr; return false; }
+            want = bytes;
+        }
+        cap = want;
+        return true;
+    }
+    template <class T> T* as() const { return (T*)p; }
+};
+
+struct PinBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    ~PinBuf() { if (p) cudaFreeHost(p); }
+    bool ensure(size_t bytes) {
+        if (bytes <= cap) return true;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(bytes * 2, 4096);
+        if (cudaMallocHost(&p, want) != cudaSuccess) { cudaGetLastError(); p = nullptr; return false; }
+        cap = want;
+        return true;
+    }
+    template <class T> T* as() const { return (T*)p; }
+};
+
+struct LsortError {
+    int code;
+    std::string msg;
+};
+
+#define CU(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e__ = (call);                                                              \
+        if (e__ != cudaSuccess)                                                                \
+            throw LsortError{LSORT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)}; \
+    } while (0)
+
+uint32_t fanout(uint64_t n, uint32_t cfg_count, uint32_t target) {
+    if (target == 0) return cfg_count;
+    uint64_t want = (n + target - 1) / target;
+    uint32_t b = 2;
+    while (b < want && b < cfg_count) b <<= 1;
+    return std::min(b, cfg_count);
+}
+
+uint64_t seg_seed_host(uint64_t cfg_seed, uint64_t begin, uint32_t depth) {
+    return splitmix64(cfg_seed ^ splitmix64(begin + ((uint64_t)depth << 48)));
+}
+uint64_t sample_size_host(double frac, uint32_t cap, uint64_t n) {
+    double v = frac * (double)n;
+    double c = (double)cap;
+    uint64_t s = (uint64_t)std::ceil(v < c ? v : c);
+    return s < 2 ? 2 : s;
+}
+
+}  // namespace
+
+struct lsort_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string err;
+    int depth = 0;  // nesting level (sample sorts run in a nested context)
+    DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux;
+    PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
+    std::unique_ptr<lsort_ctx> nested;
+    cudaEvent_t ev[6] = {};
+    uint64_t launches = 0;
+};
+
+namespace {
+
+struct SegPlan {
+    uint64_t begin, n;
+    uint32_t depth, flags;
+};
+
+void validate_cfg(const lsort_cfg& c) {
+    auto pow2 = [](uint32_t v) { return v >= 2 && (v & (v - 1)) == 0; };
+    if (!pow2(c.rmi_bucket_count) || c.rmi_bucket_count > LSORT_MAX_RMI)
+        throw LsortError{LSORT_EINVAL, "rmi_bucket_count must be a power of two in [2, 2048]"};
+    if (!pow2(c.tree_bucket_count) || c.tree_bucket_count > LSORT_MAX_TREE)
+        throw LsortError{LSORT_EINVAL, "tree_bucket_count must be a power of two in [2, 1024]"};
+    if (c.first_sample_cap < 2 || c.first_sample_cap > kSmallSampleCap)
+        throw LsortError{LSORT_EINVAL, "first_sample_cap must be in [2, 16384]"};
+    if (c.rmi_sample_cap < 2) throw LsortError{LSORT_EINVAL, "rmi_sample_cap must be >= 2"};
+    if (!(c.sample_fraction > 0.0) || c.sample_fraction > 1.0)
+        throw LsortError{LSORT_EINVAL, "sample_fraction must be in (0, 1]"};
+    if (c.base_case_capacity < 1024 || c.base_case_capacity > 16384)
+        throw LsortError{LSORT_EINVAL, "base_case_capacity must be in [1024, 16384]"};
+    if (c.insertion_base_case > c.radix_base_case)
+        throw LsortError{LSORT_EINVAL, "insertion_base_case must be <= radix_base_case"};
+}
+
+DevCfg dev_cfg(const lsort_cfg& c) {
+    DevCfg d;
+    d.min_rmi_input = c.min_rmi_input;
+    d.max_dup = c.max_duplicate_fraction;
+    d.sample_fraction = c.sample_fraction;
+    d.first_sample_cap = c.first_sample_cap;
+    d.rmi_sample_cap = c.rmi_sample_cap;
+    d.seed = c.seed;
+    return d;
+}
+
+struct Engine {
+    lsort_ctx* C;
+    const lsort_cfg& cfg;
+    cudaStream_t st;
+    Engine(lsort_ctx* c, const lsort_cfg& g) : C(c), cfg(g), st(c->stream) {}
+
+    uint32_t rmi_b(uint64_t n) const { return fanout(n, cfg.rmi_bucket_count, cfg.bucket_target); }
+    uint32_t tree_k(uint64_t n) const { return fanout(n, cfg.tree_bucket_count, cfg.bucket_target); }
+    bool is_big(const SegPlan& s) const {
+        if (s.flags & kSegForceRadix) return false;
+        if (s.n < cfg.min_rmi_input) return false;
+        return sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, s.n) > kSmallSampleCap;
+    }
+
+    void launched(int k = 1) { C->launches += k; }
+
+    // Sort the device buffer `sample` (u64) with a nested context.
+    void nested_sort(uint64_t* sample, uint64_t s) {
+        if (C->depth >= 2) throw LsortError{LSORT_EINTERNAL, "sample sort nesting too deep"};
+        if (!C->nested) {
+            C->nested.reset(new lsort_ctx());
+            C->nested->device = C->device;
+            C->nested->depth = C->depth + 1;
+            for (auto& e : C->nested->ev) CU(cudaEventCreate(&e));
+        }
+        C->nested->stream = C->stream;
+        lsort_cfg nc = cfg;
+        nc.seed = splitmix64(cfg.seed ^ 0x5a3c9e1f0b7d2468ull);
+        Engine ne(C->nested.get(), nc);
+        ne.sort(sample, s, false, nullptr);
+        C->launches += C->nested->launches;
+        C->nested->launches = 0;
+    }
+
+    // Model for one big segment (sample > one CTA): first sample + policy on
+    // one CTA; for the learned branch, a device-wide gather, a nested sort of
+    // the RMI sample and a single-CTA training pass.
+    void big_model(const SegDesc* dseg, const SegPlan& sp, const SegDesc& hseg, const void* src, bool f64) {
+        DevCfg dc = dev_cfg(cfg);
+        launch_first_sample(dseg, src, f64, C->models.as<uint8_t>(), dc, st);
+        launched();
+        ModelHdr h;
+        CU(cudaMemcpyAsync(&h, C->models.as<uint8_t>() + hseg.model_off, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (h.kind != kLearned) return;
+        uint64_t s1 = h.s1, s2 = h.s2;
+        if (!C->sample.ensure(s2 * 8)) throw LsortError{LSORT_ENOMEM, "sample buffer"};
+        uint64_t seed = seg_seed_host(cfg.seed, sp.begin, sp.depth);
+        launch_gather(dseg, src, f64, seed, s1, s2, C->sample.as<uint64_t>(), st);
+        launched();
+        nested_sort(C->sample.as<uint64_t>(), s2);
+        launch_train_rmi_global(C->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
+                                hseg.rmi_b, st);
+        launched();
+    }
+
+    // Sort n keys at `keys` (device) in place. Returns LSORT_ENAN via throw.
+    void sort(void* keys, uint64_t n, bool f64, lsort_stats* stats) {
+        if (n < 2) return;
+        if (!C->ctrl.ensure(sizeof(Ctrl)) || !C->hctrl.ensure(sizeof(Ctrl)))
+            throw LsortError{LSORT_ENOMEM, "control block"};
+        Ctrl* dctrl = C->ctrl.as<Ctrl>();
+        CU(cudaMemsetAsync(dctrl, 0, sizeof(Ctrl), st));
+        CU(cudaMemsetAsync(&dctrl->nan_index, 0xff, 8, st));
+        Ctrl* hc = C->hctrl.as<Ctrl>();
+        const uint32_t cap = cfg.base_case_capacity;
+        if (n <= cap) {
+            launch_small_sort(keys, n, f64, nullptr, dctrl, st);
+            launched();
+            CU(cudaMemcpyAsync(hc, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            if (hc->nan_index != ~0ull) throw LsortError{LSORT_ENAN, std::to_string(hc->nan_index)};
+            if (stats) { stats->level0_kind = 2; stats->base_case_keys += n; }
+            return;
+        }
+        if (!C->scratch.ensure(n * 8)) throw LsortError{LSORT_ENOMEM, "scratch keys"};
+        const uint32_t depth_cap =
+            (uint32_t)std::ceil(std::log2((double)n) / std::log2((double)cfg.tree_bucket_count)) + 4;
+        std::vector<SegPlan> segs{{0, n, 0, 0}};
+        void* src = keys;
+        bool src_f64 = f64;
+        uint64_t* dst = C->scratch.as<uint64_t>();
+        uint32_t level = 0;
+        DevCfg dc = dev_cfg(cfg);
+        while (!segs.empty()) {
+            const uint32_t ns = (uint32_t)segs.size();
+            // ---- plan the level on the host
+            if (!C->hsegs.ensure(ns * sizeof(SegDesc)) || !C->hprefix.ensure((ns + 1) * 8) ||
+                !C->hidx.ensure(ns * 4))
+                throw LsortError{LSORT_ENOMEM, "host plan"};
+            SegDesc* hs = C->hsegs.as<SegDesc>();
+            uint64_t* hp = C->hprefix.as<uint64_t>();
+            uint32_t* hi = C->hidx.as<uint32_t>();
+            uint64_t model_bytes = 0, nbuckets = 0, ntiles = 0;
+            uint32_t max_payload = 0, max_nb = 0, nsmall = 0;
+            std::vector<uint32_t> bigs;
+            for (uint32_t i = 0; i < ns; ++i) {
+                const SegPlan& s = segs[i];
+                SegDesc& d = hs[i];
+                d.begin = s.begin;
+                d.n = s.n;
+                d.depth = s.depth;
+                d.flags = s.flags;
+                d.rmi_b = rmi_b(s.n);
+                d.tree_k = tree_k(s.n);
+                uint32_t payload, nb;
+                if (s.flags & kSegForceRadix) {
+                    payload = 0;
+                    nb = 1u << kRadixBits;
+                } else {
+                    uint32_t tp = (uint32_t)((tree_payload_bytes(d.tree_k, d.tree_k - 1) + 15) & ~15ull);
+                    payload = std::max<uint32_t>(32u * d.rmi_b, tp);
+                    nb = std::max<uint32_t>(d.rmi_b, 2 * d.tree_k - 1);
+                }
+                d.nb_max = nb;
+                d.model_off = model_bytes;
+                model_bytes += sizeof(ModelHdr) + payload;
+                d.bucket_off = nbuckets;
+                nbuckets += nb;
+                max_payload = std::max(max_payload, payload);
+                max_nb = std::max(max_nb, nb);
+                hp[i] = ntiles;
+                ntiles += (s.n + kTileKeys - 1) / kTileKeys;
+                if (is_big(s)) bigs.push_back(i);
+                else hi[nsmall++] = i;
+            }
+            hp[ns] = ntiles;
+            const uint64_t list_cap = nbuckets;
+            if (!C->segs.ensure(ns * sizeof(SegDesc)) || !C->tile_prefix.ensure((ns + 1) * 8) ||
+                !C->idx.ensure(ns * 4) || !C->models.ensure(model_bytes) || !C->buckets.ensure(nbuckets * 8) ||
+                !C->rec.ensure(list_cap * sizeof(SegOut)) || !C->fill.ensure(list_cap * sizeof(FillItem)) ||
+                !C->base[0].ensure(list_cap * sizeof(BaseItem)) || !C->base[1].ensure(list_cap * sizeof(BaseItem)) ||
+                !C->base[2].ensure(list_cap * sizeof(BaseItem)))
+                throw LsortError{LSORT_ENOMEM, "level workspace"};
+            CU(cudaMemcpyAsync(C->segs.p, hs, ns * sizeof(SegDesc), cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(C->tile_prefix.p, hp, (ns + 1) * 8, cudaMemcpyHostToDevice, st));
+            if (nsmall) CU(cudaMemcpyAsync(C->idx.p, hi, nsmall * 4, cudaMemcpyHostToDevice, st));
+            CU(cudaMemsetAsync(C->buckets.p, 0, nbuckets * 8, st));
+            CU(cudaMemsetAsync(&dctrl->n_rec, 0, offsetof(Ctrl, keys_fill) - offsetof(Ctrl, n_rec), st));
+
+            LevelParams p{};
+            p.segs = C->segs.as<SegDesc>();
+            p.nsegs = ns;
+            p.tile_prefix = C->tile_prefix.as<uint64_t>();
+            p.ntiles = ntiles;
+            p.models = C->models.as<uint8_t>();
+            p.buckets = C->buckets.as<unsigned long long>();
+            p.src = src;
+            p.dst = dst;
+            p.ctrl = dctrl;
+            p.rec = C->rec.as<SegOut>();
+            for (int c = 0; c < 3; ++c) p.base[c] = C->base[c].as<BaseItem>();
+            p.fill = C->fill.as<FillItem>();
+            p.base_cap[0] = std::min<uint32_t>(1024, cap);
+            p.base_cap[1] = std::min<uint32_t>(4096, cap);
+            p.base_cap[2] = cap;
+            p.depth_cap = depth_cap;
+            p.list_cap = (uint32_t)std::min<uint64_t>(list_cap, 0xffffffffu);
+
+            // ---- models
+            launch_build_models(p.segs, C->idx.as<uint32_t>(), nsmall, src, src_f64, C->models.as<uint8_t>(), dc, 0,
+                                st);
+            if (nsmall) launched();
+            for (uint32_t b : bigs) big_model(p.segs + b, segs[b], hs[b], src, src_f64);
+            // ---- partition
+            const int nsm = num_sms();
+            int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 4);
+            int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
+            launch_classify_hist(p, src_f64, (int)max_payload, grid_h, st);
+            launch_scan_children(p, st);
+            launch_scatter(p, src_f64, (int)max_payload, (int)max_nb, grid_s, st);
+            launch_base_cases(p, dst, keys, nullptr, f64, 1, st);
+            launch_fill(p, keys, f64, nsm * 4, st);
+            launched(7);
+            CU(cudaMemcpyAsync(hc, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            CU(cudaGetLastError());
+            if (hc->nan_index != ~0ull) throw LsortError{LSORT_ENAN, std::to_string(hc->nan_index)};
+            if (hc->err) throw LsortError{LSORT_EINTERNAL, "work list overflow (" + std::to_string(hc->err) + ")"};
+            if (level == 0 && stats) {
+                ModelHdr h0;
+                CU(cudaMemcpy(&h0, C->models.p, sizeof(h0), cudaMemcpyDeviceToHost));
+                stats->level0_kind = h0.kind == kLearned ? 0 : 1;
+            }
+            if (stats) {
+                stats->levels = level + 1;
+                stats->segments += ns;
+                uint64_t moved = 0;
+                for (uint32_t i = 0; i < ns; ++i) moved += segs[i].n;
+                stats->partitioned_keys += moved;
+                stats->base_case_keys += hc->keys_base;
+                stats->fill_keys += hc->keys_fill;
+                stats->base_segments += (uint64_t)hc->n_base[0] + hc->n_base[1] + hc->n_base[2];
+            }
+            // ---- next level
+            uint32_t nrec = hc->n_rec;
+            segs.clear();
+            if (nrec) {
+                if (!C->hrec.ensure(nrec * sizeof(SegOut))) throw LsortError{LSORT_ENOMEM, "host rec list"};
+                CU(cudaMemcpyAsync(C->hrec.p, C->rec.p, nrec * sizeof(SegOut), cudaMemcpyDeviceToHost, st));
+                CU(cudaStreamSynchronize(st));
+                const SegOut* r = C->hrec.as<SegOut>();
+                segs.reserve(nrec);
+                for (uint32_t i = 0; i < nrec; ++i) segs.push_back({r[i].begin, r[i].n, r[i].depth, r[i].flags});
+                std::sort(segs.begin(), segs.end(),
+                          [](const SegPlan& a, const SegPlan& b) { return a.begin < b.begin; });
+            }
+            // ping-pong: this level's output becomes the next level's input
+            src = dst;
+            src_f64 = false;
+            dst = (dst == C->scratch.as<uint64_t>()) ? (uint64_t*)keys : C->scratch.as<uint64_t>();
+            ++level;
+            if (level > 64) throw LsortError{LSORT_EINTERNAL, "recursion did not terminate"};
+        }
+    }
+};
+
+int fail(lsort_ctx* ctx, const LsortError& e) {
+    if (ctx) ctx->err = e.msg;
+    return e.code;
+}
+
+lsort_cfg cfg_or_default(const lsort_cfg* cfg) {
+    lsort_cfg c;
+    if (cfg) c = *cfg;
+    else lsort_cfg_default(&c);
+    return c;
+}
+
+}  // namespace
+
+// ======================================================================= C-ABI
+extern "C" {
+
+void lsort_cfg_default(lsort_cfg* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->rmi_bucket_count = 1024;
+    c->tree_bucket_count = 256;
+    c->min_rmi_input = 100000;
+    c->max_duplicate_fraction = 0.10;
+    c->radix_base_case = 4096;
+    c->insertion_base_case = 16;
+    c->first_sample_cap = 2 * 256 * 16;
+    c->rmi_sample_cap = 1u << 20;
+    c->sample_fraction = 0.01;
+    c->seed = 0x5EEDull;
+    c->workers = 0;
+    c->base_case_capacity = 16384;
+    c->bucket_target = 4096;
+    c->flags = 0;
+}
+
+int lsort_cuda_ctx_create(lsort_ctx** out, int device, void* stream, size_t workspace_hint) {
+    if (!out) return LSORT_EINVAL;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) { cudaGetLastError(); return LSORT_ECUDA; }
+    if (device < 0 || device >= ndev) return LSORT_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return LSORT_ECUDA;
+    lsort_ctx* c = new lsort_ctx();
+    c->device = device;
+    try {
+        kernels_init();
+        if (stream) c->stream = (cudaStream_t)stream;
+        else {
+            CU(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+            c->stream = c->own_stream;
+        }
+        for (auto& e : c->ev) CU(cudaEventCreate(&e));
+        if (workspace_hint && !c->scratch.ensure(workspace_hint * 8)) throw LsortError{LSORT_ENOMEM, "workspace"};
+    } catch (const LsortError& e) {
+        delete c;
+        return e.code;
+    }
+    *out = c;
+    return LSORT_OK;
+}
+
+int lsort_cuda_ctx_destroy(lsort_ctx* c) {
+    if (!c) return LSORT_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto& e : c->ev) if (e) cudaEventDestroy(e);
+    if (c->nested) for (auto& e : c->nested->ev) if (e) cudaEventDestroy(e);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+    return LSORT_OK;
+}
+
+const char* lsort_cuda_last_error(const lsort_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int lsort_cuda_set_stream(lsort_ctx* c, void* stream) {
+    if (!c) return LSORT_EINVAL;
+    c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+    return LSORT_OK;
+}
+
+int lsort_cuda_sort(lsort_ctx* C, void* keys, uint64_t n, int key_kind, int mem_kind, const lsort_cfg* cfgp,
+                    lsort_stats* stats, uint64_t* nan_index_out) {
+    if (!C) return LSORT_EINVAL;
+    C->err.clear();
+    if (nan_index_out) *nan_index_out = ~0ull;
+    if (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_F64) return fail(C, {LSORT_EINVAL, "key_kind"});
+    if (mem_kind != LSORT_MEM_DEVICE && mem_kind != LSORT_MEM_HOST) return fail(C, {LSORT_EINVAL, "mem_kind"});
+    if (n > 0 && !keys) return fail(C, {LSORT_EINVAL, "null keys"});
+    lsort_cfg cfg = cfg_or_default(cfgp);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    try {
+        validate_cfg(cfg);
+        CU(cudaSetDevice(C->device));
+        const bool f64 = key_kind == LSORT_KEY_F64;
+        C->launches = 0;
+        void* dkeys = keys;
+        cudaStream_t st = C->stream;
+        if (mem_kind == LSORT_MEM_HOST) {
+            if (!C->data.ensure(std::max<uint64_t>(n, 1) * 8)) throw LsortError{LSORT_ENOMEM, "device keys"};
+            dkeys = C->data.p;
+            CU(cudaEventRecord(C->ev[2], st));
+            CU(cudaMemcpyAsync(dkeys, keys, n * 8, cudaMemcpyHostToDevice, st));
+            CU(cudaEventRecord(C->ev[3], st));
+        }
+        CU(cudaEventRecord(C->ev[0], st));
+        Engine E(C, cfg);
+        E.sort(dkeys, n, f64, stats);
+        CU(cudaEventRecord(C->ev[1], st));
+        if (mem_kind == LSORT_MEM_HOST) {
+            CU(cudaMemcpyAsync(keys, dkeys, n * 8, cudaMemcpyDeviceToHost, st));
+            CU(cudaEventRecord(C->ev[4], st));
+        }
+        CU(cudaStreamSynchronize(st));
+        if (stats) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, C->ev[0], C->ev[1]);
+            stats->ms_total = ms;
+            if (mem_kind == LSORT_MEM_HOST) {
+                cudaEventElapsedTime(&ms, C->ev[2], C->ev[3]);
+                stats->ms_h2d = ms;
+                cudaEventElapsedTime(&ms, C->ev[1], C->ev[4]);
+                stats->ms_d2h = ms;
+                stats->h2d_bytes = n * 8;
+                stats->d2h_bytes = n * 8;
+            }
+            stats->kernel_launches = C->launches;
+        }
+    } catch (const LsortError& e) {
+        if (e.code == LSORT_ENAN) {
+            if (nan_index_out) *nan_index_out = std::stoull(e.msg);
+            C->err = "NaN at index " + e.msg;
+            cudaStreamSynchronize(C->stream);
+            return LSORT_ENAN;
+        }
+        cudaStreamSynchronize(C->stream);
+        cudaGetLastError();
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+// ---------------------------------------------------------------- unit entries
+static void upload_learned(lsort_ctx* C, const lsort_rmi_header* h, const lsort_rmi_entry* e, uint32_t bucket_count,
+                           double cdf_lo, double cdf_hi) {
+    uint32_t B = h->submodels;
+    size_t bytes = sizeof(ModelHdr) + 32 * (size_t)B;
+    if (!C->models.ensure(bytes) || !C->hmodel.ensure(bytes)) throw LsortError{LSORT_ENOMEM, "model"};
+    ModelHdr* m = C->hmodel.as<ModelHdr>();
+    std::memset(m, 0, sizeof(ModelHdr));
+    m->kind = kLearned;
+    m->nbuckets = bucket_count;
+    m->B = B;
+    m->root_slope = h->root_slope;
+    m->root_icpt = h->root_intercept;
+    m->key_base = h->key_base;
+    m->key_scale = h->key_scale;
+    double span = cdf_hi - cdf_lo;  // Learned::inv_span (models.hpp:134-137)
+    m->cdf_lo = cdf_lo;
+    m->inv_span = span > 0.0 ? 1.0 / span : 0.0;
+    std::memcpy((uint8_t*)m + sizeof(ModelHdr), e, 32 * (size_t)B);
+    CU(cudaMemcpyAsync(C->models.p, m, bytes, cudaMemcpyHostToDevice, C->stream));
+}
+
+static size_t upload_tree(lsort_ctx* C, const lsort_tree* t) {
+    size_t payload = (tree_payload_bytes(t->leaf_origin, t->nsplitters) + 15) & ~15ull;
+    size_t bytes = sizeof(ModelHdr) + payload;
+    if (!C->models.ensure(bytes) || !C->hmodel.ensure(bytes)) throw LsortError{LSORT_ENOMEM, "model"};
+    ModelHdr* m = C->hmodel.as<ModelHdr>();
+    std::memset(m, 0, bytes);
+    m->kind = kTree;
+    m->nbuckets = t->bucket_count;
+    m->levels = t->levels;
+    m->leaf_origin = t->leaf_origin;
+    m->nsplit = t->nsplitters;
+    uint64_t* tree = (uint64_t*)((uint8_t*)m + sizeof(ModelHdr));
+    std::memcpy(tree, t->tree, 8 * (size_t)t->leaf_origin);
+    std::memcpy(tree + t->leaf_origin, t->splitters, 8 * (size_t)t->nsplitters);
+    std::memcpy(tree + t->leaf_origin + t->nsplitters, t->eq_offset, 4 * ((size_t)t->nsplitters + 1));
+    CU(cudaMemcpyAsync(C->models.p, m, bytes, cudaMemcpyHostToDevice, C->stream));
+    return payload;
+}
+
+static void download_tree(lsort_ctx* C, const uint8_t* dmodel, lsort_tree* out) {
+    if (!C->hmodel.ensure(sizeof(ModelHdr) + 24 * LSORT_MAX_TREE)) throw LsortError{LSORT_ENOMEM, "host model"};
+    CU(cudaMemcpyAsync(C->hmodel.p, dmodel, sizeof(ModelHdr) + 20 * LSORT_MAX_TREE + 16, cudaMemcpyDeviceToHost,
+                       C->stream));
+    CU(cudaStreamSynchronize(C->stream));
+    const ModelHdr* m = C->hmodel.as<ModelHdr>();
+    std::memset(out, 0, sizeof(*out));
+    out->levels = m->levels;
+    out->leaf_origin = m->leaf_origin;
+    out->nsplitters = m->nsplit;
+    out->bucket_count = m->nbuckets;
+    const uint64_t* tree = (const uint64_t*)((const uint8_t*)m + sizeof(ModelHdr));
+    std::memcpy(out->tree, tree, 8 * (size_t)m->leaf_origin);
+    std::memcpy(out->splitters, tree + m->leaf_origin, 8 * (size_t)m->nsplit);
+    std::memcpy(out->eq_offset, tree + m->leaf_origin + m->nsplit, 4 * ((size_t)m->nsplit + 1));
+}
+
+static void download_learned(lsort_ctx* C, const uint8_t* dmodel, uint32_t B, lsort_rmi_header* h,
+                             lsort_rmi_entry* e) {
+    size_t bytes = sizeof(ModelHdr) + 32 * (size_t)B;
+    if (!C->hmodel.ensure(bytes)) throw LsortError{LSORT_ENOMEM, "host model"};
+    CU(cudaMemcpyAsync(C->hmodel.p, dmodel, bytes, cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaStreamSynchronize(C->stream));
+    const ModelHdr* m = C->hmodel.as<ModelHdr>();
+    if (h) {
+        h->root_slope = m->root_slope;
+        h->root_intercept = m->root_icpt;
+        h->key_base = m->key_base;
+        h->key_scale = m->key_scale;
+        h->submodels = m->B;
+        h->reserved = 0;
+    }
+    if (e) std::memcpy(e, (const uint8_t*)m + sizeof(ModelHdr), 32 * (size_t)B);
+}
+
+int lsort_cuda_rmi_train(lsort_ctx* C, const uint64_t* d_sample, uint64_t s, uint32_t B, lsort_rmi_header* h_out,
+                         lsort_rmi_entry* e_out) {
+    if (!C) return LSORT_EINVAL;
+    if (s < 2 || B == 0) return fail(C, {LSORT_EINVAL, "Rmi::train: sample must hold at least 2 keys / B > 0"});
+    if (B > LSORT_MAX_RMI || s > 0xffffffffull) return fail(C, {LSORT_EINVAL, "Rmi::train: size limits"});
+    try {
+        CU(cudaSetDevice(C->device));
+        if (!C->models.ensure(sizeof(ModelHdr) + 32 * (size_t)B)) throw LsortError{LSORT_ENOMEM, "model"};
+        CU(cudaMemsetAsync(C->models.p, 0, sizeof(ModelHdr), C->stream));
+        launch_train_rmi_global(d_sample, s, B, C->models.as<uint8_t>(), B, C->stream);
+        CU(cudaGetLastError());
+        download_learned(C, C->models.as<uint8_t>(), B, h_out, e_out);
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_classify_rmi(lsort_ctx* C, const lsort_rmi_header* h, const lsort_rmi_entry* e, uint32_t bucket_count,
+                            double cdf_lo, double cdf_hi, const void* d_keys, uint64_t n, int key_kind,
+                            uint32_t* d_ids, uint64_t* d_hist) {
+    if (!C || !h || !e || bucket_count == 0 || h->submodels == 0 || h->submodels > LSORT_MAX_RMI)
+        return fail(C, {LSORT_EINVAL, "classify_rmi: bad model"});
+    try {
+        CU(cudaSetDevice(C->device));
+        upload_learned(C, h, e, bucket_count, cdf_lo, cdf_hi);
+        if (d_hist) CU(cudaMemsetAsync(d_hist, 0, 8 * (size_t)bucket_count, C->stream));
+        if (n) launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, d_ids,
+                                   (unsigned long long*)d_hist, 32 * (int)h->submodels, C->stream);
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+    } catch (const LsortError& er) {
+        return fail(C, er);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_tree_build(lsort_ctx* C, const uint64_t* d_sample, uint64_t s, uint32_t budget, int eq_mode,
+                          lsort_tree* out) {
+    if (!C || !out) return LSORT_EINVAL;
+    if (s == 0) return fail(C, {LSORT_EINVAL, "SplitterTree::build: sample must not be empty"});
+    if (budget < 2 || (budget & (budget - 1)) || budget > LSORT_MAX_TREE)
+        return fail(C, {LSORT_EINVAL, "SplitterTree::build: bucket budget must be a power of two >= 2"});
+    if (s > 16384) return fail(C, {LSORT_EINVAL, "SplitterTree::build: GPU sample limit 16384"});
+    try {
+        CU(cudaSetDevice(C->device));
+        if (!C->models.ensure(sizeof(ModelHdr) + 24 * LSORT_MAX_TREE + 16)) throw LsortError{LSORT_ENOMEM, "model"};
+        launch_tree_build(d_sample, s, budget, eq_mode, C->models.as<uint8_t>(), C->stream);
+        CU(cudaGetLastError());
+        download_tree(C, C->models.as<uint8_t>(), out);
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_classify_tree(lsort_ctx* C, const lsort_tree* t, const void* d_keys, uint64_t n, int key_kind,
+                             uint32_t* d_ids, uint64_t* d_hist) {
+    if (!C || !t || t->leaf_origin == 0 || t->leaf_origin > LSORT_MAX_TREE) return LSORT_EINVAL;
+    try {
+        CU(cudaSetDevice(C->device));
+        size_t payload = upload_tree(C, t);
+        if (d_hist) CU(cudaMemsetAsync(d_hist, 0, 8 * (size_t)t->bucket_count, C->stream));
+        if (n) launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, d_ids,
+                                   (unsigned long long*)d_hist, (int)payload, C->stream);
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+    } catch (const LsortError& er) {
+        return fail(C, er);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_build_model(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, const lsort_cfg* cfgp,
+                           lsort_model_info* info, lsort_rmi_header* h_out, lsort_rmi_entry* e_out,
+                           lsort_tree* tree_out) {
+    if (!C) return LSORT_EINVAL;
+    if (n < 2) return fail(C, {LSORT_EINVAL, "build_model: n < 2"});
+    lsort_cfg cfg = cfg_or_default(cfgp);
+    try {
+        validate_cfg(cfg);
+        CU(cudaSetDevice(C->device));
+        Engine E(C, cfg);
+        SegPlan sp{0, n, 0, 0};
+        SegDesc d{};
+        d.begin = 0;
+        d.n = n;
+        d.rmi_b = E.rmi_b(n);
+        d.tree_k = E.tree_k(n);
+        d.model_off = 0;
+        size_t bytes = sizeof(ModelHdr) + std::max<size_t>(32 * (size_t)d.rmi_b, 24 * LSORT_MAX_TREE + 16);
+        if (!C->models.ensure(bytes) || !C->segs.ensure(sizeof(SegDesc)) || !C->idx.ensure(4))
+            throw LsortError{LSORT_ENOMEM, "model"};
+        CU(cudaMemsetAsync(C->models.p, 0, bytes, C->stream));
+        CU(cudaMemcpyAsync(C->segs.p, &d, sizeof(d), cudaMemcpyHostToDevice, C->stream));
+        uint32_t zero = 0;
+        CU(cudaMemcpyAsync(C->idx.p, &zero, 4, cudaMemcpyHostToDevice, C->stream));
+        const bool f64 = key_kind == LSORT_KEY_F64;
+        if (E.is_big(sp)) E.big_model(C->segs.as<SegDesc>(), sp, d, d_keys, f64);
+        else launch_build_models(C->segs.as<SegDesc>(), C->idx.as<uint32_t>(), 1, d_keys, f64,
+                                 C->models.as<uint8_t>(), dev_cfg(cfg), 0, C->stream);
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+        ModelHdr h;
+        CU(cudaMemcpy(&h, C->models.p, sizeof(h), cudaMemcpyDeviceToHost));
+        if (info) {
+            info->kind = h.kind;
+            info->nbuckets = h.nbuckets;
+            info->first_sample = h.s1;
+            info->rmi_sample = h.kind == kLearned ? h.s2 : 0;
+            info->duplicate_fraction = h.dup;
+        }
+        if (h.kind == kLearned) download_learned(C, C->models.as<uint8_t>(), h.B, h_out, e_out);
+        else if (tree_out) download_tree(C, C->models.as<uint8_t>(), tree_out);
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_block_sort(lsort_ctx* C, uint64_t* d_keys, uint64_t n) {
+    if (!C) return LSORT_EINVAL;
+    if (n > 16384) return fail(C, {LSORT_EINVAL, "block sort holds at most 16384 keys"});
+    try {
+        CU(cudaSetDevice(C->device));
+        if (n > 1) launch_block_sort(d_keys, n, C->stream);
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_verify(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, uint64_t* first_violation,
+                      uint64_t* hash) {
+    if (!C) return LSORT_EINVAL;
+    try {
+        CU(cudaSetDevice(C->device));
+        if (!C->ctrl.ensure(sizeof(Ctrl)) || !C->hctrl.ensure(sizeof(Ctrl))) throw LsortError{LSORT_ENOMEM, "ctrl"};
+        Ctrl* d = C->ctrl.as<Ctrl>();
+        CU(cudaMemsetAsync(d, 0, sizeof(Ctrl), C->stream));
+        CU(cudaMemsetAsync(&d->verify_first, 0xff, 8, C->stream));
+        if (n) launch_verify(d_keys, n, key_kind == LSORT_KEY_F64, d, C->stream);
+        CU(cudaMemcpyAsync(C->hctrl.p, d, sizeof(Ctrl), cudaMemcpyDeviceToHost, C->stream));
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+        const Ctrl* h = C->hctrl.as<Ctrl>();
+        if (first_violation) *first_violation = h->verify_first == ~0ull ? 0 : h->verify_first;
+        if (hash) *hash = h->verify_hash;
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_decode_inplace(lsort_ctx* C, uint64_t* d_keys, uint64_t n) {
+    if (!C) return LSORT_EINVAL;
+    try {
+        CU(cudaSetDevice(C->device));
+        if (n) launch_decode(d_keys, n, C->stream);
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+// ------------------------------------------------------------ multi-GPU phases
+int lsort_cuda_dist_sample(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, uint64_t seed, uint64_t s,
+                           uint64_t* d_out) {
+    if (!C || n == 0) return LSORT_EINVAL;
+    try {
+        CU(cudaSetDevice(C->device));
+        SegDesc d{};
+        d.begin = 0;
+        d.n = n;
+        if (!C->segs.ensure(sizeof(SegDesc))) throw LsortError{LSORT_ENOMEM, "seg"};
+        CU(cudaMemcpyAsync(C->segs.p, &d, sizeof(d), cudaMemcpyHostToDevice, C->stream));
+        if (s) launch_gather(C->segs.as<SegDesc>(), d_keys, key_kind == LSORT_KEY_F64, seed, 0, s, d_out, C->stream);
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_dist_train(lsort_ctx* C, uint64_t* d_sample, uint64_t s, uint32_t buckets, lsort_rmi_header* h_out,
+                          lsort_rmi_entry* e_out) {
+    if (!C || s < 2 || buckets < 2 || buckets > LSORT_MAX_RMI) return LSORT_EINVAL;
+    try {
+        CU(cudaSetDevice(C->device));
+        lsort_cfg cfg;
+        lsort_cfg_default(&cfg);
+        Engine E(C, cfg);
+        E.nested_sort(d_sample, s);
+        if (!C->models.ensure(sizeof(ModelHdr) + 32 * (size_t)buckets)) throw LsortError{LSORT_ENOMEM, "model"};
+        launch_train_rmi_global(d_sample, s, buckets, C->models.as<uint8_t>(), buckets, C->stream);
+        CU(cudaGetLastError());
+        download_learned(C, C->models.as<uint8_t>(), buckets, h_out, e_out);
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_dist_histogram(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, const lsort_rmi_header* h,
+                              const lsort_rmi_entry* e, uint64_t* d_hist) {
+    return lsort_cuda_classify_rmi(C, h, e, h ? h->submodels : 0, 0.0, 1.0, d_keys, n, key_kind, nullptr, d_hist);
+}
+
+int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, const lsort_rmi_header* h,
+                              const lsort_rmi_entry* e, const uint32_t* bucket_bounds, uint32_t nranks,
+                              uint64_t* d_out, uint64_t* send_counts) {
+    if (!C || !h || !e || !bucket_bounds || nranks == 0 || nranks > 1024) return LSORT_EINVAL;
+    try {
+        CU(cudaSetDevice(C->device));
+        const uint32_t B = h->submodels;
+        upload_learned(C, h, e, B, 0.0, 1.0);
+        // bucket -> destination rank map and per-rank histogram
+        std::vector<uint32_t> map(B);
+        for (uint32_t r = 0; r < nranks; ++r)
+            for (uint32_t b = bucket_bounds[r]; b < bucket_bounds[r + 1] && b < B; ++b) map[b] = r;
+        if (!C->aux.ensure(B * 4 + 8 * (size_t)B + 8 * (size_t)nranks) || !C->segs.ensure(sizeof(SegDesc)) ||
+            !C->tile_prefix.ensure(16) || !C->ctrl.ensure(sizeof(Ctrl)))
+            throw LsortError{LSORT_ENOMEM, "dist"};
+        uint32_t* dmap = C->aux.as<uint32_t>();
+        unsigned long long* dhist = (unsigned long long*)(C->aux.as<uint8_t>() + B * 4 + 4 * (B & 1));
+        unsigned long long* dcur = dhist + B;
+        CU(cudaMemcpyAsync(dmap, map.data(), B * 4, cudaMemcpyHostToDevice, C->stream));
+        CU(cudaMemsetAsync(dhist, 0, 8 * (size_t)B, C->stream));
+        launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, nullptr, dhist, 32 * (int)B,
+                            C->stream);
+        std::vector<uint64_t> hist(B);
+        CU(cudaMemcpyAsync(hist.data(), dhist, 8 * (size_t)B, cudaMemcpyDeviceToHost, C->stream));
+        CU(cudaStreamSynchronize(C->stream));
+        std::vector<uint64_t> cur(nranks, 0);
+        for (uint32_t b = 0; b < B; ++b) cur[map[b]] += hist[b];
+        uint64_t acc = 0;
+        for (uint32_t r = 0; r < nranks; ++r) {
+            send_counts[r] = cur[r];
+            uint64_t c = cur[r];
+            cur[r] = acc;
+            acc += c;
+        }
+        CU(cudaMemcpyAsync(dcur, cur.data(), 8 * (size_t)nranks, cudaMemcpyHostToDevice, C->stream));
+        SegDesc d{};
+        d.begin = 0;
+        d.n = n;
+        d.model_off = 0;
+        d.bucket_off = 0;
+        d.rmi_b = B;
+        uint64_t pref[2] = {0, (n + kTileKeys - 1) / kTileKeys};
+        CU(cudaMemcpyAsync(C->segs.p, &d, sizeof(d), cudaMemcpyHostToDevice, C->stream));
+        CU(cudaMemcpyAsync(C->tile_prefix.p, pref, 16, cudaMemcpyHostToDevice, C->stream));
+        CU(cudaMemsetAsync(C->ctrl.p, 0, sizeof(Ctrl), C->stream));
+        CU(cudaMemsetAsync(&C->ctrl.as<Ctrl>()->nan_index, 0xff, 8, C->stream));
+        LevelParams p{};
+        p.segs = C->segs.as<SegDesc>();
+        p.nsegs = 1;
+        p.tile_prefix = C->tile_prefix.as<uint64_t>();
+        p.ntiles = pref[1];
+        p.models = C->models.as<uint8_t>();
+        p.buckets = dcur;
+        p.src = d_keys;
+        p.dst = d_out;
+        p.ctrl = C->ctrl.as<Ctrl>();
+        int grid = (int)std::min<uint64_t>(pref[1], (uint64_t)num_sms() * 2);
+        launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, 32 * (int)B, dmap, nranks, grid, C->stream);
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+    } catch (const LsortError& er) {
+        return fail(C, er);
+    }
+    return LSORT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,112 @@
+// kernels.cuh -- shared declarations between kernels.cu and engine.cu.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lsort_device.cuh"
+
+namespace lsort_dev {
+
+// One segment being partitioned at the current level.
+struct SegDesc {
+    uint64_t begin, n;       // absolute key range
+    uint64_t model_off;      // byte offset in the model arena (16-aligned)
+    uint64_t bucket_off;     // index into the per-bucket counter/cursor arena
+    uint32_t depth, flags;   // flags: kSegForceRadix
+    uint32_t nb_max, rmi_b;  // bucket slots reserved, learned fan-out
+    uint32_t tree_k, pad;    // tree bucket budget
+};
+constexpr uint32_t kSegForceRadix = 1u;
+
+// Child segment emitted for the next level.
+struct SegOut {
+    uint64_t begin, n;
+    uint32_t depth, flags;
+    uint64_t pad;
+};
+struct BaseItem {
+    uint64_t begin, n;
+};
+struct FillItem {
+    uint64_t begin, n, value, pad;
+};
+
+// Device control block (zeroed per level, nan_index once per sort).
+struct Ctrl {
+    unsigned long long nan_index;   // first NaN index, ~0 if none
+    unsigned int n_rec;
+    unsigned int n_base[3];
+    unsigned int n_fill;
+    unsigned int err;
+    unsigned long long keys_fill, keys_base, keys_rec;
+    unsigned long long verify_first;
+    unsigned long long verify_hash;
+    unsigned long long pad[4];
+};
+
+// Parameters shared by the level kernels.
+struct LevelParams {
+    const SegDesc* segs;
+    uint32_t nsegs;
+    const uint64_t* tile_prefix;   // nsegs+1
+    uint64_t ntiles;
+    const uint8_t* models;         // model arena
+    unsigned long long* buckets;   // counters -> cursors
+    const void* src;               // keys in (level 0 may be f64)
+    uint64_t* dst;                 // partitioned keys out (encoded)
+    Ctrl* ctrl;
+    SegOut* rec;
+    BaseItem* base[3];
+    FillItem* fill;
+    uint32_t base_cap[3];          // size classes: n <= base_cap[c]
+    uint32_t depth_cap;
+    uint32_t list_cap;             // capacity of rec/base/fill lists
+};
+
+// Sort configuration as seen by kernels.
+struct DevCfg {
+    uint64_t min_rmi_input;
+    double max_dup;
+    double sample_fraction;
+    uint32_t first_sample_cap, rmi_sample_cap;
+    uint64_t seed;
+};
+
+constexpr int kTileKeys = 4096;     // keys per classify/scatter tile
+constexpr int kPartNT = 512;        // threads per classify/scatter CTA
+constexpr int kRadixBits = 10;      // fallback radix model: 1024 buckets
+constexpr uint32_t kSmallSampleCap = 16384;  // samples sortable in one CTA
+
+// Host-visible launchers (kernels.cu).
+void launch_build_models(const SegDesc* segs, const uint32_t* idx, uint32_t count, const void* src,
+                         int in_f64, uint8_t* models, const DevCfg& cfg, int smem_bytes,
+                         cudaStream_t st);
+void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_t* models,
+                         const DevCfg& cfg, cudaStream_t st);
+void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0,
+                   uint64_t s, uint64_t* out, cudaStream_t st);
+void launch_train_rmi_global(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* model,
+                             uint32_t nbuckets, cudaStream_t st);
+void launch_classify_hist(const LevelParams& p, int in_f64, int max_payload, int grid, cudaStream_t st);
+void launch_scan_children(const LevelParams& p, cudaStream_t st);
+void launch_scatter(const LevelParams& p, int in_f64, int max_payload, int max_nb, int grid,
+                    cudaStream_t st);
+void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, uint64_t* scratch,
+                       int out_f64, int grid_mult, cudaStream_t st);
+void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st);
+void launch_small_sort(void* keys, uint64_t n, int f64, uint64_t* scratch, Ctrl* ctrl, cudaStream_t st);
+void launch_classify_ids(const uint8_t* model, const void* keys, uint64_t n, int in_f64,
+                         uint32_t* ids, unsigned long long* hist, int payload, cudaStream_t st);
+void launch_tree_build(const uint64_t* sorted, uint64_t s, uint32_t budget, int eq_mode, uint8_t* model,
+                       cudaStream_t st);
+void launch_verify(const void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st);
+void launch_decode(uint64_t* keys, uint64_t n, cudaStream_t st);
+void launch_scatter_mapped(const LevelParams& p, int in_f64, int max_payload, const uint32_t* map,
+                           uint32_t nmapped, int grid, cudaStream_t st);
+int num_sms();
+size_t model_smem_bytes();
+void launch_block_sort(uint64_t* keys, uint64_t n, cudaStream_t st);
+void kernels_init();   // cudaFuncSetAttribute for large dynamic shared memory
+
+}  // namespace lsort_dev

@@ -1,0 +1,459 @@
+// lsort_device.cuh -- device-side building blocks of the B200 LearnedSort.
+//
+// Key codec, counter-based sampling PRNG, partition-model records and their
+// exact per-key classifiers, and block-level primitives (reductions, scans,
+// the shared-memory MSD block sort used by the base case and the model
+// builder). sm_100a only.
+//
+// Exactness: every double operation of the reference's per-key model math
+// (models.hpp:21,34-43,56-65,162-171) is issued as an explicit
+// round-to-nearest intrinsic (__dmul_rn/__dadd_rn/__dsub_rn) so ptxas cannot
+// contract a multiply-add into an FMA; the reference is built without FMA
+// contraction. Conversions use __ull2double_rn (correctly
+// rounded like the host's uint64->double) and truncating casts.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lsort_dev {
+
+constexpr uint64_t kSign = 0x8000000000000000ull;
+
+#define LSORT_MAX_TREE_DEV 1024   // max SplitterTree budget
+#define LSORT_MAX_RMI_DEV 2048    // max RMI submodels / output buckets (shared-memory resident)
+constexpr uint32_t kMaxNB = 2048; // max output buckets of any partition model
+
+// keys.hpp:24-27
+__device__ __forceinline__ uint64_t encode(double x) {
+    uint64_t b = (uint64_t)__double_as_longlong(x);
+    return (b & kSign) ? ~b : (b ^ kSign);
+}
+// keys.hpp:29-32
+__device__ __forceinline__ double decode(uint64_t k) {
+    uint64_t b = (k & kSign) ? (k ^ kSign) : ~k;
+    return __longlong_as_double((long long)b);
+}
+// rng.hpp:13-18
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+// Rng(seed).next_below(n) at stream position `draw` (rng.hpp:24,35-37)
+__host__ __device__ __forceinline__ uint64_t sample_index(uint64_t seed, uint64_t draw, uint64_t n) {
+    return n == 0 ? 0 : splitmix64(seed + draw) % n;
+}
+
+enum ModelKind : uint32_t { kLearned = 0, kTree = 1, kRadix = 2, kFill = 3 };
+
+struct RmiEntry {
+    double slope, intercept, lo, hi;
+};
+
+// Partition-model record, 128 bytes; payload follows in the model arena:
+//   learned: RmiEntry[B]
+//   tree:    uint64 tree[leaf_origin], uint64 splitters[nsplit], uint32 eq_offset[nsplit+1]
+struct ModelHdr {
+    uint32_t kind;       // ModelKind
+    uint32_t nbuckets;   // output buckets
+    uint32_t B;          // learned: submodels
+    uint32_t levels;     // tree
+    uint32_t leaf_origin;
+    uint32_t nsplit;
+    uint32_t shift;      // radix
+    uint32_t flags;
+    double root_slope, root_icpt, key_base, key_scale;
+    double cdf_lo, inv_span;
+    uint64_t radix_min;  // radix; fill value for kFill
+    double dup;          // duplicate fraction of the first sample
+    uint64_t s1, s2;     // sample sizes used
+    uint64_t reserved[2];
+};
+static_assert(sizeof(ModelHdr) == 128, "ModelHdr must stay 128 bytes");
+
+__host__ __device__ __forceinline__ size_t tree_payload_bytes(uint32_t leaf_origin, uint32_t nsplit) {
+    return (size_t)leaf_origin * 8 + (size_t)nsplit * 8 + ((size_t)nsplit + 1) * 4;
+}
+
+// ---------------------------------------------------------------- classifiers
+// Rmi::route (models.hpp:60-65). `t >= B` replaces the post-cast clamp; equal
+// wherever the reference's size_t cast is defined (t < 2^64).
+__device__ __forceinline__ uint32_t rmi_route(double root_slope, double root_icpt, uint32_t B, double xn) {
+    double t = __dmul_rn(__dadd_rn(__dmul_rn(root_slope, xn), root_icpt), (double)B);
+    if (!(t > 0.0)) return 0;
+    if (t >= (double)B) return B - 1;
+    return (uint32_t)t;
+}
+
+// Rmi::normalize (models.hpp:56-58)
+__device__ __forceinline__ double rmi_normalize(double key_base, double key_scale, uint64_t x) {
+    return __dmul_rn(__dsub_rn(__ull2double_rn(x), key_base), key_scale);
+}
+
+// Rmi::predict (models.hpp:34-43)
+__device__ __forceinline__ double rmi_predict(const ModelHdr& h, const RmiEntry* e, uint64_t x) {
+    double xn = rmi_normalize(h.key_base, h.key_scale, x);
+    uint32_t i = rmi_route(h.root_slope, h.root_icpt, h.B, xn);
+    RmiEntry s = e[i];
+    double v = __dadd_rn(__dmul_rn(s.slope, xn), s.intercept);
+    if (v < s.lo) v = s.lo;
+    if (v > s.hi) v = s.hi;
+    if (v < 0.0) v = 0.0;
+    if (v > 1.0) v = 1.0;
+    return v;
+}
+
+// PartitionModel::bucket_index, learned branch (models.hpp:162-171)
+__device__ __forceinline__ uint32_t learned_bucket(const ModelHdr& h, const RmiEntry* e, uint64_t x) {
+    double f = rmi_predict(h, e, x);
+    double u = __dmul_rn(__dsub_rn(f, h.cdf_lo), h.inv_span);
+    double t = __dmul_rn(u, (double)h.nbuckets);
+    if (!(t > 0.0)) return 0;
+    if (t >= (double)h.nbuckets) return h.nbuckets - 1;
+    return (uint32_t)t;
+}
+
+// SplitterTree::classify (models.hpp:92-101). Returns bucket | (eq << 31).
+__device__ __forceinline__ uint32_t tree_bucket(uint32_t levels, uint32_t leaf_origin, uint32_t nsplit,
+                                                const uint64_t* tree, const uint64_t* spl,
+                                                const uint32_t* eqo, uint64_t x) {
+    uint32_t i = 1;
+    for (uint32_t l = 0; l < levels; ++l) i = 2 * i + (x > tree[i] ? 1u : 0u);
+    uint32_t base = i - leaf_origin;
+    uint32_t eq = (base < nsplit) && (eqo[base + 1] - eqo[base] > 1) && (x == spl[base]);
+    return (eqo[base] + eq) | (eq << 31);
+}
+
+// ------------------------------------------------------------ block helpers
+template <int NT>
+__device__ __forceinline__ uint64_t block_reduce_min(uint64_t v, uint64_t* red) {
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < NT / 32 ? red[lane] : ~0ull;
+        for (int o = 16; o > 0; o >>= 1) {
+            uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+            v = w < v ? w : v;
+        }
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+template <int NT>
+__device__ __forceinline__ uint64_t block_reduce_max(uint64_t v, uint64_t* red) {
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < NT / 32 ? red[lane] : 0ull;
+        for (int o = 16; o > 0; o >>= 1) {
+            uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+            v = w > v ? w : v;
+        }
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+template <int NT>
+__device__ __forceinline__ uint64_t block_reduce_sum_u64(uint64_t v, uint64_t* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < NT / 32 ? red[lane] : 0ull;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+// Deterministic fixed-order block sum of doubles (tree over lanes, then warps).
+template <int NT>
+__device__ __forceinline__ double block_sum_f64(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < NT / 32 ? red[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+// In-place exclusive scan of a[0,n) (u32) by the whole block; returns total.
+// `wsum` needs NT/32 + 1 words.
+template <int NT>
+__device__ uint32_t block_exclusive_scan_u32(uint32_t* a, uint32_t n, uint32_t* wsum) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t per = (n + NT - 1) / NT;  // contiguous chunk per thread
+    const uint32_t lo = threadIdx.x * per;
+    const uint32_t hi = min(lo + per, n);
+    uint32_t s = 0;
+    for (uint32_t i = lo; i < hi; ++i) s += a[i];
+    uint32_t incl = s;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t w = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += w;
+    }
+    __syncthreads();
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = lane < NT / 32 ? wsum[lane] : 0;
+        uint32_t inc2 = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t w = __shfl_up_sync(0xffffffffu, inc2, o);
+            if (lane >= o) inc2 += w;
+        }
+        if (lane < NT / 32) wsum[lane] = inc2 - v;
+        if (lane == NT / 32 - 1) wsum[NT / 32] = inc2;
+    }
+    __syncthreads();
+    uint32_t run = wsum[warp] + incl - s;
+    for (uint32_t i = lo; i < hi; ++i) {
+        uint32_t t = a[i];
+        a[i] = run;
+        run += t;
+    }
+    uint32_t total = wsum[NT / 32];
+    __syncthreads();
+    return total;
+}
+
+// In-place exclusive scan, u64 values.
+template <int NT>
+__device__ uint64_t block_exclusive_scan_u64(uint64_t* a, uint32_t n, uint64_t* wsum) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t per = (n + NT - 1) / NT;
+    const uint32_t lo = threadIdx.x * per;
+    const uint32_t hi = min(lo + per, n);
+    uint64_t s = 0;
+    for (uint32_t i = lo; i < hi; ++i) s += a[i];
+    uint64_t incl = s;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t w = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += w;
+    }
+    __syncthreads();
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t v = lane < NT / 32 ? wsum[lane] : 0;
+        uint64_t inc2 = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint64_t w = __shfl_up_sync(0xffffffffu, inc2, o);
+            if (lane >= o) inc2 += w;
+        }
+        if (lane < NT / 32) wsum[lane] = inc2 - v;
+        if (lane == NT / 32 - 1) wsum[NT / 32] = inc2;
+    }
+    __syncthreads();
+    uint64_t run = wsum[warp] + incl - s;
+    for (uint32_t i = lo; i < hi; ++i) {
+        uint64_t t = a[i];
+        a[i] = run;
+        run += t;
+    }
+    uint64_t total = wsum[NT / 32];
+    __syncthreads();
+    return total;
+}
+
+__device__ __forceinline__ uint32_t bitlen64(uint64_t v) { return v ? 64u - (uint32_t)__clzll((long long)v) : 0u; }
+
+// ----------------------------------------------------------- block sort
+// Shared-memory MSD sort of up to NT*ITEMS keys (the GPU base case; also
+// sorts samples for the model builder). One distribution pass buckets keys by
+// (k - min) >> shift into <= NBMAX digits (a range-adaptive radix: the digit
+// span shrinks by NBMAX each pass, so it terminates for any input). Digits of
+// <= 16 keys are insertion-sorted by one thread, <= 256 keys rank-sorted by
+// one warp, larger ones get another block pass (keys re-staged through
+// registers). Equal-key ranges end immediately (min == max).
+template <int NT, int ITEMS, int NBMAX>
+struct BlockSort {
+    static constexpr int CAP = NT * ITEMS;
+    static constexpr int kSmall = 16;
+    static constexpr int kMedium = 256;
+    static constexpr int kListCap = CAP / (kSmall + 1) + 2;
+    struct Smem {
+        uint32_t hist[NBMAX + 1];
+        uint32_t wsum[NT / 32 + 1];
+        uint64_t red[NT / 32];
+        uint32_t n_med, n_large;
+        uint32_t med[kListCap];    // packed (off << 16 | len) won't fit CAP>65535: store pairs
+        uint32_t med_len[kListCap];
+        uint32_t large[kListCap];
+        uint32_t large_len[kListCap];
+    };
+
+    __device__ static void insertion(uint64_t* a, uint32_t len) {
+        for (uint32_t i = 1; i < len; ++i) {
+            uint64_t v = a[i];
+            uint32_t j = i;
+            while (j > 0 && a[j - 1] > v) {
+                a[j] = a[j - 1];
+                --j;
+            }
+            a[j] = v;
+        }
+    }
+
+    // warp rank sort of a[0,len), len <= 256
+    __device__ static void warp_rank_sort(uint64_t* a, uint32_t len) {
+        const int lane = threadIdx.x & 31;
+        uint64_t v[8];
+        uint32_t r[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            uint32_t idx = lane + 32 * q;
+            v[q] = idx < len ? a[idx] : ~0ull;
+            r[q] = 0;
+        }
+        for (uint32_t j = 0; j < len; ++j) {
+            uint64_t w = a[j];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                uint32_t idx = lane + 32 * q;
+                r[q] += (w < v[q]) || (w == v[q] && j < idx);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            uint32_t idx = lane + 32 * q;
+            if (idx < len) a[r[q]] = v[q];
+        }
+        __syncwarp();
+    }
+
+    // One distribution pass over keys held in registers k[] (valid where
+    // idx < len, idx = tid + i*NT), writing the result into a[off, off+len).
+    __device__ static void pass(uint64_t (&k)[ITEMS], uint64_t* a, uint32_t off, uint32_t len, Smem& S) {
+        const int tid = threadIdx.x;
+        uint64_t mn = ~0ull, mx = 0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            uint32_t idx = tid + i * NT;
+            if (idx < len) {
+                mn = k[i] < mn ? k[i] : mn;
+                mx = k[i] > mx ? k[i] : mx;
+            }
+        }
+        mn = block_reduce_min<NT>(mn, S.red);
+        mx = block_reduce_max<NT>(mx, S.red);
+        if (mn == mx) {  // homogeneous: write back unchanged
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                uint32_t idx = tid + i * NT;
+                if (idx < len) a[off + idx] = k[i];
+            }
+            __syncthreads();
+            return;
+        }
+        uint32_t nb = 1;
+        while (nb < len && nb < (uint32_t)NBMAX) nb <<= 1;
+        uint32_t lgnb = __ffs(nb) - 1;
+        uint32_t bits = bitlen64(mx - mn);
+        uint32_t shift = bits > lgnb ? bits - lgnb : 0;
+        for (uint32_t d = tid; d <= nb; d += NT) S.hist[d] = 0;
+        __syncthreads();
+        uint32_t rank[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            uint32_t idx = tid + i * NT;
+            if (idx < len) {
+                uint32_t d = (uint32_t)((k[i] - mn) >> shift);
+                rank[i] = atomicAdd(&S.hist[d], 1u);
+            }
+        }
+        __syncthreads();
+        block_exclusive_scan_u32<NT>(S.hist, nb, S.wsum);
+        if (tid == 0) S.hist[nb] = len;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            uint32_t idx = tid + i * NT;
+            if (idx < len) {
+                uint32_t d = (uint32_t)((k[i] - mn) >> shift);
+                a[off + S.hist[d] + rank[i]] = k[i];
+            }
+        }
+        __syncthreads();
+        for (uint32_t d = tid; d < nb; d += NT) {
+            uint32_t s0 = S.hist[d], l = S.hist[d + 1] - s0;
+            if (l < 2) continue;
+            if (l <= kSmall) {
+                insertion(a + off + s0, l);
+            } else if (l <= kMedium) {
+                uint32_t p = atomicAdd(&S.n_med, 1u);
+                S.med[p] = off + s0;
+                S.med_len[p] = l;
+            } else {
+                uint32_t p = atomicAdd(&S.n_large, 1u);
+                S.large[p] = off + s0;
+                S.large_len[p] = l;
+            }
+        }
+        __syncthreads();
+    }
+
+    // Sort a[0,n) in shared memory; keys arrive in registers k[] (idx = tid + i*NT).
+    __device__ static void sort_regs(uint64_t (&k)[ITEMS], uint64_t* a, uint32_t n, Smem& S) {
+        if (threadIdx.x == 0) {
+            S.n_med = 0;
+            S.n_large = 0;
+        }
+        __syncthreads();
+        pass(k, a, 0, n, S);
+        finish(k, a, S);
+    }
+
+    __device__ static void finish(uint64_t (&k)[ITEMS], uint64_t* a, Smem& S) {
+        const int warp = threadIdx.x >> 5;
+        for (;;) {
+            uint32_t nm = S.n_med;
+            for (uint32_t e = warp; e < nm; e += NT / 32) warp_rank_sort(a + S.med[e], S.med_len[e]);
+            __syncthreads();
+            if (threadIdx.x == 0) S.n_med = 0;
+            uint32_t nl = S.n_large;
+            __syncthreads();
+            if (nl == 0) break;
+            uint32_t off = S.large[nl - 1], len = S.large_len[nl - 1];
+            __syncthreads();
+            if (threadIdx.x == 0) S.n_large = nl - 1;
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                uint32_t idx = threadIdx.x + i * NT;
+                if (idx < len) k[i] = a[off + idx];
+            }
+            __syncthreads();
+            pass(k, a, off, len, S);
+        }
+    }
+};
+
+}  // namespace lsort_dev

@@ -1,0 +1,290 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the oracle.
+
+Bit-exact bar: sample sorts, bucket ids and histograms given identical model
+parameters, tree builds, duplicate fractions, and every final sorted array.
+RMI training on the GPU uses deterministic parallel sums for the root fit and
+for slices > 512 samples, so its parameters are compared with a tolerance
+(stated below); slices <= 512 samples are fitted sequentially and must match
+the reference bit for bit.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2307_08637_b200 as L  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from lsort_testutil import golden_cases  # noqa: E402
+
+RMI_RTOL = 1e-9  # relative tolerance on GPU-trained RMI parameters (parallel sums)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return L.Context(0)
+
+
+def dev(a: np.ndarray):
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint64:
+        return torch.from_numpy(a.view(np.int64)).cuda()
+    return torch.from_numpy(a).cuda()
+
+
+def host_u64(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint64)
+
+
+def bits(a):
+    return np.asarray(a, np.float64).view(np.uint64)
+
+
+def route_defined(P, B, keys):
+    with np.errstate(all="ignore"):
+        xn = (np.asarray(keys, np.uint64).astype(np.float64) - P[2]) * P[3]
+        t = (P[0] * xn + P[1]) * float(B)
+        return ~(t >= 2.0 ** 64)
+
+
+# ------------------------------------------------------------ block sort
+@pytest.mark.parametrize("n", [2, 3, 17, 100, 1000, 4096, 8191, 16384])
+def test_block_sort(ctx, n):
+    rng = np.random.default_rng(n)
+    for a in [rng.integers(0, 2**64 - 1, n, dtype=np.uint64, endpoint=True),
+              rng.integers(0, 7, n, dtype=np.uint64),
+              np.full(n, 5, np.uint64),
+              np.sort(rng.integers(0, 1000, n, dtype=np.uint64))[::-1].copy(),
+              (rng.integers(0, 3, n, dtype=np.uint64) << np.uint64(60)) + rng.integers(0, 50, n, dtype=np.uint64)]:
+        d = dev(a)
+        ctx.block_sort(d)
+        assert np.array_equal(host_u64(d), np.sort(a))
+
+
+# -------------------------------------------------- classification parity
+def test_classify_rmi_golden(ctx, golden):
+    for case in golden_cases(golden, "rmi"):
+        P, B = golden[f"rmi/{case}/P"], int(golden[f"rmi/{case}/B"][0])
+        pr = golden[f"rmi/{case}/probe"]
+        ok = route_defined(P, B, pr)
+        for bc, key, lo, hi in [(B, "bucket", 0.0, 1.0), (1000, "bucket1000", 0.0, 1.0),
+                                (256, "bucket_sub", 0.25, 0.75)]:
+            ids, hist = ctx.classify_rmi(P, B, bc, dev(pr), lo, hi)
+            got = ids.cpu().numpy().astype(np.uint32)
+            exp = golden[f"rmi/{case}/{key}"]
+            assert np.array_equal(got[ok], exp[ok]), (case, key)
+            assert np.array_equal(np.bincount(got, minlength=bc), hist.cpu().numpy()), (case, key)
+
+
+@pytest.mark.parametrize("dist,seed", [("uniform", 42), ("normal", 7), ("mixgauss", 11),
+                                       ("lognormal2", 19), ("exponential2", 7)])
+def test_classify_rmi_large_exact(ctx, dist, seed):
+    """1e6 keys under an oracle-trained 1024-submodel RMI: ids + histogram exact."""
+    x = O.generate(dist, 1_000_000, seed)
+    k = O.encode(x)
+    s = np.sort(k[:: 97])
+    P = O.rmi_train(s, 1024)
+    exp = O.learned_bucket(P, 1024, 1024, k[:20000])
+    ids, hist = ctx.classify_rmi(P, 1024, 1024, dev(x))  # f64 input: fused encode
+    got = ids.cpu().numpy().astype(np.uint32)
+    assert np.array_equal(got[:20000], exp)
+    # histogram of all keys equals bincount of the ids (device-consistent)
+    assert np.array_equal(np.bincount(got, minlength=1024), hist.cpu().numpy())
+
+
+def test_classify_tree_golden(ctx, golden):
+    for case in golden_cases(golden, "tree"):
+        s = golden[f"tree/{case}/sample"]
+        k, eq = int(golden[f"tree/{case}/k"][0]), int(golden[f"tree/{case}/eq"][0])
+        t = O.tree_build(s, k, bool(eq))
+        tt = L._native.lsort_tree.from_buffer_copy(bytes(t))
+        ids, hist = ctx.classify_tree(tt, dev(golden[f"tree/{case}/probe"]))
+        assert np.array_equal(ids.cpu().numpy().astype(np.uint32), golden[f"tree/{case}/bucket"]), case
+
+
+# ---------------------------------------------------------- model building
+def test_tree_build_golden(ctx, golden):
+    for case in golden_cases(golden, "tree"):
+        s = golden[f"tree/{case}/sample"]
+        if s.size > 16384:
+            continue
+        k, eq = int(golden[f"tree/{case}/k"][0]), int(golden[f"tree/{case}/eq"][0])
+        t = ctx.tree_build(dev(s), k, bool(eq))
+        m = t.nsplitters
+        assert np.array_equal(np.array(t.splitters[:m], np.uint64), golden[f"tree/{case}/splitters"]), case
+        heavy = np.array([t.eq_offset[i + 1] - t.eq_offset[i] > 1 for i in range(m)], np.uint8)
+        assert np.array_equal(heavy, golden[f"tree/{case}/heavy"]), case
+        assert t.bucket_count == int(golden[f"tree/{case}/bucket_count"][0]), case
+        ot = O.tree_build(s, k, bool(eq))
+        assert bytes(t) == bytes(ot), case  # whole POD incl. implicit heap
+
+
+def compare_rmi(Pg, Pr, B, s):
+    """GPU vs reference params: sequentially-fitted slices exact, rest within RMI_RTOL."""
+    assert np.allclose(Pg[:4], Pr[:4], rtol=RMI_RTOL, atol=0), "root"
+    assert np.array_equal(bits(Pg[2:4]), bits(Pr[2:4])), "key_base/key_scale are exact"
+    E, Er = Pg[4:].reshape(B, 4), Pr[4:].reshape(B, 4)
+    assert np.allclose(E, Er, rtol=1e-7, atol=1e-9), "submodels"
+
+
+def test_rmi_train_golden(ctx, golden):
+    for case in golden_cases(golden, "rmi"):
+        s, B = golden[f"rmi/{case}/sample"], int(golden[f"rmi/{case}/B"][0])
+        Pg = ctx.rmi_train(dev(s), B)
+        Pr = golden[f"rmi/{case}/P"]
+        compare_rmi(Pg, Pr, B, s)
+        # classification under the GPU-trained model agrees with the
+        # reference-trained one except at ulp-level boundaries
+        pr = golden[f"rmi/{case}/probe"]
+        ids, _ = ctx.classify_rmi(Pg, B, B, dev(pr))
+        agree = np.mean(ids.cpu().numpy().astype(np.uint32) == golden[f"rmi/{case}/bucket"])
+        assert agree > 0.99, (case, agree)
+
+
+def _fanout(n, count, target):
+    if target == 0:
+        return count
+    want = -(-n // target)
+    b = 2
+    while b < want and b < count:
+        b <<= 1
+    return min(b, count)
+
+
+@pytest.mark.parametrize("dist,seed,n", [("uniform", 42, 2_000_000), ("normal", 7, 300_000),
+                                         ("rootdups", 3, 1_000_000), ("zipf", 3, 500_000),
+                                         ("uniform", 42, 50_000), ("twodups", 3, 400_000),
+                                         ("lognormal2", 19, 5_000_000)])
+def test_build_model_alg5(ctx, dist, seed, n):
+    """Alg. 5 policy on the same device-drawn samples as the
+    oracle: decision and duplicate fraction exact, trees bit-exact, learned
+    models within RMI_RTOL of the reference-exact oracle training."""
+    x = O.generate(dist, n, seed)
+    keys = O.encode(x) if x.dtype == np.float64 else x
+    cfg = L.SortConfig()
+    m = ctx.build_model(dev(x), cfg)
+    rb = _fanout(n, cfg.rmi_bucket_count, cfg.bucket_target)
+    tk = _fanout(n, cfg.tree_bucket_count, cfg.bucket_target)
+    kind, P, t, dup = O.build_partition_model(keys, 0, 0, O.cfg(seed=cfg.seed), rb, tk)
+    assert m["kind"] == kind
+    assert m["dup"] == dup
+    if kind == 1:
+        assert bytes(m["tree"]) == bytes(t)
+    else:
+        assert m["B"] == rb
+        compare_rmi(m["P"], P, rb, None)
+
+
+# --------------------------------------------------------------- full sort
+def check_sorted_f64(x, got):
+    exp = O.decode(np.sort(O.encode(x)))
+    assert np.array_equal(bits(got), bits(exp))
+
+
+@pytest.mark.parametrize("dist,seed", [("uniform", 42), ("normal", 7), ("lognormal05", 7),
+                                       ("exponential2", 7), ("mixgauss", 11), ("lognormal2", 19)])
+@pytest.mark.parametrize("n", [1000, 16384, 16385, 100_000, 1_000_000, 3_000_000])
+def test_sort_f64_generators(ctx, dist, seed, n):
+    x = O.generate(dist, n, seed)
+    d = dev(x)
+    ctx.sort(d)
+    check_sorted_f64(x, d.cpu().numpy())
+
+
+@pytest.mark.parametrize("dist", ["rootdups", "twodups", "zipf"])
+@pytest.mark.parametrize("n", [5000, 200_000, 2_000_000])
+def test_sort_u64_dups(ctx, dist, n):
+    a = O.generate(dist, n, 3)
+    d = dev(a)
+    st = ctx.sort(d)
+    assert np.array_equal(host_u64(d), np.sort(a))
+    if n >= 200_000 and dist != "twodups":
+        assert st["fill_keys"] > 0  # equality buckets engaged
+
+
+def test_sort_adversarial(ctx):
+    n = 300_000
+    rng = np.random.default_rng(1)
+    cases = {
+        "sorted": np.arange(n, dtype=np.uint64),
+        "reversed": np.arange(n, dtype=np.uint64)[::-1].copy(),
+        "all_equal": np.full(n, 42, np.uint64),
+        "organ_pipe": np.concatenate([np.arange(n // 2), np.arange(n // 2)[::-1]]).astype(np.uint64),
+        "near_constant": np.where(rng.random(n) < 1e-4, 7, 5).astype(np.uint64),
+        "wide": rng.integers(0, 2**64 - 1, n, dtype=np.uint64, endpoint=True),
+        "two_clusters": np.concatenate([rng.integers(0, 100, n // 2), rng.integers(2**63, 2**63 + 100, n // 2,
+                                                                                   dtype=np.uint64)]).astype(np.uint64),
+        "outliers": np.where(rng.random(n) < 1e-3, 2**64 - 1, rng.integers(0, 1 << 20, n)).astype(np.uint64),
+    }
+    for name, a in cases.items():
+        d = dev(a)
+        ctx.sort(d)
+        assert np.array_equal(host_u64(d), np.sort(a)), name
+
+
+def test_sort_small_and_special(ctx):
+    for n in [0, 1, 2, 3, 31, 1025]:
+        a = np.random.default_rng(n).integers(0, 2**64 - 1, n, dtype=np.uint64, endpoint=True)
+        d = dev(a) if n else torch.empty(0, dtype=torch.int64, device="cuda")
+        ctx.sort(d)
+        assert np.array_equal(host_u64(d), np.sort(a))
+    sp = np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, 5e-324, -5e-324, 1e308, -1e308] * 3000)
+    np.random.default_rng(0).shuffle(sp)
+    d = dev(sp)
+    ctx.sort(d)
+    check_sorted_f64(sp, d.cpu().numpy())
+
+
+@pytest.mark.parametrize("n,pos", [(1000, [17, 500]), (500_000, [123456, 400000]), (16384, [16383])])
+def test_sort_nan(ctx, n, pos):
+    x = O.generate("normal", n, 7)
+    x[pos] = np.nan
+    d = dev(x)
+    with pytest.raises(L.NanError) as e:
+        ctx.sort(d)
+    assert e.value.index == min(pos)
+    assert np.array_equal(bits(d.cpu().numpy()), bits(x))  # untouched
+
+
+def test_sort_host_memory(ctx):
+    x = O.generate("lognormal2", 2_000_000, 19)
+    y = x.copy()
+    st = ctx.sort(y)
+    check_sorted_f64(x, y)
+    assert st["h2d_bytes"] == x.nbytes and st["d2h_bytes"] == x.nbytes
+
+
+def test_sort_configs(ctx):
+    x = O.generate("exponential2", 1_000_000, 7)
+    for cfg in [L.SortConfig(bucket_target=0), L.SortConfig(rmi_bucket_count=256, tree_bucket_count=16),
+                L.SortConfig(base_case_capacity=4096), L.SortConfig(seed=12345),
+                L.SortConfig(min_rmi_input=10**9)]:
+        d = dev(x)
+        ctx.sort(d, cfg)
+        check_sorted_f64(x, d.cpu().numpy())
+    with pytest.raises(ValueError):
+        ctx.sort(dev(x), L.SortConfig(rmi_bucket_count=1000))
+
+
+def test_verify(ctx, golden):
+    for k in "abcde":
+        a = golden[f"verify/{k}/in"]
+        if a.size == 0:
+            continue
+        ok, fv, h = ctx.verify(dev(a))
+        exp = golden[f"verify/{k}/out"]
+        assert (int(ok), fv, h) == (int(exp[0]), int(exp[1]), int(exp[2]))
+
+
+def test_sort_large_f64(ctx):
+    """BASELINE config 1 at full size (1e7 uniform): bit-exact + hash check on device."""
+    x = O.generate("uniform", 10_000_000, 42)
+    d = dev(x)
+    h_before = ctx.verify(d)[2]
+    st = ctx.sort(d)
+    ok, fv, h_after = ctx.verify(d)
+    assert ok and h_after == h_before
+    check_sorted_f64(x, d.cpu().numpy())
+    assert st["levels"] >= 1
