@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark: sorted keys/s of the B200 LearnedSort (AIPS2o) on BASELINE.json's configs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+Default workload (N=1) = BASELINE.json configs[1] ("C2"): N = 1e8 float64
+keys per array, three arrays -- Normal(0,1), LogNormal(0,0.5), Exponential(2),
+i.i.d. from seed 7 (reference Rng, glibc libm, generated on the host). One
+step = sorting the three arrays (3e8 keys). Inputs (800 MB each) are larger
+than the 126 MB L2, restored from pristine device copies before every step
+(untimed), followed by an untimed 256 MB L2-flush write. Each sort is
+bracketed by barrier + synchronize and timed with CUDA events on the sort's
+stream; `value` = keys sorted / summed device time (max over ranks).
+
+N > 1 (torchrun): weak scaling, 1e8 keys of each C2 distribution per rank,
+globally sorted across ranks (RMI splitters + NCCL all-to-all, see
+paper_2307_08637_b200/dist.py).
+
+--impl reference: the reference's CPU path (oracle/ C restatement of the
+AIPS2o driver; the reference ships no sort driver) on the host cores, on a
+bounded sample of the same workload per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (workload label, [(dist, seed)], n per array, key dtype)
+    "c1": ("C1 uniform[0,1) f64 N=1e7 seed 42", [("uniform", 42)], 10_000_000, "f64"),
+    "c2": ("C2 normal/lognormal(0,0.5)/exponential(2) f64 N=1e8 each seed 7",
+           [("normal", 7), ("lognormal05", 7), ("exponential2", 7)], 100_000_000, "f64"),
+    "c3": ("C3 mixture of 5 gaussians f64 N=2e8 seed 11", [("mixgauss", 11)], 200_000_000, "f64"),
+    "c4": ("C4 rootdups/twodups/zipf(0.75) u64 N=1e8 seed 3",
+           [("rootdups", 3), ("twodups", 3), ("zipf", 3)], 100_000_000, "u64"),
+    "c5": ("C5 lognormal(0,2) f64 N=5e8 per GPU seed 19", [("lognormal2", 19)], 500_000_000, "f64"),
+}
+METRIC = "sorted keys/sec (Gkeys/s, float64) at 1/2/4/8 B200; % of HBM+NVLink roofline"
+
+
+def passes(n_gpu: int) -> int:
+    """BASELINE.md 2 / SURVEY 8(d): P = 1 + max(1, ceil(log_1024(N/16384)))."""
+    import math
+    return 1 + max(1, math.ceil(math.log(n_gpu / 16384, 1024)))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+# --------------------------------------------------------------------- CPU legs
+def cpu_sort_rate(cfg_name: str, sample_n: int, runs: int):
+    """Oracle AIPS2o restatement (OpenMP, all host threads) on `sample_n` keys
+    of each config distribution; returns (Mkeys/s list per run, threads)."""
+    from oracle import oracle as O
+    label, dists, n, kind = CONFIGS[cfg_name]
+    threads = os.cpu_count() or 1
+    arrays = [O.generate(d, n if kind == "u64" else sample_n, s) for d, s in dists]
+    if kind == "u64":  # shuffled datasets are generated whole; take a prefix
+        arrays = [a[:sample_n].copy() for a in arrays]
+    rates = []
+    c = O.cfg(workers=threads)
+    for _ in range(runs):
+        t = 0.0
+        for a in arrays:
+            b = a.copy()
+            t0 = time.perf_counter()
+            if kind == "f64":
+                O.sort_doubles(b, c)
+            else:
+                O.sort_keys(b, c)
+            t += time.perf_counter() - t0
+        rates.append(len(arrays) * sample_n / t / 1e9)
+    return rates, threads
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    cfg_name = args.config
+    label, dists, n, kind = CONFIGS[cfg_name]
+    sample_n = min(n, args.cpu_sample)
+    rates, threads = cpu_sort_rate(cfg_name, sample_n, args.warmup + args.steps)
+    timed = rates[args.warmup:]
+    v = float(np.mean(timed))
+    ms = len(dists) * sample_n / (v * 1e9) * 1e3
+    line = {"metric": METRIC, "value": v, "unit": "Gkeys/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": kind, "data": "synthetic (reference Rng, host)",
+            "impl": "reference",
+            "config": {"workload": label, "sample_keys_per_array": sample_n, "arrays": len(dists)},
+            "cpu_baseline": {"value": v, "unit": "Gkeys/s", "cores": threads, "kind": "port",
+                             "sample": f"{sample_n} keys x {len(dists)} arrays per step"},
+            "e2e": {"value": v, "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- GPU leg
+def run_ours(args):
+    import torch
+    import paper_2307_08637_b200 as L
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dist_mode = world > 1
+    if dist_mode:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    label, dists, n, kind = CONFIGS[args.config]
+    if args.n:
+        n = args.n
+    if args.config == "c5" and not dist_mode:
+        n = min(n, args.n or n)
+    f64 = kind == "f64"
+    dev = torch.device("cuda", local)
+
+    # ---- inputs (host generation, reference Rng; shard r of a world*n dataset)
+    pristine = []
+    for d, s in dists:
+        if dist_mode and kind == "f64":
+            h = L.generate(d, world * n, s, first=rank * n, count=n)
+        else:
+            h = L.generate(d, n, s)
+        t = torch.from_numpy(h.view(np.int64) if h.dtype == np.uint64 else h).to(dev)
+        pristine.append(t)
+    work = [torch.empty_like(p) for p in pristine]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ctx = L.Context(local)
+    cfg = L.SortConfig(flags=L._native.FLAG_PHASE_TIMING)
+    if dist_mode:
+        from paper_2307_08637_b200.dist import DistSorter
+        sorter = DistSorter(ctx, cfg)
+
+    def barrier():
+        if dist_mode:
+            import torch.distributed as tdist
+            tdist.barrier()
+
+    def one_sort(i):
+        """restore + flush (untimed), then timed sort of array i; returns (ms, stats)."""
+        work[i].copy_(pristine[i])
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        if dist_mode:
+            out, stats = sorter.sort(work[i])
+        else:
+            stats = ctx.sort(work[i], cfg)
+        e1.record(st)
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        return ms, stats, (out if dist_mode else work[i])
+
+    for _ in range(args.warmup):
+        for i in range(len(work)):
+            one_sort(i)
+    # correctness spot check on the last warm-up output (untimed)
+    for i in range(len(work)):
+        _, _, res = one_sort(i)
+        ok, fv, _ = ctx.verify(res)
+        if not ok:
+            raise SystemExit(f"rank {rank}: output {i} not sorted at {fv}")
+    peaks, peak_src = measured_peaks()
+    total_ms = 0.0
+    agg = {}
+    launches = 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            for i in range(len(work)):
+                ms, stats, _ = one_sort(i)
+                total_ms += ms
+                launches += stats.get("kernel_launches", 0)
+                for k, v in stats.items():
+                    if isinstance(v, (int, float)):
+                        agg[k] = agg.get(k, 0) + v
+    clocks = clk.summary()
+    keys_per_step = len(work) * n * (world if dist_mode else 1)
+    if dist_mode:
+        import torch.distributed as tdist
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = keys_per_step / (ms_per_step * 1e-3) / 1e9  # Gkeys/s whole job
+
+    # ---- roofline: dominant kernel (by measured phase share) and whole sort
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    nsteps_arrays = args.steps * len(work)
+    phases = {k: agg.get(k, 0.0) / nsteps_arrays for k in
+              ("ms_models", "ms_classify", "ms_scatter", "ms_base", "ms_fill")}
+    # algorithmic bytes per launch: scatter moves every partitioned key once
+    # (8 B read + 8 B write); base case reads + writes each base-case key once;
+    # classify reads each partitioned key once (8 B).
+    part_keys = agg.get("partitioned_keys", 0) / nsteps_arrays
+    base_keys = agg.get("base_case_keys", 0) / nsteps_arrays
+    alg = {"ms_scatter": 16.0 * part_keys, "ms_base": 16.0 * base_keys, "ms_classify": 8.0 * part_keys}
+    dom = max(alg, key=lambda k: phases[k])
+    achieved = alg[dom] / (phases[dom] * 1e-3) / 1e9 if phases[dom] > 0 else 0.0
+    names = {"ms_scatter": "k_scatter", "ms_base": "k_base", "ms_classify": "k_classify_hist"}
+    nper = n
+    P = passes(nper)
+    t_roof_ms = 16.0 * P * nper / (hbm * 1e9) * 1e3 * len(work)
+    if dist_mode:
+        t_roof_ms += 8.0 * nper * (world - 1) / world / 770e9 * 1e3 * len(work)
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": kind,
+        "data": "synthetic (reference Rng splitmix64 + glibc libm on host; BASELINE.json seeds)",
+        "config": {"workload": label, "keys_per_array_per_gpu": n, "arrays": len(work),
+                   "l2": "inputs (>=80 MB) restored + 256 MB L2 flush before every timed sort",
+                   "parallelism": f"dp{world}" if dist_mode else "single-gpu"},
+        "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg[dom]},
+        "sort_roofline": {"passes": P, "bytes_per_key": 16 * P, "t_roof_ms_per_step": t_roof_ms,
+                          "frac": t_roof_ms / ms_per_step, "hbm_gbs": hbm},
+        "phases_ms_per_sort": phases,
+        "levels_per_sort": agg.get("levels", 0) / nsteps_arrays,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    # ---- e2e through the public API with pinned host buffers (H2D + D2H inside)
+    if not dist_mode:
+        hosts = [torch.empty(n, dtype=p.dtype, pin_memory=True) for p in pristine]
+        src = [p.cpu() for p in pristine]
+        e2e_t = 0.0
+        for step in range(args.e2e_steps + 1):
+            for i in range(len(hosts)):
+                hosts[i].copy_(src[i])
+                arr = hosts[i].numpy()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                ctx.sort(arr, cfg)
+                dt = time.perf_counter() - t0
+                if step > 0:
+                    e2e_t += dt
+        e2e_ms = e2e_t / max(1, args.e2e_steps) * 1e3
+        line["e2e"] = {"value": len(hosts) * n / (e2e_ms * 1e-3) / 1e9, "unit": "Gkeys/s",
+                       "h2d_bytes_per_step": 8 * n * len(hosts), "d2h_bytes_per_step": 8 * n * len(hosts),
+                       "ms_per_step": e2e_ms}
+    else:
+        line["e2e"] = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sample_n = min(n, args.cpu_sample)
+        rates, threads = cpu_sort_rate(args.config, sample_n, 2)
+        line["cpu_baseline"] = {"value": float(np.mean(rates)), "unit": "Gkeys/s", "cores": threads,
+                                "kind": "port",
+                                "sample": f"{sample_n} keys of each of {len(work)} config arrays, 2 runs"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist_mode:
+        import torch.distributed as tdist
+        tdist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--n", type=int, default=0, help="override keys per array (testing)")
+    ap.add_argument("--cpu-sample", type=int, default=10_000_000)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: W < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

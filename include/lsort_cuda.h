@@ -113,7 +113,14 @@ typedef struct lsort_stats {
     uint64_t base_segments;
     uint64_t kernel_launches;
     uint64_t h2d_bytes, d2h_bytes;
+    /* per-phase device time (CUDA events between launch groups), filled when
+     * cfg->flags has LSORT_FLAG_PHASE_TIMING; summed over levels */
+    double ms_models, ms_classify, ms_scatter, ms_base, ms_fill;
+    double ms_level0_classify, ms_level0_scatter;
+    uint64_t level0_keys;
 } lsort_stats;
+
+#define LSORT_FLAG_PHASE_TIMING 1u
 
 typedef struct lsort_ctx lsort_ctx;
 

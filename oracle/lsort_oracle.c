@@ -221,6 +221,44 @@ void lso_enforce_monotonic(double* P, uint32_t B, const uint64_t* s, size_t n) {
     free(nonempty);
 }
 
+/* Rmi::train from the slice loop on (models.cpp:58-72), for a given root
+ * model: the test hook that checks a GPU-trained RMI whose root came from a
+ * parallel (not sequential) sum against the reference's own slicing and
+ * per-slice fits. P[0..1] (root) must be set by the caller. */
+int lso_rmi_train_given_root(const uint64_t* s, size_t n, uint32_t B, double* P) {
+    if (n < 2 || B == 0) return -1;
+    P_BASE(P) = (double)s[0];
+    double key_max = (double)s[n - 1];
+    P_SCALE(P) = key_max > P_BASE(P) ? 1.0 / (key_max - P_BASE(P)) : 0.0;
+    double* xn = (double*)malloc(n * sizeof(double));
+    double* tg = (double*)malloc(n * sizeof(double));
+    for (size_t i = 0; i < n; ++i) {
+        xn[i] = rmi_normalize(P, s[i]);
+        tg[i] = (double)i / (double)n;
+    }
+    for (uint32_t m = 0; m < B; ++m) {
+        P_SUB_S(P, m) = 0.0;
+        P_SUB_I(P, m) = 0.0;
+        P_LO(P, m) = 0.0;
+        P_HI(P, m) = 1.0;
+    }
+    size_t begin = 0;
+    for (size_t m = 0; m < B && begin < n; ++m) {
+        size_t end = begin;
+        while (end < n && lso_rmi_route(P, B, xn[end]) == m) ++end;
+        if (end > begin) {
+            lin_t f = fit_line(xn, tg, begin, end);
+            P_SUB_S(P, m) = f.slope;
+            P_SUB_I(P, m) = f.intercept;
+        }
+        begin = end;
+    }
+    free(xn);
+    free(tg);
+    lso_enforce_monotonic(P, B, s, n);
+    return 0;
+}
+
 /* models.cpp:39-73 Rmi::train. Returns -1 on the reference's
  * std::invalid_argument preconditions (n < 2, B == 0). */
 int lso_rmi_train(const uint64_t* s, size_t n, uint32_t B, double* P) {

@@ -53,6 +53,8 @@ double lso_rng_exponential(uint64_t seed, uint64_t draw, double lambda); /* :47-
  * P[3]=key_scale, then for m in [0,B): P[4+4m..4m+7] = slope, intercept,
  * clamp_lo, clamp_hi. Size 4+4B doubles. */
 int lso_rmi_train(const uint64_t* sorted, size_t n, uint32_t B, double* P); /* models.cpp:39-73 */
+/* test hook: train with a caller-provided root (P[0], P[1]) */
+int lso_rmi_train_given_root(const uint64_t* sorted, size_t n, uint32_t B, double* P);
 void lso_enforce_monotonic(double* P, uint32_t B, const uint64_t* sorted, size_t n); /* models.cpp:75-131 */
 double lso_rmi_predict(const double* P, uint32_t B, uint64_t x);    /* models.hpp:34-43 */
 uint32_t lso_rmi_route(const double* P, uint32_t B, double xn);     /* models.hpp:60-65 */

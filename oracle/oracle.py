@@ -78,6 +78,8 @@ def lib():
         L.lso_rng_normal.restype = f64; L.lso_rng_normal.argtypes = [u64, u64]
         L.lso_rng_exponential.restype = f64; L.lso_rng_exponential.argtypes = [u64, u64, f64]
         L.lso_rmi_train.restype = C.c_int; L.lso_rmi_train.argtypes = [vp, sz, C.c_uint32, vp]
+        L.lso_rmi_train_given_root.restype = C.c_int
+        L.lso_rmi_train_given_root.argtypes = [vp, sz, C.c_uint32, vp]
         L.lso_rmi_predict.restype = f64; L.lso_rmi_predict.argtypes = [vp, C.c_uint32, u64]
         L.lso_learned_bucket.restype = C.c_uint32
         L.lso_learned_bucket.argtypes = [vp, C.c_uint32, C.c_uint32, f64, f64, u64]
@@ -163,6 +165,16 @@ def rmi_train(sorted_sample, B: int) -> np.ndarray:
     s = _u64(sorted_sample)
     P = np.zeros(4 + 4 * B, np.float64)
     if lib().lso_rmi_train(_p(s), s.size, B, _p(P)) != 0:
+        raise ValueError("Rmi::train: invalid argument")
+    return P
+
+
+def rmi_train_given_root(sorted_sample, B: int, root_slope: float, root_intercept: float) -> np.ndarray:
+    """Reference slicing + fits + enforce_monotonic under a given root model."""
+    s = _u64(sorted_sample)
+    P = np.zeros(4 + 4 * B, np.float64)
+    P[0], P[1] = root_slope, root_intercept
+    if lib().lso_rmi_train_given_root(_p(s), s.size, B, _p(P)) != 0:
         raise ValueError("Rmi::train: invalid argument")
     return P
 

@@ -17,6 +17,7 @@ KEY_U64, KEY_F64 = 0, 1
 MEM_DEVICE, MEM_HOST = 0, 1
 MAX_TREE = 1024
 MAX_RMI = 2048
+FLAG_PHASE_TIMING = 1
 
 
 class lsort_cfg(C.Structure):
@@ -56,7 +57,10 @@ class lsort_stats(C.Structure):
                 ("levels", C.c_uint32), ("level0_kind", C.c_uint32),
                 ("partitioned_keys", C.c_uint64), ("base_case_keys", C.c_uint64),
                 ("fill_keys", C.c_uint64), ("segments", C.c_uint64), ("base_segments", C.c_uint64),
-                ("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("ms_models", C.c_double), ("ms_classify", C.c_double), ("ms_scatter", C.c_double),
+                ("ms_base", C.c_double), ("ms_fill", C.c_double), ("ms_level0_classify", C.c_double),
+                ("ms_level0_scatter", C.c_double), ("level0_keys", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -87,6 +88,15 @@ uint32_t fanout(uint64_t n, uint32_t cfg_count, uint32_t target) {
     return std::min(b, cfg_count);
 }
 
+bool trace_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("LSORT_TRACE");
+        v = (e && *e && *e != '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 uint64_t seg_seed_host(uint64_t cfg_seed, uint64_t begin, uint32_t depth) {
     return splitmix64(cfg_seed ^ splitmix64(begin + ((uint64_t)depth << 48)));
 }
@@ -109,6 +119,7 @@ struct lsort_ctx {
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
     std::unique_ptr<lsort_ctx> nested;
     cudaEvent_t ev[6] = {};
+    cudaEvent_t pev[8] = {};  // phase timing
     uint64_t launches = 0;
 };
 
@@ -171,12 +182,15 @@ struct Engine {
             C->nested->device = C->device;
             C->nested->depth = C->depth + 1;
             for (auto& e : C->nested->ev) CU(cudaEventCreate(&e));
+            for (auto& e : C->nested->pev) CU(cudaEventCreate(&e));
         }
         C->nested->stream = C->stream;
         lsort_cfg nc = cfg;
         nc.seed = splitmix64(cfg.seed ^ 0x5a3c9e1f0b7d2468ull);
         Engine ne(C->nested.get(), nc);
-        ne.sort(sample, s, false, nullptr);
+        lsort_stats nst{};
+        if (trace_enabled()) nc.flags |= LSORT_FLAG_PHASE_TIMING;
+        ne.sort(sample, s, false, trace_enabled() ? &nst : nullptr);
         C->launches += C->nested->launches;
         C->nested->launches = 0;
     }
@@ -198,9 +212,18 @@ struct Engine {
         launch_gather(dseg, src, f64, seed, s1, s2, C->sample.as<uint64_t>(), st);
         launched();
         nested_sort(C->sample.as<uint64_t>(), s2);
+        if (trace_enabled()) CU(cudaEventRecord(C->ev[5], st));
         launch_train_rmi_global(C->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
                                 hseg.rmi_b, st);
         launched();
+        if (trace_enabled()) {
+            CU(cudaEventRecord(C->ev[4], st));
+            CU(cudaEventSynchronize(C->ev[4]));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, C->ev[5], C->ev[4]);
+            fprintf(stderr, "[lsort d%d] big model: s1=%llu s2=%llu train %.3f ms\n", C->depth,
+                    (unsigned long long)s1, (unsigned long long)s2, ms);
+        }
     }
 
     // Sort n keys at `keys` (device) in place. Returns LSORT_ENAN via throw.
@@ -306,6 +329,11 @@ struct Engine {
             p.depth_cap = depth_cap;
             p.list_cap = (uint32_t)std::min<uint64_t>(list_cap, 0xffffffffu);
 
+            const bool timing = (cfg.flags & LSORT_FLAG_PHASE_TIMING) && stats;
+            auto mark = [&](int i) {
+                if (timing) CU(cudaEventRecord(C->pev[i], st));
+            };
+            mark(0);
             // ---- models
             launch_build_models(p.segs, C->idx.as<uint32_t>(), nsmall, src, src_f64, C->models.as<uint8_t>(), dc, 0,
                                 st);
@@ -315,17 +343,46 @@ struct Engine {
             const int nsm = num_sms();
             int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 4);
             int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
+            mark(1);
             launch_classify_hist(p, src_f64, (int)max_payload, grid_h, st);
             launch_scan_children(p, st);
+            mark(2);
             launch_scatter(p, src_f64, (int)max_payload, (int)max_nb, grid_s, st);
+            mark(3);
             launch_base_cases(p, dst, keys, nullptr, f64, 1, st);
+            mark(4);
             launch_fill(p, keys, f64, nsm * 4, st);
+            mark(5);
             launched(7);
             CU(cudaMemcpyAsync(hc, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
             CU(cudaStreamSynchronize(st));
             CU(cudaGetLastError());
             if (hc->nan_index != ~0ull) throw LsortError{LSORT_ENAN, std::to_string(hc->nan_index)};
             if (hc->err) throw LsortError{LSORT_EINTERNAL, "work list overflow (" + std::to_string(hc->err) + ")"};
+            if (timing) {
+                float t[5];
+                for (int i = 0; i < 5; ++i) CU(cudaEventElapsedTime(&t[i], C->pev[i], C->pev[i + 1]));
+                if (trace_enabled()) {
+                    uint64_t keys = 0, mx = 0;
+                    for (auto& q : segs) { keys += q.n; mx = std::max(mx, q.n); }
+                    fprintf(stderr,
+                            "[lsort d%d L%u] segs=%u big=%zu keys=%llu max=%llu tiles=%llu | models %.3f "
+                            "classify %.3f scatter %.3f base %.3f fill %.3f ms | rec=%u base=%u/%u/%u fill=%u\n",
+                            C->depth, level, ns, bigs.size(), (unsigned long long)keys, (unsigned long long)mx,
+                            (unsigned long long)ntiles, t[0], t[1], t[2], t[3], t[4], hc->n_rec, hc->n_base[0],
+                            hc->n_base[1], hc->n_base[2], hc->n_fill);
+                }
+                stats->ms_models += t[0];
+                stats->ms_classify += t[1];
+                stats->ms_scatter += t[2];
+                stats->ms_base += t[3];
+                stats->ms_fill += t[4];
+                if (level == 0) {
+                    stats->ms_level0_classify = t[1];
+                    stats->ms_level0_scatter = t[2];
+                    stats->level0_keys = n;
+                }
+            }
             if (level == 0 && stats) {
                 ModelHdr h0;
                 CU(cudaMemcpy(&h0, C->models.p, sizeof(h0), cudaMemcpyDeviceToHost));
@@ -416,6 +473,7 @@ int lsort_cuda_ctx_create(lsort_ctx** out, int device, void* stream, size_t work
             c->stream = c->own_stream;
         }
         for (auto& e : c->ev) CU(cudaEventCreate(&e));
+        for (auto& e : c->pev) CU(cudaEventCreate(&e));
         if (workspace_hint && !c->scratch.ensure(workspace_hint * 8)) throw LsortError{LSORT_ENOMEM, "workspace"};
     } catch (const LsortError& e) {
         delete c;
@@ -430,7 +488,11 @@ int lsort_cuda_ctx_destroy(lsort_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& e : c->ev) if (e) cudaEventDestroy(e);
-    if (c->nested) for (auto& e : c->nested->ev) if (e) cudaEventDestroy(e);
+    for (auto& e : c->pev) if (e) cudaEventDestroy(e);
+    if (c->nested) {
+        for (auto& e : c->nested->ev) if (e) cudaEventDestroy(e);
+        for (auto& e : c->nested->pev) if (e) cudaEventDestroy(e);
+    }
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
     return LSORT_OK;

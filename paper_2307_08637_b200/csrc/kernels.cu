@@ -1120,6 +1120,14 @@ static int g_num_sms = 148;
 
 size_t model_smem_bytes() { return sizeof(ModelSmem); }
 
+template <class F>
+static void allow_smem(F* f, int optin) {
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, f) != cudaSuccess) { cudaGetLastError(); return; }
+    int dyn = optin - (int)a.sharedSizeBytes;
+    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess) cudaGetLastError();
+}
+
 void kernels_init() {
     static bool done = false;
     if (done) return;
@@ -1127,31 +1135,32 @@ void kernels_init() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    const int maxsm = 227 * 1024;
-    cudaFuncSetAttribute(k_classify_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_classify_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_scatter<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_scatter<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_scatter<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_scatter<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_scan_children, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_build_models<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_build_models<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_first_sample<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_first_sample<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_train_rmi_global, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_tree_build, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_block_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_classify_ids<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_classify_ids<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_small_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_small_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_base<128, 8, 1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_base<128, 8, 1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_base<256, 16, 4096, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_base<256, 16, 4096, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_base<512, 32, 8192, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_base<512, 32, 8192, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    int optin = 227 * 1024;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    allow_smem(k_classify_hist<true>, optin);
+    allow_smem(k_classify_hist<false>, optin);
+    allow_smem(k_scatter<true, false>, optin);
+    allow_smem(k_scatter<false, false>, optin);
+    allow_smem(k_scatter<true, true>, optin);
+    allow_smem(k_scatter<false, true>, optin);
+    allow_smem(k_scan_children, optin);
+    allow_smem(k_build_models<true>, optin);
+    allow_smem(k_build_models<false>, optin);
+    allow_smem(k_first_sample<true>, optin);
+    allow_smem(k_first_sample<false>, optin);
+    allow_smem(k_train_rmi_global, optin);
+    allow_smem(k_tree_build, optin);
+    allow_smem(k_block_sort, optin);
+    allow_smem(k_classify_ids<true>, optin);
+    allow_smem(k_classify_ids<false>, optin);
+    allow_smem(k_small_sort<true>, optin);
+    allow_smem(k_small_sort<false>, optin);
+    allow_smem(k_base<128, 8, 1024, true>, optin);
+    allow_smem(k_base<128, 8, 1024, false>, optin);
+    allow_smem(k_base<256, 16, 4096, true>, optin);
+    allow_smem(k_base<256, 16, 4096, false>, optin);
+    allow_smem(k_base<512, 32, 8192, true>, optin);
+    allow_smem(k_base<512, 32, 8192, false>, optin);
 }
 
 int num_sms() { return g_num_sms; }
