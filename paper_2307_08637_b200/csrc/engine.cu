@@ -115,7 +115,8 @@ struct lsort_ctx {
     cudaStream_t own_stream = nullptr;
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
-    DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux;
+    DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
+        kseg, ktp, kplan;
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
     std::unique_ptr<lsort_ctx> nested;
     cudaEvent_t ev[6] = {};
@@ -213,9 +214,10 @@ struct Engine {
         launched();
         nested_sort(C->sample.as<uint64_t>(), s2);
         if (trace_enabled()) CU(cudaEventRecord(C->ev[5], st));
-        launch_train_rmi_global(C->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
-                                hseg.rmi_b, st);
-        launched();
+        if (!C->train_ws.ensure(train_workspace_bytes(s2, hseg.rmi_b))) throw LsortError{LSORT_ENOMEM, "train ws"};
+        launch_train_rmi(C->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
+                         hseg.rmi_b, C->train_ws.p, st);
+        launched(7);
         if (trace_enabled()) {
             CU(cudaEventRecord(C->ev[4], st));
             CU(cudaEventSynchronize(C->ev[4]));
@@ -237,7 +239,7 @@ struct Engine {
         Ctrl* hc = C->hctrl.as<Ctrl>();
         const uint32_t cap = cfg.base_case_capacity;
         if (n <= cap) {
-            launch_small_sort(keys, n, f64, nullptr, dctrl, st);
+            launch_small_sort(keys, n, f64, dctrl, st);
             launched();
             CU(cudaMemcpyAsync(hc, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
             CU(cudaStreamSynchronize(st));
@@ -264,7 +266,7 @@ struct Engine {
             uint64_t* hp = C->hprefix.as<uint64_t>();
             uint32_t* hi = C->hidx.as<uint32_t>();
             uint64_t model_bytes = 0, nbuckets = 0, ntiles = 0;
-            uint32_t max_payload = 0, max_nb = 0, nsmall = 0;
+            uint32_t max_payload = 0, max_nb = 0, nsmall = 0, kinds = 0;
             std::vector<uint32_t> bigs;
             for (uint32_t i = 0; i < ns; ++i) {
                 const SegPlan& s = segs[i];
@@ -295,6 +297,8 @@ struct Engine {
                 ntiles += (s.n + kTileKeys - 1) / kTileKeys;
                 if (is_big(s)) bigs.push_back(i);
                 else hi[nsmall++] = i;
+                if (s.flags & kSegForceRadix) kinds |= 4u;
+                else kinds |= (s.n >= cfg.min_rmi_input ? 1u : 0u) | 2u;
             }
             hp[ns] = ntiles;
             const uint64_t list_cap = nbuckets;
@@ -302,7 +306,8 @@ struct Engine {
                 !C->idx.ensure(ns * 4) || !C->models.ensure(model_bytes) || !C->buckets.ensure(nbuckets * 8) ||
                 !C->rec.ensure(list_cap * sizeof(SegOut)) || !C->fill.ensure(list_cap * sizeof(FillItem)) ||
                 !C->base[0].ensure(list_cap * sizeof(BaseItem)) || !C->base[1].ensure(list_cap * sizeof(BaseItem)) ||
-                !C->base[2].ensure(list_cap * sizeof(BaseItem)))
+                !C->base[2].ensure(list_cap * sizeof(BaseItem)) || !C->kseg.ensure(3 * (size_t)ns * 4 + 16) ||
+                !C->ktp.ensure(3 * ((size_t)ns + 1) * 8) || !C->kplan.ensure(3 * sizeof(KindPlan)))
                 throw LsortError{LSORT_ENOMEM, "level workspace"};
             CU(cudaMemcpyAsync(C->segs.p, hs, ns * sizeof(SegDesc), cudaMemcpyHostToDevice, st));
             CU(cudaMemcpyAsync(C->tile_prefix.p, hp, (ns + 1) * 8, cudaMemcpyHostToDevice, st));
@@ -323,11 +328,15 @@ struct Engine {
             p.rec = C->rec.as<SegOut>();
             for (int c = 0; c < 3; ++c) p.base[c] = C->base[c].as<BaseItem>();
             p.fill = C->fill.as<FillItem>();
-            p.base_cap[0] = std::min<uint32_t>(1024, cap);
+            p.base_cap[0] = std::min<uint32_t>(kWarpBaseCap, cap);
             p.base_cap[1] = std::min<uint32_t>(4096, cap);
             p.base_cap[2] = cap;
             p.depth_cap = depth_cap;
             p.list_cap = (uint32_t)std::min<uint64_t>(list_cap, 0xffffffffu);
+            p.kseg = C->kseg.as<uint32_t>();
+            p.ktp = C->ktp.as<uint64_t>();
+            p.kplan = C->kplan.as<KindPlan>();
+            p.kstride = ns;
 
             const bool timing = (cfg.flags & LSORT_FLAG_PHASE_TIMING) && stats;
             auto mark = [&](int i) {
@@ -335,25 +344,26 @@ struct Engine {
             };
             mark(0);
             // ---- models
-            launch_build_models(p.segs, C->idx.as<uint32_t>(), nsmall, src, src_f64, C->models.as<uint8_t>(), dc, 0,
-                                st);
+            launch_build_models(p.segs, C->idx.as<uint32_t>(), nsmall, src, src_f64, C->models.as<uint8_t>(), dc, st);
             if (nsmall) launched();
             for (uint32_t b : bigs) big_model(p.segs + b, segs[b], hs[b], src, src_f64);
             // ---- partition
             const int nsm = num_sms();
             int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 4);
-            int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
+            int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 3);
+            const int nk = __builtin_popcount(kinds);
             mark(1);
-            launch_classify_hist(p, src_f64, (int)max_payload, grid_h, st);
+            launch_kind_plan(p, st);
+            launch_hist(p, src_f64, kinds, grid_h, st);
             launch_scan_children(p, st);
             mark(2);
-            launch_scatter(p, src_f64, (int)max_payload, (int)max_nb, grid_s, st);
+            launch_scatter(p, src_f64, kinds, max_nb, grid_s, st);
             mark(3);
-            launch_base_cases(p, dst, keys, nullptr, f64, 1, st);
+            launch_base_cases(p, dst, keys, f64, st);
             mark(4);
             launch_fill(p, keys, f64, nsm * 4, st);
             mark(5);
-            launched(7);
+            launched(2 + 2 * nk + 3 + 1);
             CU(cudaMemcpyAsync(hc, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
             CU(cudaStreamSynchronize(st));
             CU(cudaGetLastError());
@@ -452,7 +462,7 @@ void lsort_cfg_default(lsort_cfg* c) {
     c->seed = 0x5EEDull;
     c->workers = 0;
     c->base_case_capacity = 16384;
-    c->bucket_target = 4096;
+    c->bucket_target = 512;
     c->flags = 0;
 }
 
@@ -650,9 +660,10 @@ int lsort_cuda_rmi_train(lsort_ctx* C, const uint64_t* d_sample, uint64_t s, uin
     if (B > LSORT_MAX_RMI || s > 0xffffffffull) return fail(C, {LSORT_EINVAL, "Rmi::train: size limits"});
     try {
         CU(cudaSetDevice(C->device));
-        if (!C->models.ensure(sizeof(ModelHdr) + 32 * (size_t)B)) throw LsortError{LSORT_ENOMEM, "model"};
+        if (!C->models.ensure(sizeof(ModelHdr) + 32 * (size_t)B) || !C->train_ws.ensure(train_workspace_bytes(s, B)))
+            throw LsortError{LSORT_ENOMEM, "model"};
         CU(cudaMemsetAsync(C->models.p, 0, sizeof(ModelHdr), C->stream));
-        launch_train_rmi_global(d_sample, s, B, C->models.as<uint8_t>(), B, C->stream);
+        launch_train_rmi(d_sample, s, B, C->models.as<uint8_t>(), B, C->train_ws.p, C->stream);
         CU(cudaGetLastError());
         download_learned(C, C->models.as<uint8_t>(), B, h_out, e_out);
     } catch (const LsortError& e) {
@@ -743,7 +754,7 @@ int lsort_cuda_build_model(lsort_ctx* C, const void* d_keys, uint64_t n, int key
         const bool f64 = key_kind == LSORT_KEY_F64;
         if (E.is_big(sp)) E.big_model(C->segs.as<SegDesc>(), sp, d, d_keys, f64);
         else launch_build_models(C->segs.as<SegDesc>(), C->idx.as<uint32_t>(), 1, d_keys, f64,
-                                 C->models.as<uint8_t>(), dev_cfg(cfg), 0, C->stream);
+                                 C->models.as<uint8_t>(), dev_cfg(cfg), C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
         ModelHdr h;
@@ -841,8 +852,10 @@ int lsort_cuda_dist_train(lsort_ctx* C, uint64_t* d_sample, uint64_t s, uint32_t
         lsort_cfg_default(&cfg);
         Engine E(C, cfg);
         E.nested_sort(d_sample, s);
-        if (!C->models.ensure(sizeof(ModelHdr) + 32 * (size_t)buckets)) throw LsortError{LSORT_ENOMEM, "model"};
-        launch_train_rmi_global(d_sample, s, buckets, C->models.as<uint8_t>(), buckets, C->stream);
+        if (!C->models.ensure(sizeof(ModelHdr) + 32 * (size_t)buckets) ||
+            !C->train_ws.ensure(train_workspace_bytes(s, buckets)))
+            throw LsortError{LSORT_ENOMEM, "model"};
+        launch_train_rmi(d_sample, s, buckets, C->models.as<uint8_t>(), buckets, C->train_ws.p, C->stream);
         CU(cudaGetLastError());
         download_learned(C, C->models.as<uint8_t>(), buckets, h_out, e_out);
     } catch (const LsortError& e) {
@@ -912,8 +925,21 @@ int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int 
         p.src = d_keys;
         p.dst = d_out;
         p.ctrl = C->ctrl.as<Ctrl>();
-        int grid = (int)std::min<uint64_t>(pref[1], (uint64_t)num_sms() * 2);
-        launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, 32 * (int)B, dmap, nranks, grid, C->stream);
+        // single learned segment: a one-entry kind plan
+        if (!C->kseg.ensure(16) || !C->ktp.ensure(64) || !C->kplan.ensure(3 * sizeof(KindPlan)))
+            throw LsortError{LSORT_ENOMEM, "dist"};
+        KindPlan kp[3] = {{1, 0, pref[1]}, {0, 0, 0}, {0, 0, 0}};
+        uint32_t k0 = 0;
+        uint64_t tp[2] = {0, pref[1]};
+        CU(cudaMemcpyAsync(C->kseg.p, &k0, 4, cudaMemcpyHostToDevice, C->stream));
+        CU(cudaMemcpyAsync(C->ktp.p, tp, 16, cudaMemcpyHostToDevice, C->stream));
+        CU(cudaMemcpyAsync(C->kplan.p, kp, sizeof(kp), cudaMemcpyHostToDevice, C->stream));
+        p.kseg = C->kseg.as<uint32_t>();
+        p.ktp = C->ktp.as<uint64_t>();
+        p.kplan = C->kplan.as<KindPlan>();
+        p.kstride = 1;
+        int grid = (int)std::min<uint64_t>(pref[1], (uint64_t)num_sms() * 3);
+        launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, grid, C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
     } catch (const LsortError& er) {

@@ -45,6 +45,12 @@ struct Ctrl {
     unsigned long long pad[4];
 };
 
+// Per-kind (learned / tree / radix) segment lists of a level.
+struct KindPlan {
+    uint32_t nsegs, pad;
+    uint64_t ntiles;
+};
+
 // Parameters shared by the level kernels.
 struct LevelParams {
     const SegDesc* segs;
@@ -62,6 +68,10 @@ struct LevelParams {
     uint32_t base_cap[3];          // size classes: n <= base_cap[c]
     uint32_t depth_cap;
     uint32_t list_cap;             // capacity of rec/base/fill lists
+    uint32_t* kseg;                // [3][kstride] segment indices per kind
+    uint64_t* ktp;                 // [3][kstride+1] tile prefixes per kind
+    KindPlan* kplan;               // [3]
+    uint32_t kstride;
 };
 
 // Sort configuration as seen by kernels.
@@ -78,35 +88,39 @@ constexpr int kPartNT = 512;        // threads per classify/scatter CTA
 constexpr int kRadixBits = 10;      // fallback radix model: 1024 buckets
 constexpr uint32_t kSmallSampleCap = 16384;  // samples sortable in one CTA
 
-// Host-visible launchers (kernels.cu).
+// Host-visible launchers.
+// models.cu
 void launch_build_models(const SegDesc* segs, const uint32_t* idx, uint32_t count, const void* src,
-                         int in_f64, uint8_t* models, const DevCfg& cfg, int smem_bytes,
-                         cudaStream_t st);
+                         int in_f64, uint8_t* models, const DevCfg& cfg, cudaStream_t st);
 void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_t* models,
                          const DevCfg& cfg, cudaStream_t st);
 void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0,
                    uint64_t s, uint64_t* out, cudaStream_t st);
-void launch_train_rmi_global(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* model,
-                             uint32_t nbuckets, cudaStream_t st);
-void launch_classify_hist(const LevelParams& p, int in_f64, int max_payload, int grid, cudaStream_t st);
-void launch_scan_children(const LevelParams& p, cudaStream_t st);
-void launch_scatter(const LevelParams& p, int in_f64, int max_payload, int max_nb, int grid,
-                    cudaStream_t st);
-void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, uint64_t* scratch,
-                       int out_f64, int grid_mult, cudaStream_t st);
-void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st);
-void launch_small_sort(void* keys, uint64_t n, int f64, uint64_t* scratch, Ctrl* ctrl, cudaStream_t st);
-void launch_classify_ids(const uint8_t* model, const void* keys, uint64_t n, int in_f64,
-                         uint32_t* ids, unsigned long long* hist, int payload, cudaStream_t st);
+size_t train_workspace_bytes(uint64_t s, uint32_t B);
+void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* model, uint32_t nbuckets,
+                      void* ws, cudaStream_t st);
 void launch_tree_build(const uint64_t* sorted, uint64_t s, uint32_t budget, int eq_mode, uint8_t* model,
                        cudaStream_t st);
+void launch_block_sort(uint64_t* keys, uint64_t n, cudaStream_t st);
+// partition.cu
+void launch_kind_plan(const LevelParams& p, cudaStream_t st);
+void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, int grid, cudaStream_t st);
+void launch_scan_children(const LevelParams& p, cudaStream_t st);
+void launch_scatter(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t nb_cap, int grid, cudaStream_t st);
+void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,
+                           cudaStream_t st);
+// basecase.cu
+void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
+void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st);
+void launch_small_sort(void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st);
+// util.cu
+void launch_classify_ids(const uint8_t* model, const void* keys, uint64_t n, int in_f64,
+                         uint32_t* ids, unsigned long long* hist, int payload, cudaStream_t st);
 void launch_verify(const void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st);
 void launch_decode(uint64_t* keys, uint64_t n, cudaStream_t st);
-void launch_scatter_mapped(const LevelParams& p, int in_f64, int max_payload, const uint32_t* map,
-                           uint32_t nmapped, int grid, cudaStream_t st);
 int num_sms();
-size_t model_smem_bytes();
-void launch_block_sort(uint64_t* keys, uint64_t n, cudaStream_t st);
-void kernels_init();   // cudaFuncSetAttribute for large dynamic shared memory
+void kernels_init();   // shared-memory opt-in for every kernel
+
+constexpr uint32_t kWarpBaseCap = 512;   // segments <= this: warp-level base case
 
 }  // namespace lsort_dev

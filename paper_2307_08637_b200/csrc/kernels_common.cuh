@@ -1,0 +1,186 @@
+// kernels_common.cuh -- device helpers shared by the partition, model,
+// base-case and utility kernels.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace lsort_dev {
+
+#define FULL_MASK 0xffffffffu
+
+__device__ __forceinline__ uint64_t load_key(const void* src, uint64_t i, bool f64) {
+    uint64_t v = ((const uint64_t*)src)[i];
+    return f64 ? encode(__longlong_as_double((long long)v)) : v;
+}
+
+// Per-segment sampling stream (same definition as oracle lso_seg_seed).
+__device__ __forceinline__ uint64_t seg_seed(uint64_t cfg_seed, uint64_t begin, uint32_t depth) {
+    return splitmix64(cfg_seed ^ splitmix64(begin + ((uint64_t)depth << 48)));
+}
+// SPEC.md:438 (same double arithmetic as oracle lso_first_sample_size)
+__device__ __forceinline__ uint64_t first_sample_size(const DevCfg& c, uint64_t n) {
+    double v = __dmul_rn(c.sample_fraction, __ull2double_rn(n));
+    double cap = (double)c.first_sample_cap;
+    uint64_t s = (uint64_t)ceil(v < cap ? v : cap);
+    return s < 2 ? 2 : s;
+}
+__device__ __forceinline__ uint64_t rmi_sample_size(const DevCfg& c, uint64_t n) {
+    double v = __dmul_rn(c.sample_fraction, __ull2double_rn(n));
+    double cap = (double)c.rmi_sample_cap;
+    uint64_t s = (uint64_t)ceil(v < cap ? v : cap);
+    return s < 2 ? 2 : s;
+}
+
+__device__ __forceinline__ uint32_t model_payload_bytes(const ModelHdr& h) {
+    if (h.kind == kLearned) return 32u * h.B;
+    if (h.kind == kTree) return (uint32_t)((tree_payload_bytes(h.leaf_origin, h.nsplit) + 15) & ~15ull);
+    return 0;
+}
+
+// Copy a model record (header + payload) into shared memory.
+__device__ __forceinline__ void load_model_smem(const uint8_t* g, uint8_t* s) {
+    const uint4* gs = (const uint4*)g;
+    uint4* ss = (uint4*)s;
+    if (threadIdx.x < 8) ss[threadIdx.x] = gs[threadIdx.x];
+    __syncthreads();
+    uint32_t words = model_payload_bytes(*(const ModelHdr*)s) / 16;
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) ss[8 + i] = gs[8 + i];
+    __syncthreads();
+}
+
+struct MView {
+    const ModelHdr* h;
+    const RmiEntry* e;
+    const uint64_t* tree;
+    const uint64_t* spl;
+    const uint32_t* eqo;
+};
+__device__ __forceinline__ MView model_view(const uint8_t* s) {
+    MView m;
+    m.h = (const ModelHdr*)s;
+    const uint8_t* p = s + sizeof(ModelHdr);
+    m.e = (const RmiEntry*)p;
+    m.tree = (const uint64_t*)p;
+    m.spl = m.tree + m.h->leaf_origin;
+    m.eqo = (const uint32_t*)(m.spl + m.h->nsplit);
+    return m;
+}
+
+// Generic classifier over a model copied to shared memory (unit-test and
+// multi-GPU paths; the hot partition kernels use per-kind specialisations).
+struct Classifier {
+    uint32_t kind, nb, B, levels, leaf_origin, nsplit, shift;
+    double rs, ri, base, scale, cdf_lo, inv_span;
+    uint64_t rmin;
+    MView m;
+    __device__ __forceinline__ void init(const uint8_t* s) {
+        m = model_view(s);
+        const ModelHdr& h = *m.h;
+        kind = h.kind; nb = h.nbuckets; B = h.B; levels = h.levels; leaf_origin = h.leaf_origin;
+        nsplit = h.nsplit; shift = h.shift; rs = h.root_slope; ri = h.root_icpt; base = h.key_base;
+        scale = h.key_scale; cdf_lo = h.cdf_lo; inv_span = h.inv_span; rmin = h.radix_min;
+    }
+    template <uint32_t KIND>
+    __device__ __forceinline__ uint32_t classify(uint64_t x) const {
+        if constexpr (KIND == kLearned) {
+            double xn = rmi_normalize(base, scale, x);
+            uint32_t i = rmi_route(rs, ri, B, xn);
+            const RmiEntry s = m.e[i];
+            double v = __dadd_rn(__dmul_rn(s.slope, xn), s.intercept);
+            if (v < s.lo) v = s.lo;
+            if (v > s.hi) v = s.hi;
+            if (v < 0.0) v = 0.0;
+            if (v > 1.0) v = 1.0;
+            double t = __dmul_rn(__dmul_rn(__dsub_rn(v, cdf_lo), inv_span), (double)nb);
+            if (!(t > 0.0)) return 0;
+            if (t >= (double)nb) return nb - 1;
+            return (uint32_t)t;
+        } else if constexpr (KIND == kTree) {
+            return tree_bucket(levels, leaf_origin, nsplit, m.tree, m.spl, m.eqo, x);
+        } else if constexpr (KIND == kRadix) {
+            uint64_t d = (x - rmin) >> shift;
+            return d >= nb ? nb - 1 : (uint32_t)d;
+        } else {
+            return 0u | (1u << 31);
+        }
+    }
+    __device__ __forceinline__ uint32_t classify_any(uint64_t x) const {
+        switch (kind) {
+        case kLearned: return classify<kLearned>(x);
+        case kTree: return classify<kTree>(x);
+        case kRadix: return classify<kRadix>(x);
+        default: return classify<kFill>(x);
+        }
+    }
+};
+
+// Warp-aggregated shared-memory histogram add (all lanes must call): lanes
+// holding the same bucket id are grouped with __match_any_sync and the
+// group's lowest lane adds the group size. (__reduce_add_sync over the
+// per-group mask compiles to a per-group REDUX loop -- 32 iterations for
+// distinct ids, measured 31x the instruction count -- so __popc is used.)
+__device__ __forceinline__ void hist_add_warp(uint32_t* hist, uint32_t b, bool valid) {
+    unsigned vmask = __ballot_sync(FULL_MASK, valid);
+    if (valid) {
+        unsigned peers = __match_any_sync(vmask, b);
+        if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&hist[b], (unsigned)__popc(peers));
+    }
+}
+// Warp-aggregated add returning this lane's rank within its bucket (all lanes must call).
+__device__ __forceinline__ uint32_t hist_rank_warp(uint32_t* hist, uint32_t b, bool valid) {
+    unsigned vmask = __ballot_sync(FULL_MASK, valid);
+    unsigned peers = 0;
+    int leader = 0;
+    uint32_t old = 0;
+    const int lane = threadIdx.x & 31;
+    if (valid) {
+        peers = __match_any_sync(vmask, b);
+        leader = __ffs(peers) - 1;
+        if (lane == leader) old = atomicAdd(&hist[b], (uint32_t)__popc(peers));
+    }
+    old = __shfl_sync(FULL_MASK, old, leader);
+    return valid ? old + __popc(peers & ((1u << lane) - 1u)) : 0u;
+}
+
+// last s in [0,n) with prefix[s] <= tile
+__device__ __forceinline__ uint32_t find_seg(const uint64_t* prefix, uint32_t nsegs, uint64_t tile) {
+    uint32_t lo = 0, hi = nsegs;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (prefix[mid] <= tile) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// Tile geometry: keys [lo,hi) read as 16-byte pairs over the 16-byte aligned
+// interior plus at most two single keys (head / tail).
+struct TileGeom {
+    uint64_t lo, hi, a0;
+    uint32_t npairs;
+    uint32_t nsingle;
+    uint64_t single[2];
+    __device__ __forceinline__ void init(const void* base, uint64_t l, uint64_t h) {
+        lo = l; hi = h;
+        uint64_t par = (((uintptr_t)base) >> 3) & 1;
+        a0 = lo + ((lo + par) & 1);
+        if (a0 > hi) a0 = hi;
+        npairs = (uint32_t)((hi - a0) / 2);
+        nsingle = 0;
+        if (a0 > lo) single[nsingle++] = lo;
+        uint64_t t = a0 + 2ull * npairs;
+        if (t < hi) single[nsingle++] = t;
+    }
+};
+
+template <class F>
+inline void allow_smem(F* f, int optin) {
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, f) != cudaSuccess) { cudaGetLastError(); return; }
+    int dyn = optin - (int)a.sharedSizeBytes;
+    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess) cudaGetLastError();
+}
+
+}  // namespace lsort_dev

@@ -374,8 +374,8 @@ struct BlockSort {
             __syncthreads();
             return;
         }
-        uint32_t nb = 1;
-        while (nb < len && nb < (uint32_t)NBMAX) nb <<= 1;
+        uint32_t nb = 1;  // ~2 keys per digit
+        while (2 * nb < len && nb < (uint32_t)NBMAX) nb <<= 1;
         uint32_t lgnb = __ffs(nb) - 1;
         uint32_t bits = bitlen64(mx - mn);
         uint32_t shift = bits > lgnb ? bits - lgnb : 0;

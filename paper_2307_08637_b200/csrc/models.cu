@@ -1,0 +1,794 @@
+// models.cu -- partition-model construction on the device (Alg. 5,
+// SPEC.md:375-383).
+//
+//   k_build_models   one CTA per segment: device-drawn samples (Rng stream of
+//                    the segment, rng.hpp:35-37), shared-memory sample sort,
+//                    duplicate fraction (models.cpp:187-193), then RMI
+//                    training (models.cpp:14-131) or SplitterTree::build
+//                    (models.cpp:133-185) for samples <= 16384 keys.
+//   k_first_sample   the same policy step for a big segment (first sample only).
+//   k_gather         device-wide gather of a big RMI sample.
+//   k_train_*        multi-CTA RMI training over a sorted sample in global
+//                    memory: deterministic chunked root sums, per-submodel
+//                    fits (sequential = bit-exact for slices <= 512 samples,
+//                    one CTA per larger slice), single-CTA monotone clamps.
+#include <algorithm>
+
+#include "kernels_common.cuh"
+
+namespace lsort_dev {
+
+// ------------------------------------------------------- model building
+// Fold step of the reference's running max (std::max(lo[m], lo[m-1]),
+// models.cpp:110): keep the new element unless it is strictly smaller.
+struct StepMax { __device__ double operator()(double acc, double e) const { return (e < acc) ? acc : e; } };
+// std::min(hi[m], hi[m+1]) folded right to left (models.cpp:111)
+struct StepMin { __device__ double operator()(double acc, double e) const { return (acc < e) ? acc : e; } };
+
+// Inclusive sequential-fold scan of a[0,n) in processing order (reverse =
+// right to left). Each step is `acc = op(acc, e)`; chunked per thread, with
+// chunk carries combined by the same op (exact for these fold rules).
+template <int NT, class Op>
+__device__ void block_fold_scan(double* a, uint32_t n, bool reverse, double* wtmp, Op op) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t per = (n + NT - 1) / NT;
+    const uint32_t lo = threadIdx.x * per, hi = min(lo + per, n);
+    auto at = [&](uint32_t i) -> double& { return reverse ? a[n - 1 - i] : a[i]; };
+    bool have = lo < hi;
+    double acc = 0.0;
+    if (have) {
+        acc = at(lo);
+        for (uint32_t i = lo + 1; i < hi; ++i) acc = op(acc, at(i));
+    }
+    // exclusive carry across threads in order
+    double inc = acc;
+    bool hinc = have;
+    for (int o = 1; o < 32; o <<= 1) {
+        double w = __shfl_up_sync(FULL_MASK, inc, o);
+        bool hw = __shfl_up_sync(FULL_MASK, (int)hinc, o);
+        if (lane >= o && hw) { inc = hinc ? op(w, inc) : w; hinc = true; }
+    }
+    __syncthreads();
+    if (lane == 31) { wtmp[2 * warp] = inc; wtmp[2 * warp + 1] = hinc ? 1.0 : 0.0; }
+    __syncthreads();
+    if (warp == 0) {
+        double x = lane < NT / 32 ? wtmp[2 * lane] : 0.0;
+        bool hx = lane < NT / 32 ? wtmp[2 * lane + 1] != 0.0 : false;
+        double ix = x;
+        bool hix = hx;
+        for (int o = 1; o < 32; o <<= 1) {
+            double w = __shfl_up_sync(FULL_MASK, ix, o);
+            bool hw = __shfl_up_sync(FULL_MASK, (int)hix, o);
+            if (lane >= o && hw) { ix = hix ? op(w, ix) : w; hix = true; }
+        }
+        // exclusive for warp `lane`: inclusive of lane-1
+        double ex = __shfl_up_sync(FULL_MASK, ix, 1);
+        bool hex = __shfl_up_sync(FULL_MASK, (int)hix, 1);
+        if (lane == 0) hex = false;
+        __syncwarp();
+        if (lane < NT / 32) { wtmp[2 * lane] = ex; wtmp[2 * lane + 1] = hex ? 1.0 : 0.0; }
+    }
+    __syncthreads();
+    // carry for this thread = warp carry combined with lanes before it
+    double wc = wtmp[2 * warp];
+    bool hwc = wtmp[2 * warp + 1] != 0.0;
+    double lex = __shfl_up_sync(FULL_MASK, inc, 1);
+    bool hlex = __shfl_up_sync(FULL_MASK, (int)hinc, 1);
+    if (lane == 0) hlex = false;
+    double carry = 0.0;
+    bool hc = false;
+    if (hwc) { carry = wc; hc = true; }
+    if (hlex) { carry = hc ? op(carry, lex) : lex; hc = true; }
+    if (have) {
+        double x = hc ? op(carry, at(lo)) : at(lo);
+        at(lo) = x;
+        for (uint32_t i = lo + 1; i < hi; ++i) { x = op(x, at(i)); at(i) = x; }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double dmax_ref(double a, double b) { return (a < b) ? b : a; }  // std::max
+__device__ __forceinline__ double dmin_ref(double a, double b) { return (b < a) ? b : a; }  // std::min
+__device__ __forceinline__ double dclamp01(double v) { return (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v); }
+
+// Sequential fit_line (models.cpp:14-35) over [first,last) -- bit-exact.
+struct Fit { double slope, intercept; };
+template <class XN>
+__device__ Fit fit_seq(XN xn, uint32_t first, uint32_t last, double inv_n_total, double n_total) {
+    uint32_t n = last - first;
+    if (n == 0) return {0.0, 0.0};
+    double sx = 0.0, sy = 0.0;
+    for (uint32_t i = first; i < last; ++i) {
+        sx = __dadd_rn(sx, xn(i));
+        sy = __dadd_rn(sy, __ddiv_rn((double)i, n_total));
+    }
+    double mx = __ddiv_rn(sx, (double)n), my = __ddiv_rn(sy, (double)n);
+    double sxx = 0.0, sxy = 0.0;
+    for (uint32_t i = first; i < last; ++i) {
+        double dx = __dsub_rn(xn(i), mx);
+        sxx = __dadd_rn(sxx, __dmul_rn(dx, dx));
+        sxy = __dadd_rn(sxy, __dmul_rn(dx, __dsub_rn(__ddiv_rn((double)i, n_total), my)));
+    }
+    if (!(sxx > 0.0)) return {0.0, my};
+    double slope = __ddiv_rn(sxy, sxx);
+    if (slope < 0.0) return {0.0, my};
+    return {slope, __dsub_rn(my, __dmul_rn(slope, mx))};
+}
+
+// Warp-cooperative fit (deterministic lane-chunk order; not the reference's
+// sequential order: within a few ulps of it).
+template <class XN>
+__device__ Fit fit_warp(XN xn, uint32_t first, uint32_t last, double n_total) {
+    const int lane = threadIdx.x & 31;
+    uint32_t n = last - first;
+    uint32_t per = (n + 31) / 32;
+    uint32_t lo = first + min(n, lane * per), hi = first + min(n, (lane + 1) * per);
+    double sx = 0.0, sy = 0.0;
+    for (uint32_t i = lo; i < hi; ++i) {
+        sx = __dadd_rn(sx, xn(i));
+        sy = __dadd_rn(sy, __ddiv_rn((double)i, n_total));
+    }
+    for (int o = 1; o < 32; o <<= 1) {  // fixed-order pairwise tree
+        double a = __shfl_down_sync(FULL_MASK, sx, o), b = __shfl_down_sync(FULL_MASK, sy, o);
+        if ((lane & (2 * o - 1)) == 0) { sx = __dadd_rn(sx, a); sy = __dadd_rn(sy, b); }
+    }
+    sx = __shfl_sync(FULL_MASK, sx, 0);
+    sy = __shfl_sync(FULL_MASK, sy, 0);
+    double mx = __ddiv_rn(sx, (double)n), my = __ddiv_rn(sy, (double)n);
+    double sxx = 0.0, sxy = 0.0;
+    for (uint32_t i = lo; i < hi; ++i) {
+        double dx = __dsub_rn(xn(i), mx);
+        sxx = __dadd_rn(sxx, __dmul_rn(dx, dx));
+        sxy = __dadd_rn(sxy, __dmul_rn(dx, __dsub_rn(__ddiv_rn((double)i, n_total), my)));
+    }
+    for (int o = 1; o < 32; o <<= 1) {
+        double a = __shfl_down_sync(FULL_MASK, sxx, o), b = __shfl_down_sync(FULL_MASK, sxy, o);
+        if ((lane & (2 * o - 1)) == 0) { sxx = __dadd_rn(sxx, a); sxy = __dadd_rn(sxy, b); }
+    }
+    sxx = __shfl_sync(FULL_MASK, sxx, 0);
+    sxy = __shfl_sync(FULL_MASK, sxy, 0);
+    if (!(sxx > 0.0)) return {0.0, my};
+    double slope = __ddiv_rn(sxy, sxx);
+    if (slope < 0.0) return {0.0, my};
+    return {slope, __dsub_rn(my, __dmul_rn(slope, mx))};
+}
+
+// Rmi::train + enforce_monotonic (models.cpp:39-131) by one CTA over a sorted
+// sample s[0,n) (shared or global memory). Scratch (shared): first[B+1] u32,
+// lo[B], hi[B] doubles, big-slice list. Output: header + entries (global).
+constexpr int kSeqFitMax = 512;
+template <int NT>
+__device__ void train_rmi_block(const uint64_t* s, uint32_t n, uint32_t B, ModelHdr* hdr, RmiEntry* E,
+                                uint32_t* first, double* lo, double* hi, uint32_t* biglist, double* red) {
+    const double base = __ull2double_rn(s[0]);
+    const double kmax = __ull2double_rn(s[n - 1]);
+    const double scale = kmax > base ? __ddiv_rn(1.0, __dsub_rn(kmax, base)) : 0.0;
+    const double nd = (double)n;
+    auto xn = [&](uint32_t i) { return rmi_normalize(base, scale, s[i]); };
+    // root fit_line over the whole sample: deterministic block reduction
+    const uint32_t per = (n + NT - 1) / NT;
+    const uint32_t lo0 = min(n, threadIdx.x * per), hi0 = min(n, lo0 + per);
+    double sx = 0.0, sy = 0.0;
+    for (uint32_t i = lo0; i < hi0; ++i) {
+        sx = __dadd_rn(sx, xn(i));
+        sy = __dadd_rn(sy, __ddiv_rn((double)i, nd));
+    }
+    sx = block_sum_f64<NT>(sx, red);
+    sy = block_sum_f64<NT>(sy, red);
+    const double mx = __ddiv_rn(sx, nd), my = __ddiv_rn(sy, nd);
+    double sxx = 0.0, sxy = 0.0;
+    for (uint32_t i = lo0; i < hi0; ++i) {
+        double dx = __dsub_rn(xn(i), mx);
+        sxx = __dadd_rn(sxx, __dmul_rn(dx, dx));
+        sxy = __dadd_rn(sxy, __dmul_rn(dx, __dsub_rn(__ddiv_rn((double)i, nd), my)));
+    }
+    sxx = block_sum_f64<NT>(sxx, red);
+    sxy = block_sum_f64<NT>(sxy, red);
+    double rs, ri;
+    if (!(sxx > 0.0)) { rs = 0.0; ri = my; }
+    else {
+        double sl = __ddiv_rn(sxy, sxx);
+        if (sl < 0.0) { rs = 0.0; ri = my; }
+        else { rs = sl; ri = __dsub_rn(my, __dmul_rn(sl, mx)); }
+    }
+    // fit_line never returns a negative slope, so enforce_monotonic's
+    // root/submodel negative-slope repairs (models.cpp:83-86,99-100) are no-ops.
+    // Slice boundaries: first[m] = min{i : route(xn(i)) >= m} (routes are
+    // nondecreasing along the sorted sample).
+    for (uint32_t m = threadIdx.x; m <= B; m += NT) {
+        uint32_t a = 0, b = n;
+        if (m == 0) b = 0;
+        else if (m == B) a = n;
+        while (a < b) {
+            uint32_t mid = (a + b) >> 1;
+            if (rmi_route(rs, ri, B, xn(mid)) >= m) b = mid; else a = mid + 1;
+        }
+        first[m] = a;
+    }
+    __shared__ uint32_t nbig;
+    if (threadIdx.x == 0) nbig = 0;
+    __syncthreads();
+    for (uint32_t m = threadIdx.x; m < B; m += NT) {
+        uint32_t f = first[m], l = first[m + 1];
+        if (l - f > (uint32_t)kSeqFitMax) {
+            biglist[atomicAdd(&nbig, 1u)] = m;
+            continue;
+        }
+        Fit ft = fit_seq(xn, f, l, 0.0, nd);
+        E[m].slope = ft.slope;
+        E[m].intercept = ft.intercept;
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x >> 5; q < nbig; q += NT / 32) {
+        uint32_t m = biglist[q];
+        Fit ft = fit_warp(xn, first[m], first[m + 1], nd);
+        if ((threadIdx.x & 31) == 0) {
+            E[m].slope = ft.slope;
+            E[m].intercept = ft.intercept;
+        }
+    }
+    __syncthreads();
+    // enforce_monotonic (models.cpp:101-126)
+    for (uint32_t m = threadIdx.x; m < B; m += NT) {
+        uint32_t f = first[m], l = first[m + 1];
+        if (l > f) {
+            double sl = E[m].slope, ic = E[m].intercept;
+            lo[m] = __dadd_rn(__dmul_rn(sl, xn(f)), ic);
+            hi[m] = __dadd_rn(__dmul_rn(sl, xn(l - 1)), ic);
+        } else {
+            lo[m] = -INFINITY;
+            hi[m] = INFINITY;
+        }
+    }
+    __syncthreads();
+    block_fold_scan<NT>(lo, B, false, red, StepMax());
+    block_fold_scan<NT>(hi, B, true, red, StepMin());
+    double* hi2 = lo + B;  // lo/hi arrays are adjacent? use registers instead
+    (void)hi2;
+    for (uint32_t m = threadIdx.x; m < B; m += NT) {
+        double h = hi[m];
+        if (m + 1 < B) h = dmin_ref(h, lo[m + 1]);
+        h = dmax_ref(h, lo[m]);
+        double l = dclamp01(lo[m]);
+        h = dclamp01(h);
+        if (m == 0) l = 0.0;
+        if (m == B - 1) h = 1.0;
+        if (first[m + 1] == first[m]) {
+            E[m].slope = 0.0;
+            E[m].intercept = __dmul_rn(0.5, __dadd_rn(l, h));
+        }
+        E[m].lo = l;
+        E[m].hi = h;
+    }
+    if (threadIdx.x == 0) {
+        hdr->root_slope = rs;
+        hdr->root_icpt = ri;
+        hdr->key_base = base;
+        hdr->key_scale = scale;
+        hdr->B = B;
+    }
+    __syncthreads();
+}
+
+// SplitterTree::build (models.cpp:133-185) by one CTA from a sorted sample in
+// shared memory. Scratch: u32[2k].
+template <int NT>
+__device__ void tree_build_block(const uint64_t* s, uint32_t n, uint32_t k, bool eq_mode, ModelHdr* hdr,
+                                 uint8_t* payload, uint32_t* scratch, uint32_t* wsum, uint64_t* spl_tmp) {
+    uint32_t* keep = scratch;      // k entries
+    uint32_t* eqo = scratch + k;   // k entries (+1)
+    for (uint32_t i = threadIdx.x; i + 1 < k; i += NT) {
+        uint64_t q = (uint64_t)(i + 1) * n / k;
+        uint32_t pos = (uint32_t)((q > 1 ? q : 1) - 1);
+        uint64_t v = s[pos];
+        bool kp = true;
+        if (i > 0) {
+            uint64_t qp = (uint64_t)i * n / k;
+            uint32_t pp = (uint32_t)((qp > 1 ? qp : 1) - 1);
+            kp = v > s[pp];
+        }
+        keep[i] = kp ? 1u : 0u;
+    }
+    __syncthreads();
+    uint32_t m = block_exclusive_scan_u32<NT>(keep, k - 1, wsum);
+    for (uint32_t i = threadIdx.x; i + 1 < k; i += NT) {
+        uint32_t nxt = (i + 2 < k) ? keep[i + 1] : m;
+        if (nxt != keep[i]) {  // kept
+            uint64_t q = (uint64_t)(i + 1) * n / k;
+            uint32_t pos = (uint32_t)((q > 1 ? q : 1) - 1);
+            spl_tmp[keep[i]] = s[pos];
+        }
+    }
+    __syncthreads();
+    if (m == 0) {  // defensive (k >= 2 always keeps candidate 0)
+        if (threadIdx.x == 0) spl_tmp[0] = s[0];
+        m = 1;
+        __syncthreads();
+    }
+    for (uint32_t j = threadIdx.x; j < m; j += NT) {
+        uint64_t v = spl_tmp[j];
+        uint32_t a = 0, b = n;  // lower_bound
+        while (a < b) { uint32_t mid = (a + b) >> 1; if (s[mid] < v) a = mid + 1; else b = mid; }
+        uint32_t f = a;
+        b = n;  // upper_bound
+        while (a < b) { uint32_t mid = (a + b) >> 1; if (v < s[mid]) b = mid; else a = mid + 1; }
+        uint64_t count = a - f;
+        bool heavy = eq_mode && count * (uint64_t)k > (uint64_t)n;
+        eqo[j] = heavy ? 2u : 1u;
+    }
+    __syncthreads();
+    uint32_t total = block_exclusive_scan_u32<NT>(eqo, m, wsum);
+    if (threadIdx.x == 0) eqo[m] = total;
+    __syncthreads();
+    uint32_t levels = 1;
+    while ((1u << levels) < m + 1) ++levels;
+    uint32_t leaf = 1u << levels;
+    uint64_t* tree = (uint64_t*)payload;
+    uint64_t* spl = tree + leaf;
+    uint32_t* eq_out = (uint32_t*)(spl + m);
+    for (uint32_t j = threadIdx.x; j < leaf; j += NT) {
+        if (j == 0) { tree[0] = 0; continue; }
+        uint32_t d = 31 - __clz(j);
+        uint32_t pidx = j - (1u << d);
+        uint32_t io = ((2 * pidx + 1) << (levels - 1 - d)) - 1;
+        tree[j] = io < m ? spl_tmp[io] : ~0ull;
+    }
+    for (uint32_t j = threadIdx.x; j < m; j += NT) spl[j] = spl_tmp[j];
+    for (uint32_t j = threadIdx.x; j <= m; j += NT) eq_out[j] = eqo[j];
+    if (threadIdx.x == 0) {
+        hdr->kind = kTree;
+        hdr->levels = levels;
+        hdr->leaf_origin = leaf;
+        hdr->nsplit = m;
+        hdr->nbuckets = total + 1;
+    }
+    __syncthreads();
+}
+
+constexpr int kModelNT = 512;
+using ModelSort = BlockSort<kModelNT, 32, 8192>;
+struct ModelSmem {
+    uint64_t a[16384];
+    union {
+        typename ModelSort::Smem sort;
+        struct {
+            uint32_t first[LSORT_MAX_RMI_DEV + 1];
+            double lo[LSORT_MAX_RMI_DEV];
+            double hi[LSORT_MAX_RMI_DEV];
+            uint32_t big[LSORT_MAX_RMI_DEV];
+            double red[2 * (kModelNT / 32)];
+        } rmi;
+        struct {
+            uint32_t scratch[2 * LSORT_MAX_TREE_DEV + 2];
+            uint32_t wsum[kModelNT / 32 + 1];
+            uint64_t spl[LSORT_MAX_TREE_DEV];
+        } tree;
+    } u;
+    uint64_t red64[kModelNT / 32];
+    uint32_t distinct;
+};
+
+// Radix/fill fallback model: min/max of the whole segment (one CTA).
+__device__ void build_radix_model(const SegDesc& sd, const void* src, bool f64, ModelHdr* h, uint64_t* red) {
+    uint64_t mn = ~0ull, mx = 0;
+    for (uint64_t i = threadIdx.x; i < sd.n; i += kModelNT) {
+        uint64_t k = load_key(src, sd.begin + i, f64);
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+    }
+    mn = block_reduce_min<kModelNT>(mn, red);
+    mx = block_reduce_max<kModelNT>(mx, red);
+    if (threadIdx.x == 0) {
+        if (mn == mx) {
+            h->kind = kFill;
+            h->nbuckets = 1;
+        } else {
+            uint32_t bits = bitlen64(mx - mn);
+            h->kind = kRadix;
+            h->shift = bits > kRadixBits ? bits - kRadixBits : 0;
+            h->nbuckets = (uint32_t)((mx - mn) >> h->shift) + 1;
+        }
+        h->radix_min = mn;
+    }
+    __syncthreads();
+}
+
+// Alg. 5 build_partition_model for one segment.
+template <bool IN_F64>
+__device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* models, const DevCfg& cfg,
+                                ModelSmem& S, bool first_only) {
+    ModelHdr* h = (ModelHdr*)(models + sd.model_off);
+    uint8_t* payload = models + sd.model_off + sizeof(ModelHdr);
+    if (sd.flags & kSegForceRadix) {
+        build_radix_model(sd, src, IN_F64, h, S.red64);
+        return;
+    }
+    const uint64_t n = sd.n;
+    const uint64_t seed = seg_seed(cfg.seed, sd.begin, sd.depth);
+    const uint32_t s1 = (uint32_t)first_sample_size(cfg, n);
+    uint64_t k[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        uint32_t idx = threadIdx.x + i * kModelNT;
+        if (idx < s1) k[i] = load_key(src, sd.begin + sample_index(seed, idx, n), IN_F64);
+    }
+    ModelSort::sort_regs(k, S.a, s1, S.u.sort);
+    __syncthreads();
+    uint64_t d = 0;
+    for (uint32_t i = threadIdx.x + 1; i < s1; i += kModelNT) d += S.a[i] != S.a[i - 1];
+    d = block_reduce_sum_u64<kModelNT>(d, S.red64);
+    const uint64_t distinct = 1 + d;
+    const double dup = __dsub_rn(1.0, __ddiv_rn((double)distinct, (double)s1));  // models.cpp:187-193
+    const bool learned = n >= cfg.min_rmi_input && dup <= cfg.max_dup;
+    if (threadIdx.x == 0) {
+        h->dup = dup;
+        h->s1 = s1;
+        h->flags = 0;
+        h->cdf_lo = 0.0;
+        h->inv_span = 1.0;  // Learned::inv_span() with cdf [0,1] (models.hpp:134-137)
+    }
+    if (learned) {
+        const uint32_t s2 = (uint32_t)rmi_sample_size(cfg, n);
+        if (threadIdx.x == 0) {
+            h->kind = kLearned;
+            h->nbuckets = sd.rmi_b;
+            h->B = sd.rmi_b;
+            h->s2 = s2;
+        }
+        if (first_only) { __syncthreads(); return; }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            uint32_t idx = threadIdx.x + i * kModelNT;
+            if (idx < s2) k[i] = load_key(src, sd.begin + sample_index(seed, s1 + idx, n), IN_F64);
+        }
+        __syncthreads();
+        ModelSort::sort_regs(k, S.a, s2, S.u.sort);
+        __syncthreads();
+        train_rmi_block<kModelNT>(S.a, s2, sd.rmi_b, h, (RmiEntry*)payload, S.u.rmi.first, S.u.rmi.lo,
+                                  S.u.rmi.hi, S.u.rmi.big, S.u.rmi.red);
+    } else {
+        if (threadIdx.x == 0) h->s2 = 0;
+        tree_build_block<kModelNT>(S.a, s1, sd.tree_k, true, h, payload, S.u.tree.scratch, S.u.tree.wsum,
+                                   S.u.tree.spl);
+    }
+}
+
+template <bool IN_F64>
+__global__ void __launch_bounds__(kModelNT) k_build_models(const SegDesc* segs, const uint32_t* idx, const void* src,
+                                                          uint8_t* models, DevCfg cfg) {
+    extern __shared__ uint4 smem_u4[];
+    ModelSmem& S = *(ModelSmem*)smem_u4;
+    const SegDesc sd = segs[idx[blockIdx.x]];
+    build_model_cta<IN_F64>(sd, src, models, cfg, S, false);
+}
+
+template <bool IN_F64>
+__global__ void __launch_bounds__(kModelNT) k_first_sample(const SegDesc* seg, const void* src, uint8_t* models,
+                                                          DevCfg cfg) {
+    extern __shared__ uint4 smem_u4[];
+    ModelSmem& S = *(ModelSmem*)smem_u4;
+    const SegDesc sd = *seg;
+    build_model_cta<IN_F64>(sd, src, models, cfg, S, true);
+}
+
+template <bool IN_F64>
+__global__ void k_gather(const SegDesc* seg, const void* src, uint64_t seed, uint64_t j0, uint64_t s,
+                         uint64_t* out) {
+    const SegDesc sd = *seg;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < s; j += (uint64_t)gridDim.x * blockDim.x)
+        out[j] = load_key(src, sd.begin + sample_index(seed, j0 + j, sd.n), IN_F64);
+}
+
+
+// ============================================= multi-CTA RMI training
+// Workspace layout (device): [part: 4 * nch doubles][root: 8 doubles][first: B+1 u32]
+constexpr int kTrainChunk = 4096;
+constexpr int kTrainNT = 256;
+
+struct TrainWS {
+    double* part;   // [4][nch]: sx, sy, sxx, sxy per chunk
+    double* root;   // rs, ri, base, scale, mx, my
+    uint32_t* first;
+    uint32_t nch;
+};
+__host__ __device__ inline TrainWS train_ws(void* ws, uint64_t s, uint32_t B) {
+    TrainWS w;
+    w.nch = (uint32_t)((s + kTrainChunk - 1) / kTrainChunk);
+    w.part = (double*)ws;
+    w.root = w.part + 4 * (size_t)w.nch;
+    w.first = (uint32_t*)(w.root + 8);
+    (void)B;
+    return w;
+}
+size_t train_workspace_bytes(uint64_t s, uint32_t B) {
+    uint64_t nch = (s + kTrainChunk - 1) / kTrainChunk;
+    return 8 * (4 * nch + 8) + 4 * ((size_t)B + 2);
+}
+
+__device__ __forceinline__ void base_scale(const uint64_t* s, uint32_t n, double& base, double& scale) {
+    base = __ull2double_rn(s[0]);
+    const double kmax = __ull2double_rn(s[n - 1]);
+    scale = kmax > base ? __ddiv_rn(1.0, __dsub_rn(kmax, base)) : 0.0;  // models.cpp:47-49
+}
+
+// pass 1 (pass2 = false): per-chunk sum of xn and target i/n;
+// pass 2 (pass2 = true): per-chunk centred sums (models.cpp:26-31)
+template <bool PASS2>
+__global__ void __launch_bounds__(kTrainNT) k_train_sums(const uint64_t* s, uint32_t n, void* wsp, uint32_t B) {
+    __shared__ double red[kTrainNT / 32];
+    TrainWS w = train_ws(wsp, n, B);
+    double base, scale;
+    base_scale(s, n, base, scale);
+    const double nd = (double)n;
+    const uint32_t c0 = blockIdx.x * kTrainChunk;
+    const uint32_t per = kTrainChunk / kTrainNT;
+    const uint32_t lo = min(n, c0 + threadIdx.x * per), hi = min(n, lo + per);
+    double a = 0.0, b = 0.0;
+    if (!PASS2) {
+        for (uint32_t i = lo; i < hi; ++i) {
+            a = __dadd_rn(a, rmi_normalize(base, scale, s[i]));
+            b = __dadd_rn(b, __ddiv_rn((double)i, nd));
+        }
+    } else {
+        const double mx = w.root[4], my = w.root[5];
+        for (uint32_t i = lo; i < hi; ++i) {
+            double dx = __dsub_rn(rmi_normalize(base, scale, s[i]), mx);
+            a = __dadd_rn(a, __dmul_rn(dx, dx));
+            b = __dadd_rn(b, __dmul_rn(dx, __dsub_rn(__ddiv_rn((double)i, nd), my)));
+        }
+    }
+    a = block_sum_f64<kTrainNT>(a, red);
+    b = block_sum_f64<kTrainNT>(b, red);
+    if (threadIdx.x == 0) {
+        w.part[(PASS2 ? 2 : 0) * (size_t)w.nch + blockIdx.x] = a;
+        w.part[(PASS2 ? 3 : 1) * (size_t)w.nch + blockIdx.x] = b;
+    }
+}
+
+// fixed-order reduction of the chunk partials (one CTA)
+template <bool PASS2>
+__global__ void __launch_bounds__(kTrainNT) k_train_reduce(const uint64_t* s, uint32_t n, void* wsp, uint32_t B) {
+    __shared__ double red[kTrainNT / 32];
+    TrainWS w = train_ws(wsp, n, B);
+    const uint32_t per = (w.nch + kTrainNT - 1) / kTrainNT;
+    const uint32_t lo = min(w.nch, threadIdx.x * per), hi = min(w.nch, lo + per);
+    const double* pa = w.part + (PASS2 ? 2 : 0) * (size_t)w.nch;
+    const double* pb = w.part + (PASS2 ? 3 : 1) * (size_t)w.nch;
+    double a = 0.0, b = 0.0;
+    for (uint32_t i = lo; i < hi; ++i) {
+        a = __dadd_rn(a, pa[i]);
+        b = __dadd_rn(b, pb[i]);
+    }
+    a = block_sum_f64<kTrainNT>(a, red);
+    b = block_sum_f64<kTrainNT>(b, red);
+    if (threadIdx.x == 0) {
+        const double nd = (double)n;
+        if (!PASS2) {
+            w.root[4] = __ddiv_rn(a, nd);  // mx
+            w.root[5] = __ddiv_rn(b, nd);  // my
+        } else {
+            const double mx = w.root[4], my = w.root[5];
+            double rs, ri;
+            if (!(a > 0.0)) { rs = 0.0; ri = my; }
+            else {
+                double sl = __ddiv_rn(b, a);
+                if (sl < 0.0) { rs = 0.0; ri = my; }
+                else { rs = sl; ri = __dsub_rn(my, __dmul_rn(sl, mx)); }
+            }
+            double base, scale;
+            base_scale(s, n, base, scale);
+            w.root[0] = rs;
+            w.root[1] = ri;
+            w.root[2] = base;
+            w.root[3] = scale;
+        }
+    }
+}
+
+// slice boundaries + sequential fits of slices <= kSeqFitMax (bit-exact)
+__global__ void __launch_bounds__(kTrainNT) k_train_fits(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
+                                                        RmiEntry* E) {
+    TrainWS w = train_ws(wsp, n, B);
+    const uint32_t m = blockIdx.x * kTrainNT + threadIdx.x;
+    if (m > B) return;
+    const double rs = w.root[0], ri = w.root[1], base = w.root[2], scale = w.root[3];
+    auto xn = [&](uint32_t i) { return rmi_normalize(base, scale, s[i]); };
+    auto lower = [&](uint32_t mm) -> uint32_t {  // min{i : route(xn(i)) >= mm}
+        if (mm == 0) return 0;
+        if (mm >= B) return n;
+        uint32_t a = 0, b = n;
+        while (a < b) {
+            uint32_t mid = (a + b) >> 1;
+            if (rmi_route(rs, ri, B, xn(mid)) >= mm) b = mid; else a = mid + 1;
+        }
+        return a;
+    };
+    const uint32_t f = lower(m);
+    w.first[m] = f;
+    if (m == B) return;
+    const uint32_t l = lower(m + 1);
+    if (l - f <= (uint32_t)kSeqFitMax) {
+        Fit ft = fit_seq(xn, f, l, 0.0, (double)n);
+        E[m].slope = ft.slope;
+        E[m].intercept = ft.intercept;
+    }
+}
+
+// one CTA per slice larger than kSeqFitMax: deterministic block reduction
+constexpr int kBigFitNT = 512;
+__global__ void __launch_bounds__(kBigFitNT) k_train_bigfits(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
+                                                            RmiEntry* E) {
+    __shared__ double red[kBigFitNT / 32];
+    TrainWS w = train_ws(wsp, n, B);
+    const uint32_t m = blockIdx.x;
+    const uint32_t f = w.first[m], l = w.first[m + 1];
+    if (l - f <= (uint32_t)kSeqFitMax) return;
+    const double base = w.root[2], scale = w.root[3];
+    const double nd = (double)n;
+    const uint32_t cnt = l - f;
+    const uint32_t per = (cnt + kBigFitNT - 1) / kBigFitNT;
+    const uint32_t lo = f + min(cnt, threadIdx.x * per), hi = f + min(cnt, (threadIdx.x + 1) * per);
+    double sx = 0.0, sy = 0.0;
+    for (uint32_t i = lo; i < hi; ++i) {
+        sx = __dadd_rn(sx, rmi_normalize(base, scale, s[i]));
+        sy = __dadd_rn(sy, __ddiv_rn((double)i, nd));
+    }
+    sx = block_sum_f64<kBigFitNT>(sx, red);
+    sy = block_sum_f64<kBigFitNT>(sy, red);
+    const double mx = __ddiv_rn(sx, (double)cnt), my = __ddiv_rn(sy, (double)cnt);
+    double sxx = 0.0, sxy = 0.0;
+    for (uint32_t i = lo; i < hi; ++i) {
+        double dx = __dsub_rn(rmi_normalize(base, scale, s[i]), mx);
+        sxx = __dadd_rn(sxx, __dmul_rn(dx, dx));
+        sxy = __dadd_rn(sxy, __dmul_rn(dx, __dsub_rn(__ddiv_rn((double)i, nd), my)));
+    }
+    sxx = block_sum_f64<kBigFitNT>(sxx, red);
+    sxy = block_sum_f64<kBigFitNT>(sxy, red);
+    if (threadIdx.x == 0) {
+        double sl = 0.0, ic = my;
+        if (sxx > 0.0) {
+            double q = __ddiv_rn(sxy, sxx);
+            if (!(q < 0.0)) { sl = q; ic = __dsub_rn(my, __dmul_rn(q, mx)); }
+        }
+        E[m].slope = sl;
+        E[m].intercept = ic;
+    }
+}
+
+// enforce_monotonic (models.cpp:101-126) + header, one CTA
+constexpr int kEnforceNT = 1024;
+__global__ void __launch_bounds__(kEnforceNT) k_train_enforce(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
+                                                             uint8_t* model, uint32_t nbuckets) {
+    extern __shared__ uint4 smem_u4[];
+    double* lo = (double*)smem_u4;
+    double* hi = lo + B;
+    __shared__ double red[2 * (kEnforceNT / 32)];
+    TrainWS w = train_ws(wsp, n, B);
+    ModelHdr* h = (ModelHdr*)model;
+    RmiEntry* E = (RmiEntry*)(model + sizeof(ModelHdr));
+    const double base = w.root[2], scale = w.root[3];
+    for (uint32_t m = threadIdx.x; m < B; m += kEnforceNT) {
+        uint32_t f = w.first[m], l = w.first[m + 1];
+        if (l > f) {
+            double sl = E[m].slope, ic = E[m].intercept;
+            lo[m] = __dadd_rn(__dmul_rn(sl, rmi_normalize(base, scale, s[f])), ic);
+            hi[m] = __dadd_rn(__dmul_rn(sl, rmi_normalize(base, scale, s[l - 1])), ic);
+        } else {
+            lo[m] = -INFINITY;
+            hi[m] = INFINITY;
+        }
+    }
+    __syncthreads();
+    block_fold_scan<kEnforceNT>(lo, B, false, red, StepMax());
+    block_fold_scan<kEnforceNT>(hi, B, true, red, StepMin());
+    for (uint32_t m = threadIdx.x; m < B; m += kEnforceNT) {
+        double hh = hi[m];
+        if (m + 1 < B) hh = dmin_ref(hh, lo[m + 1]);
+        hh = dmax_ref(hh, lo[m]);
+        double ll = dclamp01(lo[m]);
+        hh = dclamp01(hh);
+        if (m == 0) ll = 0.0;
+        if (m == B - 1) hh = 1.0;
+        if (w.first[m + 1] == w.first[m]) {
+            E[m].slope = 0.0;
+            E[m].intercept = __dmul_rn(0.5, __dadd_rn(ll, hh));
+        }
+        E[m].lo = ll;
+        E[m].hi = hh;
+    }
+    if (threadIdx.x == 0) {
+        h->kind = kLearned;
+        h->nbuckets = nbuckets;
+        h->B = B;
+        h->root_slope = w.root[0];
+        h->root_icpt = w.root[1];
+        h->key_base = base;
+        h->key_scale = scale;
+        h->cdf_lo = 0.0;
+        h->inv_span = 1.0;
+    }
+}
+
+__global__ void __launch_bounds__(kModelNT) k_tree_build(const uint64_t* sorted, uint32_t s, uint32_t budget,
+                                                        int eq_mode, uint8_t* model) {
+    extern __shared__ uint4 smem_u4[];
+    ModelSmem& S = *(ModelSmem*)smem_u4;
+    for (uint32_t i = threadIdx.x; i < s; i += kModelNT) S.a[i] = sorted[i];
+    __syncthreads();
+    tree_build_block<kModelNT>(S.a, s, budget, eq_mode != 0, (ModelHdr*)model, model + sizeof(ModelHdr),
+                               S.u.tree.scratch, S.u.tree.wsum, S.u.tree.spl);
+}
+
+__global__ void __launch_bounds__(kModelNT) k_block_sort(uint64_t* keys, uint32_t n) {
+    extern __shared__ uint4 smem_u4[];
+    ModelSmem& S = *(ModelSmem*)smem_u4;
+    uint64_t k[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        uint32_t idx = threadIdx.x + i * kModelNT;
+        if (idx < n) k[i] = keys[idx];
+    }
+    ModelSort::sort_regs(k, S.a, n, S.u.sort);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += kModelNT) keys[i] = S.a[i];
+}
+
+// ------------------------------------------------------------- launchers
+
+void models_init(int optin) {
+    allow_smem(k_build_models<true>, optin);
+    allow_smem(k_build_models<false>, optin);
+    allow_smem(k_first_sample<true>, optin);
+    allow_smem(k_first_sample<false>, optin);
+    allow_smem(k_train_enforce, optin);
+    allow_smem(k_tree_build, optin);
+    allow_smem(k_block_sort, optin);
+}
+
+void launch_build_models(const SegDesc* segs, const uint32_t* idx, uint32_t count, const void* src, int in_f64,
+                         uint8_t* models, const DevCfg& cfg, cudaStream_t st) {
+    if (!count) return;
+    size_t sm = sizeof(ModelSmem);
+    if (in_f64) k_build_models<true><<<count, kModelNT, sm, st>>>(segs, idx, src, models, cfg);
+    else k_build_models<false><<<count, kModelNT, sm, st>>>(segs, idx, src, models, cfg);
+}
+
+void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_t* models, const DevCfg& cfg,
+                         cudaStream_t st) {
+    size_t sm = sizeof(ModelSmem);
+    if (in_f64) k_first_sample<true><<<1, kModelNT, sm, st>>>(seg, src, models, cfg);
+    else k_first_sample<false><<<1, kModelNT, sm, st>>>(seg, src, models, cfg);
+}
+
+void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0, uint64_t s,
+                   uint64_t* out, cudaStream_t st) {
+    int grid = (int)std::min<uint64_t>((s + 255) / 256, (uint64_t)num_sms() * 8);
+    if (grid < 1) grid = 1;
+    if (in_f64) k_gather<true><<<grid, 256, 0, st>>>(seg, src, seed, j0, s, out);
+    else k_gather<false><<<grid, 256, 0, st>>>(seg, src, seed, j0, s, out);
+}
+
+void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* model, uint32_t nbuckets, void* ws,
+                      cudaStream_t st) {
+    const uint32_t n = (uint32_t)s;
+    const uint32_t nch = (uint32_t)((s + kTrainChunk - 1) / kTrainChunk);
+    RmiEntry* E = (RmiEntry*)(model + sizeof(ModelHdr));
+    k_train_sums<false><<<nch, kTrainNT, 0, st>>>(sample, n, ws, B);
+    k_train_reduce<false><<<1, kTrainNT, 0, st>>>(sample, n, ws, B);
+    k_train_sums<true><<<nch, kTrainNT, 0, st>>>(sample, n, ws, B);
+    k_train_reduce<true><<<1, kTrainNT, 0, st>>>(sample, n, ws, B);
+    k_train_fits<<<(B + 1 + kTrainNT - 1) / kTrainNT, kTrainNT, 0, st>>>(sample, n, ws, B, E);
+    k_train_bigfits<<<B, kBigFitNT, 0, st>>>(sample, n, ws, B, E);
+    k_train_enforce<<<1, kEnforceNT, 16 * (size_t)B, st>>>(sample, n, ws, B, model, nbuckets);
+}
+
+void launch_tree_build(const uint64_t* sorted, uint64_t s, uint32_t budget, int eq_mode, uint8_t* model,
+                       cudaStream_t st) {
+    k_tree_build<<<1, kModelNT, sizeof(ModelSmem), st>>>(sorted, (uint32_t)s, budget, eq_mode, model);
+}
+
+void launch_block_sort(uint64_t* keys, uint64_t n, cudaStream_t st) {
+    k_block_sort<<<1, kModelNT, sizeof(ModelSmem), st>>>(keys, (uint32_t)n);
+}
+
+}  // namespace lsort_dev

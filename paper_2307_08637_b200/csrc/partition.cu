@@ -1,0 +1,497 @@
+// partition.cu -- one distribution level: classify + histogram, per-segment
+// scan, and the shared-memory staged scatter.
+//
+//   k_kind_plan      compacts the level's segments by partition-model kind
+//                    (learned / tree / radix) and builds per-kind tile prefixes,
+//                    so each kind runs a specialised kernel over a balanced
+//                    tile range (no per-key kind dispatch, no register spill).
+//   k_hist<K>        fused decode/encode + model inference + warp-aggregated
+//                    (__match_any_sync) shared-memory histogram; 16 keys per
+//                    thread read with 128-bit loads, persistent over tiles.
+//   k_scan_children  per-segment exclusive scan -> write cursors; emits base
+//                    case / equality fill / recursion work lists.
+//   k_scatter<K>     re-classify, rank within the tile, claim one range per
+//                    bucket per tile (global atomic), stage the tile grouped by
+//                    bucket in shared memory, write each bucket run coalesced.
+//
+// Learned models stay in global memory (the 32 B/submodel table is L1
+// resident); tree models are copied to shared memory (dependent descent).
+#include <algorithm>
+
+#include "kernels_common.cuh"
+
+namespace lsort_dev {
+
+constexpr int kPNT = 256;                 // threads per partition CTA
+constexpr int kPItems = 16;               // keys per thread per tile
+constexpr int kPPairs = kPItems / 2;      // 128-bit loads per thread per tile
+static_assert(kPNT * kPItems == kTileKeys, "tile geometry");
+
+__device__ __forceinline__ uint32_t kind_slot(uint32_t kind) {
+    return kind == kLearned ? 0u : (kind == kTree ? 1u : 2u);
+}
+
+// ------------------------------------------------------------ kind plan
+constexpr int kPlanNT = 1024;
+__global__ void __launch_bounds__(kPlanNT) k_kind_plan(LevelParams p) {
+    __shared__ uint32_t wsum[kPlanNT / 32 + 1];
+    __shared__ uint64_t wsum64[kPlanNT / 32 + 1];
+    __shared__ uint32_t fl[kPlanNT];
+    __shared__ uint64_t tl[kPlanNT];
+    __shared__ uint32_t carry_n;
+    __shared__ uint64_t carry_t;
+    for (uint32_t K = 0; K < 3; ++K) {
+        if (threadIdx.x == 0) { carry_n = 0; carry_t = 0; }
+        __syncthreads();
+        uint32_t* ks = p.kseg + (size_t)K * p.kstride;
+        uint64_t* tp = p.ktp + (size_t)K * (p.kstride + 1);
+        for (uint32_t base = 0; base < p.nsegs; base += kPlanNT) {
+            uint32_t s = base + threadIdx.x;
+            uint32_t f = 0;
+            uint64_t t = 0;
+            if (s < p.nsegs) {
+                const SegDesc& sd = p.segs[s];
+                uint32_t kind = ((const ModelHdr*)(p.models + sd.model_off))->kind;
+                f = kind_slot(kind) == K;
+                t = f ? (sd.n + kTileKeys - 1) / kTileKeys : 0;
+            }
+            fl[threadIdx.x] = f;
+            tl[threadIdx.x] = t;
+            __syncthreads();
+            uint32_t tot = block_exclusive_scan_u32<kPlanNT>(fl, kPlanNT, wsum);
+            uint64_t tott = block_exclusive_scan_u64<kPlanNT>(tl, kPlanNT, wsum64);
+            if (f) {
+                ks[carry_n + fl[threadIdx.x]] = s;
+                tp[carry_n + fl[threadIdx.x]] = carry_t + tl[threadIdx.x];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) { carry_n += tot; carry_t += tott; }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            tp[carry_n] = carry_t;
+            p.kplan[K].nsegs = carry_n;
+            p.kplan[K].ntiles = carry_t;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------ per-kind models
+// Registers-resident model state; tree payload lives in shared memory.
+struct KState {
+    // learned
+    double rs, ri, base, scale, cdf_lo, inv_span;
+    const RmiEntry* E;
+    uint32_t B, nb;
+    // tree (shared memory)
+    const uint64_t* tree;
+    const uint64_t* spl;
+    const uint32_t* eqo;
+    uint32_t levels, leaf, nsplit;
+    // radix / fill
+    uint64_t rmin;
+    uint32_t shift, fill;
+};
+
+template <uint32_t KIND>
+__device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t* tree_smem) {
+    const ModelHdr* h = (const ModelHdr*)g;
+    S.nb = h->nbuckets;
+    if constexpr (KIND == kLearned) {
+        S.rs = h->root_slope; S.ri = h->root_icpt; S.base = h->key_base; S.scale = h->key_scale;
+        S.cdf_lo = h->cdf_lo; S.inv_span = h->inv_span; S.B = h->B;
+        S.E = (const RmiEntry*)(g + sizeof(ModelHdr));
+    } else if constexpr (KIND == kTree) {
+        S.levels = h->levels; S.leaf = h->leaf_origin; S.nsplit = h->nsplit;
+        uint32_t words = (uint32_t)((tree_payload_bytes(S.leaf, S.nsplit) + 15) / 16);
+        const uint4* src = (const uint4*)(g + sizeof(ModelHdr));
+        __syncthreads();  // previous users of tree_smem are done
+        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) ((uint4*)tree_smem)[i] = src[i];
+        S.tree = (const uint64_t*)tree_smem;
+        S.spl = S.tree + S.leaf;
+        S.eqo = (const uint32_t*)(S.spl + S.nsplit);
+        __syncthreads();
+    } else {
+        S.rmin = h->radix_min; S.shift = h->shift; S.fill = h->kind == kFill;
+    }
+}
+
+// bucket id | (eq << 31): bit-exact learned math of models.hpp:34-43,162-171
+template <uint32_t KIND>
+__device__ __forceinline__ uint32_t kclassify(const KState& S, uint64_t x) {
+    if constexpr (KIND == kLearned) {
+        double xn = rmi_normalize(S.base, S.scale, x);
+        uint32_t i = rmi_route(S.rs, S.ri, S.B, xn);
+        const double2* ep = (const double2*)(S.E + i);
+        double2 si = __ldg(ep), lh = __ldg(ep + 1);
+        double v = __dadd_rn(__dmul_rn(si.x, xn), si.y);
+        if (v < lh.x) v = lh.x;
+        if (v > lh.y) v = lh.y;
+        if (v < 0.0) v = 0.0;
+        if (v > 1.0) v = 1.0;
+        double t = __dmul_rn(__dmul_rn(__dsub_rn(v, S.cdf_lo), S.inv_span), (double)S.nb);
+        if (!(t > 0.0)) return 0;
+        if (t >= (double)S.nb) return S.nb - 1;
+        return (uint32_t)t;
+    } else if constexpr (KIND == kTree) {
+        return tree_bucket(S.levels, S.leaf, S.nsplit, S.tree, S.spl, S.eqo, x);
+    } else {
+        if (S.fill) return 1u << 31;
+        uint64_t d = (x - S.rmin) >> S.shift;
+        return d >= S.nb ? S.nb - 1 : (uint32_t)d;
+    }
+}
+
+template <uint32_t KIND>
+struct KindTiles {
+    uint32_t K, nks;
+    uint64_t ntiles;
+    const uint32_t* ks;
+    const uint64_t* tp;
+    __device__ __forceinline__ void init(const LevelParams& p) {
+        K = kind_slot(KIND);
+        nks = p.kplan[K].nsegs;
+        ntiles = p.kplan[K].ntiles;
+        ks = p.kseg + (size_t)K * p.kstride;
+        tp = p.ktp + (size_t)K * (p.kstride + 1);
+    }
+};
+
+// ------------------------------------------------------- classify + hist
+template <bool IN_F64, uint32_t KIND>
+__global__ void __launch_bounds__(kPNT, 4) k_hist(LevelParams p) {
+    extern __shared__ uint4 smem_u4[];
+    uint32_t* hist = (uint32_t*)smem_u4;                    // kMaxNB
+    uint8_t* tree_smem = (uint8_t*)(hist + kMaxNB);         // tree payload
+    if (!IN_F64 && p.ctrl->nan_index != ~0ull) return;
+    KindTiles<KIND> KT;
+    KT.init(p);
+    if (KT.ntiles == 0) return;
+    const uint64_t per = (KT.ntiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * per;
+    const uint64_t t1 = min(t0 + per, KT.ntiles);
+    if (t0 >= t1) return;
+    for (uint32_t b = threadIdx.x; b < kMaxNB; b += kPNT) hist[b] = 0;
+    int64_t cur = -1;
+    KState S;
+    uint64_t boff = 0, sbeg = 0, send = 0, stile0 = 0;
+    for (uint64_t tile = t0; tile < t1; ++tile) {
+        uint32_t i = find_seg(KT.tp, KT.nks, tile);
+        if ((int64_t)i != cur) {
+            if (cur >= 0) {
+                __syncthreads();
+                for (uint32_t b = threadIdx.x; b < S.nb; b += kPNT) {
+                    uint32_t c = hist[b];
+                    if (c) { atomicAdd(&p.buckets[boff + b], (unsigned long long)c); hist[b] = 0; }
+                }
+            }
+            const SegDesc& sd = p.segs[KT.ks[i]];
+            boff = sd.bucket_off;
+            sbeg = sd.begin;
+            send = sd.begin + sd.n;
+            stile0 = KT.tp[i];
+            kstate_load<KIND>(S, p.models + sd.model_off, tree_smem);
+            __syncthreads();
+            cur = i;
+        }
+        const uint64_t lo = sbeg + (tile - stile0) * (uint64_t)kTileKeys;
+        const uint64_t hi = min(lo + kTileKeys, send);
+        TileGeom g;
+        g.init(p.src, lo, hi);
+        const ulonglong2* sp = (const ulonglong2*)((const uint64_t*)p.src + g.a0);
+        ulonglong2 v[kPPairs];
+#pragma unroll
+        for (int j = 0; j < kPPairs; ++j) {
+            uint32_t q = threadIdx.x + j * kPNT;
+            if (q < g.npairs) v[j] = __ldcs(sp + q);
+        }
+#pragma unroll
+        for (int j = 0; j < kPPairs; ++j) {
+            uint32_t q = threadIdx.x + j * kPNT;
+            bool ok = q < g.npairs;
+            uint64_t k0 = v[j].x, k1 = v[j].y;
+            if (IN_F64) {
+                if (ok) {
+                    if (isnan(__longlong_as_double((long long)k0)))
+                        atomicMin(&p.ctrl->nan_index, (unsigned long long)(g.a0 + 2 * q));
+                    if (isnan(__longlong_as_double((long long)k1)))
+                        atomicMin(&p.ctrl->nan_index, (unsigned long long)(g.a0 + 2 * q + 1));
+                }
+                k0 = encode(__longlong_as_double((long long)k0));
+                k1 = encode(__longlong_as_double((long long)k1));
+            }
+            uint32_t b0 = ok ? kclassify<KIND>(S, k0) : 0;
+            uint32_t b1 = ok ? kclassify<KIND>(S, k1) : 0;
+            hist_add_warp(hist, b0 & 0x7fffffffu, ok);
+            hist_add_warp(hist, b1 & 0x7fffffffu, ok);
+        }
+        if (threadIdx.x < g.nsingle) {
+            uint64_t ix = g.single[threadIdx.x];
+            uint64_t k = ((const uint64_t*)p.src)[ix];
+            if (IN_F64) {
+                double d = __longlong_as_double((long long)k);
+                if (isnan(d)) atomicMin(&p.ctrl->nan_index, (unsigned long long)ix);
+                k = encode(d);
+            }
+            atomicAdd(&hist[kclassify<KIND>(S, k) & 0x7fffffffu], 1u);
+        }
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < S.nb; b += kPNT) {
+        uint32_t c = hist[b];
+        if (c) atomicAdd(&p.buckets[boff + b], (unsigned long long)c);
+    }
+}
+
+// ---------------------------------------------------------- scan children
+constexpr int kScanNT = 512;
+__global__ void __launch_bounds__(kScanNT) k_scan_children(LevelParams p) {
+    __shared__ uint64_t wsum[kScanNT / 32 + 1];
+    __shared__ uint8_t iseq[kMaxNB];
+    __shared__ uint64_t eqval[kMaxNB];
+    extern __shared__ uint64_t cnt[];
+    if (p.ctrl->nan_index != ~0ull) return;
+    const SegDesc sd = p.segs[blockIdx.x];
+    const uint8_t* mg = p.models + sd.model_off;
+    const ModelHdr h = *(const ModelHdr*)mg;
+    const uint32_t nb = h.nbuckets;
+    for (uint32_t b = threadIdx.x; b < nb; b += kScanNT) {
+        cnt[b] = p.buckets[sd.bucket_off + b];
+        iseq[b] = 0;
+    }
+    __syncthreads();
+    if (h.kind == kTree) {
+        MView m = model_view(mg);
+        for (uint32_t i = threadIdx.x; i < h.nsplit; i += kScanNT) {
+            if (m.eqo[i + 1] - m.eqo[i] > 1) {
+                iseq[m.eqo[i] + 1] = 1;
+                eqval[m.eqo[i] + 1] = m.spl[i];
+            }
+        }
+    } else if (h.kind == kFill && threadIdx.x == 0) {
+        iseq[0] = 1;
+        eqval[0] = h.radix_min;
+    }
+    __syncthreads();
+    block_exclusive_scan_u64<kScanNT>(cnt, nb, wsum);
+    for (uint32_t b = threadIdx.x; b < nb; b += kScanNT) {
+        uint64_t start = cnt[b];
+        uint64_t end = (b + 1 < nb) ? cnt[b + 1] : sd.n;
+        uint64_t len = end - start;
+        uint64_t begin = sd.begin + start;
+        p.buckets[sd.bucket_off + b] = begin;  // write cursor
+        if (len == 0) continue;
+        if (iseq[b]) {
+            unsigned e = atomicAdd(&p.ctrl->n_fill, 1u);
+            if (e < p.list_cap) p.fill[e] = FillItem{begin, len, eqval[b], 0};
+            else atomicOr(&p.ctrl->err, 1u);
+            atomicAdd(&p.ctrl->keys_fill, (unsigned long long)len);
+        } else if (len <= p.base_cap[2]) {
+            int c = len <= p.base_cap[0] ? 0 : (len <= p.base_cap[1] ? 1 : 2);
+            unsigned e = atomicAdd(&p.ctrl->n_base[c], 1u);
+            if (e < p.list_cap) p.base[c][e] = BaseItem{begin, len};
+            else atomicOr(&p.ctrl->err, 2u);
+            atomicAdd(&p.ctrl->keys_base, (unsigned long long)len);
+        } else {
+            unsigned e = atomicAdd(&p.ctrl->n_rec, 1u);
+            uint32_t depth = sd.depth + 1;
+            uint32_t flags = (len == sd.n || depth > p.depth_cap) ? kSegForceRadix : 0u;
+            if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, flags, 0};
+            else atomicOr(&p.ctrl->err, 4u);
+            atomicAdd(&p.ctrl->keys_rec, (unsigned long long)len);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- scatter
+template <bool IN_F64, bool MAPPED, uint32_t KIND>
+__global__ void __launch_bounds__(kPNT, 3) k_scatter(LevelParams p, uint32_t nb_cap, const uint32_t* map,
+                                                 uint32_t nmapped) {
+    extern __shared__ uint4 smem_u4[];
+    uint8_t* q = (uint8_t*)smem_u4;
+    long long* delta = (long long*)q; q += 8 * (size_t)nb_cap;
+    uint64_t* skeys = (uint64_t*)q; q += 8 * (size_t)kTileKeys;
+    uint32_t* cnt = (uint32_t*)q; q += 4 * (size_t)(nb_cap + 1);
+    q = (uint8_t*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
+    uint32_t* wsum = (uint32_t*)q; q += 4 * (kPNT / 32 + 1);
+    q = (uint8_t*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
+    uint16_t* sbid = (uint16_t*)q; q += 2 * (size_t)kTileKeys;
+    uint8_t* tree_smem = (uint8_t*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
+    if (p.ctrl->nan_index != ~0ull) return;
+    KindTiles<KIND> KT;
+    KT.init(p);
+    if (KT.ntiles == 0) return;
+    const uint64_t per = (KT.ntiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * per;
+    const uint64_t t1 = min(t0 + per, KT.ntiles);
+    if (t0 >= t1) return;
+    for (uint32_t b = threadIdx.x; b <= nb_cap; b += kPNT) cnt[b] = 0;
+    int64_t cur = -1;
+    KState S;
+    uint64_t boff = 0, sbeg = 0, send = 0, stile0 = 0;
+    uint32_t nbo = 0;
+    for (uint64_t tile = t0; tile < t1; ++tile) {
+        uint32_t i = find_seg(KT.tp, KT.nks, tile);
+        if ((int64_t)i != cur) {
+            const SegDesc& sd = p.segs[KT.ks[i]];
+            boff = sd.bucket_off;
+            sbeg = sd.begin;
+            send = sd.begin + sd.n;
+            stile0 = KT.tp[i];
+            kstate_load<KIND>(S, p.models + sd.model_off, tree_smem);
+            nbo = MAPPED ? nmapped : S.nb;
+            __syncthreads();
+            cur = i;
+        }
+        const uint64_t lo = sbeg + (tile - stile0) * (uint64_t)kTileKeys;
+        const uint64_t hi = min(lo + kTileKeys, send);
+        TileGeom g;
+        g.init(p.src, lo, hi);
+        const ulonglong2* sp = (const ulonglong2*)((const uint64_t*)p.src + g.a0);
+        ulonglong2 v[kPPairs];
+        uint32_t code[kPItems];  // bucket << 16 | rank; ~0 = not moved
+#pragma unroll
+        for (int j = 0; j < kPPairs; ++j) {
+            uint32_t qq = threadIdx.x + j * kPNT;
+            if (qq < g.npairs) v[j] = __ldcs(sp + qq);
+        }
+#pragma unroll
+        for (int j = 0; j < kPPairs; ++j) {
+            uint32_t qq = threadIdx.x + j * kPNT;
+            bool ok = qq < g.npairs;
+            if (IN_F64) {
+                v[j].x = encode(__longlong_as_double((long long)v[j].x));
+                v[j].y = encode(__longlong_as_double((long long)v[j].y));
+            }
+            uint32_t c0 = ok ? kclassify<KIND>(S, v[j].x) : (1u << 31);
+            uint32_t c1 = ok ? kclassify<KIND>(S, v[j].y) : (1u << 31);
+            bool ok0 = !(c0 >> 31), ok1 = !(c1 >> 31);
+            uint32_t b0 = c0 & 0x7fffffffu, b1 = c1 & 0x7fffffffu;
+            if (MAPPED) { if (ok0) b0 = map[b0]; if (ok1) b1 = map[b1]; }
+            uint32_t r0 = hist_rank_warp(cnt, b0, ok0);
+            uint32_t r1 = hist_rank_warp(cnt, b1, ok1);
+            code[2 * j] = ok0 ? (b0 << 16 | r0) : 0xffffffffu;
+            code[2 * j + 1] = ok1 ? (b1 << 16 | r1) : 0xffffffffu;
+        }
+        uint64_t skey = 0;
+        uint32_t scode = 0xffffffffu;
+        if (threadIdx.x < g.nsingle) {
+            uint64_t k = load_key(p.src, g.single[threadIdx.x], IN_F64);
+            uint32_t c = kclassify<KIND>(S, k);
+            if (!(c >> 31)) {
+                uint32_t b = c & 0x7fffffffu;
+                if (MAPPED) b = map[b];
+                scode = b << 16 | atomicAdd(&cnt[b], 1u);
+                skey = k;
+            }
+        }
+        __syncthreads();
+        const uint32_t total = block_exclusive_scan_u32<kPNT>(cnt, nbo, wsum);
+        if (threadIdx.x == 0) cnt[nbo] = total;
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < nbo; b += kPNT) {
+            uint32_t c = cnt[b + 1] - cnt[b];
+            if (c) delta[b] = (long long)atomicAdd(&p.buckets[boff + b], (unsigned long long)c) - (long long)cnt[b];
+        }
+#pragma unroll
+        for (int j = 0; j < kPItems; ++j) {
+            uint32_t c = code[j];
+            if (c != 0xffffffffu) {
+                uint32_t pos = cnt[c >> 16] + (c & 0xffffu);
+                skeys[pos] = (j & 1) ? v[j >> 1].y : v[j >> 1].x;
+                sbid[pos] = (uint16_t)(c >> 16);
+            }
+        }
+        if (scode != 0xffffffffu) {
+            uint32_t pos = cnt[scode >> 16] + (scode & 0xffffu);
+            skeys[pos] = skey;
+            sbid[pos] = (uint16_t)(scode >> 16);
+        }
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < total; j += kPNT) {
+            uint32_t b = sbid[j];
+            p.dst[(long long)j + delta[b]] = skeys[j];
+        }
+        for (uint32_t b = threadIdx.x; b <= nbo; b += kPNT) cnt[b] = 0;
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------- launchers
+static size_t scatter_smem(uint32_t nb_cap, uint32_t tree_cap) {
+    size_t s = 8 * (size_t)nb_cap + 8 * (size_t)kTileKeys + 4 * (size_t)(nb_cap + 1) + 16 + 4 * (kPNT / 32 + 1) +
+               16 + 2 * (size_t)kTileKeys + 16 + tree_cap;
+    return s;
+}
+static const uint32_t kTreeCap = (uint32_t)((tree_payload_bytes(LSORT_MAX_TREE_DEV, LSORT_MAX_TREE_DEV - 1) + 15) & ~15ull);
+
+void partition_init(int optin) {
+    allow_smem(k_hist<true, kLearned>, optin);
+    allow_smem(k_hist<false, kLearned>, optin);
+    allow_smem(k_hist<true, kTree>, optin);
+    allow_smem(k_hist<false, kTree>, optin);
+    allow_smem(k_hist<true, kRadix>, optin);
+    allow_smem(k_hist<false, kRadix>, optin);
+    allow_smem(k_scatter<true, false, kLearned>, optin);
+    allow_smem(k_scatter<false, false, kLearned>, optin);
+    allow_smem(k_scatter<true, false, kTree>, optin);
+    allow_smem(k_scatter<false, false, kTree>, optin);
+    allow_smem(k_scatter<true, false, kRadix>, optin);
+    allow_smem(k_scatter<false, false, kRadix>, optin);
+    allow_smem(k_scatter<true, true, kLearned>, optin);
+    allow_smem(k_scatter<false, true, kLearned>, optin);
+    allow_smem(k_scan_children, optin);
+}
+
+void launch_kind_plan(const LevelParams& p, cudaStream_t st) {
+    k_kind_plan<<<1, kPlanNT, 0, st>>>(p);
+}
+
+void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, int grid, cudaStream_t st) {
+    size_t sm_l = 4 * (size_t)kMaxNB, sm_t = sm_l + kTreeCap;
+    if (kinds & 1) {
+        if (in_f64) k_hist<true, kLearned><<<grid, kPNT, sm_l, st>>>(p);
+        else k_hist<false, kLearned><<<grid, kPNT, sm_l, st>>>(p);
+    }
+    if (kinds & 2) {
+        if (in_f64) k_hist<true, kTree><<<grid, kPNT, sm_t, st>>>(p);
+        else k_hist<false, kTree><<<grid, kPNT, sm_t, st>>>(p);
+    }
+    if (kinds & 4) {
+        if (in_f64) k_hist<true, kRadix><<<grid, kPNT, sm_l, st>>>(p);
+        else k_hist<false, kRadix><<<grid, kPNT, sm_l, st>>>(p);
+    }
+}
+
+void launch_scan_children(const LevelParams& p, cudaStream_t st) {
+    if (!p.nsegs) return;
+    k_scan_children<<<p.nsegs, kScanNT, 8 * kMaxNB, st>>>(p);
+}
+
+void launch_scatter(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t nb_cap, int grid, cudaStream_t st) {
+    if (kinds & 1) {
+        size_t sm = scatter_smem(nb_cap, 0);
+        if (in_f64) k_scatter<true, false, kLearned><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
+        else k_scatter<false, false, kLearned><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
+    }
+    if (kinds & 2) {
+        size_t sm = scatter_smem(nb_cap, kTreeCap);
+        if (in_f64) k_scatter<true, false, kTree><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
+        else k_scatter<false, false, kTree><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
+    }
+    if (kinds & 4) {
+        size_t sm = scatter_smem(nb_cap, 0);
+        if (in_f64) k_scatter<true, false, kRadix><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
+        else k_scatter<false, false, kRadix><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
+    }
+}
+
+void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,
+                           cudaStream_t st) {
+    size_t sm = scatter_smem(nmapped, 0);
+    if (in_f64) k_scatter<true, true, kLearned><<<grid, kPNT, sm, st>>>(p, nmapped, map, nmapped);
+    else k_scatter<false, true, kLearned><<<grid, kPNT, sm, st>>>(p, nmapped, map, nmapped);
+}
+
+}  // namespace lsort_dev

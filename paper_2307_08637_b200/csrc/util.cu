@@ -1,0 +1,93 @@
+// util.cu -- unit-test / utility kernels (model classification with ids,
+// verify_sorted + multiset_hash, decode) and one-time kernel setup.
+#include <algorithm>
+
+#include "kernels_common.cuh"
+
+namespace lsort_dev {
+
+template <bool IN_F64>
+__global__ void __launch_bounds__(256) k_classify_ids(const uint8_t* model, const void* keys, uint64_t n, uint32_t* ids,
+                                                     unsigned long long* hist) {
+    extern __shared__ uint4 smem_u4[];
+    uint8_t* msm = (uint8_t*)smem_u4;
+    load_model_smem(model, msm);
+    Classifier C;
+    C.init(msm);
+    for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
+        uint64_t k = load_key(keys, i, IN_F64);
+        uint32_t b = C.classify_any(k) & 0x7fffffffu;
+        if (ids) ids[i] = b;
+        if (hist) atomicAdd(&hist[b], 1ull);
+    }
+}
+
+// verify_sorted + multiset_hash (verify.hpp:17-29)
+template <bool F64>
+__global__ void __launch_bounds__(256) k_verify(const void* keys, uint64_t n, Ctrl* ctrl) {
+    __shared__ uint64_t red[8];
+    uint64_t first = ~0ull, h = 0;
+    for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
+        uint64_t k = load_key(keys, i, F64);
+        h += splitmix64(k);
+        if (i > 0 && load_key(keys, i - 1, F64) > k && i < first) first = i;
+    }
+    first = block_reduce_min<256>(first, red);
+    h = block_reduce_sum_u64<256>(h, red);
+    if (threadIdx.x == 0) {
+        if (first != ~0ull) atomicMin(&ctrl->verify_first, (unsigned long long)first);
+        atomicAdd(&ctrl->verify_hash, (unsigned long long)h);
+    }
+}
+
+__global__ void k_decode(uint64_t* keys, uint64_t n) {
+    for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256)
+        ((double*)keys)[i] = decode(keys[i]);
+}
+
+static int g_num_sms = 148;
+int num_sms() { return g_num_sms; }
+
+void partition_init(int optin);
+void models_init(int optin);
+void basecase_init(int optin);
+
+void kernels_init() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    int optin = 227 * 1024;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    partition_init(optin);
+    models_init(optin);
+    basecase_init(optin);
+    allow_smem(k_classify_ids<true>, optin);
+    allow_smem(k_classify_ids<false>, optin);
+}
+
+void launch_classify_ids(const uint8_t* model, const void* keys, uint64_t n, int in_f64, uint32_t* ids,
+                         unsigned long long* hist, int payload, cudaStream_t st) {
+    int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)g_num_sms * 8);
+    if (grid < 1) grid = 1;
+    size_t sm = sizeof(ModelHdr) + (size_t)payload + 16;
+    if (in_f64) k_classify_ids<true><<<grid, 256, sm, st>>>(model, keys, n, ids, hist);
+    else k_classify_ids<false><<<grid, 256, sm, st>>>(model, keys, n, ids, hist);
+}
+
+void launch_verify(const void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st) {
+    int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)g_num_sms * 8);
+    if (grid < 1) grid = 1;
+    if (f64) k_verify<true><<<grid, 256, 0, st>>>(keys, n, ctrl);
+    else k_verify<false><<<grid, 256, 0, st>>>(keys, n, ctrl);
+}
+
+void launch_decode(uint64_t* keys, uint64_t n, cudaStream_t st) {
+    int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)g_num_sms * 8);
+    if (grid < 1) grid = 1;
+    k_decode<<<grid, 256, 0, st>>>(keys, n);
+}
+
+}  // namespace lsort_dev

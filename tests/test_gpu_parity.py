@@ -140,8 +140,14 @@ def compare_rmi(Pg, Pr, B, s):
     route = np.where(~(t > 0), 0, np.minimum(np.floor(np.where(t > 0, t, 0)), B - 1)).astype(np.int64)
     sizes = np.bincount(route, minlength=B)
     seq = sizes <= 512
-    assert np.array_equal(bits(E[seq]), bits(Eq[seq])), "sequential slices must be bit-exact"
-    assert np.allclose(E[~seq], Eq[~seq], rtol=RMI_RTOL, atol=RMI_ATOL), "parallel slices"
+    # slope/intercept of sequentially fitted slices are bit-exact; clamp bounds
+    # propagate neighbours' values (running max/min, models.cpp:110-113), so
+    # they inherit the tolerance of any warp-fitted neighbour
+    bad = np.nonzero(seq & np.any(bits(E[:, :2]) != bits(Eq[:, :2]), axis=1))[0]
+    assert bad.size == 0, ("sequential slice fits differ", bad[:8], sizes[bad[:8]], E[bad[:4]], Eq[bad[:4]])
+    if seq.all():
+        assert np.array_equal(bits(E), bits(Eq)), "all-sequential model must be bit-exact"
+    assert np.allclose(E, Eq, rtol=RMI_RTOL, atol=RMI_ATOL), "parallel slices / clamp bounds"
 
 
 def _fanout(n, count, target):
