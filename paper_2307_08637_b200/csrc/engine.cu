@@ -349,7 +349,7 @@ struct Engine {
             for (uint32_t b : bigs) big_model(p.segs + b, segs[b], hs[b], src, src_f64);
             // ---- partition
             const int nsm = num_sms();
-            int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 4);
+            int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 3);
             int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 3);
             const int nk = __builtin_popcount(kinds);
             mark(1);

@@ -160,7 +160,7 @@ struct KindTiles {
 
 // ------------------------------------------------------- classify + hist
 template <bool IN_F64, uint32_t KIND>
-__global__ void __launch_bounds__(kPNT, 4) k_hist(LevelParams p) {
+__global__ void __launch_bounds__(kPNT, 3) k_hist(LevelParams p) {
     extern __shared__ uint4 smem_u4[];
     uint32_t* hist = (uint32_t*)smem_u4;                    // kMaxNB
     uint8_t* tree_smem = (uint8_t*)(hist + kMaxNB);         // tree payload
