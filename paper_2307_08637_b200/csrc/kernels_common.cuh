@@ -87,17 +87,9 @@ struct Classifier {
     __device__ __forceinline__ uint32_t classify(uint64_t x) const {
         if constexpr (KIND == kLearned) {
             double xn = rmi_normalize(base, scale, x);
-            uint32_t i = rmi_route(rs, ri, B, xn);
-            const RmiEntry s = m.e[i];
-            double v = __dadd_rn(__dmul_rn(s.slope, xn), s.intercept);
-            if (v < s.lo) v = s.lo;
-            if (v > s.hi) v = s.hi;
-            if (v < 0.0) v = 0.0;
-            if (v > 1.0) v = 1.0;
-            double t = __dmul_rn(__dmul_rn(__dsub_rn(v, cdf_lo), inv_span), (double)nb);
-            if (!(t > 0.0)) return 0;
-            if (t >= (double)nb) return nb - 1;
-            return (uint32_t)t;
+            const RmiEntry s = m.e[rmi_route(rs, ri, B, xn)];
+            return cdf_bucket(clamp_pred(__dadd_rn(__dmul_rn(s.slope, xn), s.intercept), s.lo, s.hi), cdf_lo,
+                              inv_span, nb);
         } else if constexpr (KIND == kTree) {
             return tree_bucket(levels, leaf_origin, nsplit, m.tree, m.spl, m.eqo, x);
         } else if constexpr (KIND == kRadix) {
@@ -117,32 +109,29 @@ struct Classifier {
     }
 };
 
-// Warp-aggregated shared-memory histogram add (all lanes must call): lanes
-// holding the same bucket id are grouped with __match_any_sync and the
-// group's lowest lane adds the group size. (__reduce_add_sync over the
-// per-group mask compiles to a per-group REDUX loop -- 32 iterations for
-// distinct ids, measured 31x the instruction count -- so __popc is used.)
-__device__ __forceinline__ void hist_add_warp(uint32_t* hist, uint32_t b, bool valid) {
-    unsigned vmask = __ballot_sync(FULL_MASK, valid);
-    if (valid) {
-        unsigned peers = __match_any_sync(vmask, b);
-        if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&hist[b], (unsigned)__popc(peers));
-    }
+// Shared-memory histogram add. Measured on B200 (tools/micro/hist_bench.cu,
+// profiles/): a plain shared atomicAdd runs at full HBM rate for spread and
+// for all-equal bins (the hardware aggregates same-address lanes), while
+// __match_any_sync warp aggregation is ADU-bound and 6.5x slower for spread
+// bins -- so aggregation is left to the hardware here.
+__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t b, bool valid) {
+    if (valid) atomicAdd(&hist[b], 1u);
 }
-// Warp-aggregated add returning this lane's rank within its bucket (all lanes must call).
+// Rank of this lane's key within its bucket (all lanes must call). Returning
+// atomics serialise on equal addresses (3x slower when a warp shares one
+// bucket), so a warp-uniform bucket takes one atomic for the whole warp.
 __device__ __forceinline__ uint32_t hist_rank_warp(uint32_t* hist, uint32_t b, bool valid) {
-    unsigned vmask = __ballot_sync(FULL_MASK, valid);
-    unsigned peers = 0;
-    int leader = 0;
-    uint32_t old = 0;
+    const unsigned vmask = __ballot_sync(FULL_MASK, valid);
     const int lane = threadIdx.x & 31;
-    if (valid) {
-        peers = __match_any_sync(vmask, b);
-        leader = __ffs(peers) - 1;
-        if (lane == leader) old = atomicAdd(&hist[b], (uint32_t)__popc(peers));
+    const int first = __ffs(vmask) - 1;
+    const uint32_t b0 = __shfl_sync(FULL_MASK, b, first < 0 ? 0 : first);
+    if (__all_sync(FULL_MASK, !valid || b == b0)) {
+        uint32_t old = 0;
+        if (lane == first) old = atomicAdd(&hist[b0], (uint32_t)__popc(vmask));
+        old = __shfl_sync(FULL_MASK, old, first < 0 ? 0 : first);
+        return old + __popc(vmask & ((1u << lane) - 1u));
     }
-    old = __shfl_sync(FULL_MASK, old, leader);
-    return valid ? old + __popc(peers & ((1u << lane) - 1u)) : 0u;
+    return valid ? atomicAdd(&hist[b], 1u) : 0u;
 }
 
 // last s in [0,n) with prefix[s] <= tile

@@ -78,13 +78,28 @@ __host__ __device__ __forceinline__ size_t tree_payload_bytes(uint32_t leaf_orig
 }
 
 // ---------------------------------------------------------------- classifiers
-// Rmi::route (models.hpp:60-65). `t >= B` replaces the post-cast clamp; equal
-// wherever the reference's size_t cast is defined (t < 2^64).
+// Rmi::route (models.hpp:60-65): !(t > 0) -> 0, truncate, clamp to B-1.
+// Branch-free: fmax maps t <= 0 and NaN to 0; the saturating truncation and
+// min() give B-1 for t >= B -- identical wherever the reference's size_t
+// cast is defined (t < 2^64).
 __device__ __forceinline__ uint32_t rmi_route(double root_slope, double root_icpt, uint32_t B, double xn) {
     double t = __dmul_rn(__dadd_rn(__dmul_rn(root_slope, xn), root_icpt), (double)B);
-    if (!(t > 0.0)) return 0;
-    if (t >= (double)B) return B - 1;
-    return (uint32_t)t;
+    return min(__double2uint_rz(fmax(t, 0.0)), B - 1);
+}
+
+// Clamp of a submodel prediction (models.hpp:38-41): [lo,hi] then [0,1].
+// fmax/fmin equal the reference's compare-and-assign for every non-NaN v
+// (up to the sign of a zero, which no later step distinguishes: t = v*B is
+// only tested with t > 0 and truncated). v is never NaN: xn and the trained
+// parameters are finite.
+__device__ __forceinline__ double clamp_pred(double v, double lo, double hi) {
+    return fmin(fmax(fmin(fmax(v, lo), hi), 0.0), 1.0);
+}
+// bucket of a CDF value: t = ((f - cdf_lo) * inv_span) * nb, !(t > 0) -> 0,
+// truncate, clamp to nb-1 (models.hpp:166-170)
+__device__ __forceinline__ uint32_t cdf_bucket(double f, double cdf_lo, double inv_span, uint32_t nb) {
+    double t = __dmul_rn(__dmul_rn(__dsub_rn(f, cdf_lo), inv_span), (double)nb);
+    return min(__double2uint_rz(fmax(t, 0.0)), nb - 1);
 }
 
 // Rmi::normalize (models.hpp:56-58)
@@ -97,22 +112,12 @@ __device__ __forceinline__ double rmi_predict(const ModelHdr& h, const RmiEntry*
     double xn = rmi_normalize(h.key_base, h.key_scale, x);
     uint32_t i = rmi_route(h.root_slope, h.root_icpt, h.B, xn);
     RmiEntry s = e[i];
-    double v = __dadd_rn(__dmul_rn(s.slope, xn), s.intercept);
-    if (v < s.lo) v = s.lo;
-    if (v > s.hi) v = s.hi;
-    if (v < 0.0) v = 0.0;
-    if (v > 1.0) v = 1.0;
-    return v;
+    return clamp_pred(__dadd_rn(__dmul_rn(s.slope, xn), s.intercept), s.lo, s.hi);
 }
 
 // PartitionModel::bucket_index, learned branch (models.hpp:162-171)
 __device__ __forceinline__ uint32_t learned_bucket(const ModelHdr& h, const RmiEntry* e, uint64_t x) {
-    double f = rmi_predict(h, e, x);
-    double u = __dmul_rn(__dsub_rn(f, h.cdf_lo), h.inv_span);
-    double t = __dmul_rn(u, (double)h.nbuckets);
-    if (!(t > 0.0)) return 0;
-    if (t >= (double)h.nbuckets) return h.nbuckets - 1;
-    return (uint32_t)t;
+    return cdf_bucket(rmi_predict(h, e, x), h.cdf_lo, h.inv_span, h.nbuckets);
 }
 
 // SplitterTree::classify (models.hpp:92-101). Returns bucket | (eq << 31).

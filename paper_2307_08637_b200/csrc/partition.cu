@@ -5,9 +5,9 @@
 //                    (learned / tree / radix) and builds per-kind tile prefixes,
 //                    so each kind runs a specialised kernel over a balanced
 //                    tile range (no per-key kind dispatch, no register spill).
-//   k_hist<K>        fused decode/encode + model inference + warp-aggregated
-//                    (__match_any_sync) shared-memory histogram; 16 keys per
-//                    thread read with 128-bit loads, persistent over tiles.
+//   k_hist<K>        fused decode/encode + model inference + shared-memory
+//                    histogram (hardware-aggregated atomics, see hist_add);
+//                    16 keys per thread read with 128-bit loads, persistent.
 //   k_scan_children  per-segment exclusive scan -> write cursors; emits base
 //                    case / equality fill / recursion work lists.
 //   k_scatter<K>     re-classify, rank within the tile, claim one range per
@@ -121,19 +121,11 @@ __device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t
 template <uint32_t KIND>
 __device__ __forceinline__ uint32_t kclassify(const KState& S, uint64_t x) {
     if constexpr (KIND == kLearned) {
-        double xn = rmi_normalize(S.base, S.scale, x);
-        uint32_t i = rmi_route(S.rs, S.ri, S.B, xn);
-        const double2* ep = (const double2*)(S.E + i);
-        double2 si = __ldg(ep), lh = __ldg(ep + 1);
-        double v = __dadd_rn(__dmul_rn(si.x, xn), si.y);
-        if (v < lh.x) v = lh.x;
-        if (v > lh.y) v = lh.y;
-        if (v < 0.0) v = 0.0;
-        if (v > 1.0) v = 1.0;
-        double t = __dmul_rn(__dmul_rn(__dsub_rn(v, S.cdf_lo), S.inv_span), (double)S.nb);
-        if (!(t > 0.0)) return 0;
-        if (t >= (double)S.nb) return S.nb - 1;
-        return (uint32_t)t;
+        const double xn = rmi_normalize(S.base, S.scale, x);
+        const double2* ep = (const double2*)(S.E + rmi_route(S.rs, S.ri, S.B, xn));
+        const double2 si = __ldg(ep), lh = __ldg(ep + 1);
+        const double v = clamp_pred(__dadd_rn(__dmul_rn(si.x, xn), si.y), lh.x, lh.y);
+        return cdf_bucket(v, S.cdf_lo, S.inv_span, S.nb);
     } else if constexpr (KIND == kTree) {
         return tree_bucket(S.levels, S.leaf, S.nsplit, S.tree, S.spl, S.eqo, x);
     } else {
@@ -223,8 +215,8 @@ __global__ void __launch_bounds__(kPNT, 3) k_hist(LevelParams p) {
             }
             uint32_t b0 = ok ? kclassify<KIND>(S, k0) : 0;
             uint32_t b1 = ok ? kclassify<KIND>(S, k1) : 0;
-            hist_add_warp(hist, b0 & 0x7fffffffu, ok);
-            hist_add_warp(hist, b1 & 0x7fffffffu, ok);
+            hist_add(hist, b0 & 0x7fffffffu, ok);
+            hist_add(hist, b1 & 0x7fffffffu, ok);
         }
         if (threadIdx.x < g.nsingle) {
             uint64_t ix = g.single[threadIdx.x];
