@@ -283,7 +283,7 @@ struct Engine {
                     nb = 1u << kRadixBits;
                 } else {
                     uint32_t tp = (uint32_t)((tree_payload_bytes(d.tree_k, d.tree_k - 1) + 15) & ~15ull);
-                    payload = std::max<uint32_t>(32u * d.rmi_b, tp);
+                    payload = std::max<uint32_t>(kLearnedEntryBytes * d.rmi_b, tp);
                     nb = std::max<uint32_t>(d.rmi_b, 2 * d.tree_k - 1);
                 }
                 d.nb_max = nb;
@@ -581,7 +581,7 @@ int lsort_cuda_sort(lsort_ctx* C, void* keys, uint64_t n, int key_kind, int mem_
 static void upload_learned(lsort_ctx* C, const lsort_rmi_header* h, const lsort_rmi_entry* e, uint32_t bucket_count,
                            double cdf_lo, double cdf_hi) {
     uint32_t B = h->submodels;
-    size_t bytes = sizeof(ModelHdr) + 32 * (size_t)B;
+    size_t bytes = sizeof(ModelHdr) + kLearnedEntryBytes * (size_t)B;
     if (!C->models.ensure(bytes) || !C->hmodel.ensure(bytes)) throw LsortError{LSORT_ENOMEM, "model"};
     ModelHdr* m = C->hmodel.as<ModelHdr>();
     std::memset(m, 0, sizeof(ModelHdr));
@@ -596,6 +596,24 @@ static void upload_learned(lsort_ctx* C, const lsort_rmi_header* h, const lsort_
     m->cdf_lo = cdf_lo;
     m->inv_span = span > 0.0 ? 1.0 / span : 0.0;
     std::memcpy((uint8_t*)m + sizeof(ModelHdr), e, 32 * (size_t)B);
+    // compiled table (lsort_device.cuh RmiBucketEntry), same arithmetic as compile_learned
+    auto gb = [&](double v) -> uint32_t {
+        if (v < 0.0) v = 0.0;
+        if (v > 1.0) v = 1.0;
+        double t = ((v - m->cdf_lo) * m->inv_span) * (double)bucket_count;
+        if (!(t > 0.0)) return 0;
+        if (t >= (double)bucket_count) return bucket_count - 1;
+        return (uint32_t)t;
+    };
+    RmiBucketEntry* cb = (RmiBucketEntry*)((uint8_t*)m + sizeof(ModelHdr) + 32 * (size_t)B);
+    for (uint32_t i = 0; i < B; ++i) {
+        cb[i].slope = e[i].slope;
+        cb[i].intercept = e[i].intercept;
+        cb[i].glo = gb(e[i].lo);
+        cb[i].ghi = gb(e[i].hi);
+        cb[i].pad = 0;
+    }
+    m->flags = (m->cdf_lo == 0.0 && m->inv_span == 1.0) ? kModelIdentityCdf : 0u;
     CU(cudaMemcpyAsync(C->models.p, m, bytes, cudaMemcpyHostToDevice, C->stream));
 }
 
@@ -660,7 +678,8 @@ int lsort_cuda_rmi_train(lsort_ctx* C, const uint64_t* d_sample, uint64_t s, uin
     if (B > LSORT_MAX_RMI || s > 0xffffffffull) return fail(C, {LSORT_EINVAL, "Rmi::train: size limits"});
     try {
         CU(cudaSetDevice(C->device));
-        if (!C->models.ensure(sizeof(ModelHdr) + 32 * (size_t)B) || !C->train_ws.ensure(train_workspace_bytes(s, B)))
+        if (!C->models.ensure(sizeof(ModelHdr) + kLearnedEntryBytes * (size_t)B) ||
+            !C->train_ws.ensure(train_workspace_bytes(s, B)))
             throw LsortError{LSORT_ENOMEM, "model"};
         CU(cudaMemsetAsync(C->models.p, 0, sizeof(ModelHdr), C->stream));
         launch_train_rmi(d_sample, s, B, C->models.as<uint8_t>(), B, C->train_ws.p, C->stream);
@@ -682,7 +701,7 @@ int lsort_cuda_classify_rmi(lsort_ctx* C, const lsort_rmi_header* h, const lsort
         upload_learned(C, h, e, bucket_count, cdf_lo, cdf_hi);
         if (d_hist) CU(cudaMemsetAsync(d_hist, 0, 8 * (size_t)bucket_count, C->stream));
         if (n) launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, d_ids,
-                                   (unsigned long long*)d_hist, 32 * (int)h->submodels, C->stream);
+                                   (unsigned long long*)d_hist, (int)kLearnedEntryBytes * (int)h->submodels, C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
     } catch (const LsortError& er) {
@@ -744,7 +763,7 @@ int lsort_cuda_build_model(lsort_ctx* C, const void* d_keys, uint64_t n, int key
         d.rmi_b = E.rmi_b(n);
         d.tree_k = E.tree_k(n);
         d.model_off = 0;
-        size_t bytes = sizeof(ModelHdr) + std::max<size_t>(32 * (size_t)d.rmi_b, 24 * LSORT_MAX_TREE + 16);
+        size_t bytes = sizeof(ModelHdr) + std::max<size_t>(kLearnedEntryBytes * (size_t)d.rmi_b, 24 * LSORT_MAX_TREE + 16);
         if (!C->models.ensure(bytes) || !C->segs.ensure(sizeof(SegDesc)) || !C->idx.ensure(4))
             throw LsortError{LSORT_ENOMEM, "model"};
         CU(cudaMemsetAsync(C->models.p, 0, bytes, C->stream));
@@ -852,7 +871,7 @@ int lsort_cuda_dist_train(lsort_ctx* C, uint64_t* d_sample, uint64_t s, uint32_t
         lsort_cfg_default(&cfg);
         Engine E(C, cfg);
         E.nested_sort(d_sample, s);
-        if (!C->models.ensure(sizeof(ModelHdr) + 32 * (size_t)buckets) ||
+        if (!C->models.ensure(sizeof(ModelHdr) + kLearnedEntryBytes * (size_t)buckets) ||
             !C->train_ws.ensure(train_workspace_bytes(s, buckets)))
             throw LsortError{LSORT_ENOMEM, "model"};
         launch_train_rmi(d_sample, s, buckets, C->models.as<uint8_t>(), buckets, C->train_ws.p, C->stream);
@@ -889,7 +908,7 @@ int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int 
         unsigned long long* dcur = dhist + B;
         CU(cudaMemcpyAsync(dmap, map.data(), B * 4, cudaMemcpyHostToDevice, C->stream));
         CU(cudaMemsetAsync(dhist, 0, 8 * (size_t)B, C->stream));
-        launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, nullptr, dhist, 32 * (int)B,
+        launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, nullptr, dhist, (int)kLearnedEntryBytes * (int)B,
                             C->stream);
         std::vector<uint64_t> hist(B);
         CU(cudaMemcpyAsync(hist.data(), dhist, 8 * (size_t)B, cudaMemcpyDeviceToHost, C->stream));

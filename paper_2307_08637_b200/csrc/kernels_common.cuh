@@ -35,7 +35,7 @@ __device__ __forceinline__ uint64_t rmi_sample_size(const DevCfg& c, uint64_t n)
 }
 
 __device__ __forceinline__ uint32_t model_payload_bytes(const ModelHdr& h) {
-    if (h.kind == kLearned) return 32u * h.B;
+    if (h.kind == kLearned) return kLearnedEntryBytes * h.B;
     if (h.kind == kTree) return (uint32_t)((tree_payload_bytes(h.leaf_origin, h.nsplit) + 15) & ~15ull);
     return 0;
 }
@@ -88,8 +88,8 @@ struct Classifier {
         if constexpr (KIND == kLearned) {
             double xn = rmi_normalize(base, scale, x);
             const RmiEntry s = m.e[rmi_route(rs, ri, B, xn)];
-            return cdf_bucket(clamp_pred(__dadd_rn(__dmul_rn(s.slope, xn), s.intercept), s.lo, s.hi), cdf_lo,
-                              inv_span, nb);
+            return cdf_bucket_clamped(clamp_pred(__dadd_rn(__dmul_rn(s.slope, xn), s.intercept), s.lo, s.hi),
+                                      cdf_lo, inv_span, nb);
         } else if constexpr (KIND == kTree) {
             return tree_bucket(levels, leaf_origin, nsplit, m.tree, m.spl, m.eqo, x);
         } else if constexpr (KIND == kRadix) {

@@ -52,6 +52,20 @@ struct RmiEntry {
     double slope, intercept, lo, hi;
 };
 
+// Compiled learned table used by the partition kernels (follows RmiEntry[B]
+// in the model record): the submodel line plus the BUCKET ids of its clamp
+// bounds. The reference bucket is g(min(max(v, lo), hi)) with
+// g = bucket_of o clamp01 monotone nondecreasing (models.hpp:38-41,166-170),
+// which equals min(max(h(v), g(lo)), g(hi)) for the unclamped bucket h(v) --
+// two integer min/max instead of six double clamps, bit-identical ids.
+struct RmiBucketEntry {
+    double slope, intercept;
+    uint32_t glo, ghi;
+    uint64_t pad;
+};
+constexpr uint32_t kLearnedEntryBytes = sizeof(RmiEntry) + sizeof(RmiBucketEntry);  // 64
+constexpr uint32_t kModelIdentityCdf = 1u;  // ModelHdr.flags: cdf_lo == 0 and inv_span == 1
+
 // Partition-model record, 128 bytes; payload follows in the model arena:
 //   learned: RmiEntry[B]
 //   tree:    uint64 tree[leaf_origin], uint64 splitters[nsplit], uint32 eq_offset[nsplit+1]
@@ -82,9 +96,11 @@ __host__ __device__ __forceinline__ size_t tree_payload_bytes(uint32_t leaf_orig
 // Branch-free: fmax maps t <= 0 and NaN to 0; the saturating truncation and
 // min() give B-1 for t >= B -- identical wherever the reference's size_t
 // cast is defined (t < 2^64).
+// The truncating conversion saturates (negative and NaN -> 0, >= 2^32 -> max),
+// which is exactly the reference's !(t > 0) -> 0 plus the clamp.
 __device__ __forceinline__ uint32_t rmi_route(double root_slope, double root_icpt, uint32_t B, double xn) {
     double t = __dmul_rn(__dadd_rn(__dmul_rn(root_slope, xn), root_icpt), (double)B);
-    return min(__double2uint_rz(fmax(t, 0.0)), B - 1);
+    return min(__double2uint_rz(t), B - 1);
 }
 
 // Clamp of a submodel prediction (models.hpp:38-41): [lo,hi] then [0,1].
@@ -99,7 +115,29 @@ __device__ __forceinline__ double clamp_pred(double v, double lo, double hi) {
 // truncate, clamp to nb-1 (models.hpp:166-170)
 __device__ __forceinline__ uint32_t cdf_bucket(double f, double cdf_lo, double inv_span, uint32_t nb) {
     double t = __dmul_rn(__dmul_rn(__dsub_rn(f, cdf_lo), inv_span), (double)nb);
-    return min(__double2uint_rz(fmax(t, 0.0)), nb - 1);
+    return min(__double2uint_rz(t), nb - 1);
+}
+// g(v) = bucket of clamp01(v) (reference compare-and-assign clamp)
+__device__ __forceinline__ uint32_t cdf_bucket_clamped(double v, double cdf_lo, double inv_span, uint32_t nb) {
+    if (v < 0.0) v = 0.0;
+    if (v > 1.0) v = 1.0;
+    return cdf_bucket(v, cdf_lo, inv_span, nb);
+}
+// Fill the compiled table of a learned model record (header + RmiEntry[B]).
+__device__ __forceinline__ void compile_learned(uint8_t* model, uint32_t tid, uint32_t nthreads) {
+    ModelHdr* h = (ModelHdr*)model;
+    const RmiEntry* E = (const RmiEntry*)(model + sizeof(ModelHdr));
+    RmiBucketEntry* C = (RmiBucketEntry*)(model + sizeof(ModelHdr) + sizeof(RmiEntry) * (size_t)h->B);
+    for (uint32_t m = tid; m < h->B; m += nthreads) {
+        RmiBucketEntry c;
+        c.slope = E[m].slope;
+        c.intercept = E[m].intercept;
+        c.glo = cdf_bucket_clamped(E[m].lo, h->cdf_lo, h->inv_span, h->nbuckets);
+        c.ghi = cdf_bucket_clamped(E[m].hi, h->cdf_lo, h->inv_span, h->nbuckets);
+        c.pad = 0;
+        C[m] = c;
+    }
+    if (tid == 0) h->flags = (h->cdf_lo == 0.0 && h->inv_span == 1.0) ? kModelIdentityCdf : 0u;
 }
 
 // Rmi::normalize (models.hpp:56-58)

@@ -268,6 +268,8 @@ __device__ void train_rmi_block(const uint64_t* s, uint32_t n, uint32_t B, Model
         hdr->B = B;
     }
     __syncthreads();
+    compile_learned((uint8_t*)hdr, threadIdx.x, NT);
+    __syncthreads();
 }
 
 // SplitterTree::build (models.cpp:133-185) by one CTA from a sorted sample in
@@ -707,6 +709,8 @@ __global__ void __launch_bounds__(kEnforceNT) k_train_enforce(const uint64_t* s,
         h->cdf_lo = 0.0;
         h->inv_span = 1.0;
     }
+    __syncthreads();
+    compile_learned(model, threadIdx.x, kEnforceNT);
 }
 
 __global__ void __launch_bounds__(kModelNT) k_tree_build(const uint64_t* sorted, uint32_t s, uint32_t budget,

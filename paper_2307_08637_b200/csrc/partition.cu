@@ -82,8 +82,8 @@ __global__ void __launch_bounds__(kPlanNT) k_kind_plan(LevelParams p) {
 struct KState {
     // learned
     double rs, ri, base, scale, cdf_lo, inv_span;
-    const RmiEntry* E;
-    uint32_t B, nb;
+    const RmiBucketEntry* E;
+    uint32_t B, nb, identity;
     // tree (shared memory)
     const uint64_t* tree;
     const uint64_t* spl;
@@ -101,7 +101,8 @@ __device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t
     if constexpr (KIND == kLearned) {
         S.rs = h->root_slope; S.ri = h->root_icpt; S.base = h->key_base; S.scale = h->key_scale;
         S.cdf_lo = h->cdf_lo; S.inv_span = h->inv_span; S.B = h->B;
-        S.E = (const RmiEntry*)(g + sizeof(ModelHdr));
+        S.identity = h->flags & kModelIdentityCdf;
+        S.E = (const RmiBucketEntry*)(g + sizeof(ModelHdr) + sizeof(RmiEntry) * (size_t)S.B);
     } else if constexpr (KIND == kTree) {
         S.levels = h->levels; S.leaf = h->leaf_origin; S.nsplit = h->nsplit;
         uint32_t words = (uint32_t)((tree_payload_bytes(S.leaf, S.nsplit) + 15) / 16);
@@ -121,11 +122,15 @@ __device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t
 template <uint32_t KIND>
 __device__ __forceinline__ uint32_t kclassify(const KState& S, uint64_t x) {
     if constexpr (KIND == kLearned) {
+        // models.hpp:34-43,56-65,162-171 via the compiled table (RmiBucketEntry)
         const double xn = rmi_normalize(S.base, S.scale, x);
-        const double2* ep = (const double2*)(S.E + rmi_route(S.rs, S.ri, S.B, xn));
-        const double2 si = __ldg(ep), lh = __ldg(ep + 1);
-        const double v = clamp_pred(__dadd_rn(__dmul_rn(si.x, xn), si.y), lh.x, lh.y);
-        return cdf_bucket(v, S.cdf_lo, S.inv_span, S.nb);
+        const RmiBucketEntry* ep = S.E + rmi_route(S.rs, S.ri, S.B, xn);
+        const double2 li = __ldg((const double2*)ep);
+        const uint2 gb = __ldg((const uint2*)ep + 2);
+        const double v = __dadd_rn(__dmul_rn(li.x, xn), li.y);
+        const double t = S.identity ? __dmul_rn(v, (double)S.nb)
+                                    : __dmul_rn(__dmul_rn(__dsub_rn(v, S.cdf_lo), S.inv_span), (double)S.nb);
+        return min(max(min(__double2uint_rz(t), S.nb - 1), gb.x), gb.y);
     } else if constexpr (KIND == kTree) {
         return tree_bucket(S.levels, S.leaf, S.nsplit, S.tree, S.spl, S.eqo, x);
     } else {
