@@ -329,41 +329,39 @@ __device__ uint64_t block_exclusive_scan_u64(uint64_t* a, uint32_t n, uint64_t* 
 __device__ __forceinline__ uint32_t bitlen64(uint64_t v) { return v ? 64u - (uint32_t)__clzll((long long)v) : 0u; }
 
 // ----------------------------------------------------------- block sort
-// Shared-memory MSD sort of up to NT*ITEMS keys (the GPU base case; also
-// sorts samples for the model builder). One distribution pass buckets keys by
-// (k - min) >> shift into <= NBMAX digits (a range-adaptive radix: the digit
-// span shrinks by NBMAX each pass, so it terminates for any input). Digits of
-// <= 16 keys are insertion-sorted by one thread, <= 256 keys rank-sorted by
-// one warp, larger ones get another block pass (keys re-staged through
-// registers). Equal-key ranges end immediately (min == max).
+// Shared-memory sort of up to NT*ITEMS keys (the GPU base case; also sorts
+// samples for the model builder). One range-adaptive counting pass buckets
+// keys by (k - min) >> shift into ~one key per digit; then every key of a
+// digit with <= 16 keys computes its final slot directly (digit start + number
+// of smaller keys in its digit, ties by staging index) -- no per-digit
+// insertion sort, no divergence. Digits of 17..256 keys are rank-sorted by one
+// warp, larger ones get another counting pass (keys re-staged through
+// registers; the digit span shrinks by NBMAX each pass, so this terminates
+// for any input). Equal-key ranges end at once (min == max).
 template <int NT, int ITEMS, int NBMAX>
 struct BlockSort {
     static constexpr int CAP = NT * ITEMS;
     static constexpr int kSmall = 16;
     static constexpr int kMedium = 256;
     static constexpr int kListCap = CAP / (kSmall + 1) + 2;
+    static_assert(CAP <= 65536, "ranks are packed in 16 bits");
+    static constexpr int kRk = (ITEMS + 1) / 2;  // two 16-bit ranks per register
+    __device__ static __forceinline__ uint32_t rk_get(const uint32_t (&r)[kRk], int i) {
+        return (i & 1) ? (r[i >> 1] >> 16) : (r[i >> 1] & 0xffffu);
+    }
+    __device__ static __forceinline__ void rk_set(uint32_t (&r)[kRk], int i, uint32_t v) {
+        r[i >> 1] = (i & 1) ? ((r[i >> 1] & 0xffffu) | (v << 16)) : ((r[i >> 1] & 0xffff0000u) | v);
+    }
     struct Smem {
         uint32_t hist[NBMAX + 1];
         uint32_t wsum[NT / 32 + 1];
         uint64_t red[NT / 32];
         uint32_t n_med, n_large;
-        uint32_t med[kListCap];    // packed (off << 16 | len) won't fit CAP>65535: store pairs
+        uint32_t med[kListCap];
         uint32_t med_len[kListCap];
         uint32_t large[kListCap];
         uint32_t large_len[kListCap];
     };
-
-    __device__ static void insertion(uint64_t* a, uint32_t len) {
-        for (uint32_t i = 1; i < len; ++i) {
-            uint64_t v = a[i];
-            uint32_t j = i;
-            while (j > 0 && a[j - 1] > v) {
-                a[j] = a[j - 1];
-                --j;
-            }
-            a[j] = v;
-        }
-    }
 
     // warp rank sort of a[0,len), len <= 256
     __device__ static void warp_rank_sort(uint64_t* a, uint32_t len) {
@@ -417,21 +415,20 @@ struct BlockSort {
             __syncthreads();
             return;
         }
-        uint32_t nb = 1;  // ~2 keys per digit
-        while (2 * nb < len && nb < (uint32_t)NBMAX) nb <<= 1;
-        uint32_t lgnb = __ffs(nb) - 1;
-        uint32_t bits = bitlen64(mx - mn);
-        uint32_t shift = bits > lgnb ? bits - lgnb : 0;
+        uint32_t nb = 1;  // ~one key per digit
+        while (nb < len && nb < (uint32_t)NBMAX) nb <<= 1;
+        const uint32_t lgnb = __ffs(nb) - 1;
+        const uint32_t bits = bitlen64(mx - mn);
+        const uint32_t shift = bits > lgnb ? bits - lgnb : 0;
         for (uint32_t d = tid; d <= nb; d += NT) S.hist[d] = 0;
         __syncthreads();
-        uint32_t rank[ITEMS];
+        uint32_t rank[kRk];
+#pragma unroll
+        for (int i = 0; i < kRk; ++i) rank[i] = 0;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             uint32_t idx = tid + i * NT;
-            if (idx < len) {
-                uint32_t d = (uint32_t)((k[i] - mn) >> shift);
-                rank[i] = atomicAdd(&S.hist[d], 1u);
-            }
+            if (idx < len) rk_set(rank, i, atomicAdd(&S.hist[(uint32_t)((k[i] - mn) >> shift)], 1u));
         }
         __syncthreads();
         block_exclusive_scan_u32<NT>(S.hist, nb, S.wsum);
@@ -440,25 +437,44 @@ struct BlockSort {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             uint32_t idx = tid + i * NT;
+            if (idx < len) a[off + S.hist[(uint32_t)((k[i] - mn) >> shift)] + rk_get(rank, i)] = k[i];
+        }
+        __syncthreads();
+        // final slots for keys of small digits (rank within digit)
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            uint32_t idx = tid + i * NT;
             if (idx < len) {
-                uint32_t d = (uint32_t)((k[i] - mn) >> shift);
-                a[off + S.hist[d] + rank[i]] = k[i];
+                const uint32_t d = (uint32_t)((k[i] - mn) >> shift);
+                const uint32_t s0 = S.hist[d], c = S.hist[d + 1] - s0, me = s0 + rk_get(rank, i);
+                uint32_t p = me;
+                if (c <= (uint32_t)kSmall) {
+                    p = s0;
+                    for (uint32_t j = s0; j < s0 + c; ++j) {
+                        const uint64_t w = a[off + j];
+                        p += (w < k[i]) || (w == k[i] && j < me);
+                    }
+                }
+                rk_set(rank, i, p);
             }
         }
         __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            uint32_t idx = tid + i * NT;
+            if (idx < len) a[off + rk_get(rank, i)] = k[i];
+        }
         for (uint32_t d = tid; d < nb; d += NT) {
             uint32_t s0 = S.hist[d], l = S.hist[d + 1] - s0;
-            if (l < 2) continue;
-            if (l <= kSmall) {
-                insertion(a + off + s0, l);
-            } else if (l <= kMedium) {
-                uint32_t p = atomicAdd(&S.n_med, 1u);
-                S.med[p] = off + s0;
-                S.med_len[p] = l;
+            if (l <= (uint32_t)kSmall) continue;
+            if (l <= (uint32_t)kMedium) {
+                uint32_t q = atomicAdd(&S.n_med, 1u);
+                S.med[q] = off + s0;
+                S.med_len[q] = l;
             } else {
-                uint32_t p = atomicAdd(&S.n_large, 1u);
-                S.large[p] = off + s0;
-                S.large_len[p] = l;
+                uint32_t q = atomicAdd(&S.n_large, 1u);
+                S.large[q] = off + s0;
+                S.large_len[q] = l;
             }
         }
         __syncthreads();
@@ -479,12 +495,15 @@ struct BlockSort {
         const int warp = threadIdx.x >> 5;
         for (;;) {
             uint32_t nm = S.n_med;
+            uint32_t nl = S.n_large;
+            if (nm == 0 && nl == 0) break;  // uniform: written before the last barrier
             for (uint32_t e = warp; e < nm; e += NT / 32) warp_rank_sort(a + S.med[e], S.med_len[e]);
             __syncthreads();
             if (threadIdx.x == 0) S.n_med = 0;
-            uint32_t nl = S.n_large;
-            __syncthreads();
-            if (nl == 0) break;
+            if (nl == 0) {
+                __syncthreads();
+                break;
+            }
             uint32_t off = S.large[nl - 1], len = S.large_len[nl - 1];
             __syncthreads();
             if (threadIdx.x == 0) S.n_large = nl - 1;
