@@ -355,7 +355,7 @@ struct BlockSort {
     struct Smem {
         uint32_t hist[NBMAX + 1];
         uint32_t wsum[NT / 32 + 1];
-        uint64_t red[NT / 32];
+        uint64_t red[2 * (NT / 32)];
         uint32_t n_med, n_large;
         uint32_t med[kListCap];
         uint32_t med_len[kListCap];
@@ -391,10 +391,24 @@ struct BlockSort {
         __syncwarp();
     }
 
+    __device__ static __forceinline__ void push_big(Smem& S, uint32_t at, uint32_t l) {
+        if (l <= (uint32_t)kMedium) {
+            uint32_t q = atomicAdd(&S.n_med, 1u);
+            S.med[q] = at;
+            S.med_len[q] = l;
+        } else {
+            uint32_t q = atomicAdd(&S.n_large, 1u);
+            S.large[q] = at;
+            S.large_len[q] = l;
+        }
+    }
+
     // One distribution pass over keys held in registers k[] (valid where
     // idx < len, idx = tid + i*NT), writing the result into a[off, off+len).
-    __device__ static void pass(uint64_t (&k)[ITEMS], uint64_t* a, uint32_t off, uint32_t len, Smem& S) {
-        const int tid = threadIdx.x;
+    __device__ static __forceinline__ void pass(uint64_t (&k)[ITEMS], uint64_t* a, uint32_t off, uint32_t len,
+                                                Smem& S) {
+        const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+        // ---- min and max in one reduction (one barrier)
         uint64_t mn = ~0ull, mx = 0;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
@@ -404,8 +418,19 @@ struct BlockSort {
                 mx = k[i] > mx ? k[i] : mx;
             }
         }
-        mn = block_reduce_min<NT>(mn, S.red);
-        mx = block_reduce_max<NT>(mx, S.red);
+        for (int o = 16; o > 0; o >>= 1) {
+            uint64_t a1 = __shfl_xor_sync(0xffffffffu, mn, o), b1 = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = a1 < mn ? a1 : mn;
+            mx = b1 > mx ? b1 : mx;
+        }
+        if (lane == 0) { S.red[2 * warp] = mn; S.red[2 * warp + 1] = mx; }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) {
+            uint64_t a1 = S.red[2 * w], b1 = S.red[2 * w + 1];
+            mn = a1 < mn ? a1 : mn;
+            mx = b1 > mx ? b1 : mx;
+        }
         if (mn == mx) {  // homogeneous: write back unchanged
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
@@ -415,12 +440,12 @@ struct BlockSort {
             __syncthreads();
             return;
         }
-        uint32_t nb = 1;  // ~one key per digit
-        while (nb < len && nb < (uint32_t)NBMAX) nb <<= 1;
+        uint32_t nb = 1;  // ~two keys per digit
+        while (2 * nb < len && nb < (uint32_t)NBMAX) nb <<= 1;
         const uint32_t lgnb = __ffs(nb) - 1;
         const uint32_t bits = bitlen64(mx - mn);
         const uint32_t shift = bits > lgnb ? bits - lgnb : 0;
-        for (uint32_t d = tid; d <= nb; d += NT) S.hist[d] = 0;
+        for (uint32_t d = tid; d < nb; d += NT) S.hist[d] = 0;
         __syncthreads();
         uint32_t rank[kRk];
 #pragma unroll
@@ -431,8 +456,29 @@ struct BlockSort {
             if (idx < len) rk_set(rank, i, atomicAdd(&S.hist[(uint32_t)((k[i] - mn) >> shift)], 1u));
         }
         __syncthreads();
-        block_exclusive_scan_u32<NT>(S.hist, nb, S.wsum);
-        if (tid == 0) S.hist[nb] = len;
+        // ---- exclusive scan of hist[0,nb) with big-digit detection
+        {
+            const uint32_t per = (nb + NT - 1) / NT;
+            const uint32_t lo = min(nb, tid * per), hi = min(nb, lo + per);
+            uint32_t sum = 0;
+            for (uint32_t d = lo; d < hi; ++d) sum += S.hist[d];
+            uint32_t incl = sum;
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t w = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += w;
+            }
+            if (lane == 31) S.wsum[warp] = incl;
+            __syncthreads();
+            uint32_t run = incl - sum;
+            for (int w = 0; w < warp; ++w) run += S.wsum[w];
+            for (uint32_t d = lo; d < hi; ++d) {
+                uint32_t t = S.hist[d];
+                S.hist[d] = run;
+                if (t > (uint32_t)kSmall) push_big(S, off + run, t);
+                run += t;
+            }
+            if (tid == 0) S.hist[nb] = len;
+        }
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
@@ -464,20 +510,19 @@ struct BlockSort {
             uint32_t idx = tid + i * NT;
             if (idx < len) a[off + rk_get(rank, i)] = k[i];
         }
-        for (uint32_t d = tid; d < nb; d += NT) {
-            uint32_t s0 = S.hist[d], l = S.hist[d + 1] - s0;
-            if (l <= (uint32_t)kSmall) continue;
-            if (l <= (uint32_t)kMedium) {
-                uint32_t q = atomicAdd(&S.n_med, 1u);
-                S.med[q] = off + s0;
-                S.med_len[q] = l;
-            } else {
-                uint32_t q = atomicAdd(&S.n_large, 1u);
-                S.large[q] = off + s0;
-                S.large_len[q] = l;
-            }
+        __syncthreads();
+    }
+
+    // fallback pass over a range already in shared memory (kept out of line)
+    __device__ static __noinline__ void pass_smem(uint64_t* a, uint32_t off, uint32_t len, Smem& S) {
+        uint64_t k[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            uint32_t idx = threadIdx.x + i * NT;
+            if (idx < len) k[i] = a[off + idx];
         }
         __syncthreads();
+        pass(k, a, off, len, S);
     }
 
     // Sort a[0,n) in shared memory; keys arrive in registers k[] (idx = tid + i*NT).
@@ -488,15 +533,15 @@ struct BlockSort {
         }
         __syncthreads();
         pass(k, a, 0, n, S);
-        finish(k, a, S);
+        if (S.n_med | S.n_large) finish(a, S);
     }
 
-    __device__ static void finish(uint64_t (&k)[ITEMS], uint64_t* a, Smem& S) {
+    __device__ static __noinline__ void finish(uint64_t* a, Smem& S) {
         const int warp = threadIdx.x >> 5;
         for (;;) {
             uint32_t nm = S.n_med;
             uint32_t nl = S.n_large;
-            if (nm == 0 && nl == 0) break;  // uniform: written before the last barrier
+            if (nm == 0 && nl == 0) break;
             for (uint32_t e = warp; e < nm; e += NT / 32) warp_rank_sort(a + S.med[e], S.med_len[e]);
             __syncthreads();
             if (threadIdx.x == 0) S.n_med = 0;
@@ -507,13 +552,7 @@ struct BlockSort {
             uint32_t off = S.large[nl - 1], len = S.large_len[nl - 1];
             __syncthreads();
             if (threadIdx.x == 0) S.n_large = nl - 1;
-#pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                uint32_t idx = threadIdx.x + i * NT;
-                if (idx < len) k[i] = a[off + idx];
-            }
-            __syncthreads();
-            pass(k, a, off, len, S);
+            pass_smem(a, off, len, S);
         }
     }
 };

@@ -25,6 +25,8 @@ def main():
     w = torch.empty_like(p)
     ctx = L.Context(0)
     cfg = L.SortConfig(flags=L._native.FLAG_PHASE_TIMING)
+    if os.environ.get("LSORT_TARGET"):
+        cfg.bucket_target = int(os.environ["LSORT_TARGET"])
     for r in range(reps):
         w.copy_(p)
         torch.cuda.synchronize()
