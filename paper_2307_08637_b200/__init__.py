@@ -66,7 +66,7 @@ class SortConfig:
     seed: int = 0x5EED
     workers: int = 0
     base_case_capacity: int = 16384
-    bucket_target: int = 512
+    bucket_target: int = 4096
     flags: int = 0
 
     def to_c(self) -> N.lsort_cfg:

@@ -462,7 +462,7 @@ void lsort_cfg_default(lsort_cfg* c) {
     c->seed = 0x5EEDull;
     c->workers = 0;
     c->base_case_capacity = 16384;
-    c->bucket_target = 512;
+    c->bucket_target = 4096;
     c->flags = 0;
 }
 
