@@ -242,6 +242,8 @@ def run_ours(args):
             for i in range(len(work)):
                 ms, stats, _ = one_sort(i)
                 total_ms += ms
+                if dist_mode:
+                    stats = dict(stats.get("local") or {})
                 launches += stats.get("kernel_launches", 0)
                 for k, v in stats.items():
                     if isinstance(v, (int, float)):

@@ -1,0 +1,206 @@
+"""Multi-GPU distributed LearnedSort: RMI splitters + one all-to-all.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch). Each rank
+holds a shard; after ``DistSorter.sort`` rank r holds the r-th key range of
+the global sorted order (variable length), so the concatenation over ranks is
+the sorted input.
+
+Steps per sort (collectives are torch.distributed; all device work is the C-ABI):
+  1. every rank draws its share of the global RMI sample (device gather,
+     reference Rng stream per rank, rng.hpp:35-37);
+  2. all_gather of the samples; every rank sorts the identical global sample
+     and trains the identical monotone RMI (deterministic kernels,
+     models.cpp:39-131) -- no broadcast of parameters is needed;
+  3. local histogram under the global model, all_reduce -> global histogram;
+  4. rank boundaries = bucket-id cut points balancing the global counts
+     (monotone F => ranks receive disjoint, ordered key ranges);
+  5. destination-major partition of the local shard (the level-0 scatter with a
+     bucket -> rank map), all_to_all of the counts, all_to_all_single of keys;
+  6. local LearnedSort of the received (encoded) keys, decoded in place for
+     float64.
+
+``ops`` abstracts the device steps: the default (``NativeOps``) calls
+liblsort_cuda.so; tests inject a CPU implementation to exercise this host
+logic with gloo on CPU. The product path never uses a CPU fallback.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def splitmix64(x: int) -> int:
+    m = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & m
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & m
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & m
+    return x ^ (x >> 31)
+
+
+def rank_bounds(hist: np.ndarray, world: int) -> np.ndarray:
+    """Bucket cut points: rank r receives buckets [b[r], b[r+1]). Greedy
+    equal-count split of the global histogram (identical on every rank)."""
+    hist = np.asarray(hist, dtype=np.int64)
+    B = hist.size
+    total = int(hist.sum())
+    pref = np.cumsum(hist)
+    bounds = [0]
+    for r in range(1, world):
+        target = math.ceil(r * total / world)
+        b = int(np.searchsorted(pref, target, side="left")) + 1  # first bucket after the cut
+        b = min(max(b, bounds[-1]), B)
+        bounds.append(b)
+    bounds.append(B)
+    return np.asarray(bounds, dtype=np.uint32)
+
+
+def sample_shares(n_local: list[int], s_total: int) -> list[int]:
+    """Per-rank sample sizes proportional to shard sizes (sum == s_total)."""
+    N = sum(n_local)
+    if N == 0:
+        return [0] * len(n_local)
+    shares = [s_total * n // N for n in n_local]
+    rem = s_total - sum(shares)
+    for i in range(rem):
+        shares[i % len(shares)] += 1
+    return [min(s, n) if n else 0 for s, n in zip(shares, n_local)]
+
+
+class NativeOps:
+    """Device steps through the C-ABI (liblsort_cuda.so)."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+
+    def sample(self, keys, s: int, seed: int):
+        import ctypes as C
+        import torch
+        from . import _native as N
+        from . import _key_kind_of
+        out = torch.empty(max(s, 1), dtype=torch.int64, device=keys.device)
+        self.ctx._sync_stream()
+        if s:
+            rc = N.lib().lsort_cuda_dist_sample(self.ctx._h, C.c_void_p(keys.data_ptr()), keys.numel(),
+                                                _key_kind_of(keys), seed, s, C.c_void_p(out.data_ptr()))
+            self._check(rc)
+        return out[:s]
+
+    def train(self, sample, buckets: int):
+        import ctypes as C
+        from . import _native as N
+        from . import pack_rmi
+        h = N.lsort_rmi_header()
+        e = np.zeros((buckets, 4), np.float64)
+        self.ctx._sync_stream()
+        rc = N.lib().lsort_cuda_dist_train(self.ctx._h, C.c_void_p(sample.data_ptr()), sample.numel(), buckets,
+                                           C.byref(h), e.ctypes.data_as(C.c_void_p))
+        self._check(rc)
+        return pack_rmi(h, e)
+
+    def histogram(self, keys, P, buckets: int):
+        _, hist = self.ctx.classify_rmi(P, buckets, buckets, keys, ids=False)
+        return hist
+
+    def partition(self, keys, P, buckets: int, bounds: np.ndarray):
+        import ctypes as C
+        import torch
+        from . import _native as N
+        from . import _key_kind_of, unpack_rmi
+        h, e = unpack_rmi(P, buckets)
+        world = bounds.size - 1
+        out = torch.empty(max(keys.numel(), 1), dtype=torch.int64, device=keys.device)
+        counts = np.zeros(world, np.uint64)
+        b = np.ascontiguousarray(bounds, dtype=np.uint32)
+        self.ctx._sync_stream()
+        rc = N.lib().lsort_cuda_dist_partition(self.ctx._h, C.c_void_p(keys.data_ptr()), keys.numel(),
+                                               _key_kind_of(keys), C.byref(h), e.ctypes.data_as(C.c_void_p),
+                                               b.ctypes.data_as(C.c_void_p), world, C.c_void_p(out.data_ptr()),
+                                               counts.ctypes.data_as(C.c_void_p))
+        self._check(rc)
+        return out[: keys.numel()], [int(c) for c in counts]
+
+    def local_sort(self, keys_u64, cfg):
+        return self.ctx.sort(keys_u64, cfg)
+
+    def decode(self, keys_u64):
+        import ctypes as C
+        from . import _native as N
+        self.ctx._sync_stream()
+        self._check(N.lib().lsort_cuda_decode_inplace(self.ctx._h, C.c_void_p(keys_u64.data_ptr()),
+                                                      keys_u64.numel()))
+        return keys_u64.view(__import__("torch").float64)
+
+    def _check(self, rc):
+        from . import _check
+        _check(self.ctx, rc)
+
+
+@dataclass
+class DistStats:
+    n_in: int = 0
+    n_out: int = 0
+    sample: int = 0
+    send_counts: tuple = ()
+    bounds: tuple = ()
+    local: dict | None = None
+
+
+class DistSorter:
+    """Globally sort per-rank shards. ``keys``: contiguous tensor (float64 or
+    int64/uint64 bits) on this rank's device (or CPU with CPU ops)."""
+
+    def __init__(self, ctx=None, cfg=None, group=None, ops=None, buckets: int = 2048):
+        from . import SortConfig
+        self.cfg = cfg or SortConfig()
+        self.group = group
+        self.ops = ops or NativeOps(ctx)
+        self.buckets = buckets
+
+    def sort(self, keys):
+        import torch
+        import torch.distributed as dist
+        g = self.group
+        rank, world = dist.get_rank(g), dist.get_world_size(g)
+        dev = keys.device
+        is_f64 = keys.dtype == torch.float64
+        n_local = keys.numel()
+        # ---- 1. sample shares
+        sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([n_local], dtype=torch.int64, device=dev), group=g)
+        n_all = [int(t.item()) for t in sizes]
+        N = sum(n_all)
+        s_total = max(2, min(int(math.ceil(self.cfg.sample_fraction * N)), self.cfg.rmi_sample_cap))
+        shares = sample_shares(n_all, s_total)
+        seed = splitmix64(self.cfg.seed ^ splitmix64(0x6A09E667F3BCC908 + rank))
+        mine = self.ops.sample(keys, shares[rank], seed)
+        # ---- 2. all_gather samples (pad to the max share), identical global sample
+        smax = max(shares)
+        pad = torch.zeros(max(smax, 1), dtype=torch.int64, device=dev)
+        pad[: mine.numel()] = mine
+        gathered = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(gathered, pad, group=g)
+        sample = torch.cat([gathered[r][: shares[r]] for r in range(world)]).contiguous()
+        P = self.ops.train(sample, self.buckets)
+        # ---- 3. global histogram
+        hist = self.ops.histogram(keys, P, self.buckets).to(torch.int64)
+        dist.all_reduce(hist, group=g)
+        # ---- 4. rank boundaries
+        bounds = rank_bounds(hist.cpu().numpy(), world)
+        # ---- 5. partition + exchange
+        part, send = self.ops.partition(keys, P, self.buckets, bounds)
+        send_t = torch.tensor(send, dtype=torch.int64, device=dev)
+        recv_t = torch.empty(world, dtype=torch.int64, device=dev)
+        dist.all_to_all_single(recv_t, send_t, group=g)
+        recv = [int(x) for x in recv_t.cpu().tolist()]
+        out = torch.empty(max(sum(recv), 1), dtype=torch.int64, device=dev)[: sum(recv)]
+        dist.all_to_all_single(out, part, output_split_sizes=recv, input_split_sizes=send, group=g)
+        # ---- 6. local sort of encoded keys, decode
+        from . import SortConfig
+        lcfg = SortConfig(**{**self.cfg.__dict__})
+        local = self.ops.local_sort(out, lcfg) if out.numel() else {}
+        result = self.ops.decode(out) if is_f64 else out
+        stats = DistStats(n_in=n_local, n_out=int(out.numel()), sample=s_total, send_counts=tuple(send),
+                          bounds=tuple(int(b) for b in bounds), local=local)
+        return result, stats.__dict__

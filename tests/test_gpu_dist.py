@@ -1,0 +1,74 @@
+"""The distributed sort's native device steps (sample, global RMI train,
+histogram, destination-major partition, local sort, decode) through the C-ABI,
+with NCCL at world size 1 on one B200 (this run has one GPU; the multi-rank
+host logic is covered by tests/test_dist_cpu.py with gloo)."""
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2307_08637_b200 as L  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import torch.distributed as dist
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_port()}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dist_name,seed", [("normal", 7), ("lognormal2", 19), ("rootdups", 3)])
+def test_dist_sort_world1(pg, dist_name, seed):
+    from paper_2307_08637_b200.dist import DistSorter
+    x = O.generate(dist_name, 2_000_000, seed)
+    t = torch.from_numpy(x if x.dtype == np.float64 else x.view(np.int64)).cuda()
+    ctx = L.Context(0)
+    out, st = DistSorter(ctx, L.SortConfig()).sort(t)
+    got = out.cpu().numpy()
+    if x.dtype == np.float64:
+        exp = O.decode(np.sort(O.encode(x)))
+        assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
+    else:
+        assert np.array_equal(got.view(np.uint64), np.sort(x))
+    assert st["n_out"] == x.size and st["send_counts"] == (x.size,)
+
+
+def test_dist_partition_destinations(pg):
+    """lsort_cuda_dist_partition: destination-major output, counts per rank,
+    every key routed by the bucket->rank map of the global model."""
+    from paper_2307_08637_b200.dist import NativeOps, rank_bounds
+    x = O.generate("uniform", 500_000, 42)
+    t = torch.from_numpy(x).cuda()
+    ops = NativeOps(L.Context(0))
+    keys = O.encode(x)
+    sample = torch.from_numpy(np.sort(keys[::50]).view(np.int64)).cuda()
+    P = ops.train(sample.clone(), 512)
+    hist = ops.histogram(t, P, 512).cpu().numpy()
+    bounds = rank_bounds(hist, 4)
+    part, counts = ops.partition(t, P, 512, bounds)
+    assert sum(counts) == x.size
+    ids = O.learned_bucket(P, 512, 512, keys)
+    dest = np.searchsorted(bounds, ids, side="right") - 1
+    assert counts == [int(c) for c in np.bincount(dest, minlength=4)]
+    got = part.cpu().numpy().view(np.uint64)
+    off = 0
+    for r in range(4):
+        seg = got[off:off + counts[r]]
+        assert np.array_equal(np.sort(seg), np.sort(keys[dest == r]))
+        off += counts[r]
