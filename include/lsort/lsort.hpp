@@ -1,0 +1,145 @@
+// lsort/lsort.hpp -- C++20 drop-in for the reference's sort entry point
+// (`sort(a, cfg)` in place over a contiguous range of keys,
+// float64 pre-encoded with keys.hpp:36-42), backed by liblsort_cuda.so
+// through the C-ABI in lsort_cuda.h. Header-only; link with -llsort_cuda.
+//
+//   lsort::SortConfig cfg;                 // SPEC.md:369-372 defaults
+//   lsort::sort(std::span<lsort::Key>(v)); // host uint64 keys (copied in/out)
+//   lsort::sort(std::span<double>(d));     // host float64; NaN -> lsort::nan_error
+//   lsort::sort(lsort::device_span<double>{dptr, n});  // keys already in HBM
+//
+// Errors mirror the reference: invalid configuration -> std::invalid_argument
+// (models.cpp:40-43), NaN -> lsort::nan_error (derived from
+// std::invalid_argument) carrying the first NaN index (keys.hpp:34-42),
+// CUDA / allocation failures -> lsort::cuda_error. One context per thread
+// (thread_local), so concurrent sorts on disjoint arrays are safe
+// (SPEC.md:445).
+#ifndef LSORT_LSORT_HPP
+#define LSORT_LSORT_HPP
+
+#include <cstddef>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+
+#include "../lsort_cuda.h"
+
+namespace lsort {
+
+using Key = std::uint64_t;  // keys.hpp:18
+
+struct SortConfig {
+    std::uint32_t rmi_bucket_count = 1024;
+    std::uint32_t tree_bucket_count = 256;
+    std::uint64_t min_rmi_input = 100000;
+    double max_duplicate_fraction = 0.10;
+    std::uint32_t radix_base_case = 4096;
+    std::uint32_t insertion_base_case = 16;
+    std::uint32_t first_sample_cap = 2 * 256 * 16;
+    std::uint32_t rmi_sample_cap = 1u << 20;
+    double sample_fraction = 0.01;
+    std::uint64_t seed = 0x5EED;
+    std::uint32_t workers = 0;
+    // GPU extensions
+    std::uint32_t base_case_capacity = 16384;
+    std::uint32_t bucket_target = 4096;
+    int device = 0;
+
+    lsort_cfg to_c() const {
+        lsort_cfg c;
+        lsort_cfg_default(&c);
+        c.rmi_bucket_count = rmi_bucket_count;
+        c.tree_bucket_count = tree_bucket_count;
+        c.min_rmi_input = min_rmi_input;
+        c.max_duplicate_fraction = max_duplicate_fraction;
+        c.radix_base_case = radix_base_case;
+        c.insertion_base_case = insertion_base_case;
+        c.first_sample_cap = first_sample_cap;
+        c.rmi_sample_cap = rmi_sample_cap;
+        c.sample_fraction = sample_fraction;
+        c.seed = seed;
+        c.workers = workers;
+        c.base_case_capacity = base_case_capacity;
+        c.bucket_target = bucket_target;
+        return c;
+    }
+};
+
+class nan_error : public std::invalid_argument {
+public:
+    explicit nan_error(std::uint64_t index)
+        : std::invalid_argument("lsort::sort: NaN at index " + std::to_string(index)), index_(index) {}
+    std::uint64_t index() const noexcept { return index_; }
+
+private:
+    std::uint64_t index_;
+};
+
+class cuda_error : public std::runtime_error {
+public:
+    cuda_error(int code, const std::string& msg) : std::runtime_error(msg), code_(code) {}
+    int code() const noexcept { return code_; }
+
+private:
+    int code_;
+};
+
+// Keys resident in device memory (HBM).
+template <class T>
+struct device_span {
+    T* data;
+    std::size_t size;
+};
+
+namespace detail {
+struct Context {
+    lsort_ctx* h = nullptr;
+    int device = -1;
+    ~Context() {
+        if (h) lsort_cuda_ctx_destroy(h);
+    }
+    lsort_ctx* get(int dev) {
+        if (h && device == dev) return h;
+        if (h) lsort_cuda_ctx_destroy(h);
+        h = nullptr;
+        int rc = lsort_cuda_ctx_create(&h, dev, nullptr, 0);
+        if (rc != LSORT_OK) throw cuda_error(rc, "lsort: cannot create a context on device " + std::to_string(dev));
+        device = dev;
+        return h;
+    }
+};
+inline Context& context() {
+    thread_local Context c;
+    return c;
+}
+inline void run(void* keys, std::size_t n, int kind, int mem, const SortConfig& cfg) {
+    lsort_ctx* h = context().get(cfg.device);
+    lsort_cfg c = cfg.to_c();
+    std::uint64_t nan_index = ~0ull;
+    int rc = lsort_cuda_sort(h, keys, n, kind, mem, &c, nullptr, &nan_index);
+    if (rc == LSORT_OK) return;
+    if (rc == LSORT_ENAN) throw nan_error(nan_index);
+    std::string msg = lsort_cuda_last_error(h);
+    if (rc == LSORT_EINVAL) throw std::invalid_argument("lsort::sort: " + msg);
+    throw cuda_error(rc, "lsort::sort: " + msg);
+}
+}  // namespace detail
+
+// sort(a, cfg) -- SPEC.md:384-392. Ascending, unstable.
+inline void sort(std::span<Key> a, const SortConfig& cfg = {}) {
+    detail::run(a.data(), a.size(), LSORT_KEY_U64, LSORT_MEM_HOST, cfg);
+}
+inline void sort(std::span<double> a, const SortConfig& cfg = {}) {
+    detail::run(a.data(), a.size(), LSORT_KEY_F64, LSORT_MEM_HOST, cfg);
+}
+inline void sort(device_span<Key> a, const SortConfig& cfg = {}) {
+    detail::run(a.data, a.size, LSORT_KEY_U64, LSORT_MEM_DEVICE, cfg);
+}
+inline void sort(device_span<double> a, const SortConfig& cfg = {}) {
+    detail::run(a.data, a.size, LSORT_KEY_F64, LSORT_MEM_DEVICE, cfg);
+}
+
+}  // namespace lsort
+
+#endif
