@@ -121,6 +121,6 @@ void launch_decode(uint64_t* keys, uint64_t n, cudaStream_t st);
 int num_sms();
 void kernels_init();   // shared-memory opt-in for every kernel
 
-constexpr uint32_t kWarpBaseCap = 512;   // segments <= this: warp-level base case
+constexpr uint32_t kWarpBaseCap = 1024;  // segments <= this: smallest base-case class
 
 }  // namespace lsort_dev
