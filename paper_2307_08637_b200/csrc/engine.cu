@@ -138,7 +138,7 @@ void validate_cfg(const lsort_cfg& c) {
     if (!pow2(c.tree_bucket_count) || c.tree_bucket_count > LSORT_MAX_TREE)
         throw LsortError{LSORT_EINVAL, "tree_bucket_count must be a power of two in [2, 1024]"};
     if (c.first_sample_cap < 2 || c.first_sample_cap > kSmallSampleCap)
-        throw LsortError{LSORT_EINVAL, "first_sample_cap must be in [2, 16384]"};
+        throw LsortError{LSORT_EINVAL, "first_sample_cap must be in [2, 8192]"};
     if (c.rmi_sample_cap < 2) throw LsortError{LSORT_EINVAL, "rmi_sample_cap must be >= 2"};
     if (!(c.sample_fraction > 0.0) || c.sample_fraction > 1.0)
         throw LsortError{LSORT_EINVAL, "sample_fraction must be in (0, 1]"};
@@ -167,11 +167,22 @@ struct Engine {
 
     uint32_t rmi_b(uint64_t n) const { return fanout(n, cfg.rmi_bucket_count, cfg.bucket_target); }
     uint32_t tree_k(uint64_t n) const { return fanout(n, cfg.tree_bucket_count, cfg.bucket_target); }
-    bool is_big(const SegPlan& s) const {
-        if (s.flags & kSegForceRadix) return false;
-        if (s.n < cfg.min_rmi_input) return false;
-        return sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, s.n) > kSmallSampleCap;
+    // largest sample the segment's model may need (the RMI sample only if the
+    // policy can pick the learned branch)
+    uint64_t sample_need(const SegPlan& s) const {
+        uint64_t s1 = sample_size_host(cfg.sample_fraction, cfg.first_sample_cap, s.n);
+        uint64_t s2 = s.n >= cfg.min_rmi_input ? sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, s.n) : 0;
+        return std::max(s1, s2);
     }
+    // 0 small model CTA, 1 mid model CTA, 2 big pipeline
+    int model_class(const SegPlan& s) const {
+        if (s.flags & kSegForceRadix) return 0;
+        uint64_t need = sample_need(s);
+        if (need <= kModelSmallCap) return 0;
+        if (need <= kSmallSampleCap) return 1;
+        return 2;
+    }
+    bool is_big(const SegPlan& s) const { return model_class(s) == 2; }
 
     void launched(int k = 1) { C->launches += k; }
 
@@ -196,36 +207,96 @@ struct Engine {
         C->nested->launches = 0;
     }
 
-    // Model for one big segment (sample > one CTA): first sample + policy on
-    // one CTA; for the learned branch, a device-wide gather, a nested sort of
-    // the RMI sample and a single-CTA training pass.
-    void big_model(const SegDesc* dseg, const SegPlan& sp, const SegDesc& hseg, const void* src, bool f64) {
-        DevCfg dc = dev_cfg(cfg);
-        launch_first_sample(dseg, src, f64, C->models.as<uint8_t>(), dc, st);
-        launched();
-        ModelHdr h;
-        CU(cudaMemcpyAsync(&h, C->models.as<uint8_t>() + hseg.model_off, sizeof(h), cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-        if (h.kind != kLearned) return;
-        uint64_t s1 = h.s1, s2 = h.s2;
-        if (!C->sample.ensure(s2 * 8)) throw LsortError{LSORT_ENOMEM, "sample buffer"};
-        uint64_t seed = seg_seed_host(cfg.seed, sp.begin, sp.depth);
-        launch_gather(dseg, src, f64, seed, s1, s2, C->sample.as<uint64_t>(), st);
-        launched();
-        nested_sort(C->sample.as<uint64_t>(), s2);
-        if (trace_enabled()) CU(cudaEventRecord(C->ev[5], st));
-        if (!C->train_ws.ensure(train_workspace_bytes(s2, hseg.rmi_b))) throw LsortError{LSORT_ENOMEM, "train ws"};
-        launch_train_rmi(C->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
-                         hseg.rmi_b, C->train_ws.p, st);
-        launched(7);
-        if (trace_enabled()) {
-            CU(cudaEventRecord(C->ev[4], st));
-            CU(cudaEventSynchronize(C->ev[4]));
-            float ms = 0;
-            cudaEventElapsedTime(&ms, C->ev[5], C->ev[4]);
-            fprintf(stderr, "[lsort d%d] big model: s1=%llu s2=%llu train %.3f ms\n", C->depth,
-                    (unsigned long long)s1, (unsigned long long)s2, ms);
+    lsort_ctx* nested_ctx() {
+        if (!C->nested) {
+            C->nested.reset(new lsort_ctx());
+            C->nested->device = C->device;
+            C->nested->depth = C->depth + 1;
+            for (auto& e : C->nested->ev) CU(cudaEventCreate(&e));
+            for (auto& e : C->nested->pev) CU(cudaEventCreate(&e));
         }
+        C->nested->stream = C->stream;
+        return C->nested.get();
+    }
+
+    // Model for one big segment (RMI sample > one CTA), with no host round
+    // trip: (1) one CTA draws + sorts the first sample, decides the policy
+    // (writes *gate) and builds a splitter tree over the first sample;
+    // (2) device-wide gather of the RMI sample; (3) the sample is sorted by one
+    // distribution level with that tree + shared-memory base cases; (4)
+    // multi-CTA training. Every step after (1) is gated on the device.
+    void big_model(const SegDesc* dseg, const SegPlan& sp, const SegDesc& hseg, const void* src, bool f64,
+                   uint32_t big_index) {
+        DevCfg dc = dev_cfg(cfg);
+        lsort_ctx* N = nested_ctx();
+        const uint64_t n = sp.n;
+        const uint64_t s1 = sample_size_host(cfg.sample_fraction, cfg.first_sample_cap, n);
+        const uint64_t s2 = sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
+        const uint32_t k = cfg.tree_bucket_count;         // sample-sort splitter budget
+        const uint32_t nb = 2 * k - 1;
+        const size_t aux_bytes = sizeof(ModelHdr) + ((tree_payload_bytes(k, k - 1) + 15) & ~15ull);
+        const uint64_t ntiles = (s2 + kTileKeys - 1) / kTileKeys;
+        if (!C->sample.ensure(s2 * 8) || !N->scratch.ensure(s2 * 8) || !N->models.ensure(aux_bytes) ||
+            !N->segs.ensure(sizeof(SegDesc)) || !N->tile_prefix.ensure(16) || !N->buckets.ensure(8 * (size_t)nb) ||
+            !N->rec.ensure(nb * sizeof(SegOut)) || !N->fill.ensure(nb * sizeof(FillItem)) ||
+            !N->base[0].ensure(nb * sizeof(BaseItem)) || !N->base[1].ensure(nb * sizeof(BaseItem)) ||
+            !N->base[2].ensure(nb * sizeof(BaseItem)) || !N->kseg.ensure(64) || !N->ktp.ensure(64) ||
+            !N->kplan.ensure(3 * sizeof(KindPlan)) || !N->ctrl.ensure(sizeof(Ctrl) * (big_index + 1)) ||
+            !N->aux.ensure(4 * (big_index + 1)) || !C->train_ws.ensure(train_workspace_bytes(s2, hseg.rmi_b)))
+            throw LsortError{LSORT_ENOMEM, "big model workspace"};
+        uint32_t* gate = N->aux.as<uint32_t>() + big_index;
+        Ctrl* nctrl = N->ctrl.as<Ctrl>() + big_index;
+        launch_first_sample(dseg, src, f64, C->models.as<uint8_t>(), dc, N->models.as<uint8_t>(), k, gate, st);
+        const uint64_t seed = seg_seed_host(cfg.seed, sp.begin, sp.depth);
+        launch_gather(dseg, src, f64, seed, s1, s2, C->sample.as<uint64_t>(), gate, st);
+        // one distribution level over the sample with the first-sample tree
+        SegDesc d{};
+        d.begin = 0;
+        d.n = s2;
+        d.model_off = 0;
+        d.bucket_off = 0;
+        d.nb_max = nb;
+        d.tree_k = k;
+        uint64_t pref[2] = {0, ntiles};
+        CU(cudaMemcpyAsync(N->segs.p, &d, sizeof(d), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(N->tile_prefix.p, pref, 16, cudaMemcpyHostToDevice, st));
+        CU(cudaMemsetAsync(N->buckets.p, 0, 8 * (size_t)nb, st));
+        CU(cudaMemsetAsync(nctrl, 0, sizeof(Ctrl), st));
+        CU(cudaMemsetAsync(&nctrl->nan_index, 0xff, 8, st));
+        LevelParams q{};
+        q.segs = N->segs.as<SegDesc>();
+        q.nsegs = 1;
+        q.tile_prefix = N->tile_prefix.as<uint64_t>();
+        q.ntiles = ntiles;
+        q.models = N->models.as<uint8_t>();
+        q.buckets = N->buckets.as<unsigned long long>();
+        q.src = C->sample.p;
+        q.dst = N->scratch.as<uint64_t>();
+        q.ctrl = nctrl;
+        q.rec = N->rec.as<SegOut>();
+        for (int c = 0; c < 3; ++c) q.base[c] = N->base[c].as<BaseItem>();
+        q.fill = N->fill.as<FillItem>();
+        q.base_cap[0] = kWarpBaseCap;
+        q.base_cap[1] = 4096;
+        q.base_cap[2] = 16384;
+        q.depth_cap = 64;
+        q.list_cap = nb;
+        q.gate = gate;
+        q.kseg = N->kseg.as<uint32_t>();
+        q.ktp = N->ktp.as<uint64_t>();
+        q.kplan = N->kplan.as<KindPlan>();
+        q.kstride = 1;
+        const int nsm = num_sms();
+        const int g = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 3);
+        launch_kind_plan(q, st);
+        launch_hist(q, 0, 2u, g, st);
+        launch_scan_children(q, st);
+        launch_scatter(q, 0, 2u, nb, g, st);
+        launch_base_cases(q, N->scratch.as<uint64_t>(), C->sample.p, 0, st);
+        launch_fill(q, C->sample.p, 0, nsm, st);
+        launch_train_rmi(C->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
+                         hseg.rmi_b, C->train_ws.p, gate, st);
+        launched(2 + 9 + 8);
     }
 
     // Sort n keys at `keys` (device) in place. Returns LSORT_ENAN via throw.
@@ -267,6 +338,7 @@ struct Engine {
             uint32_t* hi = C->hidx.as<uint32_t>();
             uint64_t model_bytes = 0, nbuckets = 0, ntiles = 0;
             uint32_t max_payload = 0, max_nb = 0, nsmall = 0, kinds = 0;
+            std::vector<uint32_t> mids;
             std::vector<uint32_t> bigs;
             for (uint32_t i = 0; i < ns; ++i) {
                 const SegPlan& s = segs[i];
@@ -295,7 +367,9 @@ struct Engine {
                 max_nb = std::max(max_nb, nb);
                 hp[i] = ntiles;
                 ntiles += (s.n + kTileKeys - 1) / kTileKeys;
-                if (is_big(s)) bigs.push_back(i);
+                const int mc = model_class(s);
+                if (mc == 2) bigs.push_back(i);
+                else if (mc == 1) mids.push_back(i);
                 else hi[nsmall++] = i;
                 if (s.flags & kSegForceRadix) kinds |= 4u;
                 else kinds |= (s.n >= cfg.min_rmi_input ? 1u : 0u) | 2u;
@@ -311,7 +385,9 @@ struct Engine {
                 throw LsortError{LSORT_ENOMEM, "level workspace"};
             CU(cudaMemcpyAsync(C->segs.p, hs, ns * sizeof(SegDesc), cudaMemcpyHostToDevice, st));
             CU(cudaMemcpyAsync(C->tile_prefix.p, hp, (ns + 1) * 8, cudaMemcpyHostToDevice, st));
-            if (nsmall) CU(cudaMemcpyAsync(C->idx.p, hi, nsmall * 4, cudaMemcpyHostToDevice, st));
+            for (uint32_t i = 0; i < mids.size(); ++i) hi[nsmall + i] = mids[i];
+            const uint32_t nmid = (uint32_t)mids.size();
+            if (nsmall + nmid) CU(cudaMemcpyAsync(C->idx.p, hi, (nsmall + nmid) * 4, cudaMemcpyHostToDevice, st));
             CU(cudaMemsetAsync(C->buckets.p, 0, nbuckets * 8, st));
             CU(cudaMemsetAsync(&dctrl->n_rec, 0, offsetof(Ctrl, keys_fill) - offsetof(Ctrl, n_rec), st));
 
@@ -344,9 +420,13 @@ struct Engine {
             };
             mark(0);
             // ---- models
-            launch_build_models(p.segs, C->idx.as<uint32_t>(), nsmall, src, src_f64, C->models.as<uint8_t>(), dc, st);
-            if (nsmall) launched();
-            for (uint32_t b : bigs) big_model(p.segs + b, segs[b], hs[b], src, src_f64);
+            launch_build_models(p.segs, C->idx.as<uint32_t>(), nsmall, src, src_f64, C->models.as<uint8_t>(), dc, 0,
+                                st);
+            launch_build_models(p.segs, C->idx.as<uint32_t>() + nsmall, nmid, src, src_f64, C->models.as<uint8_t>(),
+                                dc, 1, st);
+            launched((nsmall ? 1 : 0) + (nmid ? 1 : 0));
+            for (uint32_t bi = 0; bi < bigs.size(); ++bi) big_model(p.segs + bigs[bi], segs[bigs[bi]], hs[bigs[bi]], src,
+                                                                    src_f64, bi);
             // ---- partition
             const int nsm = num_sms();
             int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 3);
@@ -682,7 +762,7 @@ int lsort_cuda_rmi_train(lsort_ctx* C, const uint64_t* d_sample, uint64_t s, uin
             !C->train_ws.ensure(train_workspace_bytes(s, B)))
             throw LsortError{LSORT_ENOMEM, "model"};
         CU(cudaMemsetAsync(C->models.p, 0, sizeof(ModelHdr), C->stream));
-        launch_train_rmi(d_sample, s, B, C->models.as<uint8_t>(), B, C->train_ws.p, C->stream);
+        launch_train_rmi(d_sample, s, B, C->models.as<uint8_t>(), B, C->train_ws.p, nullptr, C->stream);
         CU(cudaGetLastError());
         download_learned(C, C->models.as<uint8_t>(), B, h_out, e_out);
     } catch (const LsortError& e) {
@@ -771,9 +851,10 @@ int lsort_cuda_build_model(lsort_ctx* C, const void* d_keys, uint64_t n, int key
         uint32_t zero = 0;
         CU(cudaMemcpyAsync(C->idx.p, &zero, 4, cudaMemcpyHostToDevice, C->stream));
         const bool f64 = key_kind == LSORT_KEY_F64;
-        if (E.is_big(sp)) E.big_model(C->segs.as<SegDesc>(), sp, d, d_keys, f64);
+        const int mc = E.model_class(sp);
+        if (mc == 2) E.big_model(C->segs.as<SegDesc>(), sp, d, d_keys, f64, 0);
         else launch_build_models(C->segs.as<SegDesc>(), C->idx.as<uint32_t>(), 1, d_keys, f64,
-                                 C->models.as<uint8_t>(), dev_cfg(cfg), C->stream);
+                                 C->models.as<uint8_t>(), dev_cfg(cfg), mc, C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
         ModelHdr h;
@@ -853,7 +934,8 @@ int lsort_cuda_dist_sample(lsort_ctx* C, const void* d_keys, uint64_t n, int key
         d.n = n;
         if (!C->segs.ensure(sizeof(SegDesc))) throw LsortError{LSORT_ENOMEM, "seg"};
         CU(cudaMemcpyAsync(C->segs.p, &d, sizeof(d), cudaMemcpyHostToDevice, C->stream));
-        if (s) launch_gather(C->segs.as<SegDesc>(), d_keys, key_kind == LSORT_KEY_F64, seed, 0, s, d_out, C->stream);
+        if (s) launch_gather(C->segs.as<SegDesc>(), d_keys, key_kind == LSORT_KEY_F64, seed, 0, s, d_out, nullptr,
+                             C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
     } catch (const LsortError& e) {
@@ -874,7 +956,7 @@ int lsort_cuda_dist_train(lsort_ctx* C, uint64_t* d_sample, uint64_t s, uint32_t
         if (!C->models.ensure(sizeof(ModelHdr) + kLearnedEntryBytes * (size_t)buckets) ||
             !C->train_ws.ensure(train_workspace_bytes(s, buckets)))
             throw LsortError{LSORT_ENOMEM, "model"};
-        launch_train_rmi(d_sample, s, buckets, C->models.as<uint8_t>(), buckets, C->train_ws.p, C->stream);
+        launch_train_rmi(d_sample, s, buckets, C->models.as<uint8_t>(), buckets, C->train_ws.p, nullptr, C->stream);
         CU(cudaGetLastError());
         download_learned(C, C->models.as<uint8_t>(), buckets, h_out, e_out);
     } catch (const LsortError& e) {

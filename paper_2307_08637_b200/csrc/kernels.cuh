@@ -68,6 +68,7 @@ struct LevelParams {
     uint32_t base_cap[3];          // size classes: n <= base_cap[c]
     uint32_t depth_cap;
     uint32_t list_cap;             // capacity of rec/base/fill lists
+    const uint32_t* gate;          // nullptr, or: level runs only if *gate != 0
     uint32_t* kseg;                // [3][kstride] segment indices per kind
     uint64_t* ktp;                 // [3][kstride+1] tile prefixes per kind
     KindPlan* kplan;               // [3]
@@ -86,19 +87,22 @@ struct DevCfg {
 constexpr int kTileKeys = 4096;     // keys per classify/scatter tile
 constexpr int kPartNT = 512;        // threads per classify/scatter CTA
 constexpr int kRadixBits = 10;      // fallback radix model: 1024 buckets
-constexpr uint32_t kSmallSampleCap = 16384;  // samples sortable in one CTA
+constexpr uint32_t kSmallSampleCap = 8192;   // samples sortable in one model CTA
+constexpr uint32_t kModelSmallCap = 2048;    // samples of the small model CTA
 
 // Host-visible launchers.
 // models.cu
+// mid = 0: samples <= kModelSmallCap (256 threads); 1: <= kSmallSampleCap (512 threads)
 void launch_build_models(const SegDesc* segs, const uint32_t* idx, uint32_t count, const void* src,
-                         int in_f64, uint8_t* models, const DevCfg& cfg, cudaStream_t st);
+                         int in_f64, uint8_t* models, const DevCfg& cfg, int mid, cudaStream_t st);
 void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_t* models,
-                         const DevCfg& cfg, cudaStream_t st);
+                         const DevCfg& cfg, uint8_t* aux, uint32_t aux_budget, uint32_t* gate,
+                         cudaStream_t st);
 void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0,
-                   uint64_t s, uint64_t* out, cudaStream_t st);
+                   uint64_t s, uint64_t* out, const uint32_t* gate, cudaStream_t st);
 size_t train_workspace_bytes(uint64_t s, uint32_t B);
 void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* model, uint32_t nbuckets,
-                      void* ws, cudaStream_t st);
+                      void* ws, const uint32_t* gate, cudaStream_t st);
 void launch_tree_build(const uint64_t* sorted, uint64_t s, uint32_t budget, int eq_mode, uint8_t* model,
                        cudaStream_t st);
 void launch_block_sort(uint64_t* keys, uint64_t n, cudaStream_t st);

@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "kernels_common.cuh"
+#include "smemsort.cuh"
 
 namespace lsort_dev {
 
@@ -158,7 +159,7 @@ __device__ Fit fit_warp(XN xn, uint32_t first, uint32_t last, double n_total) {
 // lo[B], hi[B] doubles, big-slice list. Output: header + entries (global).
 constexpr int kSeqFitMax = 512;
 template <int NT>
-__device__ void train_rmi_block(const uint64_t* s, uint32_t n, uint32_t B, ModelHdr* hdr, RmiEntry* E,
+__device__ __noinline__ void train_rmi_block(const uint64_t* s, uint32_t n, uint32_t B, ModelHdr* hdr, RmiEntry* E,
                                 uint32_t* first, double* lo, double* hi, uint32_t* biglist, double* red) {
     const double base = __ull2double_rn(s[0]);
     const double kmax = __ull2double_rn(s[n - 1]);
@@ -275,7 +276,7 @@ __device__ void train_rmi_block(const uint64_t* s, uint32_t n, uint32_t B, Model
 // SplitterTree::build (models.cpp:133-185) by one CTA from a sorted sample in
 // shared memory. Scratch: u32[2k].
 template <int NT>
-__device__ void tree_build_block(const uint64_t* s, uint32_t n, uint32_t k, bool eq_mode, ModelHdr* hdr,
+__device__ __noinline__ void tree_build_block(const uint64_t* s, uint32_t n, uint32_t k, bool eq_mode, ModelHdr* hdr,
                                  uint8_t* payload, uint32_t* scratch, uint32_t* wsum, uint64_t* spl_tmp) {
     uint32_t* keep = scratch;      // k entries
     uint32_t* eqo = scratch + k;   // k entries (+1)
@@ -347,39 +348,47 @@ __device__ void tree_build_block(const uint64_t* s, uint32_t n, uint32_t k, bool
     __syncthreads();
 }
 
-constexpr int kModelNT = 512;
-using ModelSort = BlockSort<kModelNT, 32, 8192>;
-struct ModelSmem {
-    uint64_t a[16384];
-    union {
-        typename ModelSort::Smem sort;
-        struct {
-            uint32_t first[LSORT_MAX_RMI_DEV + 1];
-            double lo[LSORT_MAX_RMI_DEV];
-            double hi[LSORT_MAX_RMI_DEV];
-            uint32_t big[LSORT_MAX_RMI_DEV];
-            double red[2 * (kModelNT / 32)];
-        } rmi;
-        struct {
-            uint32_t scratch[2 * LSORT_MAX_TREE_DEV + 2];
-            uint32_t wsum[kModelNT / 32 + 1];
-            uint64_t spl[LSORT_MAX_TREE_DEV];
-        } tree;
-    } u;
-    uint64_t red64[kModelNT / 32];
-    uint32_t distinct;
+// Model-building CTA configurations: NT threads, sample capacity CAP. The
+// sample is sorted in shared memory by SmemSort (rolled loops: the former
+// register-array sorter made this kernel 52K SASS instructions and
+// instruction-fetch bound).
+template <int NT, int CAP>
+struct ModelCfg {
+    using SS = SmemSort<NT, CAP, CAP / 2>;
+    struct Smem {
+        typename SS::Smem sort;  // sort.A holds the sorted sample
+        union {
+            struct {
+                uint32_t first[LSORT_MAX_RMI_DEV + 1];
+                double lo[LSORT_MAX_RMI_DEV];
+                double hi[LSORT_MAX_RMI_DEV];
+                uint32_t big[LSORT_MAX_RMI_DEV];
+                double red[2 * (NT / 32)];
+            } rmi;
+            struct {
+                uint32_t scratch[2 * LSORT_MAX_TREE_DEV + 2];
+                uint32_t wsum[NT / 32 + 1];
+                uint64_t spl[LSORT_MAX_TREE_DEV];
+            } tree;
+        } u;
+        uint64_t red64[NT / 32];
+    };
 };
+using ModelSmall = ModelCfg<256, 2048>;
+using ModelMid = ModelCfg<512, 8192>;
+constexpr int kModelNT = 512;  // utility kernels (tree build, block sort)
 
 // Radix/fill fallback model: min/max of the whole segment (one CTA).
+template <int NT>
 __device__ void build_radix_model(const SegDesc& sd, const void* src, bool f64, ModelHdr* h, uint64_t* red) {
     uint64_t mn = ~0ull, mx = 0;
-    for (uint64_t i = threadIdx.x; i < sd.n; i += kModelNT) {
+    for (uint64_t i = threadIdx.x; i < sd.n; i += NT) {
         uint64_t k = load_key(src, sd.begin + i, f64);
         mn = k < mn ? k : mn;
         mx = k > mx ? k : mx;
     }
-    mn = block_reduce_min<kModelNT>(mn, red);
-    mx = block_reduce_max<kModelNT>(mx, red);
+    mn = block_reduce_min<NT>(mn, red);
+    mx = block_reduce_max<NT>(mx, red);
     if (threadIdx.x == 0) {
         if (mn == mx) {
             h->kind = kFill;
@@ -395,30 +404,43 @@ __device__ void build_radix_model(const SegDesc& sd, const void* src, bool f64, 
     __syncthreads();
 }
 
-// Alg. 5 build_partition_model for one segment.
-template <bool IN_F64>
+// Draw sample draws [j0, j0+cnt) of the segment stream into shared A, sort.
+template <bool IN_F64, class MC>
+__device__ void sample_sorted(const SegDesc& sd, const void* src, uint64_t seed, uint32_t j0, uint32_t cnt,
+                              typename MC::Smem& S) {
+    constexpr int NT = sizeof(S.red64) / 8 * 32;
+    for (uint32_t i = threadIdx.x; i < cnt; i += NT)
+        S.sort.A[i] = load_key(src, sd.begin + sample_index(seed, j0 + i, sd.n), IN_F64);
+    __syncthreads();
+    if (cnt > 1) MC::SS::sort(S.sort.A, cnt, S.sort);
+    __syncthreads();
+}
+
+// Alg. 5 build_partition_model for one segment. With
+// aux != nullptr (first-sample-only mode for a big segment) the learned
+// branch stops after the policy decision and builds the splitter tree that
+// partitions the big RMI sample; *gate tells the following kernels which
+// branch was taken.
+template <bool IN_F64, class MC>
 __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* models, const DevCfg& cfg,
-                                ModelSmem& S, bool first_only) {
+                                typename MC::Smem& S, bool first_only, uint8_t* aux, uint32_t aux_budget,
+                                uint32_t* gate) {
+    constexpr int NT = sizeof(S.red64) / 8 * 32;
     ModelHdr* h = (ModelHdr*)(models + sd.model_off);
     uint8_t* payload = models + sd.model_off + sizeof(ModelHdr);
     if (sd.flags & kSegForceRadix) {
-        build_radix_model(sd, src, IN_F64, h, S.red64);
+        build_radix_model<NT>(sd, src, IN_F64, h, S.red64);
+        if (gate && threadIdx.x == 0) *gate = 0;
         return;
     }
     const uint64_t n = sd.n;
     const uint64_t seed = seg_seed(cfg.seed, sd.begin, sd.depth);
     const uint32_t s1 = (uint32_t)first_sample_size(cfg, n);
-    uint64_t k[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        uint32_t idx = threadIdx.x + i * kModelNT;
-        if (idx < s1) k[i] = load_key(src, sd.begin + sample_index(seed, idx, n), IN_F64);
-    }
-    ModelSort::sort_regs(k, S.a, s1, S.u.sort);
-    __syncthreads();
+    sample_sorted<IN_F64, MC>(sd, src, seed, 0, s1, S);
+    const uint64_t* A = S.sort.A;
     uint64_t d = 0;
-    for (uint32_t i = threadIdx.x + 1; i < s1; i += kModelNT) d += S.a[i] != S.a[i - 1];
-    d = block_reduce_sum_u64<kModelNT>(d, S.red64);
+    for (uint32_t i = threadIdx.x + 1; i < s1; i += NT) d += A[i] != A[i - 1];
+    d = block_reduce_sum_u64<NT>(d, S.red64);
     const uint64_t distinct = 1 + d;
     const double dup = __dsub_rn(1.0, __ddiv_rn((double)distinct, (double)s1));  // models.cpp:187-193
     const bool learned = n >= cfg.min_rmi_input && dup <= cfg.max_dup;
@@ -428,6 +450,7 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
         h->flags = 0;
         h->cdf_lo = 0.0;
         h->inv_span = 1.0;  // Learned::inv_span() with cdf [0,1] (models.hpp:134-137)
+        if (gate) *gate = learned ? 1u : 0u;
     }
     if (learned) {
         const uint32_t s2 = (uint32_t)rmi_sample_size(cfg, n);
@@ -437,45 +460,44 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
             h->B = sd.rmi_b;
             h->s2 = s2;
         }
-        if (first_only) { __syncthreads(); return; }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            uint32_t idx = threadIdx.x + i * kModelNT;
-            if (idx < s2) k[i] = load_key(src, sd.begin + sample_index(seed, s1 + idx, n), IN_F64);
+        if (first_only) {
+            // splitter tree over the first sample: partitions the RMI sample
+            tree_build_block<NT>(A, s1, aux_budget, true, (ModelHdr*)aux, aux + sizeof(ModelHdr),
+                                 S.u.tree.scratch, S.u.tree.wsum, S.u.tree.spl);
+            return;
         }
         __syncthreads();
-        ModelSort::sort_regs(k, S.a, s2, S.u.sort);
-        __syncthreads();
-        train_rmi_block<kModelNT>(S.a, s2, sd.rmi_b, h, (RmiEntry*)payload, S.u.rmi.first, S.u.rmi.lo,
-                                  S.u.rmi.hi, S.u.rmi.big, S.u.rmi.red);
+        sample_sorted<IN_F64, MC>(sd, src, seed, s1, s2, S);
+        train_rmi_block<NT>(A, s2, sd.rmi_b, h, (RmiEntry*)payload, S.u.rmi.first, S.u.rmi.lo, S.u.rmi.hi,
+                            S.u.rmi.big, S.u.rmi.red);
     } else {
         if (threadIdx.x == 0) h->s2 = 0;
-        tree_build_block<kModelNT>(S.a, s1, sd.tree_k, true, h, payload, S.u.tree.scratch, S.u.tree.wsum,
-                                   S.u.tree.spl);
+        tree_build_block<NT>(A, s1, sd.tree_k, true, h, payload, S.u.tree.scratch, S.u.tree.wsum, S.u.tree.spl);
     }
 }
 
-template <bool IN_F64>
-__global__ void __launch_bounds__(kModelNT) k_build_models(const SegDesc* segs, const uint32_t* idx, const void* src,
-                                                          uint8_t* models, DevCfg cfg) {
+template <bool IN_F64, class MC, int NT>
+__global__ void __launch_bounds__(NT) k_build_models(const SegDesc* segs, const uint32_t* idx, const void* src,
+                                                    uint8_t* models, DevCfg cfg) {
     extern __shared__ uint4 smem_u4[];
-    ModelSmem& S = *(ModelSmem*)smem_u4;
+    typename MC::Smem& S = *(typename MC::Smem*)smem_u4;
     const SegDesc sd = segs[idx[blockIdx.x]];
-    build_model_cta<IN_F64>(sd, src, models, cfg, S, false);
+    build_model_cta<IN_F64, MC>(sd, src, models, cfg, S, false, nullptr, 0, nullptr);
 }
 
 template <bool IN_F64>
-__global__ void __launch_bounds__(kModelNT) k_first_sample(const SegDesc* seg, const void* src, uint8_t* models,
-                                                          DevCfg cfg) {
+__global__ void __launch_bounds__(512) k_first_sample(const SegDesc* seg, const void* src, uint8_t* models,
+                                                     DevCfg cfg, uint8_t* aux, uint32_t aux_budget, uint32_t* gate) {
     extern __shared__ uint4 smem_u4[];
-    ModelSmem& S = *(ModelSmem*)smem_u4;
+    ModelMid::Smem& S = *(ModelMid::Smem*)smem_u4;
     const SegDesc sd = *seg;
-    build_model_cta<IN_F64>(sd, src, models, cfg, S, true);
+    build_model_cta<IN_F64, ModelMid>(sd, src, models, cfg, S, true, aux, aux_budget, gate);
 }
 
 template <bool IN_F64>
 __global__ void k_gather(const SegDesc* seg, const void* src, uint64_t seed, uint64_t j0, uint64_t s,
-                         uint64_t* out) {
+                         uint64_t* out, const uint32_t* gate) {
+    if (gate && *gate == 0) return;
     const SegDesc sd = *seg;
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < s; j += (uint64_t)gridDim.x * blockDim.x)
         out[j] = load_key(src, sd.begin + sample_index(seed, j0 + j, sd.n), IN_F64);
@@ -483,7 +505,10 @@ __global__ void k_gather(const SegDesc* seg, const void* src, uint64_t seed, uin
 
 
 // ============================================= multi-CTA RMI training
-// Workspace layout (device): [part: 4 * nch doubles][root: 8 doubles][first: B+1 u32]
+// Over a sorted sample in global memory. Every kernel takes `gate` (nullptr
+// = always run): 0 means the segment's policy chose the splitter tree and the
+// kernel exits at once (big-segment pipeline, no host round trip).
+// Workspace layout: [part: 4 * nch doubles][root: 8 doubles][first: B+1 u32]
 constexpr int kTrainChunk = 4096;
 constexpr int kTrainNT = 256;
 
@@ -506,6 +531,7 @@ size_t train_workspace_bytes(uint64_t s, uint32_t B) {
     uint64_t nch = (s + kTrainChunk - 1) / kTrainChunk;
     return 8 * (4 * nch + 8) + 4 * ((size_t)B + 2);
 }
+__device__ __forceinline__ bool gated_off(const uint32_t* gate) { return gate && *gate == 0; }
 
 __device__ __forceinline__ void base_scale(const uint64_t* s, uint32_t n, double& base, double& scale) {
     base = __ull2double_rn(s[0]);
@@ -513,11 +539,13 @@ __device__ __forceinline__ void base_scale(const uint64_t* s, uint32_t n, double
     scale = kmax > base ? __ddiv_rn(1.0, __dsub_rn(kmax, base)) : 0.0;  // models.cpp:47-49
 }
 
-// pass 1 (pass2 = false): per-chunk sum of xn and target i/n;
-// pass 2 (pass2 = true): per-chunk centred sums (models.cpp:26-31)
+// pass 1 (PASS2 = false): per-chunk sum of xn and target i/n;
+// pass 2 (PASS2 = true): per-chunk centred sums (models.cpp:26-31)
 template <bool PASS2>
-__global__ void __launch_bounds__(kTrainNT) k_train_sums(const uint64_t* s, uint32_t n, void* wsp, uint32_t B) {
+__global__ void __launch_bounds__(kTrainNT) k_train_sums(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
+                                                        const uint32_t* gate) {
     __shared__ double red[kTrainNT / 32];
+    if (gated_off(gate)) return;
     TrainWS w = train_ws(wsp, n, B);
     double base, scale;
     base_scale(s, n, base, scale);
@@ -549,8 +577,10 @@ __global__ void __launch_bounds__(kTrainNT) k_train_sums(const uint64_t* s, uint
 
 // fixed-order reduction of the chunk partials (one CTA)
 template <bool PASS2>
-__global__ void __launch_bounds__(kTrainNT) k_train_reduce(const uint64_t* s, uint32_t n, void* wsp, uint32_t B) {
+__global__ void __launch_bounds__(kTrainNT) k_train_reduce(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
+                                                          const uint32_t* gate) {
     __shared__ double red[kTrainNT / 32];
+    if (gated_off(gate)) return;
     TrainWS w = train_ws(wsp, n, B);
     const uint32_t per = (w.nch + kTrainNT - 1) / kTrainNT;
     const uint32_t lo = min(w.nch, threadIdx.x * per), hi = min(w.nch, lo + per);
@@ -587,43 +617,81 @@ __global__ void __launch_bounds__(kTrainNT) k_train_reduce(const uint64_t* s, ui
     }
 }
 
-// slice boundaries + sequential fits of slices <= kSeqFitMax (bit-exact)
-__global__ void __launch_bounds__(kTrainNT) k_train_fits(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
-                                                        RmiEntry* E) {
+// Slice boundaries in one coalesced pass: element i (route r_i, nondecreasing
+// along the sorted sample) writes first[m] = i for every m in (r_{i-1}, r_i];
+// the last element also closes (r_last, B]. Each first[m] is written once.
+__global__ void __launch_bounds__(kTrainNT) k_train_bounds(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
+                                                          const uint32_t* gate) {
+    if (gated_off(gate)) return;
     TrainWS w = train_ws(wsp, n, B);
-    const uint32_t m = blockIdx.x * kTrainNT + threadIdx.x;
-    if (m > B) return;
     const double rs = w.root[0], ri = w.root[1], base = w.root[2], scale = w.root[3];
-    auto xn = [&](uint32_t i) { return rmi_normalize(base, scale, s[i]); };
-    auto lower = [&](uint32_t mm) -> uint32_t {  // min{i : route(xn(i)) >= mm}
-        if (mm == 0) return 0;
-        if (mm >= B) return n;
-        uint32_t a = 0, b = n;
-        while (a < b) {
-            uint32_t mid = (a + b) >> 1;
-            if (rmi_route(rs, ri, B, xn(mid)) >= mm) b = mid; else a = mid + 1;
+    for (uint32_t i = blockIdx.x * kTrainNT + threadIdx.x; i < n; i += gridDim.x * kTrainNT) {
+        const uint32_t r = rmi_route(rs, ri, B, rmi_normalize(base, scale, s[i]));
+        const uint32_t rp = i == 0 ? 0u : rmi_route(rs, ri, B, rmi_normalize(base, scale, s[i - 1])) + 1;
+        for (uint32_t m = (i == 0 ? 0u : rp); m <= r; ++m) w.first[m] = i;
+        if (i == n - 1)
+            for (uint32_t m = r + 1; m <= B; ++m) w.first[m] = n;
+    }
+}
+
+// Sequential fit_line of every slice <= kSeqFitMax samples (bit-exact, the
+// reference's summation order): one warp per submodel stages xn and the
+// targets in shared memory (parallel, coalesced), then one lane runs the
+// dependent add chains.
+constexpr int kFitWarps = 4;
+__global__ void __launch_bounds__(32 * kFitWarps) k_train_fits(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
+                                                              RmiEntry* E, const uint32_t* gate) {
+    __shared__ double xs[kFitWarps][kSeqFitMax];
+    __shared__ double ys[kFitWarps][kSeqFitMax];
+    if (gated_off(gate)) return;
+    TrainWS w = train_ws(wsp, n, B);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t m = blockIdx.x * kFitWarps + warp;
+    if (m >= B) return;
+    const uint32_t f = min(w.first[m], n), l = min(max(w.first[m + 1], f), n);
+    const uint32_t len = l - f;
+    if (len == 0 || len > (uint32_t)kSeqFitMax) return;
+    const double base = w.root[2], scale = w.root[3], nd = (double)n;
+    double* x = xs[warp];
+    double* y = ys[warp];
+    for (uint32_t j = lane; j < len; j += 32) {
+        x[j] = rmi_normalize(base, scale, s[f + j]);
+        y[j] = __ddiv_rn((double)(f + j), nd);
+    }
+    __syncwarp();
+    double sx = 0.0, sy = 0.0;
+    if (lane == 0)
+        for (uint32_t j = 0; j < len; ++j) { sx = __dadd_rn(sx, x[j]); sy = __dadd_rn(sy, y[j]); }
+    const double mx = __shfl_sync(FULL_MASK, __ddiv_rn(sx, (double)len), 0);
+    const double my = __shfl_sync(FULL_MASK, __ddiv_rn(sy, (double)len), 0);
+    for (uint32_t j = lane; j < len; j += 32) {  // products in parallel, sums in order below
+        const double dx = __dsub_rn(x[j], mx);
+        x[j] = __dmul_rn(dx, dx);
+        y[j] = __dmul_rn(dx, __dsub_rn(y[j], my));
+    }
+    __syncwarp();
+    if (lane == 0) {
+        double sxx = 0.0, sxy = 0.0;
+        for (uint32_t j = 0; j < len; ++j) { sxx = __dadd_rn(sxx, x[j]); sxy = __dadd_rn(sxy, y[j]); }
+        double sl = 0.0, ic = my;  // models.cpp:32-34
+        if (sxx > 0.0) {
+            double q = __ddiv_rn(sxy, sxx);
+            if (!(q < 0.0)) { sl = q; ic = __dsub_rn(my, __dmul_rn(q, mx)); }
         }
-        return a;
-    };
-    const uint32_t f = lower(m);
-    w.first[m] = f;
-    if (m == B) return;
-    const uint32_t l = lower(m + 1);
-    if (l - f <= (uint32_t)kSeqFitMax) {
-        Fit ft = fit_seq(xn, f, l, 0.0, (double)n);
-        E[m].slope = ft.slope;
-        E[m].intercept = ft.intercept;
+        E[m].slope = sl;
+        E[m].intercept = ic;
     }
 }
 
 // one CTA per slice larger than kSeqFitMax: deterministic block reduction
 constexpr int kBigFitNT = 512;
 __global__ void __launch_bounds__(kBigFitNT) k_train_bigfits(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
-                                                            RmiEntry* E) {
+                                                            RmiEntry* E, const uint32_t* gate) {
     __shared__ double red[kBigFitNT / 32];
+    if (gated_off(gate)) return;
     TrainWS w = train_ws(wsp, n, B);
     const uint32_t m = blockIdx.x;
-    const uint32_t f = w.first[m], l = w.first[m + 1];
+    const uint32_t f = min(w.first[m], n), l = min(max(w.first[m + 1], f), n);
     if (l - f <= (uint32_t)kSeqFitMax) return;
     const double base = w.root[2], scale = w.root[3];
     const double nd = (double)n;
@@ -657,20 +725,21 @@ __global__ void __launch_bounds__(kBigFitNT) k_train_bigfits(const uint64_t* s, 
     }
 }
 
-// enforce_monotonic (models.cpp:101-126) + header, one CTA
+// enforce_monotonic (models.cpp:101-126) + header + compiled table, one CTA
 constexpr int kEnforceNT = 1024;
 __global__ void __launch_bounds__(kEnforceNT) k_train_enforce(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
-                                                             uint8_t* model, uint32_t nbuckets) {
+                                                             uint8_t* model, uint32_t nbuckets, const uint32_t* gate) {
     extern __shared__ uint4 smem_u4[];
     double* lo = (double*)smem_u4;
     double* hi = lo + B;
     __shared__ double red[2 * (kEnforceNT / 32)];
+    if (gated_off(gate)) return;
     TrainWS w = train_ws(wsp, n, B);
     ModelHdr* h = (ModelHdr*)model;
     RmiEntry* E = (RmiEntry*)(model + sizeof(ModelHdr));
     const double base = w.root[2], scale = w.root[3];
     for (uint32_t m = threadIdx.x; m < B; m += kEnforceNT) {
-        uint32_t f = w.first[m], l = w.first[m + 1];
+        uint32_t f = min(w.first[m], n), l = min(w.first[m + 1], n);
         if (l > f) {
             double sl = E[m].slope, ic = E[m].intercept;
             lo[m] = __dadd_rn(__dmul_rn(sl, rmi_normalize(base, scale, s[f])), ic);
@@ -691,7 +760,7 @@ __global__ void __launch_bounds__(kEnforceNT) k_train_enforce(const uint64_t* s,
         hh = dclamp01(hh);
         if (m == 0) ll = 0.0;
         if (m == B - 1) hh = 1.0;
-        if (w.first[m + 1] == w.first[m]) {
+        if (min(w.first[m + 1], n) <= min(w.first[m], n)) {
             E[m].slope = 0.0;
             E[m].intercept = __dmul_rn(0.5, __dadd_rn(ll, hh));
         }
@@ -713,35 +782,32 @@ __global__ void __launch_bounds__(kEnforceNT) k_train_enforce(const uint64_t* s,
     compile_learned(model, threadIdx.x, kEnforceNT);
 }
 
-__global__ void __launch_bounds__(kModelNT) k_tree_build(const uint64_t* sorted, uint32_t s, uint32_t budget,
-                                                        int eq_mode, uint8_t* model) {
+__global__ void __launch_bounds__(512) k_tree_build(const uint64_t* sorted, uint32_t s, uint32_t budget,
+                                                   int eq_mode, uint8_t* model) {
     extern __shared__ uint4 smem_u4[];
-    ModelSmem& S = *(ModelSmem*)smem_u4;
-    for (uint32_t i = threadIdx.x; i < s; i += kModelNT) S.a[i] = sorted[i];
+    ModelMid::Smem& S = *(ModelMid::Smem*)smem_u4;
+    for (uint32_t i = threadIdx.x; i < s; i += 512) S.sort.A[i] = sorted[i];
     __syncthreads();
-    tree_build_block<kModelNT>(S.a, s, budget, eq_mode != 0, (ModelHdr*)model, model + sizeof(ModelHdr),
-                               S.u.tree.scratch, S.u.tree.wsum, S.u.tree.spl);
+    tree_build_block<512>(S.sort.A, s, budget, eq_mode != 0, (ModelHdr*)model, model + sizeof(ModelHdr),
+                          S.u.tree.scratch, S.u.tree.wsum, S.u.tree.spl);
 }
 
-__global__ void __launch_bounds__(kModelNT) k_block_sort(uint64_t* keys, uint32_t n) {
+__global__ void __launch_bounds__(512) k_block_sort(uint64_t* keys, uint32_t n) {
     extern __shared__ uint4 smem_u4[];
-    ModelSmem& S = *(ModelSmem*)smem_u4;
-    uint64_t k[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        uint32_t idx = threadIdx.x + i * kModelNT;
-        if (idx < n) k[i] = keys[idx];
-    }
-    ModelSort::sort_regs(k, S.a, n, S.u.sort);
+    ModelMid::Smem& S = *(ModelMid::Smem*)smem_u4;
+    for (uint32_t i = threadIdx.x; i < n; i += 512) S.sort.A[i] = keys[i];
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += kModelNT) keys[i] = S.a[i];
+    if (n > 1) ModelMid::SS::sort(S.sort.A, n, S.sort);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += 512) keys[i] = S.sort.A[i];
 }
 
 // ------------------------------------------------------------- launchers
-
 void models_init(int optin) {
-    allow_smem(k_build_models<true>, optin);
-    allow_smem(k_build_models<false>, optin);
+    allow_smem(k_build_models<true, ModelSmall, 256>, optin);
+    allow_smem(k_build_models<false, ModelSmall, 256>, optin);
+    allow_smem(k_build_models<true, ModelMid, 512>, optin);
+    allow_smem(k_build_models<false, ModelMid, 512>, optin);
     allow_smem(k_first_sample<true>, optin);
     allow_smem(k_first_sample<false>, optin);
     allow_smem(k_train_enforce, optin);
@@ -750,49 +816,57 @@ void models_init(int optin) {
 }
 
 void launch_build_models(const SegDesc* segs, const uint32_t* idx, uint32_t count, const void* src, int in_f64,
-                         uint8_t* models, const DevCfg& cfg, cudaStream_t st) {
+                         uint8_t* models, const DevCfg& cfg, int mid, cudaStream_t st) {
     if (!count) return;
-    size_t sm = sizeof(ModelSmem);
-    if (in_f64) k_build_models<true><<<count, kModelNT, sm, st>>>(segs, idx, src, models, cfg);
-    else k_build_models<false><<<count, kModelNT, sm, st>>>(segs, idx, src, models, cfg);
+    if (mid) {
+        size_t sm = sizeof(ModelMid::Smem);
+        if (in_f64) k_build_models<true, ModelMid, 512><<<count, 512, sm, st>>>(segs, idx, src, models, cfg);
+        else k_build_models<false, ModelMid, 512><<<count, 512, sm, st>>>(segs, idx, src, models, cfg);
+    } else {
+        size_t sm = sizeof(ModelSmall::Smem);
+        if (in_f64) k_build_models<true, ModelSmall, 256><<<count, 256, sm, st>>>(segs, idx, src, models, cfg);
+        else k_build_models<false, ModelSmall, 256><<<count, 256, sm, st>>>(segs, idx, src, models, cfg);
+    }
 }
 
 void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_t* models, const DevCfg& cfg,
-                         cudaStream_t st) {
-    size_t sm = sizeof(ModelSmem);
-    if (in_f64) k_first_sample<true><<<1, kModelNT, sm, st>>>(seg, src, models, cfg);
-    else k_first_sample<false><<<1, kModelNT, sm, st>>>(seg, src, models, cfg);
+                         uint8_t* aux, uint32_t aux_budget, uint32_t* gate, cudaStream_t st) {
+    size_t sm = sizeof(ModelMid::Smem);
+    if (in_f64) k_first_sample<true><<<1, 512, sm, st>>>(seg, src, models, cfg, aux, aux_budget, gate);
+    else k_first_sample<false><<<1, 512, sm, st>>>(seg, src, models, cfg, aux, aux_budget, gate);
 }
 
 void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0, uint64_t s,
-                   uint64_t* out, cudaStream_t st) {
+                   uint64_t* out, const uint32_t* gate, cudaStream_t st) {
     int grid = (int)std::min<uint64_t>((s + 255) / 256, (uint64_t)num_sms() * 8);
     if (grid < 1) grid = 1;
-    if (in_f64) k_gather<true><<<grid, 256, 0, st>>>(seg, src, seed, j0, s, out);
-    else k_gather<false><<<grid, 256, 0, st>>>(seg, src, seed, j0, s, out);
+    if (in_f64) k_gather<true><<<grid, 256, 0, st>>>(seg, src, seed, j0, s, out, gate);
+    else k_gather<false><<<grid, 256, 0, st>>>(seg, src, seed, j0, s, out, gate);
 }
 
 void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* model, uint32_t nbuckets, void* ws,
-                      cudaStream_t st) {
+                      const uint32_t* gate, cudaStream_t st) {
     const uint32_t n = (uint32_t)s;
     const uint32_t nch = (uint32_t)((s + kTrainChunk - 1) / kTrainChunk);
     RmiEntry* E = (RmiEntry*)(model + sizeof(ModelHdr));
-    k_train_sums<false><<<nch, kTrainNT, 0, st>>>(sample, n, ws, B);
-    k_train_reduce<false><<<1, kTrainNT, 0, st>>>(sample, n, ws, B);
-    k_train_sums<true><<<nch, kTrainNT, 0, st>>>(sample, n, ws, B);
-    k_train_reduce<true><<<1, kTrainNT, 0, st>>>(sample, n, ws, B);
-    k_train_fits<<<(B + 1 + kTrainNT - 1) / kTrainNT, kTrainNT, 0, st>>>(sample, n, ws, B, E);
-    k_train_bigfits<<<B, kBigFitNT, 0, st>>>(sample, n, ws, B, E);
-    k_train_enforce<<<1, kEnforceNT, 16 * (size_t)B, st>>>(sample, n, ws, B, model, nbuckets);
+    k_train_sums<false><<<nch, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
+    k_train_reduce<false><<<1, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
+    k_train_sums<true><<<nch, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
+    k_train_reduce<true><<<1, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
+    const int gb = (int)std::min<uint64_t>((s + kTrainNT - 1) / kTrainNT, (uint64_t)num_sms() * 8);
+    k_train_bounds<<<gb, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
+    k_train_fits<<<(B + kFitWarps - 1) / kFitWarps, 32 * kFitWarps, 0, st>>>(sample, n, ws, B, E, gate);
+    k_train_bigfits<<<B, kBigFitNT, 0, st>>>(sample, n, ws, B, E, gate);
+    k_train_enforce<<<1, kEnforceNT, 16 * (size_t)B, st>>>(sample, n, ws, B, model, nbuckets, gate);
 }
 
 void launch_tree_build(const uint64_t* sorted, uint64_t s, uint32_t budget, int eq_mode, uint8_t* model,
                        cudaStream_t st) {
-    k_tree_build<<<1, kModelNT, sizeof(ModelSmem), st>>>(sorted, (uint32_t)s, budget, eq_mode, model);
+    k_tree_build<<<1, 512, sizeof(ModelMid::Smem), st>>>(sorted, (uint32_t)s, budget, eq_mode, model);
 }
 
 void launch_block_sort(uint64_t* keys, uint64_t n, cudaStream_t st) {
-    k_block_sort<<<1, kModelNT, sizeof(ModelSmem), st>>>(keys, (uint32_t)n);
+    k_block_sort<<<1, 512, sizeof(ModelMid::Smem), st>>>(keys, (uint32_t)n);
 }
 
 }  // namespace lsort_dev

@@ -34,6 +34,10 @@ __device__ __forceinline__ uint32_t kind_slot(uint32_t kind) {
 // ------------------------------------------------------------ kind plan
 constexpr int kPlanNT = 1024;
 __global__ void __launch_bounds__(kPlanNT) k_kind_plan(LevelParams p) {
+    if (p.gate && *p.gate == 0) {
+        if (threadIdx.x < 3) { p.kplan[threadIdx.x].nsegs = 0; p.kplan[threadIdx.x].ntiles = 0; }
+        return;
+    }
     __shared__ uint32_t wsum[kPlanNT / 32 + 1];
     __shared__ uint64_t wsum64[kPlanNT / 32 + 1];
     __shared__ uint32_t fl[kPlanNT];
@@ -249,6 +253,7 @@ __global__ void __launch_bounds__(kScanNT) k_scan_children(LevelParams p) {
     __shared__ uint64_t eqval[kMaxNB];
     extern __shared__ uint64_t cnt[];
     if (p.ctrl->nan_index != ~0ull) return;
+    if (p.gate && *p.gate == 0) return;
     const SegDesc sd = p.segs[blockIdx.x];
     const uint8_t* mg = p.models + sd.model_off;
     const ModelHdr h = *(const ModelHdr*)mg;
