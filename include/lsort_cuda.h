@@ -158,7 +158,7 @@ int lsort_cuda_build_model(lsort_ctx* ctx, const void* d_keys, uint64_t n, int k
                            const lsort_cfg* cfg, lsort_model_info* info,
                            lsort_rmi_header* h_out, lsort_rmi_entry* entries_out,
                            lsort_tree* tree_out);
-/* Device sort of a small device sample (the shared-memory block sort). */
+/* Device sort of a small device sample (the shared-memory block sort), n <= 8192. */
 int lsort_cuda_block_sort(lsort_ctx* ctx, uint64_t* d_keys, uint64_t n);
 /* verify_sorted + multiset_hash on device keys (F64 keys hashed encoded). */
 int lsort_cuda_verify(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,

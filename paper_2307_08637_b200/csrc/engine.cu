@@ -876,7 +876,7 @@ int lsort_cuda_build_model(lsort_ctx* C, const void* d_keys, uint64_t n, int key
 
 int lsort_cuda_block_sort(lsort_ctx* C, uint64_t* d_keys, uint64_t n) {
     if (!C) return LSORT_EINVAL;
-    if (n > 16384) return fail(C, {LSORT_EINVAL, "block sort holds at most 16384 keys"});
+    if (n > kSmallSampleCap) return fail(C, {LSORT_EINVAL, "block sort holds at most 8192 keys"});
     try {
         CU(cudaSetDevice(C->device));
         if (n > 1) launch_block_sort(d_keys, n, C->stream);

@@ -51,7 +51,12 @@ def route_defined(P, B, keys):
 
 
 # ------------------------------------------------------------ block sort
-@pytest.mark.parametrize("n", [2, 3, 17, 100, 1000, 4096, 8191, 16384])
+def test_block_sort_limit(ctx):
+    with pytest.raises(ValueError):
+        ctx.block_sort(dev(np.arange(8193, dtype=np.uint64)))
+
+
+@pytest.mark.parametrize("n", [2, 3, 17, 100, 1000, 4096, 8191, 8192])
 def test_block_sort(ctx, n):
     rng = np.random.default_rng(n)
     for a in [rng.integers(0, 2**64 - 1, n, dtype=np.uint64, endpoint=True),
