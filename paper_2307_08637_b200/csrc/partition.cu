@@ -159,6 +159,36 @@ struct KindTiles {
     }
 };
 
+// Classify the 16 keys a thread holds (8 pairs). Trees descend in lockstep
+// (16 independent shared-memory loads in flight per level instead of one
+// dependent chain per key); learned/radix keys are straight-line code.
+template <uint32_t KIND>
+__device__ __forceinline__ void classify16(const KState& S, const ulonglong2 (&v)[kPPairs], uint32_t (&c)[kPItems]) {
+    if constexpr (KIND == kTree) {
+        uint32_t idx[kPItems];
+#pragma unroll
+        for (int q = 0; q < kPItems; ++q) idx[q] = 1;
+        for (uint32_t l = 0; l < S.levels; ++l) {
+#pragma unroll
+            for (int q = 0; q < kPItems; ++q) {
+                const uint64_t x = (q & 1) ? v[q >> 1].y : v[q >> 1].x;
+                idx[q] = 2 * idx[q] + (x > S.tree[idx[q]] ? 1u : 0u);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kPItems; ++q) {
+            const uint64_t x = (q & 1) ? v[q >> 1].y : v[q >> 1].x;
+            const uint32_t base = idx[q] - S.leaf;
+            const uint32_t e0 = S.eqo[base];
+            const uint32_t eq = (base < S.nsplit) && (S.eqo[base + 1] - e0 > 1) && (x == S.spl[base]);
+            c[q] = (e0 + eq) | (eq << 31);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kPItems; ++q) c[q] = kclassify<KIND>(S, (q & 1) ? v[q >> 1].y : v[q >> 1].x);
+    }
+}
+
 // ------------------------------------------------------- classify + hist
 template <bool IN_F64, uint32_t KIND>
 __global__ void __launch_bounds__(kPNT, 3) k_hist(LevelParams p) {
@@ -206,27 +236,27 @@ __global__ void __launch_bounds__(kPNT, 3) k_hist(LevelParams p) {
         for (int j = 0; j < kPPairs; ++j) {
             uint32_t q = threadIdx.x + j * kPNT;
             if (q < g.npairs) v[j] = __ldcs(sp + q);
+            else v[j] = make_ulonglong2(0, 0);
         }
+        if (IN_F64) {
 #pragma unroll
-        for (int j = 0; j < kPPairs; ++j) {
-            uint32_t q = threadIdx.x + j * kPNT;
-            bool ok = q < g.npairs;
-            uint64_t k0 = v[j].x, k1 = v[j].y;
-            if (IN_F64) {
-                if (ok) {
-                    if (isnan(__longlong_as_double((long long)k0)))
+            for (int j = 0; j < kPPairs; ++j) {
+                uint32_t q = threadIdx.x + j * kPNT;
+                if (q < g.npairs) {
+                    if (isnan(__longlong_as_double((long long)v[j].x)))
                         atomicMin(&p.ctrl->nan_index, (unsigned long long)(g.a0 + 2 * q));
-                    if (isnan(__longlong_as_double((long long)k1)))
+                    if (isnan(__longlong_as_double((long long)v[j].y)))
                         atomicMin(&p.ctrl->nan_index, (unsigned long long)(g.a0 + 2 * q + 1));
                 }
-                k0 = encode(__longlong_as_double((long long)k0));
-                k1 = encode(__longlong_as_double((long long)k1));
+                v[j].x = encode(__longlong_as_double((long long)v[j].x));
+                v[j].y = encode(__longlong_as_double((long long)v[j].y));
             }
-            uint32_t b0 = ok ? kclassify<KIND>(S, k0) : 0;
-            uint32_t b1 = ok ? kclassify<KIND>(S, k1) : 0;
-            hist_add(hist, b0 & 0x7fffffffu, ok);
-            hist_add(hist, b1 & 0x7fffffffu, ok);
         }
+        uint32_t code[kPItems];
+        classify16<KIND>(S, v, code);
+#pragma unroll
+        for (int q = 0; q < kPItems; ++q)
+            hist_add(hist, code[q] & 0x7fffffffu, threadIdx.x + (q >> 1) * kPNT < g.npairs);
         if (threadIdx.x < g.nsingle) {
             uint64_t ix = g.single[threadIdx.x];
             uint64_t k = ((const uint64_t*)p.src)[ix];
@@ -357,24 +387,23 @@ __global__ void __launch_bounds__(kPNT, 3) k_scatter(LevelParams p, uint32_t nb_
         for (int j = 0; j < kPPairs; ++j) {
             uint32_t qq = threadIdx.x + j * kPNT;
             if (qq < g.npairs) v[j] = __ldcs(sp + qq);
+            else v[j] = make_ulonglong2(0, 0);
         }
+        if (IN_F64) {
 #pragma unroll
-        for (int j = 0; j < kPPairs; ++j) {
-            uint32_t qq = threadIdx.x + j * kPNT;
-            bool ok = qq < g.npairs;
-            if (IN_F64) {
+            for (int j = 0; j < kPPairs; ++j) {
                 v[j].x = encode(__longlong_as_double((long long)v[j].x));
                 v[j].y = encode(__longlong_as_double((long long)v[j].y));
             }
-            uint32_t c0 = ok ? kclassify<KIND>(S, v[j].x) : (1u << 31);
-            uint32_t c1 = ok ? kclassify<KIND>(S, v[j].y) : (1u << 31);
-            bool ok0 = !(c0 >> 31), ok1 = !(c1 >> 31);
-            uint32_t b0 = c0 & 0x7fffffffu, b1 = c1 & 0x7fffffffu;
-            if (MAPPED) { if (ok0) b0 = map[b0]; if (ok1) b1 = map[b1]; }
-            uint32_t r0 = hist_rank_warp(cnt, b0, ok0);
-            uint32_t r1 = hist_rank_warp(cnt, b1, ok1);
-            code[2 * j] = ok0 ? (b0 << 16 | r0) : 0xffffffffu;
-            code[2 * j + 1] = ok1 ? (b1 << 16 | r1) : 0xffffffffu;
+        }
+        classify16<KIND>(S, v, code);
+#pragma unroll
+        for (int q = 0; q < kPItems; ++q) {
+            const bool ok = threadIdx.x + (q >> 1) * kPNT < g.npairs && !(code[q] >> 31);
+            uint32_t b = code[q] & 0x7fffffffu;
+            if (MAPPED && ok) b = map[b];
+            const uint32_t r = hist_rank_warp(cnt, b, ok);
+            code[q] = ok ? (b << 16 | r) : 0xffffffffu;
         }
         uint64_t skey = 0;
         uint32_t scode = 0xffffffffu;
@@ -392,9 +421,23 @@ __global__ void __launch_bounds__(kPNT, 3) k_scatter(LevelParams p, uint32_t nb_
         const uint32_t total = block_exclusive_scan_u32<kPNT>(cnt, nbo, wsum);
         if (threadIdx.x == 0) cnt[nbo] = total;
         __syncthreads();
-        for (uint32_t b = threadIdx.x; b < nbo; b += kPNT) {
-            uint32_t c = cnt[b + 1] - cnt[b];
-            if (c) delta[b] = (long long)atomicAdd(&p.buckets[boff + b], (unsigned long long)c) - (long long)cnt[b];
+        {  // claim one output range per non-empty bucket: all atomics in flight
+            constexpr int kCl = (kMaxNB + kPNT - 1) / kPNT;
+            unsigned long long got[kCl];
+#pragma unroll
+            for (int q = 0; q < kCl; ++q) {
+                const uint32_t b = threadIdx.x + q * kPNT;
+                got[q] = 0;
+                if (b < nbo) {
+                    const uint32_t c = cnt[b + 1] - cnt[b];
+                    if (c) got[q] = atomicAdd(&p.buckets[boff + b], (unsigned long long)c);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kCl; ++q) {
+                const uint32_t b = threadIdx.x + q * kPNT;
+                if (b < nbo) delta[b] = (long long)got[q] - (long long)cnt[b];
+            }
         }
 #pragma unroll
         for (int j = 0; j < kPItems; ++j) {
@@ -411,9 +454,10 @@ __global__ void __launch_bounds__(kPNT, 3) k_scatter(LevelParams p, uint32_t nb_
             sbid[pos] = (uint16_t)(scode >> 16);
         }
         __syncthreads();
-        for (uint32_t j = threadIdx.x; j < total; j += kPNT) {
-            uint32_t b = sbid[j];
-            p.dst[(long long)j + delta[b]] = skeys[j];
+#pragma unroll
+        for (int q = 0; q < kTileKeys / kPNT; ++q) {  // unrolled: loads of all 16 rows in flight
+            const uint32_t j = threadIdx.x + q * kPNT;
+            if (j < total) p.dst[(long long)j + delta[sbid[j]]] = skeys[j];
         }
         for (uint32_t b = threadIdx.x; b <= nbo; b += kPNT) cnt[b] = 0;
         __syncthreads();
