@@ -430,7 +430,7 @@ struct Engine {
             // ---- partition
             const int nsm = num_sms();
             int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 3);
-            int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 3);
+            int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
             const int nk = __builtin_popcount(kinds);
             mark(1);
             launch_kind_plan(p, st);

@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "kernels_common.cuh"
+#include "tma.cuh"
 
 namespace lsort_dev {
 
@@ -189,12 +190,55 @@ __device__ __forceinline__ void classify16(const KState& S, const ulonglong2 (&v
     }
 }
 
+// Tile t of a kind list: its segment (index into the kind list) and geometry.
+template <uint32_t KIND>
+__device__ __forceinline__ TileGeom tile_geom(const LevelParams& p, const KindTiles<KIND>& KT, uint64_t t,
+                                              uint32_t& i) {
+    i = find_seg(KT.tp, KT.nks, t);
+    const SegDesc& sd = p.segs[KT.ks[i]];
+    const uint64_t lo = sd.begin + (t - KT.tp[i]) * (uint64_t)kTileKeys;
+    TileGeom g;
+    g.init(p.src, lo, min(lo + kTileKeys, sd.begin + sd.n));
+    return g;
+}
+
+// Double-buffered TMA tile stream: the 16-byte aligned interior of tile t is
+// bulk-copied (cp.async.bulk + mbarrier) into shared buffer (t - t0) & 1
+// while the previous tile is processed; head/tail singles are read directly.
+struct TileStream {
+    ulonglong2* buf[2];
+    uint64_t* bar;  // 2 mbarriers
+    __device__ __forceinline__ void init(uint8_t* base, uint64_t* bars) {
+        buf[0] = (ulonglong2*)base;
+        buf[1] = (ulonglong2*)(base + 8 * (size_t)kTileKeys);
+        bar = bars;
+        if (threadIdx.x == 0) {
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
+        }
+        __syncthreads();
+    }
+    __device__ __forceinline__ void issue(const void* src, const TileGeom& g, int b) {
+        if (threadIdx.x == 0 && g.npairs) {
+            mbar_expect_tx(&bar[b], g.npairs * 16);
+            tma_load_1d(buf[b], (const uint64_t*)src + g.a0, g.npairs * 16, &bar[b]);
+        }
+    }
+    __device__ __forceinline__ void wait(const TileGeom& g, int b, uint32_t use) {
+        if (g.npairs) mbar_wait(&bar[b], use & 1);
+    }
+};
+constexpr size_t kTileBytes = 8 * (size_t)kTileKeys;
+
 // ------------------------------------------------------- classify + hist
 template <bool IN_F64, uint32_t KIND>
 __global__ void __launch_bounds__(kPNT, 3) k_hist(LevelParams p) {
     extern __shared__ uint4 smem_u4[];
-    uint32_t* hist = (uint32_t*)smem_u4;                    // kMaxNB
-    uint8_t* tree_smem = (uint8_t*)(hist + kMaxNB);         // tree payload
+    uint8_t* sm = (uint8_t*)smem_u4;
+    uint64_t* bars = (uint64_t*)sm;                          // 2 mbarriers (16 B)
+    uint32_t* hist = (uint32_t*)(sm + 16);                   // kMaxNB
+    uint8_t* tiles = sm + 16 + 4 * kMaxNB;                   // 2 x kTileBytes
+    uint8_t* tree_smem = tiles + 2 * kTileBytes;             // tree payload
     if (!IN_F64 && p.ctrl->nan_index != ~0ull) return;
     KindTiles<KIND> KT;
     KT.init(p);
@@ -204,39 +248,43 @@ __global__ void __launch_bounds__(kPNT, 3) k_hist(LevelParams p) {
     const uint64_t t1 = min(t0 + per, KT.ntiles);
     if (t0 >= t1) return;
     for (uint32_t b = threadIdx.x; b < kMaxNB; b += kPNT) hist[b] = 0;
+    TileStream TS;
+    TS.init(tiles, bars);
+    uint32_t inext;
+    TileGeom gnext = tile_geom<KIND>(p, KT, t0, inext);
+    TS.issue(p.src, gnext, 0);
     int64_t cur = -1;
     KState S;
-    uint64_t boff = 0, sbeg = 0, send = 0, stile0 = 0;
+    uint64_t boff = 0;
     for (uint64_t tile = t0; tile < t1; ++tile) {
-        uint32_t i = find_seg(KT.tp, KT.nks, tile);
+        const int b = (int)((tile - t0) & 1);
+        const uint32_t i = inext;
+        const TileGeom g = gnext;
+        if (tile + 1 < t1) {  // prefetch the next tile into the other buffer
+            gnext = tile_geom<KIND>(p, KT, tile + 1, inext);
+            TS.issue(p.src, gnext, b ^ 1);
+        }
         if ((int64_t)i != cur) {
             if (cur >= 0) {
                 __syncthreads();
-                for (uint32_t b = threadIdx.x; b < S.nb; b += kPNT) {
-                    uint32_t c = hist[b];
-                    if (c) { atomicAdd(&p.buckets[boff + b], (unsigned long long)c); hist[b] = 0; }
+                for (uint32_t q = threadIdx.x; q < S.nb; q += kPNT) {
+                    uint32_t c = hist[q];
+                    if (c) { atomicAdd(&p.buckets[boff + q], (unsigned long long)c); hist[q] = 0; }
                 }
             }
             const SegDesc& sd = p.segs[KT.ks[i]];
             boff = sd.bucket_off;
-            sbeg = sd.begin;
-            send = sd.begin + sd.n;
-            stile0 = KT.tp[i];
             kstate_load<KIND>(S, p.models + sd.model_off, tree_smem);
             __syncthreads();
             cur = i;
         }
-        const uint64_t lo = sbeg + (tile - stile0) * (uint64_t)kTileKeys;
-        const uint64_t hi = min(lo + kTileKeys, send);
-        TileGeom g;
-        g.init(p.src, lo, hi);
-        const ulonglong2* sp = (const ulonglong2*)((const uint64_t*)p.src + g.a0);
+        TS.wait(g, b, (uint32_t)((tile - t0) >> 1));
+        const ulonglong2* sp = TS.buf[b];
         ulonglong2 v[kPPairs];
 #pragma unroll
         for (int j = 0; j < kPPairs; ++j) {
             uint32_t q = threadIdx.x + j * kPNT;
-            if (q < g.npairs) v[j] = __ldcs(sp + q);
-            else v[j] = make_ulonglong2(0, 0);
+            v[j] = q < g.npairs ? sp[q] : make_ulonglong2(0, 0);
         }
         if (IN_F64) {
 #pragma unroll
@@ -267,11 +315,11 @@ __global__ void __launch_bounds__(kPNT, 3) k_hist(LevelParams p) {
             }
             atomicAdd(&hist[kclassify<KIND>(S, k) & 0x7fffffffu], 1u);
         }
+        __syncthreads();  // buffer b is free for the tile after next
     }
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < S.nb; b += kPNT) {
-        uint32_t c = hist[b];
-        if (c) atomicAdd(&p.buckets[boff + b], (unsigned long long)c);
+    for (uint32_t q = threadIdx.x; q < S.nb; q += kPNT) {
+        uint32_t c = hist[q];
+        if (c) atomicAdd(&p.buckets[boff + q], (unsigned long long)c);
     }
 }
 
@@ -338,12 +386,13 @@ __global__ void __launch_bounds__(kScanNT) k_scan_children(LevelParams p) {
 
 // ---------------------------------------------------------------- scatter
 template <bool IN_F64, bool MAPPED, uint32_t KIND>
-__global__ void __launch_bounds__(kPNT, 3) k_scatter(LevelParams p, uint32_t nb_cap, const uint32_t* map,
+__global__ void __launch_bounds__(kPNT, 2) k_scatter(LevelParams p, uint32_t nb_cap, const uint32_t* map,
                                                  uint32_t nmapped) {
     extern __shared__ uint4 smem_u4[];
     uint8_t* q = (uint8_t*)smem_u4;
+    uint64_t* bars = (uint64_t*)q; q += 16;
+    uint8_t* tiles = q; q += 2 * kTileBytes;              // TMA tile buffers; the consumed one stages
     long long* delta = (long long*)q; q += 8 * (size_t)nb_cap;
-    uint64_t* skeys = (uint64_t*)q; q += 8 * (size_t)kTileKeys;
     uint32_t* cnt = (uint32_t*)q; q += 4 * (size_t)(nb_cap + 1);
     q = (uint8_t*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
     uint32_t* wsum = (uint32_t*)q; q += 4 * (kPNT / 32 + 1);
@@ -359,35 +408,40 @@ __global__ void __launch_bounds__(kPNT, 3) k_scatter(LevelParams p, uint32_t nb_
     const uint64_t t1 = min(t0 + per, KT.ntiles);
     if (t0 >= t1) return;
     for (uint32_t b = threadIdx.x; b <= nb_cap; b += kPNT) cnt[b] = 0;
+    TileStream TS;
+    TS.init(tiles, bars);
+    uint32_t inext;
+    TileGeom gnext = tile_geom<KIND>(p, KT, t0, inext);
+    TS.issue(p.src, gnext, 0);
     int64_t cur = -1;
     KState S;
-    uint64_t boff = 0, sbeg = 0, send = 0, stile0 = 0;
+    uint64_t boff = 0;
     uint32_t nbo = 0;
     for (uint64_t tile = t0; tile < t1; ++tile) {
-        uint32_t i = find_seg(KT.tp, KT.nks, tile);
+        const int tb = (int)((tile - t0) & 1);
+        const uint32_t i = inext;
+        const TileGeom g = gnext;
+        if (tile + 1 < t1) {
+            gnext = tile_geom<KIND>(p, KT, tile + 1, inext);
+            TS.issue(p.src, gnext, tb ^ 1);
+        }
         if ((int64_t)i != cur) {
             const SegDesc& sd = p.segs[KT.ks[i]];
             boff = sd.bucket_off;
-            sbeg = sd.begin;
-            send = sd.begin + sd.n;
-            stile0 = KT.tp[i];
             kstate_load<KIND>(S, p.models + sd.model_off, tree_smem);
             nbo = MAPPED ? nmapped : S.nb;
             __syncthreads();
             cur = i;
         }
-        const uint64_t lo = sbeg + (tile - stile0) * (uint64_t)kTileKeys;
-        const uint64_t hi = min(lo + kTileKeys, send);
-        TileGeom g;
-        g.init(p.src, lo, hi);
-        const ulonglong2* sp = (const ulonglong2*)((const uint64_t*)p.src + g.a0);
+        TS.wait(g, tb, (uint32_t)((tile - t0) >> 1));
+        const ulonglong2* sp = TS.buf[tb];
+        uint64_t* skeys = (uint64_t*)TS.buf[tb];  // staging reuses the consumed tile buffer
         ulonglong2 v[kPPairs];
         uint32_t code[kPItems];  // bucket << 16 | rank; ~0 = not moved
 #pragma unroll
         for (int j = 0; j < kPPairs; ++j) {
             uint32_t qq = threadIdx.x + j * kPNT;
-            if (qq < g.npairs) v[j] = __ldcs(sp + qq);
-            else v[j] = make_ulonglong2(0, 0);
+            v[j] = qq < g.npairs ? sp[qq] : make_ulonglong2(0, 0);
         }
         if (IN_F64) {
 #pragma unroll
@@ -466,9 +520,8 @@ __global__ void __launch_bounds__(kPNT, 3) k_scatter(LevelParams p, uint32_t nb_
 
 // ------------------------------------------------------------- launchers
 static size_t scatter_smem(uint32_t nb_cap, uint32_t tree_cap) {
-    size_t s = 8 * (size_t)nb_cap + 8 * (size_t)kTileKeys + 4 * (size_t)(nb_cap + 1) + 16 + 4 * (kPNT / 32 + 1) +
-               16 + 2 * (size_t)kTileKeys + 16 + tree_cap;
-    return s;
+    return 16 + 2 * kTileBytes + 8 * (size_t)nb_cap + 4 * (size_t)(nb_cap + 1) + 16 + 4 * (kPNT / 32 + 1) + 16 +
+           2 * (size_t)kTileKeys + 16 + tree_cap;
 }
 static const uint32_t kTreeCap = (uint32_t)((tree_payload_bytes(LSORT_MAX_TREE_DEV, LSORT_MAX_TREE_DEV - 1) + 15) & ~15ull);
 
@@ -495,14 +548,15 @@ void launch_kind_plan(const LevelParams& p, cudaStream_t st) {
 }
 
 void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, int grid, cudaStream_t st) {
-    size_t sm_l = 4 * (size_t)kMaxNB, sm_t = sm_l + kTreeCap;
+    size_t sm_l = 16 + 4 * (size_t)kMaxNB + 2 * kTileBytes, sm_t = sm_l + kTreeCap;
     if (kinds & 1) {
         if (in_f64) k_hist<true, kLearned><<<grid, kPNT, sm_l, st>>>(p);
         else k_hist<false, kLearned><<<grid, kPNT, sm_l, st>>>(p);
     }
-    if (kinds & 2) {
-        if (in_f64) k_hist<true, kTree><<<grid, kPNT, sm_t, st>>>(p);
-        else k_hist<false, kTree><<<grid, kPNT, sm_t, st>>>(p);
+    if (kinds & 2) {  // tree payload in shared memory: two CTAs per SM
+        const int gt = std::max(1, grid * 2 / 3);
+        if (in_f64) k_hist<true, kTree><<<gt, kPNT, sm_t, st>>>(p);
+        else k_hist<false, kTree><<<gt, kPNT, sm_t, st>>>(p);
     }
     if (kinds & 4) {
         if (in_f64) k_hist<true, kRadix><<<grid, kPNT, sm_l, st>>>(p);
