@@ -289,9 +289,9 @@ struct Engine {
         const int nsm = num_sms();
         const int g = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 3);
         launch_kind_plan(q, st);
-        launch_hist(q, 0, 2u, g, st);
+        launch_hist(q, 0, 2u, 0, g, st);
         launch_scan_children(q, st);
-        launch_scatter(q, 0, 2u, nb, g, st);
+        launch_scatter(q, 0, 2u, nb, 0, g, st);
         launch_base_cases(q, N->scratch.as<uint64_t>(), C->sample.p, 0, st);
         launch_fill(q, C->sample.p, 0, nsm, st);
         launch_train_rmi(C->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
@@ -337,7 +337,7 @@ struct Engine {
             uint64_t* hp = C->hprefix.as<uint64_t>();
             uint32_t* hi = C->hidx.as<uint32_t>();
             uint64_t model_bytes = 0, nbuckets = 0, ntiles = 0;
-            uint32_t max_payload = 0, max_nb = 0, nsmall = 0, kinds = 0;
+            uint32_t max_payload = 0, max_nb = 0, nsmall = 0, kinds = 0, max_rmi_b = 0;
             std::vector<uint32_t> mids;
             std::vector<uint32_t> bigs;
             for (uint32_t i = 0; i < ns; ++i) {
@@ -348,6 +348,7 @@ struct Engine {
                 d.depth = s.depth;
                 d.flags = s.flags;
                 d.rmi_b = rmi_b(s.n);
+                max_rmi_b = std::max(max_rmi_b, d.rmi_b);
                 d.tree_k = tree_k(s.n);
                 uint32_t payload, nb;
                 if (s.flags & kSegForceRadix) {
@@ -434,10 +435,10 @@ struct Engine {
             const int nk = __builtin_popcount(kinds);
             mark(1);
             launch_kind_plan(p, st);
-            launch_hist(p, src_f64, kinds, grid_h, st);
+            launch_hist(p, src_f64, kinds, max_rmi_b, grid_h, st);
             launch_scan_children(p, st);
             mark(2);
-            launch_scatter(p, src_f64, kinds, max_nb, grid_s, st);
+            launch_scatter(p, src_f64, kinds, max_nb, max_rmi_b, grid_s, st);
             mark(3);
             launch_base_cases(p, dst, keys, f64, st);
             mark(4);
@@ -1040,7 +1041,7 @@ int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int 
         p.kplan = C->kplan.as<KindPlan>();
         p.kstride = 1;
         int grid = (int)std::min<uint64_t>(pref[1], (uint64_t)num_sms() * 3);
-        launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, grid, C->stream);
+        launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, B, grid, C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
     } catch (const LsortError& er) {

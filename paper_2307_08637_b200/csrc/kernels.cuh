@@ -108,11 +108,12 @@ void launch_tree_build(const uint64_t* sorted, uint64_t s, uint32_t budget, int 
 void launch_block_sort(uint64_t* keys, uint64_t n, cudaStream_t st);
 // partition.cu
 void launch_kind_plan(const LevelParams& p, cudaStream_t st);
-void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, int grid, cudaStream_t st);
+void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_rmi_b, int grid, cudaStream_t st);
 void launch_scan_children(const LevelParams& p, cudaStream_t st);
-void launch_scatter(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t nb_cap, int grid, cudaStream_t st);
-void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,
-                           cudaStream_t st);
+void launch_scatter(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t nb_cap, uint32_t max_rmi_b, int grid,
+                    cudaStream_t st);
+void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, uint32_t rmi_b,
+                           int grid, cudaStream_t st);
 // basecase.cu
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
 void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st);

@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(kPlanNT) k_kind_plan(LevelParams p) {
 struct KState {
     // learned
     double rs, ri, base, scale, cdf_lo, inv_span;
-    const RmiBucketEntry* E;
+    const double2* line;      // shared: {slope, intercept} per submodel
+    const uint32_t* gbounds;  // shared: g(lo) | g(hi) << 16 per submodel
     uint32_t B, nb, identity;
     // tree (shared memory)
     const uint64_t* tree;
@@ -104,10 +105,23 @@ __device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t
     const ModelHdr* h = (const ModelHdr*)g;
     S.nb = h->nbuckets;
     if constexpr (KIND == kLearned) {
+        // compiled table -> shared memory (20 B per submodel): the L1 cannot be
+        // relied on once the TMA tile buffers take most of the SM's shared memory
         S.rs = h->root_slope; S.ri = h->root_icpt; S.base = h->key_base; S.scale = h->key_scale;
         S.cdf_lo = h->cdf_lo; S.inv_span = h->inv_span; S.B = h->B;
         S.identity = h->flags & kModelIdentityCdf;
-        S.E = (const RmiBucketEntry*)(g + sizeof(ModelHdr) + sizeof(RmiEntry) * (size_t)S.B);
+        const RmiBucketEntry* E = (const RmiBucketEntry*)(g + sizeof(ModelHdr) + sizeof(RmiEntry) * (size_t)S.B);
+        double2* line = (double2*)tree_smem;
+        uint32_t* gbounds = (uint32_t*)(line + S.B);
+        __syncthreads();  // previous users of the table are done
+        for (uint32_t m = threadIdx.x; m < S.B; m += blockDim.x) {
+            const RmiBucketEntry e = E[m];
+            line[m] = make_double2(e.slope, e.intercept);
+            gbounds[m] = e.glo | (e.ghi << 16);
+        }
+        S.line = line;
+        S.gbounds = gbounds;
+        __syncthreads();
     } else if constexpr (KIND == kTree) {
         S.levels = h->levels; S.leaf = h->leaf_origin; S.nsplit = h->nsplit;
         uint32_t words = (uint32_t)((tree_payload_bytes(S.leaf, S.nsplit) + 15) / 16);
@@ -129,13 +143,13 @@ __device__ __forceinline__ uint32_t kclassify(const KState& S, uint64_t x) {
     if constexpr (KIND == kLearned) {
         // models.hpp:34-43,56-65,162-171 via the compiled table (RmiBucketEntry)
         const double xn = rmi_normalize(S.base, S.scale, x);
-        const RmiBucketEntry* ep = S.E + rmi_route(S.rs, S.ri, S.B, xn);
-        const double2 li = __ldg((const double2*)ep);
-        const uint2 gb = __ldg((const uint2*)ep + 2);
+        const uint32_t m = rmi_route(S.rs, S.ri, S.B, xn);
+        const double2 li = S.line[m];
+        const uint32_t gb = S.gbounds[m];
         const double v = __dadd_rn(__dmul_rn(li.x, xn), li.y);
         const double t = S.identity ? __dmul_rn(v, (double)S.nb)
                                     : __dmul_rn(__dmul_rn(__dsub_rn(v, S.cdf_lo), S.inv_span), (double)S.nb);
-        return min(max(min(__double2uint_rz(t), S.nb - 1), gb.x), gb.y);
+        return min(max(min(__double2uint_rz(t), S.nb - 1), gb & 0xffffu), gb >> 16);
     } else if constexpr (KIND == kTree) {
         return tree_bucket(S.levels, S.leaf, S.nsplit, S.tree, S.spl, S.eqo, x);
     } else {
@@ -524,6 +538,7 @@ static size_t scatter_smem(uint32_t nb_cap, uint32_t tree_cap) {
            2 * (size_t)kTileKeys + 16 + tree_cap;
 }
 static const uint32_t kTreeCap = (uint32_t)((tree_payload_bytes(LSORT_MAX_TREE_DEV, LSORT_MAX_TREE_DEV - 1) + 15) & ~15ull);
+static const uint32_t kTableCap = 20u * LSORT_MAX_RMI_DEV;  // learned: double2 + u32 per submodel
 
 void partition_init(int optin) {
     allow_smem(k_hist<true, kLearned>, optin);
@@ -547,11 +562,13 @@ void launch_kind_plan(const LevelParams& p, cudaStream_t st) {
     k_kind_plan<<<1, kPlanNT, 0, st>>>(p);
 }
 
-void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, int grid, cudaStream_t st) {
-    size_t sm_l = 16 + 4 * (size_t)kMaxNB + 2 * kTileBytes, sm_t = sm_l + kTreeCap;
+void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_rmi_b, int grid, cudaStream_t st) {
+    const size_t table_bytes = 20 * (size_t)max_rmi_b;
+    size_t sm_r = 16 + 4 * (size_t)kMaxNB + 2 * kTileBytes, sm_t = sm_r + kTreeCap, sm_l = sm_r + table_bytes;
     if (kinds & 1) {
-        if (in_f64) k_hist<true, kLearned><<<grid, kPNT, sm_l, st>>>(p);
-        else k_hist<false, kLearned><<<grid, kPNT, sm_l, st>>>(p);
+        const int gl = table_bytes > 12 * 1024 ? std::max(1, grid * 2 / 3) : grid;
+        if (in_f64) k_hist<true, kLearned><<<gl, kPNT, sm_l, st>>>(p);
+        else k_hist<false, kLearned><<<gl, kPNT, sm_l, st>>>(p);
     }
     if (kinds & 2) {  // tree payload in shared memory: two CTAs per SM
         const int gt = std::max(1, grid * 2 / 3);
@@ -559,8 +576,8 @@ void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, int grid, cud
         else k_hist<false, kTree><<<gt, kPNT, sm_t, st>>>(p);
     }
     if (kinds & 4) {
-        if (in_f64) k_hist<true, kRadix><<<grid, kPNT, sm_l, st>>>(p);
-        else k_hist<false, kRadix><<<grid, kPNT, sm_l, st>>>(p);
+        if (in_f64) k_hist<true, kRadix><<<grid, kPNT, sm_r, st>>>(p);
+        else k_hist<false, kRadix><<<grid, kPNT, sm_r, st>>>(p);
     }
 }
 
@@ -569,9 +586,10 @@ void launch_scan_children(const LevelParams& p, cudaStream_t st) {
     k_scan_children<<<p.nsegs, kScanNT, 8 * kMaxNB, st>>>(p);
 }
 
-void launch_scatter(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t nb_cap, int grid, cudaStream_t st) {
+void launch_scatter(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t nb_cap, uint32_t max_rmi_b, int grid,
+                    cudaStream_t st) {
     if (kinds & 1) {
-        size_t sm = scatter_smem(nb_cap, 0);
+        size_t sm = scatter_smem(nb_cap, 20 * max_rmi_b);
         if (in_f64) k_scatter<true, false, kLearned><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
         else k_scatter<false, false, kLearned><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
     }
@@ -587,9 +605,9 @@ void launch_scatter(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t n
     }
 }
 
-void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,
-                           cudaStream_t st) {
-    size_t sm = scatter_smem(nmapped, 0);
+void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, uint32_t rmi_b,
+                           int grid, cudaStream_t st) {
+    size_t sm = scatter_smem(nmapped, 20 * rmi_b);
     if (in_f64) k_scatter<true, true, kLearned><<<grid, kPNT, sm, st>>>(p, nmapped, map, nmapped);
     else k_scatter<false, true, kLearned><<<grid, kPNT, sm, st>>>(p, nmapped, map, nmapped);
 }
