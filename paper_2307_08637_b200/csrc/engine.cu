@@ -287,7 +287,7 @@ struct Engine {
         q.kplan = N->kplan.as<KindPlan>();
         q.kstride = 1;
         const int nsm = num_sms();
-        const int g = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 3);
+        const int g = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
         launch_kind_plan(q, st);
         launch_hist(q, 0, 2u, 0, g, st);
         launch_scan_children(q, st);
@@ -430,7 +430,7 @@ struct Engine {
                                                                     src_f64, bi);
             // ---- partition
             const int nsm = num_sms();
-            int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 3);
+            int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
             int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
             const int nk = __builtin_popcount(kinds);
             mark(1);

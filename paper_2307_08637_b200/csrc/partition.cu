@@ -23,8 +23,8 @@
 
 namespace lsort_dev {
 
-constexpr int kPNT = 256;                 // threads per partition CTA
-constexpr int kPItems = 16;               // keys per thread per tile
+constexpr int kPNT = 512;                 // threads per partition CTA
+constexpr int kPItems = 8;                // keys per thread per tile
 constexpr int kPPairs = kPItems / 2;      // 128-bit loads per thread per tile
 static_assert(kPNT * kPItems == kTileKeys, "tile geometry");
 
@@ -246,7 +246,7 @@ constexpr size_t kTileBytes = 8 * (size_t)kTileKeys;
 
 // ------------------------------------------------------- classify + hist
 template <bool IN_F64, uint32_t KIND>
-__global__ void __launch_bounds__(kPNT, 3) k_hist(LevelParams p) {
+__global__ void __launch_bounds__(kPNT, 2) k_hist(LevelParams p) {
     extern __shared__ uint4 smem_u4[];
     uint8_t* sm = (uint8_t*)smem_u4;
     uint64_t* bars = (uint64_t*)sm;                          // 2 mbarriers (16 B)
@@ -566,12 +566,12 @@ void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_
     const size_t table_bytes = 20 * (size_t)max_rmi_b;
     size_t sm_r = 16 + 4 * (size_t)kMaxNB + 2 * kTileBytes, sm_t = sm_r + kTreeCap, sm_l = sm_r + table_bytes;
     if (kinds & 1) {
-        const int gl = table_bytes > 12 * 1024 ? std::max(1, grid * 2 / 3) : grid;
+        const int gl = grid;
         if (in_f64) k_hist<true, kLearned><<<gl, kPNT, sm_l, st>>>(p);
         else k_hist<false, kLearned><<<gl, kPNT, sm_l, st>>>(p);
     }
     if (kinds & 2) {  // tree payload in shared memory: two CTAs per SM
-        const int gt = std::max(1, grid * 2 / 3);
+        const int gt = grid;
         if (in_f64) k_hist<true, kTree><<<gt, kPNT, sm_t, st>>>(p);
         else k_hist<false, kTree><<<gt, kPNT, sm_t, st>>>(p);
     }
