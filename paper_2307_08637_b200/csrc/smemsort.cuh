@@ -43,7 +43,9 @@ struct SmemSort {
     }
 
     // one distribution pass over a[off, off+len), staging through b
-    __device__ static __noinline__ void pass(uint64_t* a, uint64_t* b, uint32_t off, uint32_t len, Smem& S) {
+    // (inlined: as an out-of-line call the shared-memory accesses through `S`
+    // become generic loads/stores)
+    __device__ static __forceinline__ void pass(uint64_t* a, uint64_t* b, uint32_t off, uint32_t len, Smem& S) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         uint64_t mn = ~0ull, mx = 0;
         for (uint32_t i = tid; i < len; i += NT) {
@@ -121,7 +123,7 @@ struct SmemSort {
         __syncthreads();
     }
 
-    __device__ static __noinline__ void warp_rank_sort(uint64_t* a, uint32_t len) {
+    __device__ static __forceinline__ void warp_rank_sort(uint64_t* a, uint32_t len) {
         const int lane = threadIdx.x & 31;
         uint64_t v[8];
         uint32_t r[8];
