@@ -170,7 +170,7 @@ def run_ours(args):
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
-    dist_mode = world > 1
+    dist_mode = world > 1 or args.dist
     if dist_mode:
         import torch.distributed as tdist
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -341,6 +341,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=10_000_000)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="force the distributed path (also at 1 rank)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: W < 3 violates the timing rules", file=sys.stderr)
