@@ -175,10 +175,8 @@ def run_ours(args):
         import torch.distributed as tdist
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     label, dists, n, kind = CONFIGS[args.config]
-    if args.n:
-        n = args.n
-    if args.config == "c5" and not dist_mode:
-        n = min(n, args.n or n)
+    if args.keys:
+        n = args.keys
     f64 = kind == "f64"
     dev = torch.device("cuda", local)
 
@@ -337,7 +335,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
-    ap.add_argument("--n", type=int, default=0, help="override keys per array (testing)")
+    ap.add_argument("--keys", type=int, default=0, help="override keys per array (testing)")
     ap.add_argument("--cpu-sample", type=int, default=10_000_000)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
