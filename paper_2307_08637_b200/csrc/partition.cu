@@ -221,11 +221,13 @@ __device__ __forceinline__ TileGeom tile_geom(const LevelParams& p, const KindTi
 // while the previous tile is processed; head/tail singles are read directly.
 struct TileStream {
     ulonglong2* buf[2];
-    uint64_t* bar;  // 2 mbarriers
+    uint64_t* bar;      // 2 mbarriers
+    uint32_t phase[2];  // parity of each buffer's next completion (flips only when a copy was issued)
     __device__ __forceinline__ void init(uint8_t* base, uint64_t* bars) {
         buf[0] = (ulonglong2*)base;
         buf[1] = (ulonglong2*)(base + 8 * (size_t)kTileKeys);
         bar = bars;
+        phase[0] = phase[1] = 0;
         if (threadIdx.x == 0) {
             mbar_init(&bar[0], 1);
             mbar_init(&bar[1], 1);
@@ -238,8 +240,12 @@ struct TileStream {
             tma_load_1d(buf[b], (const uint64_t*)src + g.a0, g.npairs * 16, &bar[b]);
         }
     }
-    __device__ __forceinline__ void wait(const TileGeom& g, int b, uint32_t use) {
-        if (g.npairs) mbar_wait(&bar[b], use & 1);
+    // g.npairs is uniform across the CTA, so every thread flips the same bits
+    __device__ __forceinline__ void wait(const TileGeom& g, int b) {
+        if (g.npairs) {
+            mbar_wait(&bar[b], phase[b]);
+            phase[b] ^= 1u;
+        }
     }
 };
 constexpr size_t kTileBytes = 8 * (size_t)kTileKeys;
@@ -292,7 +298,7 @@ __global__ void __launch_bounds__(kPNT, 2) k_hist(LevelParams p) {
             __syncthreads();
             cur = i;
         }
-        TS.wait(g, b, (uint32_t)((tile - t0) >> 1));
+        TS.wait(g, b);
         const ulonglong2* sp = TS.buf[b];
         ulonglong2 v[kPPairs];
 #pragma unroll
@@ -447,7 +453,7 @@ __global__ void __launch_bounds__(kPNT, 2) k_scatter(LevelParams p, uint32_t nb_
             __syncthreads();
             cur = i;
         }
-        TS.wait(g, tb, (uint32_t)((tile - t0) >> 1));
+        TS.wait(g, tb);
         const ulonglong2* sp = TS.buf[tb];
         uint64_t* skeys = (uint64_t*)TS.buf[tb];  // staging reuses the consumed tile buffer
         ulonglong2 v[kPPairs];
@@ -528,6 +534,7 @@ __global__ void __launch_bounds__(kPNT, 2) k_scatter(LevelParams p, uint32_t nb_
             if (j < total) p.dst[(long long)j + delta[sbid[j]]] = skeys[j];
         }
         for (uint32_t b = threadIdx.x; b <= nbo; b += kPNT) cnt[b] = 0;
+        fence_proxy_async_smem();  // staging writes (generic proxy) before the next bulk copy into this buffer
         __syncthreads();
     }
 }

@@ -277,6 +277,29 @@ def test_sort_nan(ctx, n, pos):
     assert np.array_equal(bits(d.cpu().numpy()), bits(x))  # untouched
 
 
+@pytest.mark.parametrize("off", [0, 1, 3])
+@pytest.mark.parametrize("n", [4096 * 40 + 1, 4096 * 40 + 2, 4096 * 300 + 1, 1_000_003])
+def test_sort_misaligned_tiles(ctx, off, n):
+    """Device views at odd key offsets with sizes = 1, 2 (mod 4096): tiles whose
+    16-byte aligned interior is empty issue no bulk copy (partition.cu TileStream)."""
+    x = O.generate("normal", n + off + 5, 7)
+    base = dev(x)
+    v = base[off:off + n]
+    ctx.sort(v)
+    got = base.cpu().numpy()
+    check_sorted_f64(x[off:off + n], got[off:off + n])
+    assert np.array_equal(bits(got[:off]), bits(x[:off]))
+    assert np.array_equal(bits(got[off + n:]), bits(x[off + n:]))
+
+
+def test_sort_u64_encoded_normal_20m(ctx):
+    """Encoded float keys sorted as u64 (the distributed local sort's input)."""
+    a = O.encode(O.generate("normal", 20_000_000, 11))
+    d = dev(a)
+    ctx.sort(d)
+    assert np.array_equal(host_u64(d), np.sort(a))
+
+
 def test_sort_host_memory(ctx):
     x = O.generate("lognormal2", 2_000_000, 19)
     y = x.copy()
