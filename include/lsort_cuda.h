@@ -121,6 +121,13 @@ typedef struct lsort_stats {
 } lsort_stats;
 
 #define LSORT_FLAG_PHASE_TIMING 1u
+/* cfg->flags: build every model exactly by the reference's Alg. 5 policy
+ * (PAPER.md:389-415). Without it the GPU replaces a learned model that puts
+ * more than 1/16 of its own sorted sample into one bucket by a splitter tree
+ * over that sample (bucket imbalance costs whole extra passes on the GPU).
+ * The sorted output is identical either way; lsort_cuda_build_model always
+ * runs strict. */
+#define LSORT_FLAG_STRICT_POLICY 2u
 
 typedef struct lsort_ctx lsort_ctx;
 

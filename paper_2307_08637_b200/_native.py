@@ -18,6 +18,7 @@ MEM_DEVICE, MEM_HOST = 0, 1
 MAX_TREE = 1024
 MAX_RMI = 2048
 FLAG_PHASE_TIMING = 1
+FLAG_STRICT_POLICY = 2  # reference Alg. 5 models only (no GPU quality fallback)
 
 
 class lsort_cfg(C.Structure):

@@ -116,12 +116,26 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan;
+        kseg, ktp, kplan, qws;
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
     std::unique_ptr<lsort_ctx> nested;
+    // lanes: workspaces + streams on which the models of the big segments of
+    // one level are built concurrently (fork/join with events on `stream`)
+    std::vector<std::unique_ptr<lsort_ctx>> lanes;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaEvent_t ev[6] = {};
     cudaEvent_t pev[8] = {};  // phase timing
     uint64_t launches = 0;
+    ~lsort_ctx() {
+        if (stream) cudaStreamSynchronize(stream);
+        lanes.clear();
+        nested.reset();
+        for (auto& e : ev) if (e) cudaEventDestroy(e);
+        for (auto& e : pev) if (e) cudaEventDestroy(e);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        if (join_ev) cudaEventDestroy(join_ev);
+        if (own_stream) cudaStreamDestroy(own_stream);
+    }
 };
 
 namespace {
@@ -156,6 +170,7 @@ DevCfg dev_cfg(const lsort_cfg& c) {
     d.first_sample_cap = c.first_sample_cap;
     d.rmi_sample_cap = c.rmi_sample_cap;
     d.seed = c.seed;
+    d.quality = (c.flags & LSORT_FLAG_STRICT_POLICY) ? 0u : 1u;
     return d;
 }
 
@@ -182,21 +197,13 @@ struct Engine {
         if (need <= kSmallSampleCap) return 1;
         return 2;
     }
-    bool is_big(const SegPlan& s) const { return model_class(s) == 2; }
 
     void launched(int k = 1) { C->launches += k; }
 
     // Sort the device buffer `sample` (u64) with a nested context.
     void nested_sort(uint64_t* sample, uint64_t s) {
         if (C->depth >= 2) throw LsortError{LSORT_EINTERNAL, "sample sort nesting too deep"};
-        if (!C->nested) {
-            C->nested.reset(new lsort_ctx());
-            C->nested->device = C->device;
-            C->nested->depth = C->depth + 1;
-            for (auto& e : C->nested->ev) CU(cudaEventCreate(&e));
-            for (auto& e : C->nested->pev) CU(cudaEventCreate(&e));
-        }
-        C->nested->stream = C->stream;
+        nested_ctx();
         lsort_cfg nc = cfg;
         nc.seed = splitmix64(cfg.seed ^ 0x5a3c9e1f0b7d2468ull);
         Engine ne(C->nested.get(), nc);
@@ -219,6 +226,38 @@ struct Engine {
         return C->nested.get();
     }
 
+    lsort_ctx* lane(uint32_t i) {
+        while (C->lanes.size() <= i) {
+            std::unique_ptr<lsort_ctx> L(new lsort_ctx());
+            L->device = C->device;
+            L->depth = C->depth + 1;
+            CU(cudaStreamCreateWithFlags(&L->own_stream, cudaStreamNonBlocking));
+            L->stream = L->own_stream;
+            CU(cudaEventCreateWithFlags(&L->join_ev, cudaEventDisableTiming));
+            C->lanes.push_back(std::move(L));
+        }
+        return C->lanes[i].get();
+    }
+    static constexpr uint32_t kLanes = 8;
+
+    // Models of the big segments `bigs` (indices into segs/hs, device
+    // descriptors at dsegs), spread over up to kLanes concurrent streams that
+    // fork from and join back into the context stream.
+    void big_models(const std::vector<uint32_t>& bigs, const SegDesc* dsegs, const std::vector<SegPlan>& segs,
+                    const SegDesc* hs, const void* src, bool f64) {
+        if (bigs.empty()) return;
+        const uint32_t nl = (uint32_t)std::min<size_t>(bigs.size(), kLanes);
+        if (!C->fork_ev) CU(cudaEventCreateWithFlags(&C->fork_ev, cudaEventDisableTiming));
+        CU(cudaEventRecord(C->fork_ev, st));
+        for (uint32_t l = 0; l < nl; ++l) CU(cudaStreamWaitEvent(lane(l)->stream, C->fork_ev, 0));
+        for (uint32_t bi = 0; bi < bigs.size(); ++bi)
+            big_model(dsegs + bigs[bi], segs[bigs[bi]], hs[bigs[bi]], src, f64, lane(bi % nl));
+        for (uint32_t l = 0; l < nl; ++l) {
+            CU(cudaEventRecord(lane(l)->join_ev, lane(l)->stream));
+            CU(cudaStreamWaitEvent(st, lane(l)->join_ev, 0));
+        }
+    }
+
     // Model for one big segment (RMI sample > one CTA), with no host round
     // trip: (1) one CTA draws + sorts the first sample, decides the policy
     // (writes *gate) and builds a splitter tree over the first sample;
@@ -226,9 +265,9 @@ struct Engine {
     // distribution level with that tree + shared-memory base cases; (4)
     // multi-CTA training. Every step after (1) is gated on the device.
     void big_model(const SegDesc* dseg, const SegPlan& sp, const SegDesc& hseg, const void* src, bool f64,
-                   uint32_t big_index) {
+                   lsort_ctx* N) {
+        const cudaStream_t st = N->stream;  // this lane's stream
         DevCfg dc = dev_cfg(cfg);
-        lsort_ctx* N = nested_ctx();
         const uint64_t n = sp.n;
         const uint64_t s1 = sample_size_host(cfg.sample_fraction, cfg.first_sample_cap, n);
         const uint64_t s2 = sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
@@ -236,19 +275,19 @@ struct Engine {
         const uint32_t nb = 2 * k - 1;
         const size_t aux_bytes = sizeof(ModelHdr) + ((tree_payload_bytes(k, k - 1) + 15) & ~15ull);
         const uint64_t ntiles = (s2 + kTileKeys - 1) / kTileKeys;
-        if (!C->sample.ensure(s2 * 8) || !N->scratch.ensure(s2 * 8) || !N->models.ensure(aux_bytes) ||
+        if (!N->sample.ensure(s2 * 8) || !N->scratch.ensure(s2 * 8) || !N->models.ensure(aux_bytes) ||
             !N->segs.ensure(sizeof(SegDesc)) || !N->tile_prefix.ensure(16) || !N->buckets.ensure(8 * (size_t)nb) ||
             !N->rec.ensure(nb * sizeof(SegOut)) || !N->fill.ensure(nb * sizeof(FillItem)) ||
             !N->base[0].ensure(nb * sizeof(BaseItem)) || !N->base[1].ensure(nb * sizeof(BaseItem)) ||
             !N->base[2].ensure(nb * sizeof(BaseItem)) || !N->kseg.ensure(64) || !N->ktp.ensure(64) ||
-            !N->kplan.ensure(3 * sizeof(KindPlan)) || !N->ctrl.ensure(sizeof(Ctrl) * (big_index + 1)) ||
-            !N->aux.ensure(4 * (big_index + 1)) || !C->train_ws.ensure(train_workspace_bytes(s2, hseg.rmi_b)))
+            !N->kplan.ensure(3 * sizeof(KindPlan)) || !N->ctrl.ensure(sizeof(Ctrl)) ||
+            !N->aux.ensure(4) || !N->train_ws.ensure(train_workspace_bytes(s2, hseg.rmi_b)))
             throw LsortError{LSORT_ENOMEM, "big model workspace"};
-        uint32_t* gate = N->aux.as<uint32_t>() + big_index;
-        Ctrl* nctrl = N->ctrl.as<Ctrl>() + big_index;
+        uint32_t* gate = N->aux.as<uint32_t>();
+        Ctrl* nctrl = N->ctrl.as<Ctrl>();
         launch_first_sample(dseg, src, f64, C->models.as<uint8_t>(), dc, N->models.as<uint8_t>(), k, gate, st);
         const uint64_t seed = seg_seed_host(cfg.seed, sp.begin, sp.depth);
-        launch_gather(dseg, src, f64, seed, s1, s2, C->sample.as<uint64_t>(), gate, st);
+        launch_gather(dseg, src, f64, seed, s1, s2, N->sample.as<uint64_t>(), gate, st);
         // one distribution level over the sample with the first-sample tree
         SegDesc d{};
         d.begin = 0;
@@ -270,7 +309,7 @@ struct Engine {
         q.ntiles = ntiles;
         q.models = N->models.as<uint8_t>();
         q.buckets = N->buckets.as<unsigned long long>();
-        q.src = C->sample.p;
+        q.src = N->sample.p;
         q.dst = N->scratch.as<uint64_t>();
         q.ctrl = nctrl;
         q.rec = N->rec.as<SegOut>();
@@ -292,11 +331,17 @@ struct Engine {
         launch_hist(q, 0, 2u, 0, g, st);
         launch_scan_children(q, st);
         launch_scatter(q, 0, 2u, nb, 0, g, st);
-        launch_base_cases(q, N->scratch.as<uint64_t>(), C->sample.p, 0, st);
-        launch_fill(q, C->sample.p, 0, nsm, st);
-        launch_train_rmi(C->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
-                         hseg.rmi_b, C->train_ws.p, gate, st);
+        launch_base_cases(q, N->scratch.as<uint64_t>(), N->sample.p, 0, st);
+        launch_fill(q, N->sample.p, 0, nsm, st);
+        launch_train_rmi(N->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
+                         hseg.rmi_b, N->train_ws.p, gate, st);
         launched(2 + 9 + 8);
+        if (dc.quality) {
+            if (!N->qws.ensure(quality_workspace_bytes())) throw LsortError{LSORT_ENOMEM, "quality workspace"};
+            launch_quality_check(N->sample.as<uint64_t>(), s2, C->models.as<uint8_t>() + hseg.model_off, hseg.tree_k,
+                                 N->qws.p, gate, st);
+            launched(2);
+        }
     }
 
     // Sort n keys at `keys` (device) in place. Returns LSORT_ENAN via throw.
@@ -426,8 +471,7 @@ struct Engine {
             launch_build_models(p.segs, C->idx.as<uint32_t>() + nsmall, nmid, src, src_f64, C->models.as<uint8_t>(),
                                 dc, 1, st);
             launched((nsmall ? 1 : 0) + (nmid ? 1 : 0));
-            for (uint32_t bi = 0; bi < bigs.size(); ++bi) big_model(p.segs + bigs[bi], segs[bigs[bi]], hs[bigs[bi]], src,
-                                                                    src_f64, bi);
+            big_models(bigs, p.segs, segs, hs, src, src_f64);
             // ---- partition
             const int nsm = num_sms();
             int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
@@ -462,6 +506,20 @@ struct Engine {
                             C->depth, level, ns, bigs.size(), (unsigned long long)keys, (unsigned long long)mx,
                             (unsigned long long)ntiles, t[0], t[1], t[2], t[3], t[4], hc->n_rec, hc->n_base[0],
                             hc->n_base[1], hc->n_base[2], hc->n_fill);
+                }
+                if (trace_enabled()) {
+                    for (uint32_t bi = 0; bi < bigs.size(); ++bi) {
+                        ModelHdr mh;
+                        CU(cudaMemcpy(&mh, C->models.as<uint8_t>() + hs[bigs[bi]].model_off, sizeof(mh),
+                                      cudaMemcpyDeviceToHost));
+                        fprintf(stderr,
+                                "    big seg begin=%llu n=%llu depth=%u: kind=%u nb=%u B=%u dup=%.4f s1=%llu s2=%llu "
+                                "root=(%.6g, %.6g) base=%.6g scale=%.6g cdf_lo=%.6g inv_span=%.6g\n",
+                                (unsigned long long)segs[bigs[bi]].begin, (unsigned long long)segs[bigs[bi]].n,
+                                segs[bigs[bi]].depth, mh.kind, mh.nbuckets, mh.B, mh.dup, (unsigned long long)mh.s1,
+                                (unsigned long long)mh.s2, mh.root_slope, mh.root_icpt, mh.key_base, mh.key_scale,
+                                mh.cdf_lo, mh.inv_span);
+                    }
                 }
                 stats->ms_models += t[0];
                 stats->ms_classify += t[1];
@@ -577,15 +635,7 @@ int lsort_cuda_ctx_create(lsort_ctx** out, int device, void* stream, size_t work
 int lsort_cuda_ctx_destroy(lsort_ctx* c) {
     if (!c) return LSORT_OK;
     cudaSetDevice(c->device);
-    if (c->stream) cudaStreamSynchronize(c->stream);
-    for (auto& e : c->ev) if (e) cudaEventDestroy(e);
-    for (auto& e : c->pev) if (e) cudaEventDestroy(e);
-    if (c->nested) {
-        for (auto& e : c->nested->ev) if (e) cudaEventDestroy(e);
-        for (auto& e : c->nested->pev) if (e) cudaEventDestroy(e);
-    }
-    if (c->own_stream) cudaStreamDestroy(c->own_stream);
-    delete c;
+    delete c;  // ~lsort_ctx: drains the stream, frees lanes / nested contexts, events, own stream
     return LSORT_OK;
 }
 
@@ -833,6 +883,7 @@ int lsort_cuda_build_model(lsort_ctx* C, const void* d_keys, uint64_t n, int key
     if (!C) return LSORT_EINVAL;
     if (n < 2) return fail(C, {LSORT_EINVAL, "build_model: n < 2"});
     lsort_cfg cfg = cfg_or_default(cfgp);
+    cfg.flags |= LSORT_FLAG_STRICT_POLICY;  // the reference's Alg. 5 model, unit-for-unit
     try {
         validate_cfg(cfg);
         CU(cudaSetDevice(C->device));
@@ -853,7 +904,7 @@ int lsort_cuda_build_model(lsort_ctx* C, const void* d_keys, uint64_t n, int key
         CU(cudaMemcpyAsync(C->idx.p, &zero, 4, cudaMemcpyHostToDevice, C->stream));
         const bool f64 = key_kind == LSORT_KEY_F64;
         const int mc = E.model_class(sp);
-        if (mc == 2) E.big_model(C->segs.as<SegDesc>(), sp, d, d_keys, f64, 0);
+        if (mc == 2) E.big_models({0u}, C->segs.as<SegDesc>(), {sp}, &d, d_keys, f64);
         else launch_build_models(C->segs.as<SegDesc>(), C->idx.as<uint32_t>(), 1, d_keys, f64,
                                  C->models.as<uint8_t>(), dev_cfg(cfg), mc, C->stream);
         CU(cudaStreamSynchronize(C->stream));

@@ -82,7 +82,10 @@ struct DevCfg {
     double sample_fraction;
     uint32_t first_sample_cap, rmi_sample_cap;
     uint64_t seed;
+    uint32_t quality;  // 1: GPU policy -- a learned model that puts > 1/kPoorShare of its own
+                       // sample into one bucket is replaced by a splitter tree over that sample
 };
+constexpr uint32_t kPoorShare = 16;
 
 constexpr int kTileKeys = 4096;     // keys per classify/scatter tile
 constexpr int kPartNT = 512;        // threads per classify/scatter CTA
@@ -101,6 +104,11 @@ void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_
 void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0,
                    uint64_t s, uint64_t* out, const uint32_t* gate, cudaStream_t st);
 size_t train_workspace_bytes(uint64_t s, uint32_t B);
+// GPU policy (DevCfg::quality) for a big segment's learned model trained on the
+// sorted sample: classify the sample, fall back to a splitter tree if poor.
+void launch_quality_check(const uint64_t* sorted, uint64_t s, uint8_t* model, uint32_t tree_k, void* ws,
+                          const uint32_t* gate, cudaStream_t st);
+size_t quality_workspace_bytes();
 void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* model, uint32_t nbuckets,
                       void* ws, const uint32_t* gate, cudaStream_t st);
 void launch_tree_build(const uint64_t* sorted, uint64_t s, uint32_t budget, int eq_mode, uint8_t* model,

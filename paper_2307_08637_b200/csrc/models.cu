@@ -376,7 +376,6 @@ struct ModelCfg {
 };
 using ModelSmall = ModelCfg<256, 2048>;
 using ModelMid = ModelCfg<512, 8192>;
-constexpr int kModelNT = 512;  // utility kernels (tree build, block sort)
 
 // Radix/fill fallback model: min/max of the whole segment (one CTA).
 template <int NT>
@@ -470,6 +469,22 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
         sample_sorted<IN_F64, MC>(sd, src, seed, s1, s2, S);
         train_rmi_block<NT>(A, s2, sd.rmi_b, h, (RmiEntry*)payload, S.u.rmi.first, S.u.rmi.lo, S.u.rmi.hi,
                             S.u.rmi.big, S.u.rmi.red);
+        if (cfg.quality) {
+            __syncthreads();
+            uint32_t* hist = S.u.rmi.first;  // free after training
+            Classifier Cl;
+            Cl.init((const uint8_t*)h);
+            for (uint32_t b = threadIdx.x; b < Cl.nb; b += NT) hist[b] = 0;
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < s2; i += NT) atomicAdd(&hist[Cl.classify<kLearned>(A[i])], 1u);
+            __syncthreads();
+            uint64_t mx = 0;
+            for (uint32_t b = threadIdx.x; b < Cl.nb; b += NT) mx = hist[b] > mx ? hist[b] : mx;
+            mx = block_reduce_max<NT>(mx, S.red64);
+            if (mx * kPoorShare > s2)
+                tree_build_block<NT>(A, s2, sd.tree_k, true, h, payload, S.u.tree.scratch, S.u.tree.wsum,
+                                     S.u.tree.spl);
+        }
     } else {
         if (threadIdx.x == 0) h->s2 = 0;
         tree_build_block<NT>(A, s1, sd.tree_k, true, h, payload, S.u.tree.scratch, S.u.tree.wsum, S.u.tree.spl);
@@ -515,21 +530,25 @@ constexpr int kTrainNT = 256;
 struct TrainWS {
     double* part;   // [4][nch]: sx, sy, sxx, sxy per chunk
     double* root;   // rs, ri, base, scale, mx, my
+    double* big;    // [B][kBigSplit][3] partial sums of the big-slice fits
     uint32_t* first;
+    uint32_t* bigcnt;  // [B] arrival counters (wrap to 0)
     uint32_t nch;
 };
+constexpr int kBigSplitWS = 16;
 __host__ __device__ inline TrainWS train_ws(void* ws, uint64_t s, uint32_t B) {
     TrainWS w;
     w.nch = (uint32_t)((s + kTrainChunk - 1) / kTrainChunk);
     w.part = (double*)ws;
     w.root = w.part + 4 * (size_t)w.nch;
-    w.first = (uint32_t*)(w.root + 8);
-    (void)B;
+    w.big = w.root + 8;
+    w.first = (uint32_t*)(w.big + (size_t)B * kBigSplitWS * 3);
+    w.bigcnt = w.first + B + 2;
     return w;
 }
 size_t train_workspace_bytes(uint64_t s, uint32_t B) {
     uint64_t nch = (s + kTrainChunk - 1) / kTrainChunk;
-    return 8 * (4 * nch + 8) + 4 * ((size_t)B + 2);
+    return 8 * (4 * nch + 8) + 24 * (size_t)B * kBigSplitWS + 4 * ((size_t)B + 2) + 4 * (size_t)B;
 }
 __device__ __forceinline__ bool gated_off(const uint32_t* gate) { return gate && *gate == 0; }
 
@@ -683,46 +702,68 @@ __global__ void __launch_bounds__(32 * kFitWarps) k_train_fits(const uint64_t* s
     }
 }
 
-// one CTA per slice larger than kSeqFitMax: deterministic block reduction
-constexpr int kBigFitNT = 512;
+// Slices larger than kSeqFitMax: kBigSplit CTAs per slice, one pass of
+// shifted sums (d = xn - xn(first), e = i - first) so no division sits in the
+// loop; the last CTA of a slice (atomicInc counter, wraps back to 0) combines
+// the partials in a fixed order -> deterministic. Within RMI_RTOL of the
+// reference's sequential sums (models.cpp:14-35).
+constexpr int kBigFitNT = 256;
+constexpr int kBigSplit = 16;
 __global__ void __launch_bounds__(kBigFitNT) k_train_bigfits(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
                                                             RmiEntry* E, const uint32_t* gate) {
     __shared__ double red[kBigFitNT / 32];
+    __shared__ uint32_t last;
     if (gated_off(gate)) return;
     TrainWS w = train_ws(wsp, n, B);
     const uint32_t m = blockIdx.x;
     const uint32_t f = min(w.first[m], n), l = min(max(w.first[m + 1], f), n);
     if (l - f <= (uint32_t)kSeqFitMax) return;
     const double base = w.root[2], scale = w.root[3];
-    const double nd = (double)n;
     const uint32_t cnt = l - f;
-    const uint32_t per = (cnt + kBigFitNT - 1) / kBigFitNT;
-    const uint32_t lo = f + min(cnt, threadIdx.x * per), hi = f + min(cnt, (threadIdx.x + 1) * per);
-    double sx = 0.0, sy = 0.0;
-    for (uint32_t i = lo; i < hi; ++i) {
-        sx = __dadd_rn(sx, rmi_normalize(base, scale, s[i]));
-        sy = __dadd_rn(sy, __ddiv_rn((double)i, nd));
+    const double c = rmi_normalize(base, scale, s[f]);
+    double sd = 0.0, sdd = 0.0, sde = 0.0;
+    for (uint32_t i = f + blockIdx.y * kBigFitNT + threadIdx.x; i < l; i += kBigSplit * kBigFitNT) {
+        const double d = __dsub_rn(rmi_normalize(base, scale, s[i]), c);
+        const double e = (double)(i - f);
+        sd = __dadd_rn(sd, d);
+        sdd = __dadd_rn(sdd, __dmul_rn(d, d));
+        sde = __dadd_rn(sde, __dmul_rn(d, e));
     }
-    sx = block_sum_f64<kBigFitNT>(sx, red);
-    sy = block_sum_f64<kBigFitNT>(sy, red);
-    const double mx = __ddiv_rn(sx, (double)cnt), my = __ddiv_rn(sy, (double)cnt);
-    double sxx = 0.0, sxy = 0.0;
-    for (uint32_t i = lo; i < hi; ++i) {
-        double dx = __dsub_rn(rmi_normalize(base, scale, s[i]), mx);
-        sxx = __dadd_rn(sxx, __dmul_rn(dx, dx));
-        sxy = __dadd_rn(sxy, __dmul_rn(dx, __dsub_rn(__ddiv_rn((double)i, nd), my)));
-    }
-    sxx = block_sum_f64<kBigFitNT>(sxx, red);
-    sxy = block_sum_f64<kBigFitNT>(sxy, red);
+    sd = block_sum_f64<kBigFitNT>(sd, red);
+    sdd = block_sum_f64<kBigFitNT>(sdd, red);
+    sde = block_sum_f64<kBigFitNT>(sde, red);
+    double* part = w.big + ((size_t)m * kBigSplit + blockIdx.y) * 3;
     if (threadIdx.x == 0) {
-        double sl = 0.0, ic = my;
-        if (sxx > 0.0) {
-            double q = __ddiv_rn(sxy, sxx);
-            if (!(q < 0.0)) { sl = q; ic = __dsub_rn(my, __dmul_rn(q, mx)); }
-        }
-        E[m].slope = sl;
-        E[m].intercept = ic;
+        part[0] = sd;
+        part[1] = sdd;
+        part[2] = sde;
+        __threadfence();
+        last = atomicInc(&w.bigcnt[m], kBigSplit - 1) == kBigSplit - 1;
     }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    const volatile double* P = w.big + (size_t)m * kBigSplit * 3;
+    double Sd = 0.0, Sdd = 0.0, Sde = 0.0;
+    for (int q = 0; q < kBigSplit; ++q) {
+        Sd = __dadd_rn(Sd, P[3 * q]);
+        Sdd = __dadd_rn(Sdd, P[3 * q + 1]);
+        Sde = __dadd_rn(Sde, P[3 * q + 2]);
+    }
+    const double cn = (double)cnt, nd = (double)n;
+    const double md = __ddiv_rn(Sd, cn);
+    const double mx = __dadd_rn(c, md);
+    const double me = __dmul_rn(0.5, (double)(cnt - 1));            // mean of e, exact
+    const double my = __ddiv_rn(__dadd_rn((double)f, me), nd);      // mean of i/n
+    const double sxx = __dsub_rn(Sdd, __dmul_rn(Sd, md));           // sum (x - mx)^2
+    const double sxy = __ddiv_rn(__dsub_rn(Sde, __dmul_rn(Sd, me)), nd);  // sum (x - mx)(y - my)
+    double sl = 0.0, ic = my;  // models.cpp:32-34
+    if (sxx > 0.0) {
+        double q = __ddiv_rn(sxy, sxx);
+        if (!(q < 0.0)) { sl = q; ic = __dsub_rn(my, __dmul_rn(q, mx)); }
+    }
+    E[m].slope = sl;
+    E[m].intercept = ic;
 }
 
 // enforce_monotonic (models.cpp:101-126) + header + compiled table, one CTA
@@ -802,6 +843,55 @@ __global__ void __launch_bounds__(512) k_block_sort(uint64_t* keys, uint32_t n) 
     for (uint32_t i = threadIdx.x; i < n; i += 512) keys[i] = S.sort.A[i];
 }
 
+// ------------------------------------------------ model quality (GPU policy)
+// Bucket histogram of a big segment's sorted RMI sample under its freshly
+// trained learned model (global counts, zeroed by the launcher).
+constexpr int kEvalNT = 512;
+__global__ void __launch_bounds__(kEvalNT) k_eval_sample(const uint64_t* s, uint32_t n, const uint8_t* model,
+                                                         uint32_t* counts, const uint32_t* gate) {
+    __shared__ uint32_t hist[LSORT_MAX_RMI_DEV];
+    if (gated_off(gate)) return;
+    Classifier Cl;
+    Cl.init(model);
+    if (Cl.kind != kLearned) return;
+    for (uint32_t b = threadIdx.x; b < Cl.nb; b += kEvalNT) hist[b] = 0;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * kEvalNT + threadIdx.x; i < n; i += gridDim.x * kEvalNT)
+        atomicAdd(&hist[Cl.classify<kLearned>(s[i])], 1u);
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < Cl.nb; b += kEvalNT)
+        if (hist[b]) atomicAdd(&counts[b], hist[b]);
+}
+
+// One CTA: if one bucket holds more than 1/kPoorShare of the sample, replace
+// the learned model by a splitter tree over the same sorted sample.
+__global__ void __launch_bounds__(512) k_quality(const uint64_t* s, uint32_t n, uint8_t* model, uint32_t tree_k,
+                                                 const uint32_t* counts, const uint32_t* gate) {
+    __shared__ uint32_t scratch[2 * LSORT_MAX_TREE_DEV + 2];
+    __shared__ uint32_t wsum[512 / 32 + 1];
+    __shared__ uint64_t spl[LSORT_MAX_TREE_DEV];
+    __shared__ uint64_t red[512 / 32];
+    if (gated_off(gate)) return;
+    ModelHdr* h = (ModelHdr*)model;
+    if (h->kind != kLearned) return;
+    const uint32_t nb = h->nbuckets;
+    uint64_t mx = 0;
+    for (uint32_t b = threadIdx.x; b < nb; b += 512) mx = counts[b] > mx ? counts[b] : mx;
+    mx = block_reduce_max<512>(mx, red);
+    if (mx * kPoorShare <= n) return;
+    tree_build_block<512>(s, n, tree_k, true, h, model + sizeof(ModelHdr), scratch, wsum, spl);
+}
+
+size_t quality_workspace_bytes() { return 4 * (size_t)LSORT_MAX_RMI_DEV; }
+
+void launch_quality_check(const uint64_t* sorted, uint64_t s, uint8_t* model, uint32_t tree_k, void* ws,
+                          const uint32_t* gate, cudaStream_t st) {
+    cudaMemsetAsync(ws, 0, quality_workspace_bytes(), st);
+    const int g = (int)std::min<uint64_t>((s + 4 * kEvalNT - 1) / (4 * kEvalNT), (uint64_t)num_sms());
+    k_eval_sample<<<g, kEvalNT, 0, st>>>(sorted, (uint32_t)s, model, (uint32_t*)ws, gate);
+    k_quality<<<1, 512, 0, st>>>(sorted, (uint32_t)s, model, tree_k, (const uint32_t*)ws, gate);
+}
+
 // ------------------------------------------------------------- launchers
 void models_init(int optin) {
     allow_smem(k_build_models<true, ModelSmall, 256>, optin);
@@ -856,7 +946,9 @@ void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* m
     const int gb = (int)std::min<uint64_t>((s + kTrainNT - 1) / kTrainNT, (uint64_t)num_sms() * 8);
     k_train_bounds<<<gb, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
     k_train_fits<<<(B + kFitWarps - 1) / kFitWarps, 32 * kFitWarps, 0, st>>>(sample, n, ws, B, E, gate);
-    k_train_bigfits<<<B, kBigFitNT, 0, st>>>(sample, n, ws, B, E, gate);
+    static_assert(kBigSplit == kBigSplitWS, "workspace layout");
+    cudaMemsetAsync(train_ws(ws, s, B).bigcnt, 0, 4 * (size_t)B, st);
+    k_train_bigfits<<<dim3(B, kBigSplit), kBigFitNT, 0, st>>>(sample, n, ws, B, E, gate);
     k_train_enforce<<<1, kEnforceNT, 16 * (size_t)B, st>>>(sample, n, ws, B, model, nbuckets, gate);
 }
 

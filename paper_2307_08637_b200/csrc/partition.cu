@@ -545,7 +545,6 @@ static size_t scatter_smem(uint32_t nb_cap, uint32_t tree_cap) {
            2 * (size_t)kTileKeys + 16 + tree_cap;
 }
 static const uint32_t kTreeCap = (uint32_t)((tree_payload_bytes(LSORT_MAX_TREE_DEV, LSORT_MAX_TREE_DEV - 1) + 15) & ~15ull);
-static const uint32_t kTableCap = 20u * LSORT_MAX_RMI_DEV;  // learned: double2 + u32 per submodel
 
 void partition_init(int optin) {
     allow_smem(k_hist<true, kLearned>, optin);

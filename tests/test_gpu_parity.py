@@ -300,6 +300,25 @@ def test_sort_u64_encoded_normal_20m(ctx):
     assert np.array_equal(host_u64(d), np.sort(a))
 
 
+@pytest.mark.parametrize("n", [600_000, 1_400_000])
+def test_sort_quality_fallback(ctx, n):
+    """A segment straddling 0.0 (normal values in [-0.003, 0.031]): encoded keys
+    are bimodal, the reference's learned model (strict policy) puts most keys in
+    one bucket; the GPU policy swaps in a splitter tree. Same sorted output."""
+    rng = np.random.default_rng(5)
+    x = rng.normal(0.0, 1.0, 4 * n)
+    x = x[(x > -0.003) & (x < 0.031)][:n] if n <= 600_000 else np.concatenate(
+        [rng.uniform(-0.003, 0.0, n // 10), rng.uniform(0.0, 0.031, n - n // 10)])
+    rng.shuffle(x)
+    levels = {}
+    for name, flags in [("strict", L._native.FLAG_STRICT_POLICY), ("gpu", 0)]:
+        d = dev(x)
+        st = ctx.sort(d, L.SortConfig(flags=flags))
+        check_sorted_f64(x, d.cpu().numpy())
+        levels[name] = st["levels"]
+    assert levels["gpu"] <= levels["strict"]
+
+
 def test_sort_host_memory(ctx):
     x = O.generate("lognormal2", 2_000_000, 19)
     y = x.copy()
