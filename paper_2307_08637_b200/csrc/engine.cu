@@ -116,7 +116,7 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws;
+        kseg, ktp, kplan, qws, ids;
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
     std::unique_ptr<lsort_ctx> nested;
     // lanes: workspaces + streams on which the models of the big segments of
@@ -280,7 +280,7 @@ struct Engine {
             !N->rec.ensure(nb * sizeof(SegOut)) || !N->fill.ensure(nb * sizeof(FillItem)) ||
             !N->base[0].ensure(nb * sizeof(BaseItem)) || !N->base[1].ensure(nb * sizeof(BaseItem)) ||
             !N->base[2].ensure(nb * sizeof(BaseItem)) || !N->kseg.ensure(64) || !N->ktp.ensure(64) ||
-            !N->kplan.ensure(3 * sizeof(KindPlan)) || !N->ctrl.ensure(sizeof(Ctrl)) ||
+            !N->kplan.ensure(3 * sizeof(KindPlan)) || !N->ctrl.ensure(sizeof(Ctrl)) || !N->ids.ensure(2 * s2) ||
             !N->aux.ensure(4) || !N->train_ws.ensure(train_workspace_bytes(s2, hseg.rmi_b)))
             throw LsortError{LSORT_ENOMEM, "big model workspace"};
         uint32_t* gate = N->aux.as<uint32_t>();
@@ -311,6 +311,7 @@ struct Engine {
         q.buckets = N->buckets.as<unsigned long long>();
         q.src = N->sample.p;
         q.dst = N->scratch.as<uint64_t>();
+        q.ids = N->ids.as<uint16_t>();
         q.ctrl = nctrl;
         q.rec = N->rec.as<SegOut>();
         for (int c = 0; c < 3; ++c) q.base[c] = N->base[c].as<BaseItem>();
@@ -330,7 +331,7 @@ struct Engine {
         launch_kind_plan(q, st);
         launch_hist(q, 0, 2u, 0, g, st);
         launch_scan_children(q, st);
-        launch_scatter(q, 0, 2u, nb, 0, g, st);
+        launch_scatter(q, 0, nb, g, st);
         launch_base_cases(q, N->scratch.as<uint64_t>(), N->sample.p, 0, st);
         launch_fill(q, N->sample.p, 0, nsm, st);
         launch_train_rmi(N->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
@@ -363,7 +364,7 @@ struct Engine {
             if (stats) { stats->level0_kind = 2; stats->base_case_keys += n; }
             return;
         }
-        if (!C->scratch.ensure(n * 8)) throw LsortError{LSORT_ENOMEM, "scratch keys"};
+        if (!C->scratch.ensure(n * 8) || !C->ids.ensure(n * 2)) throw LsortError{LSORT_ENOMEM, "scratch keys"};
         const uint32_t depth_cap =
             (uint32_t)std::ceil(std::log2((double)n) / std::log2((double)cfg.tree_bucket_count)) + 4;
         std::vector<SegPlan> segs{{0, n, 0, 0}};
@@ -446,6 +447,7 @@ struct Engine {
             p.buckets = C->buckets.as<unsigned long long>();
             p.src = src;
             p.dst = dst;
+            p.ids = C->ids.as<uint16_t>();
             p.ctrl = dctrl;
             p.rec = C->rec.as<SegOut>();
             for (int c = 0; c < 3; ++c) p.base[c] = C->base[c].as<BaseItem>();
@@ -482,7 +484,7 @@ struct Engine {
             launch_hist(p, src_f64, kinds, max_rmi_b, grid_h, st);
             launch_scan_children(p, st);
             mark(2);
-            launch_scatter(p, src_f64, kinds, max_nb, max_rmi_b, grid_s, st);
+            launch_scatter(p, src_f64, max_nb, grid_s, st);
             mark(3);
             launch_base_cases(p, dst, keys, f64, st);
             mark(4);
@@ -831,7 +833,7 @@ int lsort_cuda_classify_rmi(lsort_ctx* C, const lsort_rmi_header* h, const lsort
         CU(cudaSetDevice(C->device));
         upload_learned(C, h, e, bucket_count, cdf_lo, cdf_hi);
         if (d_hist) CU(cudaMemsetAsync(d_hist, 0, 8 * (size_t)bucket_count, C->stream));
-        if (n) launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, d_ids,
+        if (n) launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, d_ids, nullptr,
                                    (unsigned long long*)d_hist, (int)kLearnedEntryBytes * (int)h->submodels, C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
@@ -867,7 +869,7 @@ int lsort_cuda_classify_tree(lsort_ctx* C, const lsort_tree* t, const void* d_ke
         CU(cudaSetDevice(C->device));
         size_t payload = upload_tree(C, t);
         if (d_hist) CU(cudaMemsetAsync(d_hist, 0, 8 * (size_t)t->bucket_count, C->stream));
-        if (n) launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, d_ids,
+        if (n) launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, d_ids, nullptr,
                                    (unsigned long long*)d_hist, (int)payload, C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
@@ -1042,8 +1044,9 @@ int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int 
         unsigned long long* dcur = dhist + B;
         CU(cudaMemcpyAsync(dmap, map.data(), B * 4, cudaMemcpyHostToDevice, C->stream));
         CU(cudaMemsetAsync(dhist, 0, 8 * (size_t)B, C->stream));
-        launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, nullptr, dhist, (int)kLearnedEntryBytes * (int)B,
-                            C->stream);
+        if (!C->ids.ensure(2 * n)) throw LsortError{LSORT_ENOMEM, "dist ids"};
+        launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, nullptr,
+                            C->ids.as<uint16_t>(), dhist, (int)kLearnedEntryBytes * (int)B, C->stream);
         std::vector<uint64_t> hist(B);
         CU(cudaMemcpyAsync(hist.data(), dhist, 8 * (size_t)B, cudaMemcpyDeviceToHost, C->stream));
         CU(cudaStreamSynchronize(C->stream));
@@ -1092,7 +1095,8 @@ int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int 
         p.kplan = C->kplan.as<KindPlan>();
         p.kstride = 1;
         int grid = (int)std::min<uint64_t>(pref[1], (uint64_t)num_sms() * 3);
-        launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, B, grid, C->stream);
+        p.ids = C->ids.as<uint16_t>();
+        launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, grid, C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
     } catch (const LsortError& er) {

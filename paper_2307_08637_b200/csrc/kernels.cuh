@@ -61,6 +61,8 @@ struct LevelParams {
     unsigned long long* buckets;   // counters -> cursors
     const void* src;               // keys in (level 0 may be f64)
     uint64_t* dst;                 // partitioned keys out (encoded)
+    uint16_t* ids;                 // per key of src: bucket id written by k_hist, read by k_scatter
+                                   // (kNoMove: equality / fill bucket, the key is not moved)
     Ctrl* ctrl;
     SegOut* rec;
     BaseItem* base[3];
@@ -88,6 +90,7 @@ struct DevCfg {
 constexpr uint32_t kPoorShare = 16;
 
 constexpr int kTileKeys = 4096;     // keys per classify/scatter tile
+constexpr uint16_t kNoMove = 0xffff;
 constexpr int kPartNT = 512;        // threads per classify/scatter CTA
 constexpr int kRadixBits = 10;      // fallback radix model: 1024 buckets
 constexpr uint32_t kSmallSampleCap = 8192;   // samples sortable in one model CTA
@@ -118,17 +121,17 @@ void launch_block_sort(uint64_t* keys, uint64_t n, cudaStream_t st);
 void launch_kind_plan(const LevelParams& p, cudaStream_t st);
 void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_rmi_b, int grid, cudaStream_t st);
 void launch_scan_children(const LevelParams& p, cudaStream_t st);
-void launch_scatter(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t nb_cap, uint32_t max_rmi_b, int grid,
-                    cudaStream_t st);
-void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, uint32_t rmi_b,
-                           int grid, cudaStream_t st);
+// scatter of every segment of the level (all kinds), bucket ids from k_hist in p.ids
+void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid, cudaStream_t st);
+void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,
+                           cudaStream_t st);
 // basecase.cu
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
 void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st);
 void launch_small_sort(void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st);
 // util.cu
 void launch_classify_ids(const uint8_t* model, const void* keys, uint64_t n, int in_f64,
-                         uint32_t* ids, unsigned long long* hist, int payload, cudaStream_t st);
+                         uint32_t* ids, uint16_t* ids16, unsigned long long* hist, int payload, cudaStream_t st);
 void launch_verify(const void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st);
 void launch_decode(uint64_t* keys, uint64_t n, cudaStream_t st);
 int num_sms();

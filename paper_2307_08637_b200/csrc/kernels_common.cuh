@@ -150,18 +150,20 @@ struct TileGeom {
     uint64_t lo, hi, a0;
     uint32_t npairs;
     uint32_t nsingle;
-    uint64_t single[2];
+    uint64_t s0, s1;  // head / tail single (scalars: an indexed array would live in local memory)
     __device__ __forceinline__ void init(const void* base, uint64_t l, uint64_t h) {
         lo = l; hi = h;
         uint64_t par = (((uintptr_t)base) >> 3) & 1;
         a0 = lo + ((lo + par) & 1);
         if (a0 > hi) a0 = hi;
         npairs = (uint32_t)((hi - a0) / 2);
-        nsingle = 0;
-        if (a0 > lo) single[nsingle++] = lo;
-        uint64_t t = a0 + 2ull * npairs;
-        if (t < hi) single[nsingle++] = t;
+        const uint64_t t = a0 + 2ull * npairs;
+        const bool head = a0 > lo, tail = t < hi;
+        nsingle = (uint32_t)head + (uint32_t)tail;
+        s0 = head ? lo : t;
+        s1 = t;
     }
+    __device__ __forceinline__ uint64_t single(uint32_t i) const { return i == 0 ? s0 : s1; }
 };
 
 template <class F>

@@ -7,15 +7,18 @@
 //                    tile range (no per-key kind dispatch, no register spill).
 //   k_hist<K>        fused decode/encode + model inference + shared-memory
 //                    histogram (hardware-aggregated atomics, see hist_add);
-//                    16 keys per thread read with 128-bit loads, persistent.
+//                    8 keys per thread read from TMA tiles, persistent; the
+//                    bucket id of every key is stored (u16, 2 B/key) so the
+//                    scatter does not classify again.
 //   k_scan_children  per-segment exclusive scan -> write cursors; emits base
 //                    case / equality fill / recursion work lists.
-//   k_scatter<K>     re-classify, rank within the tile, claim one range per
-//                    bucket per tile (global atomic), stage the tile grouped by
-//                    bucket in shared memory, write each bucket run coalesced.
+//   k_scatter        one kernel for all model kinds: read keys + ids, rank
+//                    within the tile, claim one range per bucket per tile
+//                    (global atomic), stage the tile grouped by bucket in
+//                    shared memory, write each bucket run coalesced.
 //
-// Learned models stay in global memory (the 32 B/submodel table is L1
-// resident); tree models are copied to shared memory (dependent descent).
+// Model tables (learned: 20 B per submodel; tree payload) are copied to
+// shared memory by k_hist.
 #include <algorithm>
 
 #include "kernels_common.cuh"
@@ -220,31 +223,34 @@ __device__ __forceinline__ TileGeom tile_geom(const LevelParams& p, const KindTi
 // bulk-copied (cp.async.bulk + mbarrier) into shared buffer (t - t0) & 1
 // while the previous tile is processed; head/tail singles are read directly.
 struct TileStream {
-    ulonglong2* buf[2];
+    uint8_t* base;      // two buffers of kTileKeys keys
     uint64_t* bar;      // 2 mbarriers
-    uint32_t phase[2];  // parity of each buffer's next completion (flips only when a copy was issued)
-    __device__ __forceinline__ void init(uint8_t* base, uint64_t* bars) {
-        buf[0] = (ulonglong2*)base;
-        buf[1] = (ulonglong2*)(base + 8 * (size_t)kTileKeys);
+    uint32_t phase;     // bit b: parity of buffer b's next completion (flips only when a copy was issued)
+    __device__ __forceinline__ void init(uint8_t* b, uint64_t* bars) {
+        base = b;
         bar = bars;
-        phase[0] = phase[1] = 0;
+        phase = 0;
         if (threadIdx.x == 0) {
             mbar_init(&bar[0], 1);
             mbar_init(&bar[1], 1);
         }
         __syncthreads();
     }
+    // (arithmetic addressing: a runtime-indexed member array would live in local memory)
+    __device__ __forceinline__ ulonglong2* buf(int b) const {
+        return (ulonglong2*)(base + (size_t)b * (8 * (size_t)kTileKeys));
+    }
     __device__ __forceinline__ void issue(const void* src, const TileGeom& g, int b) {
         if (threadIdx.x == 0 && g.npairs) {
-            mbar_expect_tx(&bar[b], g.npairs * 16);
-            tma_load_1d(buf[b], (const uint64_t*)src + g.a0, g.npairs * 16, &bar[b]);
+            mbar_expect_tx(bar + b, g.npairs * 16);
+            tma_load_1d(buf(b), (const uint64_t*)src + g.a0, g.npairs * 16, bar + b);
         }
     }
     // g.npairs is uniform across the CTA, so every thread flips the same bits
     __device__ __forceinline__ void wait(const TileGeom& g, int b) {
         if (g.npairs) {
-            mbar_wait(&bar[b], phase[b]);
-            phase[b] ^= 1u;
+            mbar_wait(bar + b, (phase >> b) & 1u);
+            phase ^= 1u << b;
         }
     }
 };
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(kPNT, 2) k_hist(LevelParams p) {
             cur = i;
         }
         TS.wait(g, b);
-        const ulonglong2* sp = TS.buf[b];
+        const ulonglong2* sp = TS.buf(b);
         ulonglong2 v[kPPairs];
 #pragma unroll
         for (int j = 0; j < kPPairs; ++j) {
@@ -325,15 +331,31 @@ __global__ void __launch_bounds__(kPNT, 2) k_hist(LevelParams p) {
 #pragma unroll
         for (int q = 0; q < kPItems; ++q)
             hist_add(hist, code[q] & 0x7fffffffu, threadIdx.x + (q >> 1) * kPNT < g.npairs);
+        {  // bucket ids for the scatter (pairs start at an even index iff src is 16 B aligned)
+            const bool al = !(g.a0 & 1);
+#pragma unroll
+            for (int j = 0; j < kPPairs; ++j) {
+                const uint32_t qq = threadIdx.x + j * kPNT;
+                if (qq < g.npairs) {
+                    const uint32_t i0 = (code[2 * j] >> 31) ? kNoMove : code[2 * j];
+                    const uint32_t i1 = (code[2 * j + 1] >> 31) ? kNoMove : code[2 * j + 1];
+                    uint16_t* d = p.ids + g.a0 + 2 * qq;
+                    if (al) *(uint32_t*)d = i0 | (i1 << 16);
+                    else { d[0] = (uint16_t)i0; d[1] = (uint16_t)i1; }
+                }
+            }
+        }
         if (threadIdx.x < g.nsingle) {
-            uint64_t ix = g.single[threadIdx.x];
+            uint64_t ix = g.single(threadIdx.x);
             uint64_t k = ((const uint64_t*)p.src)[ix];
             if (IN_F64) {
                 double d = __longlong_as_double((long long)k);
                 if (isnan(d)) atomicMin(&p.ctrl->nan_index, (unsigned long long)ix);
                 k = encode(d);
             }
-            atomicAdd(&hist[kclassify<KIND>(S, k) & 0x7fffffffu], 1u);
+            const uint32_t c = kclassify<KIND>(S, k);
+            atomicAdd(&hist[c & 0x7fffffffu], 1u);
+            p.ids[ix] = (c >> 31) ? kNoMove : (uint16_t)c;
         }
         __syncthreads();  // buffer b is free for the tile after next
     }
@@ -405,36 +427,45 @@ __global__ void __launch_bounds__(kScanNT) k_scan_children(LevelParams p) {
 }
 
 // ---------------------------------------------------------------- scatter
-template <bool IN_F64, bool MAPPED, uint32_t KIND>
-__global__ void __launch_bounds__(kPNT, 2) k_scatter(LevelParams p, uint32_t nb_cap, const uint32_t* map,
-                                                 uint32_t nmapped) {
+// Shared-memory layout at compile-time offsets (NBC = bucket capacity per
+// segment): no runtime pointer arithmetic to keep live or rematerialise.
+template <uint32_t NBC>
+struct ScatterSmem {
+    uint64_t bars[2];
+    ulonglong2 tiles[2][kTileKeys / 2];  // TMA tile buffers; the consumed one stages the tile
+    long long delta[NBC];                // per bucket: claimed global position - tile-local start
+    uint32_t cnt[NBC + 1];
+    uint16_t sbid[kTileKeys];
+    uint32_t wsum[kPNT / 32 + 1];
+};
+
+// Tile t over all segments of the level.
+__device__ __forceinline__ TileGeom tile_geom_all(const LevelParams& p, uint64_t t, uint32_t& i) {
+    i = find_seg(p.tile_prefix, p.nsegs, t);
+    const SegDesc& sd = p.segs[i];
+    const uint64_t lo = sd.begin + (t - p.tile_prefix[i]) * (uint64_t)kTileKeys;
+    TileGeom g;
+    g.init(p.src, lo, min(lo + kTileKeys, sd.begin + sd.n));
+    return g;
+}
+
+template <bool IN_F64, bool MAPPED, uint32_t NBC>
+__global__ void __launch_bounds__(kPNT, 2) k_scatter(LevelParams p, const uint32_t* map, uint32_t nmapped) {
     extern __shared__ uint4 smem_u4[];
-    uint8_t* q = (uint8_t*)smem_u4;
-    uint64_t* bars = (uint64_t*)q; q += 16;
-    uint8_t* tiles = q; q += 2 * kTileBytes;              // TMA tile buffers; the consumed one stages
-    long long* delta = (long long*)q; q += 8 * (size_t)nb_cap;
-    uint32_t* cnt = (uint32_t*)q; q += 4 * (size_t)(nb_cap + 1);
-    q = (uint8_t*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
-    uint32_t* wsum = (uint32_t*)q; q += 4 * (kPNT / 32 + 1);
-    q = (uint8_t*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
-    uint16_t* sbid = (uint16_t*)q; q += 2 * (size_t)kTileKeys;
-    uint8_t* tree_smem = (uint8_t*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
+    ScatterSmem<NBC>& Q = *(ScatterSmem<NBC>*)smem_u4;
     if (p.ctrl->nan_index != ~0ull) return;
-    KindTiles<KIND> KT;
-    KT.init(p);
-    if (KT.ntiles == 0) return;
-    const uint64_t per = (KT.ntiles + gridDim.x - 1) / gridDim.x;
+    if (p.gate && *p.gate == 0) return;
+    const uint64_t per = (p.ntiles + gridDim.x - 1) / gridDim.x;
     const uint64_t t0 = (uint64_t)blockIdx.x * per;
-    const uint64_t t1 = min(t0 + per, KT.ntiles);
+    const uint64_t t1 = min(t0 + per, p.ntiles);
     if (t0 >= t1) return;
-    for (uint32_t b = threadIdx.x; b <= nb_cap; b += kPNT) cnt[b] = 0;
+    for (uint32_t b = threadIdx.x; b <= NBC; b += kPNT) Q.cnt[b] = 0;
     TileStream TS;
-    TS.init(tiles, bars);
+    TS.init((uint8_t*)Q.tiles, Q.bars);
     uint32_t inext;
-    TileGeom gnext = tile_geom<KIND>(p, KT, t0, inext);
+    TileGeom gnext = tile_geom_all(p, t0, inext);
     TS.issue(p.src, gnext, 0);
     int64_t cur = -1;
-    KState S;
     uint64_t boff = 0;
     uint32_t nbo = 0;
     for (uint64_t tile = t0; tile < t1; ++tile) {
@@ -442,20 +473,30 @@ __global__ void __launch_bounds__(kPNT, 2) k_scatter(LevelParams p, uint32_t nb_
         const uint32_t i = inext;
         const TileGeom g = gnext;
         if (tile + 1 < t1) {
-            gnext = tile_geom<KIND>(p, KT, tile + 1, inext);
+            gnext = tile_geom_all(p, tile + 1, inext);
             TS.issue(p.src, gnext, tb ^ 1);
         }
         if ((int64_t)i != cur) {
-            const SegDesc& sd = p.segs[KT.ks[i]];
+            const SegDesc& sd = p.segs[i];
             boff = sd.bucket_off;
-            kstate_load<KIND>(S, p.models + sd.model_off, tree_smem);
-            nbo = MAPPED ? nmapped : S.nb;
-            __syncthreads();
+            nbo = MAPPED ? nmapped : sd.nb_max;
             cur = i;
         }
+        // ids of this thread's pairs (global, coalesced) while the tile lands
+        const bool al = !(g.a0 & 1);
+        uint32_t idp[kPPairs];
+#pragma unroll
+        for (int j = 0; j < kPPairs; ++j) {
+            const uint32_t qq = threadIdx.x + j * kPNT;
+            idp[j] = 0xffffffffu;
+            if (qq < g.npairs) {
+                const uint16_t* d = p.ids + g.a0 + 2 * qq;
+                idp[j] = al ? *(const uint32_t*)d : ((uint32_t)d[0] | ((uint32_t)d[1] << 16));
+            }
+        }
         TS.wait(g, tb);
-        const ulonglong2* sp = TS.buf[tb];
-        uint64_t* skeys = (uint64_t*)TS.buf[tb];  // staging reuses the consumed tile buffer
+        const ulonglong2* sp = TS.buf(tb);
+        uint64_t* skeys = (uint64_t*)TS.buf(tb);  // staging reuses the consumed tile buffer
         ulonglong2 v[kPPairs];
         uint32_t code[kPItems];  // bucket << 16 | rank; ~0 = not moved
 #pragma unroll
@@ -470,80 +511,74 @@ __global__ void __launch_bounds__(kPNT, 2) k_scatter(LevelParams p, uint32_t nb_
                 v[j].y = encode(__longlong_as_double((long long)v[j].y));
             }
         }
-        classify16<KIND>(S, v, code);
 #pragma unroll
         for (int q = 0; q < kPItems; ++q) {
-            const bool ok = threadIdx.x + (q >> 1) * kPNT < g.npairs && !(code[q] >> 31);
-            uint32_t b = code[q] & 0x7fffffffu;
+            uint32_t b = (q & 1) ? (idp[q >> 1] >> 16) : (idp[q >> 1] & 0xffffu);
+            const bool ok = b != kNoMove;
             if (MAPPED && ok) b = map[b];
-            const uint32_t r = hist_rank_warp(cnt, b, ok);
+            const uint32_t r = hist_rank_warp(Q.cnt, b, ok);
             code[q] = ok ? (b << 16 | r) : 0xffffffffu;
         }
         uint64_t skey = 0;
         uint32_t scode = 0xffffffffu;
         if (threadIdx.x < g.nsingle) {
-            uint64_t k = load_key(p.src, g.single[threadIdx.x], IN_F64);
-            uint32_t c = kclassify<KIND>(S, k);
-            if (!(c >> 31)) {
-                uint32_t b = c & 0x7fffffffu;
+            const uint64_t ix = g.single(threadIdx.x);
+            uint32_t b = p.ids[ix];
+            if (b != kNoMove) {
                 if (MAPPED) b = map[b];
-                scode = b << 16 | atomicAdd(&cnt[b], 1u);
-                skey = k;
+                scode = b << 16 | atomicAdd(&Q.cnt[b], 1u);
+                skey = load_key(p.src, ix, IN_F64);
             }
         }
         __syncthreads();
-        const uint32_t total = block_exclusive_scan_u32<kPNT>(cnt, nbo, wsum);
-        if (threadIdx.x == 0) cnt[nbo] = total;
+        const uint32_t total = block_exclusive_scan_u32<kPNT>(Q.cnt, nbo, Q.wsum);
+        if (threadIdx.x == 0) Q.cnt[nbo] = total;
         __syncthreads();
         {  // claim one output range per non-empty bucket: all atomics in flight
-            constexpr int kCl = (kMaxNB + kPNT - 1) / kPNT;
+            constexpr int kCl = (NBC + kPNT - 1) / kPNT;
             unsigned long long got[kCl];
 #pragma unroll
             for (int q = 0; q < kCl; ++q) {
                 const uint32_t b = threadIdx.x + q * kPNT;
                 got[q] = 0;
                 if (b < nbo) {
-                    const uint32_t c = cnt[b + 1] - cnt[b];
+                    const uint32_t c = Q.cnt[b + 1] - Q.cnt[b];
                     if (c) got[q] = atomicAdd(&p.buckets[boff + b], (unsigned long long)c);
                 }
             }
 #pragma unroll
             for (int q = 0; q < kCl; ++q) {
                 const uint32_t b = threadIdx.x + q * kPNT;
-                if (b < nbo) delta[b] = (long long)got[q] - (long long)cnt[b];
+                if (b < nbo) Q.delta[b] = (long long)got[q] - (long long)Q.cnt[b];
             }
         }
 #pragma unroll
         for (int j = 0; j < kPItems; ++j) {
-            uint32_t c = code[j];
+            const uint32_t c = code[j];
             if (c != 0xffffffffu) {
-                uint32_t pos = cnt[c >> 16] + (c & 0xffffu);
+                const uint32_t pos = Q.cnt[c >> 16] + (c & 0xffffu);
                 skeys[pos] = (j & 1) ? v[j >> 1].y : v[j >> 1].x;
-                sbid[pos] = (uint16_t)(c >> 16);
+                Q.sbid[pos] = (uint16_t)(c >> 16);
             }
         }
         if (scode != 0xffffffffu) {
-            uint32_t pos = cnt[scode >> 16] + (scode & 0xffffu);
+            const uint32_t pos = Q.cnt[scode >> 16] + (scode & 0xffffu);
             skeys[pos] = skey;
-            sbid[pos] = (uint16_t)(scode >> 16);
+            Q.sbid[pos] = (uint16_t)(scode >> 16);
         }
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < kTileKeys / kPNT; ++q) {  // unrolled: loads of all 16 rows in flight
+        for (int q = 0; q < kTileKeys / kPNT; ++q) {  // unrolled: loads of all rows in flight
             const uint32_t j = threadIdx.x + q * kPNT;
-            if (j < total) p.dst[(long long)j + delta[sbid[j]]] = skeys[j];
+            if (j < total) p.dst[(long long)j + Q.delta[Q.sbid[j]]] = skeys[j];
         }
-        for (uint32_t b = threadIdx.x; b <= nbo; b += kPNT) cnt[b] = 0;
+        for (uint32_t b = threadIdx.x; b <= nbo; b += kPNT) Q.cnt[b] = 0;
         fence_proxy_async_smem();  // staging writes (generic proxy) before the next bulk copy into this buffer
         __syncthreads();
     }
 }
 
 // ------------------------------------------------------------- launchers
-static size_t scatter_smem(uint32_t nb_cap, uint32_t tree_cap) {
-    return 16 + 2 * kTileBytes + 8 * (size_t)nb_cap + 4 * (size_t)(nb_cap + 1) + 16 + 4 * (kPNT / 32 + 1) + 16 +
-           2 * (size_t)kTileKeys + 16 + tree_cap;
-}
 static const uint32_t kTreeCap = (uint32_t)((tree_payload_bytes(LSORT_MAX_TREE_DEV, LSORT_MAX_TREE_DEV - 1) + 15) & ~15ull);
 
 void partition_init(int optin) {
@@ -553,14 +588,12 @@ void partition_init(int optin) {
     allow_smem(k_hist<false, kTree>, optin);
     allow_smem(k_hist<true, kRadix>, optin);
     allow_smem(k_hist<false, kRadix>, optin);
-    allow_smem(k_scatter<true, false, kLearned>, optin);
-    allow_smem(k_scatter<false, false, kLearned>, optin);
-    allow_smem(k_scatter<true, false, kTree>, optin);
-    allow_smem(k_scatter<false, false, kTree>, optin);
-    allow_smem(k_scatter<true, false, kRadix>, optin);
-    allow_smem(k_scatter<false, false, kRadix>, optin);
-    allow_smem(k_scatter<true, true, kLearned>, optin);
-    allow_smem(k_scatter<false, true, kLearned>, optin);
+    allow_smem(k_scatter<true, false, 1024>, optin);
+    allow_smem(k_scatter<false, false, 1024>, optin);
+    allow_smem(k_scatter<true, false, kMaxNB>, optin);
+    allow_smem(k_scatter<false, false, kMaxNB>, optin);
+    allow_smem(k_scatter<true, true, 1024>, optin);
+    allow_smem(k_scatter<false, true, 1024>, optin);
     allow_smem(k_scan_children, optin);
 }
 
@@ -592,30 +625,23 @@ void launch_scan_children(const LevelParams& p, cudaStream_t st) {
     k_scan_children<<<p.nsegs, kScanNT, 8 * kMaxNB, st>>>(p);
 }
 
-void launch_scatter(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t nb_cap, uint32_t max_rmi_b, int grid,
-                    cudaStream_t st) {
-    if (kinds & 1) {
-        size_t sm = scatter_smem(nb_cap, 20 * max_rmi_b);
-        if (in_f64) k_scatter<true, false, kLearned><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
-        else k_scatter<false, false, kLearned><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
-    }
-    if (kinds & 2) {
-        size_t sm = scatter_smem(nb_cap, kTreeCap);
-        if (in_f64) k_scatter<true, false, kTree><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
-        else k_scatter<false, false, kTree><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
-    }
-    if (kinds & 4) {
-        size_t sm = scatter_smem(nb_cap, 0);
-        if (in_f64) k_scatter<true, false, kRadix><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
-        else k_scatter<false, false, kRadix><<<grid, kPNT, sm, st>>>(p, nb_cap, nullptr, 0);
+void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid, cudaStream_t st) {
+    if (nb_cap <= 1024) {
+        constexpr size_t sm = sizeof(ScatterSmem<1024>);
+        if (in_f64) k_scatter<true, false, 1024><<<grid, kPNT, sm, st>>>(p, nullptr, 0);
+        else k_scatter<false, false, 1024><<<grid, kPNT, sm, st>>>(p, nullptr, 0);
+    } else {
+        constexpr size_t sm = sizeof(ScatterSmem<kMaxNB>);
+        if (in_f64) k_scatter<true, false, kMaxNB><<<grid, kPNT, sm, st>>>(p, nullptr, 0);
+        else k_scatter<false, false, kMaxNB><<<grid, kPNT, sm, st>>>(p, nullptr, 0);
     }
 }
 
-void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, uint32_t rmi_b,
-                           int grid, cudaStream_t st) {
-    size_t sm = scatter_smem(nmapped, 20 * rmi_b);
-    if (in_f64) k_scatter<true, true, kLearned><<<grid, kPNT, sm, st>>>(p, nmapped, map, nmapped);
-    else k_scatter<false, true, kLearned><<<grid, kPNT, sm, st>>>(p, nmapped, map, nmapped);
+void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,
+                           cudaStream_t st) {
+    constexpr size_t sm = sizeof(ScatterSmem<1024>);
+    if (in_f64) k_scatter<true, true, 1024><<<grid, kPNT, sm, st>>>(p, map, nmapped);
+    else k_scatter<false, true, 1024><<<grid, kPNT, sm, st>>>(p, map, nmapped);
 }
 
 }  // namespace lsort_dev

@@ -8,17 +8,29 @@ namespace lsort_dev {
 
 template <bool IN_F64>
 __global__ void __launch_bounds__(256) k_classify_ids(const uint8_t* model, const void* keys, uint64_t n, uint32_t* ids,
-                                                     unsigned long long* hist) {
+                                                     uint16_t* ids16, unsigned long long* hist) {
     extern __shared__ uint4 smem_u4[];
+    __shared__ uint32_t sh[kMaxNB];
     uint8_t* msm = (uint8_t*)smem_u4;
     load_model_smem(model, msm);
     Classifier C;
     C.init(msm);
+    if (hist) {
+        for (uint32_t b = threadIdx.x; b < C.nb; b += 256) sh[b] = 0;
+        __syncthreads();
+    }
     for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
         uint64_t k = load_key(keys, i, IN_F64);
-        uint32_t b = C.classify_any(k) & 0x7fffffffu;
+        const uint32_t c = C.classify_any(k);
+        const uint32_t b = c & 0x7fffffffu;
         if (ids) ids[i] = b;
-        if (hist) atomicAdd(&hist[b], 1ull);
+        if (ids16) ids16[i] = (c >> 31) ? kNoMove : (uint16_t)b;
+        if (hist) atomicAdd(&sh[b], 1u);
+    }
+    if (hist) {
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < C.nb; b += 256)
+            if (sh[b]) atomicAdd(&hist[b], (unsigned long long)sh[b]);
     }
 }
 
@@ -69,12 +81,12 @@ void kernels_init() {
 }
 
 void launch_classify_ids(const uint8_t* model, const void* keys, uint64_t n, int in_f64, uint32_t* ids,
-                         unsigned long long* hist, int payload, cudaStream_t st) {
+                         uint16_t* ids16, unsigned long long* hist, int payload, cudaStream_t st) {
     int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)g_num_sms * 8);
     if (grid < 1) grid = 1;
     size_t sm = sizeof(ModelHdr) + (size_t)payload + 16;
-    if (in_f64) k_classify_ids<true><<<grid, 256, sm, st>>>(model, keys, n, ids, hist);
-    else k_classify_ids<false><<<grid, 256, sm, st>>>(model, keys, n, ids, hist);
+    if (in_f64) k_classify_ids<true><<<grid, 256, sm, st>>>(model, keys, n, ids, ids16, hist);
+    else k_classify_ids<false><<<grid, 256, sm, st>>>(model, keys, n, ids, ids16, hist);
 }
 
 void launch_verify(const void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st) {
