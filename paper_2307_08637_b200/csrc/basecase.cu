@@ -45,9 +45,45 @@ __global__ void __launch_bounds__(NT) k_base_smem(const BaseItem* items, const u
         if (body) mbar_wait(&S.mbar, phase);
         phase ^= (body ? 1u : 0u);
         __syncthreads();
-        if (n > 1) SS::sort(a, n, S);
+        const uint64_t* res = a;
+        if (n > 1) {
+            SS::sort_fast(a, n, S);
+            res = S.B;
+        }
         for (uint32_t i = threadIdx.x; i < n; i += NT) {
-            const uint64_t v = a[i];
+            const uint64_t v = res[i];
+            if (OUT_F64) __stcs((double*)out + it.begin + i, decode(v));
+            else __stcs((unsigned long long*)out + it.begin + i, (unsigned long long)v);
+        }
+        __syncthreads();
+    }
+}
+
+// Keys read straight into registers (coalesced 8-byte loads, no staging
+// array): shared memory holds only the output array + digit histogram, so
+// three CTAs share an SM and hide each other's load latency. The segment's
+// own input range doubles as scratch for the rare large-digit passes.
+template <int NT, int CAP, int NBMAX, bool OUT_F64>
+__global__ void __launch_bounds__(NT, 2) k_base_reg(const BaseItem* items, const unsigned int* count, uint64_t* src,
+                                                   void* out, Ctrl* ctrl, uint32_t list_cap) {
+    using SS = SmemSort<NT, CAP, NBMAX>;
+    extern __shared__ uint4 smem_u4[];
+    typename SS::SmemR& S = *(typename SS::SmemR*)smem_u4;
+    if (ctrl->nan_index != ~0ull) return;
+    const uint32_t ni = min(*count, list_cap);
+    for (uint32_t e = blockIdx.x; e < ni; e += gridDim.x) {
+        const BaseItem it = items[e];
+        const uint32_t n = (uint32_t)it.n;
+        uint64_t* g = src + it.begin;
+        uint64_t k[SS::ITEMS];
+#pragma unroll
+        for (int i = 0; i < SS::ITEMS; ++i) {
+            const uint32_t j = threadIdx.x + i * NT;
+            k[i] = j < n ? __ldcs((const unsigned long long*)g + j) : 0ull;
+        }
+        SS::sort_regs(k, n, S, g);
+        for (uint32_t i = threadIdx.x; i < n; i += NT) {
+            const uint64_t v = S.B[i];
             if (OUT_F64) __stcs((double*)out + it.begin + i, decode(v));
             else __stcs((unsigned long long*)out + it.begin + i, (unsigned long long)v);
         }
@@ -152,16 +188,16 @@ __global__ void __launch_bounds__(256) k_fill(const FillItem* items, const unsig
 
 // ------------------------------------------------------------- launchers
 // size classes: <= 1024 and <= 4096 keys in shared memory (TMA), <= 16384 in registers
-using SmallSS = SmemSort<128, 1024, 512>;
-using MidSS = SmemSort<512, 4096, 2048>;
+using SmallSS = SmemSort<128, 1024, 1024>;
+using MidSS = SmemSort<512, 4096, 4096>;
 using BaseL = BaseCfg<1024, 16, 8192>;
 static_assert(1024 == kWarpBaseCap, "small base-case class");
 
 void basecase_init(int optin) {
-    allow_smem(k_base_smem<128, 1024, 512, true>, optin);
-    allow_smem(k_base_smem<128, 1024, 512, false>, optin);
-    allow_smem(k_base_smem<512, 4096, 2048, true>, optin);
-    allow_smem(k_base_smem<512, 4096, 2048, false>, optin);
+    allow_smem(k_base_smem<128, 1024, 1024, true>, optin);
+    allow_smem(k_base_smem<128, 1024, 1024, false>, optin);
+    allow_smem(k_base_reg<512, 4096, 4096, true>, optin);
+    allow_smem(k_base_reg<512, 4096, 4096, false>, optin);
     allow_smem(k_base<1024, 16, 8192, true>, optin);
     allow_smem(k_base<1024, 16, 8192, false>, optin);
     allow_smem(k_small_sort<true>, optin);
@@ -171,15 +207,15 @@ void basecase_init(int optin) {
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st) {
     const int nsm = num_sms();
     const int g0 = nsm * 8, g1 = nsm * 2, gl = nsm;
-    const size_t s0 = sizeof(SmallSS::Smem), s1 = sizeof(MidSS::Smem);
+    const size_t s0 = sizeof(SmallSS::Smem), s1 = sizeof(MidSS::SmemR);
     unsigned int* cnt = &p.ctrl->n_base[0];
     if (out_f64) {
-        k_base_smem<128, 1024, 512, true><<<g0, 128, s0, st>>>(p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
-        k_base_smem<512, 4096, 2048, true><<<g1, 512, s1, st>>>(p.base[1], cnt + 1, src, out, p.ctrl, p.list_cap);
+        k_base_smem<128, 1024, 1024, true><<<g0, 128, s0, st>>>(p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
+        k_base_reg<512, 4096, 4096, true><<<g1, 512, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
         k_base<1024, 16, 8192, true><<<gl, 1024, BaseL::smem, st>>>(p.base[2], cnt + 2, src, out, p.ctrl, p.list_cap);
     } else {
-        k_base_smem<128, 1024, 512, false><<<g0, 128, s0, st>>>(p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
-        k_base_smem<512, 4096, 2048, false><<<g1, 512, s1, st>>>(p.base[1], cnt + 1, src, out, p.ctrl, p.list_cap);
+        k_base_smem<128, 1024, 1024, false><<<g0, 128, s0, st>>>(p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
+        k_base_reg<512, 4096, 4096, false><<<g1, 512, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
         k_base<1024, 16, 8192, false><<<gl, 1024, BaseL::smem, st>>>(p.base[2], cnt + 2, src, out, p.ctrl, p.list_cap);
     }
 }

@@ -29,8 +29,20 @@ struct SmemSort {
         uint32_t med_off[kStk], med_len[kStk], large_off[kStk], large_len[kStk];
         uint64_t mbar;
     };
+    // the same without the input array A (keys arrive in registers; scratch
+    // for the rare large-digit passes is supplied by the caller)
+    struct SmemR {
+        uint64_t B[CAP];
+        uint32_t hist[NBMAX + 1];
+        uint16_t R[CAP];
+        uint32_t wsum[NT / 32 + 1];
+        uint64_t red[2 * (NT / 32)];
+        uint32_t n_med, n_large;
+        uint32_t med_off[kStk], med_len[kStk], large_off[kStk], large_len[kStk];
+    };
 
-    __device__ static __forceinline__ void push(Smem& S, uint32_t at, uint32_t l) {
+    template <class SM>
+    __device__ static __forceinline__ void push(SM& S, uint32_t at, uint32_t l) {
         if (l <= (uint32_t)kMedium) {
             uint32_t q = atomicAdd(&S.n_med, 1u);
             S.med_off[q] = at;
@@ -45,7 +57,8 @@ struct SmemSort {
     // one distribution pass over a[off, off+len), staging through b
     // (inlined: as an out-of-line call the shared-memory accesses through `S`
     // become generic loads/stores)
-    __device__ static __forceinline__ void pass(uint64_t* a, uint64_t* b, uint32_t off, uint32_t len, Smem& S) {
+    template <class SM>
+    __device__ static __forceinline__ void pass(uint64_t* a, uint64_t* b, uint32_t off, uint32_t len, SM& S) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         uint64_t mn = ~0ull, mx = 0;
         for (uint32_t i = tid; i < len; i += NT) {
@@ -145,26 +158,205 @@ struct SmemSort {
         __syncwarp();
     }
 
-    // sort a[0,n) (keys already in shared memory)
-    __device__ static void sort(uint64_t* a, uint32_t n, Smem& S) {
-        if (threadIdx.x == 0) { S.n_med = 0; S.n_large = 0; }
-        __syncthreads();
-        pass(a, S.B, 0, n, S);
-        __syncthreads();
+    // Sort the pushed medium / large digit ranges of arr (scratch: same size).
+    template <class SM>
+    __device__ static void drain(uint64_t* arr, uint64_t* scratch, SM& S) {
         const int warp = threadIdx.x >> 5;
         for (;;) {
             const uint32_t nm = S.n_med, nl = S.n_large;
             if (nm == 0 && nl == 0) break;
-            for (uint32_t e = warp; e < nm; e += NT / 32) warp_rank_sort(a + S.med_off[e], S.med_len[e]);
+            for (uint32_t e = warp; e < nm; e += NT / 32) warp_rank_sort(arr + S.med_off[e], S.med_len[e]);
             __syncthreads();
             if (threadIdx.x == 0) S.n_med = 0;
             if (nl == 0) { __syncthreads(); break; }
             const uint32_t off = S.large_off[nl - 1], len = S.large_len[nl - 1];
             __syncthreads();
             if (threadIdx.x == 0) S.n_large = nl - 1;
-            pass(a, S.B, off, len, S);
+            pass(arr, scratch, off, len, S);
             __syncthreads();
         }
+    }
+
+    // sort a[0,n) (keys already in shared memory)
+    __device__ static void sort(uint64_t* a, uint32_t n, Smem& S) {
+        if (threadIdx.x == 0) { S.n_med = 0; S.n_large = 0; }
+        __syncthreads();
+        pass(a, S.B, 0, n, S);
+        __syncthreads();
+        drain(a, S.B, S);
+    }
+
+    __device__ static __forceinline__ void cswap(uint64_t& a, uint64_t& b) {
+        const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+        a = lo;
+        b = hi;
+    }
+
+    // Register-resident first pass (ITEMS = CAP / NT keys per thread, read once
+    // from a): min/max, one counting pass with >= 1 digit per key, placement
+    // into S.B, in-place rank fix of digits with 2..kSmall keys. Then the
+    // remaining digits are drained with S.A as scratch. Result in S.B.
+    // (a may alias S.A: it is not read after the first pass.)
+    static constexpr int ITEMS = CAP / NT;
+    __device__ static void sort_fast(const uint64_t* a, uint32_t n, Smem& S) {
+        static_assert(ITEMS * NT == CAP, "CAP must be a multiple of NT");
+        uint64_t k[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const uint32_t j = threadIdx.x + i * NT;
+            k[i] = j < n ? a[j] : 0ull;
+        }
+        sort_regs(k, n, S, S.A);
+    }
+    // keys j = threadIdx.x + i * NT in k[i]; result in S.B; scratch: >= n keys
+    template <class SM>
+    __device__ static void sort_regs(uint64_t (&k)[ITEMS], uint32_t n, SM& S, uint64_t* scratch) {
+        const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+        uint64_t mn = ~0ull, mx = 0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const uint32_t j = tid + i * NT;
+            if (j < n) {
+                mn = k[i] < mn ? k[i] : mn;
+                mx = k[i] > mx ? k[i] : mx;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t a1 = __shfl_xor_sync(FULL_MASK, mn, o), b1 = __shfl_xor_sync(FULL_MASK, mx, o);
+            mn = a1 < mn ? a1 : mn;
+            mx = b1 > mx ? b1 : mx;
+        }
+        if (lane == 0) { S.red[2 * warp] = mn; S.red[2 * warp + 1] = mx; }
+        if (tid == 0) { S.n_med = 0; S.n_large = 0; }
+        constexpr uint32_t kNb = CAP < NBMAX ? CAP : NBMAX;  // digits: >= 1 per key for n near CAP
+        __syncthreads();
+        {  // every warp combines the per-warp partials with shuffles
+            constexpr int NW = NT / 32;
+            uint64_t a1 = lane < NW ? S.red[2 * lane] : ~0ull, b1 = lane < NW ? S.red[2 * lane + 1] : 0ull;
+#pragma unroll
+            for (int o = NW / 2; o > 0; o >>= 1) {
+                const uint64_t a2 = __shfl_xor_sync(FULL_MASK, a1, o), b2 = __shfl_xor_sync(FULL_MASK, b1, o);
+                a1 = a2 < a1 ? a2 : a1;
+                b1 = b2 > b1 ? b2 : b1;
+            }
+            mn = __shfl_sync(FULL_MASK, a1, 0);
+            mx = __shfl_sync(FULL_MASK, b1, 0);
+        }
+        uint64_t* B = S.B;
+        if (mn == mx) {  // homogeneous: already sorted
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const uint32_t j = tid + i * NT;
+                if (j < n) B[j] = k[i];
+            }
+            __syncthreads();
+            return;
+        }
+        // nb = smallest power of two >= n (capped): <= 1 key per digit on average
+        const uint32_t lgnb = min(32u - __clz(max(n, 2u) - 1u), 31u - __clz(kNb));
+        const uint32_t nb = 1u << lgnb;
+        const uint32_t bits = bitlen64(mx - mn);
+        const uint32_t shift = bits > lgnb ? bits - lgnb : 0;
+        for (uint32_t d = tid; d < nb; d += NT) S.hist[d] = 0;
+        __syncthreads();
+        uint32_t dg[ITEMS], pos[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const uint32_t j = tid + i * NT;
+            dg[i] = (uint32_t)((k[i] - mn) >> shift);
+            pos[i] = j < n ? atomicAdd(&S.hist[dg[i]], 1u) : 0u;
+        }
+        __syncthreads();
+        {  // exclusive scan; digits with > kSmall keys are pushed
+            const uint32_t per = (nb + NT - 1) / NT;
+            const uint32_t lo = min(nb, tid * per), hi = min(nb, lo + per);
+            uint32_t sum = 0;
+            if (per % 4 == 0) {  // 16-byte reads: no bank conflicts between the threads' chunks
+                for (uint32_t d = lo; d < hi; d += 4) {
+                    const uint4 h4 = *(const uint4*)&S.hist[d];
+                    sum += h4.x + h4.y + h4.z + h4.w;
+                }
+            } else {
+                for (uint32_t d = lo; d < hi; ++d) sum += S.hist[d];
+            }
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t w = __shfl_up_sync(FULL_MASK, incl, o);
+                if (lane >= o) incl += w;
+            }
+            if (lane == 31) S.wsum[warp] = incl;
+            __syncthreads();
+            constexpr int NW = NT / 32;
+            uint32_t wv = lane < NW ? S.wsum[lane] : 0u, wincl = wv;
+#pragma unroll
+            for (int o = 1; o < NW; o <<= 1) {
+                const uint32_t w = __shfl_up_sync(FULL_MASK, wincl, o);
+                if (lane >= o) wincl += w;
+            }
+            uint32_t run = incl - sum + __shfl_sync(FULL_MASK, wincl - wv, warp);
+            if (per % 4 == 0) {
+                for (uint32_t d = lo; d < hi; d += 4) {
+                    const uint4 h4 = *(const uint4*)&S.hist[d];
+                    uint4 o4;
+                    o4.x = run; run += h4.x;
+                    o4.y = run; run += h4.y;
+                    o4.z = run; run += h4.z;
+                    o4.w = run; run += h4.w;
+                    *(uint4*)&S.hist[d] = o4;
+                    if (h4.x > (uint32_t)kSmall) push(S, o4.x, h4.x);
+                    if (h4.y > (uint32_t)kSmall) push(S, o4.y, h4.y);
+                    if (h4.z > (uint32_t)kSmall) push(S, o4.z, h4.z);
+                    if (h4.w > (uint32_t)kSmall) push(S, o4.w, h4.w);
+                }
+            } else {
+                for (uint32_t d = lo; d < hi; ++d) {
+                    const uint32_t t = S.hist[d];
+                    S.hist[d] = run;
+                    if (t > (uint32_t)kSmall) push(S, run, t);
+                    run += t;
+                }
+            }
+            if (tid == 0) S.hist[nb] = n;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const uint32_t j = tid + i * NT;
+            if (j < n) {
+                pos[i] += S.hist[dg[i]];
+                B[pos[i]] = k[i];
+            }
+        }
+        __syncthreads();
+        // digits with 2..kSmall keys: sorted in place by the thread that owns
+        // the digit in the scan (fixed-size networks for 2..4 keys: no
+        // warp-divergent per-key loops)
+        {
+            for (uint32_t d = tid; d < nb; d += NT) {  // interleaved: conflict-free hist reads
+                const uint32_t s0 = S.hist[d], c = S.hist[d + 1] - s0;
+                if (c < 2 || c > (uint32_t)kSmall) continue;
+                if (c == 2) {
+                    const uint64_t x0 = B[s0], x1 = B[s0 + 1];
+                    if (x1 < x0) { B[s0] = x1; B[s0 + 1] = x0; }
+                } else if (c <= 4) {
+                    uint64_t x0 = B[s0], x1 = B[s0 + 1], x2 = B[s0 + 2], x3 = c == 4 ? B[s0 + 3] : ~0ull;
+                    cswap(x0, x1); cswap(x2, x3); cswap(x0, x2); cswap(x1, x3); cswap(x1, x2);
+                    B[s0] = x0; B[s0 + 1] = x1; B[s0 + 2] = x2;
+                    if (c == 4) B[s0 + 3] = x3;
+                } else {  // insertion sort (rare: 5..kSmall keys in one digit)
+                    for (uint32_t t = s0 + 1; t < s0 + c; ++t) {
+                        const uint64_t x = B[t];
+                        uint32_t u = t;
+                        while (u > s0 && B[u - 1] > x) { B[u] = B[u - 1]; --u; }
+                        B[u] = x;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        drain(B, scratch, S);
     }
 };
 
