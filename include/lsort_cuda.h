@@ -122,11 +122,13 @@ typedef struct lsort_stats {
 
 #define LSORT_FLAG_PHASE_TIMING 1u
 /* cfg->flags: build every model exactly by the reference's Alg. 5 policy
- * (PAPER.md:389-415). Without it the GPU replaces a learned model that puts
- * more than 1/16 of its own sorted sample into one bucket by a splitter tree
- * over that sample (bucket imbalance costs whole extra passes on the GPU).
- * The sorted output is identical either way; lsort_cuda_build_model always
- * runs strict. */
+ * (PAPER.md:389-415). Without it the GPU policy (1) lets segments of
+ * >= min(min_rmi_input, 32768) keys take the learned branch (a learned model
+ * classifies faster than a splitter-tree descent on the GPU) and (2) replaces
+ * a learned model that puts more than 1/16 of its own sorted sample into one
+ * bucket by a splitter tree over that sample (bucket imbalance costs whole
+ * extra passes). The sorted output is identical either way;
+ * lsort_cuda_build_model always runs strict. */
 #define LSORT_FLAG_STRICT_POLICY 2u
 
 typedef struct lsort_ctx lsort_ctx;

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(NT) k_base_smem(const BaseItem* items, const u
 // three CTAs share an SM and hide each other's load latency. The segment's
 // own input range doubles as scratch for the rare large-digit passes.
 template <int NT, int CAP, int NBMAX, bool OUT_F64>
-__global__ void __launch_bounds__(NT, 2) k_base_reg(const BaseItem* items, const unsigned int* count, uint64_t* src,
+__global__ void __launch_bounds__(NT, 3) k_base_reg(const BaseItem* items, const unsigned int* count, uint64_t* src,
                                                    void* out, Ctrl* ctrl, uint32_t list_cap) {
     using SS = SmemSort<NT, CAP, NBMAX>;
     extern __shared__ uint4 smem_u4[];
@@ -189,15 +189,15 @@ __global__ void __launch_bounds__(256) k_fill(const FillItem* items, const unsig
 // ------------------------------------------------------------- launchers
 // size classes: <= 1024 and <= 4096 keys in shared memory (TMA), <= 16384 in registers
 using SmallSS = SmemSort<128, 1024, 1024>;
-using MidSS = SmemSort<512, 4096, 4096>;
+using MidSS = SmemSort<256, 4096, 4096>;
 using BaseL = BaseCfg<1024, 16, 8192>;
 static_assert(1024 == kWarpBaseCap, "small base-case class");
 
 void basecase_init(int optin) {
     allow_smem(k_base_smem<128, 1024, 1024, true>, optin);
     allow_smem(k_base_smem<128, 1024, 1024, false>, optin);
-    allow_smem(k_base_reg<512, 4096, 4096, true>, optin);
-    allow_smem(k_base_reg<512, 4096, 4096, false>, optin);
+    allow_smem(k_base_reg<256, 4096, 4096, true>, optin);
+    allow_smem(k_base_reg<256, 4096, 4096, false>, optin);
     allow_smem(k_base<1024, 16, 8192, true>, optin);
     allow_smem(k_base<1024, 16, 8192, false>, optin);
     allow_smem(k_small_sort<true>, optin);
@@ -206,16 +206,16 @@ void basecase_init(int optin) {
 
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st) {
     const int nsm = num_sms();
-    const int g0 = nsm * 8, g1 = nsm * 2, gl = nsm;
+    const int g0 = nsm * 8, g1 = nsm * 3, gl = nsm;
     const size_t s0 = sizeof(SmallSS::Smem), s1 = sizeof(MidSS::SmemR);
     unsigned int* cnt = &p.ctrl->n_base[0];
     if (out_f64) {
         k_base_smem<128, 1024, 1024, true><<<g0, 128, s0, st>>>(p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
-        k_base_reg<512, 4096, 4096, true><<<g1, 512, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        k_base_reg<256, 4096, 4096, true><<<g1, 256, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
         k_base<1024, 16, 8192, true><<<gl, 1024, BaseL::smem, st>>>(p.base[2], cnt + 2, src, out, p.ctrl, p.list_cap);
     } else {
         k_base_smem<128, 1024, 1024, false><<<g0, 128, s0, st>>>(p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
-        k_base_reg<512, 4096, 4096, false><<<g1, 512, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        k_base_reg<256, 4096, 4096, false><<<g1, 256, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
         k_base<1024, 16, 8192, false><<<gl, 1024, BaseL::smem, st>>>(p.base[2], cnt + 2, src, out, p.ctrl, p.list_cap);
     }
 }

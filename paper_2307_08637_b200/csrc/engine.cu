@@ -162,9 +162,18 @@ void validate_cfg(const lsort_cfg& c) {
         throw LsortError{LSORT_EINVAL, "insertion_base_case must be <= radix_base_case"};
 }
 
+// GPU policy (unless LSORT_FLAG_STRICT_POLICY): segments from kGpuMinRmi keys
+// up may take the learned branch of Alg. 5 -- on the GPU a learned model
+// classifies at ~2/3 of the cost of a splitter-tree descent, and poor learned
+// models are caught by the quality check. Sorted output is the same.
+constexpr uint64_t kGpuMinRmi = 32768;
+uint64_t effective_min_rmi(const lsort_cfg& c) {
+    return (c.flags & LSORT_FLAG_STRICT_POLICY) ? c.min_rmi_input : std::min<uint64_t>(c.min_rmi_input, kGpuMinRmi);
+}
+
 DevCfg dev_cfg(const lsort_cfg& c) {
     DevCfg d;
-    d.min_rmi_input = c.min_rmi_input;
+    d.min_rmi_input = effective_min_rmi(c);
     d.max_dup = c.max_duplicate_fraction;
     d.sample_fraction = c.sample_fraction;
     d.first_sample_cap = c.first_sample_cap;
@@ -186,7 +195,7 @@ struct Engine {
     // policy can pick the learned branch)
     uint64_t sample_need(const SegPlan& s) const {
         uint64_t s1 = sample_size_host(cfg.sample_fraction, cfg.first_sample_cap, s.n);
-        uint64_t s2 = s.n >= cfg.min_rmi_input ? sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, s.n) : 0;
+        uint64_t s2 = s.n >= effective_min_rmi(cfg) ? sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, s.n) : 0;
         return std::max(s1, s2);
     }
     // 0 small model CTA, 1 mid model CTA, 2 big pipeline
@@ -419,7 +428,7 @@ struct Engine {
                 else if (mc == 1) mids.push_back(i);
                 else hi[nsmall++] = i;
                 if (s.flags & kSegForceRadix) kinds |= 4u;
-                else kinds |= (s.n >= cfg.min_rmi_input ? 1u : 0u) | 2u;
+                else kinds |= (s.n >= effective_min_rmi(cfg) ? 1u : 0u) | 2u;
             }
             hp[ns] = ntiles;
             const uint64_t list_cap = nbuckets;

@@ -25,7 +25,7 @@ struct SmemSort {
         uint16_t R[CAP];
         uint32_t wsum[NT / 32 + 1];
         uint64_t red[2 * (NT / 32)];
-        uint32_t n_med, n_large;
+        uint32_t n_med, n_large, n_l4, n_l16;
         uint32_t med_off[kStk], med_len[kStk], large_off[kStk], large_len[kStk];
         uint64_t mbar;
     };
@@ -37,7 +37,7 @@ struct SmemSort {
         uint16_t R[CAP];
         uint32_t wsum[NT / 32 + 1];
         uint64_t red[2 * (NT / 32)];
-        uint32_t n_med, n_large;
+        uint32_t n_med, n_large, n_l4, n_l16;
         uint32_t med_off[kStk], med_len[kStk], large_off[kStk], large_len[kStk];
     };
 
@@ -228,7 +228,7 @@ struct SmemSort {
             mx = b1 > mx ? b1 : mx;
         }
         if (lane == 0) { S.red[2 * warp] = mn; S.red[2 * warp + 1] = mx; }
-        if (tid == 0) { S.n_med = 0; S.n_large = 0; }
+        if (tid == 0) { S.n_med = 0; S.n_large = 0; S.n_l4 = 0; S.n_l16 = 0; }
         constexpr uint32_t kNb = CAP < NBMAX ? CAP : NBMAX;  // digits: >= 1 per key for n near CAP
         __syncthreads();
         {  // every warp combines the per-warp partials with shuffles
@@ -260,12 +260,12 @@ struct SmemSort {
         const uint32_t shift = bits > lgnb ? bits - lgnb : 0;
         for (uint32_t d = tid; d < nb; d += NT) S.hist[d] = 0;
         __syncthreads();
-        uint32_t dg[ITEMS], pos[ITEMS];
+        uint32_t dp[ITEMS];  // digit << 16 | rank within the digit
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const uint32_t j = tid + i * NT;
-            dg[i] = (uint32_t)((k[i] - mn) >> shift);
-            pos[i] = j < n ? atomicAdd(&S.hist[dg[i]], 1u) : 0u;
+            const uint32_t d = (uint32_t)((k[i] - mn) >> shift);
+            dp[i] = j < n ? (d << 16 | atomicAdd(&S.hist[d], 1u)) : 0u;
         }
         __syncthreads();
         {  // exclusive scan; digits with > kSmall keys are pushed
@@ -325,33 +325,51 @@ struct SmemSort {
         for (int i = 0; i < ITEMS; ++i) {
             const uint32_t j = tid + i * NT;
             if (j < n) {
-                pos[i] += S.hist[dg[i]];
-                B[pos[i]] = k[i];
+                B[S.hist[dp[i] >> 16] + (dp[i] & 0xffffu)] = k[i];
             }
         }
         __syncthreads();
-        // digits with 2..kSmall keys: sorted in place by the thread that owns
-        // the digit in the scan (fixed-size networks for 2..4 keys: no
-        // warp-divergent per-key loops)
+        // digits with 2..kSmall keys, compacted into two lists in S.R (free
+        // until the drain): 2..4 keys (fixed 4-key network, pad ~0) from the
+        // front, 5..kSmall keys (insertion sort, rare) from the back; then all
+        // lanes work on list entries instead of idling on 0/1-key digits
         {
-            for (uint32_t d = tid; d < nb; d += NT) {  // interleaved: conflict-free hist reads
-                const uint32_t s0 = S.hist[d], c = S.hist[d + 1] - s0;
-                if (c < 2 || c > (uint32_t)kSmall) continue;
-                if (c == 2) {
-                    const uint64_t x0 = B[s0], x1 = B[s0 + 1];
-                    if (x1 < x0) { B[s0] = x1; B[s0 + 1] = x0; }
-                } else if (c <= 4) {
-                    uint64_t x0 = B[s0], x1 = B[s0 + 1], x2 = B[s0 + 2], x3 = c == 4 ? B[s0 + 3] : ~0ull;
-                    cswap(x0, x1); cswap(x2, x3); cswap(x0, x2); cswap(x1, x3); cswap(x1, x2);
-                    B[s0] = x0; B[s0 + 1] = x1; B[s0 + 2] = x2;
-                    if (c == 4) B[s0 + 3] = x3;
-                } else {  // insertion sort (rare: 5..kSmall keys in one digit)
-                    for (uint32_t t = s0 + 1; t < s0 + c; ++t) {
-                        const uint64_t x = B[t];
-                        uint32_t u = t;
-                        while (u > s0 && B[u - 1] > x) { B[u] = B[u - 1]; --u; }
-                        B[u] = x;
-                    }
+            const unsigned lt = (1u << lane) - 1u;
+            for (uint32_t r = 0; r < (nb + NT - 1) / NT; ++r) {  // CTA-uniform trip count
+                const uint32_t d = tid + r * NT;
+                uint32_t s0 = 0, c = 0;
+                if (d < nb) { s0 = S.hist[d]; c = S.hist[d + 1] - s0; }
+                const bool t4 = c >= 2 && c <= 4, t16 = c > 4 && c <= (uint32_t)kSmall;
+                const unsigned m4 = __ballot_sync(FULL_MASK, t4), m16 = __ballot_sync(FULL_MASK, t16);
+                uint32_t b4 = 0, b16 = 0;
+                if (lane == 0) {
+                    if (m4) b4 = atomicAdd(&S.n_l4, (uint32_t)__popc(m4));
+                    if (m16) b16 = atomicAdd(&S.n_l16, (uint32_t)__popc(m16));
+                }
+                b4 = __shfl_sync(FULL_MASK, b4, 0);
+                b16 = __shfl_sync(FULL_MASK, b16, 0);
+                if (t4) S.R[b4 + __popc(m4 & lt)] = (uint16_t)(s0 << 2 | (c - 1));
+                if (t16) S.R[CAP - 1 - (b16 + __popc(m16 & lt))] = (uint16_t)(s0 << 4 | (c - 1));
+            }
+            __syncthreads();
+            const uint32_t n4 = S.n_l4, n16 = S.n_l16;
+            for (uint32_t e = tid; e < n4; e += NT) {
+                const uint32_t v = S.R[e], s0 = v >> 2, c = (v & 3u) + 1;
+                uint64_t x0 = B[s0], x1 = B[s0 + 1];
+                uint64_t x2 = c >= 3 ? B[s0 + 2] : ~0ull, x3 = c == 4 ? B[s0 + 3] : ~0ull;
+                cswap(x0, x1); cswap(x2, x3); cswap(x0, x2); cswap(x1, x3); cswap(x1, x2);
+                B[s0] = x0;
+                B[s0 + 1] = x1;
+                if (c >= 3) B[s0 + 2] = x2;
+                if (c == 4) B[s0 + 3] = x3;
+            }
+            for (uint32_t e = tid; e < n16; e += NT) {
+                const uint32_t v = S.R[CAP - 1 - e], s0 = v >> 4, c = (v & 15u) + 1;
+                for (uint32_t t = s0 + 1; t < s0 + c; ++t) {
+                    const uint64_t x = B[t];
+                    uint32_t u = t;
+                    while (u > s0 && B[u - 1] > x) { B[u] = B[u - 1]; --u; }
+                    B[u] = x;
                 }
             }
         }
