@@ -411,7 +411,10 @@ __device__ void sample_sorted(const SegDesc& sd, const void* src, uint64_t seed,
     for (uint32_t i = threadIdx.x; i < cnt; i += NT)
         S.sort.A[i] = load_key(src, sd.begin + sample_index(seed, j0 + i, sd.n), IN_F64);
     __syncthreads();
-    if (cnt > 1) MC::SS::sort(S.sort.A, cnt, S.sort);
+    if (cnt > 1) {
+        MC::SS::sort_fast(S.sort.A, cnt, S.sort);  // -> S.sort.B
+        for (uint32_t i = threadIdx.x; i < cnt; i += NT) S.sort.A[i] = S.sort.B[i];
+    }
     __syncthreads();
 }
 
@@ -492,7 +495,7 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
 }
 
 template <bool IN_F64, class MC, int NT>
-__global__ void __launch_bounds__(NT) k_build_models(const SegDesc* segs, const uint32_t* idx, const void* src,
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) k_build_models(const SegDesc* segs, const uint32_t* idx, const void* src,
                                                     uint8_t* models, DevCfg cfg) {
     extern __shared__ uint4 smem_u4[];
     typename MC::Smem& S = *(typename MC::Smem*)smem_u4;
@@ -501,7 +504,7 @@ __global__ void __launch_bounds__(NT) k_build_models(const SegDesc* segs, const 
 }
 
 template <bool IN_F64>
-__global__ void __launch_bounds__(512) k_first_sample(const SegDesc* seg, const void* src, uint8_t* models,
+__global__ void __launch_bounds__(512, 1) k_first_sample(const SegDesc* seg, const void* src, uint8_t* models,
                                                      DevCfg cfg, uint8_t* aux, uint32_t aux_budget, uint32_t* gate) {
     extern __shared__ uint4 smem_u4[];
     ModelMid::Smem& S = *(ModelMid::Smem*)smem_u4;
@@ -838,7 +841,10 @@ __global__ void __launch_bounds__(512) k_block_sort(uint64_t* keys, uint32_t n) 
     ModelMid::Smem& S = *(ModelMid::Smem*)smem_u4;
     for (uint32_t i = threadIdx.x; i < n; i += 512) S.sort.A[i] = keys[i];
     __syncthreads();
-    if (n > 1) ModelMid::SS::sort(S.sort.A, n, S.sort);
+    if (n > 1) {
+        ModelMid::SS::sort_fast(S.sort.A, n, S.sort);
+        for (uint32_t i = threadIdx.x; i < n; i += 512) S.sort.A[i] = S.sort.B[i];
+    }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < n; i += 512) keys[i] = S.sort.A[i];
 }

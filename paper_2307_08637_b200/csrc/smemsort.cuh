@@ -14,6 +14,7 @@ namespace lsort_dev {
 // for larger digits. Decode fused into the coalesced store.
 template <int NT, int CAP, int NBMAX>
 struct SmemSort {
+    static_assert(NBMAX <= 65536, "digit indices are kept in 16 bits");
     static constexpr int kSmall = 16;
     static constexpr int kMedium = 256;
     static constexpr int kStk = CAP / (kSmall + 1) + 2;
@@ -348,13 +349,13 @@ struct SmemSort {
                 }
                 b4 = __shfl_sync(FULL_MASK, b4, 0);
                 b16 = __shfl_sync(FULL_MASK, b16, 0);
-                if (t4) S.R[b4 + __popc(m4 & lt)] = (uint16_t)(s0 << 2 | (c - 1));
-                if (t16) S.R[CAP - 1 - (b16 + __popc(m16 & lt))] = (uint16_t)(s0 << 4 | (c - 1));
+                if (t4) S.R[b4 + __popc(m4 & lt)] = (uint16_t)d;  // digit index (< NBMAX <= 65536)
+                if (t16) S.R[CAP - 1 - (b16 + __popc(m16 & lt))] = (uint16_t)d;
             }
             __syncthreads();
             const uint32_t n4 = S.n_l4, n16 = S.n_l16;
             for (uint32_t e = tid; e < n4; e += NT) {
-                const uint32_t v = S.R[e], s0 = v >> 2, c = (v & 3u) + 1;
+                const uint32_t d = S.R[e], s0 = S.hist[d], c = S.hist[d + 1] - s0;
                 uint64_t x0 = B[s0], x1 = B[s0 + 1];
                 uint64_t x2 = c >= 3 ? B[s0 + 2] : ~0ull, x3 = c == 4 ? B[s0 + 3] : ~0ull;
                 cswap(x0, x1); cswap(x2, x3); cswap(x0, x2); cswap(x1, x3); cswap(x1, x2);
@@ -364,7 +365,7 @@ struct SmemSort {
                 if (c == 4) B[s0 + 3] = x3;
             }
             for (uint32_t e = tid; e < n16; e += NT) {
-                const uint32_t v = S.R[CAP - 1 - e], s0 = v >> 4, c = (v & 15u) + 1;
+                const uint32_t d = S.R[CAP - 1 - e], s0 = S.hist[d], c = S.hist[d + 1] - s0;
                 for (uint32_t t = s0 + 1; t < s0 + c; ++t) {
                     const uint64_t x = B[t];
                     uint32_t u = t;
