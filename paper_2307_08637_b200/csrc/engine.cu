@@ -336,7 +336,7 @@ struct Engine {
         q.kplan = N->kplan.as<KindPlan>();
         q.kstride = 1;
         const int nsm = num_sms();
-        const int g = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
+        const int g = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
         launch_kind_plan(q, st);
         launch_hist(q, 0, 2u, 0, g, st);
         launch_scan_children(q, st);
@@ -485,8 +485,8 @@ struct Engine {
             big_models(bigs, p.segs, segs, hs, src, src_f64);
             // ---- partition
             const int nsm = num_sms();
-            int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
-            int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * 2);
+            int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
+            int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
             const int nk = __builtin_popcount(kinds);
             mark(1);
             launch_kind_plan(p, st);
@@ -1103,7 +1103,7 @@ int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int 
         p.ktp = C->ktp.as<uint64_t>();
         p.kplan = C->kplan.as<KindPlan>();
         p.kstride = 1;
-        int grid = (int)std::min<uint64_t>(pref[1], (uint64_t)num_sms() * 3);
+        int grid = (int)std::min<uint64_t>(pref[1], (uint64_t)num_sms() * kPartPerSM);
         p.ids = C->ids.as<uint16_t>();
         launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, grid, C->stream);
         CU(cudaStreamSynchronize(C->stream));

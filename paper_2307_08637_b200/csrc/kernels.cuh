@@ -92,6 +92,7 @@ constexpr uint32_t kPoorShare = 16;
 constexpr int kTileKeys = 4096;     // keys per classify/scatter tile
 constexpr uint16_t kNoMove = 0xffff;
 constexpr int kPartNT = 512;        // threads per classify/scatter CTA
+constexpr int kPartPerSM = 2;       // resident classify/scatter CTAs per SM
 constexpr int kRadixBits = 10;      // fallback radix model: 1024 buckets
 constexpr uint32_t kSmallSampleCap = 8192;   // samples sortable in one model CTA
 constexpr uint32_t kModelSmallCap = 2048;    // samples of the small model CTA

@@ -26,13 +26,15 @@ constexpr uint32_t kMaxNB = 2048; // max output buckets of any partition model
 
 // keys.hpp:24-27
 __device__ __forceinline__ uint64_t encode(double x) {
-    uint64_t b = (uint64_t)__double_as_longlong(x);
-    return (b & kSign) ? ~b : (b ^ kSign);
+    // branch-free: negative -> ~b, else b ^ sign  (mask = all ones iff negative)
+    const long long b = __double_as_longlong(x);
+    return (uint64_t)(b ^ ((b >> 63) | (long long)kSign));
 }
 // keys.hpp:29-32
 __device__ __forceinline__ double decode(uint64_t k) {
-    uint64_t b = (k & kSign) ? (k ^ kSign) : ~k;
-    return __longlong_as_double((long long)b);
+    // branch-free inverse: sign bit set -> k ^ sign, else ~k
+    const long long b = (long long)k;
+    return __longlong_as_double(b ^ ((~b >> 63) | (long long)kSign));
 }
 // rng.hpp:13-18
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {

@@ -26,7 +26,7 @@
 
 namespace lsort_dev {
 
-constexpr int kPNT = 512;                 // threads per partition CTA
+constexpr int kPNT = kPartNT;             // threads per partition CTA
 constexpr int kPItems = 8;                // keys per thread per tile
 constexpr int kPPairs = kPItems / 2;      // 128-bit loads per thread per tile
 static_assert(kPNT * kPItems == kTileKeys, "tile geometry");
@@ -258,7 +258,7 @@ constexpr size_t kTileBytes = 8 * (size_t)kTileKeys;
 
 // ------------------------------------------------------- classify + hist
 template <bool IN_F64, uint32_t KIND>
-__global__ void __launch_bounds__(kPNT, 2) k_hist(LevelParams p) {
+__global__ void __launch_bounds__(kPNT, kPartPerSM) k_hist(LevelParams p) {
     extern __shared__ uint4 smem_u4[];
     uint8_t* sm = (uint8_t*)smem_u4;
     uint64_t* bars = (uint64_t*)sm;                          // 2 mbarriers (16 B)
@@ -450,7 +450,7 @@ __device__ __forceinline__ TileGeom tile_geom_all(const LevelParams& p, uint64_t
 }
 
 template <bool IN_F64, bool MAPPED, uint32_t NBC>
-__global__ void __launch_bounds__(kPNT, 2) k_scatter(LevelParams p, const uint32_t* map, uint32_t nmapped) {
+__global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, const uint32_t* map, uint32_t nmapped) {
     extern __shared__ uint4 smem_u4[];
     ScatterSmem<NBC>& Q = *(ScatterSmem<NBC>*)smem_u4;
     if (p.ctrl->nan_index != ~0ull) return;
