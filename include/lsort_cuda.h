@@ -130,6 +130,11 @@ typedef struct lsort_stats {
  * extra passes). The sorted output is identical either way;
  * lsort_cuda_build_model always runs strict. */
 #define LSORT_FLAG_STRICT_POLICY 2u
+/* cfg->flags: run the last distribution level fused with the base case in
+ * distributed shared memory (thread-block clusters, cluster.cu) for segments
+ * of 16 Ki..128 Ki keys. Experimental: exact, but not yet faster than the
+ * classify + scatter + base-case path. */
+#define LSORT_FLAG_CLUSTER 4u
 
 typedef struct lsort_ctx lsort_ctx;
 

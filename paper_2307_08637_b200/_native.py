@@ -19,6 +19,7 @@ MAX_TREE = 1024
 MAX_RMI = 2048
 FLAG_PHASE_TIMING = 1
 FLAG_STRICT_POLICY = 2  # reference Alg. 5 models only (no GPU quality fallback)
+FLAG_CLUSTER = 4  # experimental fused cluster (DSMEM) last level
 
 
 class lsort_cfg(C.Structure):

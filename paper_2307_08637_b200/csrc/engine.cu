@@ -116,7 +116,7 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws, ids;
+        kseg, ktp, kplan, qws, ids, clus;
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
     std::unique_ptr<lsort_ctx> nested;
     // lanes: workspaces + streams on which the models of the big segments of
@@ -395,9 +395,22 @@ struct Engine {
             uint32_t max_payload = 0, max_nb = 0, nsmall = 0, kinds = 0, max_rmi_b = 0;
             std::vector<uint32_t> mids;
             std::vector<uint32_t> bigs;
+            // segments of the last distribution level that fit a cluster go to the
+            // fused DSMEM kernel (cluster.cu); the rest are partitioned here
+            const bool use_cluster = level >= 1 && !src_f64 && cluster_available() &&
+                                     (cfg.flags & LSORT_FLAG_CLUSTER) && cap >= 16384;
+            std::vector<BaseItem> clus;
+            std::vector<SegPlan> psegs;
+            psegs.reserve(ns);
             for (uint32_t i = 0; i < ns; ++i) {
                 const SegPlan& s = segs[i];
-                SegDesc& d = hs[i];
+                if (use_cluster && s.n > cap && s.n <= kClCap) {
+                    clus.push_back(BaseItem{s.begin, s.n});
+                    continue;
+                }
+                const uint32_t j = (uint32_t)psegs.size();
+                psegs.push_back(s);
+                SegDesc& d = hs[j];
                 d.begin = s.begin;
                 d.n = s.n;
                 d.depth = s.depth;
@@ -421,35 +434,41 @@ struct Engine {
                 nbuckets += nb;
                 max_payload = std::max(max_payload, payload);
                 max_nb = std::max(max_nb, nb);
-                hp[i] = ntiles;
+                hp[j] = ntiles;
                 ntiles += (s.n + kTileKeys - 1) / kTileKeys;
                 const int mc = model_class(s);
-                if (mc == 2) bigs.push_back(i);
-                else if (mc == 1) mids.push_back(i);
-                else hi[nsmall++] = i;
+                if (mc == 2) bigs.push_back(j);
+                else if (mc == 1) mids.push_back(j);
+                else hi[nsmall++] = j;
                 if (s.flags & kSegForceRadix) kinds |= 4u;
                 else kinds |= (s.n >= effective_min_rmi(cfg) ? 1u : 0u) | 2u;
             }
-            hp[ns] = ntiles;
-            const uint64_t list_cap = nbuckets;
-            if (!C->segs.ensure(ns * sizeof(SegDesc)) || !C->tile_prefix.ensure((ns + 1) * 8) ||
-                !C->idx.ensure(ns * 4) || !C->models.ensure(model_bytes) || !C->buckets.ensure(nbuckets * 8) ||
-                !C->rec.ensure(list_cap * sizeof(SegOut)) || !C->fill.ensure(list_cap * sizeof(FillItem)) ||
-                !C->base[0].ensure(list_cap * sizeof(BaseItem)) || !C->base[1].ensure(list_cap * sizeof(BaseItem)) ||
-                !C->base[2].ensure(list_cap * sizeof(BaseItem)) || !C->kseg.ensure(3 * (size_t)ns * 4 + 16) ||
-                !C->ktp.ensure(3 * ((size_t)ns + 1) * 8) || !C->kplan.ensure(3 * sizeof(KindPlan)))
+            const uint32_t np = (uint32_t)psegs.size();
+            const uint32_t ncl = (uint32_t)clus.size();
+            hp[np] = ntiles;
+            const uint64_t list_cap = nbuckets + (uint64_t)ncl * kClSub;
+            if (!C->segs.ensure(np * sizeof(SegDesc) + 16) || !C->tile_prefix.ensure((np + 1) * 8) ||
+                !C->idx.ensure(np * 4 + 4) || !C->models.ensure(model_bytes + 16) ||
+                !C->buckets.ensure(nbuckets * 8 + 8) || !C->rec.ensure(list_cap * sizeof(SegOut)) ||
+                !C->fill.ensure(list_cap * sizeof(FillItem)) || !C->base[0].ensure(list_cap * sizeof(BaseItem)) ||
+                !C->base[1].ensure(list_cap * sizeof(BaseItem)) || !C->base[2].ensure(list_cap * sizeof(BaseItem)) ||
+                !C->kseg.ensure(3 * (size_t)np * 4 + 16) || !C->ktp.ensure(3 * ((size_t)np + 1) * 8) ||
+                !C->kplan.ensure(3 * sizeof(KindPlan)) || !C->clus.ensure(ncl * sizeof(BaseItem) + 16))
                 throw LsortError{LSORT_ENOMEM, "level workspace"};
-            CU(cudaMemcpyAsync(C->segs.p, hs, ns * sizeof(SegDesc), cudaMemcpyHostToDevice, st));
-            CU(cudaMemcpyAsync(C->tile_prefix.p, hp, (ns + 1) * 8, cudaMemcpyHostToDevice, st));
+            if (np) {
+                CU(cudaMemcpyAsync(C->segs.p, hs, np * sizeof(SegDesc), cudaMemcpyHostToDevice, st));
+                CU(cudaMemcpyAsync(C->tile_prefix.p, hp, (np + 1) * 8, cudaMemcpyHostToDevice, st));
+            }
+            if (ncl) CU(cudaMemcpyAsync(C->clus.p, clus.data(), ncl * sizeof(BaseItem), cudaMemcpyHostToDevice, st));
             for (uint32_t i = 0; i < mids.size(); ++i) hi[nsmall + i] = mids[i];
             const uint32_t nmid = (uint32_t)mids.size();
             if (nsmall + nmid) CU(cudaMemcpyAsync(C->idx.p, hi, (nsmall + nmid) * 4, cudaMemcpyHostToDevice, st));
-            CU(cudaMemsetAsync(C->buckets.p, 0, nbuckets * 8, st));
+            if (nbuckets) CU(cudaMemsetAsync(C->buckets.p, 0, nbuckets * 8, st));
             CU(cudaMemsetAsync(&dctrl->n_rec, 0, offsetof(Ctrl, keys_fill) - offsetof(Ctrl, n_rec), st));
 
             LevelParams p{};
             p.segs = C->segs.as<SegDesc>();
-            p.nsegs = ns;
+            p.nsegs = np;
             p.tile_prefix = C->tile_prefix.as<uint64_t>();
             p.ntiles = ntiles;
             p.models = C->models.as<uint8_t>();
@@ -469,7 +488,7 @@ struct Engine {
             p.kseg = C->kseg.as<uint32_t>();
             p.ktp = C->ktp.as<uint64_t>();
             p.kplan = C->kplan.as<KindPlan>();
-            p.kstride = ns;
+            p.kstride = np;
 
             const bool timing = (cfg.flags & LSORT_FLAG_PHASE_TIMING) && stats;
             auto mark = [&](int i) {
@@ -477,29 +496,41 @@ struct Engine {
             };
             mark(0);
             // ---- models
-            launch_build_models(p.segs, C->idx.as<uint32_t>(), nsmall, src, src_f64, C->models.as<uint8_t>(), dc, 0,
-                                st);
-            launch_build_models(p.segs, C->idx.as<uint32_t>() + nsmall, nmid, src, src_f64, C->models.as<uint8_t>(),
-                                dc, 1, st);
-            launched((nsmall ? 1 : 0) + (nmid ? 1 : 0));
-            big_models(bigs, p.segs, segs, hs, src, src_f64);
-            // ---- partition
             const int nsm = num_sms();
-            int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
-            int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
+            if (np) {
+                launch_build_models(p.segs, C->idx.as<uint32_t>(), nsmall, src, src_f64, C->models.as<uint8_t>(), dc,
+                                    0, st);
+                launch_build_models(p.segs, C->idx.as<uint32_t>() + nsmall, nmid, src, src_f64,
+                                    C->models.as<uint8_t>(), dc, 1, st);
+                launched((nsmall ? 1 : 0) + (nmid ? 1 : 0));
+                big_models(bigs, p.segs, psegs, hs, src, src_f64);
+            }
+            // ---- partition
+            const int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
+            const int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
             const int nk = __builtin_popcount(kinds);
             mark(1);
-            launch_kind_plan(p, st);
-            launch_hist(p, src_f64, kinds, max_rmi_b, grid_h, st);
-            launch_scan_children(p, st);
+            if (np) {
+                launch_kind_plan(p, st);
+                launch_hist(p, src_f64, kinds, max_rmi_b, grid_h, st);
+                launch_scan_children(p, st);
+            }
             mark(2);
-            launch_scatter(p, src_f64, max_nb, grid_s, st);
+            if (np) {
+                launch_scatter(p, src_f64, max_nb, grid_s, st);
+                launched(3 + nk);
+            }
             mark(3);
+            if (ncl) {
+                launch_cluster_sort(C->clus.as<BaseItem>(), ncl, (const uint64_t*)src, dst, keys, f64, p, level + 1,
+                                    st);
+                launched();
+            }
             launch_base_cases(p, dst, keys, f64, st);
             mark(4);
             launch_fill(p, keys, f64, nsm * 4, st);
             mark(5);
-            launched(2 + 2 * nk + 3 + 1);
+            launched(3 + 1);
             CU(cudaMemcpyAsync(hc, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
             CU(cudaStreamSynchronize(st));
             CU(cudaGetLastError());
@@ -512,9 +543,9 @@ struct Engine {
                     uint64_t keys = 0, mx = 0;
                     for (auto& q : segs) { keys += q.n; mx = std::max(mx, q.n); }
                     fprintf(stderr,
-                            "[lsort d%d L%u] segs=%u big=%zu keys=%llu max=%llu tiles=%llu | models %.3f "
+                            "[lsort d%d L%u] segs=%u clus=%u big=%zu keys=%llu max=%llu tiles=%llu | models %.3f "
                             "classify %.3f scatter %.3f base %.3f fill %.3f ms | rec=%u base=%u/%u/%u fill=%u\n",
-                            C->depth, level, ns, bigs.size(), (unsigned long long)keys, (unsigned long long)mx,
+                            C->depth, level, ns, ncl, bigs.size(), (unsigned long long)keys, (unsigned long long)mx,
                             (unsigned long long)ntiles, t[0], t[1], t[2], t[3], t[4], hc->n_rec, hc->n_base[0],
                             hc->n_base[1], hc->n_base[2], hc->n_fill);
                 }
@@ -526,8 +557,8 @@ struct Engine {
                         fprintf(stderr,
                                 "    big seg begin=%llu n=%llu depth=%u: kind=%u nb=%u B=%u dup=%.4f s1=%llu s2=%llu "
                                 "root=(%.6g, %.6g) base=%.6g scale=%.6g cdf_lo=%.6g inv_span=%.6g\n",
-                                (unsigned long long)segs[bigs[bi]].begin, (unsigned long long)segs[bigs[bi]].n,
-                                segs[bigs[bi]].depth, mh.kind, mh.nbuckets, mh.B, mh.dup, (unsigned long long)mh.s1,
+                                (unsigned long long)psegs[bigs[bi]].begin, (unsigned long long)psegs[bigs[bi]].n,
+                                psegs[bigs[bi]].depth, mh.kind, mh.nbuckets, mh.B, mh.dup, (unsigned long long)mh.s1,
                                 (unsigned long long)mh.s2, mh.root_slope, mh.root_icpt, mh.key_base, mh.key_scale,
                                 mh.cdf_lo, mh.inv_span);
                     }

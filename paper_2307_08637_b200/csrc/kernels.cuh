@@ -95,6 +95,14 @@ constexpr int kPartNT = 512;        // threads per classify/scatter CTA
 constexpr int kPartPerSM = 2;       // resident classify/scatter CTAs per SM
 constexpr int kRadixBits = 10;      // fallback radix model: 1024 buckets
 constexpr uint32_t kSmallSampleCap = 8192;   // samples sortable in one model CTA
+// cluster.cu: last level fused with the base case in distributed shared memory
+constexpr int kClNT = 512;          // threads per CTA
+constexpr int kClSize = 8;          // CTAs per cluster (portable maximum)
+constexpr int kClRecv = 20480;      // keys an owner CTA can receive (160 KB)
+constexpr int kClSub = 128;         // max sub-buckets per segment (kClCap / kClTarget <= 128)
+constexpr int kClSortCap = 4096;    // max keys of a sub-bucket sorted in shared memory
+constexpr uint32_t kClTarget = 1536;               // sub-bucket size target (upper bound of the mean)
+constexpr uint32_t kClCap = kClSize * (kClRecv - kClSortCap);  // max keys per cluster segment
 constexpr uint32_t kModelSmallCap = 2048;    // samples of the small model CTA
 
 // Host-visible launchers.
@@ -130,6 +138,10 @@ void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
 void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st);
 void launch_small_sort(void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st);
+// cluster.cu
+bool cluster_available();
+void launch_cluster_sort(const BaseItem* segs, uint32_t nsegs, const uint64_t* src, uint64_t* dst, void* out,
+                         int out_f64, const LevelParams& p, uint32_t depth, cudaStream_t st);
 // util.cu
 void launch_classify_ids(const uint8_t* model, const void* keys, uint64_t n, int in_f64,
                          uint32_t* ids, uint16_t* ids16, unsigned long long* hist, int payload, cudaStream_t st);

@@ -259,14 +259,29 @@ struct SmemSort {
         const uint32_t nb = 1u << lgnb;
         const uint32_t bits = bitlen64(mx - mn);
         const uint32_t shift = bits > lgnb ? bits - lgnb : 0;
+        uint32_t dg[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) dg[i] = (uint32_t)((k[i] - mn) >> shift);
+        sort_digits(k, dg, n, nb, S, scratch);
+    }
+
+    // Counting pass on caller-supplied digits (dg[i] < nb <= NBMAX, monotone in
+    // the key), placement into S.B, collision fix-up, drain of large digits.
+    // Result in S.B. The caller has zeroed nothing; S.n_* are reset here.
+    template <class SM>
+    __device__ static void sort_digits(uint64_t (&k)[ITEMS], const uint32_t (&dg)[ITEMS], uint32_t n, uint32_t nb,
+                                       SM& S, uint64_t* scratch) {
+        const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+        uint64_t* B = S.B;
+        nb = (nb + 3) & ~3u;  // whole 16-byte groups for the vectorised scan (extra digits stay empty)
+        if (tid == 0) { S.n_med = 0; S.n_large = 0; S.n_l4 = 0; S.n_l16 = 0; }
         for (uint32_t d = tid; d < nb; d += NT) S.hist[d] = 0;
         __syncthreads();
         uint32_t dp[ITEMS];  // digit << 16 | rank within the digit
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const uint32_t j = tid + i * NT;
-            const uint32_t d = (uint32_t)((k[i] - mn) >> shift);
-            dp[i] = j < n ? (d << 16 | atomicAdd(&S.hist[d], 1u)) : 0u;
+            dp[i] = j < n ? (dg[i] << 16 | atomicAdd(&S.hist[dg[i]], 1u)) : 0u;
         }
         __syncthreads();
         {  // exclusive scan; digits with > kSmall keys are pushed

@@ -63,6 +63,7 @@ int num_sms() { return g_num_sms; }
 void partition_init(int optin);
 void models_init(int optin);
 void basecase_init(int optin);
+void cluster_init(int optin);
 
 void kernels_init() {
     static bool done = false;
@@ -76,6 +77,7 @@ void kernels_init() {
     partition_init(optin);
     models_init(optin);
     basecase_init(optin);
+    cluster_init(optin);
     allow_smem(k_classify_ids<true>, optin);
     allow_smem(k_classify_ids<false>, optin);
 }

@@ -319,6 +319,25 @@ def test_sort_quality_fallback(ctx, n):
     assert levels["gpu"] <= levels["strict"]
 
 
+@pytest.mark.parametrize("dist,seed", [("uniform", 42), ("normal", 7), ("lognormal2", 19), ("mixgauss", 11),
+                                       ("zipf", 3), ("rootdups", 3)])
+def test_sort_cluster_level(ctx, dist, seed):
+    """The fused DSMEM last level (cluster.cu, LSORT_FLAG_CLUSTER) takes
+    segments of 16K..131K keys: 3e7 keys put the level-0 buckets there. Exact
+    against np.sort with and without it."""
+    n = 30_000_000
+    a = O.generate(dist, n, seed)
+    ref = np.sort(O.encode(a)) if a.dtype != np.uint64 else np.sort(a)
+    for flags in (L._native.FLAG_CLUSTER, 0):
+        d = dev(a)
+        ctx.sort(d, L.SortConfig(flags=flags))
+        got = d.cpu().numpy()
+        if a.dtype == np.uint64:
+            assert np.array_equal(got.view(np.uint64), ref), flags
+        else:
+            assert np.array_equal(O.encode(got), ref), flags
+
+
 def test_sort_host_memory(ctx):
     x = O.generate("lognormal2", 2_000_000, 19)
     y = x.copy()
