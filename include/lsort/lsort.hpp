@@ -22,6 +22,8 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
+#include <vector>
 
 #include "../lsort_cuda.h"
 
@@ -125,6 +127,32 @@ inline void run(void* keys, std::size_t n, int kind, int mem, const SortConfig& 
     throw cuda_error(rc, "lsort::sort: " + msg);
 }
 }  // namespace detail
+
+// Several independent host arrays in one call (copies pipelined against the
+// sorts). Throws nan_error for the first array holding a NaN (that array is
+// left untouched, the others are sorted).
+template <class T>
+inline void sort_batch(std::span<std::span<T>> arrays, const SortConfig& cfg = {}) {
+    static_assert(std::is_same_v<T, Key> || std::is_same_v<T, double>, "uint64 or double keys");
+    lsort_ctx* h = detail::context().get(cfg.device);
+    lsort_cfg c = cfg.to_c();
+    std::vector<void*> ptrs;
+    std::vector<std::uint64_t> ns, nans(arrays.size());
+    for (auto& a : arrays) {
+        ptrs.push_back(a.data());
+        ns.push_back(a.size());
+    }
+    const int kind = std::is_same_v<T, double> ? LSORT_KEY_F64 : LSORT_KEY_U64;
+    int rc = lsort_cuda_sort_batch(h, ptrs.data(), ns.data(), (std::uint32_t)arrays.size(), kind, &c, nullptr,
+                                   nans.data());
+    if (rc == LSORT_OK) return;
+    if (rc == LSORT_ENAN)
+        for (auto v : nans)
+            if (v != ~0ull) throw nan_error(v);
+    std::string msg = lsort_cuda_last_error(h);
+    if (rc == LSORT_EINVAL) throw std::invalid_argument("lsort::sort_batch: " + msg);
+    throw cuda_error(rc, "lsort::sort_batch: " + msg);
+}
 
 // sort(a, cfg) -- SPEC.md:384-392. Ascending, unstable.
 inline void sort(std::span<Key> a, const SortConfig& cfg = {}) {

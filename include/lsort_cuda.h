@@ -154,6 +154,18 @@ int lsort_cuda_set_stream(lsort_ctx* ctx, void* cuda_stream);
 int lsort_cuda_sort(lsort_ctx* ctx, void* keys, uint64_t n, int key_kind, int mem_kind,
                     const lsort_cfg* cfg, lsort_stats* stats, uint64_t* nan_index_out);
 
+/* sort(a, cfg) over `count` independent HOST arrays in one call -- the
+ * reference sorts each array with its own sort() (the
+ * C2/C4 configs are three arrays). The copies are pipelined on two copy
+ * streams against the sorts: array i+1 is copied in and array i-1 out while
+ * array i sorts (three device buffers in flight; pinned host memory makes the
+ * copies asynchronous). Arrays holding a NaN are left untouched and reported
+ * in nan_index_out[i] (~0 otherwise); the call then returns LSORT_ENAN after
+ * sorting all other arrays. stats (nullable) sums over the batch; ms_total is
+ * the device time from the first copy-in to the last copy-out. */
+int lsort_cuda_sort_batch(lsort_ctx* ctx, void* const* keys, const uint64_t* n, uint32_t count, int key_kind,
+                          const lsort_cfg* cfg, lsort_stats* stats, uint64_t* nan_index_out);
+
 /* ---- unit entry points (parity tests; device pointers) ---- */
 int lsort_cuda_rmi_train(lsort_ctx* ctx, const uint64_t* d_sorted_sample, uint64_t s,
                          uint32_t submodels, lsort_rmi_header* h_out,

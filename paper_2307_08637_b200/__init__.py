@@ -154,6 +154,35 @@ class Context:
         _check(self, rc)
         return stats.as_dict()
 
+    def sort_batch(self, arrays, cfg: SortConfig | None = None) -> dict:
+        """Sort several host arrays (numpy, one key kind) in one call: copies in /
+        out are pipelined against the sorts (lsort_cuda_sort_batch). Raises
+        NanError(index, array=i) for the first array holding a NaN (left
+        untouched; the others are sorted)."""
+        if not arrays:
+            return {}
+        kinds = {_key_kind_of(a) for a in arrays}
+        if len(kinds) != 1:
+            raise ValueError("sort_batch: all arrays must have the same key kind")
+        for a in arrays:
+            if not isinstance(a, np.ndarray) or not a.flags["C_CONTIGUOUS"]:
+                raise ValueError("sort_batch: host arrays must be contiguous numpy arrays")
+        m = len(arrays)
+        ptrs = (C.c_void_p * m)(*[a.ctypes.data for a in arrays])
+        ns = (C.c_uint64 * m)(*[a.size for a in arrays])
+        nans = (C.c_uint64 * m)()
+        cfg_c = (cfg or SortConfig()).to_c()
+        stats = N.lsort_stats()
+        N.lib().lsort_cuda_set_stream(self._h, None)
+        rc = N.lib().lsort_cuda_sort_batch(self._h, ptrs, ns, m, kinds.pop(), C.byref(cfg_c), C.byref(stats), nans)
+        if rc == N.LSORT_ENAN:
+            i = next(i for i in range(m) if nans[i] != (1 << 64) - 1)
+            err = NanError(int(nans[i]))
+            err.array = i
+            raise err
+        _check(self, rc)
+        return stats.as_dict()
+
     # -- unit entry points (parity tests) --------------------------------------
     def rmi_train(self, d_sorted_sample, submodels: int):
         """Rmi::train + enforce_monotonic on a sorted device sample -> packed P."""

@@ -116,12 +116,17 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws, ids, clus;
+        kseg, ktp, kplan, qws, ids, clus, bat[3];
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+    cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
     std::unique_ptr<lsort_ctx> nested;
     // lanes: workspaces + streams on which the models of the big segments of
     // one level are built concurrently (fork/join with events on `stream`)
     std::vector<std::unique_ptr<lsort_ctx>> lanes;
+    bool zero_copy = false;  // control transfers as kernels (copy engines busy with a batch)
+    PinBuf hstage;           // staging for small host->device transfers from pageable memory
+    size_t hstage_off = 0;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaEvent_t ev[6] = {};
     cudaEvent_t pev[8] = {};  // phase timing
@@ -133,6 +138,9 @@ struct lsort_ctx {
         for (auto& e : ev) if (e) cudaEventDestroy(e);
         for (auto& e : pev) if (e) cudaEventDestroy(e);
         if (fork_ev) cudaEventDestroy(fork_ev);
+        if (h2d_stream) { cudaStreamSynchronize(h2d_stream); cudaStreamDestroy(h2d_stream); }
+        if (d2h_stream) { cudaStreamSynchronize(d2h_stream); cudaStreamDestroy(d2h_stream); }
+        for (auto& e : bev) if (e) cudaEventDestroy(e);
         if (join_ev) cudaEventDestroy(join_ev);
         if (own_stream) cudaStreamDestroy(own_stream);
     }
@@ -208,6 +216,42 @@ struct Engine {
     }
 
     void launched(int k = 1) { C->launches += k; }
+
+    // host -> device of a small control block. `h` may be pageable: with zero
+    // copy it is staged in mapped pinned memory that stays untouched until
+    // the level's closing stream synchronisation (stage_reset).
+    void up(void* d, const void* h, size_t bytes, bool h_pinned = false, cudaStream_t s = nullptr) {
+        if (!bytes) return;
+        if (!s) s = st;
+        if (!C->zero_copy) {
+            CU(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+            return;
+        }
+        const void* src = h;
+        if (!h_pinned) {
+            const size_t off = (C->hstage_off + 15) & ~(size_t)15;
+            if (off + bytes > C->hstage.cap) {  // does not fit the staging area: plain DMA
+                CU(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+                return;
+            }
+            std::memcpy(C->hstage.as<uint8_t>() + off, h, bytes);
+            src = C->hstage.as<uint8_t>() + off;
+            C->hstage_off = off + bytes;
+        }
+        launch_copy_bytes(d, src, bytes, s);
+        launched();
+    }
+    // device -> pinned host
+    void down(void* hpinned, const void* d, size_t bytes) {
+        if (!bytes) return;
+        if (!C->zero_copy) {
+            CU(cudaMemcpyAsync(hpinned, d, bytes, cudaMemcpyDeviceToHost, st));
+            return;
+        }
+        launch_copy_bytes(hpinned, d, bytes, st);
+        launched();
+    }
+    void stage_reset() { C->hstage_off = 0; }
 
     // Sort the device buffer `sample` (u64) with a nested context.
     void nested_sort(uint64_t* sample, uint64_t s) {
@@ -306,8 +350,8 @@ struct Engine {
         d.nb_max = nb;
         d.tree_k = k;
         uint64_t pref[2] = {0, ntiles};
-        CU(cudaMemcpyAsync(N->segs.p, &d, sizeof(d), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(N->tile_prefix.p, pref, 16, cudaMemcpyHostToDevice, st));
+        up(N->segs.p, &d, sizeof(d), false, st);
+        up(N->tile_prefix.p, pref, 16, false, st);
         CU(cudaMemsetAsync(N->buckets.p, 0, 8 * (size_t)nb, st));
         CU(cudaMemsetAsync(nctrl, 0, sizeof(Ctrl), st));
         CU(cudaMemsetAsync(&nctrl->nan_index, 0xff, 8, st));
@@ -357,7 +401,7 @@ struct Engine {
     // Sort n keys at `keys` (device) in place. Returns LSORT_ENAN via throw.
     void sort(void* keys, uint64_t n, bool f64, lsort_stats* stats) {
         if (n < 2) return;
-        if (!C->ctrl.ensure(sizeof(Ctrl)) || !C->hctrl.ensure(sizeof(Ctrl)))
+        if (!C->ctrl.ensure(sizeof(Ctrl)) || !C->hctrl.ensure(sizeof(Ctrl)) || !C->hmodel.ensure(sizeof(ModelHdr)))
             throw LsortError{LSORT_ENOMEM, "control block"};
         Ctrl* dctrl = C->ctrl.as<Ctrl>();
         CU(cudaMemsetAsync(dctrl, 0, sizeof(Ctrl), st));
@@ -367,7 +411,7 @@ struct Engine {
         if (n <= cap) {
             launch_small_sort(keys, n, f64, dctrl, st);
             launched();
-            CU(cudaMemcpyAsync(hc, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+            down(hc, dctrl, sizeof(Ctrl));
             CU(cudaStreamSynchronize(st));
             if (hc->nan_index != ~0ull) throw LsortError{LSORT_ENAN, std::to_string(hc->nan_index)};
             if (stats) { stats->level0_kind = 2; stats->base_case_keys += n; }
@@ -456,13 +500,13 @@ struct Engine {
                 !C->kplan.ensure(3 * sizeof(KindPlan)) || !C->clus.ensure(ncl * sizeof(BaseItem) + 16))
                 throw LsortError{LSORT_ENOMEM, "level workspace"};
             if (np) {
-                CU(cudaMemcpyAsync(C->segs.p, hs, np * sizeof(SegDesc), cudaMemcpyHostToDevice, st));
-                CU(cudaMemcpyAsync(C->tile_prefix.p, hp, (np + 1) * 8, cudaMemcpyHostToDevice, st));
+                up(C->segs.p, hs, np * sizeof(SegDesc), true);
+                up(C->tile_prefix.p, hp, (np + 1) * 8, true);
             }
-            if (ncl) CU(cudaMemcpyAsync(C->clus.p, clus.data(), ncl * sizeof(BaseItem), cudaMemcpyHostToDevice, st));
+            if (ncl) up(C->clus.p, clus.data(), ncl * sizeof(BaseItem));
             for (uint32_t i = 0; i < mids.size(); ++i) hi[nsmall + i] = mids[i];
             const uint32_t nmid = (uint32_t)mids.size();
-            if (nsmall + nmid) CU(cudaMemcpyAsync(C->idx.p, hi, (nsmall + nmid) * 4, cudaMemcpyHostToDevice, st));
+            if (nsmall + nmid) up(C->idx.p, hi, (nsmall + nmid) * 4, true);
             if (nbuckets) CU(cudaMemsetAsync(C->buckets.p, 0, nbuckets * 8, st));
             CU(cudaMemsetAsync(&dctrl->n_rec, 0, offsetof(Ctrl, keys_fill) - offsetof(Ctrl, n_rec), st));
 
@@ -531,8 +575,10 @@ struct Engine {
             launch_fill(p, keys, f64, nsm * 4, st);
             mark(5);
             launched(3 + 1);
-            CU(cudaMemcpyAsync(hc, dctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+            down(hc, dctrl, sizeof(Ctrl));
+            if (level == 0 && stats) down(C->hmodel.p, C->models.p, sizeof(ModelHdr));
             CU(cudaStreamSynchronize(st));
+            stage_reset();
             CU(cudaGetLastError());
             if (hc->nan_index != ~0ull) throw LsortError{LSORT_ENAN, std::to_string(hc->nan_index)};
             if (hc->err) throw LsortError{LSORT_EINTERNAL, "work list overflow (" + std::to_string(hc->err) + ")"};
@@ -575,8 +621,7 @@ struct Engine {
                 }
             }
             if (level == 0 && stats) {
-                ModelHdr h0;
-                CU(cudaMemcpy(&h0, C->models.p, sizeof(h0), cudaMemcpyDeviceToHost));
+                const ModelHdr& h0 = *C->hmodel.as<ModelHdr>();
                 stats->level0_kind = h0.kind == kLearned ? 0 : 1;
             }
             if (stats) {
@@ -594,7 +639,7 @@ struct Engine {
             segs.clear();
             if (nrec) {
                 if (!C->hrec.ensure(nrec * sizeof(SegOut))) throw LsortError{LSORT_ENOMEM, "host rec list"};
-                CU(cudaMemcpyAsync(C->hrec.p, C->rec.p, nrec * sizeof(SegOut), cudaMemcpyDeviceToHost, st));
+                down(C->hrec.p, C->rec.p, nrec * sizeof(SegOut));
                 CU(cudaStreamSynchronize(st));
                 const SegOut* r = C->hrec.as<SegOut>();
                 segs.reserve(nrec);
@@ -746,6 +791,111 @@ int lsort_cuda_sort(lsort_ctx* C, void* keys, uint64_t n, int key_kind, int mem_
         cudaStreamSynchronize(C->stream);
         cudaGetLastError();
         return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_sort_batch(lsort_ctx* C, void* const* keys, const uint64_t* n, uint32_t count, int key_kind,
+                          const lsort_cfg* cfgp, lsort_stats* stats, uint64_t* nan_index_out) {
+    if (!C) return LSORT_EINVAL;
+    C->err.clear();
+    if (count && (!keys || !n)) return fail(C, {LSORT_EINVAL, "null batch"});
+    if (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_F64) return fail(C, {LSORT_EINVAL, "key_kind"});
+    for (uint32_t i = 0; i < count; ++i) {
+        if (nan_index_out) nan_index_out[i] = ~0ull;
+        if (n[i] > 0 && !keys[i]) return fail(C, {LSORT_EINVAL, "null keys"});
+    }
+    lsort_cfg cfg = cfg_or_default(cfgp);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    bool any_nan = false;
+    try {
+        validate_cfg(cfg);
+        CU(cudaSetDevice(C->device));
+        const bool f64 = key_kind == LSORT_KEY_F64;
+        uint64_t nmax = 1;
+        for (uint32_t i = 0; i < count; ++i) nmax = std::max(nmax, n[i]);
+        const uint32_t slots = std::min<uint32_t>(3, std::max<uint32_t>(count, 1));
+        for (uint32_t s = 0; s < slots; ++s)
+            if (!C->bat[s].ensure(nmax * 8)) throw LsortError{LSORT_ENOMEM, "batch buffers"};
+        if (!C->h2d_stream) CU(cudaStreamCreateWithFlags(&C->h2d_stream, cudaStreamNonBlocking));
+        if (!C->d2h_stream) CU(cudaStreamCreateWithFlags(&C->d2h_stream, cudaStreamNonBlocking));
+        for (auto& e : C->bev)
+            if (!e) CU(cudaEventCreate(&e));
+        cudaEvent_t* ev_h2d = C->bev;
+        cudaEvent_t* ev_sorted = C->bev + 3;
+        cudaEvent_t* ev_d2h = C->bev + 6;
+        if (!C->hstage.ensure(1u << 20)) throw LsortError{LSORT_ENOMEM, "staging"};
+        C->zero_copy = true;  // the copy engines stream the arrays: control traffic goes by kernels
+        CU(cudaEventRecord(C->bev[9], C->h2d_stream));
+        std::vector<bool> used(slots, false);
+        auto issue_h2d = [&](uint32_t i) {
+            const uint32_t s = i % slots;
+            if (used[s]) CU(cudaStreamWaitEvent(C->h2d_stream, ev_d2h[s], 0));  // slot's previous copy-out
+            CU(cudaMemcpyAsync(C->bat[s].p, keys[i], n[i] * 8, cudaMemcpyHostToDevice, C->h2d_stream));
+            CU(cudaEventRecord(ev_h2d[s], C->h2d_stream));
+            used[s] = true;
+        };
+        for (uint32_t i = 0; i < std::min(count, slots - 1); ++i) issue_h2d(i);
+        lsort_stats sti;
+        for (uint32_t i = 0; i < count; ++i) {
+            if (i + slots - 1 < count) issue_h2d(i + slots - 1);
+            const uint32_t s = i % slots;
+            CU(cudaStreamWaitEvent(C->stream, ev_h2d[s], 0));
+            bool nan = false;
+            try {
+                std::memset(&sti, 0, sizeof(sti));
+                C->launches = 0;
+                Engine E(C, cfg);
+                E.sort(C->bat[s].p, n[i], f64, stats ? &sti : nullptr);
+            } catch (const LsortError& e) {
+                if (e.code != LSORT_ENAN) throw;
+                nan = any_nan = true;
+                if (nan_index_out) nan_index_out[i] = std::stoull(e.msg);
+            }
+            CU(cudaEventRecord(ev_sorted[s], C->stream));
+            CU(cudaStreamWaitEvent(C->d2h_stream, ev_sorted[s], 0));
+            if (!nan) CU(cudaMemcpyAsync(keys[i], C->bat[s].p, n[i] * 8, cudaMemcpyDeviceToHost, C->d2h_stream));
+            CU(cudaEventRecord(ev_d2h[s], C->d2h_stream));
+            if (stats) {
+                stats->levels = std::max(stats->levels, sti.levels);
+                stats->partitioned_keys += sti.partitioned_keys;
+                stats->base_case_keys += sti.base_case_keys;
+                stats->fill_keys += sti.fill_keys;
+                stats->segments += sti.segments;
+                stats->base_segments += sti.base_segments;
+                stats->kernel_launches += C->launches;
+                stats->h2d_bytes += n[i] * 8;
+                stats->d2h_bytes += nan ? 0 : n[i] * 8;
+                stats->ms_models += sti.ms_models;
+                stats->ms_classify += sti.ms_classify;
+                stats->ms_scatter += sti.ms_scatter;
+                stats->ms_base += sti.ms_base;
+                stats->ms_fill += sti.ms_fill;
+            }
+        }
+        CU(cudaStreamWaitEvent(C->d2h_stream, C->bev[9], 0));
+        CU(cudaEventRecord(C->bev[10], C->d2h_stream));
+        CU(cudaStreamSynchronize(C->d2h_stream));
+        CU(cudaStreamSynchronize(C->h2d_stream));
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+        if (stats) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, C->bev[9], C->bev[10]);
+            stats->ms_total = ms;
+        }
+        C->zero_copy = false;
+    } catch (const LsortError& e) {
+        C->zero_copy = false;
+        if (C->h2d_stream) cudaStreamSynchronize(C->h2d_stream);
+        if (C->d2h_stream) cudaStreamSynchronize(C->d2h_stream);
+        cudaStreamSynchronize(C->stream);
+        cudaGetLastError();
+        return fail(C, e);
+    }
+    if (any_nan) {
+        C->err = "NaN in batch";
+        return LSORT_ENAN;
     }
     return LSORT_OK;
 }

@@ -57,6 +57,24 @@ __global__ void k_decode(uint64_t* keys, uint64_t n) {
         ((double*)keys)[i] = decode(keys[i]);
 }
 
+// Small host<->device transfers as kernels over mapped pinned memory (UVA):
+// used while the copy engines stream whole arrays (lsort_cuda_sort_batch), so
+// a level's control traffic does not queue behind a multi-MB copy.
+__global__ void __launch_bounds__(256) k_copy_bytes(uint8_t* dst, const uint8_t* src, size_t bytes) {
+    const size_t tid = blockIdx.x * 256ull + threadIdx.x, step = gridDim.x * 256ull;
+    if ((((uintptr_t)dst | (uintptr_t)src | bytes) & 15) == 0) {
+        for (size_t i = tid; i < bytes / 16; i += step) ((uint4*)dst)[i] = ((const uint4*)src)[i];
+    } else {
+        for (size_t i = tid; i < bytes; i += step) dst[i] = src[i];
+    }
+}
+
+void launch_copy_bytes(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (!bytes) return;
+    const int grid = (int)std::min<size_t>((bytes + 4095) / 4096, 64);
+    k_copy_bytes<<<grid, 256, 0, st>>>((uint8_t*)dst, (const uint8_t*)src, bytes);
+}
+
 static int g_num_sms = 148;
 int num_sms() { return g_num_sms; }
 

@@ -346,6 +346,30 @@ def test_sort_host_memory(ctx):
     assert st["h2d_bytes"] == x.nbytes and st["d2h_bytes"] == x.nbytes
 
 
+def test_sort_batch_host(ctx):
+    """lsort_cuda_sort_batch: pipelined host arrays, NaN array untouched."""
+    xs = [O.generate("normal", 3_000_000, 7), O.generate("lognormal05", 1_000_000, 7),
+          O.generate("exponential2", 5, 7), O.generate("uniform", 2_000_001, 42)]
+    ys = [x.copy() for x in xs]
+    st = ctx.sort_batch(ys)
+    for x, y in zip(xs, ys):
+        check_sorted_f64(x, y)
+    assert st["h2d_bytes"] == sum(x.nbytes for x in xs)
+    bad = [O.generate("uniform", 100_000, 42), O.generate("normal", 200_000, 7)]
+    bad[1][12345] = np.nan
+    keep = bad[1].copy()
+    with pytest.raises(L.NanError) as e:
+        ctx.sort_batch(bad)
+    assert e.value.index == 12345 and e.value.array == 1
+    assert np.array_equal(bits(bad[1]), bits(keep))
+    assert np.all(np.diff(bad[0]) >= 0)
+    us = [O.generate(d, 400_000, 3) for d in ("rootdups", "zipf")]
+    vs = [u.copy() for u in us]
+    ctx.sort_batch(vs)
+    for u, v in zip(us, vs):
+        assert np.array_equal(np.sort(u), v)
+
+
 def test_sort_configs(ctx):
     x = O.generate("exponential2", 1_000_000, 7)
     for cfg in [L.SortConfig(bucket_target=0), L.SortConfig(rmi_bucket_count=256, tree_bucket_count=16),
