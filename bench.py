@@ -295,7 +295,7 @@ def run_ours(args):
         "clocks": clocks,
     }
     # ---- e2e through the public API with pinned host buffers (H2D + D2H inside)
-    if not dist_mode:
+    if not dist_mode and args.e2e_steps > 0:
         hosts = [torch.empty(n, dtype=p.dtype, pin_memory=True) for p in pristine]
         src = [p.cpu() for p in pristine]
         # the public batch entry point (lsort_cuda_sort_batch): one call sorts

@@ -63,8 +63,8 @@ __global__ void __launch_bounds__(NT) k_base_smem(const BaseItem* items, const u
 // array): shared memory holds only the output array + digit histogram, so
 // three CTAs share an SM and hide each other's load latency. The segment's
 // own input range doubles as scratch for the rare large-digit passes.
-template <int NT, int CAP, int NBMAX, bool OUT_F64>
-__global__ void __launch_bounds__(NT, 3) k_base_reg(const BaseItem* items, const unsigned int* count, uint64_t* src,
+template <int NT, int CAP, int NBMAX, int MINB, bool OUT_F64>
+__global__ void __launch_bounds__(NT, MINB) k_base_reg(const BaseItem* items, const unsigned int* count, uint64_t* src,
                                                    void* out, Ctrl* ctrl, uint32_t list_cap) {
     using SS = SmemSort<NT, CAP, NBMAX>;
     extern __shared__ uint4 smem_u4[];
@@ -196,10 +196,10 @@ static_assert(1024 == kWarpBaseCap, "small base-case class");
 void basecase_init(int optin) {
     allow_smem(k_base_smem<128, 1024, 1024, true>, optin);
     allow_smem(k_base_smem<128, 1024, 1024, false>, optin);
-    allow_smem(k_base_reg<256, 4096, 4096, true>, optin);
-    allow_smem(k_base_reg<256, 4096, 4096, false>, optin);
-    allow_smem(k_base<1024, 16, 8192, true>, optin);
-    allow_smem(k_base<1024, 16, 8192, false>, optin);
+    allow_smem(k_base_reg<256, 4096, 4096, 3, true>, optin);
+    allow_smem(k_base_reg<256, 4096, 4096, 3, false>, optin);
+    allow_smem(k_base_reg<1024, 16384, 8192, 1, true>, optin);
+    allow_smem(k_base_reg<1024, 16384, 8192, 1, false>, optin);
     allow_smem(k_small_sort<true>, optin);
     allow_smem(k_small_sort<false>, optin);
 }
@@ -207,16 +207,16 @@ void basecase_init(int optin) {
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st) {
     const int nsm = num_sms();
     const int g0 = nsm * 8, g1 = nsm * 3, gl = nsm;
-    const size_t s0 = sizeof(SmallSS::Smem), s1 = sizeof(MidSS::SmemR);
+    const size_t s0 = sizeof(SmallSS::Smem), s1 = sizeof(MidSS::SmemR), s2 = sizeof(SmemSort<1024, 16384, 8192>::SmemR);
     unsigned int* cnt = &p.ctrl->n_base[0];
     if (out_f64) {
         k_base_smem<128, 1024, 1024, true><<<g0, 128, s0, st>>>(p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
-        k_base_reg<256, 4096, 4096, true><<<g1, 256, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
-        k_base<1024, 16, 8192, true><<<gl, 1024, BaseL::smem, st>>>(p.base[2], cnt + 2, src, out, p.ctrl, p.list_cap);
+        k_base_reg<256, 4096, 4096, 3, true><<<g1, 256, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        k_base_reg<1024, 16384, 8192, 1, true><<<gl, 1024, s2, st>>>(p.base[2], cnt + 2, (uint64_t*)src, out, p.ctrl, p.list_cap);
     } else {
         k_base_smem<128, 1024, 1024, false><<<g0, 128, s0, st>>>(p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
-        k_base_reg<256, 4096, 4096, false><<<g1, 256, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
-        k_base<1024, 16, 8192, false><<<gl, 1024, BaseL::smem, st>>>(p.base[2], cnt + 2, src, out, p.ctrl, p.list_cap);
+        k_base_reg<256, 4096, 4096, 3, false><<<g1, 256, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        k_base_reg<1024, 16384, 8192, 1, false><<<gl, 1024, s2, st>>>(p.base[2], cnt + 2, (uint64_t*)src, out, p.ctrl, p.list_cap);
     }
 }
 
