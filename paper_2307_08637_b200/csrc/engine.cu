@@ -284,7 +284,12 @@ struct Engine {
             std::unique_ptr<lsort_ctx> L(new lsort_ctx());
             L->device = C->device;
             L->depth = C->depth + 1;
-            CU(cudaStreamCreateWithFlags(&L->own_stream, cudaStreamNonBlocking));
+            // lanes carry the dependent chains (big-segment pipelines, mid
+            // models): highest priority so their CTAs are scheduled ahead of
+            // the wide small-model grid on the context stream
+            int lo = 0, hi = 0;
+            CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CU(cudaStreamCreateWithPriority(&L->own_stream, cudaStreamNonBlocking, hi));
             L->stream = L->own_stream;
             CU(cudaEventCreateWithFlags(&L->join_ev, cudaEventDisableTiming));
             C->lanes.push_back(std::move(L));
@@ -293,22 +298,35 @@ struct Engine {
     }
     static constexpr uint32_t kLanes = 8;
 
-    // Models of the big segments `bigs` (indices into segs/hs, device
-    // descriptors at dsegs), spread over up to kLanes concurrent streams that
-    // fork from and join back into the context stream.
-    void big_models(const std::vector<uint32_t>& bigs, const SegDesc* dsegs, const std::vector<SegPlan>& segs,
-                    const SegDesc* hs, const void* src, bool f64) {
-        if (bigs.empty()) return;
+    // All models of a level: the big segments' pipelines on up to kLanes
+    // lane streams, the mid-size CTAs (8192-sample, the long pole among the
+    // one-CTA models) on one more lane, the small models on the context
+    // stream -- forked from and joined back into the context stream.
+    void level_models(const std::vector<uint32_t>& bigs, const SegDesc* dsegs, const std::vector<SegPlan>& segs,
+                      const SegDesc* hs, const void* src, bool f64, const uint32_t* didx, uint32_t nsmall,
+                      uint32_t nmid, const DevCfg& dc) {
         const uint32_t nl = (uint32_t)std::min<size_t>(bigs.size(), kLanes);
-        if (!C->fork_ev) CU(cudaEventCreateWithFlags(&C->fork_ev, cudaEventDisableTiming));
-        CU(cudaEventRecord(C->fork_ev, st));
-        for (uint32_t l = 0; l < nl; ++l) CU(cudaStreamWaitEvent(lane(l)->stream, C->fork_ev, 0));
+        const bool mid_lane = nmid && (nsmall || !bigs.empty());
+        const uint32_t used = nl + (mid_lane ? 1 : 0);
+        if (used) {
+            if (!C->fork_ev) CU(cudaEventCreateWithFlags(&C->fork_ev, cudaEventDisableTiming));
+            CU(cudaEventRecord(C->fork_ev, st));
+            for (uint32_t l = 0; l < used; ++l) CU(cudaStreamWaitEvent(lane(l)->stream, C->fork_ev, 0));
+        }
         for (uint32_t bi = 0; bi < bigs.size(); ++bi)
             big_model(dsegs + bigs[bi], segs[bigs[bi]], hs[bigs[bi]], src, f64, lane(bi % nl));
-        for (uint32_t l = 0; l < nl; ++l) {
+        launch_build_models(dsegs, didx + nsmall, nmid, src, f64, C->models.as<uint8_t>(), dc, 1,
+                            mid_lane ? lane(nl)->stream : st);
+        launch_build_models(dsegs, didx, nsmall, src, f64, C->models.as<uint8_t>(), dc, 0, st);
+        launched((nsmall ? 1 : 0) + (nmid ? 1 : 0));
+        for (uint32_t l = 0; l < used; ++l) {
             CU(cudaEventRecord(lane(l)->join_ev, lane(l)->stream));
             CU(cudaStreamWaitEvent(st, lane(l)->join_ev, 0));
         }
+    }
+    void big_models(const std::vector<uint32_t>& bigs, const SegDesc* dsegs, const std::vector<SegPlan>& segs,
+                    const SegDesc* hs, const void* src, bool f64) {
+        level_models(bigs, dsegs, segs, hs, src, f64, nullptr, 0, 0, dev_cfg(cfg));
     }
 
     // Model for one big segment (RMI sample > one CTA), with no host round
@@ -542,12 +560,7 @@ struct Engine {
             // ---- models
             const int nsm = num_sms();
             if (np) {
-                launch_build_models(p.segs, C->idx.as<uint32_t>(), nsmall, src, src_f64, C->models.as<uint8_t>(), dc,
-                                    0, st);
-                launch_build_models(p.segs, C->idx.as<uint32_t>() + nsmall, nmid, src, src_f64,
-                                    C->models.as<uint8_t>(), dc, 1, st);
-                launched((nsmall ? 1 : 0) + (nmid ? 1 : 0));
-                big_models(bigs, p.segs, psegs, hs, src, src_f64);
+                level_models(bigs, p.segs, psegs, hs, src, src_f64, C->idx.as<uint32_t>(), nsmall, nmid, dc);
             }
             // ---- partition
             const int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);

@@ -137,26 +137,34 @@ struct SmemSort {
         __syncthreads();
     }
 
-    __device__ static __forceinline__ void warp_rank_sort(uint64_t* a, uint32_t len) {
+    // rank sort of a[0,len) by one warp, Q keys per lane (len <= 32 * Q)
+    template <int Q>
+    __device__ static __forceinline__ void warp_rank_sort_q(uint64_t* a, uint32_t len) {
         const int lane = threadIdx.x & 31;
-        uint64_t v[8];
-        uint32_t r[8];
+        uint64_t v[Q];
+        uint32_t r[Q];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            uint32_t idx = lane + 32 * q;
+        for (int q = 0; q < Q; ++q) {
+            const uint32_t idx = lane + 32 * q;
             v[q] = idx < len ? a[idx] : ~0ull;
             r[q] = 0;
         }
         for (uint32_t j = 0; j < len; ++j) {
-            uint64_t w = a[j];
+            const uint64_t w = a[j];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) r[q] += (w < v[q]) || (w == v[q] && j < (uint32_t)(lane + 32 * q));
+            for (int q = 0; q < Q; ++q) r[q] += (w < v[q]) || (w == v[q] && j < (uint32_t)(lane + 32 * q));
         }
         __syncwarp();
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < Q; ++q)
             if ((uint32_t)(lane + 32 * q) < len) a[r[q]] = v[q];
         __syncwarp();
+    }
+    __device__ static __forceinline__ void warp_rank_sort(uint64_t* a, uint32_t len) {
+        if (len <= 32) warp_rank_sort_q<1>(a, len);
+        else if (len <= 64) warp_rank_sort_q<2>(a, len);
+        else if (len <= 128) warp_rank_sort_q<4>(a, len);
+        else warp_rank_sort_q<8>(a, len);
     }
 
     // Sort the pushed medium / large digit ranges of arr (scratch: same size).
