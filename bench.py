@@ -270,6 +270,15 @@ def run_ours(args):
     dom = max(alg, key=lambda k: phases[k])
     achieved = alg[dom] / (phases[dom] * 1e-3) / 1e9 if phases[dom] > 0 else 0.0
     names = {"ms_scatter": "k_scatter", "ms_base": "k_base", "ms_classify": "k_classify_hist"}
+    # measured DRAM bytes of the same phase (ncu counters, profiles/r1_kernel_traffic.json),
+    # scaled to this run's keys per sort
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r1_kernel_traffic.json")))
+        ph = {"ms_scatter": "scatter", "ms_base": "base", "ms_classify": "classify"}[dom]
+        traffic = tj["phases"][ph]["dram_bytes_per_key"] * n
+    except (OSError, KeyError, ValueError):
+        traffic = None
     nper = n
     P = passes(nper)
     t_roof_ms = 16.0 * P * nper / (hbm * 1e9) * 1e3 * len(work)
@@ -284,7 +293,8 @@ def run_ours(args):
                    "l2": "inputs (>=80 MB) restored + 256 MB L2 flush before every timed sort",
                    "parallelism": f"dp{world}" if dist_mode else "single-gpu"},
         "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     "traffic_source": "profiles/r1_kernel_traffic.json (ncu DRAM counters, C2 normal 1e8)",
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg[dom]},
         "sort_roofline": {"passes": P, "bytes_per_key": 16 * P, "t_roof_ms_per_step": t_roof_ms,
