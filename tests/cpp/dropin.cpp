@@ -35,6 +35,19 @@ int main() {
     } catch (const lsort::nan_error& e) {
         if (e.index() != 123) { std::puts("wrong NaN index"); return 1; }
     }
+    // several host arrays in one call (copies pipelined against the sorts)
+    std::vector<std::vector<double>> arrs(3);
+    std::vector<std::span<double>> spans;
+    for (size_t a = 0; a < arrs.size(); ++a) {
+        arrs[a].resize(700'000 + 1000 * a);
+        for (auto& v : arrs[a]) v = nd(g) * (double)(a + 1);
+        spans.emplace_back(arrs[a]);
+    }
+    std::vector<std::vector<double>> aref = arrs;
+    for (auto& r : aref) std::sort(r.begin(), r.end());
+    lsort::sort_batch(std::span<std::span<double>>(spans));
+    if (arrs != aref) { std::puts("batch mismatch"); return 1; }
+
     lsort::SortConfig bad;
     bad.rmi_bucket_count = 1000;  // not a power of two
     try {
