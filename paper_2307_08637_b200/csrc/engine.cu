@@ -49,6 +49,10 @@ struct DevBuf {
         return true;
     }
     template <class T> T* as() const { return (T*)p; }
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(cap, o.cap);
+    }
 };
 
 struct PinBuf {
@@ -116,7 +120,7 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws, ids, clus, bat[3];
+        kseg, ktp, kplan, qws, ids, clus, bat[3], psample, slices;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
@@ -151,6 +155,7 @@ namespace {
 struct SegPlan {
     uint64_t begin, n;
     uint32_t depth, flags;
+    uint64_t pslice = 0;  // slice of the parent's sorted sample (SegDesc::pslice)
 };
 
 void validate_cfg(const lsort_cfg& c) {
@@ -188,6 +193,7 @@ DevCfg dev_cfg(const lsort_cfg& c) {
     d.rmi_sample_cap = c.rmi_sample_cap;
     d.seed = c.seed;
     d.quality = (c.flags & LSORT_FLAG_STRICT_POLICY) ? 0u : 1u;
+    d.psample = nullptr;
     return d;
 }
 
@@ -209,7 +215,7 @@ struct Engine {
     // 0 small model CTA, 1 mid model CTA, 2 big pipeline
     int model_class(const SegPlan& s) const {
         if (s.flags & kSegForceRadix) return 0;
-        uint64_t need = sample_need(s);
+        uint64_t need = s.pslice ? std::min<uint64_t>(s.pslice & 0xffffffu, kSmallSampleCap) : sample_need(s);
         if (need <= kModelSmallCap) return 0;
         if (need <= kSmallSampleCap) return 1;
         return 2;
@@ -304,7 +310,7 @@ struct Engine {
     // stream -- forked from and joined back into the context stream.
     void level_models(const std::vector<uint32_t>& bigs, const SegDesc* dsegs, const std::vector<SegPlan>& segs,
                       const SegDesc* hs, const void* src, bool f64, const uint32_t* didx, uint32_t nsmall,
-                      uint32_t nmid, const DevCfg& dc) {
+                      uint32_t nmid, const DevCfg& dc, uint32_t* root_slices = nullptr) {
         const uint32_t nl = (uint32_t)std::min<size_t>(bigs.size(), kLanes);
         const bool mid_lane = nmid && (nsmall || !bigs.empty());
         const uint32_t used = nl + (mid_lane ? 1 : 0);
@@ -314,7 +320,9 @@ struct Engine {
             for (uint32_t l = 0; l < used; ++l) CU(cudaStreamWaitEvent(lane(l)->stream, C->fork_ev, 0));
         }
         for (uint32_t bi = 0; bi < bigs.size(); ++bi)
-            big_model(dsegs + bigs[bi], segs[bigs[bi]], hs[bigs[bi]], src, f64, lane(bi % nl));
+            big_model(dsegs + bigs[bi], segs[bigs[bi]], hs[bigs[bi]], src, f64, lane(bi % nl),
+                      bi == 0 ? root_slices : nullptr);
+        if (root_slices && !bigs.empty()) C->psample.swap(lane(0)->sample);  // keep the root's sorted sample
         launch_build_models(dsegs, didx + nsmall, nmid, src, f64, C->models.as<uint8_t>(), dc, 1,
                             mid_lane ? lane(nl)->stream : st);
         launch_build_models(dsegs, didx, nsmall, src, f64, C->models.as<uint8_t>(), dc, 0, st);
@@ -336,7 +344,7 @@ struct Engine {
     // distribution level with that tree + shared-memory base cases; (4)
     // multi-CTA training. Every step after (1) is gated on the device.
     void big_model(const SegDesc* dseg, const SegPlan& sp, const SegDesc& hseg, const void* src, bool f64,
-                   lsort_ctx* N) {
+                   lsort_ctx* N, uint32_t* slices = nullptr) {
         const cudaStream_t st = N->stream;  // this lane's stream
         DevCfg dc = dev_cfg(cfg);
         const uint64_t n = sp.n;
@@ -414,6 +422,11 @@ struct Engine {
                                  N->qws.p, gate, st);
             launched(2);
         }
+        if (slices) {  // children's model samples: bucket boundaries in the sorted sample
+            launch_sample_slices(N->sample.as<uint64_t>(), s2, C->models.as<uint8_t>() + hseg.model_off, slices,
+                                 hseg.nb_max, gate, st);
+            launched();
+        }
     }
 
     // Sort n keys at `keys` (device) in place. Returns LSORT_ENAN via throw.
@@ -477,6 +490,7 @@ struct Engine {
                 d.n = s.n;
                 d.depth = s.depth;
                 d.flags = s.flags;
+                d.pslice = s.pslice;
                 d.rmi_b = rmi_b(s.n);
                 max_rmi_b = std::max(max_rmi_b, d.rmi_b);
                 d.tree_k = tree_k(s.n);
@@ -559,8 +573,18 @@ struct Engine {
             mark(0);
             // ---- models
             const int nsm = num_sms();
+            // GPU policy: the root's sorted model sample seeds its children's models
+            uint32_t* root_slices = nullptr;
+            dc.psample = (level == 1 && C->psample.p) ? C->psample.as<uint64_t>() : nullptr;
+            if (level == 0 && np == 1 && bigs.size() == 1 && !(cfg.flags & LSORT_FLAG_STRICT_POLICY)) {
+                if (!C->slices.ensure(4 * ((size_t)hs[0].nb_max + 2))) throw LsortError{LSORT_ENOMEM, "slices"};
+                CU(cudaMemsetAsync(C->slices.p, 0, 4 * ((size_t)hs[0].nb_max + 2), st));
+                root_slices = C->slices.as<uint32_t>();
+                p.slices = root_slices;
+            }
             if (np) {
-                level_models(bigs, p.segs, psegs, hs, src, src_f64, C->idx.as<uint32_t>(), nsmall, nmid, dc);
+                level_models(bigs, p.segs, psegs, hs, src, src_f64, C->idx.as<uint32_t>(), nsmall, nmid, dc,
+                             root_slices);
             }
             // ---- partition
             const int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
@@ -656,7 +680,8 @@ struct Engine {
                 CU(cudaStreamSynchronize(st));
                 const SegOut* r = C->hrec.as<SegOut>();
                 segs.reserve(nrec);
-                for (uint32_t i = 0; i < nrec; ++i) segs.push_back({r[i].begin, r[i].n, r[i].depth, r[i].flags});
+                for (uint32_t i = 0; i < nrec; ++i)
+                    segs.push_back({r[i].begin, r[i].n, r[i].depth, r[i].flags, C->psample.p ? r[i].pslice : 0});
                 std::sort(segs.begin(), segs.end(),
                           [](const SegPlan& a, const SegPlan& b) { return a.begin < b.begin; });
             }

@@ -16,6 +16,8 @@ struct SegDesc {
     uint32_t depth, flags;   // flags: kSegForceRadix
     uint32_t nb_max, rmi_b;  // bucket slots reserved, learned fan-out
     uint32_t tree_k, pad;    // tree bucket budget
+    uint64_t pslice;         // GPU policy: (offset << 24 | len) of this segment's keys in the
+                             // parent level's sorted sample (DevCfg::psample), 0 = draw a sample
 };
 constexpr uint32_t kSegForceRadix = 1u;
 
@@ -23,7 +25,7 @@ constexpr uint32_t kSegForceRadix = 1u;
 struct SegOut {
     uint64_t begin, n;
     uint32_t depth, flags;
-    uint64_t pad;
+    uint64_t pslice;  // see SegDesc::pslice
 };
 struct BaseItem {
     uint64_t begin, n;
@@ -62,6 +64,8 @@ struct LevelParams {
     const void* src;               // keys in (level 0 may be f64)
     uint64_t* dst;                 // partitioned keys out (encoded)
     uint16_t* ids;                 // per key of src: bucket id written by k_hist, read by k_scatter
+    const uint32_t* slices;        // level 0 only: [nb+1] offsets of each bucket's keys in the sorted
+                                   // model sample (children train on them), or nullptr
                                    // (kNoMove: equality / fill bucket, the key is not moved)
     Ctrl* ctrl;
     SegOut* rec;
@@ -86,7 +90,10 @@ struct DevCfg {
     uint64_t seed;
     uint32_t quality;  // 1: GPU policy -- a learned model that puts > 1/kPoorShare of its own
                        // sample into one bucket is replaced by a splitter tree over that sample
+    const uint64_t* psample;  // GPU policy: the parent level's sorted sample (children's
+                              // models train on their slice of it instead of drawing)
 };
+constexpr uint32_t kMinSlice = 64;  // shorter slices: draw a fresh sample
 constexpr uint32_t kPoorShare = 16;
 
 constexpr int kTileKeys = 4096;     // keys per classify/scatter tile
@@ -121,6 +128,9 @@ size_t train_workspace_bytes(uint64_t s, uint32_t B);
 void launch_quality_check(const uint64_t* sorted, uint64_t s, uint8_t* model, uint32_t tree_k, void* ws,
                           const uint32_t* gate, cudaStream_t st);
 size_t quality_workspace_bytes();
+// offsets[b] = first index of the sorted sample whose bucket (under `model`) is >= b, b <= nb
+void launch_sample_slices(const uint64_t* sorted, uint64_t s, const uint8_t* model, uint32_t* offsets,
+                          uint32_t nb_cap, const uint32_t* gate, cudaStream_t st);
 void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* model, uint32_t nbuckets,
                       void* ws, const uint32_t* gate, cudaStream_t st);
 void launch_tree_build(const uint64_t* sorted, uint64_t s, uint32_t budget, int eq_mode, uint8_t* model,

@@ -354,6 +354,7 @@ __device__ __noinline__ void tree_build_block(const uint64_t* s, uint32_t n, uin
 // instruction-fetch bound).
 template <int NT, int CAP>
 struct ModelCfg {
+    static constexpr int kCap = CAP;
     using SS = SmemSort<NT, CAP, CAP / 2>;
     struct Smem {
         typename SS::Smem sort;  // sort.A holds the sorted sample
@@ -437,8 +438,23 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
     }
     const uint64_t n = sd.n;
     const uint64_t seed = seg_seed(cfg.seed, sd.begin, sd.depth);
-    const uint32_t s1 = (uint32_t)first_sample_size(cfg, n);
-    sample_sorted<IN_F64, MC>(sd, src, seed, 0, s1, S);
+    // GPU policy: a child of the level-0 partition trains on its slice of the
+    // parent's sorted sample (a uniform random sample of exactly its keys, of
+    // the size the reference would draw) -- evenly thinned to the CTA's
+    // capacity, still sorted: no gather, no sort
+    const bool slice = cfg.psample != nullptr && sd.pslice != 0 && !first_only;
+    uint32_t s1;
+    if (slice) {
+        const uint64_t off = sd.pslice >> 24;
+        const uint32_t len = (uint32_t)(sd.pslice & 0xffffffu);
+        s1 = min(len, (uint32_t)MC::kCap);
+        for (uint32_t i = threadIdx.x; i < s1; i += NT)
+            S.sort.A[i] = cfg.psample[off + (uint64_t)i * len / s1];
+        __syncthreads();
+    } else {
+        s1 = (uint32_t)first_sample_size(cfg, n);
+        sample_sorted<IN_F64, MC>(sd, src, seed, 0, s1, S);
+    }
     const uint64_t* A = S.sort.A;
     uint64_t d = 0;
     for (uint32_t i = threadIdx.x + 1; i < s1; i += NT) d += A[i] != A[i - 1];
@@ -455,7 +471,7 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
         if (gate) *gate = learned ? 1u : 0u;
     }
     if (learned) {
-        const uint32_t s2 = (uint32_t)rmi_sample_size(cfg, n);
+        const uint32_t s2 = slice ? s1 : (uint32_t)rmi_sample_size(cfg, n);
         if (threadIdx.x == 0) {
             h->kind = kLearned;
             h->nbuckets = sd.rmi_b;
@@ -469,7 +485,7 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
             return;
         }
         __syncthreads();
-        sample_sorted<IN_F64, MC>(sd, src, seed, s1, s2, S);
+        if (!slice) sample_sorted<IN_F64, MC>(sd, src, seed, s1, s2, S);
         train_rmi_block<NT>(A, s2, sd.rmi_b, h, (RmiEntry*)payload, S.u.rmi.first, S.u.rmi.lo, S.u.rmi.hi,
                             S.u.rmi.big, S.u.rmi.red);
         if (cfg.quality) {
@@ -889,6 +905,32 @@ __global__ void __launch_bounds__(512) k_quality(const uint64_t* s, uint32_t n, 
 }
 
 size_t quality_workspace_bytes() { return 4 * (size_t)LSORT_MAX_RMI_DEV; }
+
+// Bucket boundaries in a sorted sample (monotone bucket function): element i
+// writes offsets[b] = i for every b in (bucket(s[i-1]), bucket(s[i])].
+__global__ void __launch_bounds__(256) k_sample_slices(const uint64_t* s, uint32_t n, const uint8_t* model,
+                                                       uint32_t* off, const uint32_t* gate) {
+    if (gated_off(gate)) return;
+    Classifier Cl;
+    Cl.init(model);
+    const uint32_t nb = Cl.nb;
+    for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const uint32_t bi = Cl.classify_any(s[i]) & 0x7fffffffu;
+        const uint32_t lo = i == 0 ? 0u : (Cl.classify_any(s[i - 1]) & 0x7fffffffu) + 1;
+        for (uint32_t b = lo; b <= bi; ++b) off[b] = i;
+        if (i == n - 1)
+            for (uint32_t b = bi + 1; b <= nb; ++b) off[b] = n;
+    }
+}
+
+void launch_sample_slices(const uint64_t* sorted, uint64_t s, const uint8_t* model, uint32_t* offsets,
+                          uint32_t nb_cap, const uint32_t* gate, cudaStream_t st) {
+    (void)nb_cap;
+    const int g = (int)std::min<uint64_t>((s + 1023) / 1024, (uint64_t)num_sms() * 4);
+    k_sample_slices<<<g, 256, 0, st>>>(sorted, (uint32_t)s, model, offsets, gate);
+}
+
+
 
 void launch_quality_check(const uint64_t* sorted, uint64_t s, uint8_t* model, uint32_t tree_k, void* ws,
                           const uint32_t* gate, cudaStream_t st) {

@@ -419,7 +419,12 @@ __global__ void __launch_bounds__(kScanNT) k_scan_children(LevelParams p) {
             unsigned e = atomicAdd(&p.ctrl->n_rec, 1u);
             uint32_t depth = sd.depth + 1;
             uint32_t flags = (len == sd.n || depth > p.depth_cap) ? kSegForceRadix : 0u;
-            if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, flags, 0};
+            uint64_t ps = 0;
+            if (p.slices) {
+                const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
+                if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
+            }
+            if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, flags, ps};
             else atomicOr(&p.ctrl->err, 4u);
             atomicAdd(&p.ctrl->keys_rec, (unsigned long long)len);
         }
