@@ -350,7 +350,9 @@ struct Engine {
         const uint64_t n = sp.n;
         const uint64_t s1 = sample_size_host(cfg.sample_fraction, cfg.first_sample_cap, n);
         const uint64_t s2 = sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
-        const uint32_t k = cfg.tree_bucket_count;         // sample-sort splitter budget
+        // sample-sort splitter budget: ~2 Ki samples per bucket (base-case class <= 4 Ki)
+        uint32_t k = cfg.tree_bucket_count;
+        while (k < LSORT_MAX_TREE_DEV && (uint64_t)k * 2048 < s2) k <<= 1;
         const uint32_t nb = 2 * k - 1;
         const size_t aux_bytes = sizeof(ModelHdr) + ((tree_payload_bytes(k, k - 1) + 15) & ~15ull);
         const uint64_t ntiles = (s2 + kTileKeys - 1) / kTileKeys;
@@ -364,9 +366,23 @@ struct Engine {
             throw LsortError{LSORT_ENOMEM, "big model workspace"};
         uint32_t* gate = N->aux.as<uint32_t>();
         Ctrl* nctrl = N->ctrl.as<Ctrl>();
-        launch_first_sample(dseg, src, f64, C->models.as<uint8_t>(), dc, N->models.as<uint8_t>(), k, gate, st);
+        // the RMI-sample gather does not depend on the first sample: it runs on
+        // the lane's helper stream while k_first_sample decides the policy
+        // (ungated: wasted work only if the policy picks the tree branch)
+        if (!N->h2d_stream) {
+            int lo = 0, hi = 0;
+            CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CU(cudaStreamCreateWithPriority(&N->h2d_stream, cudaStreamNonBlocking, hi));
+        }
+        for (int e = 0; e < 2; ++e)
+            if (!N->bev[e]) CU(cudaEventCreateWithFlags(&N->bev[e], cudaEventDisableTiming));
+        CU(cudaEventRecord(N->bev[0], st));
+        CU(cudaStreamWaitEvent(N->h2d_stream, N->bev[0], 0));
         const uint64_t seed = seg_seed_host(cfg.seed, sp.begin, sp.depth);
-        launch_gather(dseg, src, f64, seed, s1, s2, N->sample.as<uint64_t>(), gate, st);
+        launch_gather(dseg, src, f64, seed, s1, s2, N->sample.as<uint64_t>(), nullptr, N->h2d_stream);
+        CU(cudaEventRecord(N->bev[1], N->h2d_stream));
+        launch_first_sample(dseg, src, f64, C->models.as<uint8_t>(), dc, N->models.as<uint8_t>(), k, gate, st);
+        CU(cudaStreamWaitEvent(st, N->bev[1], 0));
         // one distribution level over the sample with the first-sample tree
         SegDesc d{};
         d.begin = 0;
@@ -416,13 +432,12 @@ struct Engine {
         launch_train_rmi(N->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
                          hseg.rmi_b, N->train_ws.p, gate, st);
         launched(2 + 9 + 8);
-        if (dc.quality) {
+        if (dc.quality) {  // (and the children's sample slices for the root)
             if (!N->qws.ensure(quality_workspace_bytes())) throw LsortError{LSORT_ENOMEM, "quality workspace"};
             launch_quality_check(N->sample.as<uint64_t>(), s2, C->models.as<uint8_t>() + hseg.model_off, hseg.tree_k,
-                                 N->qws.p, gate, st);
-            launched(2);
-        }
-        if (slices) {  // children's model samples: bucket boundaries in the sorted sample
+                                 N->qws.p, slices, gate, st);
+            launched(slices ? 3 : 2);
+        } else if (slices) {
             launch_sample_slices(N->sample.as<uint64_t>(), s2, C->models.as<uint8_t>() + hseg.model_off, slices,
                                  hseg.nb_max, gate, st);
             launched();

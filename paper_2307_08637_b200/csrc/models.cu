@@ -677,6 +677,7 @@ __global__ void __launch_bounds__(kTrainNT) k_train_bounds(const uint64_t* s, ui
 // targets in shared memory (parallel, coalesced), then one lane runs the
 // dependent add chains.
 constexpr int kFitWarps = 4;
+constexpr int kMedFitMax = 16384;  // slices up to this: one warp (k_train_fits); above: k_train_bigfits
 __global__ void __launch_bounds__(32 * kFitWarps) k_train_fits(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
                                                               RmiEntry* E, const uint32_t* gate) {
     __shared__ double xs[kFitWarps][kSeqFitMax];
@@ -688,8 +689,44 @@ __global__ void __launch_bounds__(32 * kFitWarps) k_train_fits(const uint64_t* s
     if (m >= B) return;
     const uint32_t f = min(w.first[m], n), l = min(max(w.first[m + 1], f), n);
     const uint32_t len = l - f;
-    if (len == 0 || len > (uint32_t)kSeqFitMax) return;
+    if (len == 0 || len > (uint32_t)kMedFitMax) return;
     const double base = w.root[2], scale = w.root[3], nd = (double)n;
+    if (len > (uint32_t)kSeqFitMax) {
+        // medium slice: shifted one-pass sums, lane-strided, fixed shuffle
+        // tree -> deterministic, within the test tolerance (as k_train_bigfits)
+        const double c = rmi_normalize(base, scale, s[f]);
+        double sd = 0.0, sdd = 0.0, sde = 0.0;
+        for (uint32_t i = f + lane; i < l; i += 32) {
+            const double dd = __dsub_rn(rmi_normalize(base, scale, s[i]), c);
+            const double e = (double)(i - f);
+            sd = __dadd_rn(sd, dd);
+            sdd = __dadd_rn(sdd, __dmul_rn(dd, dd));
+            sde = __dadd_rn(sde, __dmul_rn(dd, e));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sd = __dadd_rn(sd, __shfl_xor_sync(FULL_MASK, sd, o));
+            sdd = __dadd_rn(sdd, __shfl_xor_sync(FULL_MASK, sdd, o));
+            sde = __dadd_rn(sde, __shfl_xor_sync(FULL_MASK, sde, o));
+        }
+        if (lane == 0) {
+            const double cn = (double)len;
+            const double md = __ddiv_rn(sd, cn);
+            const double mx = __dadd_rn(c, md);
+            const double me = __dmul_rn(0.5, (double)(len - 1));
+            const double my = __ddiv_rn(__dadd_rn((double)f, me), nd);
+            const double sxx = __dsub_rn(sdd, __dmul_rn(sd, md));
+            const double sxy = __ddiv_rn(__dsub_rn(sde, __dmul_rn(sd, me)), nd);
+            double sl = 0.0, ic = my;  // models.cpp:32-34
+            if (sxx > 0.0) {
+                const double q = __ddiv_rn(sxy, sxx);
+                if (!(q < 0.0)) { sl = q; ic = __dsub_rn(my, __dmul_rn(q, mx)); }
+            }
+            E[m].slope = sl;
+            E[m].intercept = ic;
+        }
+        return;
+    }
     double* x = xs[warp];
     double* y = ys[warp];
     for (uint32_t j = lane; j < len; j += 32) {
@@ -734,14 +771,15 @@ __global__ void __launch_bounds__(kBigFitNT) k_train_bigfits(const uint64_t* s, 
     __shared__ uint32_t last;
     if (gated_off(gate)) return;
     TrainWS w = train_ws(wsp, n, B);
-    const uint32_t m = blockIdx.x;
+    for (uint32_t item = blockIdx.x; item < B * kBigSplit; item += gridDim.x) {
+    const uint32_t m = item / kBigSplit, ysp = item % kBigSplit;
     const uint32_t f = min(w.first[m], n), l = min(max(w.first[m + 1], f), n);
-    if (l - f <= (uint32_t)kSeqFitMax) return;
+    if (l - f <= (uint32_t)kMedFitMax) continue;
     const double base = w.root[2], scale = w.root[3];
     const uint32_t cnt = l - f;
     const double c = rmi_normalize(base, scale, s[f]);
     double sd = 0.0, sdd = 0.0, sde = 0.0;
-    for (uint32_t i = f + blockIdx.y * kBigFitNT + threadIdx.x; i < l; i += kBigSplit * kBigFitNT) {
+    for (uint32_t i = f + ysp * kBigFitNT + threadIdx.x; i < l; i += kBigSplit * kBigFitNT) {
         const double d = __dsub_rn(rmi_normalize(base, scale, s[i]), c);
         const double e = (double)(i - f);
         sd = __dadd_rn(sd, d);
@@ -751,7 +789,7 @@ __global__ void __launch_bounds__(kBigFitNT) k_train_bigfits(const uint64_t* s, 
     sd = block_sum_f64<kBigFitNT>(sd, red);
     sdd = block_sum_f64<kBigFitNT>(sdd, red);
     sde = block_sum_f64<kBigFitNT>(sde, red);
-    double* part = w.big + ((size_t)m * kBigSplit + blockIdx.y) * 3;
+    double* part = w.big + ((size_t)m * kBigSplit + ysp) * 3;
     if (threadIdx.x == 0) {
         part[0] = sd;
         part[1] = sdd;
@@ -760,7 +798,9 @@ __global__ void __launch_bounds__(kBigFitNT) k_train_bigfits(const uint64_t* s, 
         last = atomicInc(&w.bigcnt[m], kBigSplit - 1) == kBigSplit - 1;
     }
     __syncthreads();
-    if (!last || threadIdx.x != 0) return;
+    const bool fin = last;
+    __syncthreads();  // `last` is rewritten by the next item
+    if (!fin || threadIdx.x != 0) continue;
     __threadfence();
     const volatile double* P = w.big + (size_t)m * kBigSplit * 3;
     double Sd = 0.0, Sdd = 0.0, Sde = 0.0;
@@ -783,6 +823,7 @@ __global__ void __launch_bounds__(kBigFitNT) k_train_bigfits(const uint64_t* s, 
     }
     E[m].slope = sl;
     E[m].intercept = ic;
+    }
 }
 
 // enforce_monotonic (models.cpp:101-126) + header + compiled table, one CTA
@@ -866,45 +907,33 @@ __global__ void __launch_bounds__(512) k_block_sort(uint64_t* keys, uint32_t n) 
 }
 
 // ------------------------------------------------ model quality (GPU policy)
-// Bucket histogram of a big segment's sorted RMI sample under its freshly
-// trained learned model (global counts, zeroed by the launcher).
-constexpr int kEvalNT = 512;
-__global__ void __launch_bounds__(kEvalNT) k_eval_sample(const uint64_t* s, uint32_t n, const uint8_t* model,
-                                                         uint32_t* counts, const uint32_t* gate) {
-    __shared__ uint32_t hist[LSORT_MAX_RMI_DEV];
-    if (gated_off(gate)) return;
-    Classifier Cl;
-    Cl.init(model);
-    if (Cl.kind != kLearned) return;
-    for (uint32_t b = threadIdx.x; b < Cl.nb; b += kEvalNT) hist[b] = 0;
-    __syncthreads();
-    for (uint32_t i = blockIdx.x * kEvalNT + threadIdx.x; i < n; i += gridDim.x * kEvalNT)
-        atomicAdd(&hist[Cl.classify<kLearned>(s[i])], 1u);
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < Cl.nb; b += kEvalNT)
-        if (hist[b]) atomicAdd(&counts[b], hist[b]);
-}
-
 // One CTA: if one bucket holds more than 1/kPoorShare of the sample, replace
 // the learned model by a splitter tree over the same sorted sample.
+// (bucket sizes = differences of the sample's bucket offsets; *redo = 1 when
+// the model was replaced, so the offsets are recomputed for the tree)
 __global__ void __launch_bounds__(512) k_quality(const uint64_t* s, uint32_t n, uint8_t* model, uint32_t tree_k,
-                                                 const uint32_t* counts, const uint32_t* gate) {
+                                                 const uint32_t* offs, uint32_t* redo, const uint32_t* gate) {
     __shared__ uint32_t scratch[2 * LSORT_MAX_TREE_DEV + 2];
     __shared__ uint32_t wsum[512 / 32 + 1];
     __shared__ uint64_t spl[LSORT_MAX_TREE_DEV];
     __shared__ uint64_t red[512 / 32];
+    if (threadIdx.x == 0) *redo = 0;
     if (gated_off(gate)) return;
     ModelHdr* h = (ModelHdr*)model;
     if (h->kind != kLearned) return;
     const uint32_t nb = h->nbuckets;
     uint64_t mx = 0;
-    for (uint32_t b = threadIdx.x; b < nb; b += 512) mx = counts[b] > mx ? counts[b] : mx;
+    for (uint32_t b = threadIdx.x; b < nb; b += 512) {
+        const uint32_t c = offs[b + 1] - offs[b];
+        mx = c > mx ? c : mx;
+    }
     mx = block_reduce_max<512>(mx, red);
     if (mx * kPoorShare <= n) return;
     tree_build_block<512>(s, n, tree_k, true, h, model + sizeof(ModelHdr), scratch, wsum, spl);
+    if (threadIdx.x == 0) *redo = 1;
 }
 
-size_t quality_workspace_bytes() { return 4 * (size_t)LSORT_MAX_RMI_DEV; }
+size_t quality_workspace_bytes() { return 4 * ((size_t)LSORT_MAX_RMI_DEV + 8); }
 
 // Bucket boundaries in a sorted sample (monotone bucket function): element i
 // writes offsets[b] = i for every b in (bucket(s[i-1]), bucket(s[i])].
@@ -933,11 +962,12 @@ void launch_sample_slices(const uint64_t* sorted, uint64_t s, const uint8_t* mod
 
 
 void launch_quality_check(const uint64_t* sorted, uint64_t s, uint8_t* model, uint32_t tree_k, void* ws,
-                          const uint32_t* gate, cudaStream_t st) {
-    cudaMemsetAsync(ws, 0, quality_workspace_bytes(), st);
-    const int g = (int)std::min<uint64_t>((s + 4 * kEvalNT - 1) / (4 * kEvalNT), (uint64_t)num_sms());
-    k_eval_sample<<<g, kEvalNT, 0, st>>>(sorted, (uint32_t)s, model, (uint32_t*)ws, gate);
-    k_quality<<<1, 512, 0, st>>>(sorted, (uint32_t)s, model, tree_k, (const uint32_t*)ws, gate);
+                          uint32_t* offs, const uint32_t* gate, cudaStream_t st) {
+    uint32_t* o = offs ? offs : (uint32_t*)ws;
+    uint32_t* redo = (uint32_t*)ws + LSORT_MAX_RMI_DEV + 4;
+    launch_sample_slices(sorted, s, model, o, 0, gate, st);
+    k_quality<<<1, 512, 0, st>>>(sorted, (uint32_t)s, model, tree_k, o, redo, gate);
+    if (offs) launch_sample_slices(sorted, s, model, o, 0, redo, st);  // the tree's offsets
 }
 
 // ------------------------------------------------------------- launchers
@@ -996,7 +1026,8 @@ void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* m
     k_train_fits<<<(B + kFitWarps - 1) / kFitWarps, 32 * kFitWarps, 0, st>>>(sample, n, ws, B, E, gate);
     static_assert(kBigSplit == kBigSplitWS, "workspace layout");
     cudaMemsetAsync(train_ws(ws, s, B).bigcnt, 0, 4 * (size_t)B, st);
-    k_train_bigfits<<<dim3(B, kBigSplit), kBigFitNT, 0, st>>>(sample, n, ws, B, E, gate);
+    const int gbig = (int)std::min<uint64_t>((uint64_t)B * kBigSplit, (uint64_t)num_sms() * 4);
+    k_train_bigfits<<<gbig, kBigFitNT, 0, st>>>(sample, n, ws, B, E, gate);
     k_train_enforce<<<1, kEnforceNT, 16 * (size_t)B, st>>>(sample, n, ws, B, model, nbuckets, gate);
 }
 
