@@ -292,34 +292,55 @@ struct SmemSort {
             dp[i] = j < n ? (dg[i] << 16 | atomicAdd(&S.hist[dg[i]], 1u)) : 0u;
         }
         __syncthreads();
-        {  // exclusive scan; digits with > kSmall keys are pushed
+        // exclusive scan of the digit counts, fused with the compaction of the
+        // collision digits: one packed 64-bit scan carries (keys | digits with
+        // 2..4 keys << 16 | digits with 5..kSmall keys << 32), so every thread
+        // knows where its collision digits go in the two lists (S.R front /
+        // back) without atomics or a second pass over the digits
+        uint32_t n4, n16;
+        {
+            static_assert(CAP < 65536, "packed 16-bit scan fields");
             const uint32_t per = (nb + NT - 1) / NT;
             const uint32_t lo = min(nb, tid * per), hi = min(nb, lo + per);
-            uint32_t sum = 0;
+            auto pk = [](uint32_t h) -> uint64_t {
+                return (uint64_t)h | ((uint64_t)(h >= 2 && h <= 4) << 16) |
+                       ((uint64_t)(h > 4 && h <= (uint32_t)kSmall) << 32);
+            };
+            uint64_t sum = 0;
             if (per % 4 == 0) {  // 16-byte reads: no bank conflicts between the threads' chunks
                 for (uint32_t d = lo; d < hi; d += 4) {
                     const uint4 h4 = *(const uint4*)&S.hist[d];
-                    sum += h4.x + h4.y + h4.z + h4.w;
+                    sum += pk(h4.x) + pk(h4.y) + pk(h4.z) + pk(h4.w);
                 }
             } else {
-                for (uint32_t d = lo; d < hi; ++d) sum += S.hist[d];
+                for (uint32_t d = lo; d < hi; ++d) sum += pk(S.hist[d]);
             }
-            uint32_t incl = sum;
+            uint64_t incl = sum;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t w = __shfl_up_sync(FULL_MASK, incl, o);
+                const uint64_t w = __shfl_up_sync(FULL_MASK, incl, o);
                 if (lane >= o) incl += w;
             }
-            if (lane == 31) S.wsum[warp] = incl;
+            if (lane == 31) S.red[warp] = incl;
             __syncthreads();
             constexpr int NW = NT / 32;
-            uint32_t wv = lane < NW ? S.wsum[lane] : 0u, wincl = wv;
+            uint64_t wv = lane < NW ? S.red[lane] : 0ull, wincl = wv;
 #pragma unroll
             for (int o = 1; o < NW; o <<= 1) {
-                const uint32_t w = __shfl_up_sync(FULL_MASK, wincl, o);
+                const uint64_t w = __shfl_up_sync(FULL_MASK, wincl, o);
                 if (lane >= o) wincl += w;
             }
-            uint32_t run = incl - sum + __shfl_sync(FULL_MASK, wincl - wv, warp);
+            const uint64_t total = __shfl_sync(FULL_MASK, wincl, NW - 1);
+            n4 = (uint32_t)(total >> 16) & 0xffffu;
+            n16 = (uint32_t)(total >> 32) & 0xffffu;
+            const uint64_t ex = incl - sum + __shfl_sync(FULL_MASK, wincl - wv, warp);
+            uint32_t run = (uint32_t)ex & 0xffffu, p4 = (uint32_t)(ex >> 16) & 0xffffu,
+                     p16 = (uint32_t)(ex >> 32) & 0xffffu;
+            auto place = [&](uint32_t d, uint32_t h, uint32_t at) {
+                if (h > (uint32_t)kSmall) push(S, at, h);
+                else if (h >= 2 && h <= 4) S.R[p4++] = (uint16_t)d;  // digit index (< NBMAX <= 65536)
+                else if (h > 4) S.R[CAP - 1 - (p16++)] = (uint16_t)d;
+            };
             if (per % 4 == 0) {
                 for (uint32_t d = lo; d < hi; d += 4) {
                     const uint4 h4 = *(const uint4*)&S.hist[d];
@@ -329,16 +350,16 @@ struct SmemSort {
                     o4.z = run; run += h4.z;
                     o4.w = run; run += h4.w;
                     *(uint4*)&S.hist[d] = o4;
-                    if (h4.x > (uint32_t)kSmall) push(S, o4.x, h4.x);
-                    if (h4.y > (uint32_t)kSmall) push(S, o4.y, h4.y);
-                    if (h4.z > (uint32_t)kSmall) push(S, o4.z, h4.z);
-                    if (h4.w > (uint32_t)kSmall) push(S, o4.w, h4.w);
+                    place(d, h4.x, o4.x);
+                    place(d + 1, h4.y, o4.y);
+                    place(d + 2, h4.z, o4.z);
+                    place(d + 3, h4.w, o4.w);
                 }
             } else {
                 for (uint32_t d = lo; d < hi; ++d) {
                     const uint32_t t = S.hist[d];
                     S.hist[d] = run;
-                    if (t > (uint32_t)kSmall) push(S, run, t);
+                    place(d, t, run);
                     run += t;
                 }
             }
@@ -353,48 +374,25 @@ struct SmemSort {
             }
         }
         __syncthreads();
-        // digits with 2..kSmall keys, compacted into two lists in S.R (free
-        // until the drain): 2..4 keys (fixed 4-key network, pad ~0) from the
-        // front, 5..kSmall keys (insertion sort, rare) from the back; then all
-        // lanes work on list entries instead of idling on 0/1-key digits
-        {
-            const unsigned lt = (1u << lane) - 1u;
-            for (uint32_t r = 0; r < (nb + NT - 1) / NT; ++r) {  // CTA-uniform trip count
-                const uint32_t d = tid + r * NT;
-                uint32_t s0 = 0, c = 0;
-                if (d < nb) { s0 = S.hist[d]; c = S.hist[d + 1] - s0; }
-                const bool t4 = c >= 2 && c <= 4, t16 = c > 4 && c <= (uint32_t)kSmall;
-                const unsigned m4 = __ballot_sync(FULL_MASK, t4), m16 = __ballot_sync(FULL_MASK, t16);
-                uint32_t b4 = 0, b16 = 0;
-                if (lane == 0) {
-                    if (m4) b4 = atomicAdd(&S.n_l4, (uint32_t)__popc(m4));
-                    if (m16) b16 = atomicAdd(&S.n_l16, (uint32_t)__popc(m16));
-                }
-                b4 = __shfl_sync(FULL_MASK, b4, 0);
-                b16 = __shfl_sync(FULL_MASK, b16, 0);
-                if (t4) S.R[b4 + __popc(m4 & lt)] = (uint16_t)d;  // digit index (< NBMAX <= 65536)
-                if (t16) S.R[CAP - 1 - (b16 + __popc(m16 & lt))] = (uint16_t)d;
-            }
-            __syncthreads();
-            const uint32_t n4 = S.n_l4, n16 = S.n_l16;
-            for (uint32_t e = tid; e < n4; e += NT) {
-                const uint32_t d = S.R[e], s0 = S.hist[d], c = S.hist[d + 1] - s0;
-                uint64_t x0 = B[s0], x1 = B[s0 + 1];
-                uint64_t x2 = c >= 3 ? B[s0 + 2] : ~0ull, x3 = c == 4 ? B[s0 + 3] : ~0ull;
-                cswap(x0, x1); cswap(x2, x3); cswap(x0, x2); cswap(x1, x3); cswap(x1, x2);
-                B[s0] = x0;
-                B[s0 + 1] = x1;
-                if (c >= 3) B[s0 + 2] = x2;
-                if (c == 4) B[s0 + 3] = x3;
-            }
-            for (uint32_t e = tid; e < n16; e += NT) {
-                const uint32_t d = S.R[CAP - 1 - e], s0 = S.hist[d], c = S.hist[d + 1] - s0;
-                for (uint32_t t = s0 + 1; t < s0 + c; ++t) {
-                    const uint64_t x = B[t];
-                    uint32_t u = t;
-                    while (u > s0 && B[u - 1] > x) { B[u] = B[u - 1]; --u; }
-                    B[u] = x;
-                }
+        // collision digits: 2..4 keys by a fixed 4-key network (pad ~0),
+        // 5..kSmall keys by insertion sort (rare); all lanes on list entries
+        for (uint32_t e = tid; e < n4; e += NT) {
+            const uint32_t d = S.R[e], s0 = S.hist[d], c = S.hist[d + 1] - s0;
+            uint64_t x0 = B[s0], x1 = B[s0 + 1];
+            uint64_t x2 = c >= 3 ? B[s0 + 2] : ~0ull, x3 = c == 4 ? B[s0 + 3] : ~0ull;
+            cswap(x0, x1); cswap(x2, x3); cswap(x0, x2); cswap(x1, x3); cswap(x1, x2);
+            B[s0] = x0;
+            B[s0 + 1] = x1;
+            if (c >= 3) B[s0 + 2] = x2;
+            if (c == 4) B[s0 + 3] = x3;
+        }
+        for (uint32_t e = tid; e < n16; e += NT) {
+            const uint32_t d = S.R[CAP - 1 - e], s0 = S.hist[d], c = S.hist[d + 1] - s0;
+            for (uint32_t t = s0 + 1; t < s0 + c; ++t) {
+                const uint64_t x = B[t];
+                uint32_t u = t;
+                while (u > s0 && B[u - 1] > x) { B[u] = B[u - 1]; --u; }
+                B[u] = x;
             }
         }
         __syncthreads();
