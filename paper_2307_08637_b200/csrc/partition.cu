@@ -209,9 +209,14 @@ __device__ __forceinline__ void classify16(const KState& S, const ulonglong2 (&v
 
 // Tile t of a kind list: its segment (index into the kind list) and geometry.
 template <uint32_t KIND>
+// i: the segment of the previous tile of this CTA (tiles ascend), or ~0 for
+// a binary search -- a CTA walks its contiguous tile range, so the segment
+// index only ever advances (no dependent search chain per tile).
 __device__ __forceinline__ TileGeom tile_geom(const LevelParams& p, const KindTiles<KIND>& KT, uint64_t t,
                                               uint32_t& i) {
-    i = find_seg(KT.tp, KT.nks, t);
+    if (i == ~0u) i = find_seg(KT.tp, KT.nks, t);
+    else
+        while (i + 1 < KT.nks && KT.tp[i + 1] <= t) ++i;
     const SegDesc& sd = p.segs[KT.ks[i]];
     const uint64_t lo = sd.begin + (t - KT.tp[i]) * (uint64_t)kTileKeys;
     TileGeom g;
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_hist(LevelParams p) {
     for (uint32_t b = threadIdx.x; b < kMaxNB; b += kPNT) hist[b] = 0;
     TileStream TS;
     TS.init(tiles, bars);
-    uint32_t inext;
+    uint32_t inext = ~0u;
     TileGeom gnext = tile_geom<KIND>(p, KT, t0, inext);
     TS.issue(p.src, gnext, 0);
     int64_t cur = -1;
@@ -446,7 +451,9 @@ struct ScatterSmem {
 
 // Tile t over all segments of the level.
 __device__ __forceinline__ TileGeom tile_geom_all(const LevelParams& p, uint64_t t, uint32_t& i) {
-    i = find_seg(p.tile_prefix, p.nsegs, t);
+    if (i == ~0u) i = find_seg(p.tile_prefix, p.nsegs, t);
+    else
+        while (i + 1 < p.nsegs && p.tile_prefix[i + 1] <= t) ++i;
     const SegDesc& sd = p.segs[i];
     const uint64_t lo = sd.begin + (t - p.tile_prefix[i]) * (uint64_t)kTileKeys;
     TileGeom g;
@@ -467,7 +474,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
     for (uint32_t b = threadIdx.x; b <= NBC; b += kPNT) Q.cnt[b] = 0;
     TileStream TS;
     TS.init((uint8_t*)Q.tiles, Q.bars);
-    uint32_t inext;
+    uint32_t inext = ~0u;
     TileGeom gnext = tile_geom_all(p, t0, inext);
     TS.issue(p.src, gnext, 0);
     int64_t cur = -1;
