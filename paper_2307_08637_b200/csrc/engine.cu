@@ -629,6 +629,12 @@ struct Engine {
             launched(3 + 1);
             down(hc, dctrl, sizeof(Ctrl));
             if (level == 0 && stats) down(C->hmodel.p, C->models.p, sizeof(ModelHdr));
+            // the child list rides along speculatively (one round trip per level
+            // when it has <= kRecSpec entries)
+            constexpr uint32_t kRecSpec = 4096;
+            const uint32_t spec = (uint32_t)std::min<uint64_t>(kRecSpec, list_cap);
+            if (!C->hrec.ensure((size_t)spec * sizeof(SegOut) + 64)) throw LsortError{LSORT_ENOMEM, "host rec list"};
+            down(C->hrec.p, C->rec.p, (size_t)spec * sizeof(SegOut));
             CU(cudaStreamSynchronize(st));
             stage_reset();
             CU(cudaGetLastError());
@@ -690,9 +696,11 @@ struct Engine {
             uint32_t nrec = hc->n_rec;
             segs.clear();
             if (nrec) {
-                if (!C->hrec.ensure(nrec * sizeof(SegOut))) throw LsortError{LSORT_ENOMEM, "host rec list"};
-                down(C->hrec.p, C->rec.p, nrec * sizeof(SegOut));
-                CU(cudaStreamSynchronize(st));
+                if (nrec > spec) {
+                    if (!C->hrec.ensure(nrec * sizeof(SegOut))) throw LsortError{LSORT_ENOMEM, "host rec list"};
+                    down(C->hrec.p, C->rec.p, nrec * sizeof(SegOut));
+                    CU(cudaStreamSynchronize(st));
+                }
                 const SegOut* r = C->hrec.as<SegOut>();
                 segs.reserve(nrec);
                 for (uint32_t i = 0; i < nrec; ++i)
