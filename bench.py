@@ -192,7 +192,11 @@ def run_ours(args):
     work = [torch.empty_like(p) for p in pristine]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ctx = L.Context(local)
-    cfg = L.SortConfig(flags=L._native.FLAG_PHASE_TIMING)
+    # timed sorts run without per-phase events (those force a host sync per
+    # level); an extra untimed pass with LSORT_FLAG_PHASE_TIMING feeds the
+    # per-phase roofline. The distributed path keeps them (per-rank phases).
+    cfg_phase = L.SortConfig(flags=L._native.FLAG_PHASE_TIMING)
+    cfg = cfg_phase if dist_mode else L.SortConfig()
     if dist_mode:
         from paper_2307_08637_b200.dist import DistSorter
         sorter = DistSorter(ctx, cfg)
@@ -247,6 +251,14 @@ def run_ours(args):
                     if isinstance(v, (int, float)):
                         agg[k] = agg.get(k, 0) + v
     clocks = clk.summary()
+    if not dist_mode:  # phase breakdown (untimed)
+        for k in ("ms_models", "ms_classify", "ms_scatter", "ms_base", "ms_fill"):
+            agg[k] = 0.0
+        for i in range(len(work)):
+            work[i].copy_(pristine[i])
+            st_ph = ctx.sort(work[i], cfg_phase)
+            for k in ("ms_models", "ms_classify", "ms_scatter", "ms_base", "ms_fill"):
+                agg[k] += st_ph.get(k, 0.0) * args.steps  # scaled like the timed aggregate
     keys_per_step = len(work) * n * (world if dist_mode else 1)
     if dist_mode:
         import torch.distributed as tdist

@@ -612,6 +612,23 @@ struct Engine {
                 launch_scan_children(p, st);
             }
             mark(2);
+            // The next level is planned from the child list, which is final once
+            // k_scan_children has run: it is read back here and the host plans
+            // level L+1 while the GPU still scatters / sorts level L (unless the
+            // cluster level appends children, or per-level timing wants a sync).
+            constexpr uint32_t kRecSpec = 4096;  // children read back speculatively
+            const uint32_t spec = (uint32_t)std::min<uint64_t>(kRecSpec, list_cap);
+            if (!C->hrec.ensure((size_t)spec * sizeof(SegOut) + 64)) throw LsortError{LSORT_ENOMEM, "host rec list"};
+            const bool early = ncl == 0 && !timing;
+            auto read_back = [&]() {
+                down(hc, dctrl, sizeof(Ctrl));
+                if (level == 0 && stats) down(C->hmodel.p, C->models.p, sizeof(ModelHdr));
+                down(C->hrec.p, C->rec.p, (size_t)spec * sizeof(SegOut));
+            };
+            if (early) {
+                read_back();
+                CU(cudaEventRecord(C->ev[5], st));
+            }
             if (np) {
                 launch_scatter(p, src_f64, max_nb, grid_s, st);
                 launched(3 + nk);
@@ -627,15 +644,12 @@ struct Engine {
             launch_fill(p, keys, f64, nsm * 4, st);
             mark(5);
             launched(3 + 1);
-            down(hc, dctrl, sizeof(Ctrl));
-            if (level == 0 && stats) down(C->hmodel.p, C->models.p, sizeof(ModelHdr));
-            // the child list rides along speculatively (one round trip per level
-            // when it has <= kRecSpec entries)
-            constexpr uint32_t kRecSpec = 4096;
-            const uint32_t spec = (uint32_t)std::min<uint64_t>(kRecSpec, list_cap);
-            if (!C->hrec.ensure((size_t)spec * sizeof(SegOut) + 64)) throw LsortError{LSORT_ENOMEM, "host rec list"};
-            down(C->hrec.p, C->rec.p, (size_t)spec * sizeof(SegOut));
-            CU(cudaStreamSynchronize(st));
+            if (early) {
+                CU(cudaEventSynchronize(C->ev[5]));
+            } else {
+                read_back();
+                CU(cudaStreamSynchronize(st));
+            }
             stage_reset();
             CU(cudaGetLastError());
             if (hc->nan_index != ~0ull) throw LsortError{LSORT_ENAN, std::to_string(hc->nan_index)};
