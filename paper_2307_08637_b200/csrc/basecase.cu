@@ -165,24 +165,25 @@ __global__ void __launch_bounds__(1024) k_small_sort(void* keys, uint32_t n, Ctr
 }
 
 // --------------------------------------------------------------- fills
-constexpr uint64_t kFillChunk = 1 << 16;
+constexpr uint64_t kFillChunk = 1 << 14;
+// Equality fills: CTA (x, y) of a (G, kFillSplit) grid takes items x, x+G, ...
+// and within an item the chunks y, y+kFillSplit, ... -- no CTA walks the whole
+// item list, and large items still spread over kFillSplit CTAs.
+constexpr uint32_t kFillSplit = 8;
 template <bool OUT_F64>
 __global__ void __launch_bounds__(256) k_fill(const FillItem* items, const unsigned int* count, void* out,
                                              Ctrl* ctrl, uint32_t list_cap) {
     if (ctrl->nan_index != ~0ull) return;
     const uint32_t ni = min(*count, list_cap);
-    uint64_t chunk0 = 0;
-    for (uint32_t e = 0; e < ni; ++e) {
+    for (uint32_t e = blockIdx.x; e < ni; e += gridDim.x) {
         const FillItem it = items[e];
-        const uint64_t nch = (it.n + kFillChunk - 1) / kFillChunk;
-        const uint64_t first = (blockIdx.x + gridDim.x - (chunk0 % gridDim.x)) % gridDim.x;
         const uint64_t v = OUT_F64 ? (uint64_t)__double_as_longlong(decode(it.value)) : it.value;
-        for (uint64_t c = first; c < nch; c += gridDim.x) {
-            uint64_t lo = it.begin + c * kFillChunk;
-            uint64_t hi = min(lo + kFillChunk, it.begin + it.n);
+        const uint64_t nch = (it.n + kFillChunk - 1) / kFillChunk;
+        for (uint64_t c = blockIdx.y; c < nch; c += gridDim.y) {
+            const uint64_t lo = it.begin + c * kFillChunk;
+            const uint64_t hi = min(lo + kFillChunk, it.begin + it.n);
             for (uint64_t i = lo + threadIdx.x; i < hi; i += 256) __stcs((unsigned long long*)out + i, v);
         }
-        chunk0 += nch;
     }
 }
 
@@ -221,8 +222,9 @@ void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int
 }
 
 void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st) {
-    if (out_f64) k_fill<true><<<grid, 256, 0, st>>>(p.fill, &p.ctrl->n_fill, out, p.ctrl, p.list_cap);
-    else k_fill<false><<<grid, 256, 0, st>>>(p.fill, &p.ctrl->n_fill, out, p.ctrl, p.list_cap);
+    const dim3 g((unsigned)grid, kFillSplit);
+    if (out_f64) k_fill<true><<<g, 256, 0, st>>>(p.fill, &p.ctrl->n_fill, out, p.ctrl, p.list_cap);
+    else k_fill<false><<<g, 256, 0, st>>>(p.fill, &p.ctrl->n_fill, out, p.ctrl, p.list_cap);
 }
 
 void launch_small_sort(void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st) {

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <chrono>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -598,8 +599,12 @@ struct Engine {
                 p.slices = root_slices;
             }
             if (np) {
+                const auto th0 = std::chrono::steady_clock::now();
                 level_models(bigs, p.segs, psegs, hs, src, src_f64, C->idx.as<uint32_t>(), nsmall, nmid, dc,
                              root_slices);
+                if (trace_enabled())
+                    fprintf(stderr, "    level_models host %.3f ms\n",
+                            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
             }
             // ---- partition
             const int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);

@@ -143,12 +143,24 @@ struct SmemSort {
         const int lane = threadIdx.x & 31;
         uint64_t v[Q];
         uint32_t r[Q];
+        uint64_t mn = ~0ull, mx = 0;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const uint32_t idx = lane + 32 * q;
             v[q] = idx < len ? a[idx] : ~0ull;
             r[q] = 0;
+            if (idx < len) {
+                mn = v[q] < mn ? v[q] : mn;
+                mx = v[q] > mx ? v[q] : mx;
+            }
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t a1 = __shfl_xor_sync(FULL_MASK, mn, o), b1 = __shfl_xor_sync(FULL_MASK, mx, o);
+            mn = a1 < mn ? a1 : mn;
+            mx = b1 > mx ? b1 : mx;
+        }
+        if (mn == mx) return;  // all equal (duplicate-heavy digit): already sorted
         for (uint32_t j = 0; j < len; ++j) {
             const uint64_t w = a[j];
 #pragma unroll
