@@ -19,6 +19,7 @@ namespace lsort_dev {
 template <int NT, int CAP, int NBMAX, bool OUT_F64>
 __global__ void __launch_bounds__(NT) k_base_smem(const BaseItem* items, const unsigned int* count, const uint64_t* src,
                                                  void* out, Ctrl* ctrl, uint32_t list_cap) {
+    griddep_wait();
     using SS = SmemSort<NT, CAP, NBMAX>;
     extern __shared__ uint4 smem_u4[];
     typename SS::Smem& S = *(typename SS::Smem*)smem_u4;
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(NT) k_base_smem(const BaseItem* items, const u
 template <int NT, int CAP, int NBMAX, int MINB, bool OUT_F64>
 __global__ void __launch_bounds__(NT, MINB) k_base_reg(const BaseItem* items, const unsigned int* count, uint64_t* src,
                                                    void* out, Ctrl* ctrl, uint32_t list_cap) {
+    griddep_wait();
     using SS = SmemSort<NT, CAP, NBMAX>;
     extern __shared__ uint4 smem_u4[];
     typename SS::SmemR& S = *(typename SS::SmemR*)smem_u4;
@@ -101,6 +103,7 @@ struct BaseCfg {
 template <int NT, int ITEMS, int NBMAX, bool OUT_F64>
 __global__ void __launch_bounds__(NT) k_base(const BaseItem* items, const unsigned int* count, const uint64_t* src,
                                             void* out, Ctrl* ctrl, uint32_t list_cap) {
+    griddep_wait();
     using BS = BlockSort<NT, ITEMS, NBMAX>;
     extern __shared__ uint4 smem_u4[];
     uint64_t* a = (uint64_t*)smem_u4;
@@ -130,6 +133,7 @@ __global__ void __launch_bounds__(NT) k_base(const BaseItem* items, const unsign
 // Whole-input sort for n <= 16384 (one CTA, in place). Detects NaN first.
 template <bool F64>
 __global__ void __launch_bounds__(1024) k_small_sort(void* keys, uint32_t n, Ctrl* ctrl) {
+    griddep_wait();
     using BS = BlockSort<1024, 16, 8192>;
     extern __shared__ uint4 smem_u4[];
     uint64_t* a = (uint64_t*)smem_u4;
@@ -173,6 +177,7 @@ constexpr uint32_t kFillSplit = 8;
 template <bool OUT_F64>
 __global__ void __launch_bounds__(256) k_fill(const FillItem* items, const unsigned int* count, void* out,
                                              Ctrl* ctrl, uint32_t list_cap) {
+    griddep_wait();
     if (ctrl->nan_index != ~0ull) return;
     const uint32_t ni = min(*count, list_cap);
     for (uint32_t e = blockIdx.x; e < ni; e += gridDim.x) {
@@ -211,25 +216,25 @@ void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int
     const size_t s0 = sizeof(SmallSS::Smem), s1 = sizeof(MidSS::SmemR), s2 = sizeof(SmemSort<1024, 16384, 8192>::SmemR);
     unsigned int* cnt = &p.ctrl->n_base[0];
     if (out_f64) {
-        k_base_smem<128, 1024, 1024, true><<<g0, 128, s0, st>>>(p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
-        k_base_reg<256, 4096, 4096, 3, true><<<g1, 256, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
-        k_base_reg<1024, 16384, 8192, 1, true><<<gl, 1024, s2, st>>>(p.base[2], cnt + 2, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        pdl(k_base_smem<128, 1024, 1024, true>, g0, 128, s0, st, p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
+        pdl(k_base_reg<256, 4096, 4096, 3, true>, g1, 256, s1, st, p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        pdl(k_base_reg<1024, 16384, 8192, 1, true>, gl, 1024, s2, st, p.base[2], cnt + 2, (uint64_t*)src, out, p.ctrl, p.list_cap);
     } else {
-        k_base_smem<128, 1024, 1024, false><<<g0, 128, s0, st>>>(p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
-        k_base_reg<256, 4096, 4096, 3, false><<<g1, 256, s1, st>>>(p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
-        k_base_reg<1024, 16384, 8192, 1, false><<<gl, 1024, s2, st>>>(p.base[2], cnt + 2, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        pdl(k_base_smem<128, 1024, 1024, false>, g0, 128, s0, st, p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
+        pdl(k_base_reg<256, 4096, 4096, 3, false>, g1, 256, s1, st, p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        pdl(k_base_reg<1024, 16384, 8192, 1, false>, gl, 1024, s2, st, p.base[2], cnt + 2, (uint64_t*)src, out, p.ctrl, p.list_cap);
     }
 }
 
 void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st) {
     const dim3 g((unsigned)grid, kFillSplit);
-    if (out_f64) k_fill<true><<<g, 256, 0, st>>>(p.fill, &p.ctrl->n_fill, out, p.ctrl, p.list_cap);
-    else k_fill<false><<<g, 256, 0, st>>>(p.fill, &p.ctrl->n_fill, out, p.ctrl, p.list_cap);
+    if (out_f64) pdl(k_fill<true>, g, 256, 0, st, p.fill, &p.ctrl->n_fill, out, p.ctrl, p.list_cap);
+    else pdl(k_fill<false>, g, 256, 0, st, p.fill, &p.ctrl->n_fill, out, p.ctrl, p.list_cap);
 }
 
 void launch_small_sort(void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st) {
-    if (f64) k_small_sort<true><<<1, 1024, BaseL::smem, st>>>(keys, (uint32_t)n, ctrl);
-    else k_small_sort<false><<<1, 1024, BaseL::smem, st>>>(keys, (uint32_t)n, ctrl);
+    if (f64) pdl(k_small_sort<true>, 1, 1024, BaseL::smem, st, keys, (uint32_t)n, ctrl);
+    else pdl(k_small_sort<false>, 1, 1024, BaseL::smem, st, keys, (uint32_t)n, ctrl);
 }
 
 }  // namespace lsort_dev

@@ -166,6 +166,28 @@ struct TileGeom {
     __device__ __forceinline__ uint64_t single(uint32_t i) const { return i == 0 ? s0 : s1; }
 };
 
+// Programmatic dependent launch: every kernel is launched with programmatic
+// stream serialisation (pdl() below) and waits here for its predecessor's
+// results -- the next kernel's launch overlaps the previous kernel's tail
+// instead of a full launch gap after it (the sort is a chain of ~40 kernels).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();  // false when LSORT_NO_PDL is set (A/B measurement)
+template <typename... KArgs, typename... Args>
+inline void pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t sm, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t c = {};
+    c.gridDim = g;
+    c.blockDim = b;
+    c.dynamicSmemBytes = sm;
+    c.stream = st;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    c.attrs = a;
+    c.numAttrs = 1;
+    cudaLaunchKernelEx(&c, k, args...);
+}
+
 template <class F>
 inline void allow_smem(F* f, int optin) {
     cudaFuncAttributes a;

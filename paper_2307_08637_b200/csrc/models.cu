@@ -513,6 +513,7 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
 template <bool IN_F64, class MC, int NT>
 __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) k_build_models(const SegDesc* segs, const uint32_t* idx, const void* src,
                                                     uint8_t* models, DevCfg cfg) {
+    griddep_wait();
     extern __shared__ uint4 smem_u4[];
     typename MC::Smem& S = *(typename MC::Smem*)smem_u4;
     const SegDesc sd = segs[idx[blockIdx.x]];
@@ -522,6 +523,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) k_build_models(const Se
 template <bool IN_F64>
 __global__ void __launch_bounds__(512, 1) k_first_sample(const SegDesc* seg, const void* src, uint8_t* models,
                                                      DevCfg cfg, uint8_t* aux, uint32_t aux_budget, uint32_t* gate) {
+    griddep_wait();
     extern __shared__ uint4 smem_u4[];
     ModelMid::Smem& S = *(ModelMid::Smem*)smem_u4;
     const SegDesc sd = *seg;
@@ -531,6 +533,7 @@ __global__ void __launch_bounds__(512, 1) k_first_sample(const SegDesc* seg, con
 template <bool IN_F64>
 __global__ void k_gather(const SegDesc* seg, const void* src, uint64_t seed, uint64_t j0, uint64_t s,
                          uint64_t* out, const uint32_t* gate) {
+    griddep_wait();
     if (gate && *gate == 0) return;
     const SegDesc sd = *seg;
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < s; j += (uint64_t)gridDim.x * blockDim.x)
@@ -582,6 +585,7 @@ __device__ __forceinline__ void base_scale(const uint64_t* s, uint32_t n, double
 template <bool PASS2>
 __global__ void __launch_bounds__(kTrainNT) k_train_sums(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
                                                         const uint32_t* gate) {
+    griddep_wait();
     __shared__ double red[kTrainNT / 32];
     if (gated_off(gate)) return;
     TrainWS w = train_ws(wsp, n, B);
@@ -617,6 +621,7 @@ __global__ void __launch_bounds__(kTrainNT) k_train_sums(const uint64_t* s, uint
 template <bool PASS2>
 __global__ void __launch_bounds__(kTrainNT) k_train_reduce(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
                                                           const uint32_t* gate) {
+    griddep_wait();
     __shared__ double red[kTrainNT / 32];
     if (gated_off(gate)) return;
     TrainWS w = train_ws(wsp, n, B);
@@ -660,6 +665,7 @@ __global__ void __launch_bounds__(kTrainNT) k_train_reduce(const uint64_t* s, ui
 // the last element also closes (r_last, B]. Each first[m] is written once.
 __global__ void __launch_bounds__(kTrainNT) k_train_bounds(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
                                                           const uint32_t* gate) {
+    griddep_wait();
     if (gated_off(gate)) return;
     TrainWS w = train_ws(wsp, n, B);
     const double rs = w.root[0], ri = w.root[1], base = w.root[2], scale = w.root[3];
@@ -680,6 +686,7 @@ constexpr int kFitWarps = 4;
 constexpr int kMedFitMax = 16384;  // slices up to this: one warp (k_train_fits); above: k_train_bigfits
 __global__ void __launch_bounds__(32 * kFitWarps) k_train_fits(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
                                                               RmiEntry* E, const uint32_t* gate) {
+    griddep_wait();
     __shared__ double xs[kFitWarps][kSeqFitMax];
     __shared__ double ys[kFitWarps][kSeqFitMax];
     if (gated_off(gate)) return;
@@ -767,6 +774,7 @@ constexpr int kBigFitNT = 256;
 constexpr int kBigSplit = 16;
 __global__ void __launch_bounds__(kBigFitNT) k_train_bigfits(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
                                                             RmiEntry* E, const uint32_t* gate) {
+    griddep_wait();
     __shared__ double red[kBigFitNT / 32];
     __shared__ uint32_t last;
     if (gated_off(gate)) return;
@@ -830,6 +838,7 @@ __global__ void __launch_bounds__(kBigFitNT) k_train_bigfits(const uint64_t* s, 
 constexpr int kEnforceNT = 1024;
 __global__ void __launch_bounds__(kEnforceNT) k_train_enforce(const uint64_t* s, uint32_t n, void* wsp, uint32_t B,
                                                              uint8_t* model, uint32_t nbuckets, const uint32_t* gate) {
+    griddep_wait();
     extern __shared__ uint4 smem_u4[];
     double* lo = (double*)smem_u4;
     double* hi = lo + B;
@@ -885,6 +894,7 @@ __global__ void __launch_bounds__(kEnforceNT) k_train_enforce(const uint64_t* s,
 
 __global__ void __launch_bounds__(512) k_tree_build(const uint64_t* sorted, uint32_t s, uint32_t budget,
                                                    int eq_mode, uint8_t* model) {
+    griddep_wait();
     extern __shared__ uint4 smem_u4[];
     ModelMid::Smem& S = *(ModelMid::Smem*)smem_u4;
     for (uint32_t i = threadIdx.x; i < s; i += 512) S.sort.A[i] = sorted[i];
@@ -894,6 +904,7 @@ __global__ void __launch_bounds__(512) k_tree_build(const uint64_t* sorted, uint
 }
 
 __global__ void __launch_bounds__(512) k_block_sort(uint64_t* keys, uint32_t n) {
+    griddep_wait();
     extern __shared__ uint4 smem_u4[];
     ModelMid::Smem& S = *(ModelMid::Smem*)smem_u4;
     for (uint32_t i = threadIdx.x; i < n; i += 512) S.sort.A[i] = keys[i];
@@ -913,6 +924,7 @@ __global__ void __launch_bounds__(512) k_block_sort(uint64_t* keys, uint32_t n) 
 // the model was replaced, so the offsets are recomputed for the tree)
 __global__ void __launch_bounds__(512) k_quality(const uint64_t* s, uint32_t n, uint8_t* model, uint32_t tree_k,
                                                  const uint32_t* offs, uint32_t* redo, const uint32_t* gate) {
+    griddep_wait();
     __shared__ uint32_t scratch[2 * LSORT_MAX_TREE_DEV + 2];
     __shared__ uint32_t wsum[512 / 32 + 1];
     __shared__ uint64_t spl[LSORT_MAX_TREE_DEV];
@@ -939,6 +951,7 @@ size_t quality_workspace_bytes() { return 4 * ((size_t)LSORT_MAX_RMI_DEV + 8); }
 // writes offsets[b] = i for every b in (bucket(s[i-1]), bucket(s[i])].
 __global__ void __launch_bounds__(256) k_sample_slices(const uint64_t* s, uint32_t n, const uint8_t* model,
                                                        uint32_t* off, const uint32_t* gate) {
+    griddep_wait();
     if (gated_off(gate)) return;
     Classifier Cl;
     Cl.init(model);
@@ -956,7 +969,7 @@ void launch_sample_slices(const uint64_t* sorted, uint64_t s, const uint8_t* mod
                           uint32_t nb_cap, const uint32_t* gate, cudaStream_t st) {
     (void)nb_cap;
     const int g = (int)std::min<uint64_t>((s + 1023) / 1024, (uint64_t)num_sms() * 4);
-    k_sample_slices<<<g, 256, 0, st>>>(sorted, (uint32_t)s, model, offsets, gate);
+    pdl(k_sample_slices, g, 256, 0, st, sorted, (uint32_t)s, model, offsets, gate);
 }
 
 
@@ -966,7 +979,7 @@ void launch_quality_check(const uint64_t* sorted, uint64_t s, uint8_t* model, ui
     uint32_t* o = offs ? offs : (uint32_t*)ws;
     uint32_t* redo = (uint32_t*)ws + LSORT_MAX_RMI_DEV + 4;
     launch_sample_slices(sorted, s, model, o, 0, gate, st);
-    k_quality<<<1, 512, 0, st>>>(sorted, (uint32_t)s, model, tree_k, o, redo, gate);
+    pdl(k_quality, 1, 512, 0, st, sorted, (uint32_t)s, model, tree_k, o, redo, gate);
     if (offs) launch_sample_slices(sorted, s, model, o, 0, redo, st);  // the tree's offsets
 }
 
@@ -988,28 +1001,28 @@ void launch_build_models(const SegDesc* segs, const uint32_t* idx, uint32_t coun
     if (!count) return;
     if (mid) {
         size_t sm = sizeof(ModelMid::Smem);
-        if (in_f64) k_build_models<true, ModelMid, 512><<<count, 512, sm, st>>>(segs, idx, src, models, cfg);
-        else k_build_models<false, ModelMid, 512><<<count, 512, sm, st>>>(segs, idx, src, models, cfg);
+        if (in_f64) pdl(k_build_models<true, ModelMid, 512>, count, 512, sm, st, segs, idx, src, models, cfg);
+        else pdl(k_build_models<false, ModelMid, 512>, count, 512, sm, st, segs, idx, src, models, cfg);
     } else {
         size_t sm = sizeof(ModelSmall::Smem);
-        if (in_f64) k_build_models<true, ModelSmall, 256><<<count, 256, sm, st>>>(segs, idx, src, models, cfg);
-        else k_build_models<false, ModelSmall, 256><<<count, 256, sm, st>>>(segs, idx, src, models, cfg);
+        if (in_f64) pdl(k_build_models<true, ModelSmall, 256>, count, 256, sm, st, segs, idx, src, models, cfg);
+        else pdl(k_build_models<false, ModelSmall, 256>, count, 256, sm, st, segs, idx, src, models, cfg);
     }
 }
 
 void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_t* models, const DevCfg& cfg,
                          uint8_t* aux, uint32_t aux_budget, uint32_t* gate, cudaStream_t st) {
     size_t sm = sizeof(ModelMid::Smem);
-    if (in_f64) k_first_sample<true><<<1, 512, sm, st>>>(seg, src, models, cfg, aux, aux_budget, gate);
-    else k_first_sample<false><<<1, 512, sm, st>>>(seg, src, models, cfg, aux, aux_budget, gate);
+    if (in_f64) pdl(k_first_sample<true>, 1, 512, sm, st, seg, src, models, cfg, aux, aux_budget, gate);
+    else pdl(k_first_sample<false>, 1, 512, sm, st, seg, src, models, cfg, aux, aux_budget, gate);
 }
 
 void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0, uint64_t s,
                    uint64_t* out, const uint32_t* gate, cudaStream_t st) {
     int grid = (int)std::min<uint64_t>((s + 255) / 256, (uint64_t)num_sms() * 8);
     if (grid < 1) grid = 1;
-    if (in_f64) k_gather<true><<<grid, 256, 0, st>>>(seg, src, seed, j0, s, out, gate);
-    else k_gather<false><<<grid, 256, 0, st>>>(seg, src, seed, j0, s, out, gate);
+    if (in_f64) pdl(k_gather<true>, grid, 256, 0, st, seg, src, seed, j0, s, out, gate);
+    else pdl(k_gather<false>, grid, 256, 0, st, seg, src, seed, j0, s, out, gate);
 }
 
 void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* model, uint32_t nbuckets, void* ws,
@@ -1017,27 +1030,27 @@ void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* m
     const uint32_t n = (uint32_t)s;
     const uint32_t nch = (uint32_t)((s + kTrainChunk - 1) / kTrainChunk);
     RmiEntry* E = (RmiEntry*)(model + sizeof(ModelHdr));
-    k_train_sums<false><<<nch, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
-    k_train_reduce<false><<<1, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
-    k_train_sums<true><<<nch, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
-    k_train_reduce<true><<<1, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
+    pdl(k_train_sums<false>, nch, kTrainNT, 0, st, sample, n, ws, B, gate);
+    pdl(k_train_reduce<false>, 1, kTrainNT, 0, st, sample, n, ws, B, gate);
+    pdl(k_train_sums<true>, nch, kTrainNT, 0, st, sample, n, ws, B, gate);
+    pdl(k_train_reduce<true>, 1, kTrainNT, 0, st, sample, n, ws, B, gate);
     const int gb = (int)std::min<uint64_t>((s + kTrainNT - 1) / kTrainNT, (uint64_t)num_sms() * 8);
-    k_train_bounds<<<gb, kTrainNT, 0, st>>>(sample, n, ws, B, gate);
-    k_train_fits<<<(B + kFitWarps - 1) / kFitWarps, 32 * kFitWarps, 0, st>>>(sample, n, ws, B, E, gate);
+    pdl(k_train_bounds, gb, kTrainNT, 0, st, sample, n, ws, B, gate);
+    pdl(k_train_fits, (B + kFitWarps - 1) / kFitWarps, 32 * kFitWarps, 0, st, sample, n, ws, B, E, gate);
     static_assert(kBigSplit == kBigSplitWS, "workspace layout");
     cudaMemsetAsync(train_ws(ws, s, B).bigcnt, 0, 4 * (size_t)B, st);
     const int gbig = (int)std::min<uint64_t>((uint64_t)B * kBigSplit, (uint64_t)num_sms() * 4);
-    k_train_bigfits<<<gbig, kBigFitNT, 0, st>>>(sample, n, ws, B, E, gate);
-    k_train_enforce<<<1, kEnforceNT, 16 * (size_t)B, st>>>(sample, n, ws, B, model, nbuckets, gate);
+    pdl(k_train_bigfits, gbig, kBigFitNT, 0, st, sample, n, ws, B, E, gate);
+    pdl(k_train_enforce, 1, kEnforceNT, 16 * (size_t)B, st, sample, n, ws, B, model, nbuckets, gate);
 }
 
 void launch_tree_build(const uint64_t* sorted, uint64_t s, uint32_t budget, int eq_mode, uint8_t* model,
                        cudaStream_t st) {
-    k_tree_build<<<1, 512, sizeof(ModelMid::Smem), st>>>(sorted, (uint32_t)s, budget, eq_mode, model);
+    pdl(k_tree_build, 1, 512, sizeof(ModelMid::Smem), st, sorted, (uint32_t)s, budget, eq_mode, model);
 }
 
 void launch_block_sort(uint64_t* keys, uint64_t n, cudaStream_t st) {
-    k_block_sort<<<1, 512, sizeof(ModelMid::Smem), st>>>(keys, (uint32_t)n);
+    pdl(k_block_sort, 1, 512, sizeof(ModelMid::Smem), st, keys, (uint32_t)n);
 }
 
 }  // namespace lsort_dev

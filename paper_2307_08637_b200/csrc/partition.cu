@@ -38,6 +38,7 @@ __device__ __forceinline__ uint32_t kind_slot(uint32_t kind) {
 // ------------------------------------------------------------ kind plan
 constexpr int kPlanNT = 1024;
 __global__ void __launch_bounds__(kPlanNT) k_kind_plan(LevelParams p) {
+    griddep_wait();
     if (p.gate && *p.gate == 0) {
         if (threadIdx.x < 3) { p.kplan[threadIdx.x].nsegs = 0; p.kplan[threadIdx.x].ntiles = 0; }
         return;
@@ -264,6 +265,7 @@ constexpr size_t kTileBytes = 8 * (size_t)kTileKeys;
 // ------------------------------------------------------- classify + hist
 template <bool IN_F64, uint32_t KIND>
 __global__ void __launch_bounds__(kPNT, kPartPerSM) k_hist(LevelParams p) {
+    griddep_wait();
     extern __shared__ uint4 smem_u4[];
     uint8_t* sm = (uint8_t*)smem_u4;
     uint64_t* bars = (uint64_t*)sm;                          // 2 mbarriers (16 B)
@@ -373,6 +375,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_hist(LevelParams p) {
 // ---------------------------------------------------------- scan children
 constexpr int kScanNT = 512;
 __global__ void __launch_bounds__(kScanNT) k_scan_children(LevelParams p) {
+    griddep_wait();
     __shared__ uint64_t wsum[kScanNT / 32 + 1];
     __shared__ uint8_t iseq[kMaxNB];
     __shared__ uint64_t eqval[kMaxNB];
@@ -463,6 +466,7 @@ __device__ __forceinline__ TileGeom tile_geom_all(const LevelParams& p, uint64_t
 
 template <bool IN_F64, bool MAPPED, uint32_t NBC>
 __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, const uint32_t* map, uint32_t nmapped) {
+    griddep_wait();
     extern __shared__ uint4 smem_u4[];
     ScatterSmem<NBC>& Q = *(ScatterSmem<NBC>*)smem_u4;
     if (p.ctrl->nan_index != ~0ull) return;
@@ -610,7 +614,7 @@ void partition_init(int optin) {
 }
 
 void launch_kind_plan(const LevelParams& p, cudaStream_t st) {
-    k_kind_plan<<<1, kPlanNT, 0, st>>>(p);
+    pdl(k_kind_plan, 1, kPlanNT, 0, st, p);
 }
 
 void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_rmi_b, int grid, cudaStream_t st) {
@@ -618,42 +622,42 @@ void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_
     size_t sm_r = 16 + 4 * (size_t)kMaxNB + 2 * kTileBytes, sm_t = sm_r + kTreeCap, sm_l = sm_r + table_bytes;
     if (kinds & 1) {
         const int gl = grid;
-        if (in_f64) k_hist<true, kLearned><<<gl, kPNT, sm_l, st>>>(p);
-        else k_hist<false, kLearned><<<gl, kPNT, sm_l, st>>>(p);
+        if (in_f64) pdl(k_hist<true, kLearned>, gl, kPNT, sm_l, st, p);
+        else pdl(k_hist<false, kLearned>, gl, kPNT, sm_l, st, p);
     }
     if (kinds & 2) {  // tree payload in shared memory: two CTAs per SM
         const int gt = grid;
-        if (in_f64) k_hist<true, kTree><<<gt, kPNT, sm_t, st>>>(p);
-        else k_hist<false, kTree><<<gt, kPNT, sm_t, st>>>(p);
+        if (in_f64) pdl(k_hist<true, kTree>, gt, kPNT, sm_t, st, p);
+        else pdl(k_hist<false, kTree>, gt, kPNT, sm_t, st, p);
     }
     if (kinds & 4) {
-        if (in_f64) k_hist<true, kRadix><<<grid, kPNT, sm_r, st>>>(p);
-        else k_hist<false, kRadix><<<grid, kPNT, sm_r, st>>>(p);
+        if (in_f64) pdl(k_hist<true, kRadix>, grid, kPNT, sm_r, st, p);
+        else pdl(k_hist<false, kRadix>, grid, kPNT, sm_r, st, p);
     }
 }
 
 void launch_scan_children(const LevelParams& p, cudaStream_t st) {
     if (!p.nsegs) return;
-    k_scan_children<<<p.nsegs, kScanNT, 8 * kMaxNB, st>>>(p);
+    pdl(k_scan_children, p.nsegs, kScanNT, 8 * kMaxNB, st, p);
 }
 
 void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid, cudaStream_t st) {
     if (nb_cap <= 1024) {
         constexpr size_t sm = sizeof(ScatterSmem<1024>);
-        if (in_f64) k_scatter<true, false, 1024><<<grid, kPNT, sm, st>>>(p, nullptr, 0);
-        else k_scatter<false, false, 1024><<<grid, kPNT, sm, st>>>(p, nullptr, 0);
+        if (in_f64) pdl(k_scatter<true, false, 1024>, grid, kPNT, sm, st, p, nullptr, 0);
+        else pdl(k_scatter<false, false, 1024>, grid, kPNT, sm, st, p, nullptr, 0);
     } else {
         constexpr size_t sm = sizeof(ScatterSmem<kMaxNB>);
-        if (in_f64) k_scatter<true, false, kMaxNB><<<grid, kPNT, sm, st>>>(p, nullptr, 0);
-        else k_scatter<false, false, kMaxNB><<<grid, kPNT, sm, st>>>(p, nullptr, 0);
+        if (in_f64) pdl(k_scatter<true, false, kMaxNB>, grid, kPNT, sm, st, p, nullptr, 0);
+        else pdl(k_scatter<false, false, kMaxNB>, grid, kPNT, sm, st, p, nullptr, 0);
     }
 }
 
 void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,
                            cudaStream_t st) {
     constexpr size_t sm = sizeof(ScatterSmem<1024>);
-    if (in_f64) k_scatter<true, true, 1024><<<grid, kPNT, sm, st>>>(p, map, nmapped);
-    else k_scatter<false, true, 1024><<<grid, kPNT, sm, st>>>(p, map, nmapped);
+    if (in_f64) pdl(k_scatter<true, true, 1024>, grid, kPNT, sm, st, p, map, nmapped);
+    else pdl(k_scatter<false, true, 1024>, grid, kPNT, sm, st, p, map, nmapped);
 }
 
 }  // namespace lsort_dev

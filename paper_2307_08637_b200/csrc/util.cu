@@ -1,6 +1,7 @@
 // util.cu -- unit-test / utility kernels (model classification with ids,
 // verify_sorted + multiset_hash, decode) and one-time kernel setup.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels_common.cuh"
 
@@ -9,6 +10,7 @@ namespace lsort_dev {
 template <bool IN_F64>
 __global__ void __launch_bounds__(256) k_classify_ids(const uint8_t* model, const void* keys, uint64_t n, uint32_t* ids,
                                                      uint16_t* ids16, unsigned long long* hist) {
+    griddep_wait();
     extern __shared__ uint4 smem_u4[];
     __shared__ uint32_t sh[kMaxNB];
     uint8_t* msm = (uint8_t*)smem_u4;
@@ -37,6 +39,7 @@ __global__ void __launch_bounds__(256) k_classify_ids(const uint8_t* model, cons
 // verify_sorted + multiset_hash (verify.hpp:17-29)
 template <bool F64>
 __global__ void __launch_bounds__(256) k_verify(const void* keys, uint64_t n, Ctrl* ctrl) {
+    griddep_wait();
     __shared__ uint64_t red[8];
     uint64_t first = ~0ull, h = 0;
     for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
@@ -53,6 +56,7 @@ __global__ void __launch_bounds__(256) k_verify(const void* keys, uint64_t n, Ct
 }
 
 __global__ void k_decode(uint64_t* keys, uint64_t n) {
+    griddep_wait();
     for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256)
         ((double*)keys)[i] = decode(keys[i]);
 }
@@ -61,6 +65,7 @@ __global__ void k_decode(uint64_t* keys, uint64_t n) {
 // used while the copy engines stream whole arrays (lsort_cuda_sort_batch), so
 // a level's control traffic does not queue behind a multi-MB copy.
 __global__ void __launch_bounds__(256) k_copy_bytes(uint8_t* dst, const uint8_t* src, size_t bytes) {
+    griddep_wait();
     const size_t tid = blockIdx.x * 256ull + threadIdx.x, step = gridDim.x * 256ull;
     if ((((uintptr_t)dst | (uintptr_t)src | bytes) & 15) == 0) {
         for (size_t i = tid; i < bytes / 16; i += step) ((uint4*)dst)[i] = ((const uint4*)src)[i];
@@ -72,10 +77,14 @@ __global__ void __launch_bounds__(256) k_copy_bytes(uint8_t* dst, const uint8_t*
 void launch_copy_bytes(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (!bytes) return;
     const int grid = (int)std::min<size_t>((bytes + 4095) / 4096, 64);
-    k_copy_bytes<<<grid, 256, 0, st>>>((uint8_t*)dst, (const uint8_t*)src, bytes);
+    pdl(k_copy_bytes, grid, 256, 0, st, (uint8_t*)dst, (const uint8_t*)src, bytes);
 }
 
 static int g_num_sms = 148;
+bool pdl_enabled() {
+    static const bool on = getenv("LSORT_NO_PDL") == nullptr;
+    return on;
+}
 int num_sms() { return g_num_sms; }
 
 void partition_init(int optin);
@@ -105,21 +114,21 @@ void launch_classify_ids(const uint8_t* model, const void* keys, uint64_t n, int
     int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)g_num_sms * 8);
     if (grid < 1) grid = 1;
     size_t sm = sizeof(ModelHdr) + (size_t)payload + 16;
-    if (in_f64) k_classify_ids<true><<<grid, 256, sm, st>>>(model, keys, n, ids, ids16, hist);
-    else k_classify_ids<false><<<grid, 256, sm, st>>>(model, keys, n, ids, ids16, hist);
+    if (in_f64) pdl(k_classify_ids<true>, grid, 256, sm, st, model, keys, n, ids, ids16, hist);
+    else pdl(k_classify_ids<false>, grid, 256, sm, st, model, keys, n, ids, ids16, hist);
 }
 
 void launch_verify(const void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st) {
     int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)g_num_sms * 8);
     if (grid < 1) grid = 1;
-    if (f64) k_verify<true><<<grid, 256, 0, st>>>(keys, n, ctrl);
-    else k_verify<false><<<grid, 256, 0, st>>>(keys, n, ctrl);
+    if (f64) pdl(k_verify<true>, grid, 256, 0, st, keys, n, ctrl);
+    else pdl(k_verify<false>, grid, 256, 0, st, keys, n, ctrl);
 }
 
 void launch_decode(uint64_t* keys, uint64_t n, cudaStream_t st) {
     int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)g_num_sms * 8);
     if (grid < 1) grid = 1;
-    k_decode<<<grid, 256, 0, st>>>(keys, n);
+    pdl(k_decode, grid, 256, 0, st, keys, n);
 }
 
 }  // namespace lsort_dev
