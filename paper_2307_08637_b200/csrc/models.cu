@@ -409,8 +409,21 @@ template <bool IN_F64, class MC>
 __device__ void sample_sorted(const SegDesc& sd, const void* src, uint64_t seed, uint32_t j0, uint32_t cnt,
                               typename MC::Smem& S) {
     constexpr int NT = sizeof(S.red64) / 8 * 32;
-    for (uint32_t i = threadIdx.x; i < cnt; i += NT)
-        S.sort.A[i] = load_key(src, sd.begin + sample_index(seed, j0 + i, sd.n), IN_F64);
+    // random gather: 8 independent loads in flight per thread (a rolled loop
+    // waits one DRAM latency per key)
+    for (uint32_t i0 = threadIdx.x; i0 < cnt; i0 += 8 * NT) {
+        uint64_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = i0 + u * NT;
+            v[u] = i < cnt ? load_key(src, sd.begin + sample_index(seed, j0 + i, sd.n), IN_F64) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = i0 + u * NT;
+            if (i < cnt) S.sort.A[i] = v[u];
+        }
+    }
     __syncthreads();
     if (cnt > 1) {
         MC::SS::sort_fast(S.sort.A, cnt, S.sort);  // -> S.sort.B
