@@ -314,9 +314,9 @@ struct SmemSort {
             static_assert(CAP < 65536, "packed 16-bit scan fields");
             const uint32_t per = (nb + NT - 1) / NT;
             const uint32_t lo = min(nb, tid * per), hi = min(nb, lo + per);
-            auto pk = [](uint32_t h) -> uint64_t {
-                return (uint64_t)h | ((uint64_t)(h >= 2 && h <= 4) << 16) |
-                       ((uint64_t)(h > 4 && h <= (uint32_t)kSmall) << 32);
+            auto pk = [](uint32_t h) -> uint64_t {  // (h-2) <= 2 <=> 2..4; (h-5) <= kSmall-5 <=> 5..kSmall
+                return (uint64_t)h | ((uint64_t)(h - 2u <= 2u) << 16) |
+                       ((uint64_t)(h - 5u <= (uint32_t)kSmall - 5u) << 32);
             };
             uint64_t sum = 0;
             if (per % 4 == 0) {  // 16-byte reads: no bank conflicts between the threads' chunks
@@ -349,9 +349,10 @@ struct SmemSort {
             uint32_t run = (uint32_t)ex & 0xffffu, p4 = (uint32_t)(ex >> 16) & 0xffffu,
                      p16 = (uint32_t)(ex >> 32) & 0xffffu;
             auto place = [&](uint32_t d, uint32_t h, uint32_t at) {
-                if (h > (uint32_t)kSmall) push(S, at, h);
-                else if (h >= 2 && h <= 4) S.R[p4++] = (uint16_t)d;  // digit index (< NBMAX <= 65536)
-                else if (h > 4) S.R[CAP - 1 - (p16++)] = (uint16_t)d;
+                if (h < 2) return;  // the common case: empty / single-key digit
+                if (h <= 4) S.R[p4++] = (uint16_t)d;  // digit index (< NBMAX <= 65536)
+                else if (h <= (uint32_t)kSmall) S.R[CAP - 1 - (p16++)] = (uint16_t)d;
+                else push(S, at, h);
             };
             if (per % 4 == 0) {
                 for (uint32_t d = lo; d < hi; d += 4) {
