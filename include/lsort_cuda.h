@@ -166,6 +166,16 @@ int lsort_cuda_sort(lsort_ctx* ctx, void* keys, uint64_t n, int key_kind, int me
 int lsort_cuda_sort_batch(lsort_ctx* ctx, void* const* keys, const uint64_t* n, uint32_t count, int key_kind,
                           const lsort_cfg* cfg, lsort_stats* stats, uint64_t* nan_index_out);
 
+/* sort(a, cfg) over `count` independent DEVICE arrays in one call: up to three
+ * sorts run concurrently, each on its own internal context (stream +
+ * workspace) driven by its own host thread, so one array's latency-bound
+ * phases (model building, level hand-over) overlap another's partition and
+ * base-case kernels. Synchronous on return; the same NaN / error contract as
+ * lsort_cuda_sort_batch; stats (nullable) sums over the arrays (ms_total
+ * is not filled). */
+int lsort_cuda_sort_many(lsort_ctx* ctx, void* const* keys, const uint64_t* n, uint32_t count, int key_kind,
+                         const lsort_cfg* cfg, lsort_stats* stats, uint64_t* nan_index_out);
+
 /* ---- unit entry points (parity tests; device pointers) ---- */
 int lsort_cuda_rmi_train(lsort_ctx* ctx, const uint64_t* d_sorted_sample, uint64_t s,
                          uint32_t submodels, lsort_rmi_header* h_out,

@@ -155,8 +155,9 @@ class Context:
         return stats.as_dict()
 
     def sort_batch(self, arrays, cfg: SortConfig | None = None) -> dict:
-        """Sort several host arrays (numpy, one key kind) in one call: copies in /
-        out are pipelined against the sorts (lsort_cuda_sort_batch). Raises
+        """Sort several arrays (one key kind) in one call. Host (numpy) arrays:
+        copies in / out pipelined against the sorts (lsort_cuda_sort_batch);
+        CUDA tensors: up to three sorts run concurrently (lsort_cuda_sort_many). Raises
         NanError(index, array=i) for the first array holding a NaN (left
         untouched; the others are sorted)."""
         if not arrays:
@@ -164,10 +165,30 @@ class Context:
         kinds = {_key_kind_of(a) for a in arrays}
         if len(kinds) != 1:
             raise ValueError("sort_batch: all arrays must have the same key kind")
+        device = not isinstance(arrays[0], np.ndarray)
         for a in arrays:
-            if not isinstance(a, np.ndarray) or not a.flags["C_CONTIGUOUS"]:
+            if device:
+                if isinstance(a, np.ndarray) or not a.is_cuda or not a.is_contiguous():
+                    raise ValueError("sort_batch: device arrays must be contiguous CUDA tensors")
+            elif not isinstance(a, np.ndarray) or not a.flags["C_CONTIGUOUS"]:
                 raise ValueError("sort_batch: host arrays must be contiguous numpy arrays")
         m = len(arrays)
+        if device:
+            self._sync_stream()
+            ptrs = (C.c_void_p * m)(*[a.data_ptr() for a in arrays])
+            ns = (C.c_uint64 * m)(*[a.numel() for a in arrays])
+            nans = (C.c_uint64 * m)()
+            cfg_c = (cfg or SortConfig()).to_c()
+            stats = N.lsort_stats()
+            rc = N.lib().lsort_cuda_sort_many(self._h, ptrs, ns, m, kinds.pop(), C.byref(cfg_c), C.byref(stats),
+                                              nans)
+            if rc == N.LSORT_ENAN:
+                i = next(i for i in range(m) if nans[i] != (1 << 64) - 1)
+                err = NanError(int(nans[i]))
+                err.array = i
+                raise err
+            _check(self, rc)
+            return stats.as_dict()
         ptrs = (C.c_void_p * m)(*[a.ctypes.data for a in arrays])
         ns = (C.c_uint64 * m)(*[a.size for a in arrays])
         nans = (C.c_uint64 * m)()

@@ -70,7 +70,7 @@ class lsort_stats(C.Structure):
 
 EXPORTS = [
     "lsort_cfg_default", "lsort_cuda_ctx_create", "lsort_cuda_ctx_destroy", "lsort_cuda_last_error",
-    "lsort_cuda_set_stream", "lsort_cuda_sort", "lsort_cuda_sort_batch", "lsort_cuda_rmi_train", "lsort_cuda_classify_rmi",
+    "lsort_cuda_set_stream", "lsort_cuda_sort", "lsort_cuda_sort_batch", "lsort_cuda_sort_many", "lsort_cuda_rmi_train", "lsort_cuda_classify_rmi",
     "lsort_cuda_tree_build", "lsort_cuda_classify_tree", "lsort_cuda_build_model",
     "lsort_cuda_block_sort", "lsort_cuda_verify", "lsort_gen_keys", "lsort_cuda_dist_sample",
     "lsort_cuda_dist_train", "lsort_cuda_dist_histogram", "lsort_cuda_dist_partition",
@@ -103,6 +103,8 @@ def lib():
     L.lsort_cuda_set_stream.argtypes = [vp, vp]
     L.lsort_cuda_sort.restype = i32
     L.lsort_cuda_sort.argtypes = [vp, vp, u64, i32, i32, P(lsort_cfg), P(lsort_stats), P(u64)]
+    L.lsort_cuda_sort_many.restype = i32
+    L.lsort_cuda_sort_many.argtypes = [vp, P(vp), P(u64), C.c_uint32, i32, P(lsort_cfg), P(lsort_stats), P(u64)]
     L.lsort_cuda_sort_batch.restype = i32
     L.lsort_cuda_sort_batch.argtypes = [vp, P(vp), P(u64), C.c_uint32, i32, P(lsort_cfg), P(lsort_stats),
                                         P(u64)]

@@ -18,7 +18,10 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <atomic>
 #include <chrono>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -129,6 +132,7 @@ struct lsort_ctx {
     // lanes: workspaces + streams on which the models of the big segments of
     // one level are built concurrently (fork/join with events on `stream`)
     std::vector<std::unique_ptr<lsort_ctx>> lanes;
+    std::vector<std::unique_ptr<lsort_ctx>> subs;  // sort_many: one context per concurrent sort
     bool zero_copy = false;  // control transfers as kernels (copy engines busy with a batch)
     PinBuf hstage;           // staging for small host->device transfers from pageable memory
     size_t hstage_off = 0;
@@ -139,6 +143,7 @@ struct lsort_ctx {
     ~lsort_ctx() {
         if (stream) cudaStreamSynchronize(stream);
         lanes.clear();
+        subs.clear();
         nested.reset();
         for (auto& e : ev) if (e) cudaEventDestroy(e);
         for (auto& e : pev) if (e) cudaEventDestroy(e);
@@ -737,6 +742,8 @@ struct Engine {
     }
 };
 
+constexpr uint32_t kManyWays = 3;  // concurrent sorts in lsort_cuda_sort_many
+
 int fail(lsort_ctx* ctx, const LsortError& e) {
     if (ctx) ctx->err = e.msg;
     return e.code;
@@ -871,6 +878,95 @@ int lsort_cuda_sort(lsort_ctx* C, void* keys, uint64_t n, int key_kind, int mem_
         cudaStreamSynchronize(C->stream);
         cudaGetLastError();
         return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_sort_many(lsort_ctx* C, void* const* keys, const uint64_t* n, uint32_t count, int key_kind,
+                         const lsort_cfg* cfgp, lsort_stats* stats, uint64_t* nan_index_out) {
+    if (!C) return LSORT_EINVAL;
+    C->err.clear();
+    if (count && (!keys || !n)) return fail(C, {LSORT_EINVAL, "null batch"});
+    if (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_F64) return fail(C, {LSORT_EINVAL, "key_kind"});
+    for (uint32_t i = 0; i < count; ++i) {
+        if (nan_index_out) nan_index_out[i] = ~0ull;
+        if (n[i] > 0 && !keys[i]) return fail(C, {LSORT_EINVAL, "null keys"});
+    }
+    lsort_cfg cfg = cfg_or_default(cfgp);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    try {
+        validate_cfg(cfg);
+        CU(cudaSetDevice(C->device));
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    const bool f64 = key_kind == LSORT_KEY_F64;
+    const uint32_t nt = std::min<uint32_t>(count, kManyWays);
+    try {
+        CU(cudaStreamSynchronize(C->stream));  // work the caller queued on the context stream comes first
+        while (C->subs.size() < nt) {
+            std::unique_ptr<lsort_ctx> s(new lsort_ctx());
+            s->device = C->device;
+            CU(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking));
+            s->stream = s->own_stream;
+            for (auto& e : s->ev) CU(cudaEventCreate(&e));
+            for (auto& e : s->pev) CU(cudaEventCreate(&e));
+            C->subs.push_back(std::move(s));
+        }
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    std::atomic<uint32_t> next{0};
+    std::mutex mu;
+    LsortError first_err{LSORT_OK, ""};
+    bool any_nan = false;
+    auto worker = [&](uint32_t t) {
+        lsort_ctx* S = C->subs[t].get();
+        cudaSetDevice(S->device);
+        for (uint32_t i = next++; i < count; i = next++) {
+            lsort_stats sti;
+            std::memset(&sti, 0, sizeof(sti));
+            try {
+                S->launches = 0;
+                Engine E(S, cfg);
+                E.sort(keys[i], n[i], f64, stats ? &sti : nullptr);
+                CU(cudaStreamSynchronize(S->stream));
+            } catch (const LsortError& e) {
+                cudaStreamSynchronize(S->stream);
+                std::lock_guard<std::mutex> g(mu);
+                if (e.code == LSORT_ENAN) {
+                    any_nan = true;
+                    if (nan_index_out) nan_index_out[i] = std::stoull(e.msg);
+                } else if (first_err.code == LSORT_OK) {
+                    first_err = e;
+                }
+                continue;
+            }
+            if (stats) {
+                std::lock_guard<std::mutex> g(mu);
+                stats->levels = std::max(stats->levels, sti.levels);
+                stats->partitioned_keys += sti.partitioned_keys;
+                stats->base_case_keys += sti.base_case_keys;
+                stats->fill_keys += sti.fill_keys;
+                stats->segments += sti.segments;
+                stats->base_segments += sti.base_segments;
+                stats->kernel_launches += S->launches;
+                stats->ms_models += sti.ms_models;
+                stats->ms_classify += sti.ms_classify;
+                stats->ms_scatter += sti.ms_scatter;
+                stats->ms_base += sti.ms_base;
+                stats->ms_fill += sti.ms_fill;
+            }
+        }
+    };
+    std::vector<std::thread> th;
+    for (uint32_t t = 1; t < nt; ++t) th.emplace_back(worker, t);
+    if (nt) worker(0);
+    for (auto& x : th) x.join();
+    if (first_err.code != LSORT_OK) return fail(C, first_err);
+    if (any_nan) {
+        C->err = "NaN in batch";
+        return LSORT_ENAN;
     }
     return LSORT_OK;
 }

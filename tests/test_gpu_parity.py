@@ -370,6 +370,24 @@ def test_sort_batch_host(ctx):
         assert np.array_equal(np.sort(u), v)
 
 
+def test_sort_batch_device(ctx):
+    """lsort_cuda_sort_many: concurrent device sorts, NaN array untouched."""
+    xs = [O.generate("normal", 3_000_000, 7), O.generate("lognormal2", 2_500_000, 19),
+          O.generate("mixgauss", 7, 11), O.generate("uniform", 4_000_001, 42)]
+    ds = [dev(x) for x in xs]
+    ctx.sort_batch(ds)
+    for x, d in zip(xs, ds):
+        check_sorted_f64(x, d.cpu().numpy())
+    bad = [O.generate("uniform", 300_000, 42), O.generate("normal", 200_000, 7)]
+    bad[1][4321] = np.nan
+    db = [dev(b) for b in bad]
+    with pytest.raises(L.NanError) as e:
+        ctx.sort_batch(db)
+    assert e.value.index == 4321 and e.value.array == 1
+    assert np.array_equal(bits(db[1].cpu().numpy()), bits(bad[1]))
+    check_sorted_f64(bad[0], db[0].cpu().numpy())
+
+
 def test_sort_configs(ctx):
     x = O.generate("exponential2", 1_000_000, 7)
     for cfg in [L.SortConfig(bucket_target=0), L.SortConfig(rmi_bucket_count=256, tree_bucket_count=16),
