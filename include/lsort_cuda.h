@@ -19,6 +19,8 @@
  *   lsort_cuda_classify_tree <- SplitterTree::classify       proj/src/models.hpp:92-101
  *   lsort_cuda_verify        <- verify_sorted, multiset_hash proj/src/verify.hpp:17-29
  *   lsort_gen_keys           <- data.generate
+ *   lsort_read_keys / lsort_write_keys <- data.read_keys / write_keys SPEC.md:480-497
+ *   (lsort_cli, csrc/cli.cpp  <- bench-cli generate / bench / verify SPEC.md:521-590)
  *   lsort_cuda_dist_*        <- (none: multi-GPU layer is new)
  *
  * Conventions: return 0 (LSORT_OK) or an LSORT_E* code; the message is
@@ -45,6 +47,7 @@ extern "C" {
 #define LSORT_ECUDA 4
 #define LSORT_ENCCL 5
 #define LSORT_EINTERNAL 6
+#define LSORT_EIO 7
 
 #define LSORT_KEY_U64 0
 #define LSORT_KEY_F64 1
@@ -207,6 +210,16 @@ int lsort_cuda_verify(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_ki
  * memory `out` (double for 0-4,8; uint64 for 5-7). */
 int lsort_gen_keys(int dist, uint64_t total, uint64_t seed, uint64_t first, uint64_t count,
                    void* out, int threads);
+
+/* ---- key files (SPEC.md data module :480-497): an 8-byte little-endian count,
+ * then count 8-byte little-endian keys. Host-only; no context needed. ---- */
+/* read_keys: with keys == NULL only validates the file and returns its count
+ * in *n_out; a truncated / oversized file is LSORT_EIO with the expected and
+ * actual byte ranges in `err`. */
+int lsort_read_keys(const char* path, uint64_t* keys, uint64_t capacity, uint64_t* n_out, char* err,
+                    size_t errlen);
+/* write_keys: inverse of read_keys (n == 0 writes the 8-byte zero count). */
+int lsort_write_keys(const char* path, const uint64_t* keys, uint64_t n, char* err, size_t errlen);
 
 /* ---- multi-GPU phases (one process per GPU; collectives via the caller) ---- */
 /* Draw this rank's sample share (encoded keys) into device d_out[s]. */

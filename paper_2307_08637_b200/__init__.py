@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _native as N
 
-__all__ = ["SortConfig", "Context", "NanError", "LsortError", "sort", "generate", "DISTS",
+__all__ = ["SortConfig", "Context", "NanError", "LsortError", "sort", "generate", "read_keys", "write_keys", "DISTS",
            "build", "default_context"]
 
 DISTS = {"uniform": 0, "normal": 1, "lognormal05": 2, "exponential2": 3, "mixgauss": 4,
@@ -331,4 +331,31 @@ def generate(dist: str, n: int, seed: int, first: int = 0, count: int | None = N
                                 threads)
     if rc != N.LSORT_OK:
         raise ValueError("generate: bad arguments")
+    return out
+
+
+# --------------------------------------------------------------- key files
+def write_keys(path: str, keys) -> None:
+    """data.write_keys: 8-byte LE count + count 8-byte LE keys."""
+    a = np.ascontiguousarray(keys)
+    if a.dtype.itemsize != 8:
+        raise ValueError("write_keys: 8-byte keys expected")
+    err = C.create_string_buffer(512)
+    rc = N.lib().lsort_write_keys(str(path).encode(), C.c_void_p(a.ctypes.data), a.size, err, 512)
+    if rc != N.LSORT_OK:
+        raise OSError(err.value.decode())
+
+
+def read_keys(path: str) -> np.ndarray:
+    """data.read_keys -> uint64 array; a truncated or
+    oversized file raises OSError naming the expected and actual byte ranges."""
+    err = C.create_string_buffer(512)
+    n = C.c_uint64(0)
+    rc = N.lib().lsort_read_keys(str(path).encode(), None, 0, C.byref(n), err, 512)
+    if rc != N.LSORT_OK:
+        raise OSError(err.value.decode())
+    out = np.empty(n.value, np.uint64)
+    rc = N.lib().lsort_read_keys(str(path).encode(), C.c_void_p(out.ctypes.data), out.size, C.byref(n), err, 512)
+    if rc != N.LSORT_OK:
+        raise OSError(err.value.decode())
     return out

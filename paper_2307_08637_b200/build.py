@@ -16,12 +16,13 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(CSRC, "build")
 LIB = os.path.join(PKG, "liblsort_cuda.so")
+CLI = os.path.join(PKG, "lsort_cli")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
            "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 CU_SOURCES = ["partition.cu", "models.cu", "basecase.cu", "cluster.cu", "util.cu", "engine.cu"]
-CPP_SOURCES = ["gen.cpp"]
+CPP_SOURCES = ["gen.cpp", "keyio.cpp"]
 
 
 def _headers():
@@ -60,7 +61,7 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)
         if _stale(o, [s] + hdrs):
-            jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-c", s, "-o", o])
+            jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o])
     logs = []
     if jobs:
         with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
@@ -71,6 +72,14 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
         _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs +
              ["-Xcompiler", "-fopenmp", "-lcudart", "-lgomp"])
         os.replace(tmp, LIB)
+    # the command-line harness (SPEC.md bench-cli), linked against the library
+    cli_src = os.path.join(CSRC, "cli.cpp")
+    if _stale(CLI, [cli_src, LIB] + hdrs):
+        tmp = CLI + ".tmp"
+        _run(["g++", "-O2", "-std=c++20", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+              cli_src, "-o", tmp, "-L", os.path.dirname(LIB), "-llsort_cuda", "-L", "/usr/local/cuda/lib64",
+              "-lcudart", "-Wl,-rpath,$ORIGIN"])
+        os.replace(tmp, CLI)
     text = "\n".join(logs)
     if verbose and text:
         print(text)
