@@ -51,6 +51,9 @@ extern "C" {
 
 #define LSORT_KEY_U64 0
 #define LSORT_KEY_F64 1
+/* keys already encoded as u64 (keys.hpp:36-42), result decoded to float64 in
+ * place (lsort_cuda_sort only; the distributed local sort) */
+#define LSORT_KEY_ENC_F64 2
 
 #define LSORT_MEM_DEVICE 0
 #define LSORT_MEM_HOST 1

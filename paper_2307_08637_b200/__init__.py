@@ -130,7 +130,7 @@ class Context:
         N.lib().lsort_cuda_set_stream(self._h, C.c_void_p(s))
 
     # -- the drop-in sort ----------------------------------------------------
-    def sort(self, keys, cfg: SortConfig | None = None) -> dict:
+    def sort(self, keys, cfg: SortConfig | None = None, encoded_f64: bool = False) -> dict:
         """In-place ascending sort. `keys`: torch CUDA tensor (device) or a
         contiguous numpy array (host; copied in/out inside the call)."""
         L = N.lib()
@@ -147,6 +147,8 @@ class Context:
                 raise ValueError("device keys must be a contiguous CUDA tensor")
             self._sync_stream()
             kind, mem, ptr, n = _key_kind_of(keys), N.MEM_DEVICE, keys.data_ptr(), keys.numel()
+        if encoded_f64:  # u64 keys in encoded form; sorted result decoded to float64 in place
+            kind = N.KEY_ENC_F64
         rc = L.lsort_cuda_sort(self._h, C.c_void_p(ptr), n, kind, mem, C.byref(cfg_c), C.byref(stats),
                                C.byref(nan))
         if rc == N.LSORT_ENAN:

@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "liblsort_cuda.so")
 
 LSORT_OK, LSORT_EINVAL, LSORT_ENAN, LSORT_ENOMEM, LSORT_ECUDA, LSORT_ENCCL, LSORT_EINTERNAL, LSORT_EIO = range(8)
-KEY_U64, KEY_F64 = 0, 1
+KEY_U64, KEY_F64, KEY_ENC_F64 = 0, 1, 2
 MEM_DEVICE, MEM_HOST = 0, 1
 MAX_TREE = 1024
 MAX_RMI = 2048

@@ -124,7 +124,7 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws, ids, clus, bat[3], psample, slices;
+        kseg, ktp, kplan, qws, ids, clus, bat[3], psample, slices, dist_hist;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
@@ -134,6 +134,11 @@ struct lsort_ctx {
     std::vector<std::unique_ptr<lsort_ctx>> lanes;
     std::vector<std::unique_ptr<lsort_ctx>> subs;  // sort_many: one context per concurrent sort
     bool zero_copy = false;  // control transfers as kernels (copy engines busy with a batch)
+    // dist: bucket ids of (keys, n, kind) under the model with this fingerprint,
+    // left in `ids` by lsort_cuda_dist_histogram for lsort_cuda_dist_partition
+    const void* dist_keys = nullptr;
+    uint64_t dist_n = 0, dist_fp = 0;
+    int dist_kind = -1;
     PinBuf hstage;           // staging for small host->device transfers from pageable memory
     size_t hstage_off = 0;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
@@ -451,8 +456,17 @@ struct Engine {
     }
 
     // Sort n keys at `keys` (device) in place. Returns LSORT_ENAN via throw.
-    void sort(void* keys, uint64_t n, bool f64, lsort_stats* stats) {
-        if (n < 2) return;
+    // in_encoded: the keys are already encoded u64 (keys.hpp:36-42); with f64
+    // the sorted result is decoded to float64 in place (the decode fused into
+    // the final stores -- used for the keys a multi-GPU exchange delivers)
+    void sort(void* keys, uint64_t n, bool f64, lsort_stats* stats, bool in_encoded = false) {
+        if (n < 2) {
+            if (n == 1 && f64 && in_encoded) {
+                launch_decode((uint64_t*)keys, n, st);
+                launched();
+            }
+            return;
+        }
         if (!C->ctrl.ensure(sizeof(Ctrl)) || !C->hctrl.ensure(sizeof(Ctrl)) || !C->hmodel.ensure(sizeof(ModelHdr)))
             throw LsortError{LSORT_ENOMEM, "control block"};
         Ctrl* dctrl = C->ctrl.as<Ctrl>();
@@ -461,8 +475,12 @@ struct Engine {
         Ctrl* hc = C->hctrl.as<Ctrl>();
         const uint32_t cap = cfg.base_case_capacity;
         if (n <= cap) {
-            launch_small_sort(keys, n, f64, dctrl, st);
+            launch_small_sort(keys, n, f64 && !in_encoded, dctrl, st);
             launched();
+            if (f64 && in_encoded) {
+                launch_decode((uint64_t*)keys, n, st);
+                launched();
+            }
             down(hc, dctrl, sizeof(Ctrl));
             CU(cudaStreamSynchronize(st));
             if (hc->nan_index != ~0ull) throw LsortError{LSORT_ENAN, std::to_string(hc->nan_index)};
@@ -474,7 +492,7 @@ struct Engine {
             (uint32_t)std::ceil(std::log2((double)n) / std::log2((double)cfg.tree_bucket_count)) + 4;
         std::vector<SegPlan> segs{{0, n, 0, 0}};
         void* src = keys;
-        bool src_f64 = f64;
+        bool src_f64 = f64 && !in_encoded;
         uint64_t* dst = C->scratch.as<uint64_t>();
         uint32_t level = 0;
         DevCfg dc = dev_cfg(cfg);
@@ -826,7 +844,8 @@ int lsort_cuda_sort(lsort_ctx* C, void* keys, uint64_t n, int key_kind, int mem_
     if (!C) return LSORT_EINVAL;
     C->err.clear();
     if (nan_index_out) *nan_index_out = ~0ull;
-    if (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_F64) return fail(C, {LSORT_EINVAL, "key_kind"});
+    if (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_F64 && key_kind != LSORT_KEY_ENC_F64)
+        return fail(C, {LSORT_EINVAL, "key_kind"});
     if (mem_kind != LSORT_MEM_DEVICE && mem_kind != LSORT_MEM_HOST) return fail(C, {LSORT_EINVAL, "mem_kind"});
     if (n > 0 && !keys) return fail(C, {LSORT_EINVAL, "null keys"});
     lsort_cfg cfg = cfg_or_default(cfgp);
@@ -834,7 +853,8 @@ int lsort_cuda_sort(lsort_ctx* C, void* keys, uint64_t n, int key_kind, int mem_
     try {
         validate_cfg(cfg);
         CU(cudaSetDevice(C->device));
-        const bool f64 = key_kind == LSORT_KEY_F64;
+        const bool f64 = key_kind == LSORT_KEY_F64 || key_kind == LSORT_KEY_ENC_F64;
+        const bool enc = key_kind == LSORT_KEY_ENC_F64;
         C->launches = 0;
         void* dkeys = keys;
         cudaStream_t st = C->stream;
@@ -847,7 +867,7 @@ int lsort_cuda_sort(lsort_ctx* C, void* keys, uint64_t n, int key_kind, int mem_
         }
         CU(cudaEventRecord(C->ev[0], st));
         Engine E(C, cfg);
-        E.sort(dkeys, n, f64, stats);
+        E.sort(dkeys, n, f64, stats, enc);
         CU(cudaEventRecord(C->ev[1], st));
         if (mem_kind == LSORT_MEM_HOST) {
             CU(cudaMemcpyAsync(keys, dkeys, n * 8, cudaMemcpyDeviceToHost, st));
@@ -1385,34 +1405,137 @@ int lsort_cuda_dist_train(lsort_ctx* C, uint64_t* d_sample, uint64_t s, uint32_t
     return LSORT_OK;
 }
 
+}  // extern "C"
+
+namespace {
+uint64_t model_fingerprint(const lsort_rmi_header* h, const lsort_rmi_entry* e) {
+    uint64_t f = splitmix64(h->submodels);
+    auto mix = [&](const void* p, size_t bytes) {
+        const uint64_t* w = (const uint64_t*)p;
+        for (size_t i = 0; i < bytes / 8; ++i) f = splitmix64(f ^ w[i]);
+    };
+    mix(&h->root_slope, 8);
+    mix(&h->root_intercept, 8);
+    mix(&h->key_base, 8);
+    mix(&h->key_scale, 8);
+    mix(e, 32 * (size_t)h->submodels);
+    return f;
+}
+
+// One learned segment over all n keys: LevelParams with a one-entry kind plan
+// (the level-0 classify / scatter kernels of the single-GPU sort).
+LevelParams dist_level(lsort_ctx* C, const void* d_keys, uint64_t n, uint32_t B, unsigned long long* counters,
+                       uint64_t* d_out) {
+    if (!C->segs.ensure(sizeof(SegDesc)) || !C->tile_prefix.ensure(16) || !C->ctrl.ensure(sizeof(Ctrl)) ||
+        !C->kseg.ensure(16) || !C->ktp.ensure(64) || !C->kplan.ensure(3 * sizeof(KindPlan)) ||
+        !C->ids.ensure(2 * std::max<uint64_t>(n, 1)))
+        throw LsortError{LSORT_ENOMEM, "dist"};
+    SegDesc d{};
+    d.begin = 0;
+    d.n = n;
+    d.model_off = 0;
+    d.bucket_off = 0;
+    d.rmi_b = B;
+    d.nb_max = B;
+    const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
+    uint64_t pref[2] = {0, ntiles};
+    KindPlan kp[3] = {{1, 0, ntiles}, {0, 0, 0}, {0, 0, 0}};
+    uint32_t k0 = 0;
+    CU(cudaMemcpyAsync(C->segs.p, &d, sizeof(d), cudaMemcpyHostToDevice, C->stream));
+    CU(cudaMemcpyAsync(C->tile_prefix.p, pref, 16, cudaMemcpyHostToDevice, C->stream));
+    CU(cudaMemcpyAsync(C->kseg.p, &k0, 4, cudaMemcpyHostToDevice, C->stream));
+    CU(cudaMemcpyAsync(C->ktp.p, pref, 16, cudaMemcpyHostToDevice, C->stream));
+    CU(cudaMemcpyAsync(C->kplan.p, kp, sizeof(kp), cudaMemcpyHostToDevice, C->stream));
+    CU(cudaMemsetAsync(C->ctrl.p, 0, sizeof(Ctrl), C->stream));
+    CU(cudaMemsetAsync(&C->ctrl.as<Ctrl>()->nan_index, 0xff, 8, C->stream));
+    LevelParams p{};
+    p.segs = C->segs.as<SegDesc>();
+    p.nsegs = 1;
+    p.tile_prefix = C->tile_prefix.as<uint64_t>();
+    p.ntiles = ntiles;
+    p.models = C->models.as<uint8_t>();
+    p.buckets = counters;
+    p.src = d_keys;
+    p.dst = d_out;
+    p.ids = C->ids.as<uint16_t>();
+    p.ctrl = C->ctrl.as<Ctrl>();
+    p.kseg = C->kseg.as<uint32_t>();
+    p.ktp = C->ktp.as<uint64_t>();
+    p.kplan = C->kplan.as<KindPlan>();
+    p.kstride = 1;
+    return p;
+}
+
+// classify + histogram (d_hist, zeroed here) + bucket ids in C->ids
+void dist_hist_ids(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, const lsort_rmi_header* h,
+                   const lsort_rmi_entry* e, unsigned long long* d_hist) {
+    const uint32_t B = h->submodels;
+    upload_learned(C, h, e, B, 0.0, 1.0);
+    CU(cudaMemsetAsync(d_hist, 0, 8 * (size_t)B, C->stream));
+    LevelParams p = dist_level(C, d_keys, n, B, d_hist, nullptr);
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(p.ntiles, (uint64_t)num_sms() * kPartPerSM));
+    if (n) launch_hist(p, key_kind == LSORT_KEY_F64, 1u, B, grid, C->stream);
+    C->dist_keys = d_keys;
+    C->dist_n = n;
+    C->dist_kind = key_kind;
+    C->dist_fp = model_fingerprint(h, e);
+}
+}  // namespace
+
+extern "C" {
+
 int lsort_cuda_dist_histogram(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, const lsort_rmi_header* h,
                               const lsort_rmi_entry* e, uint64_t* d_hist) {
-    return lsort_cuda_classify_rmi(C, h, e, h ? h->submodels : 0, 0.0, 1.0, d_keys, n, key_kind, nullptr, d_hist);
+    if (!C || !h || !e || !d_hist || h->submodels < 2 || h->submodels > LSORT_MAX_RMI) return LSORT_EINVAL;
+    try {
+        CU(cudaSetDevice(C->device));
+        dist_hist_ids(C, d_keys, n, key_kind, h, e, (unsigned long long*)d_hist);
+        // the local histogram stays with the ids (the caller all-reduces d_hist)
+        if (!C->dist_hist.ensure(8 * (size_t)h->submodels)) throw LsortError{LSORT_ENOMEM, "dist"};
+        CU(cudaMemcpyAsync(C->dist_hist.p, d_hist, 8 * (size_t)h->submodels, cudaMemcpyDeviceToDevice, C->stream));
+        Ctrl hc;
+        CU(cudaMemcpyAsync(&hc, C->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, C->stream));
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+        if (hc.nan_index != ~0ull) {
+            C->dist_keys = nullptr;
+            C->err = "NaN at index " + std::to_string(hc.nan_index);
+            return LSORT_ENAN;
+        }
+    } catch (const LsortError& er) {
+        C->dist_keys = nullptr;
+        return fail(C, er);
+    }
+    return LSORT_OK;
 }
 
 int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, const lsort_rmi_header* h,
                               const lsort_rmi_entry* e, const uint32_t* bucket_bounds, uint32_t nranks,
                               uint64_t* d_out, uint64_t* send_counts) {
-    if (!C || !h || !e || !bucket_bounds || nranks == 0 || nranks > 1024) return LSORT_EINVAL;
+    if (!C || !h || !e || !bucket_bounds || nranks == 0 || nranks > 1024 || h->submodels < 2 ||
+        h->submodels > LSORT_MAX_RMI)
+        return LSORT_EINVAL;
     try {
         CU(cudaSetDevice(C->device));
         const uint32_t B = h->submodels;
-        upload_learned(C, h, e, B, 0.0, 1.0);
         // bucket -> destination rank map and per-rank histogram
         std::vector<uint32_t> map(B);
         for (uint32_t r = 0; r < nranks; ++r)
             for (uint32_t b = bucket_bounds[r]; b < bucket_bounds[r + 1] && b < B; ++b) map[b] = r;
-        if (!C->aux.ensure(B * 4 + 8 * (size_t)B + 8 * (size_t)nranks) || !C->segs.ensure(sizeof(SegDesc)) ||
-            !C->tile_prefix.ensure(16) || !C->ctrl.ensure(sizeof(Ctrl)))
-            throw LsortError{LSORT_ENOMEM, "dist"};
+        if (!C->aux.ensure(B * 4 + 8 * (size_t)B + 8 * (size_t)nranks + 16)) throw LsortError{LSORT_ENOMEM, "dist"};
         uint32_t* dmap = C->aux.as<uint32_t>();
         unsigned long long* dhist = (unsigned long long*)(C->aux.as<uint8_t>() + B * 4 + 4 * (B & 1));
         unsigned long long* dcur = dhist + B;
         CU(cudaMemcpyAsync(dmap, map.data(), B * 4, cudaMemcpyHostToDevice, C->stream));
-        CU(cudaMemsetAsync(dhist, 0, 8 * (size_t)B, C->stream));
-        if (!C->ids.ensure(2 * n)) throw LsortError{LSORT_ENOMEM, "dist ids"};
-        launch_classify_ids(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, nullptr,
-                            C->ids.as<uint16_t>(), dhist, (int)kLearnedEntryBytes * (int)B, C->stream);
+        // the ids from lsort_cuda_dist_histogram of the same keys under the same model are reused
+        const bool have_ids = C->dist_keys == d_keys && C->dist_n == n && C->dist_kind == key_kind &&
+                              C->dist_fp == model_fingerprint(h, e);
+        if (have_ids) {
+            upload_learned(C, h, e, B, 0.0, 1.0);  // (the model arena may have been reused since)
+            CU(cudaMemcpyAsync(dhist, C->dist_hist.p, 8 * (size_t)B, cudaMemcpyDeviceToDevice, C->stream));
+        } else {
+            dist_hist_ids(C, d_keys, n, key_kind, h, e, dhist);
+        }
         std::vector<uint64_t> hist(B);
         CU(cudaMemcpyAsync(hist.data(), dhist, 8 * (size_t)B, cudaMemcpyDeviceToHost, C->stream));
         CU(cudaStreamSynchronize(C->stream));
@@ -1426,43 +1549,9 @@ int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int 
             acc += c;
         }
         CU(cudaMemcpyAsync(dcur, cur.data(), 8 * (size_t)nranks, cudaMemcpyHostToDevice, C->stream));
-        SegDesc d{};
-        d.begin = 0;
-        d.n = n;
-        d.model_off = 0;
-        d.bucket_off = 0;
-        d.rmi_b = B;
-        uint64_t pref[2] = {0, (n + kTileKeys - 1) / kTileKeys};
-        CU(cudaMemcpyAsync(C->segs.p, &d, sizeof(d), cudaMemcpyHostToDevice, C->stream));
-        CU(cudaMemcpyAsync(C->tile_prefix.p, pref, 16, cudaMemcpyHostToDevice, C->stream));
-        CU(cudaMemsetAsync(C->ctrl.p, 0, sizeof(Ctrl), C->stream));
-        CU(cudaMemsetAsync(&C->ctrl.as<Ctrl>()->nan_index, 0xff, 8, C->stream));
-        LevelParams p{};
-        p.segs = C->segs.as<SegDesc>();
-        p.nsegs = 1;
-        p.tile_prefix = C->tile_prefix.as<uint64_t>();
-        p.ntiles = pref[1];
-        p.models = C->models.as<uint8_t>();
-        p.buckets = dcur;
-        p.src = d_keys;
-        p.dst = d_out;
-        p.ctrl = C->ctrl.as<Ctrl>();
-        // single learned segment: a one-entry kind plan
-        if (!C->kseg.ensure(16) || !C->ktp.ensure(64) || !C->kplan.ensure(3 * sizeof(KindPlan)))
-            throw LsortError{LSORT_ENOMEM, "dist"};
-        KindPlan kp[3] = {{1, 0, pref[1]}, {0, 0, 0}, {0, 0, 0}};
-        uint32_t k0 = 0;
-        uint64_t tp[2] = {0, pref[1]};
-        CU(cudaMemcpyAsync(C->kseg.p, &k0, 4, cudaMemcpyHostToDevice, C->stream));
-        CU(cudaMemcpyAsync(C->ktp.p, tp, 16, cudaMemcpyHostToDevice, C->stream));
-        CU(cudaMemcpyAsync(C->kplan.p, kp, sizeof(kp), cudaMemcpyHostToDevice, C->stream));
-        p.kseg = C->kseg.as<uint32_t>();
-        p.ktp = C->ktp.as<uint64_t>();
-        p.kplan = C->kplan.as<KindPlan>();
-        p.kstride = 1;
-        int grid = (int)std::min<uint64_t>(pref[1], (uint64_t)num_sms() * kPartPerSM);
-        p.ids = C->ids.as<uint16_t>();
-        launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, grid, C->stream);
+        LevelParams p = dist_level(C, d_keys, n, B, dcur, d_out);
+        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(p.ntiles, (uint64_t)num_sms() * kPartPerSM));
+        if (n) launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, grid, C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
     } catch (const LsortError& er) {

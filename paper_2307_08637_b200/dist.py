@@ -71,6 +71,8 @@ def sample_shares(n_local: list[int], s_total: int) -> list[int]:
 class NativeOps:
     """Device steps through the C-ABI (liblsort_cuda.so)."""
 
+    fused_decode = True  # local_sort(to_f64=True) decodes in its final stores
+
     def __init__(self, ctx):
         self.ctx = ctx
 
@@ -100,7 +102,19 @@ class NativeOps:
         return pack_rmi(h, e)
 
     def histogram(self, keys, P, buckets: int):
-        _, hist = self.ctx.classify_rmi(P, buckets, buckets, keys, ids=False)
+        # lsort_cuda_dist_histogram: the level-0 classify kernel; it also keeps
+        # the bucket ids, which lsort_cuda_dist_partition then reuses
+        import ctypes as C
+        import torch
+        from . import _native as N
+        from . import _key_kind_of, unpack_rmi
+        h, e = unpack_rmi(P, buckets)
+        hist = torch.zeros(buckets, dtype=torch.int64, device=keys.device)
+        self.ctx._sync_stream()
+        rc = N.lib().lsort_cuda_dist_histogram(self.ctx._h, C.c_void_p(keys.data_ptr()), keys.numel(),
+                                               _key_kind_of(keys), C.byref(h), e.ctypes.data_as(C.c_void_p),
+                                               C.c_void_p(hist.data_ptr()))
+        self._check(rc)
         return hist
 
     def partition(self, keys, P, buckets: int, bounds: np.ndarray):
@@ -121,8 +135,9 @@ class NativeOps:
         self._check(rc)
         return out[: keys.numel()], [int(c) for c in counts]
 
-    def local_sort(self, keys_u64, cfg):
-        return self.ctx.sort(keys_u64, cfg)
+    def local_sort(self, keys_u64, cfg, to_f64: bool = False):
+        # to_f64: the decode is fused into the local sort's final stores
+        return self.ctx.sort(keys_u64, cfg, encoded_f64=to_f64)
 
     def decode(self, keys_u64):
         import ctypes as C
@@ -163,6 +178,17 @@ class DistSorter:
         import torch.distributed as dist
         g = self.group
         rank, world = dist.get_rank(g), dist.get_world_size(g)
+        import os
+        import time
+        trace = bool(os.environ.get("LSORT_DIST_TRACE")) and keys.is_cuda
+        marks = []
+
+        def mark(name):
+            if trace:
+                torch.cuda.synchronize()
+                marks.append((name, time.perf_counter()))
+
+        mark("start")
         dev = keys.device
         is_f64 = keys.dtype == torch.float64
         n_local = keys.numel()
@@ -182,25 +208,41 @@ class DistSorter:
         gathered = [torch.empty_like(pad) for _ in range(world)]
         dist.all_gather(gathered, pad, group=g)
         sample = torch.cat([gathered[r][: shares[r]] for r in range(world)]).contiguous()
+        mark("sample+gather")
         P = self.ops.train(sample, self.buckets)
+        mark("train")
         # ---- 3. global histogram
         hist = self.ops.histogram(keys, P, self.buckets).to(torch.int64)
+        mark("histogram")
         dist.all_reduce(hist, group=g)
         # ---- 4. rank boundaries
         bounds = rank_bounds(hist.cpu().numpy(), world)
         # ---- 5. partition + exchange
+        mark("allreduce+bounds")
         part, send = self.ops.partition(keys, P, self.buckets, bounds)
+        mark("partition")
         send_t = torch.tensor(send, dtype=torch.int64, device=dev)
         recv_t = torch.empty(world, dtype=torch.int64, device=dev)
         dist.all_to_all_single(recv_t, send_t, group=g)
         recv = [int(x) for x in recv_t.cpu().tolist()]
         out = torch.empty(max(sum(recv), 1), dtype=torch.int64, device=dev)[: sum(recv)]
         dist.all_to_all_single(out, part, output_split_sizes=recv, input_split_sizes=send, group=g)
+        mark("exchange")
         # ---- 6. local sort of encoded keys, decode
         from . import SortConfig
         lcfg = SortConfig(**{**self.cfg.__dict__})
-        local = self.ops.local_sort(out, lcfg) if out.numel() else {}
-        result = self.ops.decode(out) if is_f64 else out
+        fused = is_f64 and getattr(self.ops, "fused_decode", False)
+        local = self.ops.local_sort(out, lcfg, to_f64=True) if fused else \
+            (self.ops.local_sort(out, lcfg) if out.numel() else {})
+        mark("local sort")
+        if fused:
+            result = out.view(torch.float64)
+        else:
+            result = self.ops.decode(out) if is_f64 else out
+        mark("decode")
+        if trace and rank == 0:
+            print("[dist] " + " ".join(f"{marks[i][0]} {1e3 * (marks[i][1] - marks[i - 1][1]):.3f}"
+                                     for i in range(1, len(marks))) + " ms", flush=True)
         stats = DistStats(n_in=n_local, n_out=int(out.numel()), sample=s_total, send_counts=tuple(send),
                           bounds=tuple(int(b) for b in bounds), local=local)
         return result, stats.__dict__

@@ -388,6 +388,16 @@ def test_sort_batch_device(ctx):
     check_sorted_f64(bad[0], db[0].cpu().numpy())
 
 
+@pytest.mark.parametrize("n", [1, 5000, 2_000_000])
+def test_sort_encoded_to_f64(ctx, n):
+    """LSORT_KEY_ENC_F64: encoded u64 keys in, decoded float64 out (the
+    distributed local sort's fused decode)."""
+    x = O.generate("lognormal2", n, 19)
+    d = dev(O.encode(x))
+    ctx.sort(d, encoded_f64=True)
+    check_sorted_f64(x, d.cpu().numpy().view(np.float64))
+
+
 def test_sort_configs(ctx):
     x = O.generate("exponential2", 1_000_000, 7)
     for cfg in [L.SortConfig(bucket_target=0), L.SortConfig(rmi_bucket_count=256, tree_bucket_count=16),
