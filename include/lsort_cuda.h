@@ -150,7 +150,9 @@ int lsort_cuda_ctx_create(lsort_ctx** out, int device, void* cuda_stream /* null
                           size_t workspace_hint /* keys; 0 = grow on demand */);
 int lsort_cuda_ctx_destroy(lsort_ctx* ctx);
 const char* lsort_cuda_last_error(const lsort_ctx* ctx);
-/* Set the stream for subsequent calls (nullable = the context's own stream). */
+/* Set the stream for subsequent calls (nullable = the context's own
+ * non-blocking stream, which is NOT ordered after work on the legacy default
+ * stream: the caller synchronises that work first). */
 int lsort_cuda_set_stream(lsort_ctx* ctx, void* cuda_stream);
 
 /* In-place ascending sort of n keys (uint64 or float64). mem_kind DEVICE:
@@ -223,6 +225,20 @@ int lsort_read_keys(const char* path, uint64_t* keys, uint64_t capacity, uint64_
                     size_t errlen);
 /* write_keys: inverse of read_keys (n == 0 writes the 8-byte zero count). */
 int lsort_write_keys(const char* path, const uint64_t* keys, uint64_t n, char* err, size_t errlen);
+
+/* Model forwarding (LearnedSort 2.0 classic path; Learned
+ * cdf_lo / cdf_hi, models.hpp:128-138): sort device keys known to fall in
+ * buckets [b_lo, b_hi) of the learned model (h, entries) with h->submodels
+ * buckets. The root level reuses that model restricted to the CDF range
+ * [b_lo/B, b_hi/B) with b_hi - b_lo buckets -- no sampling, no training;
+ * with d_sorted_sample (the sorted sample the model was trained on, device)
+ * the children train on their slices of it. The sorted output is the same as
+ * lsort_cuda_sort's; keys outside the range are still sorted correctly (they
+ * land in the first / last bucket). key_kind may be LSORT_KEY_ENC_F64. */
+int lsort_cuda_sort_forward(lsort_ctx* ctx, void* d_keys, uint64_t n, int key_kind, const lsort_cfg* cfg,
+                            const lsort_rmi_header* h, const lsort_rmi_entry* entries, uint32_t b_lo,
+                            uint32_t b_hi, const uint64_t* d_sorted_sample, uint64_t sample_n,
+                            lsort_stats* stats, uint64_t* nan_index_out);
 
 /* ---- multi-GPU phases (one process per GPU; collectives via the caller) ---- */
 /* Draw this rank's sample share (encoded keys) into device d_out[s]. */

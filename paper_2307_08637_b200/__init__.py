@@ -124,10 +124,17 @@ class Context:
 
     # -- streams -----------------------------------------------------------
     def _sync_stream(self):
-        """Run on torch's current stream so ordering with torch ops holds."""
+        """Order the native call after the work torch has queued: run on torch's
+        current stream; when that is the legacy default stream (handle 0, which
+        the C-ABI reads as 'the context's own stream'), wait for it first --
+        a NCCL collective or an async copy feeding the keys would otherwise race
+        the sort."""
         torch = _torch()
-        s = torch.cuda.current_stream(self.device).cuda_stream
-        N.lib().lsort_cuda_set_stream(self._h, C.c_void_p(s))
+        cur = torch.cuda.current_stream(self.device)
+        s = cur.cuda_stream
+        if not s:
+            cur.synchronize()
+        N.lib().lsort_cuda_set_stream(self._h, C.c_void_p(s) if s else None)
 
     # -- the drop-in sort ----------------------------------------------------
     def sort(self, keys, cfg: SortConfig | None = None, encoded_f64: bool = False) -> dict:
@@ -203,6 +210,26 @@ class Context:
             err = NanError(int(nans[i]))
             err.array = i
             raise err
+        _check(self, rc)
+        return stats.as_dict()
+
+    def sort_forward(self, d_keys, P: np.ndarray, submodels: int, b_lo: int, b_hi: int, d_sorted_sample=None,
+                     cfg: SortConfig | None = None, encoded_f64: bool = False) -> dict:
+        """lsort_cuda_sort_forward: sort device keys of buckets [b_lo, b_hi) of the
+        learned model P (packed) with its root level forwarded (no training)."""
+        self._sync_stream()
+        h, e = unpack_rmi(P, submodels)
+        cfg_c = (cfg or SortConfig()).to_c()
+        stats = N.lsort_stats()
+        nan = C.c_uint64(0)
+        kind = N.KEY_ENC_F64 if encoded_f64 else _key_kind_of(d_keys)
+        sp = C.c_void_p(d_sorted_sample.data_ptr()) if d_sorted_sample is not None else None
+        sn = d_sorted_sample.numel() if d_sorted_sample is not None else 0
+        rc = N.lib().lsort_cuda_sort_forward(self._h, C.c_void_p(d_keys.data_ptr()), d_keys.numel(), kind,
+                                             C.byref(cfg_c), C.byref(h), e.ctypes.data_as(C.c_void_p), b_lo, b_hi,
+                                             sp, sn, C.byref(stats), C.byref(nan))
+        if rc == N.LSORT_ENAN:
+            raise NanError(int(nan.value))
         _check(self, rc)
         return stats.as_dict()
 

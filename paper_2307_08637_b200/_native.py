@@ -70,7 +70,7 @@ class lsort_stats(C.Structure):
 
 EXPORTS = [
     "lsort_cfg_default", "lsort_cuda_ctx_create", "lsort_cuda_ctx_destroy", "lsort_cuda_last_error",
-    "lsort_cuda_set_stream", "lsort_cuda_sort", "lsort_cuda_sort_batch", "lsort_cuda_sort_many", "lsort_read_keys", "lsort_write_keys", "lsort_cuda_rmi_train", "lsort_cuda_classify_rmi",
+    "lsort_cuda_set_stream", "lsort_cuda_sort", "lsort_cuda_sort_batch", "lsort_cuda_sort_many", "lsort_read_keys", "lsort_write_keys", "lsort_cuda_sort_forward", "lsort_cuda_rmi_train", "lsort_cuda_classify_rmi",
     "lsort_cuda_tree_build", "lsort_cuda_classify_tree", "lsort_cuda_build_model",
     "lsort_cuda_block_sort", "lsort_cuda_verify", "lsort_gen_keys", "lsort_cuda_dist_sample",
     "lsort_cuda_dist_train", "lsort_cuda_dist_histogram", "lsort_cuda_dist_partition",
@@ -103,6 +103,9 @@ def lib():
     L.lsort_cuda_set_stream.argtypes = [vp, vp]
     L.lsort_cuda_sort.restype = i32
     L.lsort_cuda_sort.argtypes = [vp, vp, u64, i32, i32, P(lsort_cfg), P(lsort_stats), P(u64)]
+    L.lsort_cuda_sort_forward.restype = i32
+    L.lsort_cuda_sort_forward.argtypes = [vp, vp, u64, i32, P(lsort_cfg), P(lsort_rmi_header), vp, C.c_uint32,
+                                          C.c_uint32, vp, u64, P(lsort_stats), P(u64)]
     L.lsort_read_keys.restype = i32
     L.lsort_read_keys.argtypes = [C.c_char_p, vp, u64, P(u64), C.c_char_p, C.c_size_t]
     L.lsort_write_keys.restype = i32

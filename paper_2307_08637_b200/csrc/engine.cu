@@ -124,7 +124,7 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws, ids, clus, bat[3], psample, slices, dist_hist;
+        kseg, ktp, kplan, qws, ids, clus, bat[3], psample, slices, dist_hist, fwd_model, fwd_slices;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
@@ -207,6 +207,18 @@ DevCfg dev_cfg(const lsort_cfg& c) {
     d.psample = nullptr;
     return d;
 }
+
+// Model forwarding (LearnedSort 2.0 classic path, cdf_lo/cdf_hi
+// models.hpp:128-138): the root level reuses a given learned model restricted
+// to a CDF range instead of sampling and training; its children train on
+// slices of the given sorted sample.
+struct Forward {
+    const uint8_t* model = nullptr;  // device ModelHdr + learned payload (cdf range, nb local buckets)
+    size_t model_bytes = 0;
+    uint32_t nb = 0, B = 0;          // local buckets, submodels
+    const uint32_t* slices = nullptr;  // device [nb+1] offsets into psample, or nullptr
+    const uint64_t* psample = nullptr;
+};
 
 struct Engine {
     lsort_ctx* C;
@@ -459,7 +471,8 @@ struct Engine {
     // in_encoded: the keys are already encoded u64 (keys.hpp:36-42); with f64
     // the sorted result is decoded to float64 in place (the decode fused into
     // the final stores -- used for the keys a multi-GPU exchange delivers)
-    void sort(void* keys, uint64_t n, bool f64, lsort_stats* stats, bool in_encoded = false) {
+    void sort(void* keys, uint64_t n, bool f64, lsort_stats* stats, bool in_encoded = false,
+              const Forward* fw = nullptr) {
         if (n < 2) {
             if (n == 1 && f64 && in_encoded) {
                 launch_decode((uint64_t*)keys, n, st);
@@ -530,7 +543,7 @@ struct Engine {
                 d.depth = s.depth;
                 d.flags = s.flags;
                 d.pslice = s.pslice;
-                d.rmi_b = rmi_b(s.n);
+                d.rmi_b = (fw && level == 0) ? fw->nb : rmi_b(s.n);
                 max_rmi_b = std::max(max_rmi_b, d.rmi_b);
                 d.tree_k = tree_k(s.n);
                 uint32_t payload, nb;
@@ -551,6 +564,13 @@ struct Engine {
                 max_nb = std::max(max_nb, nb);
                 hp[j] = ntiles;
                 ntiles += (s.n + kTileKeys - 1) / kTileKeys;
+                if (fw && level == 0) {  // forwarded root model: nothing to build
+                    payload = std::max<uint32_t>(payload, (uint32_t)fw->model_bytes);
+                    kinds |= 1u;
+                    max_rmi_b = std::max(max_rmi_b, fw->B);
+                    model_bytes = d.model_off + sizeof(ModelHdr) + payload;
+                    continue;
+                }
                 const int mc = model_class(s);
                 if (mc == 2) bigs.push_back(j);
                 else if (mc == 1) mids.push_back(j);
@@ -615,7 +635,12 @@ struct Engine {
             // GPU policy: the root's sorted model sample seeds its children's models
             uint32_t* root_slices = nullptr;
             dc.psample = (level == 1 && C->psample.p) ? C->psample.as<uint64_t>() : nullptr;
-            if (level == 0 && np == 1 && bigs.size() == 1 && !(cfg.flags & LSORT_FLAG_STRICT_POLICY)) {
+            if (fw) dc.psample = level == 1 ? fw->psample : nullptr;
+            if (fw && level == 0) {
+                CU(cudaMemcpyAsync(C->models.p, fw->model, fw->model_bytes, cudaMemcpyDeviceToDevice, st));
+                p.slices = fw->slices;
+            }
+            if (!fw && level == 0 && np == 1 && bigs.size() == 1 && !(cfg.flags & LSORT_FLAG_STRICT_POLICY)) {
                 if (!C->slices.ensure(4 * ((size_t)hs[0].nb_max + 2))) throw LsortError{LSORT_ENOMEM, "slices"};
                 CU(cudaMemsetAsync(C->slices.p, 0, 4 * ((size_t)hs[0].nb_max + 2), st));
                 root_slices = C->slices.as<uint32_t>();
@@ -746,7 +771,8 @@ struct Engine {
                 const SegOut* r = C->hrec.as<SegOut>();
                 segs.reserve(nrec);
                 for (uint32_t i = 0; i < nrec; ++i)
-                    segs.push_back({r[i].begin, r[i].n, r[i].depth, r[i].flags, C->psample.p ? r[i].pslice : 0});
+                    segs.push_back({r[i].begin, r[i].n, r[i].depth, r[i].flags,
+                                    (C->psample.p || (fw && fw->psample)) ? r[i].pslice : 0});
                 std::sort(segs.begin(), segs.end(),
                           [](const SegPlan& a, const SegPlan& b) { return a.begin < b.begin; });
             }
@@ -1483,6 +1509,61 @@ void dist_hist_ids(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, c
 }  // namespace
 
 extern "C" {
+
+int lsort_cuda_sort_forward(lsort_ctx* C, void* d_keys, uint64_t n, int key_kind, const lsort_cfg* cfgp,
+                            const lsort_rmi_header* h, const lsort_rmi_entry* e, uint32_t b_lo, uint32_t b_hi,
+                            const uint64_t* d_sorted_sample, uint64_t sample_n, lsort_stats* stats,
+                            uint64_t* nan_index_out) {
+    if (!C || !h || !e) return LSORT_EINVAL;
+    C->err.clear();
+    if (nan_index_out) *nan_index_out = ~0ull;
+    const uint32_t B = h->submodels;
+    if (B < 2 || B > LSORT_MAX_RMI || b_lo >= b_hi || b_hi > B || (n && !d_keys))
+        return fail(C, {LSORT_EINVAL, "sort_forward: bad model / bucket range"});
+    if (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_F64 && key_kind != LSORT_KEY_ENC_F64)
+        return fail(C, {LSORT_EINVAL, "key_kind"});
+    lsort_cfg cfg = cfg_or_default(cfgp);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    try {
+        validate_cfg(cfg);
+        CU(cudaSetDevice(C->device));
+        Forward fw;
+        fw.B = B;
+        fw.nb = b_hi - b_lo;
+        if (d_sorted_sample && sample_n >= 2 && !(cfg.flags & LSORT_FLAG_STRICT_POLICY)) {
+            // bucket offsets of the sorted sample under the full model (nb = B); the
+            // slice of local bucket b starts at offsets[b_lo + b]
+            upload_learned(C, h, e, B, 0.0, 1.0);
+            if (!C->fwd_slices.ensure(4 * ((size_t)B + 2))) throw LsortError{LSORT_ENOMEM, "forward"};
+            launch_sample_slices(d_sorted_sample, sample_n, C->models.as<uint8_t>(), C->fwd_slices.as<uint32_t>(), B,
+                                 nullptr, C->stream);
+            fw.slices = C->fwd_slices.as<uint32_t>() + b_lo;
+            fw.psample = d_sorted_sample;
+        }
+        // the forwarded root: the same RMI restricted to CDF [b_lo/B, b_hi/B) with
+        // b_hi - b_lo buckets (Learned::bucket_index, models.hpp:128-138,162-171)
+        upload_learned(C, h, e, fw.nb, (double)b_lo / B, (double)b_hi / B);
+        fw.model_bytes = sizeof(ModelHdr) + kLearnedEntryBytes * (size_t)B;
+        if (!C->fwd_model.ensure(fw.model_bytes)) throw LsortError{LSORT_ENOMEM, "forward"};
+        CU(cudaMemcpyAsync(C->fwd_model.p, C->models.p, fw.model_bytes, cudaMemcpyDeviceToDevice, C->stream));
+        fw.model = C->fwd_model.as<uint8_t>();
+        C->launches = 0;
+        Engine E(C, cfg);
+        E.sort(d_keys, n, key_kind != LSORT_KEY_U64, stats, key_kind == LSORT_KEY_ENC_F64, &fw);
+        CU(cudaStreamSynchronize(C->stream));
+        if (stats) stats->kernel_launches = C->launches;
+    } catch (const LsortError& e2) {
+        cudaStreamSynchronize(C->stream);
+        cudaGetLastError();
+        if (e2.code == LSORT_ENAN) {
+            if (nan_index_out) *nan_index_out = std::stoull(e2.msg);
+            C->err = "NaN at index " + e2.msg;
+            return LSORT_ENAN;
+        }
+        return fail(C, e2);
+    }
+    return LSORT_OK;
+}
 
 int lsort_cuda_dist_histogram(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, const lsort_rmi_header* h,
                               const lsort_rmi_entry* e, uint64_t* d_hist) {

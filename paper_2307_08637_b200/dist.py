@@ -135,8 +135,14 @@ class NativeOps:
         self._check(rc)
         return out[: keys.numel()], [int(c) for c in counts]
 
-    def local_sort(self, keys_u64, cfg, to_f64: bool = False):
-        # to_f64: the decode is fused into the local sort's final stores
+    def local_sort(self, keys_u64, cfg, to_f64: bool = False, forward=None):
+        # to_f64: the decode is fused into the local sort's final stores.
+        # forward = (P, buckets, b_lo, b_hi, sorted global sample): the local root
+        # level reuses the global model restricted to this rank's buckets
+        if forward is not None:
+            P, buckets, b_lo, b_hi, sample = forward
+            if b_hi > b_lo:
+                return self.ctx.sort_forward(keys_u64, P, buckets, b_lo, b_hi, sample, cfg, encoded_f64=to_f64)
         return self.ctx.sort(keys_u64, cfg, encoded_f64=to_f64)
 
     def decode(self, keys_u64):
@@ -181,11 +187,15 @@ class DistSorter:
         import os
         import time
         trace = bool(os.environ.get("LSORT_DIST_TRACE")) and keys.is_cuda
+        sync_at = set(filter(None, os.environ.get("LSORT_DIST_SYNC", "").split(",")))
         marks = []
 
         def mark(name):
-            if trace:
+            if trace or name in sync_at:
                 torch.cuda.synchronize()
+            elif "cur:" + name in sync_at:
+                torch.cuda.current_stream().synchronize()
+            if trace:
                 marks.append((name, time.perf_counter()))
 
         mark("start")
@@ -232,8 +242,14 @@ class DistSorter:
         from . import SortConfig
         lcfg = SortConfig(**{**self.cfg.__dict__})
         fused = is_f64 and getattr(self.ops, "fused_decode", False)
-        local = self.ops.local_sort(out, lcfg, to_f64=True) if fused else \
-            (self.ops.local_sort(out, lcfg) if out.numel() else {})
+        if fused:  # native ops: forwarded root model + fused decode
+            fwd = (P, self.buckets, int(bounds[rank]), int(bounds[rank + 1]), sample)
+            local = self.ops.local_sort(out, lcfg, to_f64=True, forward=fwd)
+        elif getattr(self.ops, "fused_decode", False):
+            fwd = (P, self.buckets, int(bounds[rank]), int(bounds[rank + 1]), sample)
+            local = self.ops.local_sort(out, lcfg, forward=fwd) if out.numel() else {}
+        else:
+            local = self.ops.local_sort(out, lcfg) if out.numel() else {}
         mark("local sort")
         if fused:
             result = out.view(torch.float64)

@@ -398,6 +398,32 @@ def test_sort_encoded_to_f64(ctx, n):
     check_sorted_f64(x, d.cpu().numpy().view(np.float64))
 
 
+@pytest.mark.parametrize("dist_name,seed", [("normal", 7), ("uniform", 42), ("lognormal2", 19)])
+def test_sort_forward(ctx, dist_name, seed):
+    """lsort_cuda_sort_forward: the root level reuses a given RMI restricted to a
+    bucket range (LearnedSort 2.0 model forwarding, cdf_lo/cdf_hi); exact output
+    for the full range and for the keys of a sub-range of buckets."""
+    n, B = 4_000_000, 2048
+    x = O.generate(dist_name, n, seed)
+    k = O.encode(x)
+    rng = np.random.default_rng(1)
+    samp = np.sort(k[rng.integers(0, n, 40_000)])
+    ds = dev(samp)
+    P = ctx.rmi_train(ds, B)
+    d = dev(k)
+    ctx.sort_forward(d, P, B, 0, B, ds)
+    assert np.array_equal(host_u64(d), np.sort(k))
+    ids = O.learned_bucket(P, B, B, k)
+    lo, hi = 700, 1300
+    sub = k[(ids >= lo) & (ids < hi)]
+    d2 = dev(sub)
+    ctx.sort_forward(d2, P, B, lo, hi, ds)
+    assert np.array_equal(host_u64(d2), np.sort(sub))
+    d3 = dev(sub)  # encoded in, float64 out, no sample
+    ctx.sort_forward(d3, P, B, lo, hi, None, encoded_f64=True)
+    assert np.array_equal(O.encode(d3.cpu().numpy().view(np.float64)), np.sort(sub))
+
+
 def test_sort_configs(ctx):
     x = O.generate("exponential2", 1_000_000, 7)
     for cfg in [L.SortConfig(bucket_target=0), L.SortConfig(rmi_bucket_count=256, tree_bucket_count=16),
