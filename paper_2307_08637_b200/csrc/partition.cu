@@ -450,7 +450,16 @@ struct ScatterSmem {
     uint32_t cnt[NBC + 1];
     uint16_t sbid[kTileKeys];
     uint32_t wsum[kPNT / 32 + 1];
+    alignas(16) uint16_t sids[2][kTileKeys + 16];  // the tile's bucket ids, bulk-copied with its keys
 };
+
+// ids of a tile's 16-byte interior: the covering 16-byte aligned range of the
+// u16 id array (ids [a0 & ~7, roundup8(a0 + 2 npairs)))
+__device__ __forceinline__ void ids_range(const TileGeom& g, uint64_t& start, uint32_t& bytes) {
+    start = g.a0 & ~7ull;
+    const uint64_t end = (g.a0 + 2ull * g.npairs + 7) & ~7ull;
+    bytes = (uint32_t)(end - start) * 2;
+}
 
 // Tile t over all segments of the level.
 __device__ __forceinline__ TileGeom tile_geom_all(const LevelParams& p, uint64_t t, uint32_t& i) {
@@ -478,8 +487,20 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
     for (uint32_t b = threadIdx.x; b <= NBC; b += kPNT) Q.cnt[b] = 0;
     TileStream TS;
     TS.init((uint8_t*)Q.tiles, Q.bars);
+    // the ids ride on the keys' mbarrier: extra transaction bytes, no extra arrival
+    // (added before the keys' arrive.expect_tx so the phase cannot complete early)
+    auto issue_ids = [&](const TileGeom& g, int b) {
+        if (threadIdx.x == 0 && g.npairs) {
+            uint64_t st0;
+            uint32_t bytes;
+            ids_range(g, st0, bytes);
+            mbar_add_tx(TS.bar + b, bytes);
+            tma_load_1d(Q.sids[b], p.ids + st0, bytes, TS.bar + b);
+        }
+    };
     uint32_t inext = ~0u;
     TileGeom gnext = tile_geom_all(p, t0, inext);
+    issue_ids(gnext, 0);
     TS.issue(p.src, gnext, 0);
     int64_t cur = -1;
     uint64_t boff = 0;
@@ -490,6 +511,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
         const TileGeom g = gnext;
         if (tile + 1 < t1) {
             gnext = tile_geom_all(p, tile + 1, inext);
+            issue_ids(gnext, tb ^ 1);
             TS.issue(p.src, gnext, tb ^ 1);
         }
         if ((int64_t)i != cur) {
@@ -498,19 +520,21 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
             nbo = MAPPED ? nmapped : sd.nb_max;
             cur = i;
         }
-        // ids of this thread's pairs (global, coalesced) while the tile lands
+        TS.wait(g, tb);  // keys and ids of this tile have landed
         const bool al = !(g.a0 & 1);
         uint32_t idp[kPPairs];
+        {
+            const uint16_t* sid = Q.sids[tb] + (g.a0 & 7);
 #pragma unroll
-        for (int j = 0; j < kPPairs; ++j) {
-            const uint32_t qq = threadIdx.x + j * kPNT;
-            idp[j] = 0xffffffffu;
-            if (qq < g.npairs) {
-                const uint16_t* d = p.ids + g.a0 + 2 * qq;
-                idp[j] = al ? *(const uint32_t*)d : ((uint32_t)d[0] | ((uint32_t)d[1] << 16));
+            for (int j = 0; j < kPPairs; ++j) {
+                const uint32_t qq = threadIdx.x + j * kPNT;
+                idp[j] = 0xffffffffu;
+                if (qq < g.npairs) {
+                    const uint16_t* d = sid + 2 * qq;
+                    idp[j] = al ? *(const uint32_t*)d : ((uint32_t)d[0] | ((uint32_t)d[1] << 16));
+                }
             }
         }
-        TS.wait(g, tb);
         const ulonglong2* sp = TS.buf(tb);
         uint64_t* skeys = (uint64_t*)TS.buf(tb);  // staging reuses the consumed tile buffer
         ulonglong2 v[kPPairs];
