@@ -448,7 +448,7 @@ struct Engine {
         const int g = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
         launch_kind_plan(q, st);
         launch_hist(q, 0, 2u, 0, g, st);
-        launch_scan_children(q, st);
+        launch_scan_children(q, nb, st);
         launch_scatter(q, 0, nb, g, st);
         launch_base_cases(q, N->scratch.as<uint64_t>(), N->sample.p, 0, st);
         launch_fill(q, N->sample.p, 0, nsm, st);
@@ -662,7 +662,7 @@ struct Engine {
             if (np) {
                 launch_kind_plan(p, st);
                 launch_hist(p, src_f64, kinds, max_rmi_b, grid_h, st);
-                launch_scan_children(p, st);
+                launch_scan_children(p, max_nb, st);
             }
             mark(2);
             // The next level is planned from the child list, which is final once

@@ -140,7 +140,7 @@ void launch_block_sort(uint64_t* keys, uint64_t n, cudaStream_t st);
 // partition.cu
 void launch_kind_plan(const LevelParams& p, cudaStream_t st);
 void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_rmi_b, int grid, cudaStream_t st);
-void launch_scan_children(const LevelParams& p, cudaStream_t st);
+void launch_scan_children(const LevelParams& p, uint32_t max_nb, cudaStream_t st);
 // scatter of every segment of the level (all kinds), bucket ids from k_hist in p.ids
 void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid, cudaStream_t st);
 void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,

@@ -373,27 +373,35 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_hist(LevelParams p) {
 }
 
 // ---------------------------------------------------------- scan children
-constexpr int kScanNT = 512;
-__global__ void __launch_bounds__(kScanNT) k_scan_children(LevelParams p) {
+// One CTA per segment: exclusive scan of the bucket counts -> write cursors;
+// children become fill / base-case / recursion work items. The list appends
+// are aggregated per CTA (one global atomic per list per round instead of one
+// per child: ~32K children hammered the same counters at level 1).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_scan_children(LevelParams p) {
     griddep_wait();
-    __shared__ uint64_t wsum[kScanNT / 32 + 1];
-    __shared__ uint8_t iseq[kMaxNB];
-    __shared__ uint64_t eqval[kMaxNB];
-    extern __shared__ uint64_t cnt[];
+    __shared__ uint64_t wsum[NT / 32 + 1];
+    __shared__ uint32_t lcount[5];             // fill, base0, base1, base2, rec
+    __shared__ unsigned long long lkeys[3];    // keys: fill, base, rec
+    __shared__ uint32_t gbase[5];
+    extern __shared__ uint64_t dyn[];           // cnt[nb], eqval[nb], iseq[nb] (u8)
     if (p.ctrl->nan_index != ~0ull) return;
     if (p.gate && *p.gate == 0) return;
     const SegDesc sd = p.segs[blockIdx.x];
     const uint8_t* mg = p.models + sd.model_off;
     const ModelHdr h = *(const ModelHdr*)mg;
     const uint32_t nb = h.nbuckets;
-    for (uint32_t b = threadIdx.x; b < nb; b += kScanNT) {
+    uint64_t* cnt = dyn;
+    uint64_t* eqval = dyn + sd.nb_max;
+    uint8_t* iseq = (uint8_t*)(dyn + 2 * (size_t)sd.nb_max);
+    for (uint32_t b = threadIdx.x; b < nb; b += NT) {
         cnt[b] = p.buckets[sd.bucket_off + b];
         iseq[b] = 0;
     }
     __syncthreads();
     if (h.kind == kTree) {
         MView m = model_view(mg);
-        for (uint32_t i = threadIdx.x; i < h.nsplit; i += kScanNT) {
+        for (uint32_t i = threadIdx.x; i < h.nsplit; i += NT) {
             if (m.eqo[i + 1] - m.eqo[i] > 1) {
                 iseq[m.eqo[i] + 1] = 1;
                 eqval[m.eqo[i] + 1] = m.spl[i];
@@ -404,37 +412,82 @@ __global__ void __launch_bounds__(kScanNT) k_scan_children(LevelParams p) {
         eqval[0] = h.radix_min;
     }
     __syncthreads();
-    block_exclusive_scan_u64<kScanNT>(cnt, nb, wsum);
-    for (uint32_t b = threadIdx.x; b < nb; b += kScanNT) {
-        uint64_t start = cnt[b];
-        uint64_t end = (b + 1 < nb) ? cnt[b + 1] : sd.n;
-        uint64_t len = end - start;
-        uint64_t begin = sd.begin + start;
-        p.buckets[sd.bucket_off + b] = begin;  // write cursor
-        if (len == 0) continue;
-        if (iseq[b]) {
-            unsigned e = atomicAdd(&p.ctrl->n_fill, 1u);
-            if (e < p.list_cap) p.fill[e] = FillItem{begin, len, eqval[b], 0};
-            else atomicOr(&p.ctrl->err, 1u);
-            atomicAdd(&p.ctrl->keys_fill, (unsigned long long)len);
-        } else if (len <= p.base_cap[2]) {
-            int c = len <= p.base_cap[0] ? 0 : (len <= p.base_cap[1] ? 1 : 2);
-            unsigned e = atomicAdd(&p.ctrl->n_base[c], 1u);
-            if (e < p.list_cap) p.base[c][e] = BaseItem{begin, len};
-            else atomicOr(&p.ctrl->err, 2u);
-            atomicAdd(&p.ctrl->keys_base, (unsigned long long)len);
-        } else {
-            unsigned e = atomicAdd(&p.ctrl->n_rec, 1u);
-            uint32_t depth = sd.depth + 1;
-            uint32_t flags = (len == sd.n || depth > p.depth_cap) ? kSegForceRadix : 0u;
-            uint64_t ps = 0;
-            if (p.slices) {
-                const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
-                if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
+    block_exclusive_scan_u64<NT>(cnt, nb, wsum);
+    for (uint32_t b0 = 0; b0 < nb; b0 += NT) {  // CTA-uniform rounds
+        const uint32_t b = b0 + threadIdx.x;
+        int cls = -1;  // 0 fill, 1..3 base class, 4 rec
+        uint64_t begin = 0, len = 0;
+        if (threadIdx.x < 5) lcount[threadIdx.x] = 0;
+        if (threadIdx.x < 3) lkeys[threadIdx.x] = 0;
+        __syncthreads();
+        if (b < nb) {
+            const uint64_t start = cnt[b];
+            const uint64_t end = (b + 1 < nb) ? cnt[b + 1] : sd.n;
+            len = end - start;
+            begin = sd.begin + start;
+            p.buckets[sd.bucket_off + b] = begin;  // write cursor
+            if (len) {
+                if (iseq[b]) cls = 0;
+                else if (len <= p.base_cap[2]) cls = 1 + (len <= p.base_cap[0] ? 0 : (len <= p.base_cap[1] ? 1 : 2));
+                else cls = 4;
             }
-            if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, flags, ps};
-            else atomicOr(&p.ctrl->err, 4u);
-            atomicAdd(&p.ctrl->keys_rec, (unsigned long long)len);
+        }
+        // warp-aggregated: one shared atomic per class and per key counter per warp
+        // (a thousand lanes on one shared address serialise)
+        uint32_t li = 0;
+        const int lane = threadIdx.x & 31;
+        const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            const unsigned m = __ballot_sync(FULL_MASK, cls == c);
+            if (m) {
+                const int leader = __ffs(m) - 1;
+                uint32_t base = 0;
+                if (lane == leader) base = atomicAdd(&lcount[c], (uint32_t)__popc(m));
+                base = __shfl_sync(FULL_MASK, base, leader);
+                if (cls == c) li = base + __popc(m & lt);
+            }
+        }
+#pragma unroll
+        for (int gk = 0; gk < 3; ++gk) {
+            const int grp = cls < 0 ? -1 : (cls == 0 ? 0 : (cls == 4 ? 2 : 1));
+            unsigned long long v = grp == gk ? (unsigned long long)len : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+            if (lane == 0 && v) atomicAdd(&lkeys[gk], v);
+        }
+        __syncthreads();
+        if (threadIdx.x < 5) {
+            const uint32_t c = lcount[threadIdx.x];
+            unsigned int* ctr = threadIdx.x == 0 ? &p.ctrl->n_fill
+                                : (threadIdx.x == 4 ? &p.ctrl->n_rec : &p.ctrl->n_base[threadIdx.x - 1]);
+            gbase[threadIdx.x] = c ? atomicAdd(ctr, c) : 0u;
+        }
+        if (threadIdx.x < 3 && lkeys[threadIdx.x]) {
+            unsigned long long* kc = threadIdx.x == 0 ? &p.ctrl->keys_fill
+                                     : (threadIdx.x == 1 ? &p.ctrl->keys_base : &p.ctrl->keys_rec);
+            atomicAdd(kc, lkeys[threadIdx.x]);
+        }
+        __syncthreads();
+        if (cls >= 0) {
+            const unsigned e = gbase[cls] + li;
+            if (cls == 0) {
+                if (e < p.list_cap) p.fill[e] = FillItem{begin, len, eqval[b], 0};
+                else atomicOr(&p.ctrl->err, 1u);
+            } else if (cls < 4) {
+                if (e < p.list_cap) p.base[cls - 1][e] = BaseItem{begin, len};
+                else atomicOr(&p.ctrl->err, 2u);
+            } else {
+                const uint32_t depth = sd.depth + 1;
+                const uint32_t flags = (len == sd.n || depth > p.depth_cap) ? kSegForceRadix : 0u;
+                uint64_t ps = 0;
+                if (p.slices) {
+                    const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
+                    if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
+                }
+                if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, flags, ps};
+                else atomicOr(&p.ctrl->err, 4u);
+            }
         }
     }
 }
@@ -634,7 +687,9 @@ void partition_init(int optin) {
     allow_smem(k_scatter<false, false, kMaxNB>, optin);
     allow_smem(k_scatter<true, true, 1024>, optin);
     allow_smem(k_scatter<false, true, 1024>, optin);
-    allow_smem(k_scan_children, optin);
+    allow_smem(k_scan_children<128>, optin);
+    allow_smem(k_scan_children<512>, optin);
+    allow_smem(k_scan_children<1024>, optin);
 }
 
 void launch_kind_plan(const LevelParams& p, cudaStream_t st) {
@@ -660,9 +715,12 @@ void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_
     }
 }
 
-void launch_scan_children(const LevelParams& p, cudaStream_t st) {
+void launch_scan_children(const LevelParams& p, uint32_t max_nb, cudaStream_t st) {
     if (!p.nsegs) return;
-    pdl(k_scan_children, p.nsegs, kScanNT, 8 * kMaxNB, st, p);
+    const size_t sm = 17 * (size_t)max_nb + 16;  // cnt + eqval (u64) + iseq (u8) per bucket slot
+    if (max_nb <= 256) pdl(k_scan_children<128>, p.nsegs, 128, sm, st, p);
+    else if (max_nb <= 512) pdl(k_scan_children<512>, p.nsegs, 512, sm, st, p);
+    else pdl(k_scan_children<1024>, p.nsegs, 1024, sm, st, p);
 }
 
 void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid, cudaStream_t st) {
