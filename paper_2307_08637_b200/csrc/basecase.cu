@@ -64,6 +64,30 @@ __global__ void __launch_bounds__(NT) k_base_smem(const BaseItem* items, const u
 // array): shared memory holds only the output array + digit histogram, so
 // three CTAs share an SM and hide each other's load latency. The segment's
 // own input range doubles as scratch for the rare large-digit passes.
+template <int IT, class SS, bool OUT_F64>
+__device__ __forceinline__ void base_reg_one(uint64_t* g, uint32_t n, typename SS::SmemR& S, void* out,
+                                             uint64_t begin) {
+    constexpr int NT = SS::kThreads;
+    uint64_t k[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const uint32_t j = threadIdx.x + i * NT;
+        k[i] = j < n ? __ldcs((const unsigned long long*)g + j) : 0ull;
+    }
+    SS::sort_regs(k, n, S, g);
+    for (uint32_t i = threadIdx.x; i < n; i += NT) {
+        const uint64_t v = S.B[i];
+        if (OUT_F64) __stcs((double*)out + begin + i, decode(v));
+        else __stcs((unsigned long long*)out + begin + i, (unsigned long long)v);
+    }
+}
+
+// Keys read straight into registers (coalesced 8-byte loads, no staging
+// array): shared memory holds only the output array + digit histogram, so
+// three CTAs share an SM and hide each other's load latency. The segment's
+// own input range doubles as scratch for the rare large-digit passes.
+// Segments of at most CAP / 2 keys take a half-width register array so no
+// thread issues work for slots past n.
 template <int NT, int CAP, int NBMAX, int MINB, bool OUT_F64>
 __global__ void __launch_bounds__(NT, MINB) k_base_reg(const BaseItem* items, const unsigned int* count, uint64_t* src,
                                                    void* out, Ctrl* ctrl, uint32_t list_cap) {
@@ -77,18 +101,8 @@ __global__ void __launch_bounds__(NT, MINB) k_base_reg(const BaseItem* items, co
         const BaseItem it = items[e];
         const uint32_t n = (uint32_t)it.n;
         uint64_t* g = src + it.begin;
-        uint64_t k[SS::ITEMS];
-#pragma unroll
-        for (int i = 0; i < SS::ITEMS; ++i) {
-            const uint32_t j = threadIdx.x + i * NT;
-            k[i] = j < n ? __ldcs((const unsigned long long*)g + j) : 0ull;
-        }
-        SS::sort_regs(k, n, S, g);
-        for (uint32_t i = threadIdx.x; i < n; i += NT) {
-            const uint64_t v = S.B[i];
-            if (OUT_F64) __stcs((double*)out + it.begin + i, decode(v));
-            else __stcs((unsigned long long*)out + it.begin + i, (unsigned long long)v);
-        }
+        if (n <= (uint32_t)CAP / 2) base_reg_one<SS::ITEMS / 2, SS, OUT_F64>(g, n, S, out, it.begin);
+        else base_reg_one<SS::ITEMS, SS, OUT_F64>(g, n, S, out, it.begin);
         __syncthreads();
     }
 }

@@ -219,6 +219,7 @@ struct SmemSort {
     // remaining digits are drained with S.A as scratch. Result in S.B.
     // (a may alias S.A: it is not read after the first pass.)
     static constexpr int ITEMS = CAP / NT;
+    static constexpr int kThreads = NT;
     __device__ static void sort_fast(const uint64_t* a, uint32_t n, Smem& S) {
         static_assert(ITEMS * NT == CAP, "CAP must be a multiple of NT");
         uint64_t k[ITEMS];
@@ -230,30 +231,94 @@ struct SmemSort {
         sort_regs(k, n, S, S.A);
     }
     // keys j = threadIdx.x + i * NT in k[i]; result in S.B; scratch: >= n keys
-    template <class SM>
-    __device__ static void sort_regs(uint64_t (&k)[ITEMS], uint32_t n, SM& S, uint64_t* scratch) {
+    template <int IT = ITEMS, class SM>
+    __device__ static void sort_regs(uint64_t (&k)[IT], uint32_t n, SM& S, uint64_t* scratch) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-        uint64_t mn = ~0ull, mx = 0;
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const uint32_t j = tid + i * NT;
-            if (j < n) {
-                mn = k[i] < mn ? k[i] : mn;
-                mx = k[i] > mx ? k[i] : mx;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const uint64_t a1 = __shfl_xor_sync(FULL_MASK, mn, o), b1 = __shfl_xor_sync(FULL_MASK, mx, o);
-            mn = a1 < mn ? a1 : mn;
-            mx = b1 > mx ? b1 : mx;
-        }
-        if (lane == 0) { S.red[2 * warp] = mn; S.red[2 * warp + 1] = mx; }
-        if (tid == 0) { S.n_med = 0; S.n_large = 0; S.n_l4 = 0; S.n_l16 = 0; }
+        constexpr int NW = NT / 32;
         constexpr uint32_t kNb = CAP < NBMAX ? CAP : NBMAX;  // digits: >= 1 per key for n near CAP
-        __syncthreads();
-        {  // every warp combines the per-warp partials with shuffles
-            constexpr int NW = NT / 32;
+        // nb = smallest power of two >= n (capped): <= 1 key per digit on average
+        const uint32_t lgnb = min(32u - __clz(max(n, 2u) - 1u), 31u - __clz(kNb));
+        const uint32_t nb = 1u << lgnb;
+        // digit = (key - base) >> shift, monotone and < nb. base / shift come
+        // from 32-bit reductions: the range of the high words, and when every
+        // key shares one high word, the range of the low words; only a high
+        // range of 1..7 words (keys straddling a 2^32 boundary) needs the
+        // exact 64-bit min / max.
+        uint32_t* redh = (uint32_t*)S.red;  // 2 * NW words (S.red holds 2 * NW u64)
+        auto reduce32 = [&](uint32_t lo, uint32_t hi, uint32_t& mn, uint32_t& mx) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo = min(lo, __shfl_xor_sync(FULL_MASK, lo, o));
+                hi = max(hi, __shfl_xor_sync(FULL_MASK, hi, o));
+            }
+            if (lane == 0) { redh[2 * warp] = lo; redh[2 * warp + 1] = hi; }
+            __syncthreads();
+            uint32_t a1 = lane < NW ? redh[2 * lane] : ~0u, b1 = lane < NW ? redh[2 * lane + 1] : 0u;
+#pragma unroll
+            for (int o = NW / 2; o > 0; o >>= 1) {
+                a1 = min(a1, __shfl_xor_sync(FULL_MASK, a1, o));
+                b1 = max(b1, __shfl_xor_sync(FULL_MASK, b1, o));
+            }
+            mn = __shfl_sync(FULL_MASK, a1, 0);
+            mx = __shfl_sync(FULL_MASK, b1, 0);
+            __syncthreads();  // redh free again
+        };
+        uint32_t mnh, mxh;
+        {
+            uint32_t lo = ~0u, hi = 0;
+#pragma unroll
+            for (int i = 0; i < IT; ++i) {
+                const uint32_t j = tid + i * NT;
+                const uint32_t h = (uint32_t)(k[i] >> 32);
+                if (j < n) { lo = min(lo, h); hi = max(hi, h); }
+            }
+            reduce32(lo, hi, mnh, mxh);
+        }
+        const uint32_t dh = mxh - mnh;
+        uint64_t base = (uint64_t)mnh << 32;
+        uint32_t shift;
+        if (dh >= 8) {
+            // window [mnh << 32, (mxh + 1) << 32) of 2^(32 + bits) keys; the
+            // true span is at least (dh - 1) << 32, >= 7/16 of it
+            shift = 32u + (32u - __clz(dh)) - lgnb;
+        } else if (dh == 0) {
+            uint32_t lo = ~0u, hi = 0, mnl, mxl;
+#pragma unroll
+            for (int i = 0; i < IT; ++i) {
+                const uint32_t j = tid + i * NT;
+                if (j < n) { lo = min(lo, (uint32_t)k[i]); hi = max(hi, (uint32_t)k[i]); }
+            }
+            reduce32(lo, hi, mnl, mxl);
+            if (mnl == mxl) {  // homogeneous: already sorted
+#pragma unroll
+                for (int i = 0; i < IT; ++i) {
+                    const uint32_t j = tid + i * NT;
+                    if (j < n) S.B[j] = k[i];
+                }
+                __syncthreads();
+                return;
+            }
+            const uint32_t bits = 32u - __clz(mxl - mnl);
+            base |= mnl;
+            shift = bits > lgnb ? bits - lgnb : 0;
+        } else {  // keys straddle 1..7 high-word boundaries: exact 64-bit range
+            uint64_t mn = ~0ull, mx = 0;
+#pragma unroll
+            for (int i = 0; i < IT; ++i) {
+                const uint32_t j = tid + i * NT;
+                if (j < n) {
+                    mn = k[i] < mn ? k[i] : mn;
+                    mx = k[i] > mx ? k[i] : mx;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t a1 = __shfl_xor_sync(FULL_MASK, mn, o), b1 = __shfl_xor_sync(FULL_MASK, mx, o);
+                mn = a1 < mn ? a1 : mn;
+                mx = b1 > mx ? b1 : mx;
+            }
+            if (lane == 0) { S.red[2 * warp] = mn; S.red[2 * warp + 1] = mx; }
+            __syncthreads();
             uint64_t a1 = lane < NW ? S.red[2 * lane] : ~0ull, b1 = lane < NW ? S.red[2 * lane + 1] : 0ull;
 #pragma unroll
             for (int o = NW / 2; o > 0; o >>= 1) {
@@ -263,33 +328,24 @@ struct SmemSort {
             }
             mn = __shfl_sync(FULL_MASK, a1, 0);
             mx = __shfl_sync(FULL_MASK, b1, 0);
+            __syncthreads();  // S.red is reused by the scan
+            const uint32_t bits = bitlen64(mx - mn);  // mx > mn: the high words differ
+            base = mn;
+            shift = bits > lgnb ? bits - lgnb : 0;
         }
-        uint64_t* B = S.B;
-        if (mn == mx) {  // homogeneous: already sorted
+        uint32_t dg[IT];
 #pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                const uint32_t j = tid + i * NT;
-                if (j < n) B[j] = k[i];
-            }
-            __syncthreads();
-            return;
+        for (int i = 0; i < IT; ++i) {
+            dg[i] = (uint32_t)((k[i] - base) >> shift);
         }
-        // nb = smallest power of two >= n (capped): <= 1 key per digit on average
-        const uint32_t lgnb = min(32u - __clz(max(n, 2u) - 1u), 31u - __clz(kNb));
-        const uint32_t nb = 1u << lgnb;
-        const uint32_t bits = bitlen64(mx - mn);
-        const uint32_t shift = bits > lgnb ? bits - lgnb : 0;
-        uint32_t dg[ITEMS];
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) dg[i] = (uint32_t)((k[i] - mn) >> shift);
         sort_digits(k, dg, n, nb, S, scratch);
     }
 
     // Counting pass on caller-supplied digits (dg[i] < nb <= NBMAX, monotone in
     // the key), placement into S.B, collision fix-up, drain of large digits.
     // Result in S.B. The caller has zeroed nothing; S.n_* are reset here.
-    template <class SM>
-    __device__ static void sort_digits(uint64_t (&k)[ITEMS], const uint32_t (&dg)[ITEMS], uint32_t n, uint32_t nb,
+    template <int IT = ITEMS, class SM>
+    __device__ static void sort_digits(uint64_t (&k)[IT], const uint32_t (&dg)[IT], uint32_t n, uint32_t nb,
                                        SM& S, uint64_t* scratch) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         uint64_t* B = S.B;
@@ -297,9 +353,9 @@ struct SmemSort {
         if (tid == 0) { S.n_med = 0; S.n_large = 0; S.n_l4 = 0; S.n_l16 = 0; }
         for (uint32_t d = tid; d < nb; d += NT) S.hist[d] = 0;
         __syncthreads();
-        uint32_t dp[ITEMS];  // digit << 16 | rank within the digit
+        uint32_t dp[IT];  // digit << 16 | rank within the digit
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
+        for (int i = 0; i < IT; ++i) {
             const uint32_t j = tid + i * NT;
             dp[i] = j < n ? (dg[i] << 16 | atomicAdd(&S.hist[dg[i]], 1u)) : 0u;
         }
@@ -380,7 +436,7 @@ struct SmemSort {
         }
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
+        for (int i = 0; i < IT; ++i) {
             const uint32_t j = tid + i * NT;
             if (j < n) {
                 B[S.hist[dp[i] >> 16] + (dp[i] & 0xffffu)] = k[i];
