@@ -500,7 +500,7 @@ struct ScatterSmem {
     uint64_t bars[2];
     ulonglong2 tiles[2][kTileKeys / 2];  // TMA tile buffers; the consumed one stages the tile
     long long delta[NBC];                // per bucket: claimed global position - tile-local start
-    uint32_t cnt[NBC + 1];
+    alignas(16) uint32_t cnt[NBC + 1];
     uint16_t sbid[kTileKeys];
     uint32_t wsum[kPNT / 32 + 1];
     alignas(16) uint16_t sids[2][kTileKeys + 16];  // the tile's bucket ids, bulk-copied with its keys
@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
     const uint64_t t0 = (uint64_t)blockIdx.x * per;
     const uint64_t t1 = min(t0 + per, p.ntiles);
     if (t0 >= t1) return;
-    for (uint32_t b = threadIdx.x; b <= NBC; b += kPNT) Q.cnt[b] = 0;
+    for (uint32_t b = threadIdx.x; b < NBC; b += kPNT) Q.cnt[b] = 0;
     TileStream TS;
     TS.init((uint8_t*)Q.tiles, Q.bars);
     // the ids ride on the keys' mbarrier: extra transaction bytes, no extra arrival
@@ -623,15 +623,51 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
                 skey = load_key(p.src, ix, IN_F64);
             }
         }
-        __syncthreads();
-        const uint32_t total = block_exclusive_scan_u32<kPNT>(Q.cnt, nbo, Q.wsum);
-        if (threadIdx.x == 0) Q.cnt[nbo] = total;
-        __syncthreads();
-        {  // claim one output range per non-empty bucket: all atomics in flight
-            constexpr int kCl = (NBC + kPNT - 1) / kPNT;
-            unsigned long long got[kCl];
+        __syncthreads();  // (1) tile counts complete
+        // Fused tile scan + claims at a fixed geometry: thread t owns buckets
+        // [t*kPer, t*kPer + kPer) (vector load), one warp scan, warp offsets by
+        // REDUX (no single-warp phase), claim atomics issued before the staging
+        // and consumed after it (their latency hides behind the staging stores).
+        constexpr int kPer = NBC / kPNT;
+        static_assert(kPer * kPNT == NBC && (kPer == 2 || kPer == 4), "scatter geometry");
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint32_t bb = threadIdx.x * kPer;
+        uint32_t cn[kPer];
+        if constexpr (kPer == 2) {
+            const uint2 t2 = *(const uint2*)&Q.cnt[bb];
+            cn[0] = t2.x; cn[1] = t2.y;
+        } else {
+            const uint4 t4 = *(const uint4*)&Q.cnt[bb];
+            cn[0] = t4.x; cn[1] = t4.y; cn[2] = t4.z; cn[3] = t4.w;
+        }
+        uint32_t sum = 0;
 #pragma unroll
-            for (int q = 0; q < kCl; ++q) {
+        for (int k = 0; k < kPer; ++k) sum += cn[k];
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t w = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o) incl += w;
+        }
+        if (lane == 31) Q.wsum[warp] = incl;
+        __syncthreads();  // (2)
+        const uint32_t wv = lane < kPNT / 32 ? Q.wsum[lane] : 0u;
+        const uint32_t total = __reduce_add_sync(FULL_MASK, wv);
+        uint32_t run = __reduce_add_sync(FULL_MASK, lane < warp ? wv : 0u) + incl - sum;
+        uint32_t st[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            st[k] = run;
+            run += cn[k];
+        }
+        if constexpr (kPer == 2) *(uint2*)&Q.cnt[bb] = make_uint2(st[0], st[1]);
+        else *(uint4*)&Q.cnt[bb] = make_uint4(st[0], st[1], st[2], st[3]);
+        if (threadIdx.x == 0) Q.cnt[NBC] = total;
+        __syncthreads();  // (3) tile-local bucket starts visible
+        {  // claims strided over the threads (bucket t, t + kPNT, ...): all atomics in flight
+            unsigned long long got[kPer];
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
                 const uint32_t b = threadIdx.x + q * kPNT;
                 got[q] = 0;
                 if (b < nbo) {
@@ -640,9 +676,9 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
                 }
             }
 #pragma unroll
-            for (int q = 0; q < kCl; ++q) {
+            for (int q = 0; q < kPer; ++q) {
                 const uint32_t b = threadIdx.x + q * kPNT;
-                if (b < nbo) Q.delta[b] = (long long)got[q] - (long long)Q.cnt[b];
+                Q.delta[b] = (long long)got[q] - (long long)Q.cnt[b];
             }
         }
 #pragma unroll
@@ -659,13 +695,14 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
             skeys[pos] = skey;
             Q.sbid[pos] = (uint16_t)(scode >> 16);
         }
-        __syncthreads();
+        __syncthreads();  // (4)
 #pragma unroll
         for (int q = 0; q < kTileKeys / kPNT; ++q) {  // unrolled: loads of all rows in flight
             const uint32_t j = threadIdx.x + q * kPNT;
             if (j < total) p.dst[(long long)j + Q.delta[Q.sbid[j]]] = skeys[j];
         }
-        for (uint32_t b = threadIdx.x; b <= nbo; b += kPNT) Q.cnt[b] = 0;
+        if constexpr (kPer == 2) *(uint2*)&Q.cnt[bb] = make_uint2(0, 0);
+        else *(uint4*)&Q.cnt[bb] = make_uint4(0, 0, 0, 0);
         fence_proxy_async_smem();  // staging writes (generic proxy) before the next bulk copy into this buffer
         __syncthreads();
     }
