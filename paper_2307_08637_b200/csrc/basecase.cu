@@ -240,6 +240,27 @@ void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int
     }
 }
 
+// One size class (0: <= 1 Ki keys, 1: <= 4 Ki, 2: <= 16 Ki) on its own stream:
+// the classes are independent, so they run side by side instead of each
+// waiting for the previous class's tail.
+void launch_base_class(const LevelParams& p, int cls, const uint64_t* src, void* out, int out_f64, cudaStream_t st) {
+    const int nsm = num_sms();
+    unsigned int* cnt = &p.ctrl->n_base[cls];
+    if (cls == 0) {
+        const size_t sm = sizeof(SmallSS::Smem);
+        if (out_f64) pdl(k_base_smem<128, 1024, 1024, true>, nsm * 8, 128, sm, st, p.base[0], cnt, src, out, p.ctrl, p.list_cap);
+        else pdl(k_base_smem<128, 1024, 1024, false>, nsm * 8, 128, sm, st, p.base[0], cnt, src, out, p.ctrl, p.list_cap);
+    } else if (cls == 1) {
+        const size_t sm = sizeof(MidSS::SmemR);
+        if (out_f64) pdl(k_base_reg<256, 4096, 4096, 3, true>, nsm * 3, 256, sm, st, p.base[1], cnt, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        else pdl(k_base_reg<256, 4096, 4096, 3, false>, nsm * 3, 256, sm, st, p.base[1], cnt, (uint64_t*)src, out, p.ctrl, p.list_cap);
+    } else {
+        const size_t sm = sizeof(SmemSort<1024, 16384, 8192>::SmemR);
+        if (out_f64) pdl(k_base_reg<1024, 16384, 8192, 1, true>, nsm, 1024, sm, st, p.base[2], cnt, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        else pdl(k_base_reg<1024, 16384, 8192, 1, false>, nsm, 1024, sm, st, p.base[2], cnt, (uint64_t*)src, out, p.ctrl, p.list_cap);
+    }
+}
+
 void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st) {
     const dim3 g((unsigned)grid, kFillSplit);
     if (out_f64) pdl(k_fill<true>, g, 256, 0, st, p.fill, &p.ctrl->n_fill, out, p.ctrl, p.list_cap);

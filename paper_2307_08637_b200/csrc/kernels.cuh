@@ -147,6 +147,7 @@ void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map
                            cudaStream_t st);
 // basecase.cu
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
+void launch_base_class(const LevelParams& p, int cls, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
 void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st);
 void launch_small_sort(void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st);
 // cluster.cu
