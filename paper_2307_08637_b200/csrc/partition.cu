@@ -151,9 +151,12 @@ __device__ __forceinline__ uint32_t kclassify(const KState& S, uint64_t x) {
         const double2 li = S.line[m];
         const uint32_t gb = S.gbounds[m];
         const double v = __dadd_rn(__dmul_rn(li.x, xn), li.y);
-        const double t = S.identity ? __dmul_rn(v, (double)S.nb)
-                                    : __dmul_rn(__dmul_rn(__dsub_rn(v, S.cdf_lo), S.inv_span), (double)S.nb);
-        return min(max(min(__double2uint_rz(t), S.nb - 1), gb & 0xffffu), gb >> 16);
+        // one formula for every model: with the identity range (cdf_lo 0, inv_span 1)
+        // the subtraction and the first product are exact, so t == v * nb bit for bit
+        // (no per-key select between two paths)
+        const double t = __dmul_rn(__dmul_rn(__dsub_rn(v, S.cdf_lo), S.inv_span), (double)S.nb);
+        // g(hi) <= nb - 1, so the clamp to nb - 1 is implied by the last min
+        return min(max(__double2uint_rz(t), gb & 0xffffu), gb >> 16);
     } else if constexpr (KIND == kTree) {
         return tree_bucket(S.levels, S.leaf, S.nsplit, S.tree, S.spl, S.eqo, x);
     } else {
@@ -320,15 +323,26 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_hist(LevelParams p) {
             v[j] = q < g.npairs ? sp[q] : make_ulonglong2(0, 0);
         }
         if (IN_F64) {
+            // NaN (keys.hpp:34-42): one predicate OR per key, the exact index only
+            // in the (never taken on clean input) slow path
+            bool anynan = false;
+#pragma unroll
+            for (int j = 0; j < kPPairs; ++j)
+                anynan |= isnan(__longlong_as_double((long long)v[j].x)) | isnan(__longlong_as_double((long long)v[j].y));
+            if (anynan) {
+#pragma unroll
+                for (int j = 0; j < kPPairs; ++j) {
+                    uint32_t q = threadIdx.x + j * kPNT;
+                    if (q < g.npairs) {
+                        if (isnan(__longlong_as_double((long long)v[j].x)))
+                            atomicMin(&p.ctrl->nan_index, (unsigned long long)(g.a0 + 2 * q));
+                        if (isnan(__longlong_as_double((long long)v[j].y)))
+                            atomicMin(&p.ctrl->nan_index, (unsigned long long)(g.a0 + 2 * q + 1));
+                    }
+                }
+            }
 #pragma unroll
             for (int j = 0; j < kPPairs; ++j) {
-                uint32_t q = threadIdx.x + j * kPNT;
-                if (q < g.npairs) {
-                    if (isnan(__longlong_as_double((long long)v[j].x)))
-                        atomicMin(&p.ctrl->nan_index, (unsigned long long)(g.a0 + 2 * q));
-                    if (isnan(__longlong_as_double((long long)v[j].y)))
-                        atomicMin(&p.ctrl->nan_index, (unsigned long long)(g.a0 + 2 * q + 1));
-                }
                 v[j].x = encode(__longlong_as_double((long long)v[j].x));
                 v[j].y = encode(__longlong_as_double((long long)v[j].y));
             }
