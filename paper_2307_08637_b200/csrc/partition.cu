@@ -99,13 +99,53 @@ struct KState {
     const uint64_t* spl;
     const uint32_t* eqo;
     uint32_t levels, leaf, nsplit;
+    // radix-assisted tree lookup: lut[c] = #splitters below the start of cell c of
+    // the splitter range (cells of 2^lshift keys); rank search of <= lutT steps
+    const uint16_t* lut;
+    uint64_t lbase;
+    uint32_t lshift, lutT, llog;
     // radix / fill
     uint64_t rmin;
     uint32_t shift, fill;
 };
 
+// tree payload capacity (tree_payload_bytes(1024, 1023), 16-byte rounded)
+constexpr size_t kTreeCapBytes =
+    ((size_t)LSORT_MAX_TREE_DEV * 8 + (size_t)(LSORT_MAX_TREE_DEV - 1) * 8 + (size_t)LSORT_MAX_TREE_DEV * 4 + 15) & ~(size_t)15;
+constexpr int kLutBits = 12;
+constexpr uint32_t kLutCells = 1u << kLutBits;
+constexpr uint32_t kLutMaxT = 4;  // longer in-cell searches: descend the tree instead
+constexpr size_t kLutBytes = 2 * (kLutCells + 2);
+// Log-spaced cells (skewed splitters, e.g. Zipf ranks): offsets r < 64 get a cell
+// each, then every octave [2^e, 2^(e+1)) is split into 64 equal cells.
+constexpr uint32_t kLogSub = 6;
+__device__ __forceinline__ uint32_t log_cell(uint64_t r) {
+    if (r < (1ull << kLogSub)) return (uint32_t)r;
+    const uint32_t e = 63 - __clzll((long long)r);
+    return ((e - kLogSub + 1) << kLogSub) | (uint32_t)((r >> (e - kLogSub)) & ((1u << kLogSub) - 1));
+}
+__device__ __forceinline__ uint64_t log_cell_start(uint32_t c) {
+    if (c < (1u << kLogSub)) return c;
+    const uint32_t k = c >> kLogSub, low = c & ((1u << kLogSub) - 1);
+    return ((1ull << kLogSub) + low) << (k - 1);
+}
+constexpr uint32_t kLogCells = (64 - kLogSub + 1) << kLogSub;  // 3776 <= kLutCells
+static_assert(kLogCells <= kLutCells, "log cells fit the table");
+
+// #{i < n : a[i] < x} over a strictly increasing array
+__device__ __forceinline__ uint32_t lower_rank(const uint64_t* a, uint32_t n, uint64_t x) {
+    uint32_t b = 0;
+    while (n > 0) {
+        const uint32_t h = n >> 1;
+        if (a[b + h] < x) { b += h + 1; n -= h + 1; }
+        else n = h;
+    }
+    return b;
+}
+
 template <uint32_t KIND>
-__device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t* tree_smem) {
+__device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t* tree_smem,
+                                            uint16_t* lut_smem = nullptr, uint32_t* red = nullptr) {
     const ModelHdr* h = (const ModelHdr*)g;
     S.nb = h->nbuckets;
     if constexpr (KIND == kLearned) {
@@ -135,7 +175,42 @@ __device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t
         S.tree = (const uint64_t*)tree_smem;
         S.spl = S.tree + S.leaf;
         S.eqo = (const uint32_t*)(S.spl + S.nsplit);
+        S.lutT = ~0u;
         __syncthreads();
+        if (lut_smem && S.nsplit >= 8) {
+            // the tree's leaf is the splitters' lower rank (padding is UINT64_MAX,
+            // models.cpp:133-185): index a cell of the splitter range, then search
+            // the few splitters inside it
+            const uint64_t s0 = S.spl[0], range = S.spl[S.nsplit - 1] - s0;
+            const int bl = 64 - __clzll((long long)range);
+            S.lbase = s0;
+            S.lshift = bl > kLutBits ? (uint32_t)(bl - kLutBits) : 0u;
+            for (uint32_t mode = 0; mode < 2 && S.lutT == ~0u; ++mode) {  // linear cells, then log cells
+                const uint32_t ncell = mode ? kLogCells : kLutCells;
+                if (threadIdx.x == 0) *red = 0;
+                for (uint32_t c = threadIdx.x; c <= ncell; c += blockDim.x) {
+                    uint32_t r = S.nsplit;
+                    if (c < ncell) {
+                        const uint64_t off = mode ? log_cell_start(c) : (uint64_t)c << S.lshift;
+                        const uint64_t start = off > ~0ull - s0 ? ~0ull : s0 + off;
+                        r = lower_rank(S.spl, S.nsplit, start);
+                    }
+                    lut_smem[c] = (uint16_t)r;
+                }
+                __syncthreads();
+                uint32_t mx = 0;
+                for (uint32_t c = threadIdx.x; c < ncell; c += blockDim.x)
+                    mx = max(mx, (uint32_t)lut_smem[c + 1] - lut_smem[c]);
+                for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+                if ((threadIdx.x & 31) == 0 && mx) atomicMax(red, mx);
+                __syncthreads();
+                const uint32_t T = 32 - __clz(*red);  // steps of a lower-bound search over <= max keys
+                S.lutT = T <= kLutMaxT ? T : ~0u;
+                S.llog = mode;
+                __syncthreads();  // *red and the table are reused by the next mode
+            }
+            S.lut = lut_smem;
+        }
     } else {
         S.rmin = h->radix_min; S.shift = h->shift; S.fill = h->kind == kFill;
     }
@@ -188,13 +263,38 @@ template <uint32_t KIND>
 __device__ __forceinline__ void classify16(const KState& S, const ulonglong2 (&v)[kPPairs], uint32_t (&c)[kPItems]) {
     if constexpr (KIND == kTree) {
         uint32_t idx[kPItems];
-#pragma unroll
-        for (int q = 0; q < kPItems; ++q) idx[q] = 1;
-        for (uint32_t l = 0; l < S.levels; ++l) {
+        if (S.lutT != ~0u) {  // radix-assisted: cell lookup + a short lockstep search
+            uint32_t n[kPItems];
 #pragma unroll
             for (int q = 0; q < kPItems; ++q) {
                 const uint64_t x = (q & 1) ? v[q >> 1].y : v[q >> 1].x;
-                idx[q] = 2 * idx[q] + (x > S.tree[idx[q]] ? 1u : 0u);
+                const uint64_t rel = x < S.lbase ? 0ull : x - S.lbase;
+                const uint32_t d = S.llog ? log_cell(rel) : (uint32_t)min(rel >> S.lshift, (uint64_t)(kLutCells - 1));
+                const uint32_t b = S.lut[d];
+                idx[q] = b;
+                n[q] = S.lut[d + 1] - b;
+            }
+            for (uint32_t it = 0; it < S.lutT; ++it) {
+#pragma unroll
+                for (int q = 0; q < kPItems; ++q) {
+                    const uint64_t x = (q & 1) ? v[q >> 1].y : v[q >> 1].x;
+                    const uint32_t h = n[q] >> 1;
+                    const bool lt = n[q] > 0 && S.spl[min(idx[q] + h, S.nsplit - 1)] < x;
+                    idx[q] = lt ? idx[q] + h + 1 : idx[q];
+                    n[q] = lt ? n[q] - h - 1 : h;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kPItems; ++q) idx[q] += S.leaf;
+        } else {
+#pragma unroll
+            for (int q = 0; q < kPItems; ++q) idx[q] = 1;
+            for (uint32_t l = 0; l < S.levels; ++l) {
+#pragma unroll
+                for (int q = 0; q < kPItems; ++q) {
+                    const uint64_t x = (q & 1) ? v[q >> 1].y : v[q >> 1].x;
+                    idx[q] = 2 * idx[q] + (x > S.tree[idx[q]] ? 1u : 0u);
+                }
             }
         }
 #pragma unroll
@@ -274,7 +374,8 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_hist(LevelParams p) {
     uint64_t* bars = (uint64_t*)sm;                          // 2 mbarriers (16 B)
     uint32_t* hist = (uint32_t*)(sm + 16);                   // kMaxNB
     uint8_t* tiles = sm + 16 + 4 * kMaxNB;                   // 2 x kTileBytes
-    uint8_t* tree_smem = tiles + 2 * kTileBytes;             // tree payload
+    uint8_t* tree_smem = tiles + 2 * kTileBytes;             // tree payload (+ lookup table)
+    __shared__ uint32_t lut_red;
     if (!IN_F64 && p.ctrl->nan_index != ~0ull) return;
     KindTiles<KIND> KT;
     KT.init(p);
@@ -310,7 +411,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_hist(LevelParams p) {
             }
             const SegDesc& sd = p.segs[KT.ks[i]];
             boff = sd.bucket_off;
-            kstate_load<KIND>(S, p.models + sd.model_off, tree_smem);
+            kstate_load<KIND>(S, p.models + sd.model_off, tree_smem, (uint16_t*)(tree_smem + kTreeCapBytes), &lut_red);
             __syncthreads();
             cur = i;
         }
@@ -723,7 +824,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
 }
 
 // ------------------------------------------------------------- launchers
-static const uint32_t kTreeCap = (uint32_t)((tree_payload_bytes(LSORT_MAX_TREE_DEV, LSORT_MAX_TREE_DEV - 1) + 15) & ~15ull);
+static const uint32_t kTreeCap = (uint32_t)(kTreeCapBytes + kLutBytes);
 
 void partition_init(int optin) {
     allow_smem(k_hist<true, kLearned>, optin);

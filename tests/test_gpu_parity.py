@@ -233,6 +233,30 @@ def test_sort_heavy_hitters(ctx):
     assert st["fill_keys"] >= 0.35 * n
 
 
+@pytest.mark.parametrize("case", ["top_of_range", "dense_low_cells", "skewed_cells", "two_ends"])
+def test_sort_tree_lookup_table(ctx, case):
+    """Radix-assisted splitter lookup (partition.cu kstate_load<kTree>): cells of
+    the splitter range, saturation near 2^64, cells holding many splitters
+    (tree descent fallback) -- duplicate-heavy inputs so the trees are used."""
+    rng = np.random.default_rng(11)
+    n = 3_000_000
+    top = np.uint64(2**64 - 1)
+    if case == "top_of_range":
+        a = top - rng.integers(0, 5000, n, dtype=np.uint64)
+    elif case == "dense_low_cells":
+        a = rng.integers(0, 3000, n, dtype=np.uint64) * np.uint64(1 << 40)
+    elif case == "skewed_cells":  # many distinct splitters in the first cells, sparse above
+        a = np.where(rng.random(n) < 0.7, rng.integers(0, 600, n), rng.integers(0, 1 << 50, n)).astype(np.uint64)
+        a[rng.random(n) < 0.2] = 5
+    else:
+        a = np.where(rng.random(n) < 0.5, rng.integers(0, 2000, n),
+                     top - rng.integers(0, 2000, n, dtype=np.uint64)).astype(np.uint64)
+    d = dev(a)
+    st = ctx.sort(d)
+    assert st["level0_kind"] == 1, "expected a splitter tree at level 0"
+    assert np.array_equal(host_u64(d), np.sort(a))
+
+
 def test_sort_adversarial(ctx):
     n = 300_000
     rng = np.random.default_rng(1)
