@@ -719,13 +719,29 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
                 v[j].y = encode(__longlong_as_double((long long)v[j].y));
             }
         }
+        // Rank within the tile. A warp whose first key slot shares one bucket
+        // (sorted runs, heavy buckets) takes the warp-uniform path for the tile
+        // (one atomic per warp when a slot is uniform); spread warps use plain
+        // returning atomics (distinct addresses: no serialisation) without the
+        // per-key uniformity votes.
+        const uint32_t b00 = idp[0] & 0xffffu;
+        if (__all_sync(FULL_MASK, b00 == __shfl_sync(FULL_MASK, b00, 0))) {
 #pragma unroll
-        for (int q = 0; q < kPItems; ++q) {
-            uint32_t b = (q & 1) ? (idp[q >> 1] >> 16) : (idp[q >> 1] & 0xffffu);
-            const bool ok = b != kNoMove;
-            if (MAPPED && ok) b = map[b];
-            const uint32_t r = hist_rank_warp(Q.cnt, b, ok);
-            code[q] = ok ? (b << 16 | r) : 0xffffffffu;
+            for (int q = 0; q < kPItems; ++q) {
+                uint32_t b = (q & 1) ? (idp[q >> 1] >> 16) : (idp[q >> 1] & 0xffffu);
+                const bool ok = b != kNoMove;
+                if (MAPPED && ok) b = map[b];
+                const uint32_t r = hist_rank_warp(Q.cnt, b, ok);
+                code[q] = ok ? (b << 16 | r) : 0xffffffffu;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < kPItems; ++q) {
+                uint32_t b = (q & 1) ? (idp[q >> 1] >> 16) : (idp[q >> 1] & 0xffffu);
+                const bool ok = b != kNoMove;
+                if (MAPPED && ok) b = map[b];
+                code[q] = ok ? (b << 16 | atomicAdd(&Q.cnt[b], 1u)) : 0xffffffffu;
+            }
         }
         uint64_t skey = 0;
         uint32_t scode = 0xffffffffu;
