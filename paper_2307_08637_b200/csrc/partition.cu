@@ -615,7 +615,7 @@ struct ScatterSmem {
     uint64_t bars[2];
     ulonglong2 tiles[2][kTileKeys / 2];  // TMA tile buffers; the consumed one stages the tile
     long long delta[NBC];                // per bucket: claimed global position - tile-local start
-    alignas(16) uint32_t cnt[NBC + 1];
+    alignas(16) uint32_t cnt[2][NBC + 4];  // per tile parity: counts -> tile-local starts
     uint16_t sbid[kTileKeys];
     uint32_t wsum[kPNT / 32 + 1];
     alignas(16) uint16_t sids[2][kTileKeys + 16];  // the tile's bucket ids, bulk-copied with its keys
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
     const uint64_t t0 = (uint64_t)blockIdx.x * per;
     const uint64_t t1 = min(t0 + per, p.ntiles);
     if (t0 >= t1) return;
-    for (uint32_t b = threadIdx.x; b < NBC; b += kPNT) Q.cnt[b] = 0;
+    for (uint32_t b = threadIdx.x; b < NBC; b += kPNT) Q.cnt[0][b] = Q.cnt[1][b] = 0;
     TileStream TS;
     TS.init((uint8_t*)Q.tiles, Q.bars);
     // the ids ride on the keys' mbarrier: extra transaction bytes, no extra arrival
@@ -677,11 +677,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
         const int tb = (int)((tile - t0) & 1);
         const uint32_t i = inext;
         const TileGeom g = gnext;
-        if (tile + 1 < t1) {
-            gnext = tile_geom_all(p, tile + 1, inext);
-            issue_ids(gnext, tb ^ 1);
-            TS.issue(p.src, gnext, tb ^ 1);
-        }
+        uint32_t* cnt = Q.cnt[tb];
         if ((int64_t)i != cur) {
             const SegDesc& sd = p.segs[i];
             boff = sd.bucket_off;
@@ -731,7 +727,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
                 uint32_t b = (q & 1) ? (idp[q >> 1] >> 16) : (idp[q >> 1] & 0xffffu);
                 const bool ok = b != kNoMove;
                 if (MAPPED && ok) b = map[b];
-                const uint32_t r = hist_rank_warp(Q.cnt, b, ok);
+                const uint32_t r = hist_rank_warp(cnt, b, ok);
                 code[q] = ok ? (b << 16 | r) : 0xffffffffu;
             }
         } else {
@@ -740,7 +736,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
                 uint32_t b = (q & 1) ? (idp[q >> 1] >> 16) : (idp[q >> 1] & 0xffffu);
                 const bool ok = b != kNoMove;
                 if (MAPPED && ok) b = map[b];
-                code[q] = ok ? (b << 16 | atomicAdd(&Q.cnt[b], 1u)) : 0xffffffffu;
+                code[q] = ok ? (b << 16 | atomicAdd(&cnt[b], 1u)) : 0xffffffffu;
             }
         }
         uint64_t skey = 0;
@@ -750,11 +746,16 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
             uint32_t b = p.ids[ix];
             if (b != kNoMove) {
                 if (MAPPED) b = map[b];
-                scode = b << 16 | atomicAdd(&Q.cnt[b], 1u);
+                scode = b << 16 | atomicAdd(&cnt[b], 1u);
                 skey = load_key(p.src, ix, IN_F64);
             }
         }
-        __syncthreads();  // (1) tile counts complete
+        __syncthreads();  // (1) tile counts complete; every thread is past the previous tile
+        if (tile + 1 < t1) {  // prefetch the next tile into the buffer the previous tile staged in
+            gnext = tile_geom_all(p, tile + 1, inext);
+            issue_ids(gnext, tb ^ 1);
+            TS.issue(p.src, gnext, tb ^ 1);
+        }
         // Fused tile scan + claims at a fixed geometry: thread t owns buckets
         // [t*kPer, t*kPer + kPer) (vector load), one warp scan, warp offsets by
         // REDUX (no single-warp phase), claim atomics issued before the staging
@@ -765,10 +766,10 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
         const uint32_t bb = threadIdx.x * kPer;
         uint32_t cn[kPer];
         if constexpr (kPer == 2) {
-            const uint2 t2 = *(const uint2*)&Q.cnt[bb];
+            const uint2 t2 = *(const uint2*)&cnt[bb];
             cn[0] = t2.x; cn[1] = t2.y;
         } else {
-            const uint4 t4 = *(const uint4*)&Q.cnt[bb];
+            const uint4 t4 = *(const uint4*)&cnt[bb];
             cn[0] = t4.x; cn[1] = t4.y; cn[2] = t4.z; cn[3] = t4.w;
         }
         uint32_t sum = 0;
@@ -791,9 +792,9 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
             st[k] = run;
             run += cn[k];
         }
-        if constexpr (kPer == 2) *(uint2*)&Q.cnt[bb] = make_uint2(st[0], st[1]);
-        else *(uint4*)&Q.cnt[bb] = make_uint4(st[0], st[1], st[2], st[3]);
-        if (threadIdx.x == 0) Q.cnt[NBC] = total;
+        if constexpr (kPer == 2) *(uint2*)&cnt[bb] = make_uint2(st[0], st[1]);
+        else *(uint4*)&cnt[bb] = make_uint4(st[0], st[1], st[2], st[3]);
+        if (threadIdx.x == 0) cnt[NBC] = total;
         __syncthreads();  // (3) tile-local bucket starts visible
         {  // claims strided over the threads (bucket t, t + kPNT, ...): all atomics in flight
             unsigned long long got[kPer];
@@ -802,27 +803,27 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
                 const uint32_t b = threadIdx.x + q * kPNT;
                 got[q] = 0;
                 if (b < nbo) {
-                    const uint32_t c = Q.cnt[b + 1] - Q.cnt[b];
+                    const uint32_t c = cnt[b + 1] - cnt[b];
                     if (c) got[q] = atomicAdd(&p.buckets[boff + b], (unsigned long long)c);
                 }
             }
 #pragma unroll
             for (int q = 0; q < kPer; ++q) {
                 const uint32_t b = threadIdx.x + q * kPNT;
-                Q.delta[b] = (long long)got[q] - (long long)Q.cnt[b];
+                Q.delta[b] = (long long)got[q] - (long long)cnt[b];
             }
         }
 #pragma unroll
         for (int j = 0; j < kPItems; ++j) {
             const uint32_t c = code[j];
             if (c != 0xffffffffu) {
-                const uint32_t pos = Q.cnt[c >> 16] + (c & 0xffffu);
+                const uint32_t pos = cnt[c >> 16] + (c & 0xffffu);
                 skeys[pos] = (j & 1) ? v[j >> 1].y : v[j >> 1].x;
                 Q.sbid[pos] = (uint16_t)(c >> 16);
             }
         }
         if (scode != 0xffffffffu) {
-            const uint32_t pos = Q.cnt[scode >> 16] + (scode & 0xffffu);
+            const uint32_t pos = cnt[scode >> 16] + (scode & 0xffffu);
             skeys[pos] = skey;
             Q.sbid[pos] = (uint16_t)(scode >> 16);
         }
@@ -832,10 +833,12 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
             const uint32_t j = threadIdx.x + q * kPNT;
             if (j < total) p.dst[(long long)j + Q.delta[Q.sbid[j]]] = skeys[j];
         }
-        if constexpr (kPer == 2) *(uint2*)&Q.cnt[bb] = make_uint2(0, 0);
-        else *(uint4*)&Q.cnt[bb] = make_uint4(0, 0, 0, 0);
-        fence_proxy_async_smem();  // staging writes (generic proxy) before the next bulk copy into this buffer
-        __syncthreads();
+        if constexpr (kPer == 2) *(uint2*)&cnt[bb] = make_uint2(0, 0);
+        else *(uint4*)&cnt[bb] = make_uint4(0, 0, 0, 0);
+        // staging writes (generic proxy) before the next bulk copy into this buffer,
+        // which is issued after the next tile's first barrier (no end-of-tile
+        // barrier: the counters alternate by tile parity)
+        fence_proxy_async_smem();
     }
 }
 
