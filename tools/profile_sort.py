@@ -27,6 +27,8 @@ def main():
     cfg = L.SortConfig(flags=L._native.FLAG_PHASE_TIMING)
     if os.environ.get("LSORT_TARGET"):
         cfg.bucket_target = int(os.environ["LSORT_TARGET"])
+    if os.environ.get("LSORT_FLAGS"):
+        cfg.flags |= int(os.environ["LSORT_FLAGS"])
     if os.environ.get("LSORT_RMI_B"):
         cfg.rmi_bucket_count = int(os.environ["LSORT_RMI_B"])
     for r in range(reps):
