@@ -97,10 +97,17 @@ __global__ void __launch_bounds__(NT, MINB) k_base_reg(const BaseItem* items, co
     typename SS::SmemR& S = *(typename SS::SmemR*)smem_u4;
     if (ctrl->nan_index != ~0ull) return;
     const uint32_t ni = min(*count, list_cap);
+    // the next segment of this CTA is pulled into L2 while this one sorts
+    // (its register loads then wait on L2, not HBM, latency)
+    if (threadIdx.x == 0 && blockIdx.x < ni) l2_prefetch(src + items[blockIdx.x].begin, 8 * items[blockIdx.x].n);
     for (uint32_t e = blockIdx.x; e < ni; e += gridDim.x) {
         const BaseItem it = items[e];
         const uint32_t n = (uint32_t)it.n;
         uint64_t* g = src + it.begin;
+        if (threadIdx.x == 0 && e + gridDim.x < ni) {
+            const BaseItem nx = items[e + gridDim.x];
+            l2_prefetch(src + nx.begin, 8 * nx.n);
+        }
         if (n <= (uint32_t)CAP / 2) base_reg_one<SS::ITEMS / 2, SS, OUT_F64>(g, n, S, out, it.begin);
         else base_reg_one<SS::ITEMS, SS, OUT_F64>(g, n, S, out, it.begin);
         __syncthreads();

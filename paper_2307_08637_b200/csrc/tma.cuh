@@ -52,6 +52,15 @@ __device__ __forceinline__ void tma_store_commit_and_wait_read() {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// L2 prefetch of a global range (bulk, no shared memory, no completion):
+// rounded out to 16-byte boundaries
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
+    const uintptr_t a = (uintptr_t)p & ~(uintptr_t)15, e = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
+    for (uintptr_t q = a; q < e; q += (1u << 20)) {  // size operand is 32-bit: chunk
+        const uint32_t n = (uint32_t)((e - q) < (1u << 20) ? (e - q) : (1u << 20));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(n) : "memory");
+    }
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
