@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(NT, MINB) k_base_reg(const BaseItem* items, co
         }
         if (n <= (uint32_t)CAP / 2) base_reg_one<SS::ITEMS / 2, SS, OUT_F64>(g, n, S, out, it.begin);
         else base_reg_one<SS::ITEMS, SS, OUT_F64>(g, n, S, out, it.begin);
-        __syncthreads();
+        // no barrier: the next segment writes shared memory (hist, reduction
+        // words) that the output loop does not read, and S.B only after its
+        // first barrier
     }
 }
 

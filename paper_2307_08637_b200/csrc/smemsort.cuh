@@ -261,8 +261,14 @@ struct SmemSort {
             }
             mn = __shfl_sync(FULL_MASK, a1, 0);
             mx = __shfl_sync(FULL_MASK, b1, 0);
-            __syncthreads();  // redh free again
+            // (no trailing barrier: the next writer of redh / S.red syncs first)
         };
+        // the digit histogram is zeroed here, before the first barrier, instead
+        // of behind a barrier of its own in sort_digits
+        {
+            const uint32_t nbz = (nb + 3) & ~3u;
+            for (uint32_t d = tid; d < nbz; d += NT) S.hist[d] = 0;
+        }
         uint32_t mnh, mxh;
         {
             uint32_t lo = ~0u, hi = 0;
@@ -288,6 +294,7 @@ struct SmemSort {
                 const uint32_t j = tid + i * NT;
                 if (j < n) { lo = min(lo, (uint32_t)k[i]); hi = max(hi, (uint32_t)k[i]); }
             }
+            __syncthreads();  // redh of the high-word reduction is read
             reduce32(lo, hi, mnl, mxl);
             if (mnl == mxl) {  // homogeneous: already sorted
 #pragma unroll
@@ -317,6 +324,7 @@ struct SmemSort {
                 mn = a1 < mn ? a1 : mn;
                 mx = b1 > mx ? b1 : mx;
             }
+            __syncthreads();  // redh of the high-word reduction is read
             if (lane == 0) { S.red[2 * warp] = mn; S.red[2 * warp + 1] = mx; }
             __syncthreads();
             uint64_t a1 = lane < NW ? S.red[2 * lane] : ~0ull, b1 = lane < NW ? S.red[2 * lane + 1] : 0ull;
@@ -338,21 +346,24 @@ struct SmemSort {
         for (int i = 0; i < IT; ++i) {
             dg[i] = (uint32_t)((k[i] - base) >> shift);
         }
-        sort_digits(k, dg, n, nb, S, scratch);
+        sort_digits<IT, SM, true>(k, dg, n, nb, S, scratch);
     }
 
     // Counting pass on caller-supplied digits (dg[i] < nb <= NBMAX, monotone in
     // the key), placement into S.B, collision fix-up, drain of large digits.
     // Result in S.B. The caller has zeroed nothing; S.n_* are reset here.
-    template <int IT = ITEMS, class SM>
+    // ZEROED: the caller zeroed hist[0, roundup4(nb)) before a barrier it has passed
+    template <int IT = ITEMS, class SM, bool ZEROED = false>
     __device__ static void sort_digits(uint64_t (&k)[IT], const uint32_t (&dg)[IT], uint32_t n, uint32_t nb,
                                        SM& S, uint64_t* scratch) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         uint64_t* B = S.B;
         nb = (nb + 3) & ~3u;  // whole 16-byte groups for the vectorised scan (extra digits stay empty)
         if (tid == 0) { S.n_med = 0; S.n_large = 0; S.n_l4 = 0; S.n_l16 = 0; }
-        for (uint32_t d = tid; d < nb; d += NT) S.hist[d] = 0;
-        __syncthreads();
+        if (!ZEROED) {
+            for (uint32_t d = tid; d < nb; d += NT) S.hist[d] = 0;
+            __syncthreads();
+        }
         uint32_t dp[IT];  // digit << 16 | rank within the digit
 #pragma unroll
         for (int i = 0; i < IT; ++i) {
