@@ -741,6 +741,26 @@ struct Engine {
                             (unsigned long long)ntiles, t[0], t[1], t[2], t[3], t[4], hc->n_rec, hc->n_base[0],
                             hc->n_base[1], hc->n_base[2], hc->n_fill);
                 }
+                if (trace_enabled() && np) {
+                    KindPlan kp[3];
+                    CU(cudaMemcpy(kp, C->kplan.p, sizeof(kp), cudaMemcpyDeviceToHost));
+                    fprintf(stderr, "    kinds: learned %u segs / %llu tiles, tree %u / %llu, radix %u / %llu\n",
+                            kp[0].nsegs, (unsigned long long)kp[0].ntiles, kp[1].nsegs, (unsigned long long)kp[1].ntiles,
+                            kp[2].nsegs, (unsigned long long)kp[2].ntiles);
+                    if (getenv("LSORT_TRACE_KINDS")) {
+                        std::string ks;
+                        for (uint32_t j = 0; j < np; ++j) {
+                            ModelHdr mh;
+                            CU(cudaMemcpy(&mh, C->models.as<uint8_t>() + hs[j].model_off, sizeof(mh), cudaMemcpyDeviceToHost));
+                            ks += mh.kind == kLearned ? (mh.s2 ? 'L' : 'l') : (mh.kind == kTree ? 'T' : 'R');
+                            if (j % 37 == 1)
+                                fprintf(stderr, "      seg %u n=%llu slice=%llu kind=%u nb=%u dup=%.4f s1=%llu s2=%llu rmi_b=%u\n", j,
+                                        (unsigned long long)hs[j].n, (unsigned long long)(hs[j].pslice & 0xffffff), mh.kind,
+                                        mh.nbuckets, mh.dup, (unsigned long long)mh.s1, (unsigned long long)mh.s2, hs[j].rmi_b);
+                        }
+                        fprintf(stderr, "    seg kinds: %s\n", ks.c_str());
+                    }
+                }
                 if (trace_enabled()) {
                     for (uint32_t bi = 0; bi < bigs.size(); ++bi) {
                         ModelHdr mh;

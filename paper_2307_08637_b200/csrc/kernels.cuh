@@ -95,6 +95,14 @@ struct DevCfg {
 };
 constexpr uint32_t kMinSlice = 64;  // shorter slices: draw a fresh sample
 constexpr uint32_t kPoorShare = 16;
+// GPU policy quality test: a learned model is poor when its largest bucket
+// holds more than 1/kPoorShare of the sample AND more than kPoorMean times the
+// mean bucket share (with 16 buckets, 1/16 alone would reject every model whose
+// largest bucket is merely above average)
+constexpr uint32_t kPoorMean = 4;
+__host__ __device__ __forceinline__ bool poor_model(uint64_t mx, uint64_t s, uint32_t nb) {
+    return mx * kPoorShare > s && mx * nb > (uint64_t)kPoorMean * s;
+}
 
 constexpr int kTileKeys = 4096;     // keys per classify/scatter tile
 constexpr uint16_t kNoMove = 0xffff;

@@ -513,7 +513,7 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
             uint64_t mx = 0;
             for (uint32_t b = threadIdx.x; b < Cl.nb; b += NT) mx = hist[b] > mx ? hist[b] : mx;
             mx = block_reduce_max<NT>(mx, S.red64);
-            if (mx * kPoorShare > s2)
+            if (poor_model(mx, s2, Cl.nb))
                 tree_build_block<NT>(A, s2, sd.tree_k, true, h, payload, S.u.tree.scratch, S.u.tree.wsum,
                                      S.u.tree.spl);
         }
@@ -931,7 +931,7 @@ __global__ void __launch_bounds__(512) k_block_sort(uint64_t* keys, uint32_t n) 
 }
 
 // ------------------------------------------------ model quality (GPU policy)
-// One CTA: if one bucket holds more than 1/kPoorShare of the sample, replace
+// One CTA: if the model is poor (poor_model: largest bucket share), replace
 // the learned model by a splitter tree over the same sorted sample.
 // (bucket sizes = differences of the sample's bucket offsets; *redo = 1 when
 // the model was replaced, so the offsets are recomputed for the tree)
@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(512) k_quality(const uint64_t* s, uint32_t n, 
         mx = c > mx ? c : mx;
     }
     mx = block_reduce_max<512>(mx, red);
-    if (mx * kPoorShare <= n) return;
+    if (!poor_model(mx, n, nb)) return;
     tree_build_block<512>(s, n, tree_k, true, h, model + sizeof(ModelHdr), scratch, wsum, spl);
     if (threadIdx.x == 0) *redo = 1;
 }
