@@ -18,6 +18,9 @@
  *   lsort_cuda_tree_build    <- SplitterTree::build          proj/src/models.cpp:133-185
  *   lsort_cuda_classify_tree <- SplitterTree::classify       proj/src/models.hpp:92-101
  *   lsort_cuda_verify        <- verify_sorted, multiset_hash proj/src/verify.hpp:17-29
+ *   lsort_cuda_learned_pivots / lsort_cuda_pivot_quality / lsort_cuda_eta
+ *                            <- learned_pivots_for_samplesort, pivot_quality, eta
+ *                               SPEC.md:236-262 (Alg. 4, Table 1)
  *   lsort_gen_keys           <- data.generate
  *   lsort_read_keys / lsort_write_keys <- data.read_keys / write_keys SPEC.md:480-497
  *   (lsort_cli, csrc/cli.cpp  <- bench-cli generate / bench / verify SPEC.md:521-590)
@@ -207,6 +210,26 @@ int lsort_cuda_block_sort(lsort_ctx* ctx, uint64_t* d_keys, uint64_t n);
 /* verify_sorted + multiset_hash on device keys (F64 keys hashed encoded). */
 int lsort_cuda_verify(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,
                       uint64_t* first_violation /* 0 = sorted */, uint64_t* multiset_hash);
+
+/* ---- pivot analysis ----
+ * lsort_cuda_learned_pivots <- learned_pivots_for_samplesort (Alg. 4): the
+ *   largest key of every learned cell i < b-1 under the given RMI (b output
+ *   buckets, cdf range [0,1]); cells never hit are dropped; ascending,
+ *   deduplicated. pivots_out (host) needs b-1 slots; keys in key_kind's
+ *   representation (float64 bit patterns for LSORT_KEY_F64).
+ * lsort_cuda_pivot_quality <- pivot_quality: sum_i |P(A <= p_i) - (i+1)/b| over
+ *   the device-resident SORTED keys; LSORT_EINVAL unless np + 1 == b
+ *   (SPEC.md:249). ranks_out (nullable, host, np) gets #keys <= p_i.
+ * lsort_cuda_eta <- eta: max(P(A <= p), 1 - P(A <= p)) - 1/2. */
+int lsort_cuda_learned_pivots(lsort_ctx* ctx, const lsort_rmi_header* h, const lsort_rmi_entry* entries,
+                              uint32_t b, const void* d_keys, uint64_t n, int key_kind,
+                              uint64_t* pivots_out, uint32_t* cells_out /* nullable: cell of each pivot */,
+                              uint32_t* count_out);
+int lsort_cuda_pivot_quality(lsort_ctx* ctx, const void* d_sorted, uint64_t n, int key_kind,
+                             const uint64_t* pivots, uint32_t np, uint32_t b, double* distance_out,
+                             uint64_t* ranks_out);
+int lsort_cuda_eta(lsort_ctx* ctx, const void* d_sorted, uint64_t n, int key_kind, uint64_t pivot,
+                   double* eta_out);
 
 /* ---- host-side synthetic generators (BASELINE.json configs) ---- */
 /* dist: 0 uniform, 1 normal, 2 lognormal(0,0.5), 3 exponential(2),

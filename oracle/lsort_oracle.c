@@ -747,3 +747,50 @@ int lso_sort_doubles(double* a, uint64_t n, const lso_cfg* c, int64_t* nan_index
     free(k);
     return 0;
 }
+
+/* ------------------------------------------------ pivot analysis */
+/* PAPER.md:324-349 (Alg. 4) */
+size_t lso_learned_pivots(const uint64_t* a, size_t n, const double* P, uint32_t B, uint32_t b, uint64_t* out) {
+    if (b < 2) return 0;
+    uint64_t* mx = (uint64_t*)calloc(b, sizeof(uint64_t));
+    unsigned char* hit = (unsigned char*)calloc(b, 1);
+    for (size_t w = 0; w < n; ++w) {
+        const uint32_t g = lso_learned_bucket(P, B, b, 0.0, 1.0, a[w]);
+        if (!hit[g] || a[w] > mx[g]) { mx[g] = a[w]; hit[g] = 1; }
+    }
+    size_t np = 0;
+    for (uint32_t i = 0; i + 1 < b; ++i)
+        if (hit[i] && (np == 0 || mx[i] > out[np - 1])) out[np++] = mx[i];
+    free(mx);
+    free(hit);
+    return np;
+}
+
+uint64_t lso_rank_le(const uint64_t* s, size_t n, uint64_t p) {
+    size_t lo = 0, hi = n;
+    while (lo < hi) {
+        const size_t mid = lo + (hi - lo) / 2;
+        if (s[mid] <= p) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+/* sum_{i=0}^{B-2} |P(A <= p_i) - (i+1)/B| */
+double lso_pivot_quality(const uint64_t* s, size_t n, const uint64_t* pv, size_t np, uint32_t b) {
+    if (np + 1 != b || n == 0) return -1.0;
+    double d = 0.0;
+    for (size_t i = 0; i < np; ++i) {
+        const double c = (double)lso_rank_le(s, n, pv[i]) / (double)n;
+        const double t = (double)(i + 1) / (double)b;
+        d += c > t ? c - t : t - c;
+    }
+    return d;
+}
+
+/* PAPER.md §3.1: eta = max(P(A <= p), 1 - P(A <= p)) - 1/2 */
+double lso_eta(const uint64_t* s, size_t n, uint64_t p) {
+    if (n == 0) return 0.0;
+    const double c = (double)lso_rank_le(s, n, p) / (double)n;
+    const double o = 1.0 - c;
+    return (c > o ? c : o) - 0.5;
+}

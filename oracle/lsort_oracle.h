@@ -133,6 +133,22 @@ int lso_sort_keys(uint64_t* a, uint64_t n, const lso_cfg* c);
  * sort, decode. */
 int lso_sort_doubles(double* a, uint64_t n, const lso_cfg* c, int64_t* nan_index);
 
+/* ---- pivot analysis -------- */
+/* Alg. 4 learned_pivots_for_samplesort: for every key, g = the learned bucket
+ * of F(key) with b buckets (models.hpp:162-171, cdf range [0,1]); the pivot
+ * for boundary (i+1)/b is the largest key of cell i, i in [0, b-2]; cells
+ * never hit are dropped (Alg. 4 "p.filter(v >= 0)"); output strictly
+ * increasing. Returns the pivot count (<= b-1); out holds b-1 keys. */
+size_t lso_learned_pivots(const uint64_t* a, size_t n, const double* P, uint32_t B, uint32_t b, uint64_t* out);
+/* P(A <= p) * N: number of keys <= p in the sorted array (upper bound) */
+uint64_t lso_rank_le(const uint64_t* sorted, size_t n, uint64_t p);
+/* pivot_quality: sum_{i<np} |P(A <= p_i) - (i+1)/b| (summed in
+ * pivot order). Returns -1.0 when np + 1 != b (the metric is defined
+ * against b). */
+double lso_pivot_quality(const uint64_t* sorted, size_t n, const uint64_t* pivots, size_t np, uint32_t b);
+/* eta(pivot) = max(P(A <= p), 1 - P(A <= p)) - 1/2 (§3.1) */
+double lso_eta(const uint64_t* sorted, size_t n, uint64_t pivot);
+
 /* radix_base_case_sort: MSD byte radix, insertion <= 16 */
 void lso_radix_base_case_sort(uint64_t* a, uint64_t n, uint32_t insertion_threshold);
 

@@ -108,6 +108,11 @@ def lib():
         L.lso_sort_doubles.argtypes = [vp, u64, C.POINTER(Cfg), C.POINTER(C.c_int64)]
         L.lso_radix_base_case_sort.restype = None
         L.lso_radix_base_case_sort.argtypes = [vp, u64, C.c_uint32]
+        L.lso_learned_pivots.restype = sz
+        L.lso_learned_pivots.argtypes = [vp, sz, vp, C.c_uint32, C.c_uint32, vp]
+        L.lso_rank_le.restype = u64; L.lso_rank_le.argtypes = [vp, sz, u64]
+        L.lso_pivot_quality.restype = f64; L.lso_pivot_quality.argtypes = [vp, sz, vp, sz, C.c_uint32]
+        L.lso_eta.restype = f64; L.lso_eta.argtypes = [vp, sz, u64]
         _lib = L
     return _lib
 
@@ -206,6 +211,28 @@ def tree_classify(t: Tree, keys) -> np.ndarray:
 def duplicate_fraction(sorted_sample) -> float:
     s = _u64(sorted_sample)
     return lib().lso_duplicate_fraction(_p(s), s.size)
+
+
+def learned_pivots(keys, P, B: int, b: int) -> np.ndarray:
+    """Alg. 4: largest key per learned cell i < b-1, empty cells dropped."""
+    a = _u64(keys)
+    out = np.zeros(max(b - 1, 1), np.uint64)
+    m = lib().lso_learned_pivots(_p(a), a.size, _p(np.ascontiguousarray(P, np.float64)), B, b, _p(out))
+    return out[:m].copy()
+
+
+def pivot_quality(sorted_keys, pivots, b: int) -> float:
+    """sum_i |P(A <= p_i) - (i+1)/b|; ValueError unless len(pivots) + 1 == b."""
+    s, p = _u64(sorted_keys), _u64(pivots)
+    if p.size + 1 != b:
+        raise ValueError("pivot count + 1 != b")
+    return float(lib().lso_pivot_quality(_p(s), s.size, _p(p), p.size, b))
+
+
+def eta(sorted_keys, pivot: int) -> float:
+    """max(P(A <= p), 1 - P(A <= p)) - 1/2 (§3.1)."""
+    s = _u64(sorted_keys)
+    return float(lib().lso_eta(_p(s), s.size, int(pivot)))
 
 
 def verify_sorted(a):

@@ -303,6 +303,49 @@ class Context:
             out["tree"] = t
         return out
 
+    # -- pivot analysis (Alg. 4 / Table 1) -----------
+    def learned_pivots(self, P: np.ndarray, submodels: int, b: int, d_keys, cells: bool = False):
+        """Alg. 4: largest key of each learned cell i < b-1 (empty cells dropped),
+        ascending; in the keys' representation (float64 for float keys).
+        cells=True also returns each pivot's cell index."""
+        self._sync_stream()
+        h, e = unpack_rmi(P, submodels)
+        out = np.zeros(max(b - 1, 1), np.uint64)
+        cel = np.zeros(max(b - 1, 1), np.uint32)
+        cnt = C.c_uint32(0)
+        rc = N.lib().lsort_cuda_learned_pivots(self._h, C.byref(h), e.ctypes.data_as(C.c_void_p), b,
+                                               C.c_void_p(d_keys.data_ptr()), d_keys.numel(),
+                                               _key_kind_of(d_keys), out.ctypes.data_as(C.c_void_p),
+                                               cel.ctypes.data_as(C.c_void_p), C.byref(cnt))
+        _check(self, rc)
+        out = out[:cnt.value].copy()
+        if _key_kind_of(d_keys) == N.KEY_F64:
+            out = out.view(np.float64)
+        return (out, cel[:cnt.value].copy()) if cells else out
+
+    def pivot_quality(self, d_sorted, pivots, b: int):
+        """(distance, ranks): sum_i |P(A <= p_i) - (i+1)/b| over device-resident
+        sorted keys; LsortError (EINVAL) unless len(pivots) + 1 == b."""
+        self._sync_stream()
+        p = np.ascontiguousarray(np.asarray(pivots)).view(np.uint64)
+        d = C.c_double(0.0)
+        ranks = np.zeros(max(p.size, 1), np.uint64)
+        rc = N.lib().lsort_cuda_pivot_quality(self._h, C.c_void_p(d_sorted.data_ptr()), d_sorted.numel(),
+                                              _key_kind_of(d_sorted), p.ctypes.data_as(C.c_void_p), p.size, b,
+                                              C.byref(d), ranks.ctypes.data_as(C.c_void_p))
+        _check(self, rc)
+        return d.value, ranks[:p.size]
+
+    def eta(self, d_sorted, pivot) -> float:
+        """max(P(A <= p), 1 - P(A <= p)) - 1/2 (§3.1)."""
+        self._sync_stream()
+        pv = int(np.asarray(pivot).reshape(1).view(np.uint64)[0])
+        out = C.c_double(0.0)
+        rc = N.lib().lsort_cuda_eta(self._h, C.c_void_p(d_sorted.data_ptr()), d_sorted.numel(),
+                                    _key_kind_of(d_sorted), pv, C.byref(out))
+        _check(self, rc)
+        return out.value
+
     def block_sort(self, d_keys):
         self._sync_stream()
         _check(self, N.lib().lsort_cuda_block_sort(self._h, C.c_void_p(d_keys.data_ptr()), d_keys.numel()))

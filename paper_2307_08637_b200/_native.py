@@ -74,7 +74,7 @@ EXPORTS = [
     "lsort_cuda_tree_build", "lsort_cuda_classify_tree", "lsort_cuda_build_model",
     "lsort_cuda_block_sort", "lsort_cuda_verify", "lsort_gen_keys", "lsort_cuda_dist_sample",
     "lsort_cuda_dist_train", "lsort_cuda_dist_histogram", "lsort_cuda_dist_partition",
-    "lsort_cuda_decode_inplace",
+    "lsort_cuda_decode_inplace", "lsort_cuda_learned_pivots", "lsort_cuda_pivot_quality", "lsort_cuda_eta",
 ]
 
 _lib = None
@@ -130,6 +130,12 @@ def lib():
     L.lsort_cuda_block_sort.argtypes = [vp, vp, u64]
     L.lsort_cuda_verify.restype = i32
     L.lsort_cuda_verify.argtypes = [vp, vp, u64, i32, P(u64), P(u64)]
+    L.lsort_cuda_learned_pivots.restype = i32
+    L.lsort_cuda_learned_pivots.argtypes = [vp, P(lsort_rmi_header), vp, u32, vp, u64, i32, vp, vp, P(u32)]
+    L.lsort_cuda_pivot_quality.restype = i32
+    L.lsort_cuda_pivot_quality.argtypes = [vp, vp, u64, i32, vp, u32, u32, P(f64), vp]
+    L.lsort_cuda_eta.restype = i32
+    L.lsort_cuda_eta.argtypes = [vp, vp, u64, i32, u64, P(f64)]
     L.lsort_gen_keys.restype = i32
     L.lsort_gen_keys.argtypes = [i32, u64, u64, u64, u64, vp, i32]
     L.lsort_cuda_dist_sample.restype = i32

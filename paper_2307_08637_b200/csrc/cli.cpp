@@ -6,6 +6,7 @@
 //   lsort_cli verify <file> [--f64]
 //   lsort_cli bench --dataset <name|file> [--n N] [--runs R] [--seed S] [--warmup W]
 //                   [--algo gpu-aips2o|reference]... [--csv out.csv] [--resident] [--device D]
+//   lsort_cli pivot-quality <dataset> <n> <pivots> <trials> <seed> [csv_out] [--device D]
 //
 // Key files: 8-byte little-endian count + count 8-byte keys (lsort_read_keys /
 // lsort_write_keys). Float datasets are written as encoded keys (keys.hpp:36-42,
@@ -14,6 +15,12 @@
 // SPEC.md:544), verify_sorted + multiset hash against the input, one CSV row
 // `algorithm,dataset,n,workers,run,elapsed_ns,keys_per_second,verified`, then a
 // summary block per algorithm; a failed verification fails the exit status.
+// pivot-quality (Table 1): per trial, random-sampling
+// pivots (IPS4o-style oversampling) and the RMI's implicit pivots (Alg. 4,
+// lsort_cuda_learned_pivots) scored by pivot_quality against the sorted data;
+// CSV `trial,method,requested,pivots,distance,flagged` plus a mean row per method
+// (flagged: Alg. 4 dropped empty cells; the RMI set is still scored against b,
+// an empty cell's boundary taking the last pivot below it).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -69,6 +76,7 @@ int usage() {
                  "  lsort_cli bench --dataset <name|file> [--n N] [--runs R] [--seed S]\n"
                  "                  [--algo gpu-aips2o|reference]... [--csv out.csv] [--resident] [--device D]\n"
                  "                  [--warmup W]\n"
+                 "  lsort_cli pivot-quality <dataset> <n> <pivots> <trials> <seed> [csv_out] [--device D]\n"
                  "generators: %s\n",
                  registry_names().c_str());
     return 2;
@@ -310,6 +318,117 @@ int cmd_bench(int argc, char** argv) {
     return all_ok ? 0 : 1;
 }
 
+// SPEC.md:550-558 cmd_pivot_quality
+int cmd_pivot_quality(int argc, char** argv) {
+    if (argc < 7) return usage();
+    const std::string dataset = argv[2];
+    const uint64_t n = std::strtoull(argv[3], nullptr, 10);
+    const uint32_t want = (uint32_t)std::strtoul(argv[4], nullptr, 10);
+    const int trials = std::atoi(argv[5]);
+    const uint64_t seed = std::strtoull(argv[6], nullptr, 10);
+    std::string csv;
+    int device = 0;
+    for (int i = 7; i < argc; ++i) {
+        if (!std::strcmp(argv[i], "--device") && i + 1 < argc) device = std::atoi(argv[++i]);
+        else csv = argv[i];
+    }
+    const uint32_t b = want + 1;
+    if (n < 2 || want < 1 || trials < 1 || b > 2048) {
+        std::fprintf(stderr, "pivot-quality: need n >= 2, 1 <= pivots <= 2047, trials >= 1\n");
+        return 2;
+    }
+    Data data;
+    if (!generate(dataset, n, seed, data)) return 2;
+    std::vector<uint64_t> keys(n);  // encoded keys (keys.hpp:36-42): the model's domain
+    for (uint64_t i = 0; i < n; ++i) keys[i] = data.f64 ? encode(data.d[i]) : data.u[i];
+    lsort_ctx* ctx = nullptr;
+    if (lsort_cuda_ctx_create(&ctx, device, nullptr, 0) != LSORT_OK) {
+        std::fprintf(stderr, "pivot-quality: no CUDA device\n");
+        return 1;
+    }
+    uint64_t *d_keys = nullptr, *d_sorted = nullptr, *d_smp = nullptr;
+    const uint64_t smax = std::max<uint64_t>(2, std::min<uint64_t>((n + 99) / 100, 1ull << 20));
+    cudaMalloc(&d_keys, n * 8);
+    cudaMalloc(&d_sorted, n * 8);
+    cudaMalloc(&d_smp, smax * 8);
+    cudaMemcpy(d_keys, keys.data(), n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_sorted, keys.data(), n * 8, cudaMemcpyHostToDevice);
+    int rc = lsort_cuda_sort(ctx, d_sorted, n, LSORT_KEY_U64, LSORT_MEM_DEVICE, nullptr, nullptr, nullptr);
+    FILE* out = csv.empty() ? stdout : std::fopen(csv.c_str(), "w");
+    if (!out) {
+        std::fprintf(stderr, "cannot write %s\n", csv.c_str());
+        return 1;
+    }
+    std::fprintf(out, "trial,method,requested,pivots,distance,flagged\n");
+    // IPS4o oversampling factor alpha = 0.2 log2 n (at least 1)
+    const uint32_t alpha = std::max<uint32_t>(1, (uint32_t)(0.2 * std::log2((double)n)));
+    double sum[2] = {0, 0};
+    std::vector<lsort_rmi_entry> ent(b);
+    for (int t = 0; t < trials && rc == LSORT_OK; ++t) {
+        const uint64_t st = splitmix(seed + 1 + (uint64_t)t);
+        // random-sampling pivots: alpha * b keys, every alpha-th of the sorted sample
+        std::vector<uint64_t> smp((size_t)alpha * b);
+        for (size_t j = 0; j < smp.size(); ++j) smp[j] = keys[splitmix(st + j) % n];
+        std::sort(smp.begin(), smp.end());
+        std::vector<uint64_t> rp;
+        for (uint32_t i = 0; i + 1 < b; ++i) {
+            const uint64_t v = smp[(size_t)alpha * (i + 1) - 1];
+            if (rp.empty() || v > rp.back()) rp.push_back(v);
+        }
+        // the RMI's pivots: model on a sorted sample (SPEC.md:438 size), Alg. 4 over all keys
+        const uint64_t s = smax;
+        std::vector<uint64_t> rs(s);
+        const uint64_t st2 = splitmix(st ^ 0x5a3c9e1f0b7d2468ull);
+        for (uint64_t j = 0; j < s; ++j) rs[j] = keys[splitmix(st2 + j) % n];
+        std::sort(rs.begin(), rs.end());
+        cudaMemcpy(d_smp, rs.data(), s * 8, cudaMemcpyHostToDevice);
+        lsort_rmi_header h{};
+        std::vector<uint64_t> lp(b);
+        std::vector<uint32_t> cells(b);
+        uint32_t nlp = 0;
+        rc = lsort_cuda_rmi_train(ctx, d_smp, s, b, &h, ent.data());
+        if (rc == LSORT_OK)
+            rc = lsort_cuda_learned_pivots(ctx, &h, ent.data(), b, d_keys, n, LSORT_KEY_U64, lp.data(), cells.data(),
+                                           &nlp);
+        lp.resize(nlp);
+        const std::vector<uint64_t>* sets[2] = {&rp, &lp};
+        const char* names[2] = {"random", "rmi"};
+        for (int m = 0; m < 2 && rc == LSORT_OK; ++m) {
+            const auto& pv = *sets[m];
+            double d = 0;
+            std::vector<uint64_t> rk(pv.size() + 1);
+            rc = lsort_cuda_pivot_quality(ctx, d_sorted, n, LSORT_KEY_U64, pv.data(), (uint32_t)pv.size(),
+                                          (uint32_t)pv.size() + 1, &d, rk.data());
+            if (rc == LSORT_OK && m == 1 && pv.size() != want) {
+                // dropped cells: the pivot of boundary (g+1)/b is the largest key with
+                // F < (g+1)/b (Alg. 4's definition) = the last pivot of a cell <= g
+                // (rank 0 before the first one); scored against b
+                d = 0;
+                size_t j = 0;
+                uint64_t r = 0;
+                for (uint32_t g = 0; g + 1 < b; ++g) {
+                    while (j < pv.size() && cells[j] <= g) r = rk[j++];
+                    const double c = (double)r / (double)n, tg = (double)(g + 1) / (double)b;
+                    d += c > tg ? c - tg : tg - c;
+                }
+            }
+            sum[m] += d;
+            std::fprintf(out, "%d,%s,%u,%zu,%.6f,%d\n", t, names[m], want, pv.size(), d, (int)(pv.size() != want));
+        }
+    }
+    if (rc == LSORT_OK)
+        for (int m = 0; m < 2; ++m)
+            std::fprintf(out, "mean,%s,%u,,%.6f,\n", m ? "rmi" : "random", want, sum[m] / trials);
+    else
+        std::fprintf(stderr, "pivot-quality: %s\n", lsort_cuda_last_error(ctx));
+    if (out != stdout) std::fclose(out);
+    cudaFree(d_keys);
+    cudaFree(d_sorted);
+    cudaFree(d_smp);
+    lsort_cuda_ctx_destroy(ctx);
+    return rc == LSORT_OK ? 0 : 1;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -319,5 +438,6 @@ int main(int argc, char** argv) {
     if (cmd == "sort") return cmd_sort(argc, argv);
     if (cmd == "verify") return cmd_verify(argc, argv);
     if (cmd == "bench") return cmd_bench(argc, argv);
+    if (cmd == "pivot-quality") return cmd_pivot_quality(argc, argv);
     return usage();
 }

@@ -124,7 +124,7 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws, ids, clus, bat[3], psample, slices, dist_hist, fwd_model, fwd_slices;
+        kseg, ktp, kplan, qws, ids, clus, bat[3], psample, slices, dist_hist, fwd_model, fwd_slices, piv;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
@@ -1391,6 +1391,104 @@ int lsort_cuda_block_sort(lsort_ctx* C, uint64_t* d_keys, uint64_t n) {
         CU(cudaGetLastError());
     } catch (const LsortError& e) {
         return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+// ------------------------------------------------------------ pivot analysis
+// keys.hpp:24-32 on the host, on bit patterns: f64 bits -> encoded key and back
+static inline uint64_t encode_host(uint64_t bits) {
+    return (bits >> 63) ? ~bits : (bits ^ 0x8000000000000000ull);
+}
+static inline uint64_t decode_bits_host(uint64_t k) {
+    return (k >> 63) ? (k ^ 0x8000000000000000ull) : ~k;
+}
+int lsort_cuda_learned_pivots(lsort_ctx* C, const lsort_rmi_header* h, const lsort_rmi_entry* e, uint32_t b,
+                              const void* d_keys, uint64_t n, int key_kind, uint64_t* pivots_out,
+                              uint32_t* cells_out, uint32_t* count_out) {
+    if (!C || !h || !e || !pivots_out || !count_out || b < 2 || b > kMaxNB || h->submodels == 0 ||
+        h->submodels > LSORT_MAX_RMI || (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_F64))
+        return fail(C, {LSORT_EINVAL, "learned_pivots: bad arguments"});
+    try {
+        CU(cudaSetDevice(C->device));
+        const size_t bytes = 12 * (size_t)b;
+        // host staging sized first: upload_learned copies from it asynchronously
+        const size_t mb = sizeof(ModelHdr) + kLearnedEntryBytes * (size_t)h->submodels;
+        if (!C->piv.ensure(bytes) || !C->hmodel.ensure(std::max(bytes, mb))) throw LsortError{LSORT_ENOMEM, "pivots"};
+        upload_learned(C, h, e, b, 0.0, 1.0);
+        unsigned long long* gmax = C->piv.as<unsigned long long>();
+        unsigned int* ghit = (unsigned int*)(gmax + b);
+        CU(cudaMemsetAsync(C->piv.p, 0, bytes, C->stream));
+        if (n) launch_learned_pivots(C->models.as<uint8_t>(), d_keys, n, key_kind == LSORT_KEY_F64, gmax, ghit,
+                                     (int)kLearnedEntryBytes * (int)h->submodels, C->stream);
+        CU(cudaStreamSynchronize(C->stream));  // the model upload's staging buffer is reused below
+        CU(cudaMemcpy(C->hmodel.p, C->piv.p, bytes, cudaMemcpyDeviceToHost));
+        CU(cudaGetLastError());
+        const uint64_t* hm = C->hmodel.as<uint64_t>();
+        const uint32_t* hh = (const uint32_t*)(hm + b);
+        uint32_t np = 0;
+        uint64_t last = 0;
+        for (uint32_t i = 0; i + 1 < b; ++i) {  // cells 0..b-2: boundaries (i+1)/b
+            if (!hh[i] || (np && hm[i] <= last)) continue;
+            last = hm[i];
+            if (cells_out) cells_out[np] = i;
+            pivots_out[np++] = key_kind == LSORT_KEY_F64 ? decode_bits_host(hm[i]) : hm[i];
+        }
+        *count_out = np;
+    } catch (const LsortError& er) {
+        return fail(C, er);
+    }
+    return LSORT_OK;
+}
+
+static void pivot_ranks(lsort_ctx* C, const void* d_sorted, uint64_t n, int key_kind, const uint64_t* pivots,
+                        uint32_t np, uint64_t* ranks) {
+    if (!C->piv.ensure(16 * (size_t)np + 16) || !C->hmodel.ensure(16 * (size_t)np + 16))
+        throw LsortError{LSORT_ENOMEM, "pivots"};
+    uint64_t* hp = C->hmodel.as<uint64_t>();
+    for (uint32_t i = 0; i < np; ++i) hp[i] = key_kind == LSORT_KEY_F64 ? encode_host(pivots[i]) : pivots[i];
+    uint64_t* dp = C->piv.as<uint64_t>();
+    CU(cudaMemcpyAsync(dp, hp, 8 * (size_t)np, cudaMemcpyHostToDevice, C->stream));
+    launch_rank_le(d_sorted, n, key_kind == LSORT_KEY_F64, dp, np, dp + np, C->stream);
+    CU(cudaMemcpyAsync(ranks, dp + np, 8 * (size_t)np, cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaStreamSynchronize(C->stream));
+    CU(cudaGetLastError());
+}
+
+int lsort_cuda_pivot_quality(lsort_ctx* C, const void* d_sorted, uint64_t n, int key_kind, const uint64_t* pivots,
+                             uint32_t np, uint32_t b, double* distance_out, uint64_t* ranks_out) {
+    if (!C || !distance_out || (np && !pivots) || n == 0 ||
+        (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_F64))
+        return fail(C, {LSORT_EINVAL, "pivot_quality: bad arguments"});
+    if ((uint64_t)np + 1 != b) return fail(C, {LSORT_EINVAL, "pivot_quality: pivot count + 1 != b"});
+    try {
+        CU(cudaSetDevice(C->device));
+        std::vector<uint64_t> r(np ? np : 1);
+        if (np) pivot_ranks(C, d_sorted, n, key_kind, pivots, np, r.data());
+        double d = 0.0;  // summed in pivot order, as the oracle does
+        for (uint32_t i = 0; i < np; ++i) {
+            const double c = (double)r[i] / (double)n, t = (double)(i + 1) / (double)b;
+            d += c > t ? c - t : t - c;
+        }
+        *distance_out = d;
+        if (ranks_out) std::memcpy(ranks_out, r.data(), 8 * (size_t)np);
+    } catch (const LsortError& er) {
+        return fail(C, er);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_eta(lsort_ctx* C, const void* d_sorted, uint64_t n, int key_kind, uint64_t pivot, double* eta_out) {
+    if (!C || !eta_out || n == 0 || (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_F64))
+        return fail(C, {LSORT_EINVAL, "eta: bad arguments"});
+    try {
+        CU(cudaSetDevice(C->device));
+        uint64_t r = 0;
+        pivot_ranks(C, d_sorted, n, key_kind, &pivot, 1, &r);
+        const double c = (double)r / (double)n, o = 1.0 - c;
+        *eta_out = (c > o ? c : o) - 0.5;
+    } catch (const LsortError& er) {
+        return fail(C, er);
     }
     return LSORT_OK;
 }

@@ -166,6 +166,12 @@ void launch_cluster_sort(const BaseItem* segs, uint32_t nsegs, const uint64_t* s
 void launch_classify_ids(const uint8_t* model, const void* keys, uint64_t n, int in_f64,
                          uint32_t* ids, uint16_t* ids16, unsigned long long* hist, int payload, cudaStream_t st);
 void launch_verify(const void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st);
+// Alg. 4 per-cell maxima (gmax / ghit zeroed by the caller, nbuckets cells)
+void launch_learned_pivots(const uint8_t* model, const void* keys, uint64_t n, int in_f64, unsigned long long* gmax,
+                           unsigned int* ghit, int payload, cudaStream_t st);
+// ranks[i] = #keys <= pivots[i] (pivots encoded when f64)
+void launch_rank_le(const void* sorted, uint64_t n, int f64, const uint64_t* pivots, uint32_t np, uint64_t* ranks,
+                    cudaStream_t st);
 void launch_copy_bytes(void* dst, const void* src, size_t bytes, cudaStream_t st);  // UVA pointers
 void launch_decode(uint64_t* keys, uint64_t n, cudaStream_t st);
 int num_sms();

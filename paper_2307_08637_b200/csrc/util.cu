@@ -36,6 +36,52 @@ __global__ void __launch_bounds__(256) k_classify_ids(const uint8_t* model, cons
     }
 }
 
+// Alg. 4 learned_pivots_for_samplesort: per learned cell
+// the largest key and whether the cell was hit (per-CTA shared maxima, one
+// global atomic per hit cell per CTA). The host drops empty cells.
+template <bool IN_F64>
+__global__ void __launch_bounds__(256) k_learned_pivots(const uint8_t* model, const void* keys, uint64_t n,
+                                                       unsigned long long* gmax, unsigned int* ghit) {
+    griddep_wait();
+    extern __shared__ uint4 smem_u4[];
+    __shared__ unsigned long long smax[kMaxNB];
+    __shared__ unsigned int shit[kMaxNB];
+    uint8_t* msm = (uint8_t*)smem_u4;
+    load_model_smem(model, msm);
+    Classifier C;
+    C.init(msm);
+    for (uint32_t b = threadIdx.x; b < C.nb; b += 256) { smax[b] = 0; shit[b] = 0; }
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
+        const uint64_t k = load_key(keys, i, IN_F64);
+        const uint32_t g = C.classify<kLearned>(k);
+        atomicMax(&smax[g], (unsigned long long)k);
+        shit[g] = 1u;
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < C.nb; b += 256)
+        if (shit[b]) {
+            atomicMax(&gmax[b], smax[b]);
+            atomicOr(&ghit[b], 1u);
+        }
+}
+
+// P(A <= p) * N for each pivot (upper bound over the sorted keys, compared encoded)
+template <bool F64>
+__global__ void k_rank_le(const void* sorted, uint64_t n, const uint64_t* pivots, uint32_t np, uint64_t* ranks) {
+    griddep_wait();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    const uint64_t p = pivots[i];
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (load_key(sorted, mid, F64) <= p) lo = mid + 1;
+        else hi = mid;
+    }
+    ranks[i] = lo;
+}
+
 // verify_sorted + multiset_hash (verify.hpp:17-29)
 template <bool F64>
 __global__ void __launch_bounds__(256) k_verify(const void* keys, uint64_t n, Ctrl* ctrl) {
@@ -107,6 +153,23 @@ void kernels_init() {
     cluster_init(optin);
     allow_smem(k_classify_ids<true>, optin);
     allow_smem(k_classify_ids<false>, optin);
+    allow_smem(k_learned_pivots<true>, optin);
+    allow_smem(k_learned_pivots<false>, optin);
+}
+
+void launch_learned_pivots(const uint8_t* model, const void* keys, uint64_t n, int in_f64, unsigned long long* gmax,
+                           unsigned int* ghit, int payload, cudaStream_t st) {
+    const size_t sm = sizeof(ModelHdr) + (size_t)payload;
+    const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms() * 4);
+    if (in_f64) pdl(k_learned_pivots<true>, grid, 256, sm, st, model, keys, n, gmax, ghit);
+    else pdl(k_learned_pivots<false>, grid, 256, sm, st, model, keys, n, gmax, ghit);
+}
+
+void launch_rank_le(const void* sorted, uint64_t n, int f64, const uint64_t* pivots, uint32_t np, uint64_t* ranks,
+                    cudaStream_t st) {
+    const int grid = (int)((np + 127) / 128);
+    if (f64) pdl(k_rank_le<true>, grid, 128, 0, st, sorted, n, pivots, np, ranks);
+    else pdl(k_rank_le<false>, grid, 128, 0, st, sorted, n, pivots, np, ranks);
 }
 
 void launch_classify_ids(const uint8_t* model, const void* keys, uint64_t n, int in_f64, uint32_t* ids,
