@@ -70,11 +70,13 @@ def test_header_struct_layouts_match_ctypes(tmp_path):
             assert int(out[f"{name}.{f}"]) == getattr(cls, f).offset, f"{name}.{f}"
 
 
-@pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="GPU present")
 def test_context_without_gpu_fails_cleanly():
     h = C.c_void_p()
     rc = N.lib().lsort_cuda_ctx_create(C.byref(h), 0, None, 0)
-    assert rc != N.LSORT_OK and not h.value
+    if rc == N.LSORT_OK:  # a visible GPU (whatever its device node is called)
+        N.lib().lsort_cuda_ctx_destroy(h)
+        pytest.skip("GPU present")
+    assert not h.value
 
 
 @pytest.mark.parametrize("dist,seed", [("uniform", 42), ("normal", 7), ("lognormal05", 7),
