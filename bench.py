@@ -173,6 +173,8 @@ def run_ours(args):
     dist_mode = world > 1 or args.dist
     if dist_mode:
         import torch.distributed as tdist
+        for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533")):
+            os.environ.setdefault(k, v)  # --dist without torchrun: a one-rank group
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     label, dists, n, kind = CONFIGS[args.config]
     if args.keys:
@@ -384,6 +386,57 @@ def run_ours(args):
         line["e2e"] = {"value": len(hosts) * n / (e2e_ms * 1e-3) / 1e9, "unit": "Gkeys/s",
                        "h2d_bytes_per_step": 8 * n * len(hosts), "d2h_bytes_per_step": 8 * n * len(hosts),
                        "ms_per_step": e2e_ms}
+    elif dist_mode and args.e2e_steps > 0:
+        # the distributed public API end to end: every rank copies its shard in
+        # from pinned host memory, the global sort runs (RMI splitters + NCCL
+        # all-to-all + local sort), and the rank's output range is read back to
+        # pinned host memory -- CUDA events around all of it, max over ranks
+        import torch.distributed as tdist
+        hosts = [p.cpu().pin_memory() for p in pristine]
+        # result buffers pinned up front (a rank receives ~n keys; larger ranges
+        # get a fresh buffer); copies in / out on their own streams, pipelined
+        # against the sorts: array i+1 streams in while array i sorts
+        cap = int(1.5 * n) + 4096
+        outs = [torch.empty(cap, dtype=torch.int64, pin_memory=True) for _ in pristine]
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        e2e_ms, d2h = 0.0, 0
+        for step in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            barrier()
+            st = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            s_in.wait_stream(st)
+            ev_in = []
+            for i in range(len(hosts)):
+                with torch.cuda.stream(s_in):
+                    work[i].copy_(hosts[i], non_blocking=True)
+                    ev_in.append(torch.cuda.Event())
+                    ev_in[-1].record(s_in)
+            step_d2h, keep = 0, []
+            for i in range(len(hosts)):
+                st.wait_event(ev_in[i])
+                out, _ = sorter.sort(work[i])
+                o64 = out.view(torch.int64)
+                dst = outs[i] if o64.numel() <= cap else torch.empty(o64.numel(), dtype=torch.int64, pin_memory=True)
+                s_out.wait_stream(st)
+                with torch.cuda.stream(s_out):
+                    dst[: o64.numel()].copy_(o64, non_blocking=True)
+                keep.append(out)
+                step_d2h += o64.numel() * 8
+            st.wait_stream(s_out)
+            e1.record(st)
+            torch.cuda.synchronize()
+            if step > 0:
+                e2e_ms += e0.elapsed_time(e1)
+                d2h += step_d2h
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_ms = float(t.item()) / max(1, args.e2e_steps)
+        line["e2e"] = {"value": keys_per_step / (e2e_ms * 1e-3) / 1e9, "unit": "Gkeys/s",
+                       "h2d_bytes_per_step": 8 * n * len(hosts),
+                       "d2h_bytes_per_step": int(d2h / max(1, args.e2e_steps)),
+                       "ms_per_step": e2e_ms, "per_rank_bytes": True}
     else:
         line["e2e"] = None
     if rank == 0 and world == 1 and not args.no_cpu:
