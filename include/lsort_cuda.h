@@ -282,6 +282,21 @@ int lsort_cuda_dist_partition(lsort_ctx* ctx, const void* d_keys, uint64_t n, in
                               const lsort_rmi_header* h, const lsort_rmi_entry* entries,
                               const uint32_t* bucket_bounds, uint32_t nranks, uint64_t* d_out,
                               uint64_t* send_counts);
+/* Local sort of a rank's received keys when they are already grouped by the
+ * global model's buckets [b_lo, b_hi) (bucket_sizes[b - b_lo] keys each, in
+ * bucket order): buckets within the base-case capacity are sorted in place, the
+ * others start the recursion at level 1 (children train on their slice of the
+ * sorted global sample) -- no second level-0 pass. key_kind LSORT_KEY_U64 or
+ * LSORT_KEY_ENC_F64 (decoded to float64 in the final stores). */
+int lsort_cuda_sort_buckets(lsort_ctx* ctx, void* d_keys, uint64_t n, int key_kind, const lsort_cfg* cfg,
+                            const lsort_rmi_header* h, const lsort_rmi_entry* entries, uint32_t b_lo,
+                            uint32_t b_hi, const uint64_t* bucket_sizes /* host */,
+                            const uint64_t* d_sorted_sample, uint64_t sample_n, lsort_stats* stats);
+/* Device run gather: for r < nruns, copy runs[3r+2] keys from d_src + runs[3r]
+ * to d_dst + runs[3r+1] (runs: host array) -- the all-to-all's source-major
+ * receive buffer to bucket-major order. */
+int lsort_cuda_copy_runs(lsort_ctx* ctx, const uint64_t* d_src, uint64_t* d_dst, const uint64_t* runs,
+                         uint64_t nruns);
 /* Decode encoded keys to float64 in place (after a distributed sort). */
 int lsort_cuda_decode_inplace(lsort_ctx* ctx, uint64_t* d_keys, uint64_t n);
 

@@ -233,6 +233,33 @@ class Context:
         _check(self, rc)
         return stats.as_dict()
 
+    def sort_buckets(self, d_keys, P: np.ndarray, submodels: int, b_lo: int, b_hi: int, sizes, d_sorted_sample=None,
+                     cfg: SortConfig | None = None, encoded_f64: bool = False) -> dict:
+        """lsort_cuda_sort_buckets: keys already grouped by the model's buckets
+        [b_lo, b_hi) (sizes per bucket, in order); small buckets sorted in place,
+        the rest recursed from level 1. encoded_f64: decode in the final stores."""
+        self._sync_stream()
+        h, e = unpack_rmi(P, submodels)
+        sz = np.ascontiguousarray(np.asarray(sizes, dtype=np.uint64))
+        stats = N.lsort_stats()
+        c = (cfg or SortConfig()).to_c()
+        kind = N.KEY_ENC_F64 if encoded_f64 else N.KEY_U64
+        sp = C.c_void_p(d_sorted_sample.data_ptr()) if d_sorted_sample is not None else None
+        sn = d_sorted_sample.numel() if d_sorted_sample is not None else 0
+        rc = N.lib().lsort_cuda_sort_buckets(self._h, C.c_void_p(d_keys.data_ptr()), d_keys.numel(), kind, C.byref(c),
+                                             C.byref(h), e.ctypes.data_as(C.c_void_p), b_lo, b_hi,
+                                             sz.ctypes.data_as(C.c_void_p), sp, sn, C.byref(stats))
+        _check(self, rc)
+        return stats.as_dict()
+
+    def copy_runs(self, d_src, d_dst, runs: np.ndarray):
+        """lsort_cuda_copy_runs: d_dst[dst_off:+len] = d_src[src_off:+len] per run row."""
+        self._sync_stream()
+        r = np.ascontiguousarray(np.asarray(runs, dtype=np.uint64).reshape(-1, 3))
+        rc = N.lib().lsort_cuda_copy_runs(self._h, C.c_void_p(d_src.data_ptr()), C.c_void_p(d_dst.data_ptr()),
+                                          r.ctypes.data_as(C.c_void_p), r.shape[0])
+        _check(self, rc)
+
     # -- unit entry points (parity tests) --------------------------------------
     def rmi_train(self, d_sorted_sample, submodels: int):
         """Rmi::train + enforce_monotonic on a sorted device sample -> packed P."""

@@ -75,6 +75,7 @@ EXPORTS = [
     "lsort_cuda_block_sort", "lsort_cuda_verify", "lsort_gen_keys", "lsort_cuda_dist_sample",
     "lsort_cuda_dist_train", "lsort_cuda_dist_histogram", "lsort_cuda_dist_partition",
     "lsort_cuda_decode_inplace", "lsort_cuda_learned_pivots", "lsort_cuda_pivot_quality", "lsort_cuda_eta",
+    "lsort_cuda_sort_buckets", "lsort_cuda_copy_runs",
 ]
 
 _lib = None
@@ -135,6 +136,11 @@ def lib():
     L.lsort_cuda_pivot_quality.restype = i32
     L.lsort_cuda_pivot_quality.argtypes = [vp, vp, u64, i32, vp, u32, u32, P(f64), vp]
     L.lsort_cuda_eta.restype = i32
+    L.lsort_cuda_sort_buckets.restype = i32
+    L.lsort_cuda_sort_buckets.argtypes = [vp, vp, u64, i32, P(lsort_cfg), P(lsort_rmi_header), vp, u32, u32, vp, vp,
+                                          u64, P(lsort_stats)]
+    L.lsort_cuda_copy_runs.restype = i32
+    L.lsort_cuda_copy_runs.argtypes = [vp, vp, vp, vp, u64]
     L.lsort_cuda_eta.argtypes = [vp, vp, u64, i32, u64, P(f64)]
     L.lsort_gen_keys.restype = i32
     L.lsort_gen_keys.argtypes = [i32, u64, u64, u64, u64, vp, i32]

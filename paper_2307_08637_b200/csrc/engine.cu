@@ -492,8 +492,11 @@ struct Engine {
     // in_encoded: the keys are already encoded u64 (keys.hpp:36-42); with f64
     // the sorted result is decoded to float64 in place (the decode fused into
     // the final stores -- used for the keys a multi-GPU exchange delivers)
+    // start (nullable): the keys are already partitioned into these segments
+    // (contiguous, each > the base-case capacity); the recursion starts at
+    // level 1 with them instead of sampling a root model over all n keys.
     void sort(void* keys, uint64_t n, bool f64, lsort_stats* stats, bool in_encoded = false,
-              const Forward* fw = nullptr) {
+              const Forward* fw = nullptr, const std::vector<SegPlan>* start = nullptr) {
         if (n < 2) {
             if (n == 1 && f64 && in_encoded) {
                 launch_decode((uint64_t*)keys, n, st);
@@ -508,7 +511,7 @@ struct Engine {
         CU(cudaMemsetAsync(&dctrl->nan_index, 0xff, 8, st));
         Ctrl* hc = C->hctrl.as<Ctrl>();
         const uint32_t cap = cfg.base_case_capacity;
-        if (n <= cap) {
+        if (n <= cap && !start) {
             launch_small_sort(keys, n, f64 && !in_encoded, dctrl, st);
             launched();
             if (f64 && in_encoded) {
@@ -525,10 +528,11 @@ struct Engine {
         const uint32_t depth_cap =
             (uint32_t)std::ceil(std::log2((double)n) / std::log2((double)cfg.tree_bucket_count)) + 4;
         std::vector<SegPlan> segs{{0, n, 0, 0}};
+        if (start) segs = *start;
         void* src = keys;
-        bool src_f64 = f64 && !in_encoded;
+        bool src_f64 = f64 && !in_encoded && !start;
         uint64_t* dst = C->scratch.as<uint64_t>();
-        uint32_t level = 0;
+        uint32_t level = start ? 1 : 0;
         DevCfg dc = dev_cfg(cfg);
         while (!segs.empty()) {
             const uint32_t ns = (uint32_t)segs.size();
@@ -1704,6 +1708,125 @@ int lsort_cuda_sort_forward(lsort_ctx* C, void* d_keys, uint64_t n, int key_kind
     return LSORT_OK;
 }
 
+int lsort_cuda_copy_runs(lsort_ctx* C, const uint64_t* d_src, uint64_t* d_dst, const uint64_t* runs,
+                         uint64_t nruns) {
+    if (!C || (nruns && (!runs || !d_src || !d_dst))) return fail(C, {LSORT_EINVAL, "copy_runs: bad arguments"});
+    try {
+        CU(cudaSetDevice(C->device));
+        if (!nruns) return LSORT_OK;
+        if (!C->piv.ensure(24 * nruns) || !C->hmodel.ensure(24 * nruns)) throw LsortError{LSORT_ENOMEM, "runs"};
+        std::memcpy(C->hmodel.p, runs, 24 * nruns);
+        CU(cudaMemcpyAsync(C->piv.p, C->hmodel.p, 24 * nruns, cudaMemcpyHostToDevice, C->stream));
+        launch_copy_runs(d_src, d_dst, C->piv.as<uint64_t>(), nruns, C->stream);
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+    } catch (const LsortError& e) {
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_sort_buckets(lsort_ctx* C, void* d_keys, uint64_t n, int key_kind, const lsort_cfg* cfgp,
+                            const lsort_rmi_header* h, const lsort_rmi_entry* e, uint32_t b_lo, uint32_t b_hi,
+                            const uint64_t* bucket_sizes, const uint64_t* d_sorted_sample, uint64_t sample_n,
+                            lsort_stats* stats) {
+    if (!C || !h || !e) return LSORT_EINVAL;
+    C->err.clear();
+    const uint32_t B = h->submodels;
+    if (B < 2 || B > LSORT_MAX_RMI || b_lo > b_hi || b_hi > B || (n && (!d_keys || !bucket_sizes)))
+        return fail(C, {LSORT_EINVAL, "sort_buckets: bad model / bucket range"});
+    if (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_ENC_F64)
+        return fail(C, {LSORT_EINVAL, "sort_buckets: keys must be u64 or encoded f64"});
+    uint64_t tot = 0;
+    for (uint32_t j = 0; j < b_hi - b_lo; ++j) tot += bucket_sizes[j];
+    if (tot != n) return fail(C, {LSORT_EINVAL, "sort_buckets: bucket sizes do not add up to n"});
+    lsort_cfg cfg = cfg_or_default(cfgp);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    try {
+        validate_cfg(cfg);
+        CU(cudaSetDevice(C->device));
+        if (n == 0) return LSORT_OK;
+        const bool f64 = key_kind == LSORT_KEY_ENC_F64;
+        const uint32_t nb = b_hi - b_lo, cap = cfg.base_case_capacity;
+        // children train on their slice of the sorted global sample (GPU policy)
+        std::vector<uint32_t> offs;
+        Forward fw;
+        const bool slices = d_sorted_sample && sample_n >= 2 && !(cfg.flags & LSORT_FLAG_STRICT_POLICY);
+        if (slices) {
+            upload_learned(C, h, e, B, 0.0, 1.0);
+            if (!C->fwd_slices.ensure(4 * ((size_t)B + 2))) throw LsortError{LSORT_ENOMEM, "slices"};
+            launch_sample_slices(d_sorted_sample, sample_n, C->models.as<uint8_t>(), C->fwd_slices.as<uint32_t>(), B,
+                                 nullptr, C->stream);
+            offs.resize(B + 1);
+            CU(cudaMemcpyAsync(offs.data(), C->fwd_slices.p, 4 * ((size_t)B + 1), cudaMemcpyDeviceToHost, C->stream));
+            CU(cudaStreamSynchronize(C->stream));
+            fw.psample = d_sorted_sample;
+        }
+        // buckets within the base-case capacity are sorted in place right away;
+        // the others start the recursion at level 1
+        std::vector<SegPlan> big;
+        std::vector<BaseItem> small[3];
+        uint64_t at = 0, small_keys = 0;
+        const uint32_t cls_cap[3] = {std::min<uint32_t>(kWarpBaseCap, cap), std::min<uint32_t>(4096, cap), cap};
+        for (uint32_t j = 0; j < nb; ++j) {
+            const uint64_t len = bucket_sizes[j];
+            if (len > cap) {
+                uint64_t ps = 0;
+                if (slices) {
+                    const uint32_t o = offs[b_lo + j], l = offs[b_lo + j + 1] - o;
+                    if (l >= kMinSlice) ps = (uint64_t)o << 24 | std::min<uint32_t>(l, 0xffffffu);
+                }
+                big.push_back({at, len, 1, 0, ps});
+            } else if (len > 1 || (len == 1 && f64)) {
+                const int c = len <= cls_cap[0] ? 0 : (len <= cls_cap[1] ? 1 : 2);
+                small[c].push_back(BaseItem{at, len});
+                small_keys += len;
+            }
+            at += len;
+        }
+        C->launches = 0;
+        if (small_keys) {
+            size_t maxl = 1;
+            for (auto& v : small) maxl = std::max(maxl, v.size());
+            if (!C->ctrl.ensure(sizeof(Ctrl)) || !C->hctrl.ensure(sizeof(Ctrl)) ||
+                !C->base[0].ensure(maxl * sizeof(BaseItem)) || !C->base[1].ensure(maxl * sizeof(BaseItem)) ||
+                !C->base[2].ensure(maxl * sizeof(BaseItem)))
+                throw LsortError{LSORT_ENOMEM, "bucket base cases"};
+            Ctrl* hc = C->hctrl.as<Ctrl>();
+            std::memset(hc, 0, sizeof(Ctrl));
+            hc->nan_index = ~0ull;
+            LevelParams p{};
+            p.ctrl = C->ctrl.as<Ctrl>();
+            for (int c = 0; c < 3; ++c) {
+                hc->n_base[c] = (unsigned)small[c].size();
+                if (!small[c].empty())
+                    CU(cudaMemcpyAsync(C->base[c].p, small[c].data(), small[c].size() * sizeof(BaseItem),
+                                       cudaMemcpyHostToDevice, C->stream));
+                p.base[c] = C->base[c].as<BaseItem>();
+            }
+            p.list_cap = (uint32_t)maxl;
+            CU(cudaMemcpyAsync(p.ctrl, hc, sizeof(Ctrl), cudaMemcpyHostToDevice, C->stream));
+            // in place: every base-case CTA holds its whole segment before it stores
+            launch_base_cases(p, (const uint64_t*)d_keys, d_keys, f64, C->stream);
+            C->launches += 3;
+            CU(cudaStreamSynchronize(C->stream));  // the host control block is reused by the engine
+            if (stats) { stats->base_case_keys += small_keys; stats->base_segments += small[0].size() + small[1].size() + small[2].size(); }
+        }
+        if (!big.empty()) {
+            Engine E(C, cfg);
+            E.sort(d_keys, n, f64, stats, f64, slices ? &fw : nullptr, &big);
+        }
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+        if (stats) stats->kernel_launches = C->launches;
+    } catch (const LsortError& e2) {
+        cudaStreamSynchronize(C->stream);
+        cudaGetLastError();
+        return fail(C, e2);
+    }
+    return LSORT_OK;
+}
+
 int lsort_cuda_dist_histogram(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, const lsort_rmi_header* h,
                               const lsort_rmi_entry* e, uint64_t* d_hist) {
     if (!C || !h || !e || !d_hist || h->submodels < 2 || h->submodels > LSORT_MAX_RMI) return LSORT_EINVAL;
@@ -1732,7 +1855,7 @@ int lsort_cuda_dist_histogram(lsort_ctx* C, const void* d_keys, uint64_t n, int 
 int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int key_kind, const lsort_rmi_header* h,
                               const lsort_rmi_entry* e, const uint32_t* bucket_bounds, uint32_t nranks,
                               uint64_t* d_out, uint64_t* send_counts) {
-    if (!C || !h || !e || !bucket_bounds || nranks == 0 || nranks > 1024 || h->submodels < 2 ||
+    if (!C || !h || !e || !bucket_bounds || nranks == 0 || nranks > kMaxNB || h->submodels < 2 ||
         h->submodels > LSORT_MAX_RMI)
         return LSORT_EINVAL;
     try {
@@ -1771,7 +1894,10 @@ int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int 
         CU(cudaMemcpyAsync(dcur, cur.data(), 8 * (size_t)nranks, cudaMemcpyHostToDevice, C->stream));
         LevelParams p = dist_level(C, d_keys, n, B, dcur, d_out);
         const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(p.ntiles, (uint64_t)num_sms() * kPartPerSM));
-        if (n) launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, grid, C->stream);
+        bool identity = nranks == B;  // one "rank" per bucket: the bucket-major partition
+        for (uint32_t b = 0; identity && b < B; ++b) identity = map[b] == b;
+        if (n && identity) launch_scatter(p, key_kind == LSORT_KEY_F64, B, grid, C->stream);  // no map lookups
+        else if (n) launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, grid, C->stream);
         CU(cudaStreamSynchronize(C->stream));
         CU(cudaGetLastError());
     } catch (const LsortError& er) {

@@ -857,6 +857,8 @@ void partition_init(int optin) {
     allow_smem(k_scatter<true, false, kMaxNB>, optin);
     allow_smem(k_scatter<false, false, kMaxNB>, optin);
     allow_smem(k_scatter<true, true, 1024>, optin);
+    allow_smem(k_scatter<true, true, kMaxNB>, optin);
+    allow_smem(k_scatter<false, true, kMaxNB>, optin);
     allow_smem(k_scatter<false, true, 1024>, optin);
     allow_smem(k_scan_children<128>, optin);
     allow_smem(k_scan_children<512>, optin);
@@ -908,9 +910,15 @@ void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid,
 
 void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,
                            cudaStream_t st) {
-    constexpr size_t sm = sizeof(ScatterSmem<1024>);
-    if (in_f64) pdl(k_scatter<true, true, 1024>, grid, kPNT, sm, st, p, map, nmapped);
-    else pdl(k_scatter<false, true, 1024>, grid, kPNT, sm, st, p, map, nmapped);
+    if (nmapped <= 1024) {
+        constexpr size_t sm = sizeof(ScatterSmem<1024>);
+        if (in_f64) pdl(k_scatter<true, true, 1024>, grid, kPNT, sm, st, p, map, nmapped);
+        else pdl(k_scatter<false, true, 1024>, grid, kPNT, sm, st, p, map, nmapped);
+    } else {  // bucket-major distributed partition of a 2048-bucket global model
+        constexpr size_t sm = sizeof(ScatterSmem<kMaxNB>);
+        if (in_f64) pdl(k_scatter<true, true, kMaxNB>, grid, kPNT, sm, st, p, map, nmapped);
+        else pdl(k_scatter<false, true, kMaxNB>, grid, kPNT, sm, st, p, map, nmapped);
+    }
 }
 
 }  // namespace lsort_dev

@@ -68,6 +68,35 @@ def sample_shares(n_local: list[int], s_total: int) -> list[int]:
     return [min(s, n) if n else 0 for s, n in zip(shares, n_local)]
 
 
+def bucket_exchange_plan(hists: np.ndarray, bounds: np.ndarray, rank: int):
+    """Host plan of the bucket-major exchange. hists: (world, B) per-source
+    bucket counts (the all-gathered local histograms); bounds: rank bucket
+    ranges. Returns (send counts per destination, receive counts per source,
+    runs (src_off, dst_off, len) that turn the source-major receive buffer --
+    source s's keys of buckets [lo, hi), bucket-major -- into bucket-major
+    order with the sources in rank order inside each bucket, per-bucket sizes)."""
+    hists = np.asarray(hists, dtype=np.int64)
+    world = hists.shape[0]
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    send = [int(hists[rank, bounds[r]:bounds[r + 1]].sum()) for r in range(world)]
+    mine = hists[:, lo:hi]
+    recv = [int(mine[s].sum()) for s in range(world)]
+    sizes = mine.sum(axis=0)
+    bstart = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    before = np.zeros(hi - lo, np.int64)  # keys of the same bucket from lower ranks
+    runs = []
+    src_base = 0
+    for s in range(world):  # vectorised over the buckets
+        h = mine[s]
+        src_off = src_base + np.concatenate([[0], np.cumsum(h)[:-1]]).astype(np.int64)
+        nz = h > 0
+        runs.append(np.stack([src_off[nz], (bstart + before)[nz], h[nz]], axis=1))
+        before += h
+        src_base += int(h.sum())
+    runs = np.concatenate(runs, axis=0) if runs else np.zeros((0, 3), np.int64)
+    return send, recv, runs.astype(np.uint64).reshape(-1, 3), sizes.astype(np.uint64)
+
+
 class NativeOps:
     """Device steps through the C-ABI (liblsort_cuda.so)."""
 
@@ -145,6 +174,19 @@ class NativeOps:
                 return self.ctx.sort_forward(keys_u64, P, buckets, b_lo, b_hi, sample, cfg, encoded_f64=to_f64)
         return self.ctx.sort(keys_u64, cfg, encoded_f64=to_f64)
 
+    bucket_major = True  # partition_buckets / copy_runs / sort_buckets below
+
+    def partition_buckets(self, keys, P, buckets: int):
+        """Level-0 scatter by bucket (identity bucket -> "rank" map): bucket-major
+        output and per-bucket counts (reuses the histogram's ids)."""
+        return self.partition(keys, P, buckets, np.arange(buckets + 1, dtype=np.uint32))
+
+    def copy_runs(self, src, dst, runs):
+        self.ctx.copy_runs(src, dst, runs)
+
+    def sort_buckets(self, keys_u64, P, buckets, b_lo, b_hi, sizes, sample, cfg, to_f64=False):
+        return self.ctx.sort_buckets(keys_u64, P, buckets, b_lo, b_hi, sizes, sample, cfg, encoded_f64=to_f64)
+
     def decode(self, keys_u64):
         import ctypes as C
         from . import _native as N
@@ -172,7 +214,7 @@ class DistSorter:
     """Globally sort per-rank shards. ``keys``: contiguous tensor (float64 or
     int64/uint64 bits) on this rank's device (or CPU with CPU ops)."""
 
-    def __init__(self, ctx=None, cfg=None, group=None, ops=None, buckets: int = 2048):
+    def __init__(self, ctx=None, cfg=None, group=None, ops=None, buckets: int = 1024):
         from . import SortConfig
         self.cfg = cfg or SortConfig()
         self.group = group
@@ -224,6 +266,8 @@ class DistSorter:
         # ---- 3. global histogram
         hist = self.ops.histogram(keys, P, self.buckets).to(torch.int64)
         mark("histogram")
+        if getattr(self.ops, "bucket_major", False):
+            return self._sort_bucket_major(keys, P, hist, sample, s_total, n_local, is_f64, mark, marks, trace)
         dist.all_reduce(hist, group=g)
         # ---- 4. rank boundaries
         bounds = rank_bounds(hist.cpu().numpy(), world)
@@ -250,6 +294,56 @@ class DistSorter:
             local = self.ops.local_sort(out, lcfg, forward=fwd) if out.numel() else {}
         else:
             local = self.ops.local_sort(out, lcfg) if out.numel() else {}
+        mark("local sort")
+        if fused:
+            result = out.view(torch.float64)
+        else:
+            result = self.ops.decode(out) if is_f64 else out
+        mark("decode")
+        if trace and rank == 0:
+            print("[dist] " + " ".join(f"{marks[i][0]} {1e3 * (marks[i][1] - marks[i - 1][1]):.3f}"
+                                     for i in range(1, len(marks))) + " ms", flush=True)
+        stats = DistStats(n_in=n_local, n_out=int(out.numel()), sample=s_total, send_counts=tuple(send),
+                          bounds=tuple(int(b) for b in bounds), local=local)
+        return result, stats.__dict__
+
+    def _sort_bucket_major(self, keys, P, hist, sample, s_total, n_local, is_f64, mark, marks, trace):
+        """Steps 3-6 with a bucket-major exchange: every rank scatters its keys by
+        bucket (not just by destination), the per-rank histograms are all-gathered
+        (instead of all-reduced) so each rank knows where every (source, bucket)
+        piece lands, the all-to-all's source-major receive buffer is regrouped by
+        bucket with one run-gather copy (nothing to do at one rank), and the local
+        sort starts at level 1 with the rank's buckets as its segments -- no second
+        level-0 classify + scatter."""
+        import torch
+        import torch.distributed as dist
+        g = self.group
+        rank, world = dist.get_rank(g), dist.get_world_size(g)
+        dev = keys.device
+        hists = [torch.empty_like(hist) for _ in range(world)]
+        dist.all_gather(hists, hist, group=g)
+        H = torch.stack(hists).cpu().numpy()
+        bounds = rank_bounds(H.sum(axis=0), world)
+        mark("allreduce+bounds")
+        part, _ = self.ops.partition_buckets(keys, P, self.buckets)
+        mark("partition")
+        send, recv, runs, sizes = bucket_exchange_plan(H, bounds, rank)
+        if world == 1:  # nothing to exchange: the partition is already bucket-major
+            out = part
+        else:
+            out = torch.empty(max(sum(recv), 1), dtype=torch.int64, device=dev)[: sum(recv)]
+            dist.all_to_all_single(out, part, output_split_sizes=recv, input_split_sizes=send, group=g)
+        if world > 1 and runs.shape[0] > 1:
+            grouped = torch.empty_like(out)
+            self.ops.copy_runs(out, grouped, runs)
+            out = grouped
+        mark("exchange")
+        from . import SortConfig
+        lcfg = SortConfig(**{**self.cfg.__dict__})
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        fused = is_f64 and getattr(self.ops, "fused_decode", False)
+        local = (self.ops.sort_buckets(out, P, self.buckets, lo, hi, sizes, sample, lcfg, to_f64=fused)
+                 if out.numel() else {})
         mark("local sort")
         if fused:
             result = out.view(torch.float64)

@@ -36,6 +36,33 @@ class CpuOps:
         counts = np.bincount(dest, minlength=bounds.size - 1)
         return torch.from_numpy(k[order].view(np.int64).copy()), [int(c) for c in counts]
 
+    bucket_major = True
+
+    def partition_buckets(self, keys, P, B):
+        k = _enc(keys)
+        ids = O.learned_bucket(P, B, B, k)
+        order = np.argsort(ids, kind="stable")
+        return torch.from_numpy(k[order].view(np.int64).copy()), [int(c) for c in np.bincount(ids, minlength=B)]
+
+    def copy_runs(self, src, dst, runs):
+        s, d = src.numpy(), dst.numpy()
+        for so, do, ln in np.asarray(runs, dtype=np.int64).reshape(-1, 3):
+            d[do:do + ln] = s[so:so + ln]
+
+    def sort_buckets(self, keys_u64, P, B, b_lo, b_hi, sizes, sample, cfg, to_f64=False):
+        """Sorts each bucket segment on its own: the output is globally sorted
+        only if the exchange put every key into its bucket's segment."""
+        a = keys_u64.numpy().view(np.uint64)
+        at = 0
+        for j, ln in enumerate(np.asarray(sizes, dtype=np.int64)):
+            seg = a[at:at + ln]
+            if ln:  # every key of the segment must carry bucket b_lo + j
+                assert np.all(O.learned_bucket(P, B, B, seg) == b_lo + j)
+            seg.sort()
+            at += ln
+        assert at == a.size
+        return {}
+
     def local_sort(self, keys_u64, cfg):
         a = keys_u64.numpy().view(np.uint64)
         a.sort()
@@ -43,3 +70,8 @@ class CpuOps:
 
     def decode(self, keys_u64):
         return torch.from_numpy(O.decode(keys_u64.numpy().view(np.uint64)))
+
+
+class CpuOpsRankMajor(CpuOps):
+    """The destination-major exchange + whole local sort (dist.py steps 3-6)."""
+    bucket_major = False

@@ -72,3 +72,32 @@ def test_dist_partition_destinations(pg):
         seg = got[off:off + counts[r]]
         assert np.array_equal(np.sort(seg), np.sort(keys[dest == r]))
         off += counts[r]
+
+
+@pytest.mark.parametrize("dist_name,seed,n", [("normal", 7, 2_000_000), ("lognormal2", 19, 1_000_000),
+                                              ("uniform", 42, 3_000_000)])
+def test_sort_buckets_from_level_one(dist_name, seed, n):
+    """lsort_cuda_sort_buckets on a bucket-major level-0 partition (identity
+    bucket map) of a sub-range [b_lo, b_hi) of the buckets: small buckets in
+    place, the rest from level 1, decode fused -- equals the sorted keys."""
+    from paper_2307_08637_b200.dist import NativeOps
+    x = O.generate(dist_name, n, seed)
+    keys = O.encode(x)
+    ctx = L.Context(0)
+    ops = NativeOps(ctx)
+    t = torch.from_numpy(x).cuda()
+    sample = torch.from_numpy(np.sort(keys[::100]).view(np.int64)).cuda()
+    B = 512
+    P = ops.train(sample.clone(), B)
+    hist = ops.histogram(t, P, B).cpu().numpy()
+    part, counts = ops.partition_buckets(t, P, B)
+    assert counts == [int(c) for c in hist]
+    starts = np.concatenate([[0], np.cumsum(hist)])
+    for b_lo, b_hi in [(0, B), (100, 300), (B - 7, B)]:
+        seg = part[starts[b_lo]:starts[b_hi]].clone()
+        st = ops.sort_buckets(seg, P, B, b_lo, b_hi, hist[b_lo:b_hi], sample, L.SortConfig(), to_f64=True)
+        got = seg.view(torch.float64).cpu().numpy()
+        ids = O.learned_bucket(P, B, B, keys)
+        exp = O.decode(np.sort(keys[(ids >= b_lo) & (ids < b_hi)]))
+        assert np.array_equal(got.view(np.uint64), exp.view(np.uint64)), (b_lo, b_hi)
+        assert st["levels"] <= 2
