@@ -281,7 +281,8 @@ int lsort_cuda_dist_histogram(lsort_ctx* ctx, const void* d_keys, uint64_t n, in
 int lsort_cuda_dist_partition(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,
                               const lsort_rmi_header* h, const lsort_rmi_entry* entries,
                               const uint32_t* bucket_bounds, uint32_t nranks, uint64_t* d_out,
-                              uint64_t* send_counts);
+                              uint64_t* send_counts /* nullable with the identity map: the
+                                                       cursors are then scanned on the device */);
 /* Local sort of a rank's received keys when they are already grouped by the
  * global model's buckets [b_lo, b_hi) (bucket_sizes[b - b_lo] keys each, in
  * bucket order): buckets within the base-case capacity are sorted in place, the

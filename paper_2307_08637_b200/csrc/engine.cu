@@ -1879,23 +1879,28 @@ int lsort_cuda_dist_partition(lsort_ctx* C, const void* d_keys, uint64_t n, int 
         } else {
             dist_hist_ids(C, d_keys, n, key_kind, h, e, dhist);
         }
-        std::vector<uint64_t> hist(B);
-        CU(cudaMemcpyAsync(hist.data(), dhist, 8 * (size_t)B, cudaMemcpyDeviceToHost, C->stream));
-        CU(cudaStreamSynchronize(C->stream));
-        std::vector<uint64_t> cur(nranks, 0);
-        for (uint32_t b = 0; b < B; ++b) cur[map[b]] += hist[b];
-        uint64_t acc = 0;
-        for (uint32_t r = 0; r < nranks; ++r) {
-            send_counts[r] = cur[r];
-            uint64_t c = cur[r];
-            cur[r] = acc;
-            acc += c;
-        }
-        CU(cudaMemcpyAsync(dcur, cur.data(), 8 * (size_t)nranks, cudaMemcpyHostToDevice, C->stream));
-        LevelParams p = dist_level(C, d_keys, n, B, dcur, d_out);
-        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(p.ntiles, (uint64_t)num_sms() * kPartPerSM));
         bool identity = nranks == B;  // one "rank" per bucket: the bucket-major partition
         for (uint32_t b = 0; identity && b < B; ++b) identity = map[b] == b;
+        if (identity && !send_counts) {
+            // cursors = exclusive scan of the histogram, on the device: no host round trip
+            launch_excl_scan_u64(dhist, dcur, B, C->stream);
+        } else {
+            std::vector<uint64_t> hist(B);
+            CU(cudaMemcpyAsync(hist.data(), dhist, 8 * (size_t)B, cudaMemcpyDeviceToHost, C->stream));
+            CU(cudaStreamSynchronize(C->stream));
+            std::vector<uint64_t> cur(nranks, 0);
+            for (uint32_t b = 0; b < B; ++b) cur[map[b]] += hist[b];
+            uint64_t acc = 0;
+            for (uint32_t r = 0; r < nranks; ++r) {
+                if (send_counts) send_counts[r] = cur[r];
+                uint64_t c = cur[r];
+                cur[r] = acc;
+                acc += c;
+            }
+            CU(cudaMemcpyAsync(dcur, cur.data(), 8 * (size_t)nranks, cudaMemcpyHostToDevice, C->stream));
+        }
+        LevelParams p = dist_level(C, d_keys, n, B, dcur, d_out);
+        const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(p.ntiles, (uint64_t)num_sms() * kPartPerSM));
         if (n && identity) launch_scatter(p, key_kind == LSORT_KEY_F64, B, grid, C->stream);  // no map lookups
         else if (n) launch_scatter_mapped(p, key_kind == LSORT_KEY_F64, dmap, nranks, grid, C->stream);
         CU(cudaStreamSynchronize(C->stream));

@@ -169,6 +169,8 @@ void launch_verify(const void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream
 // Alg. 4 per-cell maxima (gmax / ghit zeroed by the caller, nbuckets cells)
 void launch_learned_pivots(const uint8_t* model, const void* keys, uint64_t n, int in_f64, unsigned long long* gmax,
                            unsigned int* ghit, int payload, cudaStream_t st);
+// out[i] = sum(in[0, i)), n <= kMaxNB, one CTA
+void launch_excl_scan_u64(const unsigned long long* in, unsigned long long* out, uint32_t n, cudaStream_t st);
 // dst[dst_off + i] = src[src_off + i] for every run (src_off, dst_off, len) in runs (device)
 void launch_copy_runs(const uint64_t* src, uint64_t* dst, const uint64_t* runs, uint64_t nruns, cudaStream_t st);
 // ranks[i] = #keys <= pivots[i] (pivots encoded when f64)

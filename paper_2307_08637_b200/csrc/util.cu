@@ -82,6 +82,19 @@ __global__ void k_rank_le(const void* sorted, uint64_t n, const uint64_t* pivots
     ranks[i] = lo;
 }
 
+// out[i] = sum(in[0, i)) for i < n (one CTA; the partition cursors of a
+// bucket-major distributed partition, without a host round trip)
+__global__ void __launch_bounds__(1024) k_excl_scan_u64(const unsigned long long* in, unsigned long long* out,
+                                                        uint32_t n) {
+    griddep_wait();
+    __shared__ uint64_t a[kMaxNB];
+    __shared__ uint64_t wsum[1024 / 32 + 1];
+    for (uint32_t i = threadIdx.x; i < n; i += 1024) a[i] = in[i];
+    __syncthreads();
+    block_exclusive_scan_u64<1024>(a, n, wsum);
+    for (uint32_t i = threadIdx.x; i < n; i += 1024) out[i] = a[i];
+}
+
 // Run gather: run r copies len keys from src + src_off to dst + dst_off
 // (runs[3r..3r+2]); one CTA per run, grid-stride over the runs.
 __global__ void __launch_bounds__(256) k_copy_runs(const uint64_t* src, uint64_t* dst, const uint64_t* runs,
@@ -174,6 +187,10 @@ void launch_learned_pivots(const uint8_t* model, const void* keys, uint64_t n, i
     const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms() * 4);
     if (in_f64) pdl(k_learned_pivots<true>, grid, 256, sm, st, model, keys, n, gmax, ghit);
     else pdl(k_learned_pivots<false>, grid, 256, sm, st, model, keys, n, gmax, ghit);
+}
+
+void launch_excl_scan_u64(const unsigned long long* in, unsigned long long* out, uint32_t n, cudaStream_t st) {
+    pdl(k_excl_scan_u64, 1, 1024, 0, st, in, out, n);
 }
 
 void launch_copy_runs(const uint64_t* src, uint64_t* dst, const uint64_t* runs, uint64_t nruns, cudaStream_t st) {

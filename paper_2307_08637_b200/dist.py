@@ -178,8 +178,22 @@ class NativeOps:
 
     def partition_buckets(self, keys, P, buckets: int):
         """Level-0 scatter by bucket (identity bucket -> "rank" map): bucket-major
-        output and per-bucket counts (reuses the histogram's ids)."""
-        return self.partition(keys, P, buckets, np.arange(buckets + 1, dtype=np.uint32))
+        output (reuses the histogram's ids; cursors scanned on the device, so no
+        counts come back -- the caller has the histograms)."""
+        import ctypes as C
+        import torch
+        from . import _native as N
+        from . import _key_kind_of, unpack_rmi
+        h, e = unpack_rmi(P, buckets)
+        out = torch.empty(max(keys.numel(), 1), dtype=torch.int64, device=keys.device)
+        b = np.arange(buckets + 1, dtype=np.uint32)
+        self.ctx._sync_stream()
+        rc = N.lib().lsort_cuda_dist_partition(self.ctx._h, C.c_void_p(keys.data_ptr()), keys.numel(),
+                                               _key_kind_of(keys), C.byref(h), e.ctypes.data_as(C.c_void_p),
+                                               b.ctypes.data_as(C.c_void_p), buckets, C.c_void_p(out.data_ptr()),
+                                               None)
+        self._check(rc)
+        return out[: keys.numel()], None
 
     def copy_runs(self, src, dst, runs):
         self.ctx.copy_runs(src, dst, runs)
