@@ -100,3 +100,45 @@ def test_sort_buckets_from_level_one(dist_name, seed, n):
         exp = O.decode(np.sort(keys[(ids >= b_lo) & (ids < b_hi)]))
         assert np.array_equal(got.view(np.uint64), exp.view(np.uint64)), (b_lo, b_hi)
         assert st["levels"] <= 2
+
+
+def test_sort_buckets_edge_cases():
+    """Empty buckets, only small buckets (no level 1), one huge bucket, u64 keys,
+    zero keys; copy_runs with no runs and with overlapping-free reversals."""
+    from paper_2307_08637_b200.dist import NativeOps
+    ctx = L.Context(0)
+    ops = NativeOps(ctx)
+    rng = np.random.default_rng(9)
+    keys = np.sort(rng.integers(0, 2**63, 600_000, dtype=np.uint64))
+    sample = torch.from_numpy(keys[::60].copy().view(np.int64)).cuda()
+    B = 256
+    P = ops.train(sample.clone(), B)
+    ids = O.learned_bucket(P, B, B, keys)
+    for sizes_kind in ("real", "empties"):
+        k = rng.permutation(keys)
+        kid = O.learned_bucket(P, B, B, k)
+        if sizes_kind == "empties":  # drop every other bucket's keys
+            k = k[kid % 2 == 0]
+            kid = kid[kid % 2 == 0]
+        order = np.argsort(kid, kind="stable")
+        part = torch.from_numpy(k[order].view(np.int64)).cuda()
+        sizes = np.bincount(kid, minlength=B)
+        ops.sort_buckets(part, P, B, 0, B, sizes, sample, L.SortConfig())
+        assert np.array_equal(part.cpu().numpy().view(np.uint64), np.sort(k)), sizes_kind
+    # one huge bucket of random keys (the model is not asked to be right)
+    k = rng.integers(0, 2**64 - 1, 300_000, dtype=np.uint64, endpoint=True)
+    t = torch.from_numpy(k.view(np.int64)).cuda()
+    ops.sort_buckets(t, P, B, 3, 4, np.array([k.size]), None, L.SortConfig())
+    assert np.array_equal(t.cpu().numpy().view(np.uint64), np.sort(k))
+    # zero keys
+    ops.sort_buckets(torch.empty(0, dtype=torch.int64, device="cuda"), P, B, 0, B, np.zeros(B, np.uint64), sample,
+                     L.SortConfig())
+    with pytest.raises(ValueError):  # sizes must add up to n
+        ops.sort_buckets(t, P, B, 0, 2, np.array([1, 2]), None, L.SortConfig())
+    # copy_runs: none, and pieces swapped
+    src = torch.arange(10, dtype=torch.int64, device="cuda")
+    dst = torch.zeros(10, dtype=torch.int64, device="cuda")
+    ctx.copy_runs(src, dst, np.zeros((0, 3), np.uint64))
+    assert int(dst.sum()) == 0
+    ctx.copy_runs(src, dst, np.array([[0, 6, 4], [4, 0, 6]], np.uint64))
+    assert dst.cpu().tolist() == [4, 5, 6, 7, 8, 9, 0, 1, 2, 3]
