@@ -407,7 +407,7 @@ __device__ void build_radix_model(const SegDesc& sd, const void* src, bool f64, 
 // Draw sample draws [j0, j0+cnt) of the segment stream into shared A, sort.
 template <bool IN_F64, class MC>
 __device__ void sample_sorted(const SegDesc& sd, const void* src, uint64_t seed, uint32_t j0, uint32_t cnt,
-                              typename MC::Smem& S) {
+                              typename MC::Smem& S, bool eq = false) {
     constexpr int NT = sizeof(S.red64) / 8 * 32;
     // random gather: 8 independent loads in flight per thread (a rolled loop
     // waits one DRAM latency per key)
@@ -426,7 +426,7 @@ __device__ void sample_sorted(const SegDesc& sd, const void* src, uint64_t seed,
     }
     __syncthreads();
     if (cnt > 1) {
-        MC::SS::sort_fast(S.sort.A, cnt, S.sort);  // -> S.sort.B
+        MC::SS::sort_fast(S.sort.A, cnt, S.sort, eq);  // -> S.sort.B
         for (uint32_t i = threadIdx.x; i < cnt; i += NT) S.sort.A[i] = S.sort.B[i];
     }
     __syncthreads();
@@ -466,7 +466,8 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
         __syncthreads();
     } else {
         s1 = (uint32_t)first_sample_size(cfg, n);
-        sample_sorted<IN_F64, MC>(sd, src, seed, 0, s1, S);
+        // a root-level sample spans the whole key range: equalised digits
+        sample_sorted<IN_F64, MC>(sd, src, seed, 0, s1, S, first_only || sd.depth == 0);
     }
     const uint64_t* A = S.sort.A;
     uint64_t d = 0;

@@ -220,7 +220,7 @@ struct SmemSort {
     // (a may alias S.A: it is not read after the first pass.)
     static constexpr int ITEMS = CAP / NT;
     static constexpr int kThreads = NT;
-    __device__ static void sort_fast(const uint64_t* a, uint32_t n, Smem& S) {
+    __device__ static void sort_fast(const uint64_t* a, uint32_t n, Smem& S, bool eq = false) {
         static_assert(ITEMS * NT == CAP, "CAP must be a multiple of NT");
         uint64_t k[ITEMS];
 #pragma unroll
@@ -228,11 +228,17 @@ struct SmemSort {
             const uint32_t j = threadIdx.x + i * NT;
             k[i] = j < n ? a[j] : 0ull;
         }
-        sort_regs(k, n, S, S.A);
+        sort_regs(k, n, S, S.A, eq);
     }
     // keys j = threadIdx.x + i * NT in k[i]; result in S.B; scratch: >= n keys
     template <int IT = ITEMS, class SM>
-    __device__ static void sort_regs(uint64_t (&k)[IT], uint32_t n, SM& S, uint64_t* scratch) {
+    // eq: equalised digits for skewed key sets spanning a wide range (a root's
+    // sample: encoded floats crowd into a few binades -- Normal's first sample put
+    // 77% of its keys into digits of > 256 keys, drained one digit at a time):
+    // a coarse histogram of the top 10 digit bits, and each key's digit
+    // interpolated inside its coarse bin by its key offset -- monotone, ~1 key
+    // per digit for any smooth distribution.
+    __device__ static void sort_regs(uint64_t (&k)[IT], uint32_t n, SM& S, uint64_t* scratch, bool eq = false) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         constexpr int NW = NT / 32;
         constexpr uint32_t kNb = CAP < NBMAX ? CAP : NBMAX;  // digits: >= 1 per key for n near CAP
@@ -342,6 +348,32 @@ struct SmemSort {
             shift = bits > lgnb ? bits - lgnb : 0;
         }
         uint32_t dg[IT];
+        if (eq && lgnb >= 10 && NBMAX >= 1024) {
+            const uint32_t cs = shift + lgnb - 10;  // coarse bin: top 10 bits of the digit
+            // S.hist[0, nb) is zero (zeroed before the range reduction's barrier)
+#pragma unroll
+            for (int i = 0; i < IT; ++i) {
+                const uint32_t j = tid + i * NT;
+                if (j < n) atomicAdd(&S.hist[(uint32_t)((k[i] - base) >> cs)], 1u);
+            }
+            __syncthreads();
+            block_exclusive_scan_u32<NT>(S.hist, 1024, S.wsum);
+            if (tid == 0) S.hist[1024] = n;
+            __syncthreads();
+            const double scale = (double)nb / (double)n, unit = ldexp(1.0, -(int)cs);
+#pragma unroll
+            for (int i = 0; i < IT; ++i) {
+                const uint64_t off = k[i] - base;
+                const uint32_t bin = (uint32_t)(off >> cs);
+                const uint32_t c0 = S.hist[min(bin, 1023u)], c1 = S.hist[min(bin, 1023u) + 1];
+                const double t = (double)(off - ((uint64_t)bin << cs)) * unit;  // [0, 1]
+                const double f = (double)c0 + t * (double)(c1 - c0);
+                dg[i] = min((uint32_t)(f * scale), nb - 1);
+            }
+            __syncthreads();  // coarse counts read: the counting pass re-zeroes hist
+            sort_digits<IT, SM, false>(k, dg, n, nb, S, scratch);
+            return;
+        }
 #pragma unroll
         for (int i = 0; i < IT; ++i) {
             dg[i] = (uint32_t)((k[i] - base) >> shift);
