@@ -62,13 +62,63 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: an NVML
+    polling thread (~2 ms period; nvidia-smi's 200 ms minimum period missed
+    short regions), nvidia-smi as the fallback."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.p = None
+        self.samples = []  # (sm_mhz, max_mhz, reason_mask)
+        self._stop = None
+        self._thr = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            # the visible device index maps to the NVML index through the UUID
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(self.gpu).uuid)
+                for i in range(pynvml.nvmlDeviceGetCount()):
+                    hi = pynvml.nvmlDeviceGetHandleByIndex(i)
+                    u = pynvml.nvmlDeviceGetUUID(hi)
+                    u = u.decode() if isinstance(u, bytes) else u
+                    if uuid and uuid in u:
+                        h = hi
+                        break
+            except Exception:
+                pass
+            self.h = h
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.nv = None
+
+    def _poll(self):
+        import time as _t
+        nv, h = self.nv, self.h
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), self.max_mhz, int(rs)))
+            except Exception:
+                pass
+            _t.sleep(0.002)
 
     def __enter__(self):
+        if self.nv is not None:
+            import threading
+            self._stop = threading.Event()
+            self._thr = threading.Thread(target=self._poll, daemon=True)
+            self._thr.start()
+            return self
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -82,6 +132,9 @@ class ClockSampler:
 
     def __exit__(self, *a):
         self.lines = []
+        if self._thr is not None:
+            self._stop.set()
+            self._thr.join(timeout=2)
         if self.p is not None:
             self.p.terminate()
             try:
@@ -93,21 +146,31 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], 0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in self.lines:
-            f = [x.strip() for x in l.split(",")]
-            try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
+        if self.nv is not None:
+            for f, m, rs in self.samples:
+                sm.append(f)
+                mx = max(mx, m)
+                for nm, attr in self.REASONS:
+                    if rs & int(getattr(self.nv, attr, 0)):
+                        reasons.add(nm)
+            src = "nvml"
+        else:
+            names = [r[0] for r in self.REASONS]
+            for l in self.lines:
+                f = [x.strip() for x in l.split(",")]
+                try:
+                    sm.append(float(f[0]))
+                    mx = max(mx, float(f[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, f[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            src = "nvidia-smi"
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": src}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": src}
 
 
 def env_rank():
