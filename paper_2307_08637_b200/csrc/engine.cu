@@ -124,7 +124,7 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws, ids, clus, bat[3], psample, slices, dist_hist, fwd_model, fwd_slices, piv;
+        kseg, ktp, kplan, qws, ids, clus, bat[3], psample, slices, dist_hist, fwd_model, fwd_slices, piv, fsample;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
@@ -425,7 +425,13 @@ struct Engine {
         const uint64_t seed = seg_seed_host(cfg.seed, sp.begin, sp.depth);
         launch_gather(dseg, src, f64, seed, s1, s2, N->sample.as<uint64_t>(), nullptr, N->h2d_stream);
         CU(cudaEventRecord(N->bev[1], N->h2d_stream));
-        launch_first_sample(dseg, src, f64, C->models.as<uint8_t>(), dc, N->models.as<uint8_t>(), k, gate, st);
+        // the first sample's random gather over many CTAs (one CTA cannot keep
+        // 8 Ki random loads in flight: ~30 us), then the policy CTA
+        if (!N->fsample.ensure(s1 * 8)) throw LsortError{LSORT_ENOMEM, "first sample"};
+        launch_gather(dseg, src, f64, seed, 0, s1, N->fsample.as<uint64_t>(), nullptr, st);
+        launch_first_sample(dseg, src, f64, C->models.as<uint8_t>(), dc, N->models.as<uint8_t>(), k, gate, st,
+                            N->fsample.as<uint64_t>());
+        launched();
         CU(cudaStreamWaitEvent(st, N->bev[1], 0));
         // one distribution level over the sample with the first-sample tree
         SegDesc d{};

@@ -125,9 +125,10 @@ constexpr uint32_t kModelSmallCap = 2048;    // samples of the small model CTA
 // mid = 0: samples <= kModelSmallCap (256 threads); 1: <= kSmallSampleCap (512 threads)
 void launch_build_models(const SegDesc* segs, const uint32_t* idx, uint32_t count, const void* src,
                          int in_f64, uint8_t* models, const DevCfg& cfg, int mid, cudaStream_t st);
+// pre (nullable): the first sample already gathered (launch_gather draws [0, s1))
 void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_t* models,
                          const DevCfg& cfg, uint8_t* aux, uint32_t aux_budget, uint32_t* gate,
-                         cudaStream_t st);
+                         cudaStream_t st, const uint64_t* pre = nullptr);
 void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0,
                    uint64_t s, uint64_t* out, const uint32_t* gate, cudaStream_t st);
 size_t train_workspace_bytes(uint64_t s, uint32_t B);

@@ -47,6 +47,17 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 __host__ __device__ __forceinline__ uint64_t sample_index(uint64_t seed, uint64_t draw, uint64_t n) {
     return n == 0 ? 0 : splitmix64(seed + draw) % n;
 }
+// The same index without a 64-bit division (emulated on the GPU, ~100
+// instructions): x % n from the high product with minv = floor((2^64-1)/n),
+// which underestimates x / n by at most 2 -- exact after two corrections.
+__device__ __forceinline__ uint64_t mod_by_inv(uint64_t x, uint64_t n, uint64_t minv) {
+    uint64_t r = x - __umul64hi(x, minv) * n;
+    r = r >= n ? r - n : r;
+    return r >= n ? r - n : r;
+}
+__device__ __forceinline__ uint64_t sample_index_inv(uint64_t seed, uint64_t draw, uint64_t n, uint64_t minv) {
+    return n == 0 ? 0 : mod_by_inv(splitmix64(seed + draw), n, minv);
+}
 
 enum ModelKind : uint32_t { kLearned = 0, kTree = 1, kRadix = 2, kFill = 3 };
 

@@ -407,22 +407,28 @@ __device__ void build_radix_model(const SegDesc& sd, const void* src, bool f64, 
 // Draw sample draws [j0, j0+cnt) of the segment stream into shared A, sort.
 template <bool IN_F64, class MC>
 __device__ void sample_sorted(const SegDesc& sd, const void* src, uint64_t seed, uint32_t j0, uint32_t cnt,
-                              typename MC::Smem& S, bool eq = false) {
+                              typename MC::Smem& S, bool eq = false, const uint64_t* pre = nullptr) {
     constexpr int NT = sizeof(S.red64) / 8 * 32;
+    if (pre) {  // drawn by a many-CTA gather (one SM cannot keep enough random loads in flight)
+        for (uint32_t i = threadIdx.x; i < cnt; i += NT) S.sort.A[i] = pre[i];
+    } else
     // random gather: 8 independent loads in flight per thread (a rolled loop
     // waits one DRAM latency per key)
+    {
+    const uint64_t minv = sd.n ? ~0ull / sd.n : 0ull;
     for (uint32_t i0 = threadIdx.x; i0 < cnt; i0 += 8 * NT) {
         uint64_t v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint32_t i = i0 + u * NT;
-            v[u] = i < cnt ? load_key(src, sd.begin + sample_index(seed, j0 + i, sd.n), IN_F64) : 0ull;
+            v[u] = i < cnt ? load_key(src, sd.begin + sample_index_inv(seed, j0 + i, sd.n, minv), IN_F64) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint32_t i = i0 + u * NT;
             if (i < cnt) S.sort.A[i] = v[u];
         }
+    }
     }
     __syncthreads();
     if (cnt > 1) {
@@ -440,7 +446,7 @@ __device__ void sample_sorted(const SegDesc& sd, const void* src, uint64_t seed,
 template <bool IN_F64, class MC>
 __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* models, const DevCfg& cfg,
                                 typename MC::Smem& S, bool first_only, uint8_t* aux, uint32_t aux_budget,
-                                uint32_t* gate) {
+                                uint32_t* gate, const uint64_t* pre = nullptr) {
     constexpr int NT = sizeof(S.red64) / 8 * 32;
     ModelHdr* h = (ModelHdr*)(models + sd.model_off);
     uint8_t* payload = models + sd.model_off + sizeof(ModelHdr);
@@ -467,7 +473,7 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
     } else {
         s1 = (uint32_t)first_sample_size(cfg, n);
         // a root-level sample spans the whole key range: equalised digits
-        sample_sorted<IN_F64, MC>(sd, src, seed, 0, s1, S, first_only || sd.depth == 0);
+        sample_sorted<IN_F64, MC>(sd, src, seed, 0, s1, S, first_only || sd.depth == 0, first_only ? pre : nullptr);
     }
     const uint64_t* A = S.sort.A;
     uint64_t d = 0;
@@ -535,13 +541,13 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) k_build_models(const Se
 }
 
 template <bool IN_F64>
-__global__ void __launch_bounds__(512, 1) k_first_sample(const SegDesc* seg, const void* src, uint8_t* models,
+__global__ void __launch_bounds__(512, 1) k_first_sample(const uint64_t* pre, const SegDesc* seg, const void* src, uint8_t* models,
                                                      DevCfg cfg, uint8_t* aux, uint32_t aux_budget, uint32_t* gate) {
     griddep_wait();
     extern __shared__ uint4 smem_u4[];
     ModelMid::Smem& S = *(ModelMid::Smem*)smem_u4;
     const SegDesc sd = *seg;
-    build_model_cta<IN_F64, ModelMid>(sd, src, models, cfg, S, true, aux, aux_budget, gate);
+    build_model_cta<IN_F64, ModelMid>(sd, src, models, cfg, S, true, aux, aux_budget, gate, pre);
 }
 
 template <bool IN_F64>
@@ -550,8 +556,9 @@ __global__ void k_gather(const SegDesc* seg, const void* src, uint64_t seed, uin
     griddep_wait();
     if (gate && *gate == 0) return;
     const SegDesc sd = *seg;
+    const uint64_t minv = sd.n ? ~0ull / sd.n : 0ull;
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < s; j += (uint64_t)gridDim.x * blockDim.x)
-        out[j] = load_key(src, sd.begin + sample_index(seed, j0 + j, sd.n), IN_F64);
+        out[j] = load_key(src, sd.begin + sample_index_inv(seed, j0 + j, sd.n, minv), IN_F64);
 }
 
 
@@ -1025,10 +1032,10 @@ void launch_build_models(const SegDesc* segs, const uint32_t* idx, uint32_t coun
 }
 
 void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_t* models, const DevCfg& cfg,
-                         uint8_t* aux, uint32_t aux_budget, uint32_t* gate, cudaStream_t st) {
+                         uint8_t* aux, uint32_t aux_budget, uint32_t* gate, cudaStream_t st, const uint64_t* pre) {
     size_t sm = sizeof(ModelMid::Smem);
-    if (in_f64) pdl(k_first_sample<true>, 1, 512, sm, st, seg, src, models, cfg, aux, aux_budget, gate);
-    else pdl(k_first_sample<false>, 1, 512, sm, st, seg, src, models, cfg, aux, aux_budget, gate);
+    if (in_f64) pdl(k_first_sample<true>, 1, 512, sm, st, pre, seg, src, models, cfg, aux, aux_budget, gate);
+    else pdl(k_first_sample<false>, 1, 512, sm, st, pre, seg, src, models, cfg, aux, aux_budget, gate);
 }
 
 void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0, uint64_t s,
