@@ -1051,6 +1051,10 @@ void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* m
     const uint32_t n = (uint32_t)s;
     const uint32_t nch = (uint32_t)((s + kTrainChunk - 1) / kTrainChunk);
     RmiEntry* E = (RmiEntry*)(model + sizeof(ModelHdr));
+    static_assert(kBigSplit == kBigSplitWS, "workspace layout");
+    // (before the kernel chain: a memset between two programmatic-launch
+    // kernels serialises them fully; no kernel before k_train_bigfits uses it)
+    cudaMemsetAsync(train_ws(ws, s, B).bigcnt, 0, 4 * (size_t)B, st);
     pdl(k_train_sums<false>, nch, kTrainNT, 0, st, sample, n, ws, B, gate);
     pdl(k_train_reduce<false>, 1, kTrainNT, 0, st, sample, n, ws, B, gate);
     pdl(k_train_sums<true>, nch, kTrainNT, 0, st, sample, n, ws, B, gate);
@@ -1058,8 +1062,6 @@ void launch_train_rmi(const uint64_t* sample, uint64_t s, uint32_t B, uint8_t* m
     const int gb = (int)std::min<uint64_t>((s + kTrainNT - 1) / kTrainNT, (uint64_t)num_sms() * 8);
     pdl(k_train_bounds, gb, kTrainNT, 0, st, sample, n, ws, B, gate);
     pdl(k_train_fits, (B + kFitWarps - 1) / kFitWarps, 32 * kFitWarps, 0, st, sample, n, ws, B, E, gate);
-    static_assert(kBigSplit == kBigSplitWS, "workspace layout");
-    cudaMemsetAsync(train_ws(ws, s, B).bigcnt, 0, 4 * (size_t)B, st);
     const int gbig = (int)std::min<uint64_t>((uint64_t)B * kBigSplit, (uint64_t)num_sms() * 4);
     pdl(k_train_bigfits, gbig, kBigFitNT, 0, st, sample, n, ws, B, E, gate);
     pdl(k_train_enforce, 1, kEnforceNT, 16 * (size_t)B, st, sample, n, ws, B, model, nbuckets, gate);
