@@ -88,6 +88,11 @@ struct LsortError {
             throw LsortError{LSORT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)}; \
     } while (0)
 
+// leftover keys in 16 Ki..kClCap segments below which a level >= 1 goes to the
+// fused cluster kernel (measured: C1's 15 leaves of ~365 Ki keys 0.618 -> 0.562 ms
+// per sort; C2's full level 1 of 1e8 keys is 2x slower there)
+constexpr uint64_t kAutoClusterKeys = 4ull << 20;
+
 uint32_t fanout(uint64_t n, uint32_t cfg_count, uint32_t target) {
     if (target == 0) return cfg_count;
     uint64_t want = (n + target - 1) / target;
@@ -555,8 +560,19 @@ struct Engine {
             std::vector<uint32_t> bigs;
             // segments of the last distribution level that fit a cluster go to the
             // fused DSMEM kernel (cluster.cu); the rest are partitioned here
+            // GPU policy: a FEW leftover segments just above the base-case capacity
+            // (C1's handful of 16-35 Ki leaves) are cheaper in the fused cluster
+            // kernel than through a whole latency-bound partition level; many of
+            // them (a full level 1) are not -- the cluster kernel runs one CTA per SM
+            uint64_t elig_keys = 0;
+            if (level >= 1)
+                for (const SegPlan& q : segs)
+                    if (q.n > cap && q.n <= kClCap) elig_keys += q.n;
+            static const bool no_auto_cluster = getenv("LSORT_NO_AUTO_CLUSTER") != nullptr;
+            const bool auto_cluster = !no_auto_cluster && !(cfg.flags & LSORT_FLAG_STRICT_POLICY) &&
+                                      elig_keys > 0 && elig_keys <= kAutoClusterKeys;
             const bool use_cluster = level >= 1 && !src_f64 && cluster_available() &&
-                                     (cfg.flags & LSORT_FLAG_CLUSTER) && cap >= 16384;
+                                     ((cfg.flags & LSORT_FLAG_CLUSTER) || auto_cluster) && cap >= 16384;
             std::vector<BaseItem> clus;
             std::vector<SegPlan> psegs;
             psegs.reserve(ns);
