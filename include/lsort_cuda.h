@@ -139,10 +139,12 @@ typedef struct lsort_stats {
  * extra passes). The sorted output is identical either way;
  * lsort_cuda_build_model always runs strict. */
 #define LSORT_FLAG_STRICT_POLICY 2u
-/* cfg->flags: run the last distribution level fused with the base case in
- * distributed shared memory (thread-block clusters, cluster.cu) for segments
- * of 16 Ki..128 Ki keys. Experimental: exact, but not yet faster than the
- * classify + scatter + base-case path. */
+/* cfg->flags: run every level >= 1 segment of 16 Ki..128 Ki keys through the
+ * last distribution level fused with the base case in distributed shared
+ * memory (thread-block clusters, cluster.cu). Without the flag the GPU policy
+ * does so only when such segments hold at most 4 Mi keys in total (a few
+ * leftovers: cheaper than a whole partition level); for a full level the
+ * classify + scatter + base-case path is faster. */
 #define LSORT_FLAG_CLUSTER 4u
 
 typedef struct lsort_ctx lsort_ctx;
