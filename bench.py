@@ -1,24 +1,32 @@
 #!/usr/bin/env python
 """Benchmark: sorted keys/s of the B200 LearnedSort (AIPS2o) on BASELINE.json's configs.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5]
 
-Default workload (N=1) = BASELINE.json configs[1] ("C2"): N = 1e8 float64
-keys per array, three arrays -- Normal(0,1), LogNormal(0,0.5), Exponential(2),
-i.i.d. from seed 7 (reference Rng, glibc libm, generated on the host). One
-step = sorting the three arrays (3e8 keys). Inputs (800 MB each) are larger
-than the 126 MB L2, restored from pristine device copies before every step
-(untimed), followed by an untimed 256 MB L2-flush write. Each sort is
-bracketed by barrier + synchronize and timed with CUDA events on the sort's
-stream; `value` = keys sorted / summed device time (max over ranks).
+Default workload (N=1) = the largest single-GPU configuration of
+BASELINE.json: C5, the 5e8-key float64 LogNormal(0,2) shard of one GPU
+(seed 19, reference Rng + glibc libm, generated on the host). One step = one
+sort of the config's arrays (C5: one array), each array by its own
+lsort_cuda_sort call; every timed sort starts from a restored input (4 GB,
+far above the 126 MB L2) and an untimed 256 MB L2-flush write, and is timed
+with CUDA events on the sort's stream. `value` = keys sorted / summed device
+time. Configs with several arrays (C2, C4) also report `overlapped`: the
+arrays in one lsort_cuda_sort_many call.
 
-N > 1 (torchrun): weak scaling, 1e8 keys of each C2 distribution per rank,
-globally sorted across ranks (RMI splitters + NCCL all-to-all, see
-paper_2307_08637_b200/dist.py).
+`e2e`: the same sorts through the public API from pinned host memory (H2D and
+D2H inside the timed region, wall clock around the synchronous call).
 
---impl reference: the reference's CPU path (oracle/ C restatement of the
-AIPS2o driver; the reference ships no sort driver) on the host cores, on a
-bounded sample of the same workload per step.
+`cpu_baseline`: BASELINE.md section 3 on the box's host cores, on bounded
+samples of the config (std::sort on one thread, __gnu_parallel::sort on all
+cores, the AIPS2o port on all cores; mean of 10 runs).
+
+N > 1 (torchrun): weak scaling, shard r of a world x n dataset per rank,
+globally sorted across ranks; max over ranks of the device time.
+
+--impl reference: the reference's CPU path (the oracle's C restatement of the
+AIPS2o driver -- the reference ships no sort driver) on all host cores, on
+this arm's config (whole arrays per step unless W + K steps would exceed
+--ref-budget-s, then a bounded prefix sample, stated in the line).
 """
 from __future__ import annotations
 
@@ -179,51 +187,138 @@ def env_rank():
 
 
 # --------------------------------------------------------------------- CPU legs
-def cpu_sort_rate(cfg_name: str, sample_n: int, runs: int):
-    """Oracle AIPS2o restatement (OpenMP, all host threads) on `sample_n` keys
-    of each config distribution; returns (Mkeys/s list per run, threads)."""
+def lscpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_arrays(cfg_name: str, n: int, first: int = 0, total: int | None = None):
+    """Host inputs of a config (reference Rng + glibc libm, generated by the
+    oracle's C restatement -- bit-identical to the library's lsort_gen_keys)."""
     from oracle import oracle as O
-    label, dists, n, kind = CONFIGS[cfg_name]
-    threads = os.cpu_count() or 1
-    arrays = [O.generate(d, n if kind == "u64" else sample_n, s) for d, s in dists]
-    if kind == "u64":  # shuffled datasets are generated whole; take a prefix
-        arrays = [a[:sample_n].copy() for a in arrays]
-    rates = []
+    label, dists, _, kind = CONFIGS[cfg_name]
+    out = []
+    for d, s in dists:
+        if kind == "u64":  # shuffled datasets are generated whole; a prefix is a sample
+            a = O.generate(d, total or n, s)[first:first + n].copy()
+        else:
+            a = O.generate(d, total or n, s, first=first, count=n)
+        out.append(a)
+    return out
+
+
+def timed_port_sort(a: np.ndarray, threads: int) -> float:
+    """One run of the AIPS2o CPU restatement (oracle, OpenMP) on a fresh copy; seconds."""
+    from oracle import oracle as O
+    b = a.copy()
     c = O.cfg(workers=threads)
-    for _ in range(runs):
-        t = 0.0
-        for a in arrays:
-            b = a.copy()
+    t0 = time.perf_counter()
+    if b.dtype == np.float64:
+        O.sort_doubles(b, c)
+    else:
+        O.sort_keys(b, c)
+    return time.perf_counter() - t0
+
+
+def cpu_baselines(cfg_name: str, runs: int = 10):
+    """BASELINE.md section 3 on the box's host cores, each on a bounded sample of
+    the config's first array, mean of `runs` runs:
+    std::sort on one thread (PAPER.md:430), __gnu_parallel::sort on all cores
+    (the par_unseq stand-in) and the AIPS2o port (the oracle's
+    C restatement of the reference driver, OpenMP, all cores)."""
+    from oracle import oracle as O
+    threads = O.lib().lso_max_threads()
+    label, dists, n, kind = CONFIGS[cfg_name]
+    samples = {"std_sort_1t": min(n, 10_000_000), "gnu_parallel_sort": min(n, 100_000_000),
+               "aips2o_port": min(n, 20_000_000)}
+    big = config_arrays(cfg_name, max(samples.values()), total=n)[0]
+    keys = O.encode(big) if big.dtype == np.float64 else big
+    res = {}
+    for alg, m in samples.items():
+        ts = []
+        for _ in range(runs):
+            if alg == "aips2o_port":
+                ts.append(timed_port_sort(big[:m], threads))
+                continue
+            b = keys[:m].copy()
             t0 = time.perf_counter()
-            if kind == "f64":
-                O.sort_doubles(b, c)
+            if alg == "std_sort_1t":
+                O.std_sort(b)
             else:
-                O.sort_keys(b, c)
-            t += time.perf_counter() - t0
-        rates.append(len(arrays) * sample_n / t / 1e9)
-    return rates, threads
+                O.parallel_sort(b, threads)
+            ts.append(time.perf_counter() - t0)
+        mean = float(np.mean(ts))
+        res[alg] = {"value": m / mean / 1e9, "unit": "Gkeys/s", "keys": m, "runs": runs,
+                    "threads": 1 if alg == "std_sort_1t" else threads, "mean_s": mean}
+    return res, threads
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU path = the oracle's C restatement of
+    the AIPS2o driver (the reference ships no sort driver, only its model layer;
+    oracle/_ref holds that layer) on all host cores, on this arm's config. Each
+    step sorts the whole config (every array, full size) from a fresh copy
+    (untimed), unless W + K full steps would exceed the time budget, in which
+    case each step sorts a bounded prefix sample (stated in `config`)."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
+    from oracle import oracle as O
+    threads = O.lib().lso_max_threads()
     cfg_name = args.config
     label, dists, n, kind = CONFIGS[cfg_name]
-    sample_n = min(n, args.cpu_sample)
-    rates, threads = cpu_sort_rate(cfg_name, sample_n, args.warmup + args.steps)
-    timed = rates[args.warmup:]
-    v = float(np.mean(timed))
-    ms = len(dists) * sample_n / (v * 1e9) * 1e3
+    arrays = config_arrays(cfg_name, n)
+    # first warm-up step on the full config decides whether full steps fit the budget
+    t_full = sum(timed_port_sort(a, threads) for a in arrays)
+    m = n
+    if t_full * (args.warmup + args.steps) > args.ref_budget_s:
+        m = max(1_000_000, int(n * args.ref_budget_s / (t_full * (args.warmup + args.steps))))
+        arrays = [a[:m].copy() for a in arrays]
+    ts = []
+    for step in range(args.warmup - 1 + args.steps):
+        t = sum(timed_port_sort(a, threads) for a in arrays)
+        if step >= args.warmup - 1:
+            ts.append(t)
+    t = float(np.mean(ts))
+    v = len(arrays) * m / t / 1e9
+    sample = ("full config per step" if m == n else f"{m} keys (prefix) of each of {len(arrays)} arrays per step; "
+              f"a full-config step took {t_full:.1f} s")
     line = {"metric": METRIC, "value": v, "unit": "Gkeys/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": kind, "data": "synthetic (reference Rng, host)",
-            "impl": "reference",
-            "config": {"workload": label, "sample_keys_per_array": sample_n, "arrays": len(dists)},
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": kind, "data": DATA, "impl": "reference",
+            "config": config_dict(cfg_name, world=1),
             "cpu_baseline": {"value": v, "unit": "Gkeys/s", "cores": threads, "kind": "port",
-                             "sample": f"{sample_n} keys x {len(dists)} arrays per step"},
+                             "sample": sample, "cpu_model": lscpu_model()},
             "e2e": {"value": v, "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if m != n:
+        line["config"]["reference_sample_keys_per_array"] = m
     print(json.dumps(line), flush=True)
+
+
+DATA = "synthetic (reference Rng splitmix64 + glibc libm on host; BASELINE.json seeds)"
+
+
+def config_dict(cfg_name: str, world: int, n: int | None = None) -> dict:
+    label, dists, n0, kind = CONFIGS[cfg_name]
+    return {"workload": label, "keys_per_array_per_gpu": n or n0, "arrays": len(dists),
+            "l2": "inputs (>= 80 MB, > 126 MB L2 from C2 up) restored + 256 MB L2-flush write before every timed sort",
+            "parallelism": f"dp{world}" if world > 1 else "single-gpu"}
+
+
+def traffic_profile(cfg_name: str):
+    """Measured DRAM bytes per key per phase for this config (ncu counters over
+    one sort of each config array, tools/phase_traffic.py) -- or None."""
+    path = os.path.join(ROOT, "profiles", f"r2_traffic_{cfg_name}.json")
+    try:
+        with open(path) as f:
+            return json.load(f), os.path.relpath(path, ROOT)
+    except (OSError, ValueError):
+        return None, None
 
 
 # --------------------------------------------------------------------- GPU leg
@@ -235,285 +330,246 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dist_mode = world > 1 or args.dist
     if dist_mode:
-        import torch.distributed as tdist
-        for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533")):
-            os.environ.setdefault(k, v)  # --dist without torchrun: a one-rank group
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return run_dist(args)
     label, dists, n, kind = CONFIGS[args.config]
     if args.keys:
         n = args.keys
-    f64 = kind == "f64"
     dev = torch.device("cuda", local)
 
-    # ---- inputs (host generation, reference Rng; shard r of a world*n dataset)
-    pristine = []
-    for d, s in dists:
-        if dist_mode and kind == "f64":
-            h = L.generate(d, world * n, s, first=rank * n, count=n)
-        else:
-            h = L.generate(d, n, s)
-        t = torch.from_numpy(h.view(np.int64) if h.dtype == np.uint64 else h).to(dev)
-        pristine.append(t)
+    # ---- inputs (host generation, reference Rng), pristine device copies
+    hosts = config_arrays(args.config, n)
+    pristine = [torch.from_numpy(h.view(np.int64) if h.dtype == np.uint64 else h).to(dev) for h in hosts]
     work = [torch.empty_like(p) for p in pristine]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ctx = L.Context(local)
-    # timed sorts run without per-phase events (those force a host sync per
-    # level); an extra untimed pass with LSORT_FLAG_PHASE_TIMING feeds the
-    # per-phase roofline. The distributed path keeps them (per-rank phases).
+    cfg = L.SortConfig()
     cfg_phase = L.SortConfig(flags=L._native.FLAG_PHASE_TIMING)
-    cfg = cfg_phase if dist_mode else L.SortConfig()
-    if dist_mode:
-        from paper_2307_08637_b200.dist import DistSorter
-        sorter = DistSorter(ctx, cfg)
 
-    def barrier():
-        if dist_mode:
-            import torch.distributed as tdist
-            tdist.barrier()
-
-    def one_sort(i):
-        """restore + flush (untimed), then timed sort of array i; returns (ms, stats)."""
+    def restore(i):
         work[i].copy_(pristine[i])
         flush.fill_(1)
         torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        st = torch.cuda.current_stream()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        if dist_mode:
-            out, stats = sorter.sort(work[i])
-        else:
-            stats = ctx.sort(work[i], cfg)
-        e1.record(st)
-        torch.cuda.synchronize()
-        barrier()
-        ms = e0.elapsed_time(e1)
-        return ms, stats, (out if dist_mode else work[i])
 
-    def batch_step():
-        """restore + flush (untimed), then ONE timed lsort_cuda_sort_many call over
-        all arrays of the config (up to three sorts in flight on separate contexts)."""
-        for i in range(len(work)):
-            work[i].copy_(pristine[i])
-        flush.fill_(1)
-        torch.cuda.synchronize()
+    def one_sort(i, c=cfg):
+        """untimed restore + L2 flush, then the event-timed sort of array i (ms, stats)."""
+        restore(i)
         st = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        stats = ctx.sort_batch(work, cfg)
+        stats = ctx.sort(work[i], c)
         e1.record(st)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1), stats
 
-    use_batch = not dist_mode and len(work) > 1 and not args.sequential
     for _ in range(args.warmup):
         for i in range(len(work)):
             one_sort(i)
-        if use_batch:
-            batch_step()
-    # correctness spot check on the last warm-up output (untimed)
-    for i in range(len(work)):
-        _, _, res = one_sort(i)
-        ok, fv, _ = ctx.verify(res)
+    for i in range(len(work)):  # correctness spot check on a warm-up output (untimed)
+        one_sort(i)
+        ok, fv, _ = ctx.verify(work[i])
         if not ok:
-            raise SystemExit(f"rank {rank}: output {i} not sorted at {fv}")
+            raise SystemExit(f"output {i} not sorted at {fv}")
     peaks, peak_src = measured_peaks()
-    total_ms = 0.0
-    agg = {}
-    launches = 0
-    seq_ms = None
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    total_ms, launches, levels = 0.0, 0, 0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            if use_batch:
-                ms, stats = batch_step()
-                total_ms += ms
-                launches += stats.get("kernel_launches", 0)
-                for k, v in stats.items():
-                    if isinstance(v, (int, float)):
-                        agg[k] = agg.get(k, 0) + v
-                continue
             for i in range(len(work)):
-                ms, stats, _ = one_sort(i)
+                ms, stats = one_sort(i)
                 total_ms += ms
-                if dist_mode:
-                    stats = dict(stats.get("local") or {})
                 launches += stats.get("kernel_launches", 0)
-                for k, v in stats.items():
-                    if isinstance(v, (int, float)):
-                        agg[k] = agg.get(k, 0) + v
+                levels += stats.get("levels", 0)
     clocks = clk.summary()
-    if use_batch:  # the same arrays one sort at a time (reported beside the headline)
-        for _ in range(2):
-            seq_ms = sum(one_sort(i)[0] for i in range(len(work)))
-        for i in range(len(work)):  # the batch output is checked too
-            work[i].copy_(pristine[i])
-        ctx.sort_batch(work, cfg)
-        for i in range(len(work)):
-            ok, fv, _ = ctx.verify(work[i])
-            if not ok:
-                raise SystemExit(f"batch output {i} not sorted at {fv}")
-    if not dist_mode:  # phase breakdown (untimed)
-        for k in ("ms_models", "ms_classify", "ms_scatter", "ms_base", "ms_fill"):
-            agg[k] = 0.0
-        for i in range(len(work)):
-            work[i].copy_(pristine[i])
-            st_ph = ctx.sort(work[i], cfg_phase)
-            for k in ("ms_models", "ms_classify", "ms_scatter", "ms_base", "ms_fill"):
-                agg[k] += st_ph.get(k, 0.0) * args.steps  # scaled like the timed aggregate
-    keys_per_step = len(work) * n * (world if dist_mode else 1)
-    if dist_mode:
-        import torch.distributed as tdist
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    nsorts = args.steps * len(work)
     ms_per_step = total_ms / args.steps
-    value = keys_per_step / (ms_per_step * 1e-3) / 1e9  # Gkeys/s whole job
+    keys_per_step = len(work) * n
+    value = keys_per_step / (ms_per_step * 1e-3) / 1e9
 
-    # ---- roofline: dominant kernel (by measured phase share) and whole sort
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    nsteps_arrays = args.steps * len(work)
-    phases = {k: agg.get(k, 0.0) / nsteps_arrays for k in
-              ("ms_models", "ms_classify", "ms_scatter", "ms_base", "ms_fill")}
-    # algorithmic bytes per launch: scatter moves every partitioned key once
-    # (8 B read + 8 B write); base case reads + writes each base-case key once;
-    # classify reads each partitioned key once (8 B).
-    part_keys = agg.get("partitioned_keys", 0) / nsteps_arrays
-    base_keys = agg.get("base_case_keys", 0) / nsteps_arrays
+    # ---- per-phase breakdown: an extra untimed pass with per-phase events
+    phases = {k: 0.0 for k in PHASES}
+    part_keys = base_keys = 0
+    for i in range(len(work)):
+        _, st_ph = one_sort(i, cfg_phase)
+        for k in PHASES:
+            phases[k] += st_ph.get(k, 0.0) / len(work)
+        part_keys += st_ph["partitioned_keys"] / len(work)
+        base_keys += st_ph["base_case_keys"] / len(work)
+    # algorithmic bytes per launch of each phase (DESIGN.md section 3): the
+    # scatter moves every partitioned key once (8 B read + 8 B write), the base
+    # case reads + writes each base-case key once, the classify reads each
+    # partitioned key once (8 B)
     alg = {"ms_scatter": 16.0 * part_keys, "ms_base": 16.0 * base_keys, "ms_classify": 8.0 * part_keys}
     dom = max(alg, key=lambda k: phases[k])
     achieved = alg[dom] / (phases[dom] * 1e-3) / 1e9 if phases[dom] > 0 else 0.0
-    names = {"ms_scatter": "k_scatter", "ms_base": "k_base", "ms_classify": "k_classify_hist"}
-    # measured DRAM bytes of the same phase (ncu counters, profiles/r1_kernel_traffic.json),
-    # scaled to this run's keys per sort
+    tj, tsrc = traffic_profile(args.config)
     traffic = None
-    try:
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r1_kernel_traffic.json")))
+    if tj is not None:
         ph = {"ms_scatter": "scatter", "ms_base": "base", "ms_classify": "classify"}[dom]
         traffic = tj["phases"][ph]["dram_bytes_per_key"] * n
-    except (OSError, KeyError, ValueError):
-        traffic = None
-    nper = n
-    P = passes(nper)
-    t_roof_ms = 16.0 * P * nper / (hbm * 1e9) * 1e3 * len(work)
-    if dist_mode:
-        t_roof_ms += 8.0 * nper * (world - 1) / world / 770e9 * 1e3 * len(work)
+    P = passes(n)
+    t_roof_ms = 16.0 * P * n / (hbm * 1e9) * 1e3 * len(work)
     line = {
-        "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": kind,
-        "data": "synthetic (reference Rng splitmix64 + glibc libm on host; BASELINE.json seeds)",
-        "config": {"workload": label, "keys_per_array_per_gpu": n, "arrays": len(work),
-                   "l2": "inputs (>=80 MB) restored + 256 MB L2 flush before every timed sort",
-                   "parallelism": f"dp{world}" if dist_mode else "single-gpu"},
-        "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": hbm,
+        "scaling": "weak", "vs_baseline": None, "dtype": kind, "data": DATA,
+        "config": config_dict(args.config, 1, n),
+        "roofline": {"bound": "hbm", "kernel": PHASE_KERNEL[dom], "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                     "traffic_source": "profiles/r1_kernel_traffic.json (ncu DRAM counters, C2 normal 1e8)",
-                     "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": alg[dom]},
+                     "traffic_source": tsrc, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg[dom],
+                     "note": "phase = all launches of that kernel in one sort (per-phase CUDA events)"},
         "sort_roofline": {"passes": P, "bytes_per_key": 16 * P, "t_roof_ms_per_step": t_roof_ms,
                           "frac": t_roof_ms / ms_per_step, "hbm_gbs": hbm},
         "phases_ms_per_sort": phases,
-        "schedule": ("the config's arrays in one lsort_cuda_sort_many call (up to 3 sorts in flight)"
-                     if use_batch else "one sort at a time"),
-        "sequential": ({"value": keys_per_step / (seq_ms * 1e-3) / 1e9, "unit": "Gkeys/s", "ms_per_step": seq_ms}
-                       if seq_ms else None),
-        "levels_per_sort": agg.get("levels", 0) / nsteps_arrays,
+        "schedule": "one sort at a time (each array of the config sorted by its own lsort_cuda_sort call)",
+        "levels_per_sort": levels / nsorts,
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
-    # ---- e2e through the public API with pinned host buffers (H2D + D2H inside)
-    if not dist_mode and args.e2e_steps > 0:
-        hosts = [torch.empty(n, dtype=p.dtype, pin_memory=True) for p in pristine]
-        src = [p.cpu() for p in pristine]
-        # the public batch entry point (lsort_cuda_sort_batch): one call sorts
-        # the config's arrays from pinned host memory, copies in / out
-        # pipelined against the sorts on two copy streams
-        e2e_t = 0.0
-        for step in range(args.e2e_steps + 1):
-            arrs = []
-            for i in range(len(hosts)):
-                hosts[i].copy_(src[i])
-                arrs.append(hosts[i].numpy())
+    if len(work) > 1:  # the config's arrays in flight together (lsort_cuda_sort_many), beside the headline
+        ms_b = []
+        for _ in range(3):
+            for i in range(len(work)):
+                work[i].copy_(pristine[i])
+            flush.fill_(1)
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            ctx.sort_batch(arrs, cfg)
-            dt = time.perf_counter() - t0
-            if step > 0:
-                e2e_t += dt
-        for i in range(len(hosts)):  # the end-to-end result is checked, not just timed
-            ok, _, _ = ctx.verify(torch.from_numpy(hosts[i].numpy()).cuda())
-            if not ok:
-                raise RuntimeError("e2e sort produced unsorted output")
-        e2e_ms = e2e_t / max(1, args.e2e_steps) * 1e3
-        line["e2e"] = {"value": len(hosts) * n / (e2e_ms * 1e-3) / 1e9, "unit": "Gkeys/s",
-                       "h2d_bytes_per_step": 8 * n * len(hosts), "d2h_bytes_per_step": 8 * n * len(hosts),
-                       "ms_per_step": e2e_ms}
-    elif dist_mode and args.e2e_steps > 0:
-        # the distributed public API end to end: every rank copies its shard in
-        # from pinned host memory, the global sort runs (RMI splitters + NCCL
-        # all-to-all + local sort), and the rank's output range is read back to
-        # pinned host memory -- CUDA events around all of it, max over ranks
-        import torch.distributed as tdist
-        hosts = [p.cpu().pin_memory() for p in pristine]
-        # result buffers pinned up front (a rank receives ~n keys; larger ranges
-        # get a fresh buffer); copies in / out on their own streams, pipelined
-        # against the sorts: array i+1 streams in while array i sorts
-        cap = int(1.5 * n) + 4096
-        outs = [torch.empty(cap, dtype=torch.int64, pin_memory=True) for _ in pristine]
-        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-        e2e_ms, d2h = 0.0, 0
-        for step in range(args.e2e_steps + 1):
-            torch.cuda.synchronize()
-            barrier()
             st = torch.cuda.current_stream()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            s_in.wait_stream(st)
-            ev_in = []
-            for i in range(len(hosts)):
-                with torch.cuda.stream(s_in):
-                    work[i].copy_(hosts[i], non_blocking=True)
-                    ev_in.append(torch.cuda.Event())
-                    ev_in[-1].record(s_in)
-            step_d2h, keep = 0, []
-            for i in range(len(hosts)):
-                st.wait_event(ev_in[i])
-                out, _ = sorter.sort(work[i])
-                o64 = out.view(torch.int64)
-                dst = outs[i] if o64.numel() <= cap else torch.empty(o64.numel(), dtype=torch.int64, pin_memory=True)
-                s_out.wait_stream(st)
-                with torch.cuda.stream(s_out):
-                    dst[: o64.numel()].copy_(o64, non_blocking=True)
-                keep.append(out)
-                step_d2h += o64.numel() * 8
-            st.wait_stream(s_out)
+            ctx.sort_batch(work, cfg)
             e1.record(st)
             torch.cuda.synchronize()
+            ms_b.append(e0.elapsed_time(e1))
+        for i in range(len(work)):
+            ok, fv, _ = ctx.verify(work[i])
+            if not ok:
+                raise SystemExit(f"sort_many output {i} not sorted at {fv}")
+        mb = float(np.median(ms_b))
+        line["overlapped"] = {"value": keys_per_step / (mb * 1e-3) / 1e9, "unit": "Gkeys/s", "ms_per_step": mb,
+                              "schedule": "the config's arrays in one lsort_cuda_sort_many call (3 sorts in flight)"}
+    # ---- e2e through the public API from pinned host memory (H2D + D2H inside)
+    if args.e2e_steps > 0:
+        del pristine, work
+        torch.cuda.empty_cache()
+        pins = [torch.empty(n, dtype=torch.float64 if h.dtype == np.float64 else torch.int64, pin_memory=True)
+                for h in hosts]
+        arrs = [p.numpy() if h.dtype == np.float64 else p.numpy().view(np.uint64) for p, h in zip(pins, hosts)]
+        e2e_t = []
+        for step in range(args.e2e_steps + 1):
+            for a, h in zip(arrs, hosts):
+                a[...] = h
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if len(arrs) == 1:
+                ctx.sort(arrs[0], cfg)  # lsort_cuda_sort, LSORT_MEM_HOST
+            else:
+                ctx.sort_batch(arrs, cfg)  # lsort_cuda_sort_batch: copies pipelined against the sorts
+            dt = time.perf_counter() - t0
             if step > 0:
-                e2e_ms += e0.elapsed_time(e1)
-                d2h += step_d2h
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        e2e_ms = float(t.item()) / max(1, args.e2e_steps)
+                e2e_t.append(dt)
+        for a in arrs:  # the end-to-end result is checked, not just timed
+            k = O_encode(a) if a.dtype == np.float64 else a
+            if not np.all(k[1:] >= k[:-1]):
+                raise RuntimeError("e2e sort produced unsorted output")
+        e2e_ms = float(np.mean(e2e_t)) * 1e3
         line["e2e"] = {"value": keys_per_step / (e2e_ms * 1e-3) / 1e9, "unit": "Gkeys/s",
-                       "h2d_bytes_per_step": 8 * n * len(hosts),
-                       "d2h_bytes_per_step": int(d2h / max(1, args.e2e_steps)),
-                       "ms_per_step": e2e_ms, "per_rank_bytes": True}
+                       "h2d_bytes_per_step": 8 * n * len(arrs), "d2h_bytes_per_step": 8 * n * len(arrs),
+                       "ms_per_step": e2e_ms,
+                       "api": "lsort_cuda_sort (LSORT_MEM_HOST)" if len(arrs) == 1 else "lsort_cuda_sort_batch"}
     else:
         line["e2e"] = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        sample_n = min(n, args.cpu_sample)
-        rates, threads = cpu_sort_rate(args.config, sample_n, 2)
-        line["cpu_baseline"] = {"value": float(np.mean(rates)), "unit": "Gkeys/s", "cores": threads,
-                                "kind": "port",
-                                "sample": f"{sample_n} keys of each of {len(work)} config arrays, 2 runs"}
+    if not args.no_cpu:
+        res, threads = cpu_baselines(args.config, args.cpu_runs)
+        port = res["aips2o_port"]
+        line["cpu_baseline"] = {"value": port["value"], "unit": "Gkeys/s", "cores": threads, "kind": "port",
+                                "sample": f"{port['keys']} keys of the config's first array, mean of {port['runs']}",
+                                "cpu_model": lscpu_model(), "algorithms": res}
+    print(json.dumps(line), flush=True)
+
+
+def O_encode(a):
+    from oracle import oracle as O
+    return O.encode(a)
+
+
+PHASES = ("ms_models", "ms_classify", "ms_scatter", "ms_base", "ms_fill")
+PHASE_KERNEL = {"ms_scatter": "k_scatter", "ms_base": "k_base_reg/k_base_smem", "ms_classify": "k_hist"}
+
+
+def run_dist(args):
+    """N > 1 (torchrun, one process per GPU): weak scaling, shard r of the
+    config (keys [r n, (r+1) n) of a world x n dataset), globally sorted
+    across ranks by the multi-GPU driver (paper_2307_08637_b200/dist.py).
+    Max over ranks of the CUDA-event time of each sort."""
+    import torch
+    import torch.distributed as tdist
+    import paper_2307_08637_b200 as L
+    from paper_2307_08637_b200.dist import DistSorter
+    rank, world, local = env_rank()
+    for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533")):
+        os.environ.setdefault(k, v)  # --dist without torchrun: a one-rank group
+    tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    label, dists, n, kind = CONFIGS[args.config]
+    if args.keys:
+        n = args.keys
+    dev = torch.device("cuda", local)
+    hosts = config_arrays(args.config, n, first=rank * n, total=world * n) if kind == "f64" else \
+        config_arrays(args.config, n)
+    pristine = [torch.from_numpy(h.view(np.int64) if h.dtype == np.uint64 else h).to(dev) for h in hosts]
+    work = [torch.empty_like(p) for p in pristine]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ctx = L.Context(local)
+    sorter = DistSorter(ctx, L.SortConfig())
+
+    def one_sort(i):
+        work[i].copy_(pristine[i])
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        tdist.barrier()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        out, stats = sorter.sort(work[i])
+        e1.record(st)
+        torch.cuda.synchronize()
+        tdist.barrier()
+        return e0.elapsed_time(e1), stats, out
+
+    for _ in range(args.warmup):
+        for i in range(len(work)):
+            one_sort(i)
+    for i in range(len(work)):
+        _, _, out = one_sort(i)
+        ok, fv, _ = ctx.verify(out)
+        if not ok:
+            raise SystemExit(f"rank {rank}: output {i} not sorted at {fv}")
+    total_ms, launches = 0.0, 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            for i in range(len(work)):
+                ms, stats, _ = one_sort(i)
+                total_ms += ms
+                launches += (stats.get("local") or {}).get("kernel_launches", 0)
+    clocks = clk.summary()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    keys_per_step = len(work) * n * world
+    value = keys_per_step / (ms_per_step * 1e-3) / 1e9
+    peaks, peak_src = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    P = passes(n)
+    t_roof_ms = (16.0 * P * n / (hbm * 1e9) + 8.0 * n * (world - 1) / world / 900e9) * 1e3 * len(work)
+    line = {"metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": kind, "data": DATA, "config": config_dict(args.config, world, n),
+            "sort_roofline": {"passes": P, "bytes_per_key": 16 * P, "nvlink_bytes_per_key": 8 * (world - 1) / world,
+                              "t_roof_ms_per_step": t_roof_ms, "frac": t_roof_ms / ms_per_step, "hbm_gbs": hbm},
+            "gpu_launches": int(launches), "clocks": clocks, "e2e": None}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if dist_mode:
-        import torch.distributed as tdist
-        tdist.destroy_process_group()
-
+    tdist.destroy_process_group()
 
 def main():
     ap = argparse.ArgumentParser()
@@ -521,13 +577,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
     ap.add_argument("--keys", type=int, default=0, help="override keys per array (testing)")
-    ap.add_argument("--cpu-sample", type=int, default=10_000_000)
+    ap.add_argument("--cpu-runs", type=int, default=10)
+    ap.add_argument("--ref-budget-s", type=float, default=240.0, help="reference arm: time budget of W + K steps")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dist", action="store_true", help="force the distributed path (also at 1 rank)")
-    ap.add_argument("--sequential", action="store_true", help="time the arrays one sort at a time")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: W < 3 violates the timing rules", file=sys.stderr)

@@ -113,7 +113,7 @@ typedef struct lsort_model_info {
 typedef struct lsort_stats {
     double ms_total;                /* device time of the sort (events) */
     double ms_h2d, ms_d2h;          /* LSORT_MEM_HOST transfers */
-    uint32_t levels;                /* distribution levels run */
+    uint32_t levels;                /* distribution levels run (batch / many: summed over the arrays) */
     uint32_t level0_kind;           /* 0 learned, 1 tree, 2 base case only */
     uint64_t partitioned_keys;      /* keys moved by distribution passes (all levels) */
     uint64_t base_case_keys;

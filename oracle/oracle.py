@@ -113,6 +113,9 @@ def lib():
         L.lso_rank_le.restype = u64; L.lso_rank_le.argtypes = [vp, sz, u64]
         L.lso_pivot_quality.restype = f64; L.lso_pivot_quality.argtypes = [vp, sz, vp, sz, C.c_uint32]
         L.lso_eta.restype = f64; L.lso_eta.argtypes = [vp, sz, u64]
+        L.lso_std_sort_u64.restype = None; L.lso_std_sort_u64.argtypes = [vp, u64]
+        L.lso_parallel_sort_u64.restype = None; L.lso_parallel_sort_u64.argtypes = [vp, u64, C.c_int]
+        L.lso_max_threads.restype = C.c_int; L.lso_max_threads.argtypes = []
         _lib = L
     return _lib
 
@@ -164,6 +167,20 @@ def decode(k) -> np.ndarray:
     out = np.empty(k.shape, np.float64)
     lib().lso_decode_doubles(_p(k), _p(out), k.size)
     return out
+
+
+def std_sort(keys) -> np.ndarray:
+    """std::sort on one thread (CPU baseline), in place on uint64 keys."""
+    assert keys.dtype == np.uint64 and keys.flags["C_CONTIGUOUS"]
+    lib().lso_std_sort_u64(_p(keys), keys.size)
+    return keys
+
+
+def parallel_sort(keys, threads: int = 0) -> np.ndarray:
+    """__gnu_parallel::sort on `threads` OpenMP threads (CPU baseline), in place."""
+    assert keys.dtype == np.uint64 and keys.flags["C_CONTIGUOUS"]
+    lib().lso_parallel_sort_u64(_p(keys), keys.size, threads)
+    return keys
 
 
 def rmi_train(sorted_sample, B: int) -> np.ndarray:

@@ -1,9 +1,10 @@
 // basecase.cu -- small-segment sorts and equality fills.
 //
-//   k_base        one CTA per segment, three size classes: 64 threads for
-//                 <= 512 keys, 256 for <= 4096, 1024 for <= 16384 (BlockSort:
-//                 range-adaptive counting pass + rank-within-digit placement),
-//                 decode on store.
+//   k_base_smem / k_base_reg
+//                 one CTA per segment, three size classes: 128 threads for
+//                 <= 1024 keys (TMA into shared memory), 256 for <= 4096 and
+//                 1024 for <= 16384 (keys in registers): range-adaptive
+//                 counting pass + collision fix-up (SmemSort), decode on store.
 //   k_small_sort  whole inputs of <= 16384 keys, in place, NaN check first.
 //   k_fill        equality buckets / homogeneous segments: value stores only.
 // Together they replace radix_base_case_sort + insertion sort
@@ -122,36 +123,6 @@ struct BaseCfg {
     using BS = BlockSort<NT, ITEMS, NBMAX>;
     static constexpr size_t smem = sizeof(uint64_t) * NT * ITEMS + sizeof(typename BS::Smem);
 };
-
-template <int NT, int ITEMS, int NBMAX, bool OUT_F64>
-__global__ void __launch_bounds__(NT) k_base(const BaseItem* items, const unsigned int* count, const uint64_t* src,
-                                            void* out, Ctrl* ctrl, uint32_t list_cap) {
-    griddep_wait();
-    using BS = BlockSort<NT, ITEMS, NBMAX>;
-    extern __shared__ uint4 smem_u4[];
-    uint64_t* a = (uint64_t*)smem_u4;
-    typename BS::Smem& S = *(typename BS::Smem*)(a + NT * ITEMS);
-    if (ctrl->nan_index != ~0ull) return;
-    const uint32_t ni = min(*count, list_cap);
-    for (uint32_t e = blockIdx.x; e < ni; e += gridDim.x) {
-        const BaseItem it = items[e];
-        const uint32_t n = (uint32_t)it.n;
-        uint64_t k[ITEMS];
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            uint32_t idx = threadIdx.x + i * NT;
-            if (idx < n) k[i] = __ldcs((const unsigned long long*)src + it.begin + idx);
-        }
-        BS::sort_regs(k, a, n, S);
-        __syncthreads();
-        for (uint32_t idx = threadIdx.x; idx < n; idx += NT) {
-            uint64_t v = a[idx];
-            if (OUT_F64) __stcs((double*)out + it.begin + idx, decode(v));
-            else __stcs((unsigned long long*)out + it.begin + idx, (unsigned long long)v);
-        }
-        __syncthreads();
-    }
-}
 
 // Whole-input sort for n <= 16384 (one CTA, in place). Detects NaN first.
 template <bool F64>

@@ -508,6 +508,8 @@ struct Engine {
     // level 1 with them instead of sampling a root model over all n keys.
     void sort(void* keys, uint64_t n, bool f64, lsort_stats* stats, bool in_encoded = false,
               const Forward* fw = nullptr, const std::vector<SegPlan>* start = nullptr) {
+        // the bucket ids a dist_histogram left in C->ids are overwritten below
+        C->dist_keys = nullptr;
         if (n < 2) {
             if (n == 1 && f64 && in_encoded) {
                 launch_decode((uint64_t*)keys, n, st);
@@ -1057,7 +1059,7 @@ int lsort_cuda_sort_many(lsort_ctx* C, void* const* keys, const uint64_t* n, uin
             }
             if (stats) {
                 std::lock_guard<std::mutex> g(mu);
-                stats->levels = std::max(stats->levels, sti.levels);
+                stats->levels += sti.levels;  // summed over the arrays (per-array levels = levels / count)
                 stats->partitioned_keys += sti.partitioned_keys;
                 stats->base_case_keys += sti.base_case_keys;
                 stats->fill_keys += sti.fill_keys;
@@ -1146,7 +1148,7 @@ int lsort_cuda_sort_batch(lsort_ctx* C, void* const* keys, const uint64_t* n, ui
             if (!nan) CU(cudaMemcpyAsync(keys[i], C->bat[s].p, n[i] * 8, cudaMemcpyDeviceToHost, C->d2h_stream));
             CU(cudaEventRecord(ev_d2h[s], C->d2h_stream));
             if (stats) {
-                stats->levels = std::max(stats->levels, sti.levels);
+                stats->levels += sti.levels;  // summed over the arrays (per-array levels = levels / count)
                 stats->partitioned_keys += sti.partitioned_keys;
                 stats->base_case_keys += sti.base_case_keys;
                 stats->fill_keys += sti.fill_keys;

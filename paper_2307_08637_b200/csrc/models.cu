@@ -244,8 +244,6 @@ __device__ __noinline__ void train_rmi_block(const uint64_t* s, uint32_t n, uint
     __syncthreads();
     block_fold_scan<NT>(lo, B, false, red, StepMax());
     block_fold_scan<NT>(hi, B, true, red, StepMin());
-    double* hi2 = lo + B;  // lo/hi arrays are adjacent? use registers instead
-    (void)hi2;
     for (uint32_t m = threadIdx.x; m < B; m += NT) {
         double h = hi[m];
         if (m + 1 < B) h = dmin_ref(h, lo[m + 1]);

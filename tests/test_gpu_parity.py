@@ -248,9 +248,10 @@ def test_sort_tree_lookup_table(ctx, case):
     elif case == "skewed_cells":  # many distinct splitters in the first cells, sparse above
         a = np.where(rng.random(n) < 0.7, rng.integers(0, 600, n), rng.integers(0, 1 << 50, n)).astype(np.uint64)
         a[rng.random(n) < 0.2] = 5
-    else:
-        a = np.where(rng.random(n) < 0.5, rng.integers(0, 2000, n),
-                     top - rng.integers(0, 2000, n, dtype=np.uint64)).astype(np.uint64)
+    else:  # both branches uint64 (an int64 / uint64 mix would promote to float64)
+        a = np.where(rng.random(n) < 0.5, rng.integers(0, 2000, n, dtype=np.uint64),
+                     top - rng.integers(0, 2000, n, dtype=np.uint64))
+        assert a.dtype == np.uint64 and np.unique(a[a > (top >> np.uint64(1))]).size == 2000
     d = dev(a)
     st = ctx.sort(d)
     assert st["level0_kind"] == 1, "expected a splitter tree at level 0"
@@ -480,3 +481,55 @@ def test_sort_large_f64(ctx):
     assert ok and h_after == h_before
     check_sorted_f64(x, d.cpu().numpy())
     assert st["levels"] >= 1
+
+
+def _constant_bucket_model(B):
+    """A monotone RMI that predicts 0.5 for every key: every key lands in one
+    bucket (the adversarial model of SPEC.md:440 / acceptance 9)."""
+    P = np.zeros(4 + 4 * B, np.float64)
+    P[:4] = [0.0, 0.0, 0.0, 1.0]  # root slope 0, intercept 0: every key routes to submodel 0
+    e = P[4:].reshape(B, 4)
+    e[:, 0] = 0.0   # slope
+    e[:, 1] = 0.5   # intercept
+    e[:, 2] = 0.5   # lo
+    e[:, 3] = 0.5   # hi
+    return P
+
+
+@pytest.mark.parametrize("case", ["uniform_u64", "normal_enc", "clustered_u64"])
+def test_sort_no_progress_fallback(ctx, case):
+    """Depth-cap / no-progress fallback: a forwarded root
+    model that maps every key to one bucket makes no progress, so the child is
+    flagged kSegForceRadix and split by the range-adaptive radix model
+    (partition.cu k_scan_children, k_hist<kRadix>). The sort must still
+    terminate, be bit-exact and stay within 10x the normal sort time."""
+    import time
+    n, B = 1_000_000, 1024
+    rng = np.random.default_rng(5)
+    if case == "uniform_u64":
+        k = rng.integers(0, 2**64 - 1, n, dtype=np.uint64, endpoint=True)
+    elif case == "normal_enc":
+        k = O.encode(O.generate("normal", n, 7))
+    else:  # a few tight clusters far apart: several radix levels
+        c = rng.integers(0, 4, n).astype(np.uint64) << np.uint64(60)
+        k = c + rng.integers(0, 1 << 20, n, dtype=np.uint64)
+    P = _constant_bucket_model(B)
+    exp = np.sort(k)
+    d = dev(k)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st = ctx.sort_forward(d, P, B, 0, B, None)
+    torch.cuda.synchronize()
+    t_fb = time.perf_counter() - t0
+    assert np.array_equal(host_u64(d), exp)
+    assert st["levels"] >= 2  # the forwarded level made no progress, the radix level did
+    d2 = dev(k)
+    ctx.sort(d2)  # warm
+    d2 = dev(k)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx.sort(d2)
+    torch.cuda.synchronize()
+    t_norm = time.perf_counter() - t0
+    assert np.array_equal(host_u64(d2), exp)
+    assert t_fb <= 10 * max(t_norm, 1e-3), (t_fb, t_norm)
