@@ -499,12 +499,14 @@ PHASE_KERNEL = {"ms_scatter": "k_scatter", "ms_base": "k_base_reg/k_base_smem", 
 def run_dist(args):
     """N > 1 (torchrun, one process per GPU): weak scaling, shard r of the
     config (keys [r n, (r+1) n) of a world x n dataset), globally sorted
-    across ranks by the multi-GPU driver (paper_2307_08637_b200/dist.py).
+    across ranks by the multi-GPU driver (lsort_cuda_sort_dist through
+    paper_2307_08637_b200.dist.DistContext: global model, rank cuts, the
+    exchange fused into the level-0 scatter over NVLink, local sort).
     Max over ranks of the CUDA-event time of each sort."""
     import torch
     import torch.distributed as tdist
     import paper_2307_08637_b200 as L
-    from paper_2307_08637_b200.dist import DistSorter
+    from paper_2307_08637_b200.dist import DistContext
     rank, world, local = env_rank()
     for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533")):
         os.environ.setdefault(k, v)  # --dist without torchrun: a one-rank group
@@ -518,8 +520,9 @@ def run_dist(args):
     pristine = [torch.from_numpy(h.view(np.int64) if h.dtype == np.uint64 else h).to(dev) for h in hosts]
     work = [torch.empty_like(p) for p in pristine]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    ctx = L.Context(local)
-    sorter = DistSorter(ctx, L.SortConfig())
+    ctx = L.Context(local)  # (verify)
+    dc = DistContext(local)  # one rank of the multi-GPU driver (the library owns its NCCL communicator)
+    cfg = L.SortConfig()
 
     def one_sort(i):
         work[i].copy_(pristine[i])
@@ -530,7 +533,7 @@ def run_dist(args):
         st = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        out, stats = sorter.sort(work[i])
+        out, stats = dc.sort(work[i], cfg)
         e1.record(st)
         torch.cuda.synchronize()
         tdist.barrier()
@@ -550,7 +553,7 @@ def run_dist(args):
             for i in range(len(work)):
                 ms, stats, _ = one_sort(i)
                 total_ms += ms
-                launches += (stats.get("local") or {}).get("kernel_launches", 0)
+                launches += stats.get("kernel_launches", 0)
     clocks = clk.summary()
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)

@@ -7,6 +7,8 @@
 //   lsort::sort(std::span<lsort::Key>(v)); // host uint64 keys (copied in/out)
 //   lsort::sort(std::span<double>(d));     // host float64; NaN -> lsort::nan_error
 //   lsort::sort(lsort::device_span<double>{dptr, n});  // keys already in HBM
+//   lsort::dist_sorter ds(dev, world, rank, &id);    // multi-GPU (one process per GPU)
+//   size_t m = ds.sort(device_span<double>{shard, n}, device_span<double>{out, cap});
 //
 // Errors mirror the reference: invalid configuration -> std::invalid_argument
 // (models.cpp:40-43), NaN -> lsort::nan_error (derived from
@@ -17,6 +19,7 @@
 #ifndef LSORT_LSORT_HPP
 #define LSORT_LSORT_HPP
 
+#include <array>
 #include <cstddef>
 #include <cstdint>
 #include <span>
@@ -167,6 +170,52 @@ inline void sort(device_span<Key> a, const SortConfig& cfg = {}) {
 inline void sort(device_span<double> a, const SortConfig& cfg = {}) {
     detail::run(a.data, a.size, LSORT_KEY_F64, LSORT_MEM_DEVICE, cfg);
 }
+
+// ---- multi-GPU (lsort_cuda_sort_dist, one process per GPU) ----------------
+// The distributed sort(a, cfg): every rank of a `world`-rank group holds a
+// device shard; after sort() this rank holds the rank-th key range of the
+// global order in `out`. The library owns the NCCL communicator: rank 0 calls
+// nccl_unique_id() and the caller ships the 128 bytes to the other ranks (MPI,
+// a file, torch.distributed ...). world == 1 needs no id. Collective: every
+// rank calls sort() with its shard. A NaN anywhere -> nan_error on every rank
+// (index() is meaningful on the owning rank only, ~0 elsewhere).
+using nccl_id = std::array<char, 128>;
+inline nccl_id nccl_unique_id() {
+    nccl_id id{};
+    int rc = lsort_nccl_unique_id(id.data());
+    if (rc != LSORT_OK) throw cuda_error(rc, "lsort: NCCL is not available");
+    return id;
+}
+
+class dist_sorter {
+public:
+    dist_sorter(int device, int world, int rank, const nccl_id* id = nullptr) {
+        int rc = lsort_cuda_dist_create(&h_, device, world, rank, id ? id->data() : nullptr);
+        if (rc != LSORT_OK) throw cuda_error(rc, "lsort::dist_sorter: cannot join the group");
+    }
+    ~dist_sorter() {
+        if (h_) lsort_cuda_dist_destroy(h_);
+    }
+    dist_sorter(const dist_sorter&) = delete;
+    dist_sorter& operator=(const dist_sorter&) = delete;
+    // Returns the number of keys of this rank's range written to out.data.
+    template <class T>
+    std::size_t sort(device_span<T> shard, device_span<T> out, const SortConfig& cfg = {}) {
+        static_assert(std::is_same_v<T, Key> || std::is_same_v<T, double>, "uint64 or double keys");
+        lsort_cfg c = cfg.to_c();
+        std::uint64_t n_out = 0, nan = ~0ull;
+        const int kind = std::is_same_v<T, double> ? LSORT_KEY_F64 : LSORT_KEY_U64;
+        int rc = lsort_cuda_sort_dist(h_, shard.data, shard.size, kind, out.data, out.size, &n_out, &c, nullptr, &nan);
+        if (rc == LSORT_OK) return n_out;
+        if (rc == LSORT_ENAN) throw nan_error(nan);
+        std::string msg = lsort_cuda_dist_last_error(h_);
+        if (rc == LSORT_EINVAL) throw std::invalid_argument("lsort::dist_sorter::sort: " + msg);
+        throw cuda_error(rc, "lsort::dist_sorter::sort: " + msg + " (range " + std::to_string(n_out) + " keys)");
+    }
+
+private:
+    lsort_dist* h_ = nullptr;
+};
 
 }  // namespace lsort
 

@@ -24,7 +24,9 @@
  *   lsort_gen_keys           <- data.generate
  *   lsort_read_keys / lsort_write_keys <- data.read_keys / write_keys SPEC.md:480-497
  *   (lsort_cli, csrc/cli.cpp  <- bench-cli generate / bench / verify SPEC.md:521-590)
- *   lsort_cuda_dist_*        <- (none: multi-GPU layer is new)
+ *   lsort_cuda_sort_dist / lsort_cuda_sort_multi
+ *                            <- sort(a, cfg) with `workers` spanning GPUs;
+ *                               the multi-GPU layer itself is new (SURVEY.md 8(b),(e))
  *
  * Conventions: return 0 (LSORT_OK) or an LSORT_E* code; the message is
  * available from lsort_cuda_last_error(ctx). LSORT_EINVAL mirrors the
@@ -265,26 +267,6 @@ int lsort_cuda_sort_forward(lsort_ctx* ctx, void* d_keys, uint64_t n, int key_ki
                             uint32_t b_hi, const uint64_t* d_sorted_sample, uint64_t sample_n,
                             lsort_stats* stats, uint64_t* nan_index_out);
 
-/* ---- multi-GPU phases (one process per GPU; collectives via the caller) ---- */
-/* Draw this rank's sample share (encoded keys) into device d_out[s]. */
-int lsort_cuda_dist_sample(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,
-                           uint64_t seed, uint64_t s, uint64_t* d_out);
-/* Sort the gathered global sample in place and train the global RMI with
- * `buckets` output buckets (deterministic: identical on every rank). */
-int lsort_cuda_dist_train(lsort_ctx* ctx, uint64_t* d_sample, uint64_t s, uint32_t buckets,
-                          lsort_rmi_header* h_out, lsort_rmi_entry* entries_out);
-/* Histogram of the local shard under the global model: d_hist[buckets]. */
-int lsort_cuda_dist_histogram(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,
-                              const lsort_rmi_header* h, const lsort_rmi_entry* entries,
-                              uint64_t* d_hist);
-/* Partition the local shard into destination-major order in d_out (encoded
- * keys): destination r receives buckets [bucket_bounds[r], bucket_bounds[r+1]).
- * send_counts[p] (host) is filled. */
-int lsort_cuda_dist_partition(lsort_ctx* ctx, const void* d_keys, uint64_t n, int key_kind,
-                              const lsort_rmi_header* h, const lsort_rmi_entry* entries,
-                              const uint32_t* bucket_bounds, uint32_t nranks, uint64_t* d_out,
-                              uint64_t* send_counts /* nullable with the identity map: the
-                                                       cursors are then scanned on the device */);
 /* Local sort of a rank's received keys when they are already grouped by the
  * global model's buckets [b_lo, b_hi) (bucket_sizes[b - b_lo] keys each, in
  * bucket order): buckets within the base-case capacity are sorted in place, the
@@ -295,13 +277,68 @@ int lsort_cuda_sort_buckets(lsort_ctx* ctx, void* d_keys, uint64_t n, int key_ki
                             const lsort_rmi_header* h, const lsort_rmi_entry* entries, uint32_t b_lo,
                             uint32_t b_hi, const uint64_t* bucket_sizes /* host */,
                             const uint64_t* d_sorted_sample, uint64_t sample_n, lsort_stats* stats);
-/* Device run gather: for r < nruns, copy runs[3r+2] keys from d_src + runs[3r]
- * to d_dst + runs[3r+1] (runs: host array) -- the all-to-all's source-major
- * receive buffer to bucket-major order. */
-int lsort_cuda_copy_runs(lsort_ctx* ctx, const uint64_t* d_src, uint64_t* d_dst, const uint64_t* runs,
-                         uint64_t nruns);
 /* Decode encoded keys to float64 in place (after a distributed sort). */
 int lsort_cuda_decode_inplace(lsort_ctx* ctx, uint64_t* d_keys, uint64_t n);
+
+/* ---- multi-GPU driver (dist.cu; SURVEY.md 8(b),(e)) --------------------------
+ * The distributed form of sort(a, cfg) (`workers` across
+ * GPUs): every rank holds a shard; afterwards rank r holds the r-th key range
+ * of the global sorted order (variable length), so the concatenation over
+ * ranks is the sorted input. The library owns the NCCL communicator (NCCL is
+ * loaded at run time; the single-GPU API does not need it). Per sort: the
+ * global partition model (RMI, or a splitter tree when the RMI cannot balance
+ * the ranks) is trained on a gathered global sample; rank cuts are chosen on
+ * the all-gathered level-0 histograms; the exchange is fused into the level-0
+ * scatter as NVLink stores into the owners' receive buffers (CUDA IPC); each
+ * rank then sorts its range from level 1. A NaN in any shard fails every rank
+ * with LSORT_ENAN (the owning rank gets the index). Collective: every rank
+ * makes the same sequence of calls. */
+typedef struct lsort_dist lsort_dist;
+
+/* 1 when an NCCL library could be loaded into this process. */
+int lsort_nccl_available(void);
+/* ncclGetUniqueId into out[128] (rank 0; broadcast it to the other ranks). */
+int lsort_nccl_unique_id(void* out128);
+/* One rank of a `world`-rank group on `device`. nccl_id: the 128-byte id from
+ * lsort_nccl_unique_id, or NULL with world == 1 (no NCCL needed). */
+int lsort_cuda_dist_create(lsort_dist** out, int device, int world, int rank, const void* nccl_id);
+int lsort_cuda_dist_destroy(lsort_dist* d);
+const char* lsort_cuda_dist_last_error(const lsort_dist* d);
+int lsort_cuda_dist_set_stream(lsort_dist* d, void* cuda_stream);
+/* Globally sort the device shard d_keys[n] (LSORT_KEY_U64 / LSORT_KEY_F64).
+ * The rank's key range (*n_out keys) is written to d_out (capacity out_cap;
+ * d_out may equal d_keys). If any rank's out_cap is below its range, every
+ * rank returns LSORT_ENOMEM with *n_out set. d_out == NULL: the range stays
+ * in a library buffer (lsort_cuda_dist_result). stats (nullable): this rank's
+ * counters; ms_total = device time on this rank. */
+int lsort_cuda_sort_dist(lsort_dist* d, void* d_keys, uint64_t n, int key_kind, void* d_out, uint64_t out_cap,
+                         uint64_t* n_out, const lsort_cfg* cfg, lsort_stats* stats, uint64_t* nan_index_out);
+/* The library buffer holding the last range sorted with d_out == NULL
+ * (encoded keys for LSORT_KEY_F64 are decoded; valid until the next call). */
+int lsort_cuda_dist_result(lsort_dist* d, void** d_keys, uint64_t* n);
+/* One process, `ndev` GPUs (ncclCommInitAll; one host thread per device):
+ * shard i on devices[i], output range i into d_outs[i] (capacity out_caps[i]).
+ * stats / nan_index_out / n_outs: per device, nullable. err (nullable): first
+ * failing rank's message. */
+int lsort_cuda_sort_multi(uint32_t ndev, const int* devices, void* const* d_shards, const uint64_t* n, int key_kind,
+                          void* const* d_outs, const uint64_t* out_caps, uint64_t* n_outs, const lsort_cfg* cfg,
+                          lsort_stats* stats, uint64_t* nan_index_out, char* err, size_t errlen);
+/* TEST ENTRY: `world` virtual ranks on ONE device, one host thread each,
+ * collectives emulated by host barriers + device copies (no kernel waits on
+ * another). Runs the multi-GPU driver's data path -- global model, rank cuts,
+ * exchange fused into the scatter, local sorts -- at world > 1 on one GPU. */
+int lsort_cuda_dist_emulate(int device, uint32_t world, void* const* d_shards, const uint64_t* n, int key_kind,
+                            void* const* d_outs, const uint64_t* out_caps, uint64_t* n_outs, const lsort_cfg* cfg,
+                            lsort_stats* stats, uint64_t* nan_index_out, char* err, size_t errlen);
+/* Host-only: the driver's rank plan from the world x nb bucket counts H
+ * (source-major) and per-bucket equality flags eq (nullable). cuts[world+1]:
+ * positions in the global order (bucket boundaries, or anywhere inside an
+ * equality bucket); recv[world]: keys per rank; dest[nb] / dest_off[nb]
+ * (nullable): owner rank of each moved bucket (~0 for empty / equality) and
+ * the position of `rank`'s first key of it in the owner's buffer; pieces
+ * (nullable, 3 x nb): `rank`'s received (bucket, local offset, count). */
+int lsort_dist_plan(uint32_t world, uint32_t nb, const uint64_t* H, const uint8_t* eq, uint32_t rank, uint64_t* cuts,
+                    uint64_t* recv, uint32_t* dest, uint64_t* dest_off, uint64_t* pieces, uint32_t* npieces);
 
 #ifdef __cplusplus
 }

@@ -359,6 +359,15 @@ uint32_t lso_tree_classify(const lso_tree* t, uint64_t x) {
     return t->eq_offset[base] + eq;
 }
 
+/* Bulk forms of the two classifiers above (one call per array; test helpers). */
+void lso_learned_bucket_many(const double* P, uint32_t B, uint32_t bucket_count, double cdf_lo, double cdf_hi,
+                             const uint64_t* x, size_t n, uint32_t* out) {
+    for (size_t i = 0; i < n; ++i) out[i] = lso_learned_bucket(P, B, bucket_count, cdf_lo, cdf_hi, x[i]);
+}
+void lso_tree_classify_many(const lso_tree* t, const uint64_t* x, size_t n, uint32_t* out) {
+    for (size_t i = 0; i < n; ++i) out[i] = lso_tree_classify(t, x[i]);
+}
+
 /* models.cpp:187-193 */
 double lso_duplicate_fraction(const uint64_t* s, size_t n) {
     if (n == 0) return 0.0;

@@ -70,7 +70,10 @@ typedef struct lso_tree {
 } lso_tree;
 int lso_tree_build(const uint64_t* sorted, size_t n, uint32_t budget, int equality_mode,
                    lso_tree* t);                                    /* models.cpp:133-185 */
-uint32_t lso_tree_classify(const lso_tree* t, uint64_t x);          /* models.hpp:92-101 */
+uint32_t lso_tree_classify(const lso_tree* t, uint64_t x);
+void lso_learned_bucket_many(const double* P, uint32_t B, uint32_t bucket_count, double cdf_lo, double cdf_hi,
+                             const uint64_t* x, size_t n, uint32_t* out);
+void lso_tree_classify_many(const lso_tree* t, const uint64_t* x, size_t n, uint32_t* out);          /* models.hpp:92-101 */
 double lso_duplicate_fraction(const uint64_t* sorted, size_t n);    /* models.cpp:187-193 */
 
 /* ---- verify.hpp -------------------------------------------------------- */

@@ -113,6 +113,10 @@ def lib():
         L.lso_rank_le.restype = u64; L.lso_rank_le.argtypes = [vp, sz, u64]
         L.lso_pivot_quality.restype = f64; L.lso_pivot_quality.argtypes = [vp, sz, vp, sz, C.c_uint32]
         L.lso_eta.restype = f64; L.lso_eta.argtypes = [vp, sz, u64]
+        L.lso_learned_bucket_many.restype = None
+        L.lso_learned_bucket_many.argtypes = [vp, C.c_uint32, C.c_uint32, f64, f64, vp, sz, vp]
+        L.lso_tree_classify_many.restype = None
+        L.lso_tree_classify_many.argtypes = [C.POINTER(Tree), vp, sz, vp]
         L.lso_std_sort_u64.restype = None; L.lso_std_sort_u64.argtypes = [vp, u64]
         L.lso_parallel_sort_u64.restype = None; L.lso_parallel_sort_u64.argtypes = [vp, u64, C.c_int]
         L.lso_max_threads.restype = C.c_int; L.lso_max_threads.argtypes = []
@@ -207,9 +211,11 @@ def rmi_predict(P: np.ndarray, B: int, keys) -> np.ndarray:
 
 
 def learned_bucket(P, B, bucket_count, keys, cdf_lo=0.0, cdf_hi=1.0) -> np.ndarray:
-    L = lib()
-    return np.array([L.lso_learned_bucket(_p(P), B, bucket_count, cdf_lo, cdf_hi, int(k))
-                     for k in _u64(keys)], np.uint32)
+    k = _u64(keys).reshape(-1)
+    P = np.ascontiguousarray(P, np.float64)
+    out = np.empty(k.size, np.uint32)
+    lib().lso_learned_bucket_many(_p(P), B, bucket_count, cdf_lo, cdf_hi, _p(k), k.size, _p(out))
+    return out
 
 
 def tree_build(sorted_sample, budget: int, equality_mode: bool = True) -> Tree:
@@ -221,8 +227,10 @@ def tree_build(sorted_sample, budget: int, equality_mode: bool = True) -> Tree:
 
 
 def tree_classify(t: Tree, keys) -> np.ndarray:
-    L = lib()
-    return np.array([L.lso_tree_classify(C.byref(t), int(k)) for k in _u64(keys)], np.uint32)
+    k = _u64(keys).reshape(-1)
+    out = np.empty(k.size, np.uint32)
+    lib().lso_tree_classify_many(C.byref(t), _p(k), k.size, _p(out))
+    return out
 
 
 def duplicate_fraction(sorted_sample) -> float:

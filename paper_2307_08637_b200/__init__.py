@@ -47,7 +47,7 @@ class NanError(ValueError):
     """NaN in float64 input (keys.hpp:34-42: rejected at ingestion with its index)."""
 
     def __init__(self, index: int):
-        super().__init__(f"NaN at index {index}")
+        super().__init__(f"NaN at index {index}" if index >= 0 else "NaN in another rank's shard")
         self.index = index
 
 
@@ -251,14 +251,6 @@ class Context:
                                              sz.ctypes.data_as(C.c_void_p), sp, sn, C.byref(stats))
         _check(self, rc)
         return stats.as_dict()
-
-    def copy_runs(self, d_src, d_dst, runs: np.ndarray):
-        """lsort_cuda_copy_runs: d_dst[dst_off:+len] = d_src[src_off:+len] per run row."""
-        self._sync_stream()
-        r = np.ascontiguousarray(np.asarray(runs, dtype=np.uint64).reshape(-1, 3))
-        rc = N.lib().lsort_cuda_copy_runs(self._h, C.c_void_p(d_src.data_ptr()), C.c_void_p(d_dst.data_ptr()),
-                                          r.ctypes.data_as(C.c_void_p), r.shape[0])
-        _check(self, rc)
 
     # -- unit entry points (parity tests) --------------------------------------
     def rmi_train(self, d_sorted_sample, submodels: int):

@@ -72,10 +72,11 @@ EXPORTS = [
     "lsort_cfg_default", "lsort_cuda_ctx_create", "lsort_cuda_ctx_destroy", "lsort_cuda_last_error",
     "lsort_cuda_set_stream", "lsort_cuda_sort", "lsort_cuda_sort_batch", "lsort_cuda_sort_many", "lsort_read_keys", "lsort_write_keys", "lsort_cuda_sort_forward", "lsort_cuda_rmi_train", "lsort_cuda_classify_rmi",
     "lsort_cuda_tree_build", "lsort_cuda_classify_tree", "lsort_cuda_build_model",
-    "lsort_cuda_block_sort", "lsort_cuda_verify", "lsort_gen_keys", "lsort_cuda_dist_sample",
-    "lsort_cuda_dist_train", "lsort_cuda_dist_histogram", "lsort_cuda_dist_partition",
-    "lsort_cuda_decode_inplace", "lsort_cuda_learned_pivots", "lsort_cuda_pivot_quality", "lsort_cuda_eta",
-    "lsort_cuda_sort_buckets", "lsort_cuda_copy_runs",
+    "lsort_cuda_block_sort", "lsort_cuda_verify", "lsort_gen_keys", "lsort_cuda_decode_inplace", "lsort_cuda_learned_pivots", "lsort_cuda_pivot_quality", "lsort_cuda_eta",
+    "lsort_cuda_sort_buckets", "lsort_nccl_available", "lsort_nccl_unique_id",
+    "lsort_cuda_dist_create", "lsort_cuda_dist_destroy", "lsort_cuda_dist_last_error", "lsort_cuda_dist_set_stream",
+    "lsort_cuda_sort_dist", "lsort_cuda_dist_result", "lsort_cuda_sort_multi", "lsort_cuda_dist_emulate",
+    "lsort_dist_plan",
 ]
 
 _lib = None
@@ -139,20 +140,35 @@ def lib():
     L.lsort_cuda_sort_buckets.restype = i32
     L.lsort_cuda_sort_buckets.argtypes = [vp, vp, u64, i32, P(lsort_cfg), P(lsort_rmi_header), vp, u32, u32, vp, vp,
                                           u64, P(lsort_stats)]
-    L.lsort_cuda_copy_runs.restype = i32
-    L.lsort_cuda_copy_runs.argtypes = [vp, vp, vp, vp, u64]
     L.lsort_cuda_eta.argtypes = [vp, vp, u64, i32, u64, P(f64)]
     L.lsort_gen_keys.restype = i32
     L.lsort_gen_keys.argtypes = [i32, u64, u64, u64, u64, vp, i32]
-    L.lsort_cuda_dist_sample.restype = i32
-    L.lsort_cuda_dist_sample.argtypes = [vp, vp, u64, i32, u64, u64, vp]
-    L.lsort_cuda_dist_train.restype = i32
-    L.lsort_cuda_dist_train.argtypes = [vp, vp, u64, u32, P(lsort_rmi_header), vp]
-    L.lsort_cuda_dist_histogram.restype = i32
-    L.lsort_cuda_dist_histogram.argtypes = [vp, vp, u64, i32, P(lsort_rmi_header), vp, vp]
-    L.lsort_cuda_dist_partition.restype = i32
-    L.lsort_cuda_dist_partition.argtypes = [vp, vp, u64, i32, P(lsort_rmi_header), vp, vp, u32, vp, vp]
     L.lsort_cuda_decode_inplace.restype = i32
     L.lsort_cuda_decode_inplace.argtypes = [vp, vp, u64]
+    # multi-GPU driver (dist.cu)
+    L.lsort_nccl_available.restype = i32
+    L.lsort_nccl_available.argtypes = []
+    L.lsort_nccl_unique_id.restype = i32
+    L.lsort_nccl_unique_id.argtypes = [vp]
+    L.lsort_cuda_dist_create.restype = i32
+    L.lsort_cuda_dist_create.argtypes = [P(vp), i32, i32, i32, vp]
+    L.lsort_cuda_dist_destroy.restype = i32
+    L.lsort_cuda_dist_destroy.argtypes = [vp]
+    L.lsort_cuda_dist_last_error.restype = C.c_char_p
+    L.lsort_cuda_dist_last_error.argtypes = [vp]
+    L.lsort_cuda_dist_set_stream.restype = i32
+    L.lsort_cuda_dist_set_stream.argtypes = [vp, vp]
+    L.lsort_cuda_sort_dist.restype = i32
+    L.lsort_cuda_sort_dist.argtypes = [vp, vp, u64, i32, vp, u64, P(u64), P(lsort_cfg), P(lsort_stats), P(u64)]
+    L.lsort_cuda_dist_result.restype = i32
+    L.lsort_cuda_dist_result.argtypes = [vp, P(vp), P(u64)]
+    L.lsort_cuda_sort_multi.restype = i32
+    L.lsort_cuda_sort_multi.argtypes = [u32, vp, vp, vp, i32, vp, vp, vp, P(lsort_cfg), vp, vp, C.c_char_p,
+                                        C.c_size_t]
+    L.lsort_cuda_dist_emulate.restype = i32
+    L.lsort_cuda_dist_emulate.argtypes = [i32, u32, vp, vp, i32, vp, vp, vp, P(lsort_cfg), vp, vp, C.c_char_p,
+                                          C.c_size_t]
+    L.lsort_dist_plan.restype = i32
+    L.lsort_dist_plan.argtypes = [u32, u32, vp, vp, u32, vp, vp, vp, vp, vp, P(u32)]
     _lib = L
     return L

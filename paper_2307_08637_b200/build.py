@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
            "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
-CU_SOURCES = ["partition.cu", "models.cu", "basecase.cu", "cluster.cu", "util.cu", "engine.cu"]
+CU_SOURCES = ["partition.cu", "models.cu", "basecase.cu", "cluster.cu", "util.cu", "engine.cu", "dist.cu"]
 CPP_SOURCES = ["gen.cpp", "keyio.cpp"]
 
 
@@ -70,7 +70,7 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
     if jobs or _stale(LIB, objs):
         tmp = LIB + ".tmp"
         _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs +
-             ["-Xcompiler", "-fopenmp", "-lcudart", "-lgomp"])
+             ["-Xcompiler", "-fopenmp", "-lcudart", "-lgomp", "-ldl"])
         os.replace(tmp, LIB)
     # the command-line harness (SPEC.md bench-cli), linked against the library
     cli_src = os.path.join(CSRC, "cli.cpp")

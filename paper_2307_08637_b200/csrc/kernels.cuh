@@ -79,6 +79,8 @@ struct LevelParams {
     uint64_t* ktp;                 // [3][kstride+1] tile prefixes per kind
     KindPlan* kplan;               // [3]
     uint32_t kstride;
+    uint32_t remote;               // k_scatter: cursors address peer GPUs' receive buffers
+                                   // (multi-GPU exchange fused into the scatter, dist.cu)
 };
 
 // Sort configuration as seen by kernels.
@@ -135,8 +137,9 @@ size_t train_workspace_bytes(uint64_t s, uint32_t B);
 // GPU policy (DevCfg::quality) for a big segment's learned model trained on the
 // sorted sample: classify the sample, fall back to a splitter tree if poor.
 // offs (nullable): also returns the final model's bucket offsets in the sample
+// share_den > 0: also poor when the largest bucket holds more than 1/share_den of the sample
 void launch_quality_check(const uint64_t* sorted, uint64_t s, uint8_t* model, uint32_t tree_k, void* ws,
-                          uint32_t* offs, const uint32_t* gate, cudaStream_t st);
+                          uint32_t* offs, const uint32_t* gate, cudaStream_t st, uint32_t share_den = 0);
 size_t quality_workspace_bytes();
 // offsets[b] = first index of the sorted sample whose bucket (under `model`) is >= b, b <= nb
 void launch_sample_slices(const uint64_t* sorted, uint64_t s, const uint8_t* model, uint32_t* offsets,
@@ -152,8 +155,6 @@ void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_
 void launch_scan_children(const LevelParams& p, uint32_t max_nb, cudaStream_t st);
 // scatter of every segment of the level (all kinds), bucket ids from k_hist in p.ids
 void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid, cudaStream_t st);
-void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,
-                           cudaStream_t st);
 // basecase.cu
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
 void launch_base_class(const LevelParams& p, int cls, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
@@ -170,10 +171,6 @@ void launch_verify(const void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream
 // Alg. 4 per-cell maxima (gmax / ghit zeroed by the caller, nbuckets cells)
 void launch_learned_pivots(const uint8_t* model, const void* keys, uint64_t n, int in_f64, unsigned long long* gmax,
                            unsigned int* ghit, int payload, cudaStream_t st);
-// out[i] = sum(in[0, i)), n <= kMaxNB, one CTA
-void launch_excl_scan_u64(const unsigned long long* in, unsigned long long* out, uint32_t n, cudaStream_t st);
-// dst[dst_off + i] = src[src_off + i] for every run (src_off, dst_off, len) in runs (device)
-void launch_copy_runs(const uint64_t* src, uint64_t* dst, const uint64_t* runs, uint64_t nruns, cudaStream_t st);
 // ranks[i] = #keys <= pivots[i] (pivots encoded when f64)
 void launch_rank_le(const void* sorted, uint64_t n, int f64, const uint64_t* pivots, uint32_t np, uint64_t* ranks,
                     cudaStream_t st);

@@ -641,8 +641,8 @@ __device__ __forceinline__ TileGeom tile_geom_all(const LevelParams& p, uint64_t
     return g;
 }
 
-template <bool IN_F64, bool MAPPED, uint32_t NBC>
-__global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, const uint32_t* map, uint32_t nmapped) {
+template <bool IN_F64, uint32_t NBC>
+__global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
     griddep_wait();
     extern __shared__ uint4 smem_u4[];
     ScatterSmem<NBC>& Q = *(ScatterSmem<NBC>*)smem_u4;
@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
         if ((int64_t)i != cur) {
             const SegDesc& sd = p.segs[i];
             boff = sd.bucket_off;
-            nbo = MAPPED ? nmapped : sd.nb_max;
+            nbo = sd.nb_max;
             cur = i;
         }
         TS.wait(g, tb);  // keys and ids of this tile have landed
@@ -726,7 +726,6 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
             for (int q = 0; q < kPItems; ++q) {
                 uint32_t b = (q & 1) ? (idp[q >> 1] >> 16) : (idp[q >> 1] & 0xffffu);
                 const bool ok = b != kNoMove;
-                if (MAPPED && ok) b = map[b];
                 const uint32_t r = hist_rank_warp(cnt, b, ok);
                 code[q] = ok ? (b << 16 | r) : 0xffffffffu;
             }
@@ -735,7 +734,6 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
             for (int q = 0; q < kPItems; ++q) {
                 uint32_t b = (q & 1) ? (idp[q >> 1] >> 16) : (idp[q >> 1] & 0xffffu);
                 const bool ok = b != kNoMove;
-                if (MAPPED && ok) b = map[b];
                 code[q] = ok ? (b << 16 | atomicAdd(&cnt[b], 1u)) : 0xffffffffu;
             }
         }
@@ -745,7 +743,6 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
             const uint64_t ix = g.single(threadIdx.x);
             uint32_t b = p.ids[ix];
             if (b != kNoMove) {
-                if (MAPPED) b = map[b];
                 scode = b << 16 | atomicAdd(&cnt[b], 1u);
                 skey = load_key(p.src, ix, IN_F64);
             }
@@ -840,6 +837,9 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p, con
         // barrier: the counters alternate by tile parity)
         fence_proxy_async_smem();
     }
+    // stores into peer GPUs' memory are ordered before the stream-ordered
+    // barrier collective that follows this kernel (dist.cu)
+    if (p.remote) __threadfence_system();
 }
 
 // ------------------------------------------------------------- launchers
@@ -852,14 +852,10 @@ void partition_init(int optin) {
     allow_smem(k_hist<false, kTree>, optin);
     allow_smem(k_hist<true, kRadix>, optin);
     allow_smem(k_hist<false, kRadix>, optin);
-    allow_smem(k_scatter<true, false, 1024>, optin);
-    allow_smem(k_scatter<false, false, 1024>, optin);
-    allow_smem(k_scatter<true, false, kMaxNB>, optin);
-    allow_smem(k_scatter<false, false, kMaxNB>, optin);
-    allow_smem(k_scatter<true, true, 1024>, optin);
-    allow_smem(k_scatter<true, true, kMaxNB>, optin);
-    allow_smem(k_scatter<false, true, kMaxNB>, optin);
-    allow_smem(k_scatter<false, true, 1024>, optin);
+    allow_smem(k_scatter<true, 1024>, optin);
+    allow_smem(k_scatter<false, 1024>, optin);
+    allow_smem(k_scatter<true, kMaxNB>, optin);
+    allow_smem(k_scatter<false, kMaxNB>, optin);
     allow_smem(k_scan_children<128>, optin);
     allow_smem(k_scan_children<512>, optin);
     allow_smem(k_scan_children<1024>, optin);
@@ -899,25 +895,12 @@ void launch_scan_children(const LevelParams& p, uint32_t max_nb, cudaStream_t st
 void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid, cudaStream_t st) {
     if (nb_cap <= 1024) {
         constexpr size_t sm = sizeof(ScatterSmem<1024>);
-        if (in_f64) pdl(k_scatter<true, false, 1024>, grid, kPNT, sm, st, p, nullptr, 0);
-        else pdl(k_scatter<false, false, 1024>, grid, kPNT, sm, st, p, nullptr, 0);
+        if (in_f64) pdl(k_scatter<true, 1024>, grid, kPNT, sm, st, p);
+        else pdl(k_scatter<false, 1024>, grid, kPNT, sm, st, p);
     } else {
         constexpr size_t sm = sizeof(ScatterSmem<kMaxNB>);
-        if (in_f64) pdl(k_scatter<true, false, kMaxNB>, grid, kPNT, sm, st, p, nullptr, 0);
-        else pdl(k_scatter<false, false, kMaxNB>, grid, kPNT, sm, st, p, nullptr, 0);
-    }
-}
-
-void launch_scatter_mapped(const LevelParams& p, int in_f64, const uint32_t* map, uint32_t nmapped, int grid,
-                           cudaStream_t st) {
-    if (nmapped <= 1024) {
-        constexpr size_t sm = sizeof(ScatterSmem<1024>);
-        if (in_f64) pdl(k_scatter<true, true, 1024>, grid, kPNT, sm, st, p, map, nmapped);
-        else pdl(k_scatter<false, true, 1024>, grid, kPNT, sm, st, p, map, nmapped);
-    } else {  // bucket-major distributed partition of a 2048-bucket global model
-        constexpr size_t sm = sizeof(ScatterSmem<kMaxNB>);
-        if (in_f64) pdl(k_scatter<true, true, kMaxNB>, grid, kPNT, sm, st, p, map, nmapped);
-        else pdl(k_scatter<false, true, kMaxNB>, grid, kPNT, sm, st, p, map, nmapped);
+        if (in_f64) pdl(k_scatter<true, kMaxNB>, grid, kPNT, sm, st, p);
+        else pdl(k_scatter<false, kMaxNB>, grid, kPNT, sm, st, p);
     }
 }
 

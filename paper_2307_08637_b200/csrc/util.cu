@@ -82,30 +82,6 @@ __global__ void k_rank_le(const void* sorted, uint64_t n, const uint64_t* pivots
     ranks[i] = lo;
 }
 
-// out[i] = sum(in[0, i)) for i < n (one CTA; the partition cursors of a
-// bucket-major distributed partition, without a host round trip)
-__global__ void __launch_bounds__(1024) k_excl_scan_u64(const unsigned long long* in, unsigned long long* out,
-                                                        uint32_t n) {
-    griddep_wait();
-    __shared__ uint64_t a[kMaxNB];
-    __shared__ uint64_t wsum[1024 / 32 + 1];
-    for (uint32_t i = threadIdx.x; i < n; i += 1024) a[i] = in[i];
-    __syncthreads();
-    block_exclusive_scan_u64<1024>(a, n, wsum);
-    for (uint32_t i = threadIdx.x; i < n; i += 1024) out[i] = a[i];
-}
-
-// Run gather: run r copies len keys from src + src_off to dst + dst_off
-// (runs[3r..3r+2]); one CTA per run, grid-stride over the runs.
-__global__ void __launch_bounds__(256) k_copy_runs(const uint64_t* src, uint64_t* dst, const uint64_t* runs,
-                                                  uint64_t nruns) {
-    griddep_wait();
-    for (uint64_t r = blockIdx.x; r < nruns; r += gridDim.x) {
-        const uint64_t so = runs[3 * r], d0 = runs[3 * r + 1], len = runs[3 * r + 2];
-        for (uint64_t i = threadIdx.x; i < len; i += 256) dst[d0 + i] = __ldcs((const unsigned long long*)src + so + i);
-    }
-}
-
 // verify_sorted + multiset_hash (verify.hpp:17-29)
 template <bool F64>
 __global__ void __launch_bounds__(256) k_verify(const void* keys, uint64_t n, Ctrl* ctrl) {
@@ -187,15 +163,6 @@ void launch_learned_pivots(const uint8_t* model, const void* keys, uint64_t n, i
     const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms() * 4);
     if (in_f64) pdl(k_learned_pivots<true>, grid, 256, sm, st, model, keys, n, gmax, ghit);
     else pdl(k_learned_pivots<false>, grid, 256, sm, st, model, keys, n, gmax, ghit);
-}
-
-void launch_excl_scan_u64(const unsigned long long* in, unsigned long long* out, uint32_t n, cudaStream_t st) {
-    pdl(k_excl_scan_u64, 1, 1024, 0, st, in, out, n);
-}
-
-void launch_copy_runs(const uint64_t* src, uint64_t* dst, const uint64_t* runs, uint64_t nruns, cudaStream_t st) {
-    const int grid = (int)std::min<uint64_t>(nruns, (uint64_t)num_sms() * 8);
-    pdl(k_copy_runs, grid, 256, 0, st, src, dst, runs, nruns);
 }
 
 void launch_rank_le(const void* sorted, uint64_t n, int f64, const uint64_t* pivots, uint32_t np, uint64_t* ranks,

@@ -1,8 +1,10 @@
-"""Multi-rank host logic of the distributed sort (paper_2307_08637_b200/dist.py)
-on CPU with gloo, world sizes 2 and 3: the concatenation of the per-rank
-outputs in rank order must equal the sorted input (bit-exact), every rank's
-range must be ordered w.r.t. its neighbours, and the split arithmetic must
-be consistent."""
+"""Multi-rank host logic of the multi-GPU driver on CPU with gloo:
+paper_2307_08637_b200.dist's mirror of dist.cu's steps (shard sizes, sample
+shares, global model policy, the C++ rank plan lsort_dist_plan, the
+fused-scatter placement, equality fills) around CPU stand-ins of the device
+work. The concatenation of the per-rank outputs in rank order must equal the
+sorted input bit for bit, and rank loads must balance (max <= 1.10 x mean)
+where the data allows it."""
 import os
 import socket
 
@@ -12,7 +14,9 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2307_08637_b200.dist import rank_bounds, sample_shares, splitmix64
+from paper_2307_08637_b200.dist import dist_plan, sample_shares, splitmix64
+
+SEEDS = {"normal": 7, "lognormal2": 19, "uniform": 42, "zipf": 3, "mixgauss": 11, "rootdups": 3}
 
 
 def _free_port():
@@ -23,39 +27,59 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, dist_name, n_per, out_dir, bucket_major=True):
+def _make_input(dist_name, total, world):
+    from oracle import oracle as O
+    if dist_name == "heavy":  # 40% one value: an equality bucket split across ranks
+        rng = np.random.default_rng(5)
+        full = rng.integers(0, 1 << 40, total, dtype=np.uint64)
+        full[rng.random(total) < 0.4] = 123456789
+    else:
+        full = O.generate(dist_name, total, SEEDS[dist_name])
+    n_per = total // world
+    parts = [full[r * n_per:(r + 1) * n_per].copy() for r in range(world)]
+    return full, parts
+
+
+def _worker(rank, world, port, dist_name, total, out_dir, ragged, nan_rank):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from oracle import oracle as O
-    from dist_cpu_ops import CpuOps, CpuOpsRankMajor
-    from paper_2307_08637_b200 import SortConfig
+    from dist_cpu_ops import CpuOps
+    from paper_2307_08637_b200 import NanError, SortConfig
     from paper_2307_08637_b200.dist import DistSorter
-    total = n_per * world
-    full = O.generate(dist_name, total, {"normal": 7, "lognormal2": 19, "uniform": 42, "zipf": 3}[dist_name])
-    shard = full[rank * n_per:(rank + 1) * n_per].copy()
-    if rank == world - 1:  # ragged shards
-        shard = shard[: n_per // 2]
+    _, parts = _make_input(dist_name, total, world)
+    shard = parts[rank]
+    if ragged and rank == world - 1:
+        shard = shard[: shard.size // 2]
+    if ragged and world > 2 and rank == 1:
+        shard = shard[:0]  # an empty shard
+    if nan_rank == rank:
+        shard = shard.copy()
+        shard[17] = np.nan
     t = torch.from_numpy(shard if shard.dtype == np.float64 else shard.view(np.int64))
-    sorter = DistSorter(cfg=SortConfig(sample_fraction=0.05), ops=CpuOps() if bucket_major else CpuOpsRankMajor(),
-                        buckets=256)
-    out, st = sorter.sort(t)
-    np.save(os.path.join(out_dir, f"out{rank}.npy"), out.numpy())
+    sorter = DistSorter(cfg=SortConfig(), ops=CpuOps())
+    try:
+        out, st = sorter.sort(t)
+        np.save(os.path.join(out_dir, f"out{rank}.npy"), out.numpy())
+    except NanError as e:
+        np.save(os.path.join(out_dir, f"nan{rank}.npy"), np.array([e.index]))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("bucket_major", [True, False], ids=["bucket_major", "rank_major"])
-@pytest.mark.parametrize("world,dist_name", [(2, "normal"), (3, "lognormal2"), (2, "zipf")])
-def test_distributed_sort_gloo(tmp_path, world, dist_name, bucket_major):
-    n_per = 6000
+def _run(tmp_path, world, dist_name, total, ragged=False, nan_rank=-1):
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, dist_name, n_per, str(tmp_path), bucket_major), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, dist_name, total, str(tmp_path), ragged, nan_rank), nprocs=world,
+             join=True)
+    full, parts = _make_input(dist_name, total, world)
+    if ragged:
+        parts[-1] = parts[-1][: parts[-1].size // 2]
+        if world > 2:
+            parts[1] = parts[1][:0]
+    return np.concatenate(parts)
+
+
+def _check(tmp_path, world, data):
     from oracle import oracle as O
-    seed = {"normal": 7, "lognormal2": 19, "uniform": 42, "zipf": 3}[dist_name]
-    full = O.generate(dist_name, n_per * world, seed)
-    parts = [full[r * n_per:(r + 1) * n_per] for r in range(world)]
-    parts[-1] = parts[-1][: n_per // 2]
-    data = np.concatenate(parts)
     outs = [np.load(tmp_path / f"out{r}.npy") for r in range(world)]
     got = np.concatenate(outs)
     if data.dtype == np.float64:
@@ -63,43 +87,97 @@ def test_distributed_sort_gloo(tmp_path, world, dist_name, bucket_major):
         assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
     else:
         assert np.array_equal(got.view(np.uint64), np.sort(data))
-    assert sum(o.size for o in outs) == data.size
+    return [o.size for o in outs]
 
 
-def test_rank_bounds_and_shares():
-    h = np.array([5, 0, 10, 3, 2, 0, 0, 30, 1, 1])
-    for world in (1, 2, 3, 4, 8):
-        b = rank_bounds(h, world)
-        assert b[0] == 0 and b[-1] == h.size and np.all(np.diff(b.astype(np.int64)) >= 0)
-        assert b.size == world + 1
-    b = rank_bounds(np.ones(1024, np.int64), 4)
-    assert list(b) == [0, 256, 512, 768, 1024]
+@pytest.mark.parametrize("world,dist_name,ragged", [(2, "normal", True), (3, "lognormal2", True),
+                                                    (2, "zipf", False), (4, "uniform", True)])
+def test_distributed_sort_gloo(tmp_path, world, dist_name, ragged):
+    data = _run(tmp_path, world, dist_name, 24_000, ragged)
+    _check(tmp_path, world, data)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_mixgauss_balance(tmp_path, world):
+    """C3's mixture of Gaussians: the reference RMI puts ~71% of the keys into
+    one bucket (models.hpp:56-58, models.cpp:110-113); the global model falls
+    back to a splitter tree and the cuts balance the ranks."""
+    total = 2_000_000
+    data = _run(tmp_path, world, "mixgauss", total)
+    loads = _check(tmp_path, world, data)
+    assert max(loads) <= 1.10 * total / world, loads
+
+
+def test_equality_bucket_split(tmp_path):
+    """40% of the keys share one value: its equality bucket is split across
+    ranks (every rank fills its part), loads stay balanced."""
+    world, total = 4, 400_000
+    data = _run(tmp_path, world, "heavy", total)
+    loads = _check(tmp_path, world, data)
+    assert max(loads) <= 1.10 * total / world, loads
+
+
+def test_nan_on_one_rank_fails_every_rank(tmp_path):
+    world = 3
+    _run(tmp_path, world, "normal", 30_000, nan_rank=1)
+    idx = [int(np.load(tmp_path / f"nan{r}.npy")[0]) for r in range(world)]
+    assert idx == [-1, 17, -1]
+
+
+def test_dist_plan():
+    """lsort_dist_plan (dist.cu): cuts on the nearer bucket boundary, inside
+    equality buckets, empty ranks; every key position of every rank written
+    exactly once, buckets in order, sources in rank order inside a bucket."""
+    p = dist_plan(np.array([[20, 5, 75, 0]]), None, 0)
+    assert list(p["cuts"]) == [0, 100] and list(p["recv"]) == [100]
+    H = np.array([[10, 3, 40, 0], [10, 2, 35, 0]])  # global [20, 5, 75, 0]
+    p0 = dist_plan(H, None, 0)
+    assert list(p0["cuts"]) == [0, 25, 100]  # T = 50: boundary 25 is nearer than 100
+    p0 = dist_plan(H, np.array([0, 0, 1, 0]), 0)
+    assert list(p0["cuts"]) == [0, 50, 100]  # bucket 2 is an equality bucket: split at 50
+    rng = np.random.default_rng(2)
+    for world in (1, 2, 3, 5, 8):
+        for trial in range(3):
+            nb = 64
+            H = rng.integers(0, 9, (world, nb))
+            H[:, 7] = 0
+            eq = (rng.random(nb) < 0.1).astype(np.uint8)
+            if trial == 2:
+                H[:, 11] = 500  # a giant non-equality bucket: some ranks get nothing
+            plans = [dist_plan(H, eq, r) for r in range(world)]
+            cuts = plans[0]["cuts"]
+            assert all(np.array_equal(q["cuts"], cuts) for q in plans)
+            G = H.sum(axis=0)
+            Pfx = np.concatenate([[0], np.cumsum(G)])
+            assert cuts[0] == 0 and cuts[-1] == G.sum() and np.all(np.diff(cuts) >= 0)
+            for c in cuts:  # a cut inside a bucket only if it is an equality bucket
+                b = np.searchsorted(Pfx, c, side="right") - 1
+                assert c == Pfx[min(b, nb)] or eq[b]
+            # simulate the fused scatter: source s writes its keys of bucket b at dest_off[b]...
+            bufs = [np.full(int(plans[0]["recv"][r]), -1, np.int64) for r in range(world)]
+            for s in range(world):
+                q = plans[s]
+                for b in range(nb):
+                    if H[s, b] == 0 or eq[b]:
+                        continue
+                    d, o = int(q["dest"][b]), int(q["dest_off"][b])
+                    seg = bufs[d][o:o + H[s, b]]
+                    assert np.all(seg == -1), "position written twice"
+                    seg[:] = b * 100 + s
+            for r in range(world):  # ...and the receiver's pieces cover its range exactly
+                for b, at, cnt in plans[r]["pieces"]:
+                    if eq[b]:
+                        assert np.all(bufs[r][at:at + cnt] == -1)
+                        bufs[r][at:at + cnt] = b * 100 + 99
+                    else:
+                        assert cnt == G[b]
+                        assert np.all(bufs[r][at:at + cnt] // 100 == b)
+                assert np.all(bufs[r] >= 0), "position never written"
+                assert np.all(np.diff(bufs[r]) >= 0), "buckets / sources out of order"
+
+
+def test_sample_shares_and_seed():
     assert sum(sample_shares([100, 50, 0, 25], 70)) == 70
     assert sample_shares([100, 50, 0, 25], 70)[2] == 0
+    assert sample_shares([0, 0], 10) == [0, 0]
     assert splitmix64(0) == 0xE220A8397B1DCDAF
-
-
-def test_bucket_exchange_plan():
-    """Runs regroup the source-major receive buffer by bucket; sizes and counts add up."""
-    from paper_2307_08637_b200.dist import bucket_exchange_plan
-    rng = np.random.default_rng(3)
-    for world in (1, 2, 3, 5):
-        B = 64
-        H = rng.integers(0, 7, (world, B))
-        H[:, 5] = 0  # an empty bucket
-        bounds = rank_bounds(H.sum(axis=0), world)
-        sends = [bucket_exchange_plan(H, bounds, r)[0] for r in range(world)]
-        for r in range(world):
-            send, recv, runs, sizes = bucket_exchange_plan(H, bounds, r)
-            assert recv == [sends[s][r] for s in range(world)]
-            lo, hi = bounds[r], bounds[r + 1]
-            assert np.array_equal(sizes, H[:, lo:hi].sum(axis=0))
-            # simulate: source s sends its keys of my buckets bucket-major, tagged (bucket, s)
-            buf = []
-            for s_ in range(world):
-                for b in range(lo, hi):
-                    buf += [(b, s_)] * int(H[s_, b])
-            dst = [None] * len(buf)
-            for so, do, ln in runs.astype(np.int64):
-                dst[do:do + ln] = buf[so:so + ln]
-            assert dst == sorted(buf)  # bucket-major, sources in rank order inside a bucket
