@@ -657,7 +657,7 @@ struct Engine {
             const uint32_t nmid = (uint32_t)mids.size();
             if (nsmall + nmid) up(C->idx.p, hi, (nsmall + nmid) * 4, true);
             if (nbuckets) CU(cudaMemsetAsync(C->buckets.p, 0, nbuckets * 8, st));
-            CU(cudaMemsetAsync(&dctrl->n_rec, 0, offsetof(Ctrl, keys_fill) - offsetof(Ctrl, n_rec), st));
+            CU(cudaMemsetAsync(&dctrl->n_rec, 0, offsetof(Ctrl, verify_first) - offsetof(Ctrl, n_rec), st));  // per-level lists and key counters
 
             LevelParams p{};
             p.segs = C->segs.as<SegDesc>();
