@@ -171,6 +171,23 @@ inline void sort(device_span<double> a, const SortConfig& cfg = {}) {
     detail::run(a.data, a.size, LSORT_KEY_F64, LSORT_MEM_DEVICE, cfg);
 }
 
+// learned_sort_classic(a, cfg) -- SPEC.md:402-410 (the LearnedSort 2.0 path:
+// one RMI, two partition rounds with it, model-based counting sort + fix-up).
+template <class T>
+inline void learned_sort_classic(std::span<T> a, const SortConfig& cfg = {}) {
+    static_assert(std::is_same_v<T, Key> || std::is_same_v<T, double>, "uint64 or double keys");
+    lsort_ctx* h = detail::context().get(cfg.device);
+    lsort_cfg c = cfg.to_c();
+    std::uint64_t nan_index = ~0ull;
+    const int kind = std::is_same_v<T, double> ? LSORT_KEY_F64 : LSORT_KEY_U64;
+    int rc = lsort_cuda_sort_classic(h, a.data(), a.size(), kind, LSORT_MEM_HOST, &c, nullptr, &nan_index);
+    if (rc == LSORT_OK) return;
+    if (rc == LSORT_ENAN) throw nan_error(nan_index);
+    std::string msg = lsort_cuda_last_error(h);
+    if (rc == LSORT_EINVAL) throw std::invalid_argument("lsort::learned_sort_classic: " + msg);
+    throw cuda_error(rc, "lsort::learned_sort_classic: " + msg);
+}
+
 // ---- multi-GPU (lsort_cuda_sort_dist, one process per GPU) ----------------
 // The distributed sort(a, cfg): every rank of a `world`-rank group holds a
 // device shard; after sort() this rank holds the rank-th key range of the

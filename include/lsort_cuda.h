@@ -129,6 +129,7 @@ typedef struct lsort_stats {
     double ms_models, ms_classify, ms_scatter, ms_base, ms_fill;
     double ms_level0_classify, ms_level0_scatter;
     uint64_t level0_keys;
+    uint64_t round2_buckets;        /* lsort_cuda_sort_classic: non-empty sub-buckets after round two */
 } lsort_stats;
 
 #define LSORT_FLAG_PHASE_TIMING 1u
@@ -252,6 +253,27 @@ int lsort_read_keys(const char* path, uint64_t* keys, uint64_t capacity, uint64_
                     size_t errlen);
 /* write_keys: inverse of read_keys (n == 0 writes the 8-byte zero count). */
 int lsort_write_keys(const char* path, const uint64_t* keys, uint64_t n, char* err, size_t errlen);
+
+/* LearnedSort 2.0 classic path (learned_sort_classic; PAPER.md
+ * §2.2, §3.3): one RMI (cfg->rmi_bucket_count submodels) trained once on a
+ * sample of min(sample_fraction n, rmi_sample_cap) keys drawn with
+ * Rng(cfg->seed); round 1 partitions into B buckets, round 2 every bucket of
+ * more than base_case_capacity keys into B sub-buckets with the SAME model
+ * restricted to the bucket's CDF range (no sampling, no training); every
+ * finished (sub-)bucket is placed by model-based counting sort and its
+ * collisions fixed (the reference's insertion-sort sweep). Sub-buckets still
+ * above the capacity (a poorly fitting model) continue with the AIPS2o
+ * recursion. Same in-place / NaN / host-memory contract as lsort_cuda_sort. */
+int lsort_cuda_sort_classic(lsort_ctx* ctx, void* keys, uint64_t n, int key_kind, int mem_kind,
+                            const lsort_cfg* cfg, lsort_stats* stats, uint64_t* nan_index_out);
+/* model_counting_sort of one device segment (n <= 8192):
+ * d_out[] = d_keys[] placed by predicted position floor(n F(x)) over the CDF
+ * range [cdf_lo, cdf_hi) (PartitionModel::bucket_index with n buckets,
+ * models.hpp:128-138,162-171), stable for equal positions; sorted iff the
+ * model is monotone and collision-free on the segment, else almost sorted. */
+int lsort_cuda_model_counting_sort(lsort_ctx* ctx, const lsort_rmi_header* h, const lsort_rmi_entry* entries,
+                                   double cdf_lo, double cdf_hi, const uint64_t* d_keys, uint64_t n,
+                                   uint64_t* d_out);
 
 /* Model forwarding (LearnedSort 2.0 classic path; Learned
  * cdf_lo / cdf_hi, models.hpp:128-138): sort device keys known to fall in

@@ -757,6 +757,86 @@ int lso_sort_doubles(double* a, uint64_t n, const lso_cfg* c, int64_t* nan_index
     return 0;
 }
 
+/* --------------------------------------- LearnedSort 2.0 classic path */
+/* model_counting_sort: predicted position of x in a segment
+ * of len keys = PartitionModel::bucket_index with bucket_count = len over the
+ * segment's CDF range [cdf_lo, cdf_hi) (models.hpp:128-138,162-171), i.e.
+ * floor(len * F(x)) within the range; stable counting placement (ties keep
+ * the input order). Sorted iff the model is monotone and collision-free. */
+void lso_model_counting_sort(const uint64_t* a, size_t n, const double* P, uint32_t B, double cdf_lo,
+                             double cdf_hi, uint64_t* out) {
+    if (n == 0) return;
+    uint32_t* pos = (uint32_t*)malloc(n * sizeof(uint32_t));
+    size_t* start = (size_t*)calloc(n + 1, sizeof(size_t));
+    for (size_t i = 0; i < n; ++i) {
+        pos[i] = lso_learned_bucket(P, B, (uint32_t)n, cdf_lo, cdf_hi, a[i]);
+        start[pos[i] + 1]++;
+    }
+    for (size_t p = 0; p < n; ++p) start[p + 1] += start[p];
+    for (size_t i = 0; i < n; ++i) out[start[pos[i]]++] = a[i];
+    free(pos);
+    free(start);
+}
+
+/* learned_sort_classic (§2.2, §3.3): one RMI on a
+ * 1% sample (Rng(seed).next_below, capped at rmi_sample_cap); round 1 into B
+ * buckets; round 2 of every bucket b into B sub-buckets with the SAME model
+ * restricted to the CDF range [b/B, (b+1)/B); model_counting_sort of every
+ * sub-bucket over its CDF range [b/B + j/B^2, b/B + (j+1)/B^2); one final
+ * insertion-sort sweep. stats (nullable): [0] non-empty sub-buckets after
+ * round two, [1] swaps made by the final insertion sort. */
+int lso_learned_sort_classic(uint64_t* a, uint64_t n, const lso_cfg* c, uint64_t* stats) {
+    if (stats) { stats[0] = 0; stats[1] = 0; }
+    if (n < 2) return 0;
+    const uint32_t B = c->rmi_bucket_count;
+    const uint64_t s = lso_rmi_sample_size(c, n);
+    uint64_t* smp = (uint64_t*)malloc(s * sizeof(uint64_t));
+    for (uint64_t j = 0; j < s; ++j) smp[j] = a[lso_rng_below(c->seed, j, n)];
+    lso_radix_base_case_sort(smp, s, 16);
+    double* P = (double*)malloc((4 + 4 * (size_t)B) * sizeof(double));
+    lso_rmi_train(smp, s, B, P);
+    free(smp);
+    const uint64_t BB = (uint64_t)B * B;
+    uint32_t* q = (uint32_t*)malloc(n * sizeof(uint32_t));  /* b * B + j */
+    uint64_t* cnt = (uint64_t*)calloc(BB + 1, sizeof(uint64_t));
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t b = lso_learned_bucket(P, B, B, 0.0, 1.0, a[i]);
+        const uint32_t j = lso_learned_bucket(P, B, B, (double)b / B, (double)(b + 1) / B, a[i]);
+        q[i] = b * B + j;
+        cnt[q[i] + 1]++;
+    }
+    for (uint64_t k = 0; k < BB; ++k) {
+        if (stats && cnt[k + 1]) stats[0]++;
+        cnt[k + 1] += cnt[k];
+    }
+    uint64_t* y = (uint64_t*)malloc(n * sizeof(uint64_t));
+    uint64_t* cur = (uint64_t*)malloc((BB + 1) * sizeof(uint64_t));
+    memcpy(cur, cnt, (BB + 1) * sizeof(uint64_t));
+    for (uint64_t i = 0; i < n; ++i) y[cur[q[i]]++] = a[i];
+    free(cur);
+    free(q);
+    for (uint64_t k = 0; k < BB; ++k) {
+        const uint64_t lo = cnt[k], len = cnt[k + 1] - lo;
+        if (len == 0) continue;
+        const uint32_t b = (uint32_t)(k / B), j = (uint32_t)(k % B);
+        const double c0 = (double)b / B + (double)j / (double)BB;
+        lso_model_counting_sort(y + lo, len, P, B, c0, c0 + 1.0 / (double)BB, a + lo);
+    }
+    free(cnt);
+    free(y);
+    free(P);
+    /* insertion-sort sweep (§2.2: corrects the RMI's mistakes) */
+    uint64_t swaps = 0;
+    for (uint64_t i = 1; i < n; ++i) {
+        const uint64_t x = a[i];
+        uint64_t u = i;
+        while (u > 0 && a[u - 1] > x) { a[u] = a[u - 1]; --u; ++swaps; }
+        a[u] = x;
+    }
+    if (stats) stats[1] = swaps;
+    return 0;
+}
+
 /* ------------------------------------------------ pivot analysis */
 /* PAPER.md:324-349 (Alg. 4) */
 size_t lso_learned_pivots(const uint64_t* a, size_t n, const double* P, uint32_t B, uint32_t b, uint64_t* out) {

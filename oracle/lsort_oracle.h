@@ -132,6 +132,10 @@ int lso_build_partition_model(const uint64_t* a, uint64_t n, uint64_t seg_begin,
 /* In-place sort of encoded keys (AIPS2o restatement; out-of-place scratch
  * internally). Returns 0. */
 int lso_sort_keys(uint64_t* a, uint64_t n, const lso_cfg* c);
+/* LearnedSort 2.0 classic path */
+void lso_model_counting_sort(const uint64_t* a, size_t n, const double* P, uint32_t B, double cdf_lo,
+                             double cdf_hi, uint64_t* out);
+int lso_learned_sort_classic(uint64_t* a, uint64_t n, const lso_cfg* c, uint64_t* stats);
 /* double entry: encode (NaN -> returns 2, *nan_index set, array untouched),
  * sort, decode. */
 int lso_sort_doubles(double* a, uint64_t n, const lso_cfg* c, int64_t* nan_index);

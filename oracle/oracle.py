@@ -117,6 +117,10 @@ def lib():
         L.lso_learned_bucket_many.argtypes = [vp, C.c_uint32, C.c_uint32, f64, f64, vp, sz, vp]
         L.lso_tree_classify_many.restype = None
         L.lso_tree_classify_many.argtypes = [C.POINTER(Tree), vp, sz, vp]
+        L.lso_model_counting_sort.restype = None
+        L.lso_model_counting_sort.argtypes = [vp, sz, vp, C.c_uint32, f64, f64, vp]
+        L.lso_learned_sort_classic.restype = C.c_int
+        L.lso_learned_sort_classic.argtypes = [vp, u64, C.POINTER(Cfg), vp]
         L.lso_std_sort_u64.restype = None; L.lso_std_sort_u64.argtypes = [vp, u64]
         L.lso_parallel_sort_u64.restype = None; L.lso_parallel_sort_u64.argtypes = [vp, u64, C.c_int]
         L.lso_max_threads.restype = C.c_int; L.lso_max_threads.argtypes = []
@@ -171,6 +175,23 @@ def decode(k) -> np.ndarray:
     out = np.empty(k.shape, np.float64)
     lib().lso_decode_doubles(_p(k), _p(out), k.size)
     return out
+
+
+def model_counting_sort(keys, P, B: int, cdf_lo: float = 0.0, cdf_hi: float = 1.0) -> np.ndarray:
+    """stable counting placement by predicted position."""
+    k = _u64(keys).reshape(-1)
+    out = np.empty_like(k)
+    lib().lso_model_counting_sort(_p(k), k.size, _p(np.ascontiguousarray(P, np.float64)), B, cdf_lo, cdf_hi,
+                                  _p(out))
+    return out
+
+
+def learned_sort_classic(keys, c: Cfg | None = None):
+    """SPEC.md:402-410 on a copy: (sorted keys, non-empty sub-buckets, insertion swaps)."""
+    a = _u64(keys).reshape(-1).copy()
+    st = np.zeros(2, np.uint64)
+    lib().lso_learned_sort_classic(_p(a), a.size, C.byref(c or cfg()), _p(st))
+    return a, int(st[0]), int(st[1])
 
 
 def std_sort(keys) -> np.ndarray:

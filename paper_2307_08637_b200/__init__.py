@@ -163,6 +163,43 @@ class Context:
         _check(self, rc)
         return stats.as_dict()
 
+    def sort_classic(self, keys, cfg: SortConfig | None = None) -> dict:
+        """learned_sort_classic: one RMI trained once, two
+        partition rounds with that model, model-based counting sort + fix-up
+        (lsort_cuda_sort_classic). Same arguments / errors as sort()."""
+        cfg_c = (cfg or SortConfig()).to_c()
+        stats = N.lsort_stats()
+        nan = C.c_uint64(0)
+        if isinstance(keys, np.ndarray):
+            if not keys.flags["C_CONTIGUOUS"]:
+                raise ValueError("host keys must be contiguous")
+            kind, mem, ptr, n = _key_kind_of(keys), N.MEM_HOST, keys.ctypes.data, keys.size
+            N.lib().lsort_cuda_set_stream(self._h, None)
+        else:
+            if not keys.is_cuda or not keys.is_contiguous():
+                raise ValueError("device keys must be a contiguous CUDA tensor")
+            self._sync_stream()
+            kind, mem, ptr, n = _key_kind_of(keys), N.MEM_DEVICE, keys.data_ptr(), keys.numel()
+        rc = N.lib().lsort_cuda_sort_classic(self._h, C.c_void_p(ptr), n, kind, mem, C.byref(cfg_c), C.byref(stats),
+                                             C.byref(nan))
+        if rc == N.LSORT_ENAN:
+            raise NanError(int(nan.value))
+        _check(self, rc)
+        return stats.as_dict()
+
+    def model_counting_sort(self, P: np.ndarray, submodels: int, d_keys, cdf_lo: float = 0.0, cdf_hi: float = 1.0):
+        """model_counting_sort of one device segment (<= 8192
+        uint64 keys): returns a new tensor placed by predicted position, stable."""
+        torch = _torch()
+        self._sync_stream()
+        h, e = unpack_rmi(P, submodels)
+        out = torch.empty_like(d_keys)
+        rc = N.lib().lsort_cuda_model_counting_sort(self._h, C.byref(h), e.ctypes.data_as(C.c_void_p), cdf_lo, cdf_hi,
+                                                    C.c_void_p(d_keys.data_ptr()), d_keys.numel(),
+                                                    C.c_void_p(out.data_ptr()))
+        _check(self, rc)
+        return out
+
     def sort_batch(self, arrays, cfg: SortConfig | None = None) -> dict:
         """Sort several arrays (one key kind) in one call. Host (numpy) arrays:
         copies in / out pipelined against the sorts (lsort_cuda_sort_batch);

@@ -62,7 +62,7 @@ class lsort_stats(C.Structure):
                 ("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("ms_models", C.c_double), ("ms_classify", C.c_double), ("ms_scatter", C.c_double),
                 ("ms_base", C.c_double), ("ms_fill", C.c_double), ("ms_level0_classify", C.c_double),
-                ("ms_level0_scatter", C.c_double), ("level0_keys", C.c_uint64)]
+                ("ms_level0_scatter", C.c_double), ("level0_keys", C.c_uint64), ("round2_buckets", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -76,7 +76,7 @@ EXPORTS = [
     "lsort_cuda_sort_buckets", "lsort_nccl_available", "lsort_nccl_unique_id",
     "lsort_cuda_dist_create", "lsort_cuda_dist_destroy", "lsort_cuda_dist_last_error", "lsort_cuda_dist_set_stream",
     "lsort_cuda_sort_dist", "lsort_cuda_dist_result", "lsort_cuda_sort_multi", "lsort_cuda_dist_emulate",
-    "lsort_dist_plan",
+    "lsort_dist_plan", "lsort_cuda_sort_classic", "lsort_cuda_model_counting_sort",
 ]
 
 _lib = None
@@ -105,6 +105,10 @@ def lib():
     L.lsort_cuda_set_stream.argtypes = [vp, vp]
     L.lsort_cuda_sort.restype = i32
     L.lsort_cuda_sort.argtypes = [vp, vp, u64, i32, i32, P(lsort_cfg), P(lsort_stats), P(u64)]
+    L.lsort_cuda_sort_classic.restype = i32
+    L.lsort_cuda_sort_classic.argtypes = [vp, vp, u64, i32, i32, P(lsort_cfg), P(lsort_stats), P(u64)]
+    L.lsort_cuda_model_counting_sort.restype = i32
+    L.lsort_cuda_model_counting_sort.argtypes = [vp, P(lsort_rmi_header), vp, f64, f64, vp, u64, vp]
     L.lsort_cuda_sort_forward.restype = i32
     L.lsort_cuda_sort_forward.argtypes = [vp, vp, u64, i32, P(lsort_cfg), P(lsort_rmi_header), vp, C.c_uint32,
                                           C.c_uint32, vp, u64, P(lsort_stats), P(u64)]

@@ -709,6 +709,97 @@ int lsort_cuda_decode_inplace(lsort_ctx* C, uint64_t* d_keys, uint64_t n) {
 
 extern "C" {
 
+int lsort_cuda_sort_classic(lsort_ctx* C, void* keys, uint64_t n, int key_kind, int mem_kind, const lsort_cfg* cfgp,
+                            lsort_stats* stats, uint64_t* nan_index_out) {
+    if (!C) return LSORT_EINVAL;
+    C->err.clear();
+    if (nan_index_out) *nan_index_out = ~0ull;
+    if (key_kind != LSORT_KEY_U64 && key_kind != LSORT_KEY_F64) return fail(C, {LSORT_EINVAL, "key_kind"});
+    if (mem_kind != LSORT_MEM_DEVICE && mem_kind != LSORT_MEM_HOST) return fail(C, {LSORT_EINVAL, "mem_kind"});
+    if (n > 0 && !keys) return fail(C, {LSORT_EINVAL, "null keys"});
+    lsort_cfg cfg = cfg_or_default(cfgp);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    try {
+        validate_cfg(cfg);
+        CU(cudaSetDevice(C->device));
+        const bool f64 = key_kind == LSORT_KEY_F64;
+        C->launches = 0;
+        const cudaStream_t st = C->stream;
+        void* dkeys = keys;
+        if (mem_kind == LSORT_MEM_HOST) {
+            if (!C->data.ensure(std::max<uint64_t>(n, 1) * 8)) throw LsortError{LSORT_ENOMEM, "device keys"};
+            dkeys = C->data.p;
+            CU(cudaMemcpyAsync(dkeys, keys, n * 8, cudaMemcpyHostToDevice, st));
+        }
+        CU(cudaEventRecord(C->ev[0], st));
+        Engine E(C, cfg);
+        if (n <= cfg.base_case_capacity) {
+            E.sort(dkeys, n, f64, stats);  // one shared-memory sort: no model to train
+        } else {
+            // train the RMI once (§3.3: LearnedSort samples the data only once)
+            const uint32_t B = cfg.rmi_bucket_count;
+            const uint64_t s = sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
+            const size_t mb = sizeof(ModelHdr) + kLearnedEntryBytes * (size_t)B;
+            if (!C->sample.ensure(8 * s) || !C->segs.ensure(sizeof(SegDesc)) || !C->fwd_model.ensure(mb) ||
+                !C->train_ws.ensure(train_workspace_bytes(s, B)))
+                throw LsortError{LSORT_ENOMEM, "classic model"};
+            SegDesc d{};
+            d.begin = 0;
+            d.n = n;
+            CU(cudaMemcpyAsync(C->segs.p, &d, sizeof(d), cudaMemcpyHostToDevice, st));
+            launch_gather(C->segs.as<SegDesc>(), dkeys, f64, cfg.seed, 0, s, C->sample.as<uint64_t>(), nullptr, st);
+            E.nested_sort(C->sample.as<uint64_t>(), s);
+            CU(cudaMemsetAsync(C->fwd_model.p, 0, sizeof(ModelHdr), st));
+            launch_train_rmi(C->sample.as<uint64_t>(), s, B, C->fwd_model.as<uint8_t>(), B, C->train_ws.p, nullptr, st);
+            C->launches += 10;
+            Forward fw;
+            fw.model = C->fwd_model.as<uint8_t>();
+            fw.model_bytes = mb;
+            fw.nb = B;
+            fw.B = B;
+            E.classic = C->fwd_model.as<uint8_t>();
+            E.classic_B = B;
+            E.sort(dkeys, n, f64, stats, false, &fw);
+        }
+        CU(cudaEventRecord(C->ev[1], st));
+        if (mem_kind == LSORT_MEM_HOST) CU(cudaMemcpyAsync(keys, dkeys, n * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (stats) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, C->ev[0], C->ev[1]);
+            stats->ms_total = ms;
+            stats->kernel_launches = C->launches;
+        }
+    } catch (const LsortError& e) {
+        cudaStreamSynchronize(C->stream);
+        cudaGetLastError();
+        if (e.code == LSORT_ENAN) {
+            if (nan_index_out) *nan_index_out = std::stoull(e.msg);
+            C->err = "NaN at index " + e.msg;
+            return LSORT_ENAN;
+        }
+        return fail(C, e);
+    }
+    return LSORT_OK;
+}
+
+int lsort_cuda_model_counting_sort(lsort_ctx* C, const lsort_rmi_header* h, const lsort_rmi_entry* e, double cdf_lo,
+                                   double cdf_hi, const uint64_t* d_keys, uint64_t n, uint64_t* d_out) {
+    if (!C || !h || !e || h->submodels == 0 || h->submodels > LSORT_MAX_RMI || (n && (!d_keys || !d_out)))
+        return fail(C, {LSORT_EINVAL, "model_counting_sort: bad arguments"});
+    if (n > kSmallSampleCap) return fail(C, {LSORT_EINVAL, "model_counting_sort: at most 8192 keys per segment"});
+    try {
+        CU(cudaSetDevice(C->device));
+        upload_learned(C, h, e, h->submodels, cdf_lo, cdf_hi);
+        if (n) launch_model_counting_sort(C->models.as<uint8_t>(), d_keys, n, d_out, C->stream);
+        CU(cudaStreamSynchronize(C->stream));
+        CU(cudaGetLastError());
+    } catch (const LsortError& er) {
+        return fail(C, er);
+    }
+    return LSORT_OK;
+}
+
 int lsort_cuda_sort_forward(lsort_ctx* C, void* d_keys, uint64_t n, int key_kind, const lsort_cfg* cfgp,
                             const lsort_rmi_header* h, const lsort_rmi_entry* e, uint32_t b_lo, uint32_t b_hi,
                             const uint64_t* d_sorted_sample, uint64_t sample_n, lsort_stats* stats,

@@ -121,7 +121,7 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws, ids, clus, bat[3], psample, slices, fwd_model, fwd_slices, piv, fsample;
+        kseg, ktp, kplan, qws, ids, clus, cidx, bat[3], psample, slices, fwd_model, fwd_slices, piv, fsample;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
@@ -226,6 +226,13 @@ struct Engine {
     const uint64_t* given_sample = nullptr;
     uint64_t given_n = 0;
     uint32_t share_den = 0;
+    // LearnedSort 2.0 classic path (classic.cu): the root RMI (device model
+    // record, CDF [0,1), classic_B buckets) is forwarded to level 0 (Forward)
+    // and, restricted to each round-1 bucket's CDF range, to level 1; the
+    // buckets finished at levels 0 and 1 are sorted by model-based counting
+    // sort + fix-up instead of the radix base case.
+    const uint8_t* classic = nullptr;
+    uint32_t classic_B = 0;
 
     uint32_t rmi_b(uint64_t n) const { return fanout(n, cfg.rmi_bucket_count, cfg.bucket_target); }
     uint32_t tree_k(uint64_t n) const { return fanout(n, cfg.tree_bucket_count, cfg.bucket_target); }
@@ -583,7 +590,9 @@ struct Engine {
             const bool auto_cluster = !no_auto_cluster && !(cfg.flags & LSORT_FLAG_STRICT_POLICY) &&
                                       elig_keys > 0 && elig_keys <= kAutoClusterKeys;
             const bool use_cluster = level >= 1 && !src_f64 && cluster_available() &&
-                                     ((cfg.flags & LSORT_FLAG_CLUSTER) || auto_cluster) && cap >= 16384;
+                                     ((cfg.flags & LSORT_FLAG_CLUSTER) || auto_cluster) && cap >= 16384 &&
+                                     !(classic && level <= 1);
+            std::vector<uint32_t> fwd1;  // classic: level-1 segments with a forwarded model
             std::vector<BaseItem> clus;
             std::vector<SegPlan> psegs;
             psegs.reserve(ns);
@@ -601,7 +610,8 @@ struct Engine {
                 d.depth = s.depth;
                 d.flags = s.flags;
                 d.pslice = s.pslice;
-                d.rmi_b = (fw && level == 0) ? fw->nb : rmi_b(s.n);
+                const bool classic1 = classic && level == 1 && !(s.flags & kSegForceRadix);
+                d.rmi_b = (fw && level == 0) ? fw->nb : (classic1 ? classic_B : rmi_b(s.n));
                 max_rmi_b = std::max(max_rmi_b, d.rmi_b);
                 d.tree_k = tree_k(s.n);
                 uint32_t payload, nb;
@@ -627,6 +637,11 @@ struct Engine {
                     kinds |= 1u;
                     max_rmi_b = std::max(max_rmi_b, fw->B);
                     model_bytes = d.model_off + sizeof(ModelHdr) + payload;
+                    continue;
+                }
+                if (classic1) {  // the root restricted to this round-1 bucket (k_forward_models)
+                    fwd1.push_back(j);
+                    kinds |= 1u;
                     continue;
                 }
                 const int mc = model_class(s);
@@ -708,6 +723,13 @@ struct Engine {
                 const auto th0 = std::chrono::steady_clock::now();
                 level_models(bigs, p.segs, psegs, hs, src, src_f64, C->idx.as<uint32_t>(), nsmall, nmid, dc,
                              root_slices);
+                if (!fwd1.empty()) {
+                    if (!C->cidx.ensure(4 * fwd1.size())) throw LsortError{LSORT_ENOMEM, "classic models"};
+                    up(C->cidx.p, fwd1.data(), 4 * fwd1.size());
+                    launch_forward_models(p.segs, C->cidx.as<uint32_t>(), (uint32_t)fwd1.size(), (const uint64_t*)src,
+                                          classic, C->models.as<uint8_t>(), st);
+                    launched();
+                }
                 if (trace_enabled())
                     fprintf(stderr, "    level_models host %.3f ms\n",
                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
@@ -750,7 +772,12 @@ struct Engine {
                                     st);
                 launched();
             }
-            base_cases(p, dst, out, f64);
+            if (classic && level <= 1) {  // model-based counting sort of the finished buckets
+                launch_classic_base(p, dst, out, f64, classic, (int)level + 1, st);
+                launched(3);
+            } else {
+                base_cases(p, dst, out, f64);
+            }
             mark(4);
             launch_fill(p, out, f64, nsm * 4, st);
             mark(5);
@@ -836,6 +863,9 @@ struct Engine {
                 stats->base_case_keys += hc->keys_base;
                 stats->fill_keys += hc->keys_fill;
                 stats->base_segments += (uint64_t)hc->n_base[0] + hc->n_base[1] + hc->n_base[2];
+                if (classic && level == 1)  // non-empty sub-buckets after round two
+                    stats->round2_buckets =
+                        (uint64_t)hc->n_base[0] + hc->n_base[1] + hc->n_base[2] + hc->n_fill + hc->n_rec;
             }
             // ---- next level
             uint32_t nrec = hc->n_rec;

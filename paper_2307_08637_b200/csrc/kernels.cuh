@@ -160,6 +160,13 @@ void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int
 void launch_base_class(const LevelParams& p, int cls, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
 void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st);
 void launch_small_sort(void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st);
+// classic.cu (LearnedSort 2.0 classic path)
+void launch_forward_models(const SegDesc* segs, const uint32_t* idx, uint32_t count, const uint64_t* src,
+                           const uint8_t* root, uint8_t* models, cudaStream_t st);
+void launch_classic_base(const LevelParams& p, const uint64_t* src, void* out, int out_f64, const uint8_t* model,
+                         int round, cudaStream_t st);
+void launch_model_counting_sort(const uint8_t* model, const uint64_t* keys, uint64_t n, uint64_t* out,
+                                cudaStream_t st);
 // cluster.cu
 bool cluster_available();
 void launch_cluster_sort(const BaseItem* segs, uint32_t nsegs, const uint64_t* src, uint64_t* dst, void* out,

@@ -220,6 +220,7 @@ struct SmemSort {
     // (a may alias S.A: it is not read after the first pass.)
     static constexpr int ITEMS = CAP / NT;
     static constexpr int kThreads = NT;
+    static constexpr uint32_t kNbMax = CAP < NBMAX ? CAP : NBMAX;  // digits of one counting pass
     __device__ static void sort_fast(const uint64_t* a, uint32_t n, Smem& S, bool eq = false) {
         static_assert(ITEMS * NT == CAP, "CAP must be a multiple of NT");
         uint64_t k[ITEMS];

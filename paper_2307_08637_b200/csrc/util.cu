@@ -137,6 +137,7 @@ void partition_init(int optin);
 void models_init(int optin);
 void basecase_init(int optin);
 void cluster_init(int optin);
+void classic_init(int optin);
 
 void kernels_init() {
     static bool done = false;
@@ -151,6 +152,7 @@ void kernels_init() {
     models_init(optin);
     basecase_init(optin);
     cluster_init(optin);
+    classic_init(optin);
     allow_smem(k_classify_ids<true>, optin);
     allow_smem(k_classify_ids<false>, optin);
     allow_smem(k_learned_pivots<true>, optin);

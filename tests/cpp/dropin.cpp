@@ -48,6 +48,14 @@ int main() {
     lsort::sort_batch(std::span<std::span<double>>(spans));
     if (arrs != aref) { std::puts("batch mismatch"); return 1; }
 
+    // LearnedSort 2.0 classic path
+    std::vector<double> cd(1'200'000);
+    for (auto& v : cd) v = nd(g);
+    std::vector<double> cref = cd;
+    std::sort(cref.begin(), cref.end());
+    lsort::learned_sort_classic(std::span<double>(cd));
+    if (cd != cref) { std::puts("classic mismatch"); return 1; }
+
     lsort::SortConfig bad;
     bad.rmi_bucket_count = 1000;  // not a power of two
     try {
