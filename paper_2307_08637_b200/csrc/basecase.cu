@@ -89,9 +89,12 @@ __device__ __forceinline__ void base_reg_one(uint64_t* g, uint32_t n, typename S
 // own input range doubles as scratch for the rare large-digit passes.
 // Segments of at most CAP / 2 keys take a half-width register array so no
 // thread issues work for slots past n.
+// nmin < n <= nmax: the items of the list this kernel takes (one list may be
+// shared by two kernels of different CTA shapes, split by segment size).
 template <int NT, int CAP, int NBMAX, int MINB, bool OUT_F64>
 __global__ void __launch_bounds__(NT, MINB) k_base_reg(const BaseItem* items, const unsigned int* count, uint64_t* src,
-                                                   void* out, Ctrl* ctrl, uint32_t list_cap) {
+                                                   void* out, Ctrl* ctrl, uint32_t list_cap, uint32_t nmin,
+                                                   uint32_t nmax) {
     griddep_wait();
     using SS = SmemSort<NT, CAP, NBMAX>;
     extern __shared__ uint4 smem_u4[];
@@ -104,10 +107,11 @@ __global__ void __launch_bounds__(NT, MINB) k_base_reg(const BaseItem* items, co
     for (uint32_t e = blockIdx.x; e < ni; e += gridDim.x) {
         const BaseItem it = items[e];
         const uint32_t n = (uint32_t)it.n;
+        if (n <= nmin || n > nmax) continue;
         uint64_t* g = src + it.begin;
         if (threadIdx.x == 0 && e + gridDim.x < ni) {
             const BaseItem nx = items[e + gridDim.x];
-            l2_prefetch(src + nx.begin, 8 * nx.n);
+            if (nx.n > nmin && nx.n <= nmax) l2_prefetch(src + nx.begin, 8 * nx.n);
         }
         if (n <= (uint32_t)CAP / 2) base_reg_one<SS::ITEMS / 2, SS, OUT_F64>(g, n, S, out, it.begin);
         else base_reg_one<SS::ITEMS, SS, OUT_F64>(g, n, S, out, it.begin);
@@ -187,58 +191,64 @@ __global__ void __launch_bounds__(256) k_fill(const FillItem* items, const unsig
 }
 
 // ------------------------------------------------------------- launchers
-// size classes: <= 1024 and <= 4096 keys in shared memory (TMA), <= 16384 in registers
+// size classes: <= 1024 keys in shared memory (TMA), <= 4096 and <= 16384 in registers
 using SmallSS = SmemSort<128, 1024, 1024>;
-using MidSS = SmemSort<256, 4096, 4096>;
 using BaseL = BaseCfg<1024, 16, 8192>;
 static_assert(1024 == kWarpBaseCap, "small base-case class");
+
+template <int NT, int CAP, int NBMAX, int MINB>
+static void reg_init(int optin) {
+    allow_smem(k_base_reg<NT, CAP, NBMAX, MINB, true>, optin);
+    allow_smem(k_base_reg<NT, CAP, NBMAX, MINB, false>, optin);
+}
 
 void basecase_init(int optin) {
     allow_smem(k_base_smem<128, 1024, 1024, true>, optin);
     allow_smem(k_base_smem<128, 1024, 1024, false>, optin);
-    allow_smem(k_base_reg<256, 4096, 4096, 3, true>, optin);
-    allow_smem(k_base_reg<256, 4096, 4096, 3, false>, optin);
-    allow_smem(k_base_reg<1024, 16384, 8192, 1, true>, optin);
-    allow_smem(k_base_reg<1024, 16384, 8192, 1, false>, optin);
+    reg_init<256, 4096, 4096, 3>(optin);
+    reg_init<512, 8192, 4096, 2>(optin);
+    reg_init<1024, 16384, 8192, 1>(optin);
     allow_smem(k_small_sort<true>, optin);
     allow_smem(k_small_sort<false>, optin);
 }
 
-void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st) {
-    const int nsm = num_sms();
-    const int g0 = nsm * 8, g1 = nsm * 3, gl = nsm;
-    const size_t s0 = sizeof(SmallSS::Smem), s1 = sizeof(MidSS::SmemR), s2 = sizeof(SmemSort<1024, 16384, 8192>::SmemR);
-    unsigned int* cnt = &p.ctrl->n_base[0];
-    if (out_f64) {
-        pdl(k_base_smem<128, 1024, 1024, true>, g0, 128, s0, st, p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
-        pdl(k_base_reg<256, 4096, 4096, 3, true>, g1, 256, s1, st, p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
-        pdl(k_base_reg<1024, 16384, 8192, 1, true>, gl, 1024, s2, st, p.base[2], cnt + 2, (uint64_t*)src, out, p.ctrl, p.list_cap);
-    } else {
-        pdl(k_base_smem<128, 1024, 1024, false>, g0, 128, s0, st, p.base[0], cnt + 0, src, out, p.ctrl, p.list_cap);
-        pdl(k_base_reg<256, 4096, 4096, 3, false>, g1, 256, s1, st, p.base[1], cnt + 1, (uint64_t*)src, out, p.ctrl, p.list_cap);
-        pdl(k_base_reg<1024, 16384, 8192, 1, false>, gl, 1024, s2, st, p.base[2], cnt + 2, (uint64_t*)src, out, p.ctrl, p.list_cap);
-    }
+template <int NT, int CAP, int NBMAX, int MINB>
+static void launch_reg(const LevelParams& p, int cls, const uint64_t* src, void* out, int out_f64, cudaStream_t st,
+                       uint32_t nmin, uint32_t nmax) {
+    const size_t sm = sizeof(typename SmemSort<NT, CAP, NBMAX>::SmemR);
+    const int grid = num_sms() * MINB;
+    unsigned int* cnt = &p.ctrl->n_base[cls];
+    if (out_f64)
+        pdl(k_base_reg<NT, CAP, NBMAX, MINB, true>, grid, NT, sm, st, p.base[cls], cnt, (uint64_t*)src, out, p.ctrl,
+            p.list_cap, nmin, nmax);
+    else
+        pdl(k_base_reg<NT, CAP, NBMAX, MINB, false>, grid, NT, sm, st, p.base[cls], cnt, (uint64_t*)src, out, p.ctrl,
+            p.list_cap, nmin, nmax);
 }
 
-// One size class (0: <= 1 Ki keys, 1: <= 4 Ki, 2: <= 16 Ki) on its own stream:
-// the classes are independent, so they run side by side instead of each
-// waiting for the previous class's tail.
+// One size class on its own stream: 0 (<= 1 Ki keys, shared memory), 1 (<= 4 Ki),
+// and the 16 Ki list split by size into 3 (<= 8 Ki keys: 512 threads, two
+// CTAs per SM) and 2 (> 8 Ki: 1024 threads, one CTA per SM) -- a single
+// 1024-thread class cost 1.5x the 4 Ki class per key (one segment per SM,
+// no overlap); the classes are independent, so they run side by side.
 void launch_base_class(const LevelParams& p, int cls, const uint64_t* src, void* out, int out_f64, cudaStream_t st) {
     const int nsm = num_sms();
-    unsigned int* cnt = &p.ctrl->n_base[cls];
     if (cls == 0) {
+        unsigned int* cnt = &p.ctrl->n_base[0];
         const size_t sm = sizeof(SmallSS::Smem);
         if (out_f64) pdl(k_base_smem<128, 1024, 1024, true>, nsm * 8, 128, sm, st, p.base[0], cnt, src, out, p.ctrl, p.list_cap);
         else pdl(k_base_smem<128, 1024, 1024, false>, nsm * 8, 128, sm, st, p.base[0], cnt, src, out, p.ctrl, p.list_cap);
     } else if (cls == 1) {
-        const size_t sm = sizeof(MidSS::SmemR);
-        if (out_f64) pdl(k_base_reg<256, 4096, 4096, 3, true>, nsm * 3, 256, sm, st, p.base[1], cnt, (uint64_t*)src, out, p.ctrl, p.list_cap);
-        else pdl(k_base_reg<256, 4096, 4096, 3, false>, nsm * 3, 256, sm, st, p.base[1], cnt, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        launch_reg<256, 4096, 4096, 3>(p, 1, src, out, out_f64, st, 0, 4096);
+    } else if (cls == 2) {
+        launch_reg<1024, 16384, 8192, 1>(p, 2, src, out, out_f64, st, 8192, 16384);
     } else {
-        const size_t sm = sizeof(SmemSort<1024, 16384, 8192>::SmemR);
-        if (out_f64) pdl(k_base_reg<1024, 16384, 8192, 1, true>, nsm, 1024, sm, st, p.base[2], cnt, (uint64_t*)src, out, p.ctrl, p.list_cap);
-        else pdl(k_base_reg<1024, 16384, 8192, 1, false>, nsm, 1024, sm, st, p.base[2], cnt, (uint64_t*)src, out, p.ctrl, p.list_cap);
+        launch_reg<512, 8192, 4096, 2>(p, 2, src, out, out_f64, st, 0, 8192);
     }
+}
+
+void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st) {
+    for (int c = 0; c < kBaseLaunches; ++c) launch_base_class(p, c, src, out, out_f64, st);
 }
 
 void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st) {

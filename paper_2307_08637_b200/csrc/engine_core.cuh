@@ -368,8 +368,8 @@ struct Engine {
         level_models(bigs, dsegs, segs, hs, src, f64, nullptr, 0, 0, dev_cfg(cfg));
     }
 
-    // Base cases of a level: the 16 Ki and 1 Ki classes on two lane streams
-    // (high priority: the long 1024-thread CTAs start first) beside the 4 Ki
+    // Base cases of a level: the > 8 Ki, <= 8 Ki and 1 Ki classes on three
+    // lane streams (high priority: the long CTAs start first) beside the 4 Ki
     // class on the context stream, joined back before the next level.
     void base_cases(const LevelParams& p, const uint64_t* src, void* out, bool f64) {
         static const bool serial = getenv("LSORT_BASE_SERIAL") != nullptr;
@@ -379,11 +379,12 @@ struct Engine {
         }
         if (!C->fork_ev) CU(cudaEventCreateWithFlags(&C->fork_ev, cudaEventDisableTiming));
         CU(cudaEventRecord(C->fork_ev, st));
-        for (uint32_t l = 0; l < 2; ++l) CU(cudaStreamWaitEvent(lane(l)->stream, C->fork_ev, 0));
+        for (uint32_t l = 0; l < 3; ++l) CU(cudaStreamWaitEvent(lane(l)->stream, C->fork_ev, 0));
         launch_base_class(p, 2, src, out, f64, lane(0)->stream);
+        launch_base_class(p, 3, src, out, f64, lane(2)->stream);
         launch_base_class(p, 0, src, out, f64, lane(1)->stream);
         launch_base_class(p, 1, src, out, f64, st);
-        for (uint32_t l = 0; l < 2; ++l) {
+        for (uint32_t l = 0; l < 3; ++l) {
             CU(cudaEventRecord(lane(l)->join_ev, lane(l)->stream));
             CU(cudaStreamWaitEvent(st, lane(l)->join_ev, 0));
         }
@@ -781,7 +782,7 @@ struct Engine {
             mark(4);
             launch_fill(p, out, f64, nsm * 4, st);
             mark(5);
-            launched(3 + 1);
+            launched(kBaseLaunches + 1);
             if (early) {
                 CU(cudaEventSynchronize(C->ev[5]));
             } else {

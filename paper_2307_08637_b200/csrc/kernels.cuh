@@ -157,7 +157,9 @@ void launch_scan_children(const LevelParams& p, uint32_t max_nb, cudaStream_t st
 void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid, cudaStream_t st);
 // basecase.cu
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
+// cls 0: <= 1 Ki keys, 1: <= 4 Ki, 2: list 2 items > 8 Ki, 3: list 2 items <= 8 Ki
 void launch_base_class(const LevelParams& p, int cls, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
+constexpr int kBaseLaunches = 4;
 void launch_fill(const LevelParams& p, void* out, int out_f64, int grid, cudaStream_t st);
 void launch_small_sort(void* keys, uint64_t n, int f64, Ctrl* ctrl, cudaStream_t st);
 // classic.cu (LearnedSort 2.0 classic path)
