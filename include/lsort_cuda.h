@@ -130,6 +130,7 @@ typedef struct lsort_stats {
     double ms_level0_classify, ms_level0_scatter;
     uint64_t level0_keys;
     uint64_t round2_buckets;        /* lsort_cuda_sort_classic: non-empty sub-buckets after round two */
+    uint64_t direct_keys;           /* keys partitioned by the padded one-pass level 0 (no classify pass) */
 } lsort_stats;
 
 #define LSORT_FLAG_PHASE_TIMING 1u
@@ -149,6 +150,10 @@ typedef struct lsort_stats {
  * leftovers: cheaper than a whole partition level); for a full level the
  * classify + scatter + base-case path is faster. */
 #define LSORT_FLAG_CLUSTER 4u
+/* cfg->flags, TEST ONLY: size the padded level-0 regions below their expected
+ * counts so they overflow and the exact two-pass level runs instead (checks
+ * the fallback of the one-pass level 0 that large learned roots take). */
+#define LSORT_FLAG_TEST_DIRECT_OVERFLOW 8u
 
 typedef struct lsort_ctx lsort_ctx;
 

@@ -20,6 +20,7 @@ MAX_RMI = 2048
 FLAG_PHASE_TIMING = 1
 FLAG_STRICT_POLICY = 2  # reference Alg. 5 models only (no GPU quality fallback)
 FLAG_CLUSTER = 4  # experimental fused cluster (DSMEM) last level
+FLAG_TEST_DIRECT_OVERFLOW = 8  # test only: force the padded level 0 to overflow
 
 
 class lsort_cfg(C.Structure):
@@ -62,7 +63,7 @@ class lsort_stats(C.Structure):
                 ("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("ms_models", C.c_double), ("ms_classify", C.c_double), ("ms_scatter", C.c_double),
                 ("ms_base", C.c_double), ("ms_fill", C.c_double), ("ms_level0_classify", C.c_double),
-                ("ms_level0_scatter", C.c_double), ("level0_keys", C.c_uint64), ("round2_buckets", C.c_uint64)]
+                ("ms_level0_scatter", C.c_double), ("level0_keys", C.c_uint64), ("round2_buckets", C.c_uint64), ("direct_keys", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

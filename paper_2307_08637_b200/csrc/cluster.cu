@@ -160,7 +160,7 @@ __global__ void __cluster_dims__(kClSize, 1, 1) __launch_bounds__(kClNT, 1)
                     atomicAdd(&p.ctrl->keys_base, (unsigned long long)len);
                 } else {
                     const unsigned e = atomicAdd(&p.ctrl->n_rec, 1u);
-                    if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, depth > p.depth_cap ? kSegForceRadix : 0u, 0};
+                    if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, depth > p.depth_cap ? kSegForceRadix : 0u, 0, begin};
                     else atomicOr(&p.ctrl->err, 4u);
                     atomicAdd(&p.ctrl->keys_rec, (unsigned long long)len);
                 }

@@ -121,7 +121,7 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws, ids, clus, cidx, bat[3], psample, slices, fwd_model, fwd_slices, piv, fsample;
+        kseg, ktp, kplan, qws, ids, clus, cidx, scratch2, dws, bat[3], psample, slices, fwd_model, fwd_slices, piv, fsample;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
@@ -158,7 +158,9 @@ namespace lsort_host {
 struct SegPlan {
     uint64_t begin, n;
     uint32_t depth, flags;
-    uint64_t pslice = 0;  // slice of the parent's sorted sample (SegDesc::pslice)
+    uint64_t pslice = 0;       // slice of the parent's sorted sample (SegDesc::pslice)
+    uint64_t in_begin = ~0ull;  // read position (SegDesc::in_begin); ~0 = begin
+    uint64_t rd() const { return in_begin == ~0ull ? begin : in_begin; }
 };
 
 inline void validate_cfg(const lsort_cfg& c) {
@@ -590,9 +592,11 @@ struct Engine {
             static const bool no_auto_cluster = getenv("LSORT_NO_AUTO_CLUSTER") != nullptr;
             const bool auto_cluster = !no_auto_cluster && !(cfg.flags & LSORT_FLAG_STRICT_POLICY) &&
                                       elig_keys > 0 && elig_keys <= kAutoClusterKeys;
+            bool padded_in = false;  // the level reads a padded level-0 output (cluster items read `begin`)
+            for (const SegPlan& q : segs) padded_in |= q.rd() != q.begin;
             const bool use_cluster = level >= 1 && !src_f64 && cluster_available() &&
                                      ((cfg.flags & LSORT_FLAG_CLUSTER) || auto_cluster) && cap >= 16384 &&
-                                     !(classic && level <= 1);
+                                     !(classic && level <= 1) && !padded_in;
             std::vector<uint32_t> fwd1;  // classic: level-1 segments with a forwarded model
             std::vector<BaseItem> clus;
             std::vector<SegPlan> psegs;
@@ -607,6 +611,7 @@ struct Engine {
                 psegs.push_back(s);
                 SegDesc& d = hs[j];
                 d.begin = s.begin;
+                d.in_begin = s.rd();
                 d.n = s.n;
                 d.depth = s.depth;
                 d.flags = s.flags;
@@ -735,6 +740,30 @@ struct Engine {
                     fprintf(stderr, "    level_models host %.3f ms\n",
                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
             }
+            // ---- padded one-pass level 0 (k_direct) when the root is learned and its
+            // buckets are large; the exact two-pass level below runs only if it did not
+            // (Ctrl::run_exact: tree root, or a bucket outgrew its estimated region)
+            static const bool no_direct = getenv("LSORT_NO_DIRECT") != nullptr;
+            const bool direct = !no_direct && level == 0 && !fw && !classic && np == 1 && bigs.size() == 1 &&
+                                root_slices && hs[0].nb_max <= 1024 && n >= kDirectMinPerBucket * hs[0].nb_max;
+            if (direct) {
+                const uint64_t s2 = sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
+                const uint64_t alloc = direct_capacity_bound(n, s2, hs[0].nb_max);
+                if (!C->scratch2.ensure(8 * alloc) || !C->dws.ensure(direct_workspace_bytes(2048)) ||
+                    !C->ids.ensure(2 * alloc))
+                    throw LsortError{LSORT_ENOMEM, "padded level 0"};
+                LevelParams pd = p;
+                pd.dst = C->scratch2.as<uint64_t>();
+                pd.ids = C->ids.as<uint16_t>();
+                if (timing) CU(cudaEventRecord(C->pev[6], st));
+                launch_direct(pd, src_f64, lane(0)->aux.as<uint32_t>(), root_slices, s2, alloc, C->dws.p,
+                              (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM), st,
+                              (cfg.flags & LSORT_FLAG_TEST_DIRECT_OVERFLOW) != 0);
+                if (timing) CU(cudaEventRecord(C->pev[7], st));
+                launched(3);
+                p.gate = &dctrl->run_exact;
+                p.ids = C->ids.as<uint16_t>();
+            }
             // ---- partition
             const int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
             const int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
@@ -796,6 +825,12 @@ struct Engine {
             if (timing) {
                 float t[5];
                 for (int i = 0; i < 5; ++i) CU(cudaEventElapsedTime(&t[i], C->pev[i], C->pev[i + 1]));
+                if (direct) {  // the padded one-pass level 0 is a scatter (launched inside the models mark)
+                    float td = 0;
+                    CU(cudaEventElapsedTime(&td, C->pev[6], C->pev[7]));
+                    t[0] -= td;
+                    t[2] += td;
+                }
                 if (trace_enabled()) {
                     uint64_t keys = 0, mx = 0;
                     for (auto& q : segs) { keys += q.n; mx = std::max(mx, q.n); }
@@ -861,6 +896,7 @@ struct Engine {
                 uint64_t moved = 0;
                 for (uint32_t i = 0; i < ns; ++i) moved += segs[i].n;
                 stats->partitioned_keys += moved;
+                if (hc->direct) stats->direct_keys += moved;
                 stats->base_case_keys += hc->keys_base;
                 stats->fill_keys += hc->keys_fill;
                 stats->base_segments += (uint64_t)hc->n_base[0] + hc->n_base[1] + hc->n_base[2];
@@ -881,12 +917,13 @@ struct Engine {
                 segs.reserve(nrec);
                 for (uint32_t i = 0; i < nrec; ++i)
                     segs.push_back({r[i].begin, r[i].n, r[i].depth, r[i].flags,
-                                    (C->psample.p || (fw && fw->psample)) ? r[i].pslice : 0});
+                                    (C->psample.p || (fw && fw->psample)) ? r[i].pslice : 0, r[i].in_begin});
                 std::sort(segs.begin(), segs.end(),
                           [](const SegPlan& a, const SegPlan& b) { return a.begin < b.begin; });
             }
-            // ping-pong: this level's output becomes the next level's input
-            src = dst;
+            // ping-pong: this level's output becomes the next level's input (a padded
+            // level 0 wrote scratch2; the next level writes exact offsets into `keys`)
+            src = hc->direct ? (void*)C->scratch2.p : (void*)dst;
             src_f64 = false;
             dst = (dst == C->scratch.as<uint64_t>()) ? (uint64_t*)keys : C->scratch.as<uint64_t>();
             ++level;

@@ -18,6 +18,10 @@ struct SegDesc {
     uint32_t tree_k, pad;    // tree bucket budget
     uint64_t pslice;         // GPU policy: (offset << 24 | len) of this segment's keys in the
                              // parent level's sorted sample (DevCfg::psample), 0 = draw a sample
+    uint64_t in_begin;       // where the segment's keys are READ (the level's input buffer);
+                             // == begin except after a padded level-0 partition (k_direct),
+                             // whose buckets sit at estimated offsets while `begin` (the write
+                             // coordinates of this level's output) is exact
 };
 constexpr uint32_t kSegForceRadix = 1u;
 
@@ -25,7 +29,8 @@ constexpr uint32_t kSegForceRadix = 1u;
 struct SegOut {
     uint64_t begin, n;
     uint32_t depth, flags;
-    uint64_t pslice;  // see SegDesc::pslice
+    uint64_t pslice;    // see SegDesc::pslice
+    uint64_t in_begin;  // see SegDesc::in_begin
 };
 struct BaseItem {
     uint64_t begin, n;
@@ -41,6 +46,8 @@ struct Ctrl {
     unsigned int n_base[3];
     unsigned int n_fill;
     unsigned int err;
+    unsigned int direct;            // level 0 ran the padded one-pass partition (k_direct)
+    unsigned int run_exact;         // gate of the exact two-pass level (0 when k_direct succeeded)
     unsigned long long keys_fill, keys_base, keys_rec;
     unsigned long long verify_first;
     unsigned long long verify_hash;
@@ -155,6 +162,14 @@ void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_
 void launch_scan_children(const LevelParams& p, uint32_t max_nb, cudaStream_t st);
 // scatter of every segment of the level (all kinds), bucket ids from k_hist in p.ids
 void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid, cudaStream_t st);
+// Padded one-pass level 0 (k_direct, partition.cu). dw: device workspace of
+// direct_workspace_bytes(nb) bytes; alloc_keys: capacity of p.dst (keys).
+size_t direct_workspace_bytes(uint32_t nb);
+constexpr uint64_t kDirectMinPerBucket = 65536;  // mean keys per root bucket for the padded level 0
+void launch_direct(const LevelParams& p, int in_f64, const uint32_t* gate, const uint32_t* slices, uint64_t s,
+                   uint64_t alloc_keys, void* dw, int grid, cudaStream_t st, bool test_overflow = false);
+// bound on the padded output of launch_direct for n keys, a sample of s, nb buckets
+uint64_t direct_capacity_bound(uint64_t n, uint64_t s, uint32_t nb);
 // basecase.cu
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
 // cls 0: <= 1 Ki keys, 1: <= 4 Ki, 2: list 2 items > 8 Ki, 3: list 2 items <= 8 Ki

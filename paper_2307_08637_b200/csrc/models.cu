@@ -381,7 +381,7 @@ template <int NT>
 __device__ void build_radix_model(const SegDesc& sd, const void* src, bool f64, ModelHdr* h, uint64_t* red) {
     uint64_t mn = ~0ull, mx = 0;
     for (uint64_t i = threadIdx.x; i < sd.n; i += NT) {
-        uint64_t k = load_key(src, sd.begin + i, f64);
+        uint64_t k = load_key(src, sd.in_begin + i, f64);
         mn = k < mn ? k : mn;
         mx = k > mx ? k : mx;
     }
@@ -419,7 +419,7 @@ __device__ void sample_sorted(const SegDesc& sd, const void* src, uint64_t seed,
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint32_t i = i0 + u * NT;
-            v[u] = i < cnt ? load_key(src, sd.begin + sample_index_inv(seed, j0 + i, sd.n, minv), IN_F64) : 0ull;
+            v[u] = i < cnt ? load_key(src, sd.in_begin + sample_index_inv(seed, j0 + i, sd.n, minv), IN_F64) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -556,7 +556,7 @@ __global__ void k_gather(const SegDesc* seg, const void* src, uint64_t seed, uin
     const SegDesc sd = *seg;
     const uint64_t minv = sd.n ? ~0ull / sd.n : 0ull;
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < s; j += (uint64_t)gridDim.x * blockDim.x)
-        out[j] = load_key(src, sd.begin + sample_index_inv(seed, j0 + j, sd.n, minv), IN_F64);
+        out[j] = load_key(src, sd.in_begin + sample_index_inv(seed, j0 + j, sd.n, minv), IN_F64);
 }
 
 

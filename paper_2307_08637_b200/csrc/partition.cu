@@ -20,6 +20,7 @@
 // Model tables (learned: 20 B per submodel; tree payload) are copied to
 // shared memory by k_hist.
 #include <algorithm>
+#include <climits>
 
 #include "kernels_common.cuh"
 #include "tma.cuh"
@@ -322,9 +323,9 @@ __device__ __forceinline__ TileGeom tile_geom(const LevelParams& p, const KindTi
     else
         while (i + 1 < KT.nks && KT.tp[i + 1] <= t) ++i;
     const SegDesc& sd = p.segs[KT.ks[i]];
-    const uint64_t lo = sd.begin + (t - KT.tp[i]) * (uint64_t)kTileKeys;
+    const uint64_t lo = sd.in_begin + (t - KT.tp[i]) * (uint64_t)kTileKeys;
     TileGeom g;
-    g.init(p.src, lo, min(lo + kTileKeys, sd.begin + sd.n));
+    g.init(p.src, lo, min(lo + kTileKeys, sd.in_begin + sd.n));
     return g;
 }
 
@@ -600,7 +601,7 @@ __global__ void __launch_bounds__(NT) k_scan_children(LevelParams p) {
                     const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
                     if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
                 }
-                if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, flags, ps};
+                if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, flags, ps, begin};
                 else atomicOr(&p.ctrl->err, 4u);
             }
         }
@@ -635,9 +636,9 @@ __device__ __forceinline__ TileGeom tile_geom_all(const LevelParams& p, uint64_t
     else
         while (i + 1 < p.nsegs && p.tile_prefix[i + 1] <= t) ++i;
     const SegDesc& sd = p.segs[i];
-    const uint64_t lo = sd.begin + (t - p.tile_prefix[i]) * (uint64_t)kTileKeys;
+    const uint64_t lo = sd.in_begin + (t - p.tile_prefix[i]) * (uint64_t)kTileKeys;
     TileGeom g;
-    g.init(p.src, lo, min(lo + kTileKeys, sd.begin + sd.n));
+    g.init(p.src, lo, min(lo + kTileKeys, sd.in_begin + sd.n));
     return g;
 }
 
@@ -842,6 +843,315 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
     if (p.remote) __threadfence_system();
 }
 
+// ----------------------------------------------- padded one-pass level 0
+// Level 0 of a large input under a learned root model: classify, rank, claim
+// and scatter in ONE pass (no k_hist pass, no stored bucket ids: 8 + 16 B per
+// key instead of 10 + 18). The bucket counts are not known in advance, so
+// bucket b writes into a padded region [base_b, base_b + cap_b) sized from the
+// root's sorted RMI sample (c_b samples of s): cap_b = ceil(n/s (c_b +
+// 6 sqrt(c_b) + 8)) -- about six standard deviations of the sampling error.
+// A claim past its region's end is not written and raises the overflow flag;
+// the exact two-pass level (k_hist / k_scan_children / k_scatter, gated on
+// Ctrl::run_exact) then runs instead, so the result never depends on the
+// estimate. The children read their keys at the padded base (SegOut::in_begin)
+// and write the next level's output at exact offsets (SegOut::begin).
+constexpr double kDirectSigma = 6.0, kDirectSlack = 8.0;
+
+struct DirectWS {
+    unsigned long long* cur;   // [nb] claim cursors (absolute padded positions)
+    unsigned long long* base;  // [nb + 1] padded region starts (base[nb] = total)
+    unsigned long long* end;   // [nb] region ends
+    uint32_t* ovf;             // overflow flag
+};
+__host__ __device__ inline DirectWS direct_ws(void* w, uint32_t nb) {
+    DirectWS d;
+    d.cur = (unsigned long long*)w;
+    d.base = d.cur + nb;
+    d.end = d.base + nb + 1;
+    d.ovf = (uint32_t*)(d.end + nb);
+    return d;
+}
+size_t direct_workspace_bytes(uint32_t nb) { return 8 * (3 * (size_t)nb + 1) + 16; }
+
+uint64_t direct_capacity_bound(uint64_t n, uint64_t s, uint32_t nb) {
+    // sum_b sqrt(c_b) <= sqrt(nb s) (Cauchy-Schwarz); + 1 per bucket for the ceiling
+    const double r = (double)n / (double)s;
+    return (uint64_t)(r * ((double)s + kDirectSigma * sqrt((double)nb * (double)s) + kDirectSlack * nb)) + 2 * nb + 16;
+}
+
+// One CTA: direct = gate && learned model; capacities from the sample slices,
+// their exclusive scan, cursors at the region starts.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_direct_setup(LevelParams p, const uint32_t* gate, const uint32_t* off,
+                                                     uint64_t s, uint64_t alloc, DirectWS w, double sigma,
+                                                     double slack) {
+    griddep_wait();
+    __shared__ uint64_t wsum[NT / 32 + 1];
+    extern __shared__ uint64_t capv[];  // nb + 1
+    const ModelHdr* h = (const ModelHdr*)p.models;
+    const bool on = (!gate || *gate) && h->kind == kLearned;
+    const uint32_t nb = h->nbuckets;
+    const uint64_t n = p.segs[0].n;
+    if (!on) {
+        if (threadIdx.x == 0) { p.ctrl->direct = 0; p.ctrl->run_exact = 1; }
+        return;
+    }
+    const double r = (double)n / (double)s;
+    for (uint32_t b = threadIdx.x; b < nb; b += NT) {
+        const double c = (double)(off[b + 1] - off[b]);
+        const double e = c + sigma * sqrt(c) + slack;
+        capv[b] = e > 0.0 ? (uint64_t)ceil(r * e) : 0ull;
+    }
+    __syncthreads();
+    const uint64_t tot = block_exclusive_scan_u64<NT>(capv, nb, wsum);
+    for (uint32_t b = threadIdx.x; b < nb; b += NT) {
+        w.base[b] = capv[b];
+        w.cur[b] = capv[b];
+        w.end[b] = b + 1 < nb ? capv[b + 1] : tot;
+    }
+    if (threadIdx.x == 0) {
+        w.base[nb] = tot;
+        *w.ovf = tot > alloc ? 1u : 0u;  // (cannot happen: alloc is the host's bound)
+        p.ctrl->direct = 1;
+        p.ctrl->run_exact = 0;
+    }
+}
+
+struct DirectSmem {
+    uint64_t bars[2];
+    ulonglong2 tiles[2][kTileKeys / 2];  // TMA tile buffers; the consumed one stages the tile
+    long long delta[1024];               // per bucket: claimed position - tile-local start
+    alignas(16) uint32_t cnt[2][1024 + 4];
+    uint16_t sbid[kTileKeys];
+    uint32_t wsum[kPNT / 32 + 1];
+    alignas(16) uint8_t table[20 * 1024];  // the learned model's compiled table (kstate_load)
+};
+
+template <bool IN_F64>
+__global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, DirectWS w) {
+    griddep_wait();
+    extern __shared__ uint4 smem_u4[];
+    DirectSmem& Q = *(DirectSmem*)smem_u4;
+    constexpr uint32_t NBC = 1024;
+    if (!p.ctrl->direct) return;
+    const uint64_t per = (p.ntiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * per;
+    const uint64_t t1 = min(t0 + per, p.ntiles);
+    if (t0 >= t1) return;
+    // the learned model's compiled table in the (unused) id staging area
+    KState S;
+    kstate_load<kLearned>(S, p.models, Q.table);
+    const uint32_t nb = S.nb;
+    for (uint32_t b = threadIdx.x; b < NBC; b += kPNT) Q.cnt[0][b] = Q.cnt[1][b] = 0;
+    TileStream TS;
+    TS.init((uint8_t*)Q.tiles, Q.bars);
+    uint32_t inext = ~0u;
+    TileGeom gnext = tile_geom_all(p, t0, inext);
+    TS.issue(p.src, gnext, 0);
+    bool ovf = false;
+    for (uint64_t tile = t0; tile < t1; ++tile) {
+        const int tb = (int)((tile - t0) & 1);
+        const TileGeom g = gnext;
+        uint32_t* cnt = Q.cnt[tb];
+        TS.wait(g, tb);
+        const ulonglong2* sp = TS.buf(tb);
+        uint64_t* skeys = (uint64_t*)TS.buf(tb);  // staging reuses the consumed tile buffer
+        ulonglong2 v[kPPairs];
+#pragma unroll
+        for (int j = 0; j < kPPairs; ++j) {
+            const uint32_t qq = threadIdx.x + j * kPNT;
+            v[j] = qq < g.npairs ? sp[qq] : make_ulonglong2(0, 0);
+        }
+        if (IN_F64) {
+            bool anynan = false;
+#pragma unroll
+            for (int j = 0; j < kPPairs; ++j)
+                anynan |= (threadIdx.x + j * kPNT < g.npairs) &&
+                          (isnan(__longlong_as_double((long long)v[j].x)) | isnan(__longlong_as_double((long long)v[j].y)));
+            if (anynan) {
+#pragma unroll
+                for (int j = 0; j < kPPairs; ++j) {
+                    const uint32_t q = threadIdx.x + j * kPNT;
+                    if (q < g.npairs) {
+                        if (isnan(__longlong_as_double((long long)v[j].x)))
+                            atomicMin(&p.ctrl->nan_index, (unsigned long long)(g.a0 + 2 * q));
+                        if (isnan(__longlong_as_double((long long)v[j].y)))
+                            atomicMin(&p.ctrl->nan_index, (unsigned long long)(g.a0 + 2 * q + 1));
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kPPairs; ++j) {
+                v[j].x = encode(__longlong_as_double((long long)v[j].x));
+                v[j].y = encode(__longlong_as_double((long long)v[j].y));
+            }
+        }
+        uint32_t code[kPItems];  // bucket << 16 | rank within the tile; ~0 = no key
+        {
+            uint32_t bk[kPItems];
+            classify16<kLearned>(S, v, bk);
+#pragma unroll
+            for (int q = 0; q < kPItems; ++q) {
+                const bool ok = threadIdx.x + (q >> 1) * kPNT < g.npairs;
+                const uint32_t b = ok ? bk[q] : 0u;
+                code[q] = ok ? (b << 16 | atomicAdd(&cnt[b], 1u)) : 0xffffffffu;
+            }
+        }
+        uint64_t skey = 0;
+        uint32_t scode = 0xffffffffu;
+        if (threadIdx.x < g.nsingle) {
+            const uint64_t ix = g.single(threadIdx.x);
+            uint64_t k = ((const uint64_t*)p.src)[ix];
+            if (IN_F64) {
+                const double d = __longlong_as_double((long long)k);
+                if (isnan(d)) atomicMin(&p.ctrl->nan_index, (unsigned long long)ix);
+                k = encode(d);
+            }
+            const uint32_t b = kclassify<kLearned>(S, k);
+            scode = b << 16 | atomicAdd(&cnt[b], 1u);
+            skey = k;
+        }
+        __syncthreads();  // (1) tile counts complete; every thread is past the previous tile
+        if (tile + 1 < t1) {
+            gnext = tile_geom_all(p, tile + 1, inext);
+            TS.issue(p.src, gnext, tb ^ 1);
+        }
+        constexpr int kPer = NBC / kPNT;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint32_t bb = threadIdx.x * kPer;
+        const uint2 t2 = *(const uint2*)&cnt[bb];
+        const uint32_t cn0 = t2.x, cn1 = t2.y, sum = cn0 + cn1;
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o) incl += x;
+        }
+        if (lane == 31) Q.wsum[warp] = incl;
+        __syncthreads();  // (2)
+        const uint32_t wv = lane < kPNT / 32 ? Q.wsum[lane] : 0u;
+        const uint32_t total = __reduce_add_sync(FULL_MASK, wv);
+        const uint32_t run = __reduce_add_sync(FULL_MASK, lane < warp ? wv : 0u) + incl - sum;
+        *(uint2*)&cnt[bb] = make_uint2(run, run + cn0);
+        if (threadIdx.x == 0) cnt[NBC] = total;
+        __syncthreads();  // (3) tile-local bucket starts visible
+        {
+            unsigned long long got[kPer];
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                const uint32_t b = threadIdx.x + q * kPNT;
+                got[q] = 0;
+                if (b < nb) {
+                    const uint32_t c = cnt[b + 1] - cnt[b];
+                    if (c) {
+                        got[q] = atomicAdd(&w.cur[b], (unsigned long long)c);
+                        if (got[q] + c > w.end[b]) {  // region full: nothing of this run is written
+                            ovf = true;
+                            got[q] = ~0ull;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                const uint32_t b = threadIdx.x + q * kPNT;
+                Q.delta[b] = got[q] == ~0ull ? LLONG_MIN : (long long)got[q] - (long long)cnt[b];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPItems; ++j) {
+            const uint32_t c = code[j];
+            if (c != 0xffffffffu) {
+                const uint32_t pos = cnt[c >> 16] + (c & 0xffffu);
+                skeys[pos] = (j & 1) ? v[j >> 1].y : v[j >> 1].x;
+                Q.sbid[pos] = (uint16_t)(c >> 16);
+            }
+        }
+        if (scode != 0xffffffffu) {
+            const uint32_t pos = cnt[scode >> 16] + (scode & 0xffffu);
+            skeys[pos] = skey;
+            Q.sbid[pos] = (uint16_t)(scode >> 16);
+        }
+        __syncthreads();  // (4)
+#pragma unroll
+        for (int q = 0; q < kTileKeys / kPNT; ++q) {
+            const uint32_t j = threadIdx.x + q * kPNT;
+            if (j < total) {
+                const long long d = Q.delta[Q.sbid[j]];
+                if (d != LLONG_MIN) p.dst[(long long)j + d] = skeys[j];
+            }
+        }
+        *(uint2*)&cnt[bb] = make_uint2(0, 0);
+        fence_proxy_async_smem();
+    }
+    if (ovf) atomicOr(w.ovf, 1u);
+}
+
+// One CTA: unless a region overflowed, the children are the buckets -- read at
+// their padded base, written exactly (exclusive scan of the counts); all of
+// them go to the next level (the GPU policy admits a padded level only when
+// the mean bucket is far above the base-case capacity). Overflow: run_exact.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS w) {
+    griddep_wait();
+    __shared__ uint64_t wsum[NT / 32 + 1];
+    __shared__ uint32_t lbase;
+    extern __shared__ uint64_t cntv[];  // nb
+    if (!p.ctrl->direct || p.ctrl->nan_index != ~0ull) return;
+    if (*w.ovf) {
+        if (threadIdx.x == 0) { p.ctrl->direct = 0; p.ctrl->run_exact = 1; }
+        return;
+    }
+    const SegDesc sd = p.segs[0];
+    const uint32_t nb = ((const ModelHdr*)p.models)->nbuckets;
+    for (uint32_t b = threadIdx.x; b < nb; b += NT) cntv[b] = w.cur[b] - w.base[b];
+    __syncthreads();
+    block_exclusive_scan_u64<NT>(cntv, nb, wsum);
+    if (threadIdx.x == 0) lbase = 0;
+    __syncthreads();
+    for (uint32_t b0 = 0; b0 < nb; b0 += NT) {
+        const uint32_t b = b0 + threadIdx.x;
+        uint64_t st = 0, len = 0;
+        if (b < nb) {
+            st = cntv[b];
+            len = (b + 1 < nb ? cntv[b + 1] : sd.n) - st;
+        }
+        const bool emit = len > 0;
+        const unsigned m = __ballot_sync(FULL_MASK, emit);
+        uint32_t wb = 0;
+        if ((threadIdx.x & 31) == 0 && m) wb = atomicAdd(&lbase, (uint32_t)__popc(m));
+        wb = __shfl_sync(FULL_MASK, wb, 0);
+        if (emit) {
+            const uint32_t e = wb + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
+            uint64_t ps = 0;
+            if (p.slices) {
+                const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
+                if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
+            }
+            const uint32_t flags = (len == sd.n) ? kSegForceRadix : 0u;
+            if (e < p.list_cap) p.rec[e] = SegOut{sd.begin + st, len, sd.depth + 1, flags, ps, w.base[b]};
+            else atomicOr(&p.ctrl->err, 4u);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        p.ctrl->n_rec = lbase;
+        p.ctrl->keys_rec = sd.n;
+    }
+}
+
+void launch_direct(const LevelParams& p, int in_f64, const uint32_t* gate, const uint32_t* slices, uint64_t s,
+                   uint64_t alloc_keys, void* dw, int grid, cudaStream_t st, bool test_overflow) {
+    const uint32_t nbmax = 2048;
+    const DirectWS w = direct_ws(dw, nbmax);
+    const double sigma = test_overflow ? -kDirectSigma : kDirectSigma, slack = test_overflow ? 0.0 : kDirectSlack;
+    pdl(k_direct_setup<1024>, 1, 1024, 8 * ((size_t)nbmax + 2), st, p, gate, slices, s, alloc_keys, w, sigma, slack);
+    constexpr size_t sm = sizeof(DirectSmem);
+    if (in_f64) pdl(k_direct<true>, grid, kPNT, sm, st, p, w);
+    else pdl(k_direct<false>, grid, kPNT, sm, st, p, w);
+    pdl(k_direct_children<1024>, 1, 1024, 8 * ((size_t)nbmax + 2), st, p, w);
+}
+
 // ------------------------------------------------------------- launchers
 static const uint32_t kTreeCap = (uint32_t)(kTreeCapBytes + kLutBytes);
 
@@ -856,6 +1166,10 @@ void partition_init(int optin) {
     allow_smem(k_scatter<false, 1024>, optin);
     allow_smem(k_scatter<true, kMaxNB>, optin);
     allow_smem(k_scatter<false, kMaxNB>, optin);
+    allow_smem(k_direct<true>, optin);
+    allow_smem(k_direct<false>, optin);
+    allow_smem(k_direct_setup<1024>, optin);
+    allow_smem(k_direct_children<1024>, optin);
     allow_smem(k_scan_children<128>, optin);
     allow_smem(k_scan_children<512>, optin);
     allow_smem(k_scan_children<1024>, optin);

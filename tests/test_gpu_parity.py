@@ -533,3 +533,23 @@ def test_sort_no_progress_fallback(ctx, case):
     t_norm = time.perf_counter() - t0
     assert np.array_equal(host_u64(d2), exp)
     assert t_fb <= 10 * max(t_norm, 1e-3), (t_fb, t_norm)
+
+
+@pytest.mark.parametrize("dist_name,seed", [("exponential2", 7), ("lognormal2", 19)])
+def test_padded_level0_and_its_fallback(ctx, dist_name, seed):
+    """Large learned roots take the padded one-pass level 0 (k_direct: no
+    classify pass, buckets at sample-estimated offsets, children read padded
+    and written exact); with the test flag the regions are sized below their
+    counts, overflow, and the exact two-pass level runs instead -- both
+    bit-exact."""
+    n = 80_000_000
+    x = O.generate(dist_name, n, seed)
+    exp = O.decode(np.sort(O.encode(x))).view(np.uint64)
+    d = dev(x)
+    st = ctx.sort(d)
+    assert st["direct_keys"] == n
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), exp)
+    d = dev(x)
+    st = ctx.sort(d, L.SortConfig(flags=L._native.FLAG_TEST_DIRECT_OVERFLOW))
+    assert st["direct_keys"] == 0
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), exp)

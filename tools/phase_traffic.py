@@ -9,7 +9,7 @@ import csv
 import json
 import sys
 
-PHASE = [("k_base", "base"), ("k_small_sort", "base"), ("k_scatter", "scatter"), ("k_hist", "classify"),
+PHASE = [("k_base", "base"), ("k_small_sort", "base"), ("k_scatter", "scatter"), ("k_direct<", "scatter"), ("k_hist", "classify"),
          ("k_fill", "fill"), ("k_verify", None)]
 
 
