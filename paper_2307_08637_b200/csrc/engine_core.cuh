@@ -83,6 +83,8 @@ struct LsortError {
 // fused cluster kernel (measured: C1's 15 leaves of ~365 Ki keys 0.618 -> 0.562 ms
 // per sort; C2's full level 1 of 1e8 keys is 2x slower there)
 constexpr uint64_t kAutoClusterKeys = 4ull << 20;
+constexpr uint32_t kBigRootBuckets = 512;
+constexpr uint64_t kBigRootMinKeys = 32ull << 20;
 
 inline uint32_t fanout(uint64_t n, uint32_t cfg_count, uint32_t target) {
     if (target == 0) return cfg_count;
@@ -228,6 +230,9 @@ struct Engine {
     const uint64_t* given_sample = nullptr;
     uint64_t given_n = 0;
     uint32_t share_den = 0;
+    // GPU policy for a big learned root: RMI submodels (0 = the segment's
+    // rmi_b) when the root's output buckets are capped below them
+    uint32_t root_sub = 0;
     // LearnedSort 2.0 classic path (classic.cu): the root RMI (device model
     // record, CDF [0,1), classic_B buckets) is forwarded to level 0 (Forward)
     // and, restricted to each round-1 bucket's CDF range, to level 1; the
@@ -403,6 +408,7 @@ struct Engine {
         const cudaStream_t st = N->stream;  // this lane's stream
         DevCfg dc = dev_cfg(cfg);
         const uint64_t n = sp.n;
+        const uint32_t sub = (sp.depth == 0 && root_sub) ? root_sub : hseg.rmi_b;  // RMI submodels
         const uint64_t s1 = sample_size_host(cfg.sample_fraction, cfg.first_sample_cap, n);
         const uint64_t s2 = given_sample ? given_n : sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
         // sample-sort splitter budget: ~2 Ki samples per bucket (base-case class <= 4 Ki)
@@ -417,7 +423,7 @@ struct Engine {
             !N->base[0].ensure(nb * sizeof(BaseItem)) || !N->base[1].ensure(nb * sizeof(BaseItem)) ||
             !N->base[2].ensure(nb * sizeof(BaseItem)) || !N->kseg.ensure(64) || !N->ktp.ensure(64) ||
             !N->kplan.ensure(3 * sizeof(KindPlan)) || !N->ctrl.ensure(sizeof(Ctrl)) || !N->ids.ensure(2 * s2) ||
-            !N->aux.ensure(4) || !N->train_ws.ensure(train_workspace_bytes(s2, hseg.rmi_b)))
+            !N->aux.ensure(4) || !N->train_ws.ensure(train_workspace_bytes(s2, sub)))
             throw LsortError{LSORT_ENOMEM, "big model workspace"};
         uint32_t* gate = N->aux.as<uint32_t>();
         Ctrl* nctrl = N->ctrl.as<Ctrl>();
@@ -499,13 +505,17 @@ struct Engine {
         launch_scatter(q, 0, nb, g, st);
         launch_base_cases(q, N->scratch.as<uint64_t>(), N->sample.p, 0, st);
         launch_fill(q, N->sample.p, 0, nsm, st);
-        launch_train_rmi(N->sample.as<uint64_t>(), s2, hseg.rmi_b, C->models.as<uint8_t>() + hseg.model_off,
+        launch_train_rmi(N->sample.as<uint64_t>(), s2, sub, C->models.as<uint8_t>() + hseg.model_off,
                          hseg.rmi_b, N->train_ws.p, gate, st);
         launched(2 + 9 + 8);
         if (dc.quality) {  // (and the children's sample slices for the root)
             if (!N->qws.ensure(quality_workspace_bytes())) throw LsortError{LSORT_ENOMEM, "quality workspace"};
+            // a big root (>= 32 Mi keys, 512 buckets) keeps a learned model up to a
+            // bucket of 1/8 of the keys: such a bucket still makes progress, and the
+            // learned root takes the one-pass level 0 (a tree root does not)
+            const uint32_t poor_share = (sp.depth == 0 && n >= kBigRootMinKeys && !share_den) ? kPoorShare / 2 : kPoorShare;
             launch_quality_check(N->sample.as<uint64_t>(), s2, C->models.as<uint8_t>() + hseg.model_off, hseg.tree_k,
-                                 N->qws.p, slices, gate, st, share_den);
+                                 N->qws.p, slices, gate, st, share_den, poor_share);
             launched(slices ? 3 : 2);
         } else if (slices) {
             launch_sample_slices(N->sample.as<uint64_t>(), s2, C->models.as<uint8_t>() + hseg.model_off, slices,
@@ -618,6 +628,19 @@ struct Engine {
                 d.pslice = s.pslice;
                 const bool classic1 = classic && level == 1 && !(s.flags & kSegForceRadix);
                 d.rmi_b = (fw && level == 0) ? fw->nb : (classic1 ? classic_B : rmi_b(s.n));
+                // GPU policy: a learned root over >= 32 Mi keys partitions 512 ways (its
+                // level 0 writes 8-key runs instead of 4-key runs; the children, still far
+                // above the base-case capacity, take one more level either way): C5
+                // 12.11 -> 11.79 ms, C2 arrays -4%; 256 ways sent C5 segments to a third level
+                static const uint32_t root_cap =
+                    getenv("LSORT_ROOT_B") ? (uint32_t)atoi(getenv("LSORT_ROOT_B")) : kBigRootBuckets;
+                root_sub = 0;
+                if (level == 0 && !fw && !classic && !(cfg.flags & LSORT_FLAG_STRICT_POLICY) &&
+                    s.n >= kBigRootMinKeys && root_cap && root_cap < d.rmi_b) {
+                    root_sub = d.rmi_b;  // the RMI keeps its submodels; its CDF feeds fewer buckets
+                    d.rmi_b = root_cap;
+                }
+                max_rmi_b = std::max(max_rmi_b, root_sub);
                 max_rmi_b = std::max(max_rmi_b, d.rmi_b);
                 d.tree_k = tree_k(s.n);
                 uint32_t payload, nb;
@@ -626,7 +649,7 @@ struct Engine {
                     nb = 1u << kRadixBits;
                 } else {
                     uint32_t tp = (uint32_t)((tree_payload_bytes(d.tree_k, d.tree_k - 1) + 15) & ~15ull);
-                    payload = std::max<uint32_t>(kLearnedEntryBytes * d.rmi_b, tp);
+                    payload = std::max<uint32_t>(kLearnedEntryBytes * std::max(d.rmi_b, root_sub), tp);
                     nb = std::max<uint32_t>(d.rmi_b, 2 * d.tree_k - 1);
                 }
                 d.nb_max = nb;

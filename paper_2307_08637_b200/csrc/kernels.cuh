@@ -144,9 +144,11 @@ size_t train_workspace_bytes(uint64_t s, uint32_t B);
 // GPU policy (DevCfg::quality) for a big segment's learned model trained on the
 // sorted sample: classify the sample, fall back to a splitter tree if poor.
 // offs (nullable): also returns the final model's bucket offsets in the sample
-// share_den > 0: also poor when the largest bucket holds more than 1/share_den of the sample
+// share_den > 0: also poor when the largest bucket holds more than 1/share_den of the sample;
+// poor_share: the poor_model share test (1/poor_share of the sample, default kPoorShare)
 void launch_quality_check(const uint64_t* sorted, uint64_t s, uint8_t* model, uint32_t tree_k, void* ws,
-                          uint32_t* offs, const uint32_t* gate, cudaStream_t st, uint32_t share_den = 0);
+                          uint32_t* offs, const uint32_t* gate, cudaStream_t st, uint32_t share_den = 0,
+                          uint32_t poor_share = kPoorShare);
 size_t quality_workspace_bytes();
 // offsets[b] = first index of the sorted sample whose bucket (under `model`) is >= b, b <= nb
 void launch_sample_slices(const uint64_t* sorted, uint64_t s, const uint8_t* model, uint32_t* offsets,

@@ -943,7 +943,7 @@ __global__ void __launch_bounds__(512) k_block_sort(uint64_t* keys, uint32_t n) 
 // the model was replaced, so the offsets are recomputed for the tree)
 __global__ void __launch_bounds__(512) k_quality(const uint64_t* s, uint32_t n, uint8_t* model, uint32_t tree_k,
                                                  const uint32_t* offs, uint32_t* redo, const uint32_t* gate,
-                                                 uint32_t share_den) {
+                                                 uint32_t share_den, uint32_t poor_share) {
     griddep_wait();
     __shared__ uint32_t scratch[2 * LSORT_MAX_TREE_DEV + 2];
     __shared__ uint32_t wsum[512 / 32 + 1];
@@ -960,7 +960,8 @@ __global__ void __launch_bounds__(512) k_quality(const uint64_t* s, uint32_t n, 
         mx = c > mx ? c : mx;
     }
     mx = block_reduce_max<512>(mx, red);
-    if (!poor_model(mx, n, nb) && !(share_den && mx * share_den > n)) return;
+    const bool poor = mx * poor_share > n && mx * nb > (uint64_t)kPoorMean * n;
+    if (!poor && !(share_den && mx * share_den > n)) return;
     tree_build_block<512>(s, n, tree_k, true, h, model + sizeof(ModelHdr), scratch, wsum, spl);
     if (threadIdx.x == 0) *redo = 1;
 }
@@ -995,11 +996,12 @@ void launch_sample_slices(const uint64_t* sorted, uint64_t s, const uint8_t* mod
 
 
 void launch_quality_check(const uint64_t* sorted, uint64_t s, uint8_t* model, uint32_t tree_k, void* ws,
-                          uint32_t* offs, const uint32_t* gate, cudaStream_t st, uint32_t share_den) {
+                          uint32_t* offs, const uint32_t* gate, cudaStream_t st, uint32_t share_den,
+                          uint32_t poor_share) {
     uint32_t* o = offs ? offs : (uint32_t*)ws;
     uint32_t* redo = (uint32_t*)ws + LSORT_MAX_RMI_DEV + 4;
     launch_sample_slices(sorted, s, model, o, 0, gate, st);
-    pdl(k_quality, 1, 512, 0, st, sorted, (uint32_t)s, model, tree_k, o, redo, gate, share_den);
+    pdl(k_quality, 1, 512, 0, st, sorted, (uint32_t)s, model, tree_k, o, redo, gate, share_den, poor_share);
     if (offs) launch_sample_slices(sorted, s, model, o, 0, redo, st);  // the tree's offsets
 }
 
