@@ -576,6 +576,7 @@ struct Engine {
         uint64_t* dst = C->scratch.as<uint64_t>();
         uint32_t level = start ? 1 : 0;
         DevCfg dc = dev_cfg(cfg);
+        uint64_t* lvl_dout = nullptr;  // the padded output of the current level when it ran one-pass
         while (!segs.empty()) {
             const uint32_t ns = (uint32_t)segs.size();
             // ---- plan the level on the host
@@ -738,6 +739,16 @@ struct Engine {
             uint32_t* root_slices = nullptr;
             dc.psample = (level == 1 && C->psample.p) ? C->psample.as<uint64_t>() : nullptr;
             if (fw) dc.psample = level == 1 ? fw->psample : nullptr;
+            // one-pass level 0 (GPU policy): a learned root with >= 64 Ki keys per bucket.
+            // (A one-pass level 1 needs all of its segments learned with >= 32 samples per
+            // bucket; with the 6-sigma padding of C5's 8 samples per bucket it spread the
+            // writes over ~4x the keys and the level got slower, 12.3 -> 15.6 ms -- measured,
+            // not kept.)
+            static const bool no_direct = getenv("LSORT_NO_DIRECT") != nullptr;
+            // (no cluster segments: their children sit in the level's exact output)
+            const bool direct0 = !no_direct && !fw && !classic && !(cfg.flags & LSORT_FLAG_STRICT_POLICY) &&
+                                 level == 0 && np == 1 && ncl == 0 && bigs.size() == 1 &&
+                                 hs[0].nb_max <= kDirectMaxBuckets && n >= kDirectMinPerBucket * hs[0].nb_max;
             if (fw && level == 0) {
                 CU(cudaMemcpyAsync(C->models.p, fw->model, fw->model_bytes, cudaMemcpyDeviceToDevice, st));
                 p.slices = fw->slices;
@@ -763,30 +774,35 @@ struct Engine {
                     fprintf(stderr, "    level_models host %.3f ms\n",
                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
             }
-            // ---- padded one-pass level 0 (k_direct) when the root is learned and its
-            // buckets are large; the exact two-pass level below runs only if it did not
-            // (Ctrl::run_exact: tree root, or a bucket outgrew its estimated region)
-            static const bool no_direct = getenv("LSORT_NO_DIRECT") != nullptr;
-            const bool direct = !no_direct && level == 0 && !fw && !classic && np == 1 && bigs.size() == 1 &&
-                                root_slices && hs[0].nb_max <= 1024 && n >= kDirectMinPerBucket * hs[0].nb_max;
-            if (direct) {
-                const uint64_t s2 = sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
-                const uint64_t alloc = direct_capacity_bound(n, s2, hs[0].nb_max);
-                if (!C->scratch2.ensure(8 * alloc) || !C->dws.ensure(direct_workspace_bytes(2048)) ||
-                    !C->ids.ensure(2 * alloc))
-                    throw LsortError{LSORT_ENOMEM, "padded level 0"};
+            // ---- one-pass (padded) level (k_direct): launched here, after the models;
+            // the exact two-pass level below runs only if it did not (Ctrl::run_exact:
+            // an ineligible model or a region that outgrew its estimate)
+            uint64_t* dout = nullptr;
+            uint64_t root_m = 0, alloc = 0;
+            if (direct0) {
+                root_m = sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
+                alloc = direct_capacity_bound(n, root_m, hs[0].nb_max);
+                // (level 1 reads this padded output: its bucket ids are indexed by read position)
+                if (!C->scratch2.ensure(8 * alloc) || !C->ids.ensure(2 * alloc))
+                    throw LsortError{LSORT_ENOMEM, "one-pass level 0"};
+                dout = C->scratch2.as<uint64_t>();
+            }
+            if (dout) {
+                if (!C->dws.ensure(direct_workspace_bytes(nbuckets, np))) throw LsortError{LSORT_ENOMEM, "one-pass level"};
                 LevelParams pd = p;
-                pd.dst = C->scratch2.as<uint64_t>();
-                pd.ids = C->ids.as<uint16_t>();
+                pd.dst = dout;
+                pd.slices = root_slices;
                 if (timing) CU(cudaEventRecord(C->pev[6], st));
-                launch_direct(pd, src_f64, lane(0)->aux.as<uint32_t>(), root_slices, s2, alloc, C->dws.p,
+                launch_direct(pd, src_f64, root_m, alloc, C->dws.p, nbuckets,
                               (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM), st,
                               (cfg.flags & LSORT_FLAG_TEST_DIRECT_OVERFLOW) != 0);
                 if (timing) CU(cudaEventRecord(C->pev[7], st));
-                launched(3);
+                launched(4);
                 p.gate = &dctrl->run_exact;
-                p.ids = C->ids.as<uint16_t>();
             }
+            p.ids = C->ids.as<uint16_t>();  // (the one-pass setup may have grown the id array)
+            const bool direct = dout != nullptr;
+            lvl_dout = dout;
             // ---- partition
             const int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
             const int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
@@ -845,6 +861,11 @@ struct Engine {
             CU(cudaGetLastError());
             if (hc->nan_index != ~0ull) throw LsortError{LSORT_ENAN, std::to_string(hc->nan_index)};
             if (hc->err) throw LsortError{LSORT_EINTERNAL, "work list overflow (" + std::to_string(hc->err) + ")"};
+            if (trace_enabled() && direct) {
+                uint32_t fl = 0;
+                CU(cudaMemcpy(&fl, direct_flag_ptr(C->dws.p, nbuckets, np), 4, cudaMemcpyDeviceToHost));
+                fprintf(stderr, "    one-pass level %u: flag %u (0 ran, 1 overflow, 2 ineligible)\n", level, fl);
+            }
             if (timing) {
                 float t[5];
                 for (int i = 0; i < 5; ++i) CU(cudaEventElapsedTime(&t[i], C->pev[i], C->pev[i + 1]));
@@ -946,7 +967,7 @@ struct Engine {
             }
             // ping-pong: this level's output becomes the next level's input (a padded
             // level 0 wrote scratch2; the next level writes exact offsets into `keys`)
-            src = hc->direct ? (void*)C->scratch2.p : (void*)dst;
+            src = hc->direct ? (void*)lvl_dout : (void*)dst;
             src_f64 = false;
             dst = (dst == C->scratch.as<uint64_t>()) ? (uint64_t*)keys : C->scratch.as<uint64_t>();
             ++level;

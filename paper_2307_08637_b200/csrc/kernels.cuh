@@ -164,14 +164,19 @@ void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_
 void launch_scan_children(const LevelParams& p, uint32_t max_nb, cudaStream_t st);
 // scatter of every segment of the level (all kinds), bucket ids from k_hist in p.ids
 void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid, cudaStream_t st);
-// Padded one-pass level 0 (k_direct, partition.cu). dw: device workspace of
-// direct_workspace_bytes(nb) bytes; alloc_keys: capacity of p.dst (keys).
-size_t direct_workspace_bytes(uint32_t nb);
+// One-pass (padded) level (k_direct, partition.cu): level 0 with the root
+// sample's bucket offsets in p.slices (root_m samples). dw: direct_workspace_bytes(slots, nsegs)
+// bytes (slots: the level's bucket counter slots); alloc_keys: capacity of
+// p.dst (keys). Ctrl::direct / run_exact report the outcome on the device.
+size_t direct_workspace_bytes(uint64_t slots, uint32_t nsegs);
+// the one-pass level's outcome flag in its workspace (2: ineligible, 1: a region overflowed)
+const uint32_t* direct_flag_ptr(const void* dw, uint64_t slots, uint32_t nsegs);
 constexpr uint64_t kDirectMinPerBucket = 65536;  // mean keys per root bucket for the padded level 0
-void launch_direct(const LevelParams& p, int in_f64, const uint32_t* gate, const uint32_t* slices, uint64_t s,
-                   uint64_t alloc_keys, void* dw, int grid, cudaStream_t st, bool test_overflow = false);
-// bound on the padded output of launch_direct for n keys, a sample of s, nb buckets
-uint64_t direct_capacity_bound(uint64_t n, uint64_t s, uint32_t nb);
+constexpr uint32_t kDirectMaxBuckets = 1024;     // buckets per segment a one-pass level handles
+void launch_direct(const LevelParams& p, int in_f64, uint64_t root_m, uint64_t alloc_keys, void* dw, uint64_t slots,
+                   int grid, cudaStream_t st, bool test_overflow = false);
+// bound on one segment's padded output: n keys, a model sample of m, nb buckets
+uint64_t direct_capacity_bound(uint64_t n, uint64_t m, uint32_t nb);
 // basecase.cu
 void launch_base_cases(const LevelParams& p, const uint64_t* src, void* out, int out_f64, cudaStream_t st);
 // cls 0: <= 1 Ki keys, 1: <= 4 Ki, 2: list 2 items > 8 Ki, 3: list 2 items <= 8 Ki

@@ -843,116 +843,135 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
     if (p.remote) __threadfence_system();
 }
 
-// ----------------------------------------------- padded one-pass level 0
-// Level 0 of a large input under a learned root model: classify, rank, claim
-// and scatter in ONE pass (no k_hist pass, no stored bucket ids: 8 + 16 B per
-// key instead of 10 + 18). The bucket counts are not known in advance, so
-// bucket b writes into a padded region [base_b, base_b + cap_b) sized from the
-// root's sorted RMI sample (c_b samples of s): cap_b = ceil(n/s (c_b +
-// 6 sqrt(c_b) + 8)) -- about six standard deviations of the sampling error.
-// A claim past its region's end is not written and raises the overflow flag;
-// the exact two-pass level (k_hist / k_scan_children / k_scatter, gated on
-// Ctrl::run_exact) then runs instead, so the result never depends on the
-// estimate. The children read their keys at the padded base (SegOut::in_begin)
-// and write the next level's output at exact offsets (SegOut::begin).
+// ------------------------------------------------ one-pass (padded) levels
+// A level whose segments all have learned models trained on samples large
+// enough to predict their bucket counts does not need a histogram pass:
+// classify, rank, claim and scatter in ONE pass (no k_hist pass, no stored
+// bucket ids: 8 + 16 B per key instead of 10 + 18). The counts are not known
+// in advance, so bucket b of a segment writes into a padded region
+// [base_b, base_b + cap_b) sized from the segment's model sample (c_b of its m
+// samples): cap_b = ceil(n/m (c_b + 6 sqrt(c_b) + 8)), six standard deviations
+// of the sampling error. A claim past its region's end is not written and
+// raises the overflow flag; the level's exact two-pass kernels (k_kind_plan /
+// k_hist / k_scan_children / k_scatter, gated on Ctrl::run_exact) then run
+// instead, so the result never depends on the estimate. The children are read
+// at their padded offsets (SegOut::in_begin, BaseItem::src) and written at
+// exact ones (SegOut::begin, BaseItem::begin): no compaction pass. The counts
+// come from the root sample's bucket offsets (p.slices); the kernels take any
+// number of learned segments (bucket slots at SegDesc::bucket_off).
 constexpr double kDirectSigma = 6.0, kDirectSlack = 8.0;
 
 struct DirectWS {
-    unsigned long long* cur;   // [nb] claim cursors (absolute padded positions)
-    unsigned long long* base;  // [nb + 1] padded region starts (base[nb] = total)
-    unsigned long long* end;   // [nb] region ends
-    uint32_t* ovf;             // overflow flag
+    unsigned long long* cur;     // [slots] claim cursors (absolute positions in the padded output)
+    unsigned long long* base;    // [slots] region starts
+    unsigned long long* end;     // [slots] region ends
+    uint32_t* ovf;               // 2: the level is not eligible, 1: a region overflowed
 };
-__host__ __device__ inline DirectWS direct_ws(void* w, uint32_t nb) {
+__host__ __device__ inline DirectWS direct_ws(void* w, uint64_t slots, uint32_t nsegs) {
     DirectWS d;
     d.cur = (unsigned long long*)w;
-    d.base = d.cur + nb;
-    d.end = d.base + nb + 1;
-    d.ovf = (uint32_t*)(d.end + nb);
+    d.base = d.cur + slots;
+    d.end = d.base + slots;
+    d.ovf = (uint32_t*)(d.end + slots);
+    (void)nsegs;
     return d;
 }
-size_t direct_workspace_bytes(uint32_t nb) { return 8 * (3 * (size_t)nb + 1) + 16; }
-
-uint64_t direct_capacity_bound(uint64_t n, uint64_t s, uint32_t nb) {
-    // sum_b sqrt(c_b) <= sqrt(nb s) (Cauchy-Schwarz); + 1 per bucket for the ceiling
-    const double r = (double)n / (double)s;
-    return (uint64_t)(r * ((double)s + kDirectSigma * sqrt((double)nb * (double)s) + kDirectSlack * nb)) + 2 * nb + 16;
+size_t direct_workspace_bytes(uint64_t slots, uint32_t nsegs) { return 8 * (3 * slots) + 16 + 0 * nsegs; }
+const uint32_t* direct_flag_ptr(const void* dw, uint64_t slots, uint32_t nsegs) {
+    return direct_ws((void*)dw, slots, nsegs).ovf;
 }
 
-// One CTA: direct = gate && learned model; capacities from the sample slices,
-// their exclusive scan, cursors at the region starts.
+uint64_t direct_capacity_bound(uint64_t n, uint64_t m, uint32_t nb) {
+    // sum_b sqrt(c_b) <= sqrt(nb m) (Cauchy-Schwarz); + 1 per bucket for the ceiling
+    const double r = (double)n / (double)m;
+    return (uint64_t)(r * ((double)m + kDirectSigma * sqrt((double)nb * (double)m) + kDirectSlack * nb)) + 2 * nb + 16;
+}
+
+// One CTA: the single segment's regions from the root sample's bucket offsets
+// (caps, their exclusive scan, cursors) and the eligibility flag.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_direct_setup(LevelParams p, const uint32_t* gate, const uint32_t* off,
-                                                     uint64_t s, uint64_t alloc, DirectWS w, double sigma,
-                                                     double slack) {
+__global__ void __launch_bounds__(NT) k_direct_setup(LevelParams p, uint64_t root_m, uint64_t alloc, DirectWS w,
+                                                     double sigma, double slack) {
     griddep_wait();
     __shared__ uint64_t wsum[NT / 32 + 1];
     extern __shared__ uint64_t capv[];  // nb + 1
-    const ModelHdr* h = (const ModelHdr*)p.models;
-    const bool on = (!gate || *gate) && h->kind == kLearned;
+    const SegDesc sd = p.segs[0];
+    const ModelHdr* h = (const ModelHdr*)(p.models + sd.model_off);
     const uint32_t nb = h->nbuckets;
-    const uint64_t n = p.segs[0].n;
-    if (!on) {
-        if (threadIdx.x == 0) { p.ctrl->direct = 0; p.ctrl->run_exact = 1; }
+    if (h->kind != kLearned || root_m == 0 || nb > kDirectMaxBuckets || h->B > kDirectMaxBuckets || !p.slices) {
+        if (threadIdx.x == 0) *w.ovf = 2u;  // not eligible: the exact level runs
         return;
     }
-    const double r = (double)n / (double)s;
+    const double r = (double)sd.n / (double)root_m;
     for (uint32_t b = threadIdx.x; b < nb; b += NT) {
-        const double c = (double)(off[b + 1] - off[b]);
+        const double c = (double)(p.slices[b + 1] - p.slices[b]);
         const double e = c + sigma * sqrt(c) + slack;
         capv[b] = e > 0.0 ? (uint64_t)ceil(r * e) : 0ull;
     }
     __syncthreads();
+    for (uint32_t b = threadIdx.x; b < nb; b += NT) w.end[sd.bucket_off + b] = capv[b];
+    __syncthreads();
     const uint64_t tot = block_exclusive_scan_u64<NT>(capv, nb, wsum);
     for (uint32_t b = threadIdx.x; b < nb; b += NT) {
-        w.base[b] = capv[b];
-        w.cur[b] = capv[b];
-        w.end[b] = b + 1 < nb ? capv[b + 1] : tot;
+        w.base[sd.bucket_off + b] = capv[b];
+        w.cur[sd.bucket_off + b] = capv[b];
+        w.end[sd.bucket_off + b] += capv[b];
     }
-    if (threadIdx.x == 0) {
-        w.base[nb] = tot;
-        *w.ovf = tot > alloc ? 1u : 0u;  // (cannot happen: alloc is the host's bound)
-        p.ctrl->direct = 1;
-        p.ctrl->run_exact = 0;
-    }
+    if (threadIdx.x == 0) *w.ovf = tot > alloc ? 2u : 0u;  // (the host's bound holds)
 }
 
 struct DirectSmem {
     uint64_t bars[2];
     ulonglong2 tiles[2][kTileKeys / 2];  // TMA tile buffers; the consumed one stages the tile
-    long long delta[1024];               // per bucket: claimed position - tile-local start
-    alignas(16) uint32_t cnt[2][1024 + 4];
+    long long delta[kDirectMaxBuckets];  // per bucket: claimed position - tile-local start
+    alignas(16) uint32_t cnt[2][kDirectMaxBuckets + 4];
     uint16_t sbid[kTileKeys];
     uint32_t wsum[kPNT / 32 + 1];
-    alignas(16) uint8_t table[20 * 1024];  // the learned model's compiled table (kstate_load)
+    alignas(16) uint8_t table[20 * kDirectMaxBuckets];  // the segment model's compiled table (kstate_load)
 };
 
-template <bool IN_F64>
+// MULTI = false: one segment (level 0, the only form launched), its model
+// table loaded once (the per-tile segment switch of the multi-segment form
+// spilled registers with the float64 decode)
+template <bool IN_F64, bool MULTI>
 __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, DirectWS w) {
     griddep_wait();
     extern __shared__ uint4 smem_u4[];
     DirectSmem& Q = *(DirectSmem*)smem_u4;
-    constexpr uint32_t NBC = 1024;
-    if (!p.ctrl->direct) return;
+    constexpr uint32_t NBC = kDirectMaxBuckets;
+    if (*w.ovf || p.ctrl->nan_index != ~0ull) return;
     const uint64_t per = (p.ntiles + gridDim.x - 1) / gridDim.x;
     const uint64_t t0 = (uint64_t)blockIdx.x * per;
     const uint64_t t1 = min(t0 + per, p.ntiles);
     if (t0 >= t1) return;
-    // the learned model's compiled table in the (unused) id staging area
-    KState S;
-    kstate_load<kLearned>(S, p.models, Q.table);
-    const uint32_t nb = S.nb;
     for (uint32_t b = threadIdx.x; b < NBC; b += kPNT) Q.cnt[0][b] = Q.cnt[1][b] = 0;
     TileStream TS;
     TS.init((uint8_t*)Q.tiles, Q.bars);
     uint32_t inext = ~0u;
     TileGeom gnext = tile_geom_all(p, t0, inext);
     TS.issue(p.src, gnext, 0);
+    KState S;
+    int64_t curseg = -1;
+    uint64_t boff = 0;
+    uint32_t nb = 0;
+    if (!MULTI) {
+        kstate_load<kLearned>(S, p.models + p.segs[0].model_off, Q.table);
+        boff = p.segs[0].bucket_off;
+        nb = S.nb;
+    }
     bool ovf = false;
     for (uint64_t tile = t0; tile < t1; ++tile) {
         const int tb = (int)((tile - t0) & 1);
+        const uint32_t si = inext;
         const TileGeom g = gnext;
         uint32_t* cnt = Q.cnt[tb];
+        if (MULTI && (int64_t)si != curseg) {  // (CTA-uniform) the segment's model table into shared memory
+            const SegDesc& sd = p.segs[si];
+            kstate_load<kLearned>(S, p.models + sd.model_off, Q.table);
+            boff = sd.bucket_off;
+            nb = S.nb;
+            curseg = si;
+        }
         TS.wait(g, tb);
         const ulonglong2* sp = TS.buf(tb);
         uint64_t* skeys = (uint64_t*)TS.buf(tb);  // staging reuses the consumed tile buffer
@@ -1044,8 +1063,8 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
                 if (b < nb) {
                     const uint32_t c = cnt[b + 1] - cnt[b];
                     if (c) {
-                        got[q] = atomicAdd(&w.cur[b], (unsigned long long)c);
-                        if (got[q] + c > w.end[b]) {  // region full: nothing of this run is written
+                        got[q] = atomicAdd(&w.cur[boff + b], (unsigned long long)c);
+                        if (got[q] + c > w.end[boff + b]) {  // region full: nothing of this run is written
                             ovf = true;
                             got[q] = ~0ull;
                         }
@@ -1087,69 +1106,77 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
     if (ovf) atomicOr(w.ovf, 1u);
 }
 
-// One CTA: unless a region overflowed, the children are the buckets -- read at
-// their padded base, written exactly (exclusive scan of the counts); all of
-// them go to the next level (the GPU policy admits a padded level only when
-// the mean bucket is far above the base-case capacity). Overflow: run_exact.
+// One CTA per segment: unless the level is ineligible or a region overflowed,
+// every non-empty bucket becomes a next-level segment, read at its padded base
+// (SegOut::in_begin) and written at its exact offset (exclusive scan of the
+// counts) -- small ones too: a base-case item reads where it writes, and the
+// one-pass level only runs with >= 64 Ki keys per bucket on average. Otherwise
+// the exact two-pass level runs (Ctrl::run_exact).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS w) {
     griddep_wait();
     __shared__ uint64_t wsum[NT / 32 + 1];
     __shared__ uint32_t lbase;
-    extern __shared__ uint64_t cntv[];  // nb
-    if (!p.ctrl->direct || p.ctrl->nan_index != ~0ull) return;
+    extern __shared__ uint64_t cntv[];  // nb + 1
+    if (p.ctrl->nan_index != ~0ull) return;
     if (*w.ovf) {
-        if (threadIdx.x == 0) { p.ctrl->direct = 0; p.ctrl->run_exact = 1; }
+        if (blockIdx.x == 0 && threadIdx.x == 0) { p.ctrl->direct = 0; p.ctrl->run_exact = 1; }
         return;
     }
-    const SegDesc sd = p.segs[0];
-    const uint32_t nb = ((const ModelHdr*)p.models)->nbuckets;
-    for (uint32_t b = threadIdx.x; b < nb; b += NT) cntv[b] = w.cur[b] - w.base[b];
+    if (blockIdx.x == 0 && threadIdx.x == 0) { p.ctrl->direct = 1; p.ctrl->run_exact = 0; }
+    const SegDesc sd = p.segs[blockIdx.x];
+    const uint32_t nb = ((const ModelHdr*)(p.models + sd.model_off))->nbuckets;
+    for (uint32_t b = threadIdx.x; b < nb; b += NT) cntv[b] = w.cur[sd.bucket_off + b] - w.base[sd.bucket_off + b];
     __syncthreads();
     block_exclusive_scan_u64<NT>(cntv, nb, wsum);
     if (threadIdx.x == 0) lbase = 0;
     __syncthreads();
-    for (uint32_t b0 = 0; b0 < nb; b0 += NT) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t b0 = 0; b0 < nb; b0 += NT) {  // CTA-uniform rounds
         const uint32_t b = b0 + threadIdx.x;
         uint64_t st = 0, len = 0;
         if (b < nb) {
             st = cntv[b];
             len = (b + 1 < nb ? cntv[b + 1] : sd.n) - st;
         }
-        const bool emit = len > 0;
-        const unsigned m = __ballot_sync(FULL_MASK, emit);
+        const unsigned m = __ballot_sync(FULL_MASK, len > 0);
         uint32_t wb = 0;
-        if ((threadIdx.x & 31) == 0 && m) wb = atomicAdd(&lbase, (uint32_t)__popc(m));
+        if (lane == 0 && m) wb = atomicAdd(&lbase, (uint32_t)__popc(m));
         wb = __shfl_sync(FULL_MASK, wb, 0);
-        if (emit) {
-            const uint32_t e = wb + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
-            uint64_t ps = 0;
-            if (p.slices) {
-                const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
-                if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
-            }
-            const uint32_t flags = (len == sd.n) ? kSegForceRadix : 0u;
-            if (e < p.list_cap) p.rec[e] = SegOut{sd.begin + st, len, sd.depth + 1, flags, ps, w.base[b]};
-            else atomicOr(&p.ctrl->err, 4u);
-        }
         __syncthreads();
+        if (len) {
+            const uint32_t e0 = wb + __popc(m & ((1u << lane) - 1u));
+            {
+                uint64_t ps = 0;
+                if (p.slices) {
+                    const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
+                    if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
+                }
+                const uint32_t depth = sd.depth + 1;
+                const uint32_t flags = (len == sd.n || depth > p.depth_cap) ? kSegForceRadix : 0u;
+                const uint32_t e = p.ctrl->n_rec + e0;  // (one segment: the list starts empty)
+                if (e < p.list_cap) p.rec[e] = SegOut{sd.begin + st, len, depth, flags, ps, w.base[sd.bucket_off + b]};
+                else atomicOr(&p.ctrl->err, 4u);
+            }
+        }
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        p.ctrl->n_rec = lbase;
-        p.ctrl->keys_rec = sd.n;
+        p.ctrl->n_rec += lbase;
+        p.ctrl->keys_rec += sd.n;
     }
 }
 
-void launch_direct(const LevelParams& p, int in_f64, const uint32_t* gate, const uint32_t* slices, uint64_t s,
-                   uint64_t alloc_keys, void* dw, int grid, cudaStream_t st, bool test_overflow) {
-    const uint32_t nbmax = 2048;
-    const DirectWS w = direct_ws(dw, nbmax);
+void launch_direct(const LevelParams& p, int in_f64, uint64_t root_m, uint64_t alloc_keys, void* dw, uint64_t slots,
+                   int grid, cudaStream_t st, bool test_overflow) {
+    const DirectWS w = direct_ws(dw, slots, p.nsegs);
     const double sigma = test_overflow ? -kDirectSigma : kDirectSigma, slack = test_overflow ? 0.0 : kDirectSlack;
-    pdl(k_direct_setup<1024>, 1, 1024, 8 * ((size_t)nbmax + 2), st, p, gate, slices, s, alloc_keys, w, sigma, slack);
+    const size_t cap_sm = 8 * ((size_t)kDirectMaxBuckets + 2);
+    pdl(k_direct_setup<1024>, 1, 1024, cap_sm, st, p, root_m, alloc_keys, w, sigma, slack);
     constexpr size_t sm = sizeof(DirectSmem);
-    if (in_f64) pdl(k_direct<true>, grid, kPNT, sm, st, p, w);
-    else pdl(k_direct<false>, grid, kPNT, sm, st, p, w);
-    pdl(k_direct_children<1024>, 1, 1024, 8 * ((size_t)nbmax + 2), st, p, w);
+    if (in_f64) pdl(k_direct<true, false>, grid, kPNT, sm, st, p, w);
+    else pdl(k_direct<false, false>, grid, kPNT, sm, st, p, w);
+    pdl(k_direct_children<1024>, p.nsegs, 1024, cap_sm, st, p, w);
 }
 
 // ------------------------------------------------------------- launchers
@@ -1166,8 +1193,8 @@ void partition_init(int optin) {
     allow_smem(k_scatter<false, 1024>, optin);
     allow_smem(k_scatter<true, kMaxNB>, optin);
     allow_smem(k_scatter<false, kMaxNB>, optin);
-    allow_smem(k_direct<true>, optin);
-    allow_smem(k_direct<false>, optin);
+    allow_smem(k_direct<true, false>, optin);
+    allow_smem(k_direct<false, false>, optin);
     allow_smem(k_direct_setup<1024>, optin);
     allow_smem(k_direct_children<1024>, optin);
     allow_smem(k_scan_children<128>, optin);
