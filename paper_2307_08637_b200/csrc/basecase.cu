@@ -113,7 +113,10 @@ __global__ void __launch_bounds__(NT, MINB) k_base_reg(const BaseItem* items, co
             const BaseItem nx = items[e + gridDim.x];
             if (nx.n > nmin && nx.n <= nmax) l2_prefetch(src + nx.begin, 8 * nx.n);
         }
+        // register array of 1/2, 3/4 or all of CAP / NT keys per thread: every
+        // unused slot still issues its predicated loads, digit, rank and placement
         if (n <= (uint32_t)CAP / 2) base_reg_one<SS::ITEMS / 2, SS, OUT_F64>(g, n, S, out, it.begin);
+        else if (n <= (uint32_t)CAP / 4 * 3) base_reg_one<SS::ITEMS / 4 * 3, SS, OUT_F64>(g, n, S, out, it.begin);
         else base_reg_one<SS::ITEMS, SS, OUT_F64>(g, n, S, out, it.begin);
         // no barrier: the next segment writes shared memory (hist, reduction
         // words) that the output loop does not read, and S.B only after its

@@ -85,6 +85,7 @@ struct LsortError {
 constexpr uint64_t kAutoClusterKeys = 4ull << 20;
 constexpr uint32_t kBigRootBuckets = 512;
 constexpr uint64_t kBigRootMinKeys = 32ull << 20;
+constexpr uint64_t kRootSampleMin = 256ull << 10;
 
 inline uint32_t fanout(uint64_t n, uint32_t cfg_count, uint32_t target) {
     if (target == 0) return cfg_count;
@@ -242,6 +243,16 @@ struct Engine {
     uint32_t classic_B = 0;
 
     uint32_t rmi_b(uint64_t n) const { return fanout(n, cfg.rmi_bucket_count, cfg.bucket_target); }
+    // RMI sample of a root segment. GPU policy: min(SPEC size, max(256 Ki, n / 512))
+    // -- ~2 Ki samples per level-1 segment of a 512-way root still train the
+    // children's models (they take slices of this sample); a 1e8-key root sorted
+    // its 1 Mi sample for nothing (Normal 1e8: models 0.45 -> 0.29 ms, base
+    // unchanged; C5 keeps ~1 Mi). Sorted output is the same.
+    uint64_t root_rmi_sample(uint64_t n) const {
+        const uint64_t s = sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
+        if (cfg.flags & LSORT_FLAG_STRICT_POLICY) return s;
+        return std::min<uint64_t>(s, std::max<uint64_t>(kRootSampleMin, n >> 9));
+    }
     uint32_t tree_k(uint64_t n) const { return fanout(n, cfg.tree_bucket_count, cfg.bucket_target); }
     // largest sample the segment's model may need (the RMI sample only if the
     // policy can pick the learned branch)
@@ -410,7 +421,9 @@ struct Engine {
         const uint64_t n = sp.n;
         const uint32_t sub = (sp.depth == 0 && root_sub) ? root_sub : hseg.rmi_b;  // RMI submodels
         const uint64_t s1 = sample_size_host(cfg.sample_fraction, cfg.first_sample_cap, n);
-        const uint64_t s2 = given_sample ? given_n : sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
+        const uint64_t s2 = given_sample ? given_n
+                            : sp.depth == 0 ? root_rmi_sample(n)
+                                            : sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
         // sample-sort splitter budget: ~2 Ki samples per bucket (base-case class <= 4 Ki)
         uint32_t k = cfg.tree_bucket_count;
         while (k < LSORT_MAX_TREE_DEV && (uint64_t)k * 2048 < s2) k <<= 1;
@@ -780,7 +793,7 @@ struct Engine {
             uint64_t* dout = nullptr;
             uint64_t root_m = 0, alloc = 0;
             if (direct0) {
-                root_m = sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
+                root_m = root_rmi_sample(n);
                 alloc = direct_capacity_bound(n, root_m, hs[0].nb_max);
                 // (level 1 reads this padded output: its bucket ids are indexed by read position)
                 if (!C->scratch2.ensure(8 * alloc) || !C->ids.ensure(2 * alloc))

@@ -1,0 +1,5 @@
+set -x
+LSORT_TRACE=1 python tools/profile_sort.py lognormal2 500000000 2 > gpurun_out/s2_trace_c5.log 2>&1
+LSORT_TRACE=1 python tools/profile_sort.py normal 100000000 2 > gpurun_out/s2_trace_normal.log 2>&1
+timeout 1200 ncu --set full --import-source on --clock-control none -k 'regex:k_(direct|scatter|hist|base_reg|base_smem)' -c 24 -o gpurun_out/s2_c5_full python tools/profile_sort.py lognormal2 500000000 1 > gpurun_out/s2_ncu_full.log 2>&1
+ls -la gpurun_out
