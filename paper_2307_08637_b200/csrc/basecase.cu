@@ -208,7 +208,7 @@ static void reg_init(int optin) {
 void basecase_init(int optin) {
     allow_smem(k_base_smem<128, 1024, 1024, true>, optin);
     allow_smem(k_base_smem<128, 1024, 1024, false>, optin);
-    reg_init<256, 4096, 4096, 3>(optin);
+    reg_init<256, 4096, 4096, 4>(optin);
     reg_init<512, 8192, 4096, 2>(optin);
     reg_init<1024, 16384, 8192, 1>(optin);
     allow_smem(k_small_sort<true>, optin);
@@ -242,7 +242,7 @@ void launch_base_class(const LevelParams& p, int cls, const uint64_t* src, void*
         if (out_f64) pdl(k_base_smem<128, 1024, 1024, true>, nsm * 8, 128, sm, st, p.base[0], cnt, src, out, p.ctrl, p.list_cap);
         else pdl(k_base_smem<128, 1024, 1024, false>, nsm * 8, 128, sm, st, p.base[0], cnt, src, out, p.ctrl, p.list_cap);
     } else if (cls == 1) {
-        launch_reg<256, 4096, 4096, 3>(p, 1, src, out, out_f64, st, 0, 4096);
+        launch_reg<256, 4096, 4096, 4>(p, 1, src, out, out_f64, st, 0, 4096);
     } else if (cls == 2) {
         launch_reg<1024, 16384, 8192, 1>(p, 2, src, out, out_f64, st, 8192, 16384);
     } else {

@@ -18,7 +18,7 @@ struct SmemSort {
     static constexpr int kSmall = 16;
     static constexpr int kMedium = 256;
     static constexpr int kStk = CAP / (kSmall + 1) + 2;
-    static_assert(CAP <= 65536, "16-bit ranks");
+    static_assert(CAP < 65536, "16-bit offsets, lengths and ranks");
     struct Smem {
         uint64_t A[CAP + 4];  // logical key i at A[mis + i]
         uint64_t B[CAP];
@@ -27,7 +27,7 @@ struct SmemSort {
         uint32_t wsum[NT / 32 + 1];
         uint64_t red[2 * (NT / 32)];
         uint32_t n_med, n_large, n_l4, n_l16;
-        uint32_t med_off[kStk], med_len[kStk], large_off[kStk], large_len[kStk];
+        uint16_t med_off[kStk], med_len[kStk], large_off[kStk], large_len[kStk];
         uint64_t mbar;
     };
     // the same without the input array A (keys arrive in registers; scratch
@@ -35,23 +35,23 @@ struct SmemSort {
     struct SmemR {
         uint64_t B[CAP];
         uint32_t hist[NBMAX + 1];
-        uint16_t R[CAP];
+        uint16_t R[CAP / 2];  // collision-digit lists only (<= n / 2 digits hold >= 2 keys)
         uint32_t wsum[NT / 32 + 1];
         uint64_t red[2 * (NT / 32)];
         uint32_t n_med, n_large, n_l4, n_l16;
-        uint32_t med_off[kStk], med_len[kStk], large_off[kStk], large_len[kStk];
+        uint16_t med_off[kStk], med_len[kStk], large_off[kStk], large_len[kStk];
     };
 
     template <class SM>
     __device__ static __forceinline__ void push(SM& S, uint32_t at, uint32_t l) {
         if (l <= (uint32_t)kMedium) {
             uint32_t q = atomicAdd(&S.n_med, 1u);
-            S.med_off[q] = at;
-            S.med_len[q] = l;
+            S.med_off[q] = (uint16_t)at;
+            S.med_len[q] = (uint16_t)l;
         } else {
             uint32_t q = atomicAdd(&S.n_large, 1u);
-            S.large_off[q] = at;
-            S.large_len[q] = l;
+            S.large_off[q] = (uint16_t)at;
+            S.large_len[q] = (uint16_t)l;
         }
     }
 
@@ -89,8 +89,7 @@ struct SmemSort {
         const uint32_t shift = bits > lgnb ? bits - lgnb : 0;
         for (uint32_t d = tid; d < nb; d += NT) S.hist[d] = 0;
         __syncthreads();
-        for (uint32_t i = tid; i < len; i += NT)
-            S.R[off + i] = (uint16_t)atomicAdd(&S.hist[(uint32_t)((a[off + i] - mn) >> shift)], 1u);
+        for (uint32_t i = tid; i < len; i += NT) atomicAdd(&S.hist[(uint32_t)((a[off + i] - mn) >> shift)], 1u);
         __syncthreads();
         {  // exclusive scan with big-digit detection
             const uint32_t per = (nb + NT - 1) / NT;
@@ -112,18 +111,20 @@ struct SmemSort {
                 if (t > (uint32_t)kSmall) push(S, off + run, t);
                 run += t;
             }
-            if (tid == 0) S.hist[nb] = len;
         }
         __syncthreads();
+        // placement by atomic cursors (order inside a digit is arbitrary: the
+        // fix-up below ranks each key among its digit); afterwards hist[d] holds
+        // the END of digit d, i.e. the start of digit d + 1
         for (uint32_t i = tid; i < len; i += NT) {
             const uint64_t k = a[off + i];
-            b[off + S.hist[(uint32_t)((k - mn) >> shift)] + S.R[off + i]] = k;
+            b[off + atomicAdd(&S.hist[(uint32_t)((k - mn) >> shift)], 1u)] = k;
         }
         __syncthreads();
         for (uint32_t j = tid; j < len; j += NT) {
             const uint64_t k = b[off + j];
             const uint32_t d = (uint32_t)((k - mn) >> shift);
-            const uint32_t s0 = S.hist[d], c = S.hist[d + 1] - s0;
+            const uint32_t s0 = d ? S.hist[d - 1] : 0u, c = S.hist[d] - s0;
             uint32_t p = j;
             if (c <= (uint32_t)kSmall) {
                 p = s0;
@@ -410,6 +411,7 @@ struct SmemSort {
         // knows where its collision digits go in the two lists (S.R front /
         // back) without atomics or a second pass over the digits
         uint32_t n4, n16;
+        constexpr uint32_t kR = sizeof(S.R) / sizeof(S.R[0]);  // list capacity (front: 2..4 keys, back: 5..kSmall)
         {
             static_assert(CAP < 65536, "packed 16-bit scan fields");
             const uint32_t per = (nb + NT - 1) / NT;
@@ -451,7 +453,7 @@ struct SmemSort {
             auto place = [&](uint32_t d, uint32_t h, uint32_t at) {
                 if (h < 2) return;  // the common case: empty / single-key digit
                 if (h <= 4) S.R[p4++] = (uint16_t)d;  // digit index (< NBMAX <= 65536)
-                else if (h <= (uint32_t)kSmall) S.R[CAP - 1 - (p16++)] = (uint16_t)d;
+                else if (h <= (uint32_t)kSmall) S.R[kR - 1 - (p16++)] = (uint16_t)d;
                 else push(S, at, h);
             };
             if (per % 4 == 0) {
@@ -500,7 +502,7 @@ struct SmemSort {
             if (c == 4) B[s0 + 3] = x3;
         }
         for (uint32_t e = tid; e < n16; e += NT) {
-            const uint32_t d = S.R[CAP - 1 - e], s0 = S.hist[d], c = S.hist[d + 1] - s0;
+            const uint32_t d = S.R[kR - 1 - e], s0 = S.hist[d], c = S.hist[d + 1] - s0;
             for (uint32_t t = s0 + 1; t < s0 + c; ++t) {
                 const uint64_t x = B[t];
                 uint32_t u = t;
