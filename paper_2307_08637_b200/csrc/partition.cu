@@ -794,21 +794,18 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
         else *(uint4*)&cnt[bb] = make_uint4(st[0], st[1], st[2], st[3]);
         if (threadIdx.x == 0) cnt[NBC] = total;
         __syncthreads();  // (3) tile-local bucket starts visible
-        {  // claims strided over the threads (bucket t, t + kPNT, ...): all atomics in flight
-            unsigned long long got[kPer];
+        // claims strided over the threads (bucket t, t + kPNT, ...): all atomics in
+        // flight while this thread stages its keys; consumed after the staging
+        unsigned long long got[kPer];
+        uint32_t cstart[kPer];
 #pragma unroll
-            for (int q = 0; q < kPer; ++q) {
-                const uint32_t b = threadIdx.x + q * kPNT;
-                got[q] = 0;
-                if (b < nbo) {
-                    const uint32_t c = cnt[b + 1] - cnt[b];
-                    if (c) got[q] = atomicAdd(&p.buckets[boff + b], (unsigned long long)c);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < kPer; ++q) {
-                const uint32_t b = threadIdx.x + q * kPNT;
-                Q.delta[b] = (long long)got[q] - (long long)cnt[b];
+        for (int q = 0; q < kPer; ++q) {
+            const uint32_t b = threadIdx.x + q * kPNT;
+            got[q] = 0;
+            cstart[q] = cnt[b];
+            if (b < nbo) {
+                const uint32_t c = cnt[b + 1] - cstart[q];
+                if (c) got[q] = atomicAdd(&p.buckets[boff + b], (unsigned long long)c);
             }
         }
 #pragma unroll
@@ -825,6 +822,8 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
             skeys[pos] = skey;
             Q.sbid[pos] = (uint16_t)(scode >> 16);
         }
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) Q.delta[threadIdx.x + q * kPNT] = (long long)got[q] - (long long)cstart[q];
         __syncthreads();  // (4)
 #pragma unroll
         for (int q = 0; q < kTileKeys / kPNT; ++q) {  // unrolled: loads of all rows in flight
@@ -1054,27 +1053,23 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
         *(uint2*)&cnt[bb] = make_uint2(run, run + cn0);
         if (threadIdx.x == 0) cnt[NBC] = total;
         __syncthreads();  // (3) tile-local bucket starts visible
-        {
-            unsigned long long got[kPer];
+        // claims (all in flight while this thread stages its keys), the region
+        // ends loaded beside them; both consumed after the staging
+        unsigned long long got[kPer], lim[kPer];
+        uint32_t cstart[kPer], ccnt[kPer];
 #pragma unroll
-            for (int q = 0; q < kPer; ++q) {
-                const uint32_t b = threadIdx.x + q * kPNT;
-                got[q] = 0;
-                if (b < nb) {
-                    const uint32_t c = cnt[b + 1] - cnt[b];
-                    if (c) {
-                        got[q] = atomicAdd(&w.cur[boff + b], (unsigned long long)c);
-                        if (got[q] + c > w.end[boff + b]) {  // region full: nothing of this run is written
-                            ovf = true;
-                            got[q] = ~0ull;
-                        }
-                    }
+        for (int q = 0; q < kPer; ++q) {
+            const uint32_t b = threadIdx.x + q * kPNT;
+            got[q] = 0;
+            lim[q] = ~0ull;
+            cstart[q] = cnt[b];
+            ccnt[q] = 0;
+            if (b < nb) {
+                ccnt[q] = cnt[b + 1] - cstart[q];
+                if (ccnt[q]) {
+                    got[q] = atomicAdd(&w.cur[boff + b], (unsigned long long)ccnt[q]);
+                    lim[q] = w.end[boff + b];
                 }
-            }
-#pragma unroll
-            for (int q = 0; q < kPer; ++q) {
-                const uint32_t b = threadIdx.x + q * kPNT;
-                Q.delta[b] = got[q] == ~0ull ? LLONG_MIN : (long long)got[q] - (long long)cnt[b];
             }
         }
 #pragma unroll
@@ -1090,6 +1085,12 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
             const uint32_t pos = cnt[scode >> 16] + (scode & 0xffffu);
             skeys[pos] = skey;
             Q.sbid[pos] = (uint16_t)(scode >> 16);
+        }
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const bool full = ccnt[q] && got[q] + ccnt[q] > lim[q];  // region full: nothing of this run is written
+            ovf |= full;
+            Q.delta[threadIdx.x + q * kPNT] = full ? LLONG_MIN : (long long)got[q] - (long long)cstart[q];
         }
         __syncthreads();  // (4)
 #pragma unroll
