@@ -202,6 +202,8 @@ inline DevCfg dev_cfg(const lsort_cfg& c) {
     d.seed = c.seed;
     d.quality = (c.flags & LSORT_FLAG_STRICT_POLICY) ? 0u : 1u;
     d.psample = nullptr;
+    static const bool no_lut = getenv("LSORT_NO_LUT") != nullptr;
+    d.lut = d.quality && !no_lut;
     return d;
 }
 
@@ -692,7 +694,7 @@ struct Engine {
                 else if (mc == 1) mids.push_back(j);
                 else hi[nsmall++] = j;
                 if (s.flags & kSegForceRadix) kinds |= 4u;
-                else kinds |= (s.n >= effective_min_rmi(cfg) ? 1u : 0u) | 2u;
+                else kinds |= (s.n >= effective_min_rmi(cfg) ? (s.depth >= 1 && dev_cfg(cfg).lut ? 5u : 1u) : 0u) | 2u;
             }
             const uint32_t np = (uint32_t)psegs.size();
             const uint32_t ncl = (uint32_t)clus.size();

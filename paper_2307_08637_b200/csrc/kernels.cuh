@@ -101,6 +101,8 @@ struct DevCfg {
                        // sample into one bucket is replaced by a splitter tree over that sample
     const uint64_t* psample;  // GPU policy: the parent level's sorted sample (children's
                               // models train on their slice of it instead of drawing)
+    uint32_t lut;             // GPU policy: learned-eligible segments below the root get a
+                              // cell-table model (kModelLut) instead of an RMI
 };
 constexpr uint32_t kMinSlice = 64;  // shorter slices: draw a fresh sample
 constexpr uint32_t kPoorShare = 16;

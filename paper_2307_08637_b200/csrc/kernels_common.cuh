@@ -37,6 +37,7 @@ __device__ __forceinline__ uint64_t rmi_sample_size(const DevCfg& c, uint64_t n)
 __device__ __forceinline__ uint32_t model_payload_bytes(const ModelHdr& h) {
     if (h.kind == kLearned) return kLearnedEntryBytes * h.B;
     if (h.kind == kTree) return (uint32_t)((tree_payload_bytes(h.leaf_origin, h.nsplit) + 15) & ~15ull);
+    if (h.kind == kRadix && (h.flags & kModelLut)) return (2 * h.B + 15) & ~15u;
     return 0;
 }
 
@@ -72,7 +73,7 @@ __device__ __forceinline__ MView model_view(const uint8_t* s) {
 // Generic classifier over a model copied to shared memory (unit-test and
 // multi-GPU paths; the hot partition kernels use per-kind specialisations).
 struct Classifier {
-    uint32_t kind, nb, B, levels, leaf_origin, nsplit, shift;
+    uint32_t kind, nb, B, levels, leaf_origin, nsplit, shift, flags;
     double rs, ri, base, scale, cdf_lo, inv_span;
     uint64_t rmin;
     MView m;
@@ -80,7 +81,7 @@ struct Classifier {
         m = model_view(s);
         const ModelHdr& h = *m.h;
         kind = h.kind; nb = h.nbuckets; B = h.B; levels = h.levels; leaf_origin = h.leaf_origin;
-        nsplit = h.nsplit; shift = h.shift; rs = h.root_slope; ri = h.root_icpt; base = h.key_base;
+        nsplit = h.nsplit; shift = h.shift; flags = h.flags; rs = h.root_slope; ri = h.root_icpt; base = h.key_base;
         scale = h.key_scale; cdf_lo = h.cdf_lo; inv_span = h.inv_span; rmin = h.radix_min;
     }
     template <uint32_t KIND>
@@ -93,6 +94,7 @@ struct Classifier {
         } else if constexpr (KIND == kTree) {
             return tree_bucket(levels, leaf_origin, nsplit, m.tree, m.spl, m.eqo, x);
         } else if constexpr (KIND == kRadix) {
+            if (flags & kModelLut) return ((const uint16_t*)(m.h + 1))[lut_cell(x, rmin, shift, B)];
             uint64_t d = (x - rmin) >> shift;
             return d >= nb ? nb - 1 : (uint32_t)d;
         } else {

@@ -78,6 +78,22 @@ struct RmiBucketEntry {
 };
 constexpr uint32_t kLearnedEntryBytes = sizeof(RmiEntry) + sizeof(RmiBucketEntry);  // 64
 constexpr uint32_t kModelIdentityCdf = 1u;  // ModelHdr.flags: cdf_lo == 0 and inv_span == 1
+// Cell-table partition model (GPU policy for learned-eligible segments below the
+// root, see models.cu build_lut_block): kind kRadix with flags & kModelLut,
+// radix_min = origin of the cells, shift = log2 cell width, B = cells; payload
+// uint16 lut[B], the bucket of every key of cell c. Monotone: buckets are unions
+// of consecutive cells. Classifies with one table read instead of an RMI.
+constexpr uint32_t kModelLut = 2u;
+constexpr uint32_t kLutModelMaxCells = 8192;
+constexpr uint32_t kLutModelCellsPerBucket = 32;
+__host__ __device__ __forceinline__ uint32_t lut_model_cells(uint32_t nb) {
+    const uint32_t c = nb * kLutModelCellsPerBucket;
+    return c < kLutModelMaxCells ? c : kLutModelMaxCells;
+}
+__device__ __forceinline__ uint32_t lut_cell(uint64_t x, uint64_t origin, uint32_t shift, uint32_t ncell) {
+    const uint64_t c = (x > origin ? x - origin : 0ull) >> shift;
+    return c < ncell ? (uint32_t)c : ncell - 1;
+}
 
 // Partition-model record, 128 bytes; payload follows in the model arena:
 //   learned: RmiEntry[B]

@@ -376,6 +376,46 @@ struct ModelCfg {
 using ModelSmall = ModelCfg<256, 2048>;
 using ModelMid = ModelCfg<512, 8192>;
 
+// Cell-table model (kModelLut, GPU policy) over the sorted sample A[0, s): cells of
+// 2^shift keys from A[0], and cell c's bucket = floor(r_c * nb / s) with r_c the
+// number of samples below the cell's start -- the sample's empirical CDF read at
+// the cell starts (monotone; buckets are unions of cells). Cells
+// (cell(A[i-1]), cell(A[i])] all have r = i, so thread i fills them: O(cells + s).
+// Returns the largest bucket count of the sample itself (the quality check).
+// hist: >= nb words of scratch.
+template <int NT>
+__device__ uint64_t build_lut_block(const uint64_t* A, uint32_t s, uint32_t nb, ModelHdr* h, uint8_t* payload,
+                                    uint32_t* hist, uint64_t* red) {
+    const uint32_t ncell = lut_model_cells(nb);
+    const uint32_t lg = 31 - __clz(ncell);
+    const uint64_t smin = A[0];
+    const uint32_t bits = bitlen64(A[s - 1] - smin);
+    const uint32_t shift = bits > lg ? bits - lg : 0u;
+    uint16_t* lut = (uint16_t*)payload;
+    for (uint32_t i = threadIdx.x; i <= s; i += NT) {
+        const uint32_t lo = i == 0 ? 0u : lut_cell(A[i - 1], smin, shift, ncell) + 1;
+        const uint32_t hi = i == s ? ncell - 1 : lut_cell(A[i], smin, shift, ncell);
+        const uint64_t v = (uint64_t)i * nb / s;
+        const uint16_t b = (uint16_t)(v >= nb ? nb - 1 : v);
+        for (uint32_t c = lo; c <= hi; ++c) lut[c] = b;
+    }
+    for (uint32_t b = threadIdx.x; b < nb; b += NT) hist[b] = 0;
+    if (threadIdx.x == 0) {
+        h->kind = kRadix;
+        h->flags = kModelLut;
+        h->nbuckets = nb;
+        h->B = ncell;
+        h->shift = shift;
+        h->radix_min = smin;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < s; i += NT) atomicAdd(&hist[lut[lut_cell(A[i], smin, shift, ncell)]], 1u);
+    __syncthreads();
+    uint64_t mx = 0;
+    for (uint32_t b = threadIdx.x; b < nb; b += NT) mx = hist[b] > mx ? hist[b] : mx;
+    return block_reduce_max<NT>(mx, red);
+}
+
 // Radix/fill fallback model: min/max of the whole segment (one CTA).
 template <int NT>
 __device__ void build_radix_model(const SegDesc& sd, const void* src, bool f64, ModelHdr* h, uint64_t* red) {
@@ -504,6 +544,15 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
         }
         __syncthreads();
         if (!slice) sample_sorted<IN_F64, MC>(sd, src, seed, s1, s2, S);
+        if (cfg.lut && sd.depth >= 1) {  // GPU policy: cell table instead of an RMI
+            const uint64_t mx = build_lut_block<NT>(A, s2, sd.rmi_b, h, payload, S.u.rmi.first, S.red64);
+            if (poor_model(mx, s2, sd.rmi_b)) {
+                if (threadIdx.x == 0) h->flags = 0;
+                tree_build_block<NT>(A, s2, sd.tree_k, true, h, payload, S.u.tree.scratch, S.u.tree.wsum,
+                                     S.u.tree.spl);
+            }
+            return;
+        }
         train_rmi_block<NT>(A, s2, sd.rmi_b, h, (RmiEntry*)payload, S.u.rmi.first, S.u.rmi.lo, S.u.rmi.hi,
                             S.u.rmi.big, S.u.rmi.red);
         if (cfg.quality) {

@@ -105,9 +105,10 @@ struct KState {
     const uint16_t* lut;
     uint64_t lbase;
     uint32_t lshift, lutT, llog;
-    // radix / fill
+    // radix / fill / cell table (rlut: shared memory, rcells entries; nullptr = plain radix)
     uint64_t rmin;
-    uint32_t shift, fill;
+    uint32_t shift, fill, rcells;
+    const uint16_t* rlut;
 };
 
 // tree payload capacity (tree_payload_bytes(1024, 1023), 16-byte rounded)
@@ -214,6 +215,16 @@ __device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t
         }
     } else {
         S.rmin = h->radix_min; S.shift = h->shift; S.fill = h->kind == kFill;
+        S.rlut = nullptr;
+        S.rcells = h->B;
+        if (h->kind == kRadix && (h->flags & kModelLut)) {  // the cell table -> shared memory
+            const uint4* src = (const uint4*)(g + sizeof(ModelHdr));
+            const uint32_t words = (2 * S.rcells + 15) / 16;
+            __syncthreads();  // previous users of tree_smem are done
+            for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) ((uint4*)tree_smem)[i] = src[i];
+            S.rlut = (const uint16_t*)tree_smem;
+            __syncthreads();
+        }
     }
 }
 
@@ -237,6 +248,7 @@ __device__ __forceinline__ uint32_t kclassify(const KState& S, uint64_t x) {
         return tree_bucket(S.levels, S.leaf, S.nsplit, S.tree, S.spl, S.eqo, x);
     } else {
         if (S.fill) return 1u << 31;
+        if (S.rlut) return S.rlut[lut_cell(x, S.rmin, S.shift, S.rcells)];
         uint64_t d = (x - S.rmin) >> S.shift;
         return d >= S.nb ? S.nb - 1 : (uint32_t)d;
     }
@@ -1210,6 +1222,7 @@ void launch_kind_plan(const LevelParams& p, cudaStream_t st) {
 void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_rmi_b, int grid, cudaStream_t st) {
     const size_t table_bytes = 20 * (size_t)max_rmi_b;
     size_t sm_r = 16 + 4 * (size_t)kMaxNB + 2 * kTileBytes, sm_t = sm_r + kTreeCap, sm_l = sm_r + table_bytes;
+    sm_r += 2 * (size_t)kLutModelMaxCells;  // (radix kind: a cell-table model's table)
     if (kinds & 1) {
         const int gl = grid;
         if (in_f64) pdl(k_hist<true, kLearned>, gl, kPNT, sm_l, st, p);
