@@ -116,7 +116,7 @@ typedef struct lsort_stats {
     double ms_total;                /* device time of the sort (events) */
     double ms_h2d, ms_d2h;          /* LSORT_MEM_HOST transfers */
     uint32_t levels;                /* distribution levels run (batch / many: summed over the arrays) */
-    uint32_t level0_kind;           /* 0 learned, 1 tree, 2 base case only */
+    uint32_t level0_kind;           /* 0 learned (RMI), 1 tree, 2 base case only, 3 learned cell table (GPU policy) */
     uint64_t partitioned_keys;      /* keys moved by distribution passes (all levels) */
     uint64_t base_case_keys;
     uint64_t fill_keys;             /* keys written by equality/homogeneous fills */

@@ -86,6 +86,10 @@ constexpr uint64_t kAutoClusterKeys = 4ull << 20;
 constexpr uint32_t kBigRootBuckets = 512;
 constexpr uint64_t kBigRootMinKeys = 32ull << 20;
 constexpr uint64_t kRootSampleMin = 256ull << 10;
+inline bool root_lut_enabled() {
+    static const bool off = getenv("LSORT_NO_ROOT_LUT") != nullptr;
+    return !off;
+}
 
 inline uint32_t fanout(uint64_t n, uint32_t cfg_count, uint32_t target) {
     if (target == 0) return cfg_count;
@@ -124,7 +128,8 @@ struct lsort_ctx {
     std::string err;
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
-        kseg, ktp, kplan, qws, ids, clus, cidx, scratch2, dws, bat[3], psample, slices, fwd_model, fwd_slices, piv, fsample;
+        kseg, ktp, kplan, qws, ids, clus, cidx, scratch2, dws, bat[3], psample, slices, fwd_model, fwd_slices, piv, fsample,
+        lutws;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
@@ -520,9 +525,22 @@ struct Engine {
         launch_scatter(q, 0, nb, g, st);
         launch_base_cases(q, N->scratch.as<uint64_t>(), N->sample.p, 0, st);
         launch_fill(q, N->sample.p, 0, nsm, st);
+        launched(2 + 9);
+        // GPU policy: a root that takes the one-pass level 0 tries a cell table
+        // first (models.cu k_root_lut); the RMI is trained only if it is rejected
+        const uint32_t* tgate = gate;
+        if (dc.lut && sp.depth == 0 && !given_sample && root_lut_enabled() && hseg.nb_max <= kDirectMaxBuckets &&
+            n >= kDirectMinPerBucket * hseg.nb_max) {
+            if (!N->lutws.ensure(root_lut_workspace_bytes() + 16)) throw LsortError{LSORT_ENOMEM, "root cell table"};
+            uint32_t* train_gate = (uint32_t*)(N->lutws.as<uint8_t>() + root_lut_workspace_bytes());
+            launch_root_lut(N->sample.as<uint64_t>(), s2, C->models.as<uint8_t>() + hseg.model_off, N->lutws.p, gate,
+                            train_gate, st);
+            launched(2);
+            tgate = train_gate;
+        }
         launch_train_rmi(N->sample.as<uint64_t>(), s2, sub, C->models.as<uint8_t>() + hseg.model_off,
-                         hseg.rmi_b, N->train_ws.p, gate, st);
-        launched(2 + 9 + 8);
+                         hseg.rmi_b, N->train_ws.p, tgate, st);
+        launched(8);
         if (dc.quality) {  // (and the children's sample slices for the root)
             if (!N->qws.ensure(quality_workspace_bytes())) throw LsortError{LSORT_ENOMEM, "quality workspace"};
             // a big root (>= 32 Mi keys, 512 buckets) keeps a learned model up to a
@@ -694,7 +712,7 @@ struct Engine {
                 else if (mc == 1) mids.push_back(j);
                 else hi[nsmall++] = j;
                 if (s.flags & kSegForceRadix) kinds |= 4u;
-                else kinds |= (s.n >= effective_min_rmi(cfg) ? (s.depth >= 1 && dev_cfg(cfg).lut ? 5u : 1u) : 0u) | 2u;
+                else kinds |= (s.n >= effective_min_rmi(cfg) ? (dev_cfg(cfg).lut ? 5u : 1u) : 0u) | 2u;
             }
             const uint32_t np = (uint32_t)psegs.size();
             const uint32_t ncl = (uint32_t)clus.size();
@@ -947,7 +965,7 @@ struct Engine {
             }
             if (level == 0 && stats) {
                 const ModelHdr& h0 = *C->hmodel.as<ModelHdr>();
-                stats->level0_kind = h0.kind == kLearned ? 0 : 1;
+                stats->level0_kind = h0.kind == kLearned ? 0 : (h0.kind == kRadix && (h0.flags & kModelLut) ? 3 : 1);
             }
             if (stats) {
                 stats->levels = level + 1;

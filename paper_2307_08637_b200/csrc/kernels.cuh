@@ -152,6 +152,12 @@ void launch_quality_check(const uint64_t* sorted, uint64_t s, uint8_t* model, ui
                           uint32_t* offs, const uint32_t* gate, cudaStream_t st, uint32_t share_den = 0,
                           uint32_t poor_share = kPoorShare);
 size_t quality_workspace_bytes();
+// GPU policy: a learned root becomes a cell-table model (kModelLut) when the
+// table balances its sorted sample within 2x the mean bucket (models.cu)
+size_t root_lut_workspace_bytes();
+// (before the RMI training, which runs gated on *train_gate: skipped when the table is accepted)
+void launch_root_lut(const uint64_t* sorted, uint64_t s, uint8_t* model, void* ws, const uint32_t* gate,
+                     uint32_t* train_gate, cudaStream_t st);
 // offsets[b] = first index of the sorted sample whose bucket (under `model`) is >= b, b <= nb
 void launch_sample_slices(const uint64_t* sorted, uint64_t s, const uint8_t* model, uint32_t* offsets,
                           uint32_t nb_cap, const uint32_t* gate, cudaStream_t st);

@@ -86,6 +86,7 @@ constexpr uint32_t kModelIdentityCdf = 1u;  // ModelHdr.flags: cdf_lo == 0 and i
 constexpr uint32_t kModelLut = 2u;
 constexpr uint32_t kLutModelMaxCells = 8192;
 constexpr uint32_t kLutModelCellsPerBucket = 32;
+constexpr uint32_t kRootLutCells = 8192;  // a root's table (payload >= 64 B x submodels >= 2 x cells)
 __host__ __device__ __forceinline__ uint32_t lut_model_cells(uint32_t nb) {
     const uint32_t c = nb * kLutModelCellsPerBucket;
     return c < kLutModelMaxCells ? c : kLutModelMaxCells;

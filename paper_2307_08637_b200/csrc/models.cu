@@ -1017,6 +1017,103 @@ __global__ void __launch_bounds__(512) k_quality(const uint64_t* s, uint32_t n, 
 
 size_t quality_workspace_bytes() { return 4 * ((size_t)LSORT_MAX_RMI_DEV + 8); }
 
+// ---------------------------------------------- root cell table (GPU policy)
+// A learned root's RMI is replaced by a cell-table model (kModelLut) over its
+// sorted sample when the table balances the sample at least as evenly as the
+// bound below: one u16 read per key in the one-pass level 0 instead of an RMI
+// evaluation (root route + 20-byte submodel lookup, ~30 instructions).
+// (1) k_lut_ranks (many CTAs): R[c] = number of samples below the start of cell c;
+// (2) k_root_lut (one CTA): lut[c] = min(nb - 1, R[c] nb / s), the sample's
+//     bucket sizes from R at the first cell of every bucket; accepted if the
+//     largest holds <= 2x the mean -- then header + table replace the RMI.
+__device__ __forceinline__ void lut_geometry(const uint64_t* s, uint32_t n, uint32_t ncell, uint64_t& origin,
+                                             uint32_t& shift) {
+    origin = s[0];
+    const uint32_t lg = 31 - __clz(ncell);
+    const uint32_t bits = bitlen64(s[n - 1] - origin);
+    shift = bits > lg ? bits - lg : 0u;
+}
+__global__ void __launch_bounds__(256) k_lut_ranks(const uint64_t* s, uint32_t n, const uint8_t* model, uint32_t* R,
+                                                   const uint32_t* gate) {
+    griddep_wait();
+    if (gated_off(gate)) return;
+    const ModelHdr* h = (const ModelHdr*)model;
+    if (h->kind != kLearned || n < 2) return;
+    const uint32_t ncell = min(kRootLutCells, kLutModelCellsPerBucket * h->B);
+    uint64_t origin;
+    uint32_t shift;
+    lut_geometry(s, n, ncell, origin, shift);
+    // one lower-bound search per cell (a per-sample fill of the cells between
+    // consecutive samples leaves one thread thousands of cells across a gap)
+    for (uint32_t c = blockIdx.x * 256 + threadIdx.x; c < ncell; c += gridDim.x * 256) {
+        const uint64_t off = (uint64_t)c << shift;
+        const uint64_t start = off > ~0ull - origin ? ~0ull : origin + off;
+        uint32_t b = 0, m = n;
+        while (m > 0) {
+            const uint32_t h = m >> 1;
+            if (s[b + h] < start) { b += h + 1; m -= h + 1; }
+            else m = h;
+        }
+        R[c] = c ? b : 0u;
+    }
+}
+constexpr int kRootLutNT = 1024;
+__global__ void __launch_bounds__(kRootLutNT) k_root_lut(const uint64_t* s, uint32_t n, uint8_t* model,
+                                                        const uint32_t* R, const uint32_t* gate, uint32_t* train_gate) {
+    griddep_wait();
+    __shared__ uint32_t off[LSORT_MAX_RMI_DEV + 1];
+    __shared__ uint64_t red[kRootLutNT / 32];
+    // the RMI is trained (train_gate) unless the table is accepted
+    const bool on = !gated_off(gate);
+    if (threadIdx.x == 0) *train_gate = on ? 1u : 0u;
+    if (!on) return;
+    ModelHdr* h = (ModelHdr*)model;
+    if (h->kind != kLearned || n < 2) return;
+    const uint32_t nb = h->nbuckets;
+    const uint32_t ncell = min(kRootLutCells, kLutModelCellsPerBucket * h->B);
+    uint64_t origin;
+    uint32_t shift;
+    lut_geometry(s, n, ncell, origin, shift);
+    auto bucket = [&](uint32_t c) -> uint32_t {
+        const uint64_t v = (uint64_t)R[c] * nb / n;
+        return v >= nb ? nb - 1 : (uint32_t)v;
+    };
+    // off[b] = samples below bucket b's first cell (buckets no cell maps to: empty)
+    for (uint32_t b = threadIdx.x; b <= nb; b += kRootLutNT) off[b] = n;
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < ncell; c += kRootLutNT) {
+        const uint32_t b = bucket(c), lo = c == 0 ? 0u : bucket(c - 1) + 1;
+        for (uint32_t q = lo; q <= b; ++q) off[q] = R[c];
+    }
+    __syncthreads();
+    uint64_t mx = 0;
+    for (uint32_t b = threadIdx.x; b < nb; b += kRootLutNT) {
+        const uint32_t c = off[b + 1] - off[b];
+        mx = c > mx ? c : mx;
+    }
+    mx = block_reduce_max<kRootLutNT>(mx, red);
+    if (mx * nb > 2ull * n) return;  // keep the RMI
+    uint16_t* lut = (uint16_t*)(model + sizeof(ModelHdr));
+    for (uint32_t c = threadIdx.x; c < ncell; c += kRootLutNT) lut[c] = (uint16_t)bucket(c);
+    if (threadIdx.x == 0) {
+        h->kind = kRadix;
+        h->flags = kModelLut;
+        h->B = ncell;
+        h->shift = shift;
+        h->radix_min = origin;
+        *train_gate = 0;
+    }
+}
+
+size_t root_lut_workspace_bytes() { return 4 * (size_t)kRootLutCells; }
+
+void launch_root_lut(const uint64_t* sorted, uint64_t s, uint8_t* model, void* ws, const uint32_t* gate,
+                     uint32_t* train_gate, cudaStream_t st) {
+    const int g = (int)(kRootLutCells / 256);
+    pdl(k_lut_ranks, g, 256, 0, st, sorted, (uint32_t)s, (const uint8_t*)model, (uint32_t*)ws, gate);
+    pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)ws, gate, train_gate);
+}
+
 // Bucket boundaries in a sorted sample (monotone bucket function): element i
 // writes offsets[b] = i for every b in (bucket(s[i-1]), bucket(s[i])].
 __global__ void __launch_bounds__(256) k_sample_slices(const uint64_t* s, uint32_t n, const uint8_t* model,

@@ -909,7 +909,9 @@ __global__ void __launch_bounds__(NT) k_direct_setup(LevelParams p, uint64_t roo
     const SegDesc sd = p.segs[0];
     const ModelHdr* h = (const ModelHdr*)(p.models + sd.model_off);
     const uint32_t nb = h->nbuckets;
-    if (h->kind != kLearned || root_m == 0 || nb > kDirectMaxBuckets || h->B > kDirectMaxBuckets || !p.slices) {
+    const bool lutm = h->kind == kRadix && (h->flags & kModelLut);  // a root cell table
+    if ((h->kind != kLearned && !lutm) || root_m == 0 || nb > kDirectMaxBuckets ||
+        (!lutm && h->B > kDirectMaxBuckets) || !p.slices) {
         if (threadIdx.x == 0) *w.ovf = 2u;  // not eligible: the exact level runs
         return;
     }
@@ -938,8 +940,11 @@ struct DirectSmem {
     alignas(16) uint32_t cnt[2][kDirectMaxBuckets + 4];
     uint16_t sbid[kTileKeys];
     uint32_t wsum[kPNT / 32 + 1];
-    alignas(16) uint8_t table[20 * kDirectMaxBuckets];  // the segment model's compiled table (kstate_load)
+    // the segment model's compiled table or cell table (kstate_load)
+    alignas(16) uint8_t table[20 * kDirectMaxBuckets > 2 * kRootLutCells ? 20 * kDirectMaxBuckets : 2 * kRootLutCells];
 };
+
+static_assert(sizeof(DirectSmem) + 1024 <= 233472 / kPartPerSM, "one-pass level: kPartPerSM CTAs per SM");
 
 // MULTI = false: one segment (level 0, the only form launched), its model
 // table loaded once (the per-tile segment switch of the multi-segment form
@@ -965,8 +970,12 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
     int64_t curseg = -1;
     uint64_t boff = 0;
     uint32_t nb = 0;
+    bool lutm = false;  // (CTA-uniform) the root is a cell table (GPU policy), else an RMI
     if (!MULTI) {
-        kstate_load<kLearned>(S, p.models + p.segs[0].model_off, Q.table);
+        const ModelHdr* h0 = (const ModelHdr*)(p.models + p.segs[0].model_off);
+        lutm = h0->kind == kRadix;
+        if (lutm) kstate_load<kRadix>(S, p.models + p.segs[0].model_off, Q.table);
+        else kstate_load<kLearned>(S, p.models + p.segs[0].model_off, Q.table);
         boff = p.segs[0].bucket_off;
         nb = S.nb;
     }
@@ -1019,7 +1028,8 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
         uint32_t code[kPItems];  // bucket << 16 | rank within the tile; ~0 = no key
         {
             uint32_t bk[kPItems];
-            classify16<kLearned>(S, v, bk);
+            if (lutm) classify16<kRadix>(S, v, bk);
+            else classify16<kLearned>(S, v, bk);
 #pragma unroll
             for (int q = 0; q < kPItems; ++q) {
                 const bool ok = threadIdx.x + (q >> 1) * kPNT < g.npairs;
@@ -1037,7 +1047,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
                 if (isnan(d)) atomicMin(&p.ctrl->nan_index, (unsigned long long)ix);
                 k = encode(d);
             }
-            const uint32_t b = kclassify<kLearned>(S, k);
+            const uint32_t b = lutm ? kclassify<kRadix>(S, k) : kclassify<kLearned>(S, k);
             scode = b << 16 | atomicAdd(&cnt[b], 1u);
             skey = k;
         }
@@ -1222,7 +1232,7 @@ void launch_kind_plan(const LevelParams& p, cudaStream_t st) {
 void launch_hist(const LevelParams& p, int in_f64, uint32_t kinds, uint32_t max_rmi_b, int grid, cudaStream_t st) {
     const size_t table_bytes = 20 * (size_t)max_rmi_b;
     size_t sm_r = 16 + 4 * (size_t)kMaxNB + 2 * kTileBytes, sm_t = sm_r + kTreeCap, sm_l = sm_r + table_bytes;
-    sm_r += 2 * (size_t)kLutModelMaxCells;  // (radix kind: a cell-table model's table)
+    sm_r += 2 * (size_t)(kLutModelMaxCells > kRootLutCells ? kLutModelMaxCells : kRootLutCells);  // (radix kind: a cell table)
     if (kinds & 1) {
         const int gl = grid;
         if (in_f64) pdl(k_hist<true, kLearned>, gl, kPNT, sm_l, st, p);
