@@ -91,9 +91,35 @@ __host__ __device__ __forceinline__ uint32_t lut_model_cells(uint32_t nb) {
     const uint32_t c = nb * kLutModelCellsPerBucket;
     return c < kLutModelMaxCells ? c : kLutModelMaxCells;
 }
+// Cell of key x. Narrow tables (shift < 32): cells of 2^shift keys from the
+// origin. Wide tables (shift >= 32): cells aligned to multiples of 2^shift, so
+// the cell index is a 32-bit function of the key's high word (half the
+// instructions of the 64-bit offset); lut_pick_shift makes both fit ncell cells.
 __device__ __forceinline__ uint32_t lut_cell(uint64_t x, uint64_t origin, uint32_t shift, uint32_t ncell) {
+    if (shift >= 32) {
+        const uint32_t h = (uint32_t)(x >> 32) >> (shift - 32), o = (uint32_t)(origin >> shift);
+        return h > o ? min(h - o, ncell - 1) : 0u;
+    }
     const uint64_t c = (x > origin ? x - origin : 0ull) >> shift;
     return c < ncell ? (uint32_t)c : ncell - 1;
+}
+// first key of cell c >= 1 (saturating)
+__device__ __forceinline__ uint64_t lut_cell_start(uint32_t c, uint64_t origin, uint32_t shift) {
+    if (shift >= 32) {
+        const uint64_t q = (origin >> shift) + c;
+        return q >= (1ull << (64 - shift)) ? ~0ull : q << shift;
+    }
+    const uint64_t off = (uint64_t)c << shift;
+    return off > ~0ull - origin ? ~0ull : origin + off;
+}
+// smallest shift whose cells over [lo, hi] fit ncell (a power of two)
+__device__ __forceinline__ uint32_t lut_pick_shift(uint64_t lo, uint64_t hi, uint32_t ncell) {
+    const uint32_t lg = 31 - __clz(ncell);
+    const uint32_t bits = hi > lo ? 64u - (uint32_t)__clzll((long long)(hi - lo)) : 0u;
+    uint32_t s = bits > lg ? bits - lg : 0u;
+    if (s >= 32)
+        while (s < 63 && (hi >> s) - (lo >> s) > ncell - 1) ++s;
+    return s;
 }
 
 // Partition-model record, 128 bytes; payload follows in the model arena:

@@ -387,10 +387,8 @@ template <int NT>
 __device__ uint64_t build_lut_block(const uint64_t* A, uint32_t s, uint32_t nb, ModelHdr* h, uint8_t* payload,
                                     uint32_t* hist, uint64_t* red) {
     const uint32_t ncell = lut_model_cells(nb);
-    const uint32_t lg = 31 - __clz(ncell);
     const uint64_t smin = A[0];
-    const uint32_t bits = bitlen64(A[s - 1] - smin);
-    const uint32_t shift = bits > lg ? bits - lg : 0u;
+    const uint32_t shift = lut_pick_shift(smin, A[s - 1], ncell);
     uint16_t* lut = (uint16_t*)payload;
     for (uint32_t i = threadIdx.x; i <= s; i += NT) {
         const uint32_t lo = i == 0 ? 0u : lut_cell(A[i - 1], smin, shift, ncell) + 1;
@@ -1029,9 +1027,7 @@ size_t quality_workspace_bytes() { return 4 * ((size_t)LSORT_MAX_RMI_DEV + 8); }
 __device__ __forceinline__ void lut_geometry(const uint64_t* s, uint32_t n, uint32_t ncell, uint64_t& origin,
                                              uint32_t& shift) {
     origin = s[0];
-    const uint32_t lg = 31 - __clz(ncell);
-    const uint32_t bits = bitlen64(s[n - 1] - origin);
-    shift = bits > lg ? bits - lg : 0u;
+    shift = lut_pick_shift(origin, s[n - 1], ncell);
 }
 __global__ void __launch_bounds__(256) k_lut_ranks(const uint64_t* s, uint32_t n, const uint8_t* model, uint32_t* R,
                                                    const uint32_t* gate) {
@@ -1046,8 +1042,7 @@ __global__ void __launch_bounds__(256) k_lut_ranks(const uint64_t* s, uint32_t n
     // one lower-bound search per cell (a per-sample fill of the cells between
     // consecutive samples leaves one thread thousands of cells across a gap)
     for (uint32_t c = blockIdx.x * 256 + threadIdx.x; c < ncell; c += gridDim.x * 256) {
-        const uint64_t off = (uint64_t)c << shift;
-        const uint64_t start = off > ~0ull - origin ? ~0ull : origin + off;
+        const uint64_t start = lut_cell_start(c, origin, shift);
         uint32_t b = 0, m = n;
         while (m > 0) {
             const uint32_t h = m >> 1;

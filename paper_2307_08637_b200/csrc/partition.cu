@@ -109,6 +109,7 @@ struct KState {
     uint64_t rmin;
     uint32_t shift, fill, rcells;
     const uint16_t* rlut;
+    uint32_t rorg;  // wide cell tables: (rmin >> shift), the high-word origin (lut_cell)
 };
 
 // tree payload capacity (tree_payload_bytes(1024, 1023), 16-byte rounded)
@@ -217,6 +218,7 @@ __device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t
         S.rmin = h->radix_min; S.shift = h->shift; S.fill = h->kind == kFill;
         S.rlut = nullptr;
         S.rcells = h->B;
+        S.rorg = S.shift >= 32 ? (uint32_t)(S.rmin >> S.shift) : 0u;
         if (h->kind == kRadix && (h->flags & kModelLut)) {  // the cell table -> shared memory
             const uint4* src = (const uint4*)(g + sizeof(ModelHdr));
             const uint32_t words = (2 * S.rcells + 15) / 16;
@@ -248,7 +250,13 @@ __device__ __forceinline__ uint32_t kclassify(const KState& S, uint64_t x) {
         return tree_bucket(S.levels, S.leaf, S.nsplit, S.tree, S.spl, S.eqo, x);
     } else {
         if (S.fill) return 1u << 31;
-        if (S.rlut) return S.rlut[lut_cell(x, S.rmin, S.shift, S.rcells)];
+        if (S.rlut) {  // lut_cell with the origin's high word precomputed
+            if (S.shift >= 32) {
+                const uint32_t h = (uint32_t)(x >> 32) >> (S.shift - 32);
+                return S.rlut[h > S.rorg ? min(h - S.rorg, S.rcells - 1) : 0u];
+            }
+            return S.rlut[lut_cell(x, S.rmin, S.shift, S.rcells)];
+        }
         uint64_t d = (x - S.rmin) >> S.shift;
         return d >= S.nb ? S.nb - 1 : (uint32_t)d;
     }
@@ -317,6 +325,13 @@ __device__ __forceinline__ void classify16(const KState& S, const ulonglong2 (&v
             const uint32_t e0 = S.eqo[base];
             const uint32_t eq = (base < S.nsplit) && (S.eqo[base + 1] - e0 > 1) && (x == S.spl[base]);
             c[q] = (e0 + eq) | (eq << 31);
+        }
+    } else if (KIND == kRadix && S.rlut && S.shift >= 32) {  // wide cell table: 32-bit cells (lut_cell)
+        const uint32_t sh = S.shift - 32, last = S.rcells - 1;
+#pragma unroll
+        for (int q = 0; q < kPItems; ++q) {
+            const uint32_t h = (uint32_t)(((q & 1) ? v[q >> 1].y : v[q >> 1].x) >> 32) >> sh;
+            c[q] = S.rlut[h > S.rorg ? min(h - S.rorg, last) : 0u];
         }
     } else {
 #pragma unroll
