@@ -465,7 +465,7 @@ void dist_sort(lsort_dist* D, void* keys, uint64_t n, int key_kind, void* out, u
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)num_sms() * kPartPerSM));
     if (n) {
         launch_kind_plan(p, st);
-        launch_hist(p, f64, 3u, B, grid, st);
+        launch_hist(p, f64, 7u, B, grid, st);  // learned, tree or cell table
         C->launches += 3;
     }
 
@@ -624,7 +624,7 @@ void dist_sort(lsort_dist* D, void* keys, uint64_t n, int key_kind, void* out, u
     }
     if (stats) {
         stats->levels += 1;  // the distributed level 0
-        stats->level0_kind = mi.kind == kLearned ? 0 : 1;
+        stats->level0_kind = mi.kind == kLearned ? 0 : (mi.kind == kRadix ? 3 : 1);
         stats->partitioned_keys += n;
         stats->segments += 1;
     }

@@ -526,10 +526,12 @@ struct Engine {
         launch_base_cases(q, N->scratch.as<uint64_t>(), N->sample.p, 0, st);
         launch_fill(q, N->sample.p, 0, nsm, st);
         launched(2 + 9);
-        // GPU policy: a root that takes the one-pass level 0 tries a cell table
-        // first (models.cu k_root_lut); the RMI is trained only if it is rejected
+        // GPU policy: a root that takes the one-pass level 0 (or a multi-GPU global
+        // model of that size) tries a cell table first (models.cu k_root_lut); the
+        // RMI is trained only if it is rejected. (An accepted table's largest
+        // bucket holds <= 2 / nb of the sample: within the rank-balance share test.)
         const uint32_t* tgate = gate;
-        if (dc.lut && sp.depth == 0 && !given_sample && root_lut_enabled() && hseg.nb_max <= kDirectMaxBuckets &&
+        if (dc.lut && sp.depth == 0 && root_lut_enabled() && hseg.nb_max <= kDirectMaxBuckets &&
             n >= kDirectMinPerBucket * hseg.nb_max) {
             if (!N->lutws.ensure(root_lut_workspace_bytes() + 16)) throw LsortError{LSORT_ENOMEM, "root cell table"};
             uint32_t* train_gate = (uint32_t*)(N->lutws.as<uint8_t>() + root_lut_workspace_bytes());
