@@ -22,7 +22,7 @@ def parse_variant(v):
     kw = {}
     for item in filter(None, v.split(",")):
         k, x = item.split("=")
-        kw[k.strip()] = int(float(x))
+        kw[k.strip()] = float(x) if k.strip() == "sample_fraction" else int(float(x))
     return kw
 
 
