@@ -553,3 +553,28 @@ def test_padded_level0_and_its_fallback(ctx, dist_name, seed):
     st = ctx.sort(d, L.SortConfig(flags=L._native.FLAG_TEST_DIRECT_OVERFLOW))
     assert st["direct_keys"] == 0
     assert np.array_equal(d.cpu().numpy().view(np.uint64), exp)
+
+
+@pytest.mark.parametrize("case", ["lognormal2_f64", "narrow_u64"])
+def test_cell_table_models(ctx, case):
+    """GPU policy (DESIGN 3, 6): a one-pass root tries a cell table over its
+    sorted sample (level0_kind 3 when accepted; wide tables use 32-bit aligned
+    cells, narrow ones 64-bit offsets) and every learned-eligible segment
+    below the root gets one. The strict reference policy builds none; both
+    outputs equal numpy's sort bit for bit."""
+    n = 40_000_000
+    if case == "lognormal2_f64":
+        x = O.generate("lognormal2", n, 19)
+        exp = O.decode(np.sort(O.encode(x))).view(np.uint64)
+    else:  # uint64 keys over a 2^24 range: cells narrower than 2^32 keys
+        x = np.random.default_rng(5).integers(0, 1 << 24, n, dtype=np.uint64)
+        exp = np.sort(x)
+    d = dev(x)
+    st = ctx.sort(d)
+    assert st["level0_kind"] == 3, st["level0_kind"]
+    assert st["direct_keys"] == n
+    assert np.array_equal(host_u64(d), exp)
+    d = dev(x)
+    st = ctx.sort(d, L.SortConfig(flags=L._native.FLAG_STRICT_POLICY))
+    assert st["level0_kind"] != 3
+    assert np.array_equal(host_u64(d), exp)
