@@ -535,9 +535,10 @@ struct Engine {
             n >= kDirectMinPerBucket * hseg.nb_max) {
             if (!N->lutws.ensure(root_lut_workspace_bytes() + 16)) throw LsortError{LSORT_ENOMEM, "root cell table"};
             uint32_t* train_gate = (uint32_t*)(N->lutws.as<uint8_t>() + root_lut_workspace_bytes());
+            static const bool no_log = getenv("LSORT_NO_LOG_LUT") != nullptr;
             launch_root_lut(N->sample.as<uint64_t>(), s2, C->models.as<uint8_t>() + hseg.model_off, N->lutws.p, gate,
-                            train_gate, st);
-            launched(2);
+                            train_gate, st, f64 && !no_log);
+            launched(f64 && !no_log ? 6 : 2);
             tgate = train_gate;
         }
         launch_train_rmi(N->sample.as<uint64_t>(), s2, sub, C->models.as<uint8_t>() + hseg.model_off,
@@ -832,7 +833,7 @@ struct Engine {
                               (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM), st,
                               (cfg.flags & LSORT_FLAG_TEST_DIRECT_OVERFLOW) != 0);
                 if (timing) CU(cudaEventRecord(C->pev[7], st));
-                launched(4);
+                launched(6);
                 p.gate = &dctrl->run_exact;
             }
             p.ids = C->ids.as<uint16_t>();  // (the one-pass setup may have grown the id array)

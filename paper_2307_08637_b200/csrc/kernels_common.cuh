@@ -37,6 +37,7 @@ __device__ __forceinline__ uint64_t rmi_sample_size(const DevCfg& c, uint64_t n)
 __device__ __forceinline__ uint32_t model_payload_bytes(const ModelHdr& h) {
     if (h.kind == kLearned) return kLearnedEntryBytes * h.B;
     if (h.kind == kTree) return (uint32_t)((tree_payload_bytes(h.leaf_origin, h.nsplit) + 15) & ~15ull);
+    if (h.kind == kRadix && (h.flags & kModelLog)) return ((2 * h.levels + 15) & ~15u) + ((2 * h.B + 15) & ~15u);
     if (h.kind == kRadix && (h.flags & kModelLut)) return (2 * h.B + 15) & ~15u;
     return 0;
 }
@@ -94,6 +95,11 @@ struct Classifier {
         } else if constexpr (KIND == kTree) {
             return tree_bucket(levels, leaf_origin, nsplit, m.tree, m.spl, m.eqo, x);
         } else if constexpr (KIND == kRadix) {
+            if (flags & kModelLog) {
+                const uint16_t* tab = (const uint16_t*)(m.h + 1);
+                const uint16_t* lut = tab + ((levels + 7) & ~7u);
+                return lut[binade_cell(x, tab, (uint32_t)rmin, levels, B)];
+            }
             if (flags & kModelLut) return ((const uint16_t*)(m.h + 1))[lut_cell(x, rmin, shift, B)];
             uint64_t d = (x - rmin) >> shift;
             return d >= nb ? nb - 1 : (uint32_t)d;

@@ -87,6 +87,22 @@ constexpr uint32_t kModelLut = 2u;
 constexpr uint32_t kLutModelMaxCells = 8192;
 constexpr uint32_t kLutModelCellsPerBucket = 32;
 constexpr uint32_t kRootLutCells = 8192;  // a root's table (payload >= 64 B x submodels >= 2 x cells)
+// Binade-indexed ("log") cell table for roots whose keys span many binades
+// (encoded floats are log-scaled: a linear table over Normal's or a mixture's
+// range puts all keys into a few cells). flags kModelLut | kModelLog; radix_min
+// = first binade (top 12 key bits) of the table, levels = binades, B = cells;
+// payload u16 tab[levels] then u16 lut[B]. tab entry = first cell | log2(cells
+// of the binade) << 12 (empty binades: the next binade's first cell, 0 bits).
+constexpr uint32_t kModelLog = 4u;
+constexpr uint32_t kBinadeCells = 4096, kLogTabMax = 4096;
+__device__ __forceinline__ uint32_t binade_cell(uint64_t x, const uint16_t* tab, uint32_t bmin, uint32_t ntab,
+                                             uint32_t ncell) {
+    const uint32_t hi = (uint32_t)(x >> 32);
+    const int bi = (int)(hi >> 20) - (int)bmin;
+    const uint32_t e = tab[min(max(bi, 0), (int)ntab - 1)], k = e >> 12;
+    const uint32_t c = (e & 0xfffu) + ((hi >> (20 - k)) & ((1u << k) - 1u));
+    return bi < 0 ? 0u : (bi >= (int)ntab ? ncell - 1 : c);
+}
 __host__ __device__ __forceinline__ uint32_t lut_model_cells(uint32_t nb) {
     const uint32_t c = nb * kLutModelCellsPerBucket;
     return c < kLutModelMaxCells ? c : kLutModelMaxCells;

@@ -1052,9 +1052,88 @@ __global__ void __launch_bounds__(256) k_lut_ranks(const uint64_t* s, uint32_t n
         R[c] = c ? b : 0u;
     }
 }
+// Log tables (when the linear table is rejected): (3) k_binade_starts (many
+// CTAs): first sample index of every binade of the sample's span; (4)
+// k_log_tab (one CTA): 2^floor(log2(cells/2 x share)) cells per non-empty
+// binade, entries by exclusive scan; (5) k_lut_fill (many CTAs): R per cell,
+// cells (cell(s[i-1]), cell(s[i])] get i -- the cells follow the sample's
+// density, so no thread walks a long gap; (6) k_root_lut in log mode.
+struct LogWS {
+    uint32_t* R;       // [kRootLutCells]
+    uint32_t* bst;     // [kLogTabMax + 1]
+    uint16_t* tab;     // [kLogTabMax]
+    uint32_t* ncell;   // 0: rejected
+};
+__host__ __device__ inline LogWS log_ws(void* w) {
+    LogWS L;
+    L.R = (uint32_t*)w;
+    L.bst = L.R + kRootLutCells;
+    L.tab = (uint16_t*)(L.bst + kLogTabMax + 1);
+    L.ncell = (uint32_t*)(L.tab + kLogTabMax);
+    return L;
+}
+__global__ void __launch_bounds__(256) k_binade_starts(const uint64_t* s, uint32_t n, LogWS w, const uint32_t* gate) {
+    griddep_wait();
+    if (gated_off(gate) || n < 2) return;
+    const uint32_t bmin = (uint32_t)(s[0] >> 52), ntab = (uint32_t)(s[n - 1] >> 52) - bmin + 1;
+    if (ntab > kLogTabMax) return;
+    for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i <= n; i += gridDim.x * 256) {
+        const uint32_t b = i < n ? (uint32_t)(s[i] >> 52) - bmin : ntab;
+        const uint32_t lo = i ? (uint32_t)(s[i - 1] >> 52) - bmin + 1 : 0u;
+        for (uint32_t j = lo; j <= b; ++j) w.bst[j] = i;
+    }
+}
 constexpr int kRootLutNT = 1024;
+__global__ void __launch_bounds__(kRootLutNT) k_log_tab(const uint64_t* s, uint32_t n, LogWS w, const uint32_t* gate) {
+    griddep_wait();
+    __shared__ uint32_t cells[kLogTabMax];
+    __shared__ uint32_t wsum[kRootLutNT / 32 + 1];
+    if (gated_off(gate) || n < 2) return;
+    const uint32_t bmin = (uint32_t)(s[0] >> 52), ntab = (uint32_t)(s[n - 1] >> 52) - bmin + 1;
+    if (ntab > kLogTabMax) {
+        if (threadIdx.x == 0) *w.ncell = 0;
+        return;
+    }
+    uint32_t kk[kLogTabMax / kRootLutNT];
+#pragma unroll
+    for (uint32_t q = 0; q < kLogTabMax / kRootLutNT; ++q) {
+        const uint32_t j = threadIdx.x + q * kRootLutNT;
+        uint32_t c = 0, k = 0;
+        if (j < ntab) {
+            const uint32_t cnt = w.bst[j + 1] - w.bst[j];
+            if (cnt) {
+                const uint64_t want = (uint64_t)(kBinadeCells - 256) * cnt / n;
+                k = want > 1 ? min(12u, 63u - (uint32_t)__clzll((long long)want)) : 0u;
+                c = 1u << k;
+            }
+        }
+        cells[j] = c;
+        kk[q] = k;
+    }
+    __syncthreads();
+    const uint32_t total = block_exclusive_scan_u32<kRootLutNT>(cells, kLogTabMax, wsum);
+    if (threadIdx.x == 0) *w.ncell = total <= kBinadeCells ? total : 0u;
+#pragma unroll
+    for (uint32_t q = 0; q < kLogTabMax / kRootLutNT; ++q) {
+        const uint32_t j = threadIdx.x + q * kRootLutNT;
+        if (j < ntab) w.tab[j] = (uint16_t)((cells[j] & 0xfffu) | (kk[q] << 12));
+    }
+}
+__global__ void __launch_bounds__(256) k_lut_fill(const uint64_t* s, uint32_t n, LogWS w, const uint32_t* gate) {
+    griddep_wait();
+    if (gated_off(gate) || n < 2 || *w.ncell == 0) return;
+    const uint32_t ncell = *w.ncell;
+    const uint32_t bmin = (uint32_t)(s[0] >> 52), ntab = (uint32_t)(s[n - 1] >> 52) - bmin + 1;
+    for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i <= n; i += gridDim.x * 256) {
+        const uint32_t c = i < n ? binade_cell(s[i], w.tab, bmin, ntab, ncell) : ncell - 1;
+        const uint32_t lo = i ? binade_cell(s[i - 1], w.tab, bmin, ntab, ncell) + 1 : 0u;
+        const uint32_t r = i < n ? i : n;
+        for (uint32_t q = lo; q <= c; ++q) w.R[q] = r;
+    }
+}
 __global__ void __launch_bounds__(kRootLutNT) k_root_lut(const uint64_t* s, uint32_t n, uint8_t* model,
-                                                        const uint32_t* R, const uint32_t* gate, uint32_t* train_gate) {
+                                                        const uint32_t* R, const uint32_t* gate, uint32_t* train_gate,
+                                                        LogWS lw, uint32_t logm) {
     griddep_wait();
     __shared__ uint32_t off[LSORT_MAX_RMI_DEV + 1];
     __shared__ uint64_t red[kRootLutNT / 32];
@@ -1064,8 +1143,9 @@ __global__ void __launch_bounds__(kRootLutNT) k_root_lut(const uint64_t* s, uint
     if (!on) return;
     ModelHdr* h = (ModelHdr*)model;
     if (h->kind != kLearned || n < 2) return;
+    if (logm && *lw.ncell == 0) return;  // no log table (too many binades or cells)
     const uint32_t nb = h->nbuckets;
-    const uint32_t ncell = min(kRootLutCells, kLutModelCellsPerBucket * h->B);
+    const uint32_t ncell = logm ? *lw.ncell : min(kRootLutCells, kLutModelCellsPerBucket * h->B);
     uint64_t origin;
     uint32_t shift;
     lut_geometry(s, n, ncell, origin, shift);
@@ -1089,24 +1169,44 @@ __global__ void __launch_bounds__(kRootLutNT) k_root_lut(const uint64_t* s, uint
     mx = block_reduce_max<kRootLutNT>(mx, red);
     if (mx * nb > 2ull * n) return;  // keep the RMI
     uint16_t* lut = (uint16_t*)(model + sizeof(ModelHdr));
+    uint32_t ntab = 0;
+    if (logm) {  // log table: binade entries first
+        const uint32_t bmin = (uint32_t)(s[0] >> 52);
+        ntab = (uint32_t)(s[n - 1] >> 52) - bmin + 1;
+        for (uint32_t j = threadIdx.x; j < ntab; j += kRootLutNT) lut[j] = lw.tab[j];
+        lut += (ntab + 7) & ~7u;
+        origin = bmin;
+    }
     for (uint32_t c = threadIdx.x; c < ncell; c += kRootLutNT) lut[c] = (uint16_t)bucket(c);
     if (threadIdx.x == 0) {
         h->kind = kRadix;
-        h->flags = kModelLut;
+        h->flags = logm ? (kModelLut | kModelLog) : kModelLut;
         h->B = ncell;
+        h->levels = ntab;
         h->shift = shift;
         h->radix_min = origin;
         *train_gate = 0;
     }
 }
 
-size_t root_lut_workspace_bytes() { return 4 * (size_t)kRootLutCells; }
+size_t root_lut_workspace_bytes() {
+    return 4 * (size_t)kRootLutCells + 4 * ((size_t)kLogTabMax + 1) + 2 * (size_t)kLogTabMax + 16;
+}
 
 void launch_root_lut(const uint64_t* sorted, uint64_t s, uint8_t* model, void* ws, const uint32_t* gate,
-                     uint32_t* train_gate, cudaStream_t st) {
+                     uint32_t* train_gate, cudaStream_t st, bool log_table) {
     const int g = (int)(kRootLutCells / 256);
     pdl(k_lut_ranks, g, 256, 0, st, sorted, (uint32_t)s, (const uint8_t*)model, (uint32_t*)ws, gate);
-    pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)ws, gate, train_gate);
+    const LogWS w = log_ws(ws);
+    pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)ws, gate, train_gate, w, 0u);
+    if (!log_table) return;
+    // the linear table rejected (train_gate still 1): a binade-indexed one
+    const int gs = (int)std::min<uint64_t>((s + 2047) / 2048, (uint64_t)num_sms() * 2);
+    pdl(k_binade_starts, gs, 256, 0, st, sorted, (uint32_t)s, w, (const uint32_t*)train_gate);
+    pdl(k_log_tab, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, w, (const uint32_t*)train_gate);
+    pdl(k_lut_fill, gs, 256, 0, st, sorted, (uint32_t)s, w, (const uint32_t*)train_gate);
+    pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)w.R,
+        (const uint32_t*)train_gate, train_gate, w, 1u);
 }
 
 // Bucket boundaries in a sorted sample (monotone bucket function): element i

@@ -110,6 +110,8 @@ struct KState {
     uint32_t shift, fill, rcells;
     const uint16_t* rlut;
     uint32_t rorg;  // wide cell tables: (rmin >> shift), the high-word origin (lut_cell)
+    const uint16_t* rtab;  // log tables: binade entries (shared), nullptr otherwise
+    uint32_t rtabn;
 };
 
 // tree payload capacity (tree_payload_bytes(1024, 1023), 16-byte rounded)
@@ -219,12 +221,17 @@ __device__ __forceinline__ void kstate_load(KState& S, const uint8_t* g, uint8_t
         S.rlut = nullptr;
         S.rcells = h->B;
         S.rorg = S.shift >= 32 ? (uint32_t)(S.rmin >> S.shift) : 0u;
-        if (h->kind == kRadix && (h->flags & kModelLut)) {  // the cell table -> shared memory
+        S.rtab = nullptr;
+        S.rtabn = h->levels;
+        if (h->kind == kRadix && (h->flags & kModelLut)) {  // the cell table (log: binade entries first) -> shared memory
             const uint4* src = (const uint4*)(g + sizeof(ModelHdr));
-            const uint32_t words = (2 * S.rcells + 15) / 16;
+            const bool lg = h->flags & kModelLog;
+            const uint32_t tabw = lg ? (2 * S.rtabn + 15) / 16 : 0u;
+            const uint32_t words = tabw + (2 * S.rcells + 15) / 16;
             __syncthreads();  // previous users of tree_smem are done
             for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) ((uint4*)tree_smem)[i] = src[i];
-            S.rlut = (const uint16_t*)tree_smem;
+            if (lg) S.rtab = (const uint16_t*)tree_smem;
+            S.rlut = (const uint16_t*)tree_smem + 8 * tabw;
             __syncthreads();
         }
     }
@@ -251,6 +258,7 @@ __device__ __forceinline__ uint32_t kclassify(const KState& S, uint64_t x) {
     } else {
         if (S.fill) return 1u << 31;
         if (S.rlut) {  // lut_cell with the origin's high word precomputed
+            if (S.rtab) return S.rlut[binade_cell(x, S.rtab, (uint32_t)S.rmin, S.rtabn, S.rcells)];
             if (S.shift >= 32) {
                 const uint32_t h = (uint32_t)(x >> 32) >> (S.shift - 32);
                 return S.rlut[h > S.rorg ? min(h - S.rorg, S.rcells - 1) : 0u];
@@ -326,7 +334,7 @@ __device__ __forceinline__ void classify16(const KState& S, const ulonglong2 (&v
             const uint32_t eq = (base < S.nsplit) && (S.eqo[base + 1] - e0 > 1) && (x == S.spl[base]);
             c[q] = (e0 + eq) | (eq << 31);
         }
-    } else if (KIND == kRadix && S.rlut && S.shift >= 32) {  // wide cell table: 32-bit cells (lut_cell)
+    } else if (KIND == kRadix && S.rlut && !S.rtab && S.shift >= 32) {  // wide cell table: 32-bit cells (lut_cell)
         const uint32_t sh = S.shift - 32, last = S.rcells - 1;
 #pragma unroll
         for (int q = 0; q < kPItems; ++q) {
@@ -961,16 +969,34 @@ struct DirectSmem {
 
 static_assert(sizeof(DirectSmem) + 1024 <= 233472 / kPartPerSM, "one-pass level: kPartPerSM CTAs per SM");
 
-// MULTI = false: one segment (level 0, the only form launched), its model
-// table loaded once (the per-tile segment switch of the multi-segment form
-// spilled registers with the float64 decode)
-template <bool IN_F64, bool MULTI>
+// One segment (level 0), its model table loaded once. MODE: the root's
+// classifier -- 0 RMI, 1 linear cell table, 2 binade (log) cell table. The
+// host launches all three; the ones that do not match the model built on the
+// device return at once (one kernel with all three classifiers spilled).
+template <int MODE>
+__device__ __forceinline__ uint32_t direct_classify(const KState& S, uint64_t x) {
+    if constexpr (MODE == 0) return kclassify<kLearned>(S, x);
+    else if constexpr (MODE == 2) return S.rlut[binade_cell(x, S.rtab, (uint32_t)S.rmin, S.rtabn, S.rcells)];
+    else {
+        if (S.shift >= 32) {
+            const uint32_t h = (uint32_t)(x >> 32) >> (S.shift - 32);
+            return S.rlut[h > S.rorg ? min(h - S.rorg, S.rcells - 1) : 0u];
+        }
+        return S.rlut[lut_cell(x, S.rmin, S.shift, S.rcells)];
+    }
+}
+template <bool IN_F64, int MODE>
 __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, DirectWS w) {
     griddep_wait();
     extern __shared__ uint4 smem_u4[];
     DirectSmem& Q = *(DirectSmem*)smem_u4;
     constexpr uint32_t NBC = kDirectMaxBuckets;
     if (*w.ovf || p.ctrl->nan_index != ~0ull) return;
+    {
+        const ModelHdr* h0 = (const ModelHdr*)(p.models + p.segs[0].model_off);
+        const int mode = h0->kind == kRadix ? ((h0->flags & kModelLog) ? 2 : 1) : 0;
+        if (mode != MODE) return;
+    }
     const uint64_t per = (p.ntiles + gridDim.x - 1) / gridDim.x;
     const uint64_t t0 = (uint64_t)blockIdx.x * per;
     const uint64_t t1 = min(t0 + per, p.ntiles);
@@ -982,31 +1008,15 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
     TileGeom gnext = tile_geom_all(p, t0, inext);
     TS.issue(p.src, gnext, 0);
     KState S;
-    int64_t curseg = -1;
-    uint64_t boff = 0;
-    uint32_t nb = 0;
-    bool lutm = false;  // (CTA-uniform) the root is a cell table (GPU policy), else an RMI
-    if (!MULTI) {
-        const ModelHdr* h0 = (const ModelHdr*)(p.models + p.segs[0].model_off);
-        lutm = h0->kind == kRadix;
-        if (lutm) kstate_load<kRadix>(S, p.models + p.segs[0].model_off, Q.table);
-        else kstate_load<kLearned>(S, p.models + p.segs[0].model_off, Q.table);
-        boff = p.segs[0].bucket_off;
-        nb = S.nb;
-    }
+    if (MODE == 0) kstate_load<kLearned>(S, p.models + p.segs[0].model_off, Q.table);
+    else kstate_load<kRadix>(S, p.models + p.segs[0].model_off, Q.table);
+    const uint64_t boff = p.segs[0].bucket_off;
+    const uint32_t nb = S.nb;
     bool ovf = false;
     for (uint64_t tile = t0; tile < t1; ++tile) {
         const int tb = (int)((tile - t0) & 1);
-        const uint32_t si = inext;
         const TileGeom g = gnext;
         uint32_t* cnt = Q.cnt[tb];
-        if (MULTI && (int64_t)si != curseg) {  // (CTA-uniform) the segment's model table into shared memory
-            const SegDesc& sd = p.segs[si];
-            kstate_load<kLearned>(S, p.models + sd.model_off, Q.table);
-            boff = sd.bucket_off;
-            nb = S.nb;
-            curseg = si;
-        }
         TS.wait(g, tb);
         const ulonglong2* sp = TS.buf(tb);
         uint64_t* skeys = (uint64_t*)TS.buf(tb);  // staging reuses the consumed tile buffer
@@ -1043,8 +1053,12 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
         uint32_t code[kPItems];  // bucket << 16 | rank within the tile; ~0 = no key
         {
             uint32_t bk[kPItems];
-            if (lutm) classify16<kRadix>(S, v, bk);
-            else classify16<kLearned>(S, v, bk);
+            if constexpr (MODE == 0) {
+                classify16<kLearned>(S, v, bk);
+            } else {
+#pragma unroll
+                for (int q = 0; q < kPItems; ++q) bk[q] = direct_classify<MODE>(S, (q & 1) ? v[q >> 1].y : v[q >> 1].x);
+            }
 #pragma unroll
             for (int q = 0; q < kPItems; ++q) {
                 const bool ok = threadIdx.x + (q >> 1) * kPNT < g.npairs;
@@ -1062,7 +1076,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
                 if (isnan(d)) atomicMin(&p.ctrl->nan_index, (unsigned long long)ix);
                 k = encode(d);
             }
-            const uint32_t b = lutm ? kclassify<kRadix>(S, k) : kclassify<kLearned>(S, k);
+            const uint32_t b = direct_classify<MODE>(S, k);
             scode = b << 16 | atomicAdd(&cnt[b], 1u);
             skey = k;
         }
@@ -1212,8 +1226,15 @@ void launch_direct(const LevelParams& p, int in_f64, uint64_t root_m, uint64_t a
     const size_t cap_sm = 8 * ((size_t)kDirectMaxBuckets + 2);
     pdl(k_direct_setup<1024>, 1, 1024, cap_sm, st, p, root_m, alloc_keys, w, sigma, slack);
     constexpr size_t sm = sizeof(DirectSmem);
-    if (in_f64) pdl(k_direct<true, false>, grid, kPNT, sm, st, p, w);
-    else pdl(k_direct<false, false>, grid, kPNT, sm, st, p, w);
+    if (in_f64) {
+        pdl(k_direct<true, 1>, grid, kPNT, sm, st, p, w);
+        pdl(k_direct<true, 2>, grid, kPNT, sm, st, p, w);
+        pdl(k_direct<true, 0>, grid, kPNT, sm, st, p, w);
+    } else {
+        pdl(k_direct<false, 1>, grid, kPNT, sm, st, p, w);
+        pdl(k_direct<false, 2>, grid, kPNT, sm, st, p, w);
+        pdl(k_direct<false, 0>, grid, kPNT, sm, st, p, w);
+    }
     pdl(k_direct_children<1024>, p.nsegs, 1024, cap_sm, st, p, w);
 }
 
@@ -1231,8 +1252,12 @@ void partition_init(int optin) {
     allow_smem(k_scatter<false, 1024>, optin);
     allow_smem(k_scatter<true, kMaxNB>, optin);
     allow_smem(k_scatter<false, kMaxNB>, optin);
-    allow_smem(k_direct<true, false>, optin);
-    allow_smem(k_direct<false, false>, optin);
+    allow_smem(k_direct<true, 0>, optin);
+    allow_smem(k_direct<false, 0>, optin);
+    allow_smem(k_direct<true, 1>, optin);
+    allow_smem(k_direct<false, 1>, optin);
+    allow_smem(k_direct<true, 2>, optin);
+    allow_smem(k_direct<false, 2>, optin);
     allow_smem(k_direct_setup<1024>, optin);
     allow_smem(k_direct_children<1024>, optin);
     allow_smem(k_scan_children<128>, optin);

@@ -57,7 +57,7 @@ def main():
             torch.cuda.synchronize()
             ph = ctx.sort(w, cfg)
             print(f"{d:12s} n={n:.0e} [{v or 'default'}] median {np.median(ts):.3f} ms min {min(ts):.3f} ms "
-                  f"-> {n / np.median(ts) / 1e6:.2f} Gkeys/s sorted={ok} levels={ph['levels']} | models "
+                  f"-> {n / np.median(ts) / 1e6:.2f} Gkeys/s sorted={ok} levels={ph['levels']} root={ph['level0_kind']} | models "
                   f"{ph['ms_models']:.3f} classify {ph['ms_classify']:.3f} scatter {ph['ms_scatter']:.3f} "
                   f"base {ph['ms_base']:.3f} fill {ph['ms_fill']:.3f} base_keys={ph['base_case_keys']}", flush=True)
         del p, w
