@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(NT) k_base_smem(const BaseItem* items, const u
     for (uint32_t e = blockIdx.x; e < ni; e += gridDim.x) {
         const BaseItem it = items[e];
         const uint32_t n = (uint32_t)it.n;
-        const uint64_t* g = src + it.begin;
+        const uint64_t* g = src + it.rd;
         // TMA bulk load of the 16-byte aligned interior; head/tail keys by threads
         const uint32_t mis = (uint32_t)(((uintptr_t)g >> 3) & 1);
         const uint32_t head = min(mis, n);
@@ -103,15 +103,15 @@ __global__ void __launch_bounds__(NT, MINB) k_base_reg(const BaseItem* items, co
     const uint32_t ni = min(*count, list_cap);
     // the next segment of this CTA is pulled into L2 while this one sorts
     // (its register loads then wait on L2, not HBM, latency)
-    if (threadIdx.x == 0 && blockIdx.x < ni) l2_prefetch(src + items[blockIdx.x].begin, 8 * items[blockIdx.x].n);
+    if (threadIdx.x == 0 && blockIdx.x < ni) l2_prefetch(src + items[blockIdx.x].rd, 8 * items[blockIdx.x].n);
     for (uint32_t e = blockIdx.x; e < ni; e += gridDim.x) {
         const BaseItem it = items[e];
         const uint32_t n = (uint32_t)it.n;
         if (n <= nmin || n > nmax) continue;
-        uint64_t* g = src + it.begin;
+        uint64_t* g = src + it.rd;
         if (threadIdx.x == 0 && e + gridDim.x < ni) {
             const BaseItem nx = items[e + gridDim.x];
-            if (nx.n > nmin && nx.n <= nmax) l2_prefetch(src + nx.begin, 8 * nx.n);
+            if (nx.n > nmin && nx.n <= nmax) l2_prefetch(src + nx.rd, 8 * nx.n);
         }
         // register array of 1/2, 3/4 or all of CAP / NT keys per thread: every
         // unused slot still issues its predicated loads, digit, rank and placement

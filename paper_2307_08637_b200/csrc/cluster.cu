@@ -155,7 +155,7 @@ __global__ void __cluster_dims__(kClSize, 1, 1) __launch_bounds__(kClNT, 1)
                 if (len <= p.base_cap[2]) {
                     const int c = len <= p.base_cap[0] ? 0 : (len <= p.base_cap[1] ? 1 : 2);
                     const unsigned e = atomicAdd(&p.ctrl->n_base[c], 1u);
-                    if (e < p.list_cap) p.base[c][e] = BaseItem{begin, len};
+                    if (e < p.list_cap) p.base[c][e] = BaseItem{begin, len, (int64_t)begin};
                     else atomicOr(&p.ctrl->err, 2u);
                     atomicAdd(&p.ctrl->keys_base, (unsigned long long)len);
                 } else {

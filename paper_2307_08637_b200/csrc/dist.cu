@@ -571,7 +571,7 @@ void dist_sort(lsort_dist* D, void* keys, uint64_t n, int key_kind, void* out, u
             big.push_back(SegPlan{pc.at, pc.n, 1, 0, ps});
         } else {
             const int c = pc.n <= cls_cap[0] ? 0 : (pc.n <= cls_cap[1] ? 1 : 2);
-            small[c].push_back(BaseItem{pc.at, pc.n});
+            small[c].push_back(BaseItem{pc.at, pc.n, (int64_t)pc.at});
         }
     }
     if (stats) {

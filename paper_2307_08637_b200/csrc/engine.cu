@@ -908,7 +908,7 @@ int lsort_cuda_sort_buckets(lsort_ctx* C, void* d_keys, uint64_t n, int key_kind
                 big.push_back({at, len, 1, 0, ps});
             } else if (len > 1 || (len == 1 && f64)) {
                 const int c = len <= cls_cap[0] ? 0 : (len <= cls_cap[1] ? 1 : 2);
-                small[c].push_back(BaseItem{at, len});
+                small[c].push_back(BaseItem{at, len, (int64_t)at});
                 small_keys += len;
             }
             at += len;

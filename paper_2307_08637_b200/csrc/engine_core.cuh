@@ -651,7 +651,7 @@ struct Engine {
             for (uint32_t i = 0; i < ns; ++i) {
                 const SegPlan& s = segs[i];
                 if (use_cluster && s.n > cap && s.n <= kClCap) {
-                    clus.push_back(BaseItem{s.begin, s.n});
+                    clus.push_back(BaseItem{s.begin, s.n, (int64_t)s.begin});
                     continue;
                 }
                 const uint32_t j = (uint32_t)psegs.size();
@@ -831,7 +831,7 @@ struct Engine {
                 if (timing) CU(cudaEventRecord(C->pev[6], st));
                 launch_direct(pd, src_f64, root_m, alloc, C->dws.p, nbuckets,
                               (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM), st,
-                              (cfg.flags & LSORT_FLAG_TEST_DIRECT_OVERFLOW) != 0);
+                              (cfg.flags & LSORT_FLAG_TEST_DIRECT_OVERFLOW) != 0, dst);
                 if (timing) CU(cudaEventRecord(C->pev[7], st));
                 launched(6);
                 p.gate = &dctrl->run_exact;

@@ -34,6 +34,8 @@ struct SegOut {
 };
 struct BaseItem {
     uint64_t begin, n;
+    int64_t rd;  // read position, relative to the base kernels' source pointer (== begin
+                 // except for the children of the padded one-pass level 0)
 };
 struct FillItem {
     uint64_t begin, n, value, pad;
@@ -180,10 +182,12 @@ void launch_scatter(const LevelParams& p, int in_f64, uint32_t nb_cap, int grid,
 size_t direct_workspace_bytes(uint64_t slots, uint32_t nsegs);
 // the one-pass level's outcome flag in its workspace (2: ineligible, 1: a region overflowed)
 const uint32_t* direct_flag_ptr(const void* dw, uint64_t slots, uint32_t nsegs);
-constexpr uint64_t kDirectMinPerBucket = 65536;  // mean keys per root bucket for the padded level 0
+constexpr uint64_t kDirectMinPerBucket = 4096;   // mean keys per root bucket for the padded level 0
 constexpr uint32_t kDirectMaxBuckets = 1024;     // buckets per segment a one-pass level handles
+// base_src: the source pointer the level's base-case kernels are launched with (the
+// direct children that go to the base cases read p.dst through it)
 void launch_direct(const LevelParams& p, int in_f64, uint64_t root_m, uint64_t alloc_keys, void* dw, uint64_t slots,
-                   int grid, cudaStream_t st, bool test_overflow = false);
+                   int grid, cudaStream_t st, bool test_overflow, const uint64_t* base_src);
 // bound on one segment's padded output: n keys, a model sample of m, nb buckets
 uint64_t direct_capacity_bound(uint64_t n, uint64_t m, uint32_t nb);
 // basecase.cu

@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(NT) k_scan_children(LevelParams p) {
                 if (e < p.list_cap) p.fill[e] = FillItem{begin, len, eqval[b], 0};
                 else atomicOr(&p.ctrl->err, 1u);
             } else if (cls < 4) {
-                if (e < p.list_cap) p.base[cls - 1][e] = BaseItem{begin, len};
+                if (e < p.list_cap) p.base[cls - 1][e] = BaseItem{begin, len, (int64_t)begin};
                 else atomicOr(&p.ctrl->err, 2u);
             } else {
                 const uint32_t depth = sd.depth + 1;
@@ -1165,10 +1165,12 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
 // one-pass level only runs with >= 64 Ki keys per bucket on average. Otherwise
 // the exact two-pass level runs (Ctrl::run_exact).
 template <int NT>
-__global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS w) {
+__global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS w, int64_t base_delta) {
     griddep_wait();
     __shared__ uint64_t wsum[NT / 32 + 1];
     __shared__ uint32_t lbase;
+    __shared__ uint32_t lcount[3], gbase[3];
+    __shared__ unsigned long long lkeys;
     extern __shared__ uint64_t cntv[];  // nb + 1
     if (p.ctrl->nan_index != ~0ull) return;
     if (*w.ovf) {
@@ -1181,9 +1183,14 @@ __global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS 
     for (uint32_t b = threadIdx.x; b < nb; b += NT) cntv[b] = w.cur[sd.bucket_off + b] - w.base[sd.bucket_off + b];
     __syncthreads();
     block_exclusive_scan_u64<NT>(cntv, nb, wsum);
-    if (threadIdx.x == 0) lbase = 0;
+    if (threadIdx.x == 0) { lbase = 0; lkeys = 0; }
+    if (threadIdx.x < 3) lcount[threadIdx.x] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    // children of at most the base-case capacity go straight to the base cases
+    // (read at the padded base through base_delta: BaseItem::rd is relative to
+    // the base kernels' source pointer), the rest become level-1 segments
     for (uint32_t b0 = 0; b0 < nb; b0 += NT) {  // CTA-uniform rounds
         const uint32_t b = b0 + threadIdx.x;
         uint64_t st = 0, len = 0;
@@ -1191,36 +1198,63 @@ __global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS 
             st = cntv[b];
             len = (b + 1 < nb ? cntv[b + 1] : sd.n) - st;
         }
-        const unsigned m = __ballot_sync(FULL_MASK, len > 0);
+        const int cls = len == 0 ? -1 : (len <= p.base_cap[2] ? (len <= p.base_cap[0] ? 0 : (len <= p.base_cap[1] ? 1 : 2)) : 3);
+        const unsigned m = __ballot_sync(FULL_MASK, cls == 3);
         uint32_t wb = 0;
         if (lane == 0 && m) wb = atomicAdd(&lbase, (uint32_t)__popc(m));
         wb = __shfl_sync(FULL_MASK, wb, 0);
-        __syncthreads();
-        if (len) {
-            const uint32_t e0 = wb + __popc(m & ((1u << lane) - 1u));
-            {
-                uint64_t ps = 0;
-                if (p.slices) {
-                    const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
-                    if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
-                }
-                const uint32_t depth = sd.depth + 1;
-                const uint32_t flags = (len == sd.n || depth > p.depth_cap) ? kSegForceRadix : 0u;
-                const uint32_t e = p.ctrl->n_rec + e0;  // (one segment: the list starts empty)
-                if (e < p.list_cap) p.rec[e] = SegOut{sd.begin + st, len, depth, flags, ps, w.base[sd.bucket_off + b]};
-                else atomicOr(&p.ctrl->err, 4u);
+        uint32_t li = 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const unsigned mc = __ballot_sync(FULL_MASK, cls == c);
+            if (mc) {
+                const int leader = __ffs(mc) - 1;
+                uint32_t base = 0;
+                if (lane == leader) base = atomicAdd(&lcount[c], (uint32_t)__popc(mc));
+                base = __shfl_sync(FULL_MASK, base, leader);
+                if (cls == c) li = base + __popc(mc & lt);
             }
         }
+        unsigned long long kb = (cls >= 0 && cls < 3) ? (unsigned long long)len : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) kb += __shfl_xor_sync(FULL_MASK, kb, o);
+        if (lane == 0 && kb) atomicAdd(&lkeys, kb);
+        __syncthreads();
+        if (threadIdx.x < 3) {
+            const uint32_t c = lcount[threadIdx.x];
+            gbase[threadIdx.x] = c ? atomicAdd(&p.ctrl->n_base[threadIdx.x], c) : 0u;
+            lcount[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        if (cls == 3) {
+            const uint32_t e0 = wb + __popc(m & lt);
+            uint64_t ps = 0;
+            if (p.slices) {
+                const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
+                if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
+            }
+            const uint32_t depth = sd.depth + 1;
+            const uint32_t flags = (len == sd.n || depth > p.depth_cap) ? kSegForceRadix : 0u;
+            const uint32_t e = p.ctrl->n_rec + e0;  // (one segment: the list starts empty)
+            if (e < p.list_cap) p.rec[e] = SegOut{sd.begin + st, len, depth, flags, ps, w.base[sd.bucket_off + b]};
+            else atomicOr(&p.ctrl->err, 4u);
+        } else if (cls >= 0) {
+            const uint32_t e = gbase[cls] + li;
+            if (e < p.list_cap)
+                p.base[cls][e] = BaseItem{sd.begin + st, len, base_delta + (int64_t)w.base[sd.bucket_off + b]};
+            else atomicOr(&p.ctrl->err, 2u);
+        }
+        __syncthreads();
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
         p.ctrl->n_rec += lbase;
-        p.ctrl->keys_rec += sd.n;
+        p.ctrl->keys_base += lkeys;
+        p.ctrl->keys_rec += sd.n - lkeys;
     }
 }
 
 void launch_direct(const LevelParams& p, int in_f64, uint64_t root_m, uint64_t alloc_keys, void* dw, uint64_t slots,
-                   int grid, cudaStream_t st, bool test_overflow) {
+                   int grid, cudaStream_t st, bool test_overflow, const uint64_t* base_src) {
     const DirectWS w = direct_ws(dw, slots, p.nsegs);
     const double sigma = test_overflow ? -kDirectSigma : kDirectSigma, slack = test_overflow ? 0.0 : kDirectSlack;
     const size_t cap_sm = 8 * ((size_t)kDirectMaxBuckets + 2);
@@ -1235,7 +1269,7 @@ void launch_direct(const LevelParams& p, int in_f64, uint64_t root_m, uint64_t a
         pdl(k_direct<false, 2>, grid, kPNT, sm, st, p, w);
         pdl(k_direct<false, 0>, grid, kPNT, sm, st, p, w);
     }
-    pdl(k_direct_children<1024>, p.nsegs, 1024, cap_sm, st, p, w);
+    pdl(k_direct_children<1024>, p.nsegs, 1024, cap_sm, st, p, w, (int64_t)(p.dst - base_src));
 }
 
 // ------------------------------------------------------------- launchers
