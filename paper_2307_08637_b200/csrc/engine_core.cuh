@@ -537,7 +537,7 @@ struct Engine {
             uint32_t* train_gate = (uint32_t*)(N->lutws.as<uint8_t>() + root_lut_workspace_bytes());
             static const bool no_log = getenv("LSORT_NO_LOG_LUT") != nullptr;
             launch_root_lut(N->sample.as<uint64_t>(), s2, C->models.as<uint8_t>() + hseg.model_off, N->lutws.p, gate,
-                            train_gate, st, f64 && !no_log);
+                            train_gate, st, f64 && !no_log, n < kBigRootMinKeys);
             launched(f64 && !no_log ? 6 : 2);
             tgate = train_gate;
         }

@@ -158,9 +158,11 @@ size_t quality_workspace_bytes();
 // table balances its sorted sample within 2x the mean bucket (models.cu)
 size_t root_lut_workspace_bytes();
 // (before the RMI training, which runs gated on *train_gate: skipped when the table is accepted)
-// log_table: when the linear table is rejected, also try a binade-indexed one (float keys)
+// log_table: also try a binade-indexed table (float keys) -- first when log_first (a
+// linear table classifies faster, a log table is accepted more often), else when
+// the linear one is rejected
 void launch_root_lut(const uint64_t* sorted, uint64_t s, uint8_t* model, void* ws, const uint32_t* gate,
-                     uint32_t* train_gate, cudaStream_t st, bool log_table);
+                     uint32_t* train_gate, cudaStream_t st, bool log_table, bool log_first);
 // offsets[b] = first index of the sorted sample whose bucket (under `model`) is >= b, b <= nb
 void launch_sample_slices(const uint64_t* sorted, uint64_t s, const uint8_t* model, uint32_t* offsets,
                           uint32_t nb_cap, const uint32_t* gate, cudaStream_t st);

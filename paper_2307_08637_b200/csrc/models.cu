@@ -1194,19 +1194,27 @@ size_t root_lut_workspace_bytes() {
 }
 
 void launch_root_lut(const uint64_t* sorted, uint64_t s, uint8_t* model, void* ws, const uint32_t* gate,
-                     uint32_t* train_gate, cudaStream_t st, bool log_table) {
+                     uint32_t* train_gate, cudaStream_t st, bool log_table, bool log_first) {
     const int g = (int)(kRootLutCells / 256);
-    pdl(k_lut_ranks, g, 256, 0, st, sorted, (uint32_t)s, (const uint8_t*)model, (uint32_t*)ws, gate);
     const LogWS w = log_ws(ws);
-    pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)ws, gate, train_gate, w, 0u);
-    if (!log_table) return;
-    // the linear table rejected (train_gate still 1): a binade-indexed one
     const int gs = (int)std::min<uint64_t>((s + 2047) / 2048, (uint64_t)num_sms() * 2);
-    pdl(k_binade_starts, gs, 256, 0, st, sorted, (uint32_t)s, w, (const uint32_t*)train_gate);
-    pdl(k_log_tab, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, w, (const uint32_t*)train_gate);
-    pdl(k_lut_fill, gs, 256, 0, st, sorted, (uint32_t)s, w, (const uint32_t*)train_gate);
-    pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)w.R,
-        (const uint32_t*)train_gate, train_gate, w, 1u);
+    auto log_try = [&](const uint32_t* gt) {  // gt: run only while *gt != 0
+        pdl(k_binade_starts, gs, 256, 0, st, sorted, (uint32_t)s, w, gt);
+        pdl(k_log_tab, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, w, gt);
+        pdl(k_lut_fill, gs, 256, 0, st, sorted, (uint32_t)s, w, gt);
+        pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)w.R, gt, train_gate, w, 1u);
+    };
+    auto lin_try = [&](const uint32_t* gt) {
+        pdl(k_lut_ranks, g, 256, 0, st, sorted, (uint32_t)s, (const uint8_t*)model, (uint32_t*)ws, gt);
+        pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)ws, gt, train_gate, w, 0u);
+    };
+    if (log_table && log_first) {
+        log_try(gate);
+        lin_try(train_gate);  // (the log table rejected: train_gate still 1)
+        return;
+    }
+    lin_try(gate);
+    if (log_table) log_try(train_gate);  // the linear table rejected (train_gate still 1)
 }
 
 // Bucket boundaries in a sorted sample (monotone bucket function): element i
