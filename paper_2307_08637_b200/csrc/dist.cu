@@ -461,7 +461,7 @@ void dist_sort(lsort_dist* D, void* keys, uint64_t n, int key_kind, void* out, u
     p.ktp = C->ktp.as<uint64_t>();
     p.kplan = C->kplan.as<KindPlan>();
     p.kstride = 1;
-    p.remote = world > 1 ? 1u : 0u;
+    p.remote = 1u;  // cursors preset by the rank plan (no k_scan_children); peers' buffers for world > 1
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)num_sms() * kPartPerSM));
     if (n) {
         launch_kind_plan(p, st);

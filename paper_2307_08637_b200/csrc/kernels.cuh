@@ -88,8 +88,8 @@ struct LevelParams {
     uint64_t* ktp;                 // [3][kstride+1] tile prefixes per kind
     KindPlan* kplan;               // [3]
     uint32_t kstride;
-    uint32_t remote;               // k_scatter: cursors address peer GPUs' receive buffers
-                                   // (multi-GPU exchange fused into the scatter, dist.cu)
+    uint32_t remote;               // k_scatter: cursors preset by the multi-GPU rank plan, addressing
+                                   // peer GPUs' receive buffers (exchange fused into the scatter, dist.cu)
 };
 
 // Sort configuration as seen by kernels.

@@ -684,6 +684,9 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
     ScatterSmem<NBC>& Q = *(ScatterSmem<NBC>*)smem_u4;
     if (p.ctrl->nan_index != ~0ull) return;
     if (p.gate && *p.gate == 0) return;
+    // every child of the level is an equality fill (k_scan_children's key counters):
+    // nothing moves (duplicate-heavy levels, e.g. rootdups' level 1)
+    if (!p.remote && p.ctrl->keys_base + p.ctrl->keys_rec == 0) return;
     const uint64_t per = (p.ntiles + gridDim.x - 1) / gridDim.x;
     const uint64_t t0 = (uint64_t)blockIdx.x * per;
     const uint64_t t1 = min(t0 + per, p.ntiles);
