@@ -380,7 +380,9 @@ struct SmemSort {
         for (int i = 0; i < IT; ++i) {
             dg[i] = (uint32_t)((k[i] - base) >> shift);
         }
-        sort_digits<IT, SM, true>(k, dg, n, nb, S, scratch);
+        // shift 0: a digit is one key value -- keys sharing a digit are equal and need
+        // no fix-up (duplicate-heavy small-range integer segments)
+        sort_digits<IT, SM, true>(k, dg, n, nb, S, scratch, shift == 0);
     }
 
     // Counting pass on caller-supplied digits (dg[i] < nb <= NBMAX, monotone in
@@ -389,7 +391,7 @@ struct SmemSort {
     // ZEROED: the caller zeroed hist[0, roundup4(nb)) before a barrier it has passed
     template <int IT = ITEMS, class SM, bool ZEROED = false>
     __device__ static void sort_digits(uint64_t (&k)[IT], const uint32_t (&dg)[IT], uint32_t n, uint32_t nb,
-                                       SM& S, uint64_t* scratch) {
+                                       SM& S, uint64_t* scratch, bool exact = false) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         uint64_t* B = S.B;
         nb = (nb + 3) & ~3u;  // whole 16-byte groups for the vectorised scan (extra digits stay empty)
@@ -451,7 +453,7 @@ struct SmemSort {
             uint32_t run = (uint32_t)ex & 0xffffu, p4 = (uint32_t)(ex >> 16) & 0xffffu,
                      p16 = (uint32_t)(ex >> 32) & 0xffffu;
             auto place = [&](uint32_t d, uint32_t h, uint32_t at) {
-                if (h < 2) return;  // the common case: empty / single-key digit
+                if (h < 2 || exact) return;  // the common case: empty / single-key digit (exact: all equal)
                 if (h <= 4) S.R[p4++] = (uint16_t)d;  // digit index (< NBMAX <= 65536)
                 else if (h <= (uint32_t)kSmall) S.R[kR - 1 - (p16++)] = (uint16_t)d;
                 else push(S, at, h);
@@ -491,6 +493,7 @@ struct SmemSort {
         __syncthreads();
         // collision digits: 2..4 keys by a fixed 4-key network (pad ~0),
         // 5..kSmall keys by insertion sort (rare); all lanes on list entries
+        if (exact) n4 = n16 = 0;  // (CTA-uniform) equal keys: nothing to fix
         for (uint32_t e = tid; e < n4; e += NT) {
             const uint32_t d = S.R[e], s0 = S.hist[d], c = S.hist[d + 1] - s0;
             uint64_t x0 = B[s0], x1 = B[s0 + 1];
