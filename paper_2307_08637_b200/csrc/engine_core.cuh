@@ -484,7 +484,7 @@ struct Engine {
         else
             launch_gather(dseg, src, f64, seed, 0, s1, N->fsample.as<uint64_t>(), nullptr, st);
         launch_first_sample(dseg, src, f64, C->models.as<uint8_t>(), dc, N->models.as<uint8_t>(), k, gate, st,
-                            N->fsample.as<uint64_t>());
+                            N->fsample.as<uint64_t>(), given_sample ? nullptr : slices);
         launched();
         CU(cudaStreamWaitEvent(st, N->bev[1], 0));
         // one distribution level over the sample with the first-sample tree
@@ -817,7 +817,10 @@ struct Engine {
             uint64_t root_m = 0, alloc = 0;
             if (direct0) {
                 root_m = root_rmi_sample(n);
-                alloc = direct_capacity_bound(n, root_m, hs[0].nb_max);
+                // (a splitter-tree root sizes its regions from the smaller first sample)
+                alloc = direct_capacity_bound(
+                    n, std::min<uint64_t>(root_m, sample_size_host(cfg.sample_fraction, cfg.first_sample_cap, n)),
+                    hs[0].nb_max);
                 // (level 1 reads this padded output: its bucket ids are indexed by read position)
                 if (!C->scratch2.ensure(8 * alloc) || !C->ids.ensure(2 * alloc))
                     throw LsortError{LSORT_ENOMEM, "one-pass level 0"};
@@ -833,7 +836,7 @@ struct Engine {
                               (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM), st,
                               (cfg.flags & LSORT_FLAG_TEST_DIRECT_OVERFLOW) != 0, dst);
                 if (timing) CU(cudaEventRecord(C->pev[7], st));
-                launched(6);
+                launched(7);
                 p.gate = &dctrl->run_exact;
             }
             p.ids = C->ids.as<uint16_t>();  // (the one-pass setup may have grown the id array)

@@ -139,9 +139,11 @@ constexpr uint32_t kModelSmallCap = 2048;    // samples of the small model CTA
 void launch_build_models(const SegDesc* segs, const uint32_t* idx, uint32_t count, const void* src,
                          int in_f64, uint8_t* models, const DevCfg& cfg, int mid, cudaStream_t st);
 // pre (nullable): the first sample already gathered (launch_gather draws [0, s1))
+// dslices (nullable): when the policy builds a splitter tree (dup-heavy root), its
+// buckets' offsets in the sorted first sample (the one-pass level 0 sizes regions from them)
 void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_t* models,
                          const DevCfg& cfg, uint8_t* aux, uint32_t aux_budget, uint32_t* gate,
-                         cudaStream_t st, const uint64_t* pre = nullptr);
+                         cudaStream_t st, const uint64_t* pre = nullptr, uint32_t* dslices = nullptr);
 void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0,
                    uint64_t s, uint64_t* out, const uint32_t* gate, cudaStream_t st);
 size_t train_workspace_bytes(uint64_t s, uint32_t B);

@@ -482,7 +482,7 @@ __device__ void sample_sorted(const SegDesc& sd, const void* src, uint64_t seed,
 template <bool IN_F64, class MC>
 __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* models, const DevCfg& cfg,
                                 typename MC::Smem& S, bool first_only, uint8_t* aux, uint32_t aux_budget,
-                                uint32_t* gate, const uint64_t* pre = nullptr) {
+                                uint32_t* gate, const uint64_t* pre = nullptr, uint32_t* dslices = nullptr) {
     constexpr int NT = sizeof(S.red64) / 8 * 32;
     ModelHdr* h = (ModelHdr*)(models + sd.model_off);
     uint8_t* payload = models + sd.model_off + sizeof(ModelHdr);
@@ -572,6 +572,19 @@ __device__ void build_model_cta(const SegDesc& sd, const void* src, uint8_t* mod
     } else {
         if (threadIdx.x == 0) h->s2 = 0;
         tree_build_block<NT>(A, s1, sd.tree_k, true, h, payload, S.u.tree.scratch, S.u.tree.wsum, S.u.tree.spl);
+        if (dslices) {  // a tree root: its buckets' offsets in the sorted first sample (one-pass level 0)
+            __syncthreads();
+            const MView m = model_view((const uint8_t*)h);
+            const ModelHdr& th = *m.h;
+            auto bk = [&](uint64_t x) {
+                return tree_bucket(th.levels, th.leaf_origin, th.nsplit, m.tree, m.spl, m.eqo, x) & 0x7fffffffu;
+            };
+            for (uint32_t i = threadIdx.x; i <= s1; i += NT) {
+                const uint32_t b = i < s1 ? bk(A[i]) : th.nbuckets;
+                const uint32_t lo = i ? bk(A[i - 1]) + 1 : 0u;
+                for (uint32_t q = lo; q <= b; ++q) dslices[q] = i;
+            }
+        }
     }
 }
 
@@ -587,12 +600,13 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) k_build_models(const Se
 
 template <bool IN_F64>
 __global__ void __launch_bounds__(512, 1) k_first_sample(const uint64_t* pre, const SegDesc* seg, const void* src, uint8_t* models,
-                                                     DevCfg cfg, uint8_t* aux, uint32_t aux_budget, uint32_t* gate) {
+                                                     DevCfg cfg, uint8_t* aux, uint32_t aux_budget, uint32_t* gate,
+                                                     uint32_t* dslices) {
     griddep_wait();
     extern __shared__ uint4 smem_u4[];
     ModelMid::Smem& S = *(ModelMid::Smem*)smem_u4;
     const SegDesc sd = *seg;
-    build_model_cta<IN_F64, ModelMid>(sd, src, models, cfg, S, true, aux, aux_budget, gate, pre);
+    build_model_cta<IN_F64, ModelMid>(sd, src, models, cfg, S, true, aux, aux_budget, gate, pre, dslices);
 }
 
 template <bool IN_F64>
@@ -1282,10 +1296,11 @@ void launch_build_models(const SegDesc* segs, const uint32_t* idx, uint32_t coun
 }
 
 void launch_first_sample(const SegDesc* seg, const void* src, int in_f64, uint8_t* models, const DevCfg& cfg,
-                         uint8_t* aux, uint32_t aux_budget, uint32_t* gate, cudaStream_t st, const uint64_t* pre) {
+                         uint8_t* aux, uint32_t aux_budget, uint32_t* gate, cudaStream_t st, const uint64_t* pre,
+                         uint32_t* dslices) {
     size_t sm = sizeof(ModelMid::Smem);
-    if (in_f64) pdl(k_first_sample<true>, 1, 512, sm, st, pre, seg, src, models, cfg, aux, aux_budget, gate);
-    else pdl(k_first_sample<false>, 1, 512, sm, st, pre, seg, src, models, cfg, aux, aux_budget, gate);
+    if (in_f64) pdl(k_first_sample<true>, 1, 512, sm, st, pre, seg, src, models, cfg, aux, aux_budget, gate, dslices);
+    else pdl(k_first_sample<false>, 1, 512, sm, st, pre, seg, src, models, cfg, aux, aux_budget, gate, dslices);
 }
 
 void launch_gather(const SegDesc* seg, const void* src, int in_f64, uint64_t seed, uint64_t j0, uint64_t s,

@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(NT) k_scan_children(LevelParams p) {
                 const uint32_t depth = sd.depth + 1;
                 const uint32_t flags = (len == sd.n || depth > p.depth_cap) ? kSegForceRadix : 0u;
                 uint64_t ps = 0;
-                if (p.slices) {
+                if (p.slices && h.kind != kTree) {  // (a tree root's offsets index its first sample)
                     const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
                     if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
                 }
@@ -898,6 +898,8 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
 // number of learned segments (bucket slots at SegDesc::bucket_off).
 constexpr double kDirectSigma = 6.0, kDirectSlack = 8.0;
 
+constexpr size_t kDirectTableBytes = 20 * kDirectMaxBuckets > 2 * kRootLutCells ? 20 * kDirectMaxBuckets : 2 * kRootLutCells;
+
 struct DirectWS {
     unsigned long long* cur;     // [slots] claim cursors (absolute positions in the padded output)
     unsigned long long* base;    // [slots] region starts
@@ -936,12 +938,16 @@ __global__ void __launch_bounds__(NT) k_direct_setup(LevelParams p, uint64_t roo
     const ModelHdr* h = (const ModelHdr*)(p.models + sd.model_off);
     const uint32_t nb = h->nbuckets;
     const bool lutm = h->kind == kRadix && (h->flags & kModelLut);  // a root cell table
-    if ((h->kind != kLearned && !lutm) || root_m == 0 || nb > kDirectMaxBuckets ||
-        (!lutm && h->B > kDirectMaxBuckets) || !p.slices) {
+    // a splitter-tree root (dup-heavy policy): regions from its first sample, if the tree
+    // and its lookup table fit k_direct's table space
+    const bool treem = h->kind == kTree && h->s1 >= 2 &&
+                       ((tree_payload_bytes(h->leaf_origin, h->nsplit) + 15) & ~15ull) + kLutBytes <= kDirectTableBytes;
+    if ((h->kind != kLearned && !lutm && !treem) || root_m == 0 || nb > kDirectMaxBuckets ||
+        (h->kind == kLearned && h->B > kDirectMaxBuckets) || !p.slices) {
         if (threadIdx.x == 0) *w.ovf = 2u;  // not eligible: the exact level runs
         return;
     }
-    const double r = (double)sd.n / (double)root_m;
+    const double r = (double)sd.n / (double)(treem ? h->s1 : root_m);
     for (uint32_t b = threadIdx.x; b < nb; b += NT) {
         const double c = (double)(p.slices[b + 1] - p.slices[b]);
         const double e = c + sigma * sqrt(c) + slack;
@@ -966,8 +972,9 @@ struct DirectSmem {
     alignas(16) uint32_t cnt[2][kDirectMaxBuckets + 4];
     uint16_t sbid[kTileKeys];
     uint32_t wsum[kPNT / 32 + 1];
-    // the segment model's compiled table or cell table (kstate_load)
-    alignas(16) uint8_t table[20 * kDirectMaxBuckets > 2 * kRootLutCells ? 20 * kDirectMaxBuckets : 2 * kRootLutCells];
+    // the segment model's compiled table, cell table, or splitter tree + its lookup table (kstate_load)
+    alignas(16) uint8_t table[kDirectTableBytes];
+    uint8_t iseq[kDirectMaxBuckets];  // tree roots: equality buckets (their keys are counted, not moved)
 };
 
 static_assert(sizeof(DirectSmem) + 1024 <= 233472 / kPartPerSM, "one-pass level: kPartPerSM CTAs per SM");
@@ -979,6 +986,7 @@ static_assert(sizeof(DirectSmem) + 1024 <= 233472 / kPartPerSM, "one-pass level:
 template <int MODE>
 __device__ __forceinline__ uint32_t direct_classify(const KState& S, uint64_t x) {
     if constexpr (MODE == 0) return kclassify<kLearned>(S, x);
+    else if constexpr (MODE == 3) return kclassify<kTree>(S, x) & 0x7fffffffu;
     else if constexpr (MODE == 2) return S.rlut[binade_cell(x, S.rtab, (uint32_t)S.rmin, S.rtabn, S.rcells)];
     else {
         if (S.shift >= 32) {
@@ -997,7 +1005,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
     if (*w.ovf || p.ctrl->nan_index != ~0ull) return;
     {
         const ModelHdr* h0 = (const ModelHdr*)(p.models + p.segs[0].model_off);
-        const int mode = h0->kind == kRadix ? ((h0->flags & kModelLog) ? 2 : 1) : 0;
+        const int mode = h0->kind == kRadix ? ((h0->flags & kModelLog) ? 2 : 1) : (h0->kind == kTree ? 3 : 0);
         if (mode != MODE) return;
     }
     const uint64_t per = (p.ntiles + gridDim.x - 1) / gridDim.x;
@@ -1011,8 +1019,21 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
     TileGeom gnext = tile_geom_all(p, t0, inext);
     TS.issue(p.src, gnext, 0);
     KState S;
-    if (MODE == 0) kstate_load<kLearned>(S, p.models + p.segs[0].model_off, Q.table);
-    else kstate_load<kRadix>(S, p.models + p.segs[0].model_off, Q.table);
+    if constexpr (MODE == 3) {  // splitter tree + its lookup table; equality buckets flagged
+        __shared__ uint32_t lut_red;
+        const ModelHdr* th = (const ModelHdr*)(p.models + p.segs[0].model_off);
+        const size_t tb = (tree_payload_bytes(th->leaf_origin, th->nsplit) + 15) & ~15ull;
+        kstate_load<kTree>(S, p.models + p.segs[0].model_off, Q.table, (uint16_t*)(Q.table + tb), &lut_red);
+        for (uint32_t b = threadIdx.x; b < kDirectMaxBuckets; b += kPNT) Q.iseq[b] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < S.nsplit; i += kPNT)
+            if (S.eqo[i + 1] - S.eqo[i] > 1) Q.iseq[S.eqo[i] + 1] = 1;
+        __syncthreads();
+    } else if constexpr (MODE == 0) {
+        kstate_load<kLearned>(S, p.models + p.segs[0].model_off, Q.table);
+    } else {
+        kstate_load<kRadix>(S, p.models + p.segs[0].model_off, Q.table);
+    }
     const uint64_t boff = p.segs[0].bucket_off;
     const uint32_t nb = S.nb;
     bool ovf = false;
@@ -1058,6 +1079,10 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
             uint32_t bk[kPItems];
             if constexpr (MODE == 0) {
                 classify16<kLearned>(S, v, bk);
+            } else if constexpr (MODE == 3) {
+                classify16<kTree>(S, v, bk);
+#pragma unroll
+                for (int q = 0; q < kPItems; ++q) bk[q] &= 0x7fffffffu;
             } else {
 #pragma unroll
                 for (int q = 0; q < kPItems; ++q) bk[q] = direct_classify<MODE>(S, (q & 1) ? v[q >> 1].y : v[q >> 1].x);
@@ -1144,7 +1169,9 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
         for (int q = 0; q < kPer; ++q) {
             const bool full = ccnt[q] && got[q] + ccnt[q] > lim[q];  // region full: nothing of this run is written
             ovf |= full;
-            Q.delta[threadIdx.x + q * kPNT] = full ? LLONG_MIN : (long long)got[q] - (long long)cstart[q];
+            // (tree roots: an equality bucket's keys are counted by its claims, filled later)
+            const bool skip = full || (MODE == 3 && Q.iseq[threadIdx.x + q * kPNT]);
+            Q.delta[threadIdx.x + q * kPNT] = skip ? LLONG_MIN : (long long)got[q] - (long long)cstart[q];
         }
         __syncthreads();  // (4)
 #pragma unroll
@@ -1172,8 +1199,10 @@ __global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS 
     griddep_wait();
     __shared__ uint64_t wsum[NT / 32 + 1];
     __shared__ uint32_t lbase;
-    __shared__ uint32_t lcount[3], gbase[3];
-    __shared__ unsigned long long lkeys;
+    __shared__ uint32_t lcount[4], gbase[4];
+    __shared__ unsigned long long lkeys, lfill;
+    __shared__ uint8_t iseqs[kDirectMaxBuckets];
+    __shared__ uint64_t eqvs[kDirectMaxBuckets];
     extern __shared__ uint64_t cntv[];  // nb + 1
     if (p.ctrl->nan_index != ~0ull) return;
     if (*w.ovf) {
@@ -1186,8 +1215,20 @@ __global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS 
     for (uint32_t b = threadIdx.x; b < nb; b += NT) cntv[b] = w.cur[sd.bucket_off + b] - w.base[sd.bucket_off + b];
     __syncthreads();
     block_exclusive_scan_u64<NT>(cntv, nb, wsum);
-    if (threadIdx.x == 0) { lbase = 0; lkeys = 0; }
-    if (threadIdx.x < 3) lcount[threadIdx.x] = 0;
+    if (threadIdx.x == 0) { lbase = 0; lkeys = 0; lfill = 0; }
+    if (threadIdx.x < 4) lcount[threadIdx.x] = 0;
+    const ModelHdr* mh = (const ModelHdr*)(p.models + sd.model_off);
+    const bool tree = mh->kind == kTree;  // (its equality buckets become fills; its offsets index the first sample)
+    for (uint32_t b = threadIdx.x; b < kDirectMaxBuckets; b += NT) iseqs[b] = 0;
+    __syncthreads();
+    if (tree) {
+        const MView m = model_view(p.models + sd.model_off);
+        for (uint32_t i = threadIdx.x; i < mh->nsplit; i += NT)
+            if (m.eqo[i + 1] - m.eqo[i] > 1) {
+                iseqs[m.eqo[i] + 1] = 1;
+                eqvs[m.eqo[i] + 1] = m.spl[i];
+            }
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -1201,38 +1242,48 @@ __global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS 
             st = cntv[b];
             len = (b + 1 < nb ? cntv[b + 1] : sd.n) - st;
         }
-        const int cls = len == 0 ? -1 : (len <= p.base_cap[2] ? (len <= p.base_cap[0] ? 0 : (len <= p.base_cap[1] ? 1 : 2)) : 3);
+        const int cls = len == 0 ? -1
+                        : (tree && iseqs[b]) ? 4
+                        : (len <= p.base_cap[2] ? (len <= p.base_cap[0] ? 0 : (len <= p.base_cap[1] ? 1 : 2)) : 3);
         const unsigned m = __ballot_sync(FULL_MASK, cls == 3);
         uint32_t wb = 0;
         if (lane == 0 && m) wb = atomicAdd(&lbase, (uint32_t)__popc(m));
         wb = __shfl_sync(FULL_MASK, wb, 0);
         uint32_t li = 0;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
+        for (int c = 0; c < 5; ++c) {
+            if (c == 3) continue;  // (recursion: lbase above)
             const unsigned mc = __ballot_sync(FULL_MASK, cls == c);
             if (mc) {
                 const int leader = __ffs(mc) - 1;
+                const int slot = c == 4 ? 3 : c;
                 uint32_t base = 0;
-                if (lane == leader) base = atomicAdd(&lcount[c], (uint32_t)__popc(mc));
+                if (lane == leader) base = atomicAdd(&lcount[slot], (uint32_t)__popc(mc));
                 base = __shfl_sync(FULL_MASK, base, leader);
                 if (cls == c) li = base + __popc(mc & lt);
             }
         }
         unsigned long long kb = (cls >= 0 && cls < 3) ? (unsigned long long)len : 0ull;
+        unsigned long long kf = cls == 4 ? (unsigned long long)len : 0ull;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) kb += __shfl_xor_sync(FULL_MASK, kb, o);
+        for (int o = 16; o > 0; o >>= 1) {
+            kb += __shfl_xor_sync(FULL_MASK, kb, o);
+            kf += __shfl_xor_sync(FULL_MASK, kf, o);
+        }
         if (lane == 0 && kb) atomicAdd(&lkeys, kb);
+        if (lane == 0 && kf) atomicAdd(&lfill, kf);
         __syncthreads();
-        if (threadIdx.x < 3) {
+        if (threadIdx.x < 4) {
             const uint32_t c = lcount[threadIdx.x];
-            gbase[threadIdx.x] = c ? atomicAdd(&p.ctrl->n_base[threadIdx.x], c) : 0u;
+            unsigned int* ctr = threadIdx.x == 3 ? &p.ctrl->n_fill : &p.ctrl->n_base[threadIdx.x];
+            gbase[threadIdx.x] = c ? atomicAdd(ctr, c) : 0u;
             lcount[threadIdx.x] = 0;
         }
         __syncthreads();
         if (cls == 3) {
             const uint32_t e0 = wb + __popc(m & lt);
             uint64_t ps = 0;
-            if (p.slices) {
+            if (p.slices && !tree) {
                 const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
                 if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
             }
@@ -1241,6 +1292,10 @@ __global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS 
             const uint32_t e = p.ctrl->n_rec + e0;  // (one segment: the list starts empty)
             if (e < p.list_cap) p.rec[e] = SegOut{sd.begin + st, len, depth, flags, ps, w.base[sd.bucket_off + b]};
             else atomicOr(&p.ctrl->err, 4u);
+        } else if (cls == 4) {  // equality bucket: every key equals the splitter
+            const uint32_t e = gbase[3] + li;
+            if (e < p.list_cap) p.fill[e] = FillItem{sd.begin + st, len, eqvs[b], 0};
+            else atomicOr(&p.ctrl->err, 1u);
         } else if (cls >= 0) {
             const uint32_t e = gbase[cls] + li;
             if (e < p.list_cap)
@@ -1252,7 +1307,8 @@ __global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS 
     if (threadIdx.x == 0) {
         p.ctrl->n_rec += lbase;
         p.ctrl->keys_base += lkeys;
-        p.ctrl->keys_rec += sd.n - lkeys;
+        p.ctrl->keys_fill += lfill;
+        p.ctrl->keys_rec += sd.n - lkeys - lfill;
     }
 }
 
@@ -1267,10 +1323,12 @@ void launch_direct(const LevelParams& p, int in_f64, uint64_t root_m, uint64_t a
         pdl(k_direct<true, 1>, grid, kPNT, sm, st, p, w);
         pdl(k_direct<true, 2>, grid, kPNT, sm, st, p, w);
         pdl(k_direct<true, 0>, grid, kPNT, sm, st, p, w);
+        pdl(k_direct<true, 3>, grid, kPNT, sm, st, p, w);
     } else {
         pdl(k_direct<false, 1>, grid, kPNT, sm, st, p, w);
         pdl(k_direct<false, 2>, grid, kPNT, sm, st, p, w);
         pdl(k_direct<false, 0>, grid, kPNT, sm, st, p, w);
+        pdl(k_direct<false, 3>, grid, kPNT, sm, st, p, w);
     }
     pdl(k_direct_children<1024>, p.nsegs, 1024, cap_sm, st, p, w, (int64_t)(p.dst - base_src));
 }
@@ -1295,6 +1353,8 @@ void partition_init(int optin) {
     allow_smem(k_direct<false, 1>, optin);
     allow_smem(k_direct<true, 2>, optin);
     allow_smem(k_direct<false, 2>, optin);
+    allow_smem(k_direct<true, 3>, optin);
+    allow_smem(k_direct<false, 3>, optin);
     allow_smem(k_direct_setup<1024>, optin);
     allow_smem(k_direct_children<1024>, optin);
     allow_smem(k_scan_children<128>, optin);

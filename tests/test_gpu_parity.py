@@ -578,3 +578,24 @@ def test_cell_table_models(ctx, case):
     st = ctx.sort(d, L.SortConfig(flags=L._native.FLAG_STRICT_POLICY))
     assert st["level0_kind"] != 3
     assert np.array_equal(host_u64(d), exp)
+
+
+@pytest.mark.parametrize("dist_name", ["rootdups", "zipf"])
+def test_padded_level0_tree_root(ctx, dist_name):
+    """Duplicate-heavy roots (Alg. 5 picks the splitter tree) also take the
+    one-pass level 0: regions sized from the tree's buckets in the sorted first
+    sample, equality buckets counted but not moved (filled afterwards); with
+    the test flag the regions overflow and the exact two-pass level runs."""
+    n = 40_000_000
+    x = O.generate(dist_name, n, 3)
+    exp = np.sort(x)
+    d = dev(x)
+    st = ctx.sort(d)
+    assert st["level0_kind"] == 1
+    assert st["direct_keys"] == n
+    assert st["fill_keys"] > 0
+    assert np.array_equal(host_u64(d), exp)
+    d = dev(x)
+    st = ctx.sort(d, L.SortConfig(flags=L._native.FLAG_TEST_DIRECT_OVERFLOW))
+    assert st["direct_keys"] == 0
+    assert np.array_equal(host_u64(d), exp)
