@@ -1043,12 +1043,15 @@ __device__ __forceinline__ void lut_geometry(const uint64_t* s, uint32_t n, uint
     origin = s[0];
     shift = lut_pick_shift(origin, s[n - 1], ncell);
 }
+// skip_sign: float keys whose sample spans both signs -- a linear table over that
+// encoded range (>= 2^63 keys) cannot balance them; only the log table is tried
 __global__ void __launch_bounds__(256) k_lut_ranks(const uint64_t* s, uint32_t n, const uint8_t* model, uint32_t* R,
-                                                   const uint32_t* gate) {
+                                                   const uint32_t* gate, uint32_t skip_sign) {
     griddep_wait();
     if (gated_off(gate)) return;
     const ModelHdr* h = (const ModelHdr*)model;
     if (h->kind != kLearned || n < 2) return;
+    if (skip_sign && ((s[0] ^ s[n - 1]) >> 63)) return;
     const uint32_t ncell = min(kRootLutCells, kLutModelCellsPerBucket * h->B);
     uint64_t origin;
     uint32_t shift;
@@ -1147,7 +1150,7 @@ __global__ void __launch_bounds__(256) k_lut_fill(const uint64_t* s, uint32_t n,
 }
 __global__ void __launch_bounds__(kRootLutNT) k_root_lut(const uint64_t* s, uint32_t n, uint8_t* model,
                                                         const uint32_t* R, const uint32_t* gate, uint32_t* train_gate,
-                                                        LogWS lw, uint32_t logm) {
+                                                        LogWS lw, uint32_t logm, uint32_t skip_sign) {
     griddep_wait();
     __shared__ uint32_t off[LSORT_MAX_RMI_DEV + 1];
     __shared__ uint64_t red[kRootLutNT / 32];
@@ -1158,6 +1161,7 @@ __global__ void __launch_bounds__(kRootLutNT) k_root_lut(const uint64_t* s, uint
     ModelHdr* h = (ModelHdr*)model;
     if (h->kind != kLearned || n < 2) return;
     if (logm && *lw.ncell == 0) return;  // no log table (too many binades or cells)
+    if (!logm && skip_sign && ((s[0] ^ s[n - 1]) >> 63)) return;  // (k_lut_ranks)
     const uint32_t nb = h->nbuckets;
     const uint32_t ncell = logm ? *lw.ncell : min(kRootLutCells, kLutModelCellsPerBucket * h->B);
     uint64_t origin;
@@ -1216,11 +1220,13 @@ void launch_root_lut(const uint64_t* sorted, uint64_t s, uint8_t* model, void* w
         pdl(k_binade_starts, gs, 256, 0, st, sorted, (uint32_t)s, w, gt);
         pdl(k_log_tab, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, w, gt);
         pdl(k_lut_fill, gs, 256, 0, st, sorted, (uint32_t)s, w, gt);
-        pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)w.R, gt, train_gate, w, 1u);
+        pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)w.R, gt, train_gate, w, 1u,
+            0u);
     };
     auto lin_try = [&](const uint32_t* gt) {
-        pdl(k_lut_ranks, g, 256, 0, st, sorted, (uint32_t)s, (const uint8_t*)model, (uint32_t*)ws, gt);
-        pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)ws, gt, train_gate, w, 0u);
+        const uint32_t ss = log_table ? 1u : 0u;
+        pdl(k_lut_ranks, g, 256, 0, st, sorted, (uint32_t)s, (const uint8_t*)model, (uint32_t*)ws, gt, ss);
+        pdl(k_root_lut, 1, kRootLutNT, 0, st, sorted, (uint32_t)s, model, (const uint32_t*)ws, gt, train_gate, w, 0u, ss);
     };
     if (log_table && log_first) {
         log_try(gate);
