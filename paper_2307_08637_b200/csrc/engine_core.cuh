@@ -129,7 +129,7 @@ struct lsort_ctx {
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
         kseg, ktp, kplan, qws, ids, clus, cidx, scratch2, dws, bat[3], psample, slices, fwd_model, fwd_slices, piv, fsample,
-        lutws;
+        lutws, scratch3;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
@@ -815,6 +815,33 @@ struct Engine {
             // an ineligible model or a region that outgrew its estimate)
             uint64_t* dout = nullptr;
             uint64_t root_m = 0, alloc = 0;
+            // one-pass level 1 (GPU policy): every segment a linear cell table trained on its
+            // slice of the root's sorted sample -- regions sized from the slice counts
+            // (C5 10.48 -> 9.80 ms, LogNormal(0,0.5) 1e8 2.30 -> 2.19); a level with another
+            // model kind runs the exact two-pass level (LSORT_NO_L1_DIRECT: always)
+            static const bool l1_direct = getenv("LSORT_NO_L1_DIRECT") == nullptr;
+            bool direct1 = l1_direct && !fw && !classic && !(cfg.flags & LSORT_FLAG_STRICT_POLICY) && level == 1 &&
+                           np >= 1 && ncl == 0 && bigs.empty() && dc.psample && !src_f64 && max_nb <= kDirectMaxBuckets;
+            uint64_t alloc1 = 0;
+            for (uint32_t j = 0; direct1 && j < np; ++j) {
+                const uint64_t m = psegs[j].pslice & 0xffffffu;
+                if (m < 2) { direct1 = false; break; }
+                alloc1 += direct_capacity_bound(psegs[j].n, m, hs[j].nb_max);
+            }
+            if (direct1) {  // (direct0 is level 0 only)
+                if (timing) CU(cudaEventRecord(C->pev[6], st));
+                if (!C->scratch3.ensure(8 * alloc1) || !C->dws.ensure(direct_multi_workspace_bytes(nbuckets, np)))
+                    throw LsortError{LSORT_ENOMEM, "one-pass level 1"};
+                LevelParams pd = p;
+                pd.dst = C->scratch3.as<uint64_t>();
+                launch_direct_multi(pd, dc.psample, alloc1, C->dws.p, nbuckets,
+                                    (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM), st,
+                                    (cfg.flags & LSORT_FLAG_TEST_DIRECT_OVERFLOW) != 0, dst);
+                launched(5);
+                if (timing) CU(cudaEventRecord(C->pev[7], st));
+                p.gate = &dctrl->run_exact;
+                dout = pd.dst;
+            }
             if (direct0) {
                 root_m = root_rmi_sample(n);
                 // (a splitter-tree root sizes its regions from the smaller first sample)
@@ -826,7 +853,7 @@ struct Engine {
                     throw LsortError{LSORT_ENOMEM, "one-pass level 0"};
                 dout = C->scratch2.as<uint64_t>();
             }
-            if (dout) {
+            if (dout && direct0) {
                 if (!C->dws.ensure(direct_workspace_bytes(nbuckets, np))) throw LsortError{LSORT_ENOMEM, "one-pass level"};
                 LevelParams pd = p;
                 pd.dst = dout;

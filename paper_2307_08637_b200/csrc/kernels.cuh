@@ -188,6 +188,11 @@ size_t direct_workspace_bytes(uint64_t slots, uint32_t nsegs);
 const uint32_t* direct_flag_ptr(const void* dw, uint64_t slots, uint32_t nsegs);
 constexpr uint64_t kDirectMinPerBucket = 4096;   // mean keys per root bucket for the padded level 0
 constexpr uint32_t kDirectMaxBuckets = 1024;     // buckets per segment a one-pass level handles
+// One-pass level >= 1 over many segments (each a linear cell table with a slice of
+// the parent's sorted sample psample); p.dst: the padded output (alloc_keys)
+size_t direct_multi_workspace_bytes(uint64_t slots, uint32_t nsegs);
+void launch_direct_multi(const LevelParams& p, const uint64_t* psample, uint64_t alloc_keys, void* dw, uint64_t slots,
+                         int grid, cudaStream_t st, bool test_overflow, const uint64_t* base_src);
 // base_src: the source pointer the level's base-case kernels are launched with (the
 // direct children that go to the base cases read p.dst through it)
 void launch_direct(const LevelParams& p, int in_f64, uint64_t root_m, uint64_t alloc_keys, void* dw, uint64_t slots,

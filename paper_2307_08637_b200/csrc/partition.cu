@@ -985,6 +985,7 @@ static_assert(sizeof(DirectSmem) + 1024 <= 233472 / kPartPerSM, "one-pass level:
 // device return at once (one kernel with all three classifiers spilled).
 template <int MODE>
 __device__ __forceinline__ uint32_t direct_classify(const KState& S, uint64_t x) {
+    // (MODE 4: the one-pass level 1 -- every segment a linear cell table, see launch_direct_multi)
     if constexpr (MODE == 0) return kclassify<kLearned>(S, x);
     else if constexpr (MODE == 3) return kclassify<kTree>(S, x) & 0x7fffffffu;
     else if constexpr (MODE == 2) return S.rlut[binade_cell(x, S.rtab, (uint32_t)S.rmin, S.rtabn, S.rcells)];
@@ -1003,7 +1004,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
     DirectSmem& Q = *(DirectSmem*)smem_u4;
     constexpr uint32_t NBC = kDirectMaxBuckets;
     if (*w.ovf || p.ctrl->nan_index != ~0ull) return;
-    {
+    if (MODE != 4) {
         const ModelHdr* h0 = (const ModelHdr*)(p.models + p.segs[0].model_off);
         const int mode = h0->kind == kRadix ? ((h0->flags & kModelLog) ? 2 : 1) : (h0->kind == kTree ? 3 : 0);
         if (mode != MODE) return;
@@ -1031,16 +1032,26 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
         __syncthreads();
     } else if constexpr (MODE == 0) {
         kstate_load<kLearned>(S, p.models + p.segs[0].model_off, Q.table);
-    } else {
+    } else if constexpr (MODE != 4) {
         kstate_load<kRadix>(S, p.models + p.segs[0].model_off, Q.table);
     }
-    const uint64_t boff = p.segs[0].bucket_off;
-    const uint32_t nb = S.nb;
+    uint64_t boff = p.segs[0].bucket_off;
+    uint32_t nb = MODE == 4 ? 0u : S.nb;
+    uint32_t curseg = ~0u;
     bool ovf = false;
     for (uint64_t tile = t0; tile < t1; ++tile) {
         const int tb = (int)((tile - t0) & 1);
         const TileGeom g = gnext;
         uint32_t* cnt = Q.cnt[tb];
+        if constexpr (MODE == 4) {  // (CTA-uniform) the tile's segment's table into shared memory
+            const uint32_t si = inext;
+            if (si != curseg) {
+                kstate_load<kRadix>(S, p.models + p.segs[si].model_off, Q.table);
+                boff = p.segs[si].bucket_off;
+                nb = S.nb;
+                curseg = si;
+            }
+        }
         TS.wait(g, tb);
         const ulonglong2* sp = TS.buf(tb);
         uint64_t* skeys = (uint64_t*)TS.buf(tb);  // staging reuses the consumed tile buffer
@@ -1312,6 +1323,170 @@ __global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS 
     }
 }
 
+// ------------------------------------------------ one-pass level 1 (multi)
+// Every segment of a level >= 1 with a linear cell table and a slice of the
+// parent's sorted sample: bucket b of segment s gets a padded region sized from
+// its slice count (k_mdirect_caps), regions laid out segment after segment
+// (k_mdirect_scan, k_mdirect_bases), one pass classifies / ranks / claims /
+// scatters all tiles (k_direct<false, 4>), and k_mdirect_children lists the
+// children (base cases read at their padded base). Any ineligible segment or
+// overflowing region runs the exact two-pass level instead (Ctrl::run_exact).
+__global__ void __launch_bounds__(256) k_mdirect_caps(LevelParams p, DirectWS w, const uint64_t* psample,
+                                                      uint64_t* seg_tot, double sigma, double slack) {
+    griddep_wait();
+    __shared__ uint32_t hist[kDirectMaxBuckets];
+    __shared__ uint64_t red[256 / 32];
+    const SegDesc sd = p.segs[blockIdx.x];
+    const ModelHdr* h = (const ModelHdr*)(p.models + sd.model_off);
+    const uint32_t len = (uint32_t)(sd.pslice & 0xffffffu);
+    const bool ok = psample && h->kind == kRadix && (h->flags & kModelLut) && !(h->flags & kModelLog) &&
+                    h->nbuckets <= kDirectMaxBuckets && len >= 2 && !(sd.flags & kSegForceRadix);
+    if (!ok) {
+        if (threadIdx.x == 0) { atomicOr(w.ovf, 2u); seg_tot[blockIdx.x] = 0; }
+        return;
+    }
+    const uint32_t nb = h->nbuckets;
+    for (uint32_t b = threadIdx.x; b < nb; b += 256) hist[b] = 0;
+    __syncthreads();
+    const uint16_t* lut = (const uint16_t*)(h + 1);
+    const uint64_t* smp = psample + (sd.pslice >> 24);
+    for (uint32_t i = threadIdx.x; i < len; i += 256)
+        atomicAdd(&hist[lut[lut_cell(smp[i], h->radix_min, h->shift, h->B)]], 1u);
+    __syncthreads();
+    const double r = (double)sd.n / (double)len;
+    uint64_t tot = 0;
+    for (uint32_t b = threadIdx.x; b < nb; b += 256) {
+        const double c = (double)hist[b];
+        const double e = c + sigma * sqrt(c) + slack;
+        const uint64_t cap = e > 0.0 ? (uint64_t)ceil(r * e) : 0ull;
+        w.end[sd.bucket_off + b] = cap;
+        tot += cap;
+    }
+    tot = block_reduce_sum_u64<256>(tot, red);
+    if (threadIdx.x == 0) seg_tot[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(1024) k_mdirect_scan(uint32_t nsegs, uint64_t* seg_tot, uint64_t alloc, DirectWS w) {
+    griddep_wait();
+    __shared__ uint64_t wsum[1024 / 32 + 1];
+    if (*w.ovf) return;
+    const uint64_t tot = block_exclusive_scan_u64<1024>(seg_tot, nsegs, wsum);
+    if (threadIdx.x == 0 && tot > alloc) *w.ovf = 2u;
+}
+__global__ void __launch_bounds__(256) k_mdirect_bases(LevelParams p, DirectWS w, const uint64_t* seg_base) {
+    griddep_wait();
+    __shared__ uint64_t capv[kDirectMaxBuckets];
+    __shared__ uint64_t wsum[256 / 32 + 1];
+    if (*w.ovf) return;
+    const SegDesc sd = p.segs[blockIdx.x];
+    const uint32_t nb = ((const ModelHdr*)(p.models + sd.model_off))->nbuckets;
+    for (uint32_t b = threadIdx.x; b < nb; b += 256) capv[b] = w.end[sd.bucket_off + b];
+    __syncthreads();
+    block_exclusive_scan_u64<256>(capv, nb, wsum);
+    const uint64_t s0 = seg_base[blockIdx.x];
+    for (uint32_t b = threadIdx.x; b < nb; b += 256) {
+        const uint64_t c = w.end[sd.bucket_off + b];
+        w.base[sd.bucket_off + b] = s0 + capv[b];
+        w.cur[sd.bucket_off + b] = s0 + capv[b];
+        w.end[sd.bucket_off + b] = s0 + capv[b] + c;
+    }
+}
+template <int NT>
+__global__ void __launch_bounds__(NT) k_mdirect_children(LevelParams p, DirectWS w, int64_t base_delta) {
+    griddep_wait();
+    __shared__ uint64_t wsum[NT / 32 + 1];
+    __shared__ uint32_t lcount[4], gbase[4];
+    __shared__ unsigned long long lkeys[2];  // base, rec
+    __shared__ uint64_t cntv[kDirectMaxBuckets];
+    if (p.ctrl->nan_index != ~0ull) return;
+    if (*w.ovf) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) { p.ctrl->direct = 0; p.ctrl->run_exact = 1; }
+        return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) { p.ctrl->direct = 1; p.ctrl->run_exact = 0; }
+    const SegDesc sd = p.segs[blockIdx.x];
+    const uint32_t nb = ((const ModelHdr*)(p.models + sd.model_off))->nbuckets;
+    for (uint32_t b = threadIdx.x; b < nb; b += NT) cntv[b] = w.cur[sd.bucket_off + b] - w.base[sd.bucket_off + b];
+    if (threadIdx.x < 4) lcount[threadIdx.x] = 0;
+    if (threadIdx.x < 2) lkeys[threadIdx.x] = 0;
+    __syncthreads();
+    block_exclusive_scan_u64<NT>(cntv, nb, wsum);
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint32_t b0 = 0; b0 < nb; b0 += NT) {  // CTA-uniform rounds
+        const uint32_t b = b0 + threadIdx.x;
+        uint64_t st = 0, len = 0;
+        if (b < nb) {
+            st = cntv[b];
+            len = (b + 1 < nb ? cntv[b + 1] : sd.n) - st;
+        }
+        const int cls = len == 0 ? -1 : (len <= p.base_cap[2] ? (len <= p.base_cap[0] ? 0 : (len <= p.base_cap[1] ? 1 : 2)) : 3);
+        uint32_t li = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const unsigned mc = __ballot_sync(FULL_MASK, cls == c);
+            if (mc) {
+                const int leader = __ffs(mc) - 1;
+                uint32_t base = 0;
+                if (lane == leader) base = atomicAdd(&lcount[c], (uint32_t)__popc(mc));
+                base = __shfl_sync(FULL_MASK, base, leader);
+                if (cls == c) li = base + __popc(mc & lt);
+            }
+        }
+        unsigned long long kb = (cls >= 0 && cls < 3) ? (unsigned long long)len : 0ull;
+        unsigned long long kr = cls == 3 ? (unsigned long long)len : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            kb += __shfl_xor_sync(FULL_MASK, kb, o);
+            kr += __shfl_xor_sync(FULL_MASK, kr, o);
+        }
+        if (lane == 0 && kb) atomicAdd(&lkeys[0], kb);
+        if (lane == 0 && kr) atomicAdd(&lkeys[1], kr);
+        __syncthreads();
+        if (threadIdx.x < 4) {
+            const uint32_t c = lcount[threadIdx.x];
+            unsigned int* ctr = threadIdx.x == 3 ? &p.ctrl->n_rec : &p.ctrl->n_base[threadIdx.x];
+            gbase[threadIdx.x] = c ? atomicAdd(ctr, c) : 0u;
+            lcount[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        if (cls == 3) {
+            const uint32_t e = gbase[3] + li;
+            const uint32_t depth = sd.depth + 1;
+            const uint32_t flags = (len == sd.n || depth > p.depth_cap) ? kSegForceRadix : 0u;
+            if (e < p.list_cap) p.rec[e] = SegOut{sd.begin + st, len, depth, flags, 0ull, w.base[sd.bucket_off + b]};
+            else atomicOr(&p.ctrl->err, 4u);
+        } else if (cls >= 0) {
+            const uint32_t e = gbase[cls] + li;
+            if (e < p.list_cap)
+                p.base[cls][e] = BaseItem{sd.begin + st, len, base_delta + (int64_t)w.base[sd.bucket_off + b]};
+            else atomicOr(&p.ctrl->err, 2u);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (lkeys[0]) atomicAdd(&p.ctrl->keys_base, lkeys[0]);
+        if (lkeys[1]) atomicAdd(&p.ctrl->keys_rec, lkeys[1]);
+    }
+}
+
+size_t direct_multi_workspace_bytes(uint64_t slots, uint32_t nsegs) {
+    return direct_workspace_bytes(slots, nsegs) + 16 * (size_t)nsegs + 64;
+}
+
+void launch_direct_multi(const LevelParams& p, const uint64_t* psample, uint64_t alloc_keys, void* dw, uint64_t slots,
+                         int grid, cudaStream_t st, bool test_overflow, const uint64_t* base_src) {
+    const DirectWS w = direct_ws(dw, slots, p.nsegs);
+    uint64_t* seg_tot = (uint64_t*)((uint8_t*)dw + ((direct_workspace_bytes(slots, p.nsegs) + 15) & ~(size_t)15));
+    const double sigma = test_overflow ? -kDirectSigma : kDirectSigma, slack = test_overflow ? 0.0 : kDirectSlack;
+    cudaMemsetAsync(w.ovf, 0, 4, st);
+    pdl(k_mdirect_caps, p.nsegs, 256, 0, st, p, w, psample, seg_tot, sigma, slack);
+    pdl(k_mdirect_scan, 1, 1024, 0, st, p.nsegs, seg_tot, alloc_keys, w);
+    pdl(k_mdirect_bases, p.nsegs, 256, 0, st, p, w, (const uint64_t*)seg_tot);
+    constexpr size_t sm = sizeof(DirectSmem);
+    pdl(k_direct<false, 4>, grid, kPNT, sm, st, p, w);
+    pdl(k_mdirect_children<1024>, p.nsegs, 1024, 0, st, p, w, (int64_t)(p.dst - base_src));
+}
+
 void launch_direct(const LevelParams& p, int in_f64, uint64_t root_m, uint64_t alloc_keys, void* dw, uint64_t slots,
                    int grid, cudaStream_t st, bool test_overflow, const uint64_t* base_src) {
     const DirectWS w = direct_ws(dw, slots, p.nsegs);
@@ -1355,6 +1530,7 @@ void partition_init(int optin) {
     allow_smem(k_direct<false, 2>, optin);
     allow_smem(k_direct<true, 3>, optin);
     allow_smem(k_direct<false, 3>, optin);
+    allow_smem(k_direct<false, 4>, optin);
     allow_smem(k_direct_setup<1024>, optin);
     allow_smem(k_direct_children<1024>, optin);
     allow_smem(k_scan_children<128>, optin);
