@@ -129,7 +129,7 @@ struct lsort_ctx {
     int depth = 0;  // nesting level (sample sorts run in a nested context)
     DevBuf scratch, data, segs, idx, tile_prefix, models, buckets, rec, base[3], fill, ctrl, sample, aux, train_ws,
         kseg, ktp, kplan, qws, ids, clus, cidx, scratch2, dws, bat[3], psample, slices, fwd_model, fwd_slices, piv, fsample,
-        lutws, scratch3;
+        lutws, scratch3, segd;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t bev[11] = {};  // batch pipeline: h2d[3], sorted[3], d2h[3], start, end
     PinBuf hctrl, hrec, hsegs, hidx, hprefix, hmodel;
@@ -726,8 +726,8 @@ struct Engine {
                 !C->buckets.ensure(nbuckets * 8 + 8) || !C->rec.ensure(list_cap * sizeof(SegOut)) ||
                 !C->fill.ensure(list_cap * sizeof(FillItem)) || !C->base[0].ensure(list_cap * sizeof(BaseItem)) ||
                 !C->base[1].ensure(list_cap * sizeof(BaseItem)) || !C->base[2].ensure(list_cap * sizeof(BaseItem)) ||
-                !C->kseg.ensure(3 * (size_t)np * 4 + 16) || !C->ktp.ensure(3 * ((size_t)np + 1) * 8) ||
-                !C->kplan.ensure(3 * sizeof(KindPlan)) || !C->clus.ensure(ncl * sizeof(BaseItem) + 16))
+                !C->kseg.ensure(4 * (size_t)np * 4 + 16) || !C->ktp.ensure(4 * ((size_t)np + 1) * 8) ||
+                !C->kplan.ensure(4 * sizeof(KindPlan)) || !C->clus.ensure(ncl * sizeof(BaseItem) + 16))
                 throw LsortError{LSORT_ENOMEM, "level workspace"};
             if (np) {
                 up(C->segs.p, hs, np * sizeof(SegDesc), true);
@@ -830,10 +830,18 @@ struct Engine {
             }
             if (direct1) {  // (direct0 is level 0 only)
                 if (timing) CU(cudaEventRecord(C->pev[6], st));
-                if (!C->scratch3.ensure(8 * alloc1) || !C->dws.ensure(direct_multi_workspace_bytes(nbuckets, np)))
+                if (!C->scratch3.ensure(8 * alloc1) || !C->dws.ensure(direct_multi_workspace_bytes(nbuckets, np)) ||
+                    !C->segd.ensure(4 * (size_t)np + 16))
                     throw LsortError{LSORT_ENOMEM, "one-pass level 1"};
                 LevelParams pd = p;
                 pd.dst = C->scratch3.as<uint64_t>();
+                // segments of another model kind go to the exact kernels (seg_sel 2), whose
+                // recursion children are then read through the padded buffer as well
+                pd.seg_direct = C->segd.as<uint32_t>();
+                pd.seg_sel = 1;
+                p.seg_direct = C->segd.as<uint32_t>();
+                p.seg_sel = 2;
+                p.rec_delta = (int64_t)(dst - C->scratch3.as<uint64_t>());
                 launch_direct_multi(pd, dc.psample, alloc1, C->dws.p, nbuckets,
                                     (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM), st,
                                     (cfg.flags & LSORT_FLAG_TEST_DIRECT_OVERFLOW) != 0, dst);
@@ -869,6 +877,7 @@ struct Engine {
             p.ids = C->ids.as<uint16_t>();  // (the one-pass setup may have grown the id array)
             const bool direct = dout != nullptr;
             lvl_dout = dout;
+            const bool next_from_dout = direct1;  // (every next-level segment reads through it)
             // ---- partition
             const int grid_h = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
             const int grid_s = (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM);
@@ -1033,7 +1042,7 @@ struct Engine {
             }
             // ping-pong: this level's output becomes the next level's input (a padded
             // level 0 wrote scratch2; the next level writes exact offsets into `keys`)
-            src = hc->direct ? (void*)lvl_dout : (void*)dst;
+            src = (hc->direct || next_from_dout) ? (void*)lvl_dout : (void*)dst;
             src_f64 = false;
             dst = (dst == C->scratch.as<uint64_t>()) ? (uint64_t*)keys : C->scratch.as<uint64_t>();
             ++level;

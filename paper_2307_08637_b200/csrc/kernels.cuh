@@ -90,6 +90,12 @@ struct LevelParams {
     uint32_t kstride;
     uint32_t remote;               // k_scatter: cursors preset by the multi-GPU rank plan, addressing
                                    // peer GPUs' receive buffers (exchange fused into the scatter, dist.cu)
+    // one-pass level 1 over part of a level: seg_direct[j] = 1 when segment j is
+    // handled by the one-pass kernels; seg_sel 1 = process only those, 2 = only the
+    // others (the exact two-pass kernels), 0 = every segment
+    const uint32_t* seg_direct;
+    uint32_t seg_sel;
+    int64_t rec_delta;             // k_scan_children: SegOut::in_begin = begin + rec_delta
 };
 
 // Sort configuration as seen by kernels.

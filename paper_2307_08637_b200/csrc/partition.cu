@@ -36,6 +36,11 @@ __device__ __forceinline__ uint32_t kind_slot(uint32_t kind) {
     return kind == kLearned ? 0u : (kind == kTree ? 1u : 2u);
 }
 
+// one-pass level 1 over part of a level (LevelParams::seg_sel)
+__device__ __forceinline__ bool seg_selected(const LevelParams& p, uint32_t i) {
+    return p.seg_sel == 0 || (p.seg_direct[i] != 0) == (p.seg_sel == 1);
+}
+
 // ------------------------------------------------------------ kind plan
 constexpr int kPlanNT = 1024;
 __global__ void __launch_bounds__(kPlanNT) k_kind_plan(LevelParams p) {
@@ -50,7 +55,8 @@ __global__ void __launch_bounds__(kPlanNT) k_kind_plan(LevelParams p) {
     __shared__ uint64_t tl[kPlanNT];
     __shared__ uint32_t carry_n;
     __shared__ uint64_t carry_t;
-    for (uint32_t K = 0; K < 3; ++K) {
+    const uint32_t nlists = p.seg_sel == 2 ? 4u : 3u;  // (slot 3: every selected segment, for k_scatter)
+    for (uint32_t K = 0; K < nlists; ++K) {
         if (threadIdx.x == 0) { carry_n = 0; carry_t = 0; }
         __syncthreads();
         uint32_t* ks = p.kseg + (size_t)K * p.kstride;
@@ -59,10 +65,10 @@ __global__ void __launch_bounds__(kPlanNT) k_kind_plan(LevelParams p) {
             uint32_t s = base + threadIdx.x;
             uint32_t f = 0;
             uint64_t t = 0;
-            if (s < p.nsegs) {
+            if (s < p.nsegs && seg_selected(p, s)) {
                 const SegDesc& sd = p.segs[s];
                 uint32_t kind = ((const ModelHdr*)(p.models + sd.model_off))->kind;
-                f = kind_slot(kind) == K;
+                f = K == 3 || kind_slot(kind) == K;
                 t = f ? (sd.n + kTileKeys - 1) / kTileKeys : 0;
             }
             fl[threadIdx.x] = f;
@@ -538,6 +544,7 @@ __global__ void __launch_bounds__(NT) k_scan_children(LevelParams p) {
     extern __shared__ uint64_t dyn[];           // cnt[nb], eqval[nb], iseq[nb] (u8)
     if (p.ctrl->nan_index != ~0ull) return;
     if (p.gate && *p.gate == 0) return;
+    if (!seg_selected(p, blockIdx.x)) return;  // (its children come from the one-pass level)
     const SegDesc sd = p.segs[blockIdx.x];
     const uint8_t* mg = p.models + sd.model_off;
     const ModelHdr h = *(const ModelHdr*)mg;
@@ -636,7 +643,9 @@ __global__ void __launch_bounds__(NT) k_scan_children(LevelParams p) {
                     const uint32_t o = p.slices[b], l = p.slices[b + 1] - o;
                     if (l >= kMinSlice) ps = (uint64_t)o << 24 | min(l, 0xffffffu);
                 }
-                if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, flags, ps, begin};
+                // (read position relative to the next level's source: rec_delta when this
+                // level's one-pass part made that source the padded buffer)
+                if (e < p.list_cap) p.rec[e] = SegOut{begin, len, depth, flags, ps, (uint64_t)((int64_t)begin + p.rec_delta)};
                 else atomicOr(&p.ctrl->err, 4u);
             }
         }
@@ -666,14 +675,27 @@ __device__ __forceinline__ void ids_range(const TileGeom& g, uint64_t& start, ui
 }
 
 // Tile t over all segments of the level.
-__device__ __forceinline__ TileGeom tile_geom_all(const LevelParams& p, uint64_t t, uint32_t& i) {
+// selc (nullable): the selection flag of segment i, cached by the caller and re-read only
+// when the segment changes (a global load per tile ahead of the next tile's bulk copy
+// delayed the copy)
+__device__ __forceinline__ TileGeom tile_geom_all(const LevelParams& p, uint64_t t, uint32_t& i, bool* selc = nullptr) {
+    const uint32_t i0 = i;
     if (i == ~0u) i = find_seg(p.tile_prefix, p.nsegs, t);
     else
         while (i + 1 < p.nsegs && p.tile_prefix[i + 1] <= t) ++i;
     const SegDesc& sd = p.segs[i];
     const uint64_t lo = sd.in_begin + (t - p.tile_prefix[i]) * (uint64_t)kTileKeys;
     TileGeom g;
-    g.init(p.src, lo, min(lo + kTileKeys, sd.in_begin + sd.n));
+    // a segment another kernel of the level handles: an empty tile (no copy, no keys)
+    bool sel = true;
+    if (p.seg_sel) {
+        if (!selc) sel = seg_selected(p, i);
+        else {
+            if (i != i0) *selc = seg_selected(p, i);
+            sel = *selc;
+        }
+    }
+    g.init(p.src, lo, sel ? min(lo + kTileKeys, sd.in_begin + sd.n) : lo);
     return g;
 }
 
@@ -687,9 +709,27 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
     // every child of the level is an equality fill (k_scan_children's key counters):
     // nothing moves (duplicate-heavy levels, e.g. rootdups' level 1)
     if (!p.remote && p.ctrl->keys_base + p.ctrl->keys_rec == 0) return;
-    const uint64_t per = (p.ntiles + gridDim.x - 1) / gridDim.x;
+    // a level partly run one-pass (seg_sel 2): only the other segments' tiles, from
+    // k_kind_plan's list of every selected segment (slot 3)
+    const bool lst = p.seg_sel == 2;
+    const uint32_t* ks3 = p.kseg + 3 * (size_t)p.kstride;
+    const uint64_t* tp3 = p.ktp + 3 * ((size_t)p.kstride + 1);
+    const uint32_t nks3 = lst ? p.kplan[3].nsegs : 0u;
+    const uint64_t ntl = lst ? p.kplan[3].ntiles : p.ntiles;
+    auto geom = [&](uint64_t t, uint32_t& i) -> TileGeom {
+        if (!lst) return tile_geom_all(p, t, i);
+        if (i == ~0u) i = find_seg(tp3, nks3, t);
+        else
+            while (i + 1 < nks3 && tp3[i + 1] <= t) ++i;
+        const SegDesc& sd = p.segs[ks3[i]];
+        const uint64_t lo = sd.in_begin + (t - tp3[i]) * (uint64_t)kTileKeys;
+        TileGeom g;
+        g.init(p.src, lo, min(lo + kTileKeys, sd.in_begin + sd.n));
+        return g;
+    };
+    const uint64_t per = (ntl + gridDim.x - 1) / gridDim.x;
     const uint64_t t0 = (uint64_t)blockIdx.x * per;
-    const uint64_t t1 = min(t0 + per, p.ntiles);
+    const uint64_t t1 = min(t0 + per, ntl);
     if (t0 >= t1) return;
     for (uint32_t b = threadIdx.x; b < NBC; b += kPNT) Q.cnt[0][b] = Q.cnt[1][b] = 0;
     TileStream TS;
@@ -706,7 +746,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
         }
     };
     uint32_t inext = ~0u;
-    TileGeom gnext = tile_geom_all(p, t0, inext);
+    TileGeom gnext = geom(t0, inext);
     issue_ids(gnext, 0);
     TS.issue(p.src, gnext, 0);
     int64_t cur = -1;
@@ -718,7 +758,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
         const TileGeom g = gnext;
         uint32_t* cnt = Q.cnt[tb];
         if ((int64_t)i != cur) {
-            const SegDesc& sd = p.segs[i];
+            const SegDesc& sd = p.segs[lst ? ks3[i] : i];
             boff = sd.bucket_off;
             nbo = sd.nb_max;
             cur = i;
@@ -788,7 +828,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_scatter(LevelParams p) {
         }
         __syncthreads();  // (1) tile counts complete; every thread is past the previous tile
         if (tile + 1 < t1) {  // prefetch the next tile into the buffer the previous tile staged in
-            gnext = tile_geom_all(p, tile + 1, inext);
+            gnext = geom(tile + 1, inext);
             issue_ids(gnext, tb ^ 1);
             TS.issue(p.src, gnext, tb ^ 1);
         }
@@ -916,6 +956,8 @@ __host__ __device__ inline DirectWS direct_ws(void* w, uint64_t slots, uint32_t 
     return d;
 }
 size_t direct_workspace_bytes(uint64_t slots, uint32_t nsegs) { return 8 * (3 * slots) + 16 + 0 * nsegs; }
+// (ovf[0]: 2 ineligible level / alloc exceeded, 1 a region overflowed; ovf[1]: the
+// one-pass level 1 left some segments to the exact kernels)
 const uint32_t* direct_flag_ptr(const void* dw, uint64_t slots, uint32_t nsegs) {
     return direct_ws((void*)dw, slots, nsegs).ovf;
 }
@@ -1017,7 +1059,8 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
     TileStream TS;
     TS.init((uint8_t*)Q.tiles, Q.bars);
     uint32_t inext = ~0u;
-    TileGeom gnext = tile_geom_all(p, t0, inext);
+    bool selc = true;
+    TileGeom gnext = tile_geom_all(p, t0, inext, &selc);
     TS.issue(p.src, gnext, 0);
     KState S;
     if constexpr (MODE == 3) {  // splitter tree + its lookup table; equality buckets flagged
@@ -1121,7 +1164,7 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
         }
         __syncthreads();  // (1) tile counts complete; every thread is past the previous tile
         if (tile + 1 < t1) {
-            gnext = tile_geom_all(p, tile + 1, inext);
+            gnext = tile_geom_all(p, tile + 1, inext, &selc);
             TS.issue(p.src, gnext, tb ^ 1);
         }
         constexpr int kPer = NBC / kPNT;
@@ -1332,7 +1375,7 @@ __global__ void __launch_bounds__(NT) k_direct_children(LevelParams p, DirectWS 
 // children (base cases read at their padded base). Any ineligible segment or
 // overflowing region runs the exact two-pass level instead (Ctrl::run_exact).
 __global__ void __launch_bounds__(256) k_mdirect_caps(LevelParams p, DirectWS w, const uint64_t* psample,
-                                                      uint64_t* seg_tot, double sigma, double slack) {
+                                                      uint64_t* seg_tot, double sigma, double slack, uint32_t* segd) {
     griddep_wait();
     __shared__ uint32_t hist[kDirectMaxBuckets];
     __shared__ uint64_t red[256 / 32];
@@ -1341,10 +1384,11 @@ __global__ void __launch_bounds__(256) k_mdirect_caps(LevelParams p, DirectWS w,
     const uint32_t len = (uint32_t)(sd.pslice & 0xffffffu);
     const bool ok = psample && h->kind == kRadix && (h->flags & kModelLut) && !(h->flags & kModelLog) &&
                     h->nbuckets <= kDirectMaxBuckets && len >= 2 && !(sd.flags & kSegForceRadix);
-    if (!ok) {
-        if (threadIdx.x == 0) { atomicOr(w.ovf, 2u); seg_tot[blockIdx.x] = 0; }
+    if (!ok) {  // another model kind: the exact two-pass kernels take this segment
+        if (threadIdx.x == 0) { segd[blockIdx.x] = 0; seg_tot[blockIdx.x] = 0; atomicOr(w.ovf + 1, 1u); }
         return;
     }
+    if (threadIdx.x == 0) segd[blockIdx.x] = 1;
     const uint32_t nb = h->nbuckets;
     for (uint32_t b = threadIdx.x; b < nb; b += 256) hist[b] = 0;
     __syncthreads();
@@ -1376,7 +1420,7 @@ __global__ void __launch_bounds__(256) k_mdirect_bases(LevelParams p, DirectWS w
     griddep_wait();
     __shared__ uint64_t capv[kDirectMaxBuckets];
     __shared__ uint64_t wsum[256 / 32 + 1];
-    if (*w.ovf) return;
+    if (*w.ovf || !p.seg_direct[blockIdx.x]) return;
     const SegDesc sd = p.segs[blockIdx.x];
     const uint32_t nb = ((const ModelHdr*)(p.models + sd.model_off))->nbuckets;
     for (uint32_t b = threadIdx.x; b < nb; b += 256) capv[b] = w.end[sd.bucket_off + b];
@@ -1398,11 +1442,14 @@ __global__ void __launch_bounds__(NT) k_mdirect_children(LevelParams p, DirectWS
     __shared__ unsigned long long lkeys[2];  // base, rec
     __shared__ uint64_t cntv[kDirectMaxBuckets];
     if (p.ctrl->nan_index != ~0ull) return;
-    if (*w.ovf) {
+    if (*w.ovf) {  // a region overflowed: the exact two-pass level takes every segment
+        if (threadIdx.x == 0) const_cast<uint32_t*>(p.seg_direct)[blockIdx.x] = 0;
         if (blockIdx.x == 0 && threadIdx.x == 0) { p.ctrl->direct = 0; p.ctrl->run_exact = 1; }
         return;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) { p.ctrl->direct = 1; p.ctrl->run_exact = 0; }
+    // (some segments of another model kind: the exact kernels run for those)
+    if (blockIdx.x == 0 && threadIdx.x == 0) { p.ctrl->direct = 1; p.ctrl->run_exact = w.ovf[1] ? 1u : 0u; }
+    if (!p.seg_direct[blockIdx.x]) return;
     const SegDesc sd = p.segs[blockIdx.x];
     const uint32_t nb = ((const ModelHdr*)(p.models + sd.model_off))->nbuckets;
     for (uint32_t b = threadIdx.x; b < nb; b += NT) cntv[b] = w.cur[sd.bucket_off + b] - w.base[sd.bucket_off + b];
@@ -1472,14 +1519,15 @@ __global__ void __launch_bounds__(NT) k_mdirect_children(LevelParams p, DirectWS
 size_t direct_multi_workspace_bytes(uint64_t slots, uint32_t nsegs) {
     return direct_workspace_bytes(slots, nsegs) + 16 * (size_t)nsegs + 64;
 }
+// the per-segment one-pass flags live in the caller's seg_direct array (LevelParams)
 
 void launch_direct_multi(const LevelParams& p, const uint64_t* psample, uint64_t alloc_keys, void* dw, uint64_t slots,
                          int grid, cudaStream_t st, bool test_overflow, const uint64_t* base_src) {
     const DirectWS w = direct_ws(dw, slots, p.nsegs);
     uint64_t* seg_tot = (uint64_t*)((uint8_t*)dw + ((direct_workspace_bytes(slots, p.nsegs) + 15) & ~(size_t)15));
     const double sigma = test_overflow ? -kDirectSigma : kDirectSigma, slack = test_overflow ? 0.0 : kDirectSlack;
-    cudaMemsetAsync(w.ovf, 0, 4, st);
-    pdl(k_mdirect_caps, p.nsegs, 256, 0, st, p, w, psample, seg_tot, sigma, slack);
+    cudaMemsetAsync(w.ovf, 0, 8, st);
+    pdl(k_mdirect_caps, p.nsegs, 256, 0, st, p, w, psample, seg_tot, sigma, slack, (uint32_t*)p.seg_direct);
     pdl(k_mdirect_scan, 1, 1024, 0, st, p.nsegs, seg_tot, alloc_keys, w);
     pdl(k_mdirect_bases, p.nsegs, 256, 0, st, p, w, (const uint64_t*)seg_tot);
     constexpr size_t sm = sizeof(DirectSmem);
