@@ -615,6 +615,11 @@ struct Engine {
         uint64_t* lvl_dout = nullptr;  // the padded output of the current level when it ran one-pass
         while (!segs.empty()) {
             const uint32_t ns = (uint32_t)segs.size();
+            {  // bucket ids are indexed by read position: cover this level's read window
+                uint64_t rmax = 0;
+                for (const SegPlan& q : segs) rmax = std::max(rmax, q.rd() + q.n);
+                if (!C->ids.ensure(2 * std::max<uint64_t>(rmax, 1))) throw LsortError{LSORT_ENOMEM, "bucket ids"};
+            }
             // ---- plan the level on the host
             if (!C->hsegs.ensure(ns * sizeof(SegDesc)) || !C->hprefix.ensure((ns + 1) * 8) ||
                 !C->hidx.ensure(ns * 4))
@@ -823,6 +828,7 @@ struct Engine {
             bool direct1 = l1_direct && !fw && !classic && !(cfg.flags & LSORT_FLAG_STRICT_POLICY) && level == 1 &&
                            np >= 1 && ncl == 0 && bigs.empty() && dc.psample && !src_f64 && max_nb <= kDirectMaxBuckets;
             uint64_t alloc1 = 0;
+            uint64_t* ldst = dst;  // where this level's exact kernels write (and its base cases read)
             for (uint32_t j = 0; direct1 && j < np; ++j) {
                 const uint64_t m = psegs[j].pslice & 0xffffffu;
                 if (m < 2) { direct1 = false; break; }
@@ -830,7 +836,10 @@ struct Engine {
             }
             if (direct1) {  // (direct0 is level 0 only)
                 if (timing) CU(cudaEventRecord(C->pev[6], st));
-                if (!C->scratch3.ensure(8 * alloc1) || !C->dws.ensure(direct_multi_workspace_bytes(nbuckets, np)) ||
+                // scratch3 = [padded regions (alloc1) | exact output of the segments the
+                // exact kernels take (n)]: the next level reads both through one buffer,
+                // at read positions < alloc1 + n (the id array covers them)
+                if (!C->scratch3.ensure(8 * (alloc1 + n)) || !C->dws.ensure(direct_multi_workspace_bytes(nbuckets, np)) ||
                     !C->segd.ensure(4 * (size_t)np + 16))
                     throw LsortError{LSORT_ENOMEM, "one-pass level 1"};
                 LevelParams pd = p;
@@ -841,10 +850,12 @@ struct Engine {
                 pd.seg_sel = 1;
                 p.seg_direct = C->segd.as<uint32_t>();
                 p.seg_sel = 2;
-                p.rec_delta = (int64_t)(dst - C->scratch3.as<uint64_t>());
+                ldst = C->scratch3.as<uint64_t>() + alloc1;
+                p.dst = ldst;
+                p.rec_delta = (int64_t)alloc1;
                 launch_direct_multi(pd, dc.psample, alloc1, C->dws.p, nbuckets,
                                     (int)std::min<uint64_t>(ntiles, (uint64_t)nsm * kPartPerSM), st,
-                                    (cfg.flags & LSORT_FLAG_TEST_DIRECT_OVERFLOW) != 0, dst);
+                                    (cfg.flags & LSORT_FLAG_TEST_DIRECT_OVERFLOW) != 0, ldst);
                 launched(5);
                 if (timing) CU(cudaEventRecord(C->pev[7], st));
                 p.gate = &dctrl->run_exact;
@@ -920,7 +931,7 @@ struct Engine {
                 launch_classic_base(p, dst, out, f64, classic, (int)level + 1, st);
                 launched(3);
             } else {
-                base_cases(p, dst, out, f64);
+                base_cases(p, ldst, out, f64);
             }
             mark(4);
             launch_fill(p, out, f64, nsm * 4, st);

@@ -1087,12 +1087,17 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
         const TileGeom g = gnext;
         uint32_t* cnt = Q.cnt[tb];
         if constexpr (MODE == 4) {  // (CTA-uniform) the tile's segment's table into shared memory
+            // (a segment the exact kernels take has another model kind -- a tree, an
+            // RMI: its tiles are empty and its header is not read as a cell table)
             const uint32_t si = inext;
             if (si != curseg) {
-                kstate_load<kRadix>(S, p.models + p.segs[si].model_off, Q.table);
-                boff = p.segs[si].bucket_off;
-                nb = S.nb;
                 curseg = si;
+                nb = 0;
+                if (selc) {
+                    kstate_load<kRadix>(S, p.models + p.segs[si].model_off, Q.table);
+                    boff = p.segs[si].bucket_off;
+                    nb = S.nb;
+                }
             }
         }
         TS.wait(g, tb);

@@ -617,3 +617,23 @@ def test_padded_level1_and_its_fallback(ctx, dist_name, seed):
     st = ctx.sort(d, L.SortConfig(flags=L._native.FLAG_TEST_DIRECT_OVERFLOW))
     assert st["direct_keys"] == 0
     assert np.array_equal(host_u64(d), exp)
+
+
+@pytest.mark.parametrize("dist_name,n", [("uniform", 20_000_000), ("lognormal2", 30_000_000),
+                                         ("normal", 25_000_000), ("twodups", 30_000_000)])
+def test_padded_level1_other_model_kinds(ctx, dist_name, n):
+    """A one-pass level 1 whose segments are too small for cell tables (splitter
+    trees, < 32 Ki keys) or mix model kinds: the tree segments' tiles are empty in
+    k_direct (their headers are not read as cell tables) and the exact kernels
+    write them into scratch3's tail, read by the next level through the same
+    buffer. Regression: 2e7-3e7 keys failed with an illegal address."""
+    seed = {"uniform": 42, "lognormal2": 19, "normal": 7, "twodups": 3}[dist_name]
+    x = O.generate(dist_name, n, seed)
+    if x.dtype == np.uint64:
+        exp = np.sort(x)
+    else:
+        exp = O.decode(np.sort(O.encode(x))).view(np.uint64)
+    for _ in range(2):  # (a second sort reuses the grown workspaces)
+        d = dev(x)
+        ctx.sort(d)
+        assert np.array_equal(host_u64(d), exp)
