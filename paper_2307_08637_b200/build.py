@@ -20,7 +20,8 @@ CLI = os.path.join(PKG, "lsort_cli")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
-           "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+           "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")] + \
+    os.environ.get("LSORT_NVCC_EXTRA", "").split()  # e.g. -DLSORT_DEBUG_DIRECT (device-side bounds checks)
 CU_SOURCES = ["partition.cu", "models.cu", "basecase.cu", "cluster.cu", "util.cu", "engine.cu", "dist.cu", "classic.cu"]
 CPP_SOURCES = ["gen.cpp", "keyio.cpp"]
 

@@ -4,6 +4,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -194,6 +196,17 @@ inline void pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t sm, cudaStream_t st,
     c.attrs = a;
     c.numAttrs = 1;
     cudaLaunchKernelEx(&c, k, args...);
+    // LSORT_SYNC_DEBUG: synchronise after every launch and name the first kernel that
+    // faults (compute-sanitizer stand-in; never set in a measured run)
+    static const bool sync_debug = getenv("LSORT_SYNC_DEBUG") != nullptr;
+    if (sync_debug) {
+        const cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            fprintf(stderr, "[lsort sync-debug] %s after kernel %s grid %u block %u\n", cudaGetErrorString(e),
+                    __PRETTY_FUNCTION__, g.x, b.x);
+            abort();
+        }
+    }
 }
 
 template <class F>

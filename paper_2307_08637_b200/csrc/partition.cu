@@ -1078,6 +1078,13 @@ __global__ void __launch_bounds__(kPNT, kPartPerSM) k_direct(LevelParams p, Dire
     } else if constexpr (MODE != 4) {
         kstate_load<kRadix>(S, p.models + p.segs[0].model_off, Q.table);
     }
+    if constexpr (MODE == 4) {
+        // no table yet: a CTA whose first segments belong to the exact kernels classifies
+        // its empty tiles' zero slots unconditionally -- through a valid (unused) table
+        S.nb = 0; S.rmin = 0; S.shift = 0; S.fill = false; S.rcells = 1; S.rorg = 0;
+        S.rtab = nullptr; S.rtabn = 0;
+        S.rlut = (const uint16_t*)Q.table;
+    }
     uint64_t boff = p.segs[0].bucket_off;
     uint32_t nb = MODE == 4 ? 0u : S.nb;
     uint32_t curseg = ~0u;

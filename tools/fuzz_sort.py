@@ -115,6 +115,7 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--max-keys", type=float, default=6e8)
     ap.add_argument("--only", default="")
+    ap.add_argument("--case", default="", help="replay one case: name:n:seed:flags")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(a.seed)
@@ -122,6 +123,7 @@ def main():
     t_end = time.time() + a.seconds
     cases = 0
     names = [x for x in FLOATS + INTS if not a.only or x in a.only.split(",")]
+    replay = a.case.split(":") if a.case else None
     while time.time() < t_end:
         name = names[rng.integers(len(names))]
         u = rng.random()
@@ -138,6 +140,10 @@ def main():
         flags = 0
         if rng.random() < 0.1:
             flags |= L._native.FLAG_STRICT_POLICY
+        if replay:
+            name, n, seed, flags = replay[0], int(replay[1]), int(replay[2]), int(replay[3])
+            g.manual_seed(seed)
+            t_end = 0
         x = draw(g, name, n, dev) if n else torch.empty(0, device=dev, dtype=torch.float64 if name in FLOATS else torch.int64)
         exp = torch.sort(ordered_i64(x))[0]
         cfg = L.SortConfig()
