@@ -191,8 +191,11 @@ __global__ void __cluster_dims__(kClSize, 1, 1) __launch_bounds__(kClNT, 1)
                 while (b < S) {
                     const uint32_t d = M.dsl[b];
                     const uint32_t len = M.start[b + 1] - M.start[b];
-                    if (d == ~0u || (d >> 24) != rank || tot + len > (uint32_t)kClSortCap) break;
                     const uint32_t lg = len > 1 ? min(31u - __clz(len), shift) : 0u;  // pow2 floor digits
+                    // (an empty sub-bucket still takes one digit: the digits are bounded like the keys)
+                    if (d == ~0u || (d >> 24) != rank || tot + len > (uint32_t)kClSortCap ||
+                        nd + (1u << lg) > (uint32_t)kClSortCap)
+                        break;
                     dbase[b] = nd;
                     lgd[b] = lg;
                     nd += 1u << lg;

@@ -202,8 +202,10 @@ inline void pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t sm, cudaStream_t st,
     if (sync_debug) {
         const cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) {
+            const char* name = nullptr;
+            cudaFuncGetName(&name, (const void*)k);
             fprintf(stderr, "[lsort sync-debug] %s after kernel %s grid %u block %u\n", cudaGetErrorString(e),
-                    __PRETTY_FUNCTION__, g.x, b.x);
+                    name ? name : __PRETTY_FUNCTION__, g.x, b.x);
             abort();
         }
     }

@@ -426,6 +426,7 @@ __device__ void build_radix_model(const SegDesc& sd, const void* src, bool f64, 
     mn = block_reduce_min<NT>(mn, red);
     mx = block_reduce_max<NT>(mx, red);
     if (threadIdx.x == 0) {
+        h->flags = 0;  // (not a cell table: the model record is reused memory)
         if (mn == mx) {
             h->kind = kFill;
             h->nbuckets = 1;

@@ -129,10 +129,10 @@ def main():
         u = rng.random()
         if u < 0.25:
             n = int(EDGES[rng.integers(len(EDGES))] * rng.uniform(0.7, 1.5))
-        elif u < 0.35:
+        elif u < 0.30:
             n = int(rng.integers(0, 20000))
         else:
-            n = int(np.exp(rng.uniform(np.log(2), np.log(a.max_keys))))
+            n = int(np.exp(rng.uniform(np.log(1e4), np.log(a.max_keys))))
         n = min(n, int(a.max_keys))
         seed = int(rng.integers(1 << 31))
         g = torch.Generator(device=dev)
