@@ -258,7 +258,8 @@ struct Engine {
     uint64_t root_rmi_sample(uint64_t n) const {
         const uint64_t s = sample_size_host(cfg.sample_fraction, cfg.rmi_sample_cap, n);
         if (cfg.flags & LSORT_FLAG_STRICT_POLICY) return s;
-        return std::min<uint64_t>(s, std::max<uint64_t>(kRootSampleMin, n >> 9));
+        static const int sh = getenv("LSORT_ROOT_SAMPLE_SHIFT") ? atoi(getenv("LSORT_ROOT_SAMPLE_SHIFT")) : 9;
+        return std::min<uint64_t>(s, std::max<uint64_t>(kRootSampleMin, n >> sh));
     }
     uint32_t tree_k(uint64_t n) const { return fanout(n, cfg.tree_bucket_count, cfg.bucket_target); }
     // largest sample the segment's model may need (the RMI sample only if the

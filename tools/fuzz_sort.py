@@ -18,6 +18,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2307_08637_b200 as L  # noqa: E402
+from paper_2307_08637_b200.dist import sort_emulated  # noqa: E402
 
 SIGN = -(1 << 63)
 
@@ -115,7 +116,8 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--max-keys", type=float, default=6e8)
     ap.add_argument("--only", default="")
-    ap.add_argument("--case", default="", help="replay one case: name:n:seed:flags")
+    ap.add_argument("--case", default="", help="replay one case: name:n:seed:flags[:world]")
+    ap.add_argument("--dist", type=float, default=0.0, help="fraction of cases run on 2-8 virtual ranks")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(a.seed)
@@ -144,13 +146,31 @@ def main():
             name, n, seed, flags = replay[0], int(replay[1]), int(replay[2]), int(replay[3])
             g.manual_seed(seed)
             t_end = 0
+        # --dist P: with probability P the case runs the multi-rank driver on virtual
+        # ranks (lsort_cuda_dist_emulate), shards cut at random points (some empty)
+        world = 0
+        if a.dist and not replay and rng.random() < a.dist and n <= 100_000_000:
+            world = int(rng.choice([2, 3, 4, 8]))
+        if replay and len(replay) > 4:
+            world = int(replay[4])
         x = draw(g, name, n, dev) if n else torch.empty(0, device=dev, dtype=torch.float64 if name in FLOATS else torch.int64)
         exp = torch.sort(ordered_i64(x))[0]
         cfg = L.SortConfig()
         cfg.flags |= flags
         t0 = time.time()
         try:
-            st = ctx.sort(x, cfg)
+            if world:
+                crng = np.random.default_rng(seed)
+                cuts = np.sort(crng.integers(0, n + 1, world - 1)) if crng.random() < 0.5 else \
+                    (np.arange(1, world) * n) // world
+                cuts = [0] + [int(c) for c in cuts] + [n]
+                shards = [x[cuts[r]:cuts[r + 1]] for r in range(world)]
+                outs, sts = sort_emulated(shards, cfg)
+                st = sts[0]
+                x = torch.cat(outs)
+                name = f"{name}@{world}"
+            else:
+                st = ctx.sort(x, cfg)
         except Exception as e:  # noqa: BLE001
             print(f"FAIL {name} n={n} seed={seed} flags={flags}: {type(e).__name__}: {e}", flush=True)
             sys.exit(1)
