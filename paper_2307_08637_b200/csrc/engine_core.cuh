@@ -744,6 +744,10 @@ struct Engine {
             const uint32_t nmid = (uint32_t)mids.size();
             if (nsmall + nmid) up(C->idx.p, hi, (nsmall + nmid) * 4, true);
             if (nbuckets) CU(cudaMemsetAsync(C->buckets.p, 0, nbuckets * 8, st));
+            // model records start zeroed: a builder that leaves a header field unset (the
+            // depth-cap radix fallback once left `flags`) reads as 0 on every run, not as
+            // whatever the reused memory held
+            if (model_bytes) CU(cudaMemsetAsync(C->models.p, 0, model_bytes, st));
             CU(cudaMemsetAsync(&dctrl->n_rec, 0, offsetof(Ctrl, verify_first) - offsetof(Ctrl, n_rec), st));  // per-level lists and key counters
 
             LevelParams p{};
