@@ -631,7 +631,11 @@ void dist_sort(lsort_dist* D, void* keys, uint64_t n, int key_kind, void* out, u
 }
 
 int dist_fail(lsort_dist* D, const LsortError& e) {
-    if (D) D->err = e.msg;
+    if (D) {
+        D->err = e.msg;
+        if (e.code == LSORT_ENOMEM && !last_alloc_error().empty()) D->err += " (" + last_alloc_error() + ")";
+    }
+    last_alloc_error().clear();
     return e.code;
 }
 

@@ -24,6 +24,17 @@ using namespace lsort_dev;
 
 namespace lsort_host {
 
+// why the last failed allocation of this thread failed (appended to ENOMEM messages by
+// fail(): a sticky fault of an earlier kernel makes every later cudaMalloc fail too, and
+// must not read as "out of memory")
+inline std::string& last_alloc_error() {
+    static thread_local std::string s;
+    return s;
+}
+inline void note_alloc_error(cudaError_t e, size_t bytes, const char* what) {
+    last_alloc_error() = std::string(what) + " of " + std::to_string(bytes) + " bytes: " + cudaGetErrorString(e);
+}
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
@@ -37,7 +48,8 @@ struct DevBuf {
         want = want + want / 8;  // headroom against regrowth
         if (cudaMalloc(&p, want) != cudaSuccess) {
             cudaGetLastError();
-            if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); p = nullptr; return false; }
+            const cudaError_t e = cudaMalloc(&p, bytes);
+            if (e != cudaSuccess) { note_alloc_error(e, bytes, "cudaMalloc"); cudaGetLastError(); p = nullptr; return false; }
             want = bytes;
         }
         cap = want;
@@ -60,7 +72,8 @@ struct PinBuf {
         p = nullptr;
         cap = 0;
         size_t want = std::max<size_t>(bytes * 2, 4096);
-        if (cudaMallocHost(&p, want) != cudaSuccess) { cudaGetLastError(); p = nullptr; return false; }
+        const cudaError_t e = cudaMallocHost(&p, want);
+        if (e != cudaSuccess) { note_alloc_error(e, want, "cudaMallocHost"); cudaGetLastError(); p = nullptr; return false; }
         cap = want;
         return true;
     }
@@ -1069,7 +1082,11 @@ struct Engine {
 
 
 inline int fail(lsort_ctx* ctx, const LsortError& e) {
-    if (ctx) ctx->err = e.msg;
+    if (ctx) {
+        ctx->err = e.msg;
+        if (e.code == LSORT_ENOMEM && !last_alloc_error().empty()) ctx->err += " (" + last_alloc_error() + ")";
+    }
+    last_alloc_error().clear();
     return e.code;
 }
 
