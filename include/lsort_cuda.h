@@ -154,6 +154,10 @@ typedef struct lsort_stats {
  * counts so they overflow and the exact two-pass level runs instead (checks
  * the fallback of the one-pass level 0 that large learned roots take). */
 #define LSORT_FLAG_TEST_DIRECT_OVERFLOW 8u
+/* cfg->flags, TEST ONLY: behave as if the padded one-pass buffers (~1.2 N keys for
+ * level 0, ~5 N for level 1) could not be allocated: the exact two-pass levels,
+ * which need only the N-key scratch array and the bucket ids, run instead. */
+#define LSORT_FLAG_TEST_NO_PADDED_MEM 16u
 
 typedef struct lsort_ctx lsort_ctx;
 

@@ -21,6 +21,7 @@ FLAG_PHASE_TIMING = 1
 FLAG_STRICT_POLICY = 2  # reference Alg. 5 models only (no GPU quality fallback)
 FLAG_CLUSTER = 4  # experimental fused cluster (DSMEM) last level
 FLAG_TEST_DIRECT_OVERFLOW = 8  # test only: force the padded level 0 to overflow
+FLAG_TEST_NO_PADDED_MEM = 16  # test only: as if the padded one-pass buffers could not be allocated
 
 
 class lsort_cfg(C.Structure):

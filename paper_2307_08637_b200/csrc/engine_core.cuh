@@ -852,13 +852,19 @@ struct Engine {
                 if (m < 2) { direct1 = false; break; }
                 alloc1 += direct_capacity_bound(psegs[j].n, m, hs[j].nb_max);
             }
+            // the padded regions are an optimisation: without the memory for them the
+            // exact two-pass level (scratch + ids only) runs instead
+            const bool no_padded = (cfg.flags & LSORT_FLAG_TEST_NO_PADDED_MEM) != 0;
+            if (direct1 && (no_padded || !C->scratch3.ensure(8 * (alloc1 + n)))) {
+                last_alloc_error().clear();
+                direct1 = false;
+            }
             if (direct1) {  // (direct0 is level 0 only)
                 if (timing) CU(cudaEventRecord(C->pev[6], st));
                 // scratch3 = [padded regions (alloc1) | exact output of the segments the
                 // exact kernels take (n)]: the next level reads both through one buffer,
                 // at read positions < alloc1 + n (the id array covers them)
-                if (!C->scratch3.ensure(8 * (alloc1 + n)) || !C->dws.ensure(direct_multi_workspace_bytes(nbuckets, np)) ||
-                    !C->segd.ensure(4 * (size_t)np + 16))
+                if (!C->dws.ensure(direct_multi_workspace_bytes(nbuckets, np)) || !C->segd.ensure(4 * (size_t)np + 16))
                     throw LsortError{LSORT_ENOMEM, "one-pass level 1"};
                 LevelParams pd = p;
                 pd.dst = C->scratch3.as<uint64_t>();
@@ -886,9 +892,10 @@ struct Engine {
                     n, std::min<uint64_t>(root_m, sample_size_host(cfg.sample_fraction, cfg.first_sample_cap, n)),
                     hs[0].nb_max);
                 // (level 1 reads this padded output: its bucket ids are indexed by read position)
-                if (!C->scratch2.ensure(8 * alloc) || !C->ids.ensure(2 * alloc))
-                    throw LsortError{LSORT_ENOMEM, "one-pass level 0"};
-                dout = C->scratch2.as<uint64_t>();
+                // (without the memory for the padded regions the exact two-pass level runs)
+                if (!no_padded && C->scratch2.ensure(8 * alloc) && C->ids.ensure(2 * alloc)) dout = C->scratch2.as<uint64_t>();
+                else if (!C->ids.ensure(2 * std::max<uint64_t>(n, 1))) throw LsortError{LSORT_ENOMEM, "bucket ids"};
+                else last_alloc_error().clear();
             }
             if (dout && direct0) {
                 if (!C->dws.ensure(direct_workspace_bytes(nbuckets, np))) throw LsortError{LSORT_ENOMEM, "one-pass level"};

@@ -555,6 +555,23 @@ def test_padded_level0_and_its_fallback(ctx, dist_name, seed):
     assert np.array_equal(d.cpu().numpy().view(np.uint64), exp)
 
 
+@pytest.mark.parametrize("dist_name,seed,n", [("lognormal2", 19, 60_000_000), ("normal", 7, 40_000_000),
+                                              ("zipf", 3, 40_000_000)])
+def test_no_memory_for_padded_levels(ctx, dist_name, seed, n):
+    """The padded buffers of the one-pass levels (~1.2 N keys for level 0, ~5 N for
+    level 1) are an optimisation: when they cannot be allocated (test flag) the
+    exact two-pass levels run in the N-key scratch array -- same result."""
+    x = O.generate(dist_name, n, seed)
+    exp = np.sort(x) if x.dtype == np.uint64 else O.decode(np.sort(O.encode(x))).view(np.uint64)
+    d = dev(x)
+    st = ctx.sort(d, L.SortConfig(flags=L._native.FLAG_TEST_NO_PADDED_MEM))
+    assert st["direct_keys"] == 0
+    assert np.array_equal(host_u64(d), exp)
+    d = dev(x)
+    st = ctx.sort(d)
+    assert np.array_equal(host_u64(d), exp)
+
+
 @pytest.mark.parametrize("case", ["lognormal2_f64", "narrow_u64"])
 def test_cell_table_models(ctx, case):
     """GPU policy (DESIGN 3, 6): a one-pass root tries a cell table over its
