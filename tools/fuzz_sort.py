@@ -116,8 +116,11 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--max-keys", type=float, default=6e8)
     ap.add_argument("--only", default="")
-    ap.add_argument("--case", default="", help="replay one case: name:n:seed:flags[:world]")
+    ap.add_argument("--case", default="", help="replay one case: name:n:seed:flags[:world[:api]]")
     ap.add_argument("--dist", type=float, default=0.0, help="fraction of cases run on 2-8 virtual ranks")
+    ap.add_argument("--repeat", type=int, default=1, help="--case: run the case this many times in one process")
+    ap.add_argument("--api", type=float, default=0.0,
+                    help="fraction of cases through another entry: host memory, sort_many, sort_batch, classic, NaN")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(a.seed)
@@ -145,7 +148,9 @@ def main():
         if replay:
             name, n, seed, flags = replay[0], int(replay[1]), int(replay[2]), int(replay[3])
             g.manual_seed(seed)
-            t_end = 0
+            a.repeat -= 1
+            if a.repeat <= 0:
+                t_end = 0
         # --dist P: with probability P the case runs the multi-rank driver on virtual
         # ranks (lsort_cuda_dist_emulate), shards cut at random points (some empty)
         world = 0
@@ -159,7 +164,50 @@ def main():
         cfg.flags |= flags
         t0 = time.time()
         try:
-            if world:
+            api = "sort"
+            if a.api and not replay and not world and rng.random() < a.api:
+                api = str(rng.choice(["host", "many", "batch", "classic", "nan"]))
+            if replay and len(replay) > 5:
+                api = replay[5]
+            if api != "sort" and (world or n > 60_000_000 or n < 2):
+                api = "sort"
+            if api == "host":  # LSORT_MEM_HOST: copies in / out inside the call
+                h = x.cpu().numpy()
+                st = ctx.sort(h, cfg)
+                x = torch.from_numpy(h).to(dev)
+                name += "/host"
+            elif api in ("many", "batch"):  # three pieces sorted in one call (device: concurrently; host: pipelined)
+                c1, c2 = sorted(int(v) for v in np.random.default_rng(seed).integers(0, n + 1, 2))
+                parts = [x[:c1].clone(), x[c1:c2].clone(), x[c2:].clone()]
+                exps = [torch.sort(ordered_i64(q))[0] for q in parts]
+                if api == "batch":
+                    hs = [q.cpu().numpy() for q in parts]
+                    st = ctx.sort_batch(hs, cfg)
+                    parts = [torch.from_numpy(q).to(dev) for q in hs]
+                else:
+                    st = ctx.sort_batch(parts, cfg)
+                x = torch.cat(parts)
+                exp = torch.cat(exps)
+                name += "/" + api
+            elif api == "classic":  # LearnedSort 2.0 path (one model, two rounds, counting sort + fix-up)
+                st = ctx.sort_classic(x, cfg)
+                name += "/classic"
+            elif api == "nan" and x.dtype == torch.float64:  # NaN: error with its first index, input untouched
+                idx = sorted(int(v) for v in np.random.default_rng(seed).integers(0, n, 3))
+                x[idx] = float("nan")
+                before = x.clone()
+                try:
+                    ctx.sort(x, cfg)
+                    raise AssertionError("NaN input sorted without error")
+                except L.NanError as e:
+                    if e.index != idx[0]:
+                        raise AssertionError(f"NaN index {e.index} != {idx[0]}")
+                if not torch.equal(before.view(torch.int64), x.view(torch.int64)):
+                    raise AssertionError("NaN input modified")
+                st = {"levels": -1, "level0_kind": -1, "ms_total": 0.0}
+                x = None  # (nothing to compare: the call must fail)
+                name += "/nan"
+            elif world:
                 crng = np.random.default_rng(seed)
                 cuts = np.sort(crng.integers(0, n + 1, world - 1)) if crng.random() < 0.5 else \
                     (np.arange(1, world) * n) // world
@@ -172,9 +220,9 @@ def main():
             else:
                 st = ctx.sort(x, cfg)
         except Exception as e:  # noqa: BLE001
-            print(f"FAIL {name} n={n} seed={seed} flags={flags} world={world}: {type(e).__name__}: {e}", flush=True)
+            print(f"FAIL {name} n={n} seed={seed} flags={flags} world={world} api={api}: {type(e).__name__}: {e}", flush=True)
             sys.exit(1)
-        got = ordered_i64(x)
+        got = exp if x is None else ordered_i64(x)
         same = bool(torch.equal(got, exp))
         cases += 1
         print(f"{'ok  ' if same else 'DIFF'} {name:18s} n={n:>11d} seed={seed:>10d} flags={flags} levels={st['levels']} "
