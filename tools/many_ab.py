@@ -1,5 +1,5 @@
 import sys, os, numpy as np, torch
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2307_08637_b200 as L
 ctx = L.Context(0)
 for dists, seed, kind in [(["normal","lognormal05","exponential2"], 7, "f64"), (["rootdups","twodups","zipf"], 3, "u64")]:
