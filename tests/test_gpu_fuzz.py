@@ -87,3 +87,14 @@ def test_fuzz_short(ctx, seed):
         n = min(n, 100_000_000)
         flags = L._native.FLAG_STRICT_POLICY if rng.random() < 0.15 else 0
         run_case(ctx, name, n, int(rng.integers(1 << 31)), flags)
+
+
+def test_fuzz_entries_and_virtual_ranks():
+    """150 cases of tools/fuzz_sort.py with 20% on 2-8 virtual ranks and 40% through the
+    other entries (host memory, sort_many, sort_batch, classic path, NaN error path)."""
+    import subprocess
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_sort.py"), "--seed", "21", "--cases", "150",
+                        "--seconds", "600", "--max-keys", "3e7", "--dist", "0.2", "--api", "0.4"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "fuzz: 150 cases bit-exact" in r.stdout

@@ -118,6 +118,7 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--case", default="", help="replay one case: name:n:seed:flags[:world[:api]]")
     ap.add_argument("--dist", type=float, default=0.0, help="fraction of cases run on 2-8 virtual ranks")
+    ap.add_argument("--cases", type=int, default=0, help="stop after this many cases (0: run for --seconds)")
     ap.add_argument("--repeat", type=int, default=1, help="--case: run the case this many times in one process")
     ap.add_argument("--api", type=float, default=0.0,
                     help="fraction of cases through another entry: host memory, sort_many, sort_batch, classic, NaN")
@@ -232,6 +233,8 @@ def main():
             print(f"first mismatches at {bad}", flush=True)
             sys.exit(1)
         del x, exp, got
+        if a.cases and cases >= a.cases:
+            break
         if n > 20_000_000:  # torch's cached blocks are invisible to the library's own cudaMalloc
             torch.cuda.empty_cache()
     print(f"fuzz: {cases} cases bit-exact", flush=True)
