@@ -31,6 +31,19 @@ def test_library_exports_every_header_symbol():
     assert set(syms) == set(N.EXPORTS)
 
 
+def test_header_constants_match_python_binding():
+    """Every LSORT_FLAG_* / return code / memory and key kind of the header has the
+    same value in the ctypes binding (a flag added on one side only is silent)."""
+    text = open(os.path.join(ROOT, "include", "lsort_cuda.h")).read()
+    defs = {m.group(1): int(m.group(2).rstrip("u"), 0)
+            for m in re.finditer(r"#define\s+LSORT_(FLAG_[A-Z_]+)\s+(\d+u?)", text)}
+    assert {"FLAG_PHASE_TIMING", "FLAG_STRICT_POLICY", "FLAG_CLUSTER", "FLAG_TEST_DIRECT_OVERFLOW",
+            "FLAG_TEST_NO_PADDED_MEM"} <= set(defs)
+    for name, v in defs.items():
+        assert getattr(N, name) == v, name
+    assert len(set(defs.values())) == len(defs)
+
+
 def test_cfg_defaults_match_reference_sortconfig():
     c = N.lsort_cfg()
     N.lib().lsort_cfg_default(C.byref(c))
