@@ -118,6 +118,7 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--case", default="", help="replay one case: name:n:seed:flags[:world[:api]]")
     ap.add_argument("--dist", type=float, default=0.0, help="fraction of cases run on 2-8 virtual ranks")
+    ap.add_argument("--strict", type=float, default=0.1, help="fraction of cases under LSORT_FLAG_STRICT_POLICY")
     ap.add_argument("--cases", type=int, default=0, help="stop after this many cases (0: run for --seconds)")
     ap.add_argument("--repeat", type=int, default=1, help="--case: run the case this many times in one process")
     ap.add_argument("--api", type=float, default=0.0,
@@ -144,7 +145,7 @@ def main():
         g = torch.Generator(device=dev)
         g.manual_seed(seed)
         flags = 0
-        if rng.random() < 0.1:
+        if rng.random() < a.strict:
             flags |= L._native.FLAG_STRICT_POLICY
         if replay:
             name, n, seed, flags = replay[0], int(replay[1]), int(replay[2]), int(replay[3])
